@@ -1,0 +1,307 @@
+"""Benchmark: ms per GN/LM iteration (fixed PCG iterations) of the matrix-free
+solver, plus the J^T J p kernel's achieved HBM bandwidth vs the measured peak.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config arap_warp|poisson|sfs|arap_mesh] [--prec f32|f64]
+
+Workload (BASELINE.json configs[1], the metric's headline config): ARAP image
+warping 1024x1024 (Off:2 + Ang:1 unknowns, 3,145,728 columns), Gauss-Newton,
+10 nonlinear x 20 PCG iterations with pcg_rel_tol = pcg_abs_tol =
+cost_stop_tol = 0 so every iteration count is exact, fp32, synthetic seeded
+inputs (paper_1604_06525_b200/workloads.py).
+
+A step = one solve() (10 GN iterations) from the same initial state; the
+value is step time / 10.  Inputs are resident in HBM before the timer starts;
+L2 is flushed (256 MiB write) between timed steps.  `e2e` runs the same solve
+through the public API with host buffers (pinned H2D of x + arrays, D2H of x)
+inside the timed region.  `--impl reference` times the unmodified reference
+CPU solver (oracle/_ref/ref_driver, all host threads) on the same workload,
+one GN iteration per step.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+NL, LIN = 10, 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="arap_warp")
+    ap.add_argument("--prec", default="f32", choices=["f32", "f64"])
+    ap.add_argument("--size", type=int, default=0, help="override grid edge (testing)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def make_problem(cfg_name, size=0):
+    from paper_1604_06525_b200 import workloads
+    if cfg_name == "arap_warp":
+        return workloads.arap_warp(size or 1024, size or 1024)
+    if cfg_name == "poisson":
+        return workloads.poisson(size or 512, size or 512)
+    if cfg_name == "sfs":
+        return workloads.sfs(size or 640, size or 480)
+    if cfg_name == "arap_mesh":
+        return workloads.arap_mesh(size or 448)
+    raise SystemExit(f"unknown config {cfg_name}")
+
+
+def workload_name(prob):
+    d = "x".join(str(v) for v in prob.dims.values())
+    return f"{prob.name} {d}, {'LM' if prob.method == 'lm' else 'GN'} {NL} nl x {LIN} PCG"
+
+
+def solve_config(prob, prec):
+    from paper_1604_06525_b200 import Method, Precision, SolveConfig
+    return SolveConfig(method=Method.kLevenbergMarquardt if prob.method == "lm" else Method.kGaussNewton,
+                       precision=Precision.kF32 if prec == "f32" else Precision.kF64,
+                       nonlinear_iters=NL, linear_iters=LIN, pcg_rel_tol=0.0, pcg_abs_tol=0.0,
+                       cost_stop_tol=0.0)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu=0):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([v.strip() for v in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        reasons = sorted({names[k] for r in self.rows for k in range(4)
+                          if len(r) > 3 + k and r[3 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(config):
+    """dram bytes per J^T J p launch from the committed ncu summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            return json.load(f)[config]["jtj"]["dram_bytes"]
+    except Exception:
+        return None
+
+
+def cpu_reference(prob, prec, repeat, threads):
+    """The unmodified reference (oracle/_ref) on this host: one GN/LM iteration
+    of the full workload per repeat; returns per-iteration ms (IterRow.wall_ms)."""
+    from oracle import pyoracle
+    data = prob.data(np.float32 if prec == "f32" else np.float64)
+    out = pyoracle.run_ref(prob.energy, data, ["time"], dims=prob.dims, prec=prec, method=prob.method,
+                           nl=1, lin=LIN, rel=0.0, abs_tol=0.0, cost_stop=0.0, exec_mode="par",
+                           repeat=repeat, threads=threads)
+    return list(out["time_row_ms"]), list(out["time_ms"])
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    prob = make_problem(args.config, args.size)
+    threads = os.cpu_count() or 1
+    rows, solves = cpu_reference(prob, args.prec, args.warmup + args.steps, threads)
+    per_iter = rows[args.warmup:] if len(rows) >= args.warmup + args.steps else rows
+    v = float(np.mean(per_iter))
+    line = {"impl": "reference", "metric": "ms per GN/LM iteration (fixed PCG iters)", "value": v,
+            "unit": "ms/iter", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": v, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+            "dtype": args.prec, "data": "synthetic (seeded splitmix64, workloads.py)",
+            "config": {"workload": workload_name(prob), "threads": threads},
+            "cpu_baseline": {"value": v, "unit": "ms/iter", "cores": threads, "kind": "reference",
+                             "sample": f"1 nonlinear iteration x {LIN} PCG of the full workload per step"},
+            "e2e": {"value": v, "unit": "ms/iter", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1604_06525_b200 import Solver, load_plan, planinfo
+    from paper_1604_06525_b200._lib import call, lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    prob = make_problem(args.config, args.size)
+    dt = np.float32 if args.prec == "f32" else np.float64
+    cfg = solve_config(prob, args.prec)
+    plan = load_plan(prob.name, cfg, prob.dims)
+    data = prob.data(dt)
+    s = Solver(plan, data, device=local)
+    n = plan.num_cols
+
+    import ctypes
+    sp = ctypes.c_void_p()
+    call("mo_session_stream", s._h, ctypes.byref(sp))
+    st = torch.cuda.ExternalStream(sp.value, device=dev)
+    x0 = torch.from_numpy(prob.x.astype(dt)).to(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    torch.cuda.synchronize()
+
+    def restore():
+        call("mo_bind_x_device", s._h, ctypes.c_void_p(x0.data_ptr()), n)
+
+    for _ in range(args.warmup):
+        restore()
+        s.solve()
+
+    s.set_profiling(True)
+    restore()
+    s.solve()  # capture the profiled PCG graph outside the timed region
+    s.profile_reset()
+    launches0 = s.kernel_launches()
+    times = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            restore()
+            with torch.cuda.stream(st):
+                flush.zero_()  # L2 flush between timed steps
+                ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                ev0.record(st)
+            r = s.solve()
+            ev1.record(st)
+            ev1.synchronize()
+            times.append(ev0.elapsed_time(ev1))
+    torch.cuda.synchronize()
+    launches = s.kernel_launches() - launches0
+    step_ms = float(np.mean(times))
+    if world > 1:
+        t = torch.tensor([step_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        step_ms = float(t.item())
+    apply_ms, apply_n = s.profile(0)
+    upd_ms, upd_n = s.profile(1)
+    s.set_profiling(False)
+
+    # e2e through the public API with pinned host buffers.
+    pin_x = torch.from_numpy(prob.x.astype(dt)).pin_memory()
+    pin_arr = [torch.from_numpy(a.astype(dt)).pin_memory() for a in prob.arrays]
+    pin_out = torch.empty(n, dtype=torch.float32 if dt == np.float32 else torch.float64).pin_memory()
+    e2e = []
+    for k in range(max(2, args.steps)):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        call("mo_bind_x", s._h, ctypes.c_void_p(pin_x.data_ptr()), n)
+        for i, a in enumerate(pin_arr):
+            call("mo_bind_array", s._h, i, ctypes.c_void_p(a.data_ptr()), a.numel())
+        s.solve()
+        call("mo_get_x", s._h, ctypes.c_void_p(pin_out.data_ptr()), n)
+        e2e.append((time.perf_counter() - t0) * 1e3)
+    h2d = int(pin_x.numel() * pin_x.element_size() + sum(a.numel() * a.element_size() for a in pin_arr))
+    d2h = int(pin_out.numel() * pin_out.element_size())
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    info = planinfo.parse(open(os.path.join(ROOT, "paper_1604_06525_b200", "plans", prob.name + ".moplan")).read())
+    rb = np.dtype(dt).itemsize
+    units = int(np.prod(list(prob.dims.values())))
+    per_elem = planinfo.algorithmic_bytes_per_element(info, "gather_set", "jtj", rb)
+    alg = per_elem * units
+    peak, peak_kind = measured_peak()
+    avg_apply = apply_ms / max(apply_n, 1)
+    achieved = alg / (avg_apply * 1e-3) / 1e9 if apply_n else None
+    value = step_ms / NL
+    line = {
+        "metric": "ms per GN/LM iteration (fixed PCG iters)", "value": value / world, "unit": "ms/iter",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": args.prec,
+        "data": "synthetic (seeded splitmix64, workloads.py); inputs resident in HBM",
+        "config": {"workload": workload_name(prob), "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "l2": "flushed between timed steps (256 MiB write)", "step": f"solve() = {NL} iterations",
+                   "final_cost": r.final_cost},
+        "roofline": {"bound": "hbm", "kernel": "J^T J p apply (generated gather_jtj, fused p'Ap)",
+                     "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": ncu_traffic(prob.name),
+                     "alg_bytes_per_launch": alg, "alg_bytes_per_elem": per_elem,
+                     "avg_launch_us": avg_apply * 1e3, "launches": apply_n,
+                     "pcg_update_avg_us": upd_ms / max(upd_n, 1) * 1e3},
+        "e2e": {"value": float(np.median(e2e)) / NL, "unit": "ms/iter", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline:
+        try:
+            threads = os.cpu_count() or 1
+            rows, _ = cpu_reference(prob, args.prec, 1, threads)
+            line["cpu_baseline"] = {"value": float(np.mean(rows)), "unit": "ms/iter", "cores": threads,
+                                    "kind": "reference",
+                                    "sample": f"reference solver, 1 nonlinear iteration x {LIN} PCG of the full workload"}
+        except Exception as e:  # the baseline is reported, never the target
+            line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

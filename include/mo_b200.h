@@ -1,0 +1,174 @@
+/* mo_b200.h — C ABI of the B200-native matrix-free GN/LM solver core.
+ *
+ * Drop-in boundary for the reference "minopt" solver path (arXiv 1604.06525,
+ * /root/reference/proj/include/minopt).  The reference exposes header-only C++
+ * templates; each entry point below replaces one of its public routines
+ * (SURVEY.md §8b).  Plans are produced at plan time by the reference's own
+ * front end (compile_source lower.hpp:619 -> plan plan.hpp:189) and handed
+ * over through integration/minopt_b200_bridge.hpp; everything after that —
+ * residual/cost evaluation, J^T F + Jacobi, matrix-free J^T J p, Jacobi PCG,
+ * GN / LM control — runs on the GPU.  There is no CPU fallback: without a
+ * CUDA device every compute entry point returns MO_ERR_NO_DEVICE.
+ *
+ * Conventions: every function returns 0 on success or 1 + the reference Err
+ * code (common.hpp:13-32; MO_ERR_* below) and records a message retrievable
+ * with mo_last_error() (thread local).  Host buffers use the reference layout:
+ * the unknown vector is in plan column order col = ubase[f] + elem*C_f + ch
+ * (plan.hpp:212-218), arrays are channel-interleaved row-major (problem.hpp:
+ * 131-136), graphs are edge-major uint64 vertex tables (exec.hpp:36-43).
+ * Real data is float when the session precision is MO_F32, double otherwise.
+ */
+#ifndef MO_B200_H_
+#define MO_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Error codes: 1 + minopt::Err (common.hpp:13-32). */
+enum {
+  MO_OK = 0,
+  MO_ERR_SYNTAX = 1,
+  MO_ERR_UNDECLARED = 2,
+  MO_ERR_ARITY = 3,
+  MO_ERR_NONCONST_OFFSET = 4,
+  MO_ERR_MIXED_DOMAIN = 5,
+  MO_ERR_NONCONST_EXPONENT = 6,
+  MO_ERR_DOMAIN_MISMATCH = 7,
+  MO_ERR_NONBOOLEAN = 8,
+  MO_ERR_CYCLIC_COMPUTED = 9,
+  MO_ERR_SHAPE_MISMATCH = 10,
+  MO_ERR_INDEX_OUT_OF_RANGE = 11,
+  MO_ERR_FORMAT = 12,
+  MO_ERR_TRUNCATED = 13,
+  MO_ERR_GRAPH_DOMAIN = 14,
+  MO_ERR_BIND = 15,
+  MO_ERR_NONFINITE_COST = 16,
+  MO_ERR_CYCLIC_IR = 17,
+  MO_ERR_INTERNAL = 18,
+  MO_ERR_CUDA = 101,      /* device/driver failure (no reference counterpart) */
+  MO_ERR_NO_DEVICE = 102  /* no CUDA device: the product has no CPU fallback */
+};
+
+enum { MO_GAUSS_NEWTON = 0, MO_LEVENBERG_MARQUARDT = 1 }; /* plan.hpp:15 Method */
+enum { MO_F32 = 0, MO_F64 = 1 };                         /* plan.hpp:16 Precision */
+
+/* StopReason, solver.hpp:40-46 */
+enum { MO_STOP_ITER_LIMIT = 0, MO_STOP_COST_TOL = 1, MO_STOP_STALLED = 2, MO_STOP_NONFINITE = 3 };
+
+/* SolveConfig (plan.hpp:19-38).  materialize/exec/force_evalj have no device
+ * meaning (the device path is matrix-free) and are omitted. */
+typedef struct mo_solve_config {
+  int method;
+  int precision;
+  int nonlinear_iters;
+  int linear_iters;
+  double pcg_rel_tol; /* < 0: 1e-4 (f32) / 1e-8 (f64), plan.hpp:192-193 */
+  double pcg_abs_tol;
+  int use_preconditioner;
+  double lm_radius0, lm_radius_min, lm_radius_max;
+  double lm_diag_min, lm_diag_max;
+  double lm_min_decrease;
+  double cost_stop_tol;
+} mo_solve_config;
+
+/* IterRow (solver.hpp:31-38) */
+typedef struct mo_iter_row {
+  int iter;
+  double cost;
+  int accepted;
+  double radius;
+  int pcg_iters;
+  double wall_ms;
+} mo_iter_row;
+
+/* SolveResult (solver.hpp:58-74).  `trace` is owned by the session and stays
+ * valid until the next mo_solve or mo_session_destroy. */
+typedef struct mo_solve_result {
+  double final_cost;
+  int reason;
+  int nonfinite_kernels;
+  int indefinite_operator;
+  int64_t unconstrained;
+  int n_trace;
+  const mo_iter_row* trace;
+} mo_solve_result;
+
+typedef struct mo_plan_s* mo_plan;
+typedef struct mo_session_s* mo_session;
+
+/* Per-iteration callback (solver.hpp:503): may read/modify the bound data
+ * through mo_get_x / mo_bind_* before the next nonlinear iteration. */
+typedef void (*mo_iter_cb)(int iter, mo_session s, void* user);
+
+const char* mo_last_error(void);
+const char* mo_version(void);
+int mo_device_count(int* n);
+
+/* ---- plans: CompiledPlan (plan.hpp:125-137) ---------------------------- */
+/* Parse the moplan v1 interchange (integration/minopt_b200_bridge.hpp). */
+int mo_plan_parse(const char* text, size_t len, mo_plan* out);
+/* Override a declared dim's extent (programs are shape independent; the
+ * column layout is recomputed as plan.hpp:212-218 would). */
+int mo_plan_set_dim(mo_plan p, const char* name, int64_t extent);
+int mo_plan_get_config(mo_plan p, mo_solve_config* cfg);
+int mo_plan_set_config(mo_plan p, const mo_solve_config* cfg); /* plan(spec, cfg) checks, plan.hpp:190-199 */
+int mo_plan_num_cols(mo_plan p, int64_t* n);
+/* Generate + NVRTC-compile the plan's sm_100a module into the kernel cache
+ * (no GPU needed); sessions then load it without compiling. */
+int mo_plan_precompile(mo_plan p, int precision);
+int mo_plan_counts(mo_plan p, int* n_params, int* n_arrays, int* n_graphs, int* n_unknowns);
+int mo_plan_array_size(mo_plan p, int i, int64_t* n_scalars);
+int mo_plan_graph_arity(mo_plan p, int i, int* arity);
+void mo_plan_destroy(mo_plan p);
+
+/* ---- sessions: Solver<Real> (solver.hpp:84-635) ------------------------ */
+/* Bind the plan to a device; precision comes from the plan config.  The
+ * session owns one stream and every device vector (solver.hpp:616-632). */
+int mo_session_create(mo_plan p, int device, mo_session* out);
+void mo_session_destroy(mo_session s);
+
+/* SolveData<Real> (solver.hpp:23-29), copied host -> device. */
+int mo_bind_x(mo_session s, const void* x, int64_t n);
+int mo_bind_array(mo_session s, int i, const void* data, int64_t n);
+int mo_bind_params(mo_session s, const double* params, int64_t n);
+int mo_bind_graph(mo_session s, int i, const uint64_t* verts, int64_t n_entries, int arity);
+/* Device-resident variants (pointers on the session's device). */
+int mo_bind_x_device(mo_session s, const void* x, int64_t n);
+int mo_bind_array_device(mo_session s, int i, const void* data, int64_t n);
+
+/* refresh (solver.hpp:125-168): validate binds, computed arrays, masks. */
+int mo_refresh(mo_session s);
+int mo_num_cols(mo_session s, int64_t* n);
+int mo_num_rows(mo_session s, int64_t* n);
+int mo_get_excluded(mo_session s, uint8_t* out, int64_t n);
+
+int mo_cost(mo_session s, double* out);                    /* solver.hpp:174 */
+int mo_residuals(mo_session s, void* out, int64_t n);      /* solver.hpp:196 */
+int mo_build_normal(mo_session s);                         /* solver.hpp:220 */
+int mo_get_rhs(mo_session s, void* out, int64_t n);        /* rhs()  :108 */
+int mo_get_precond(mo_session s, void* out, int64_t n);    /* precond() :109 */
+int mo_apply_jtj(mo_session s, const void* v, void* out, int64_t n); /* :255 */
+int mo_apply_jtj_device(mo_session s, const void* v, void* out);
+int mo_solve(mo_session s, mo_iter_cb cb, void* user, mo_solve_result* out); /* :389 */
+int mo_get_x(mo_session s, void* out, int64_t n);
+int mo_saw_nonfinite(mo_session s, int* out);               /* :110 */
+
+/* ---- measurement hooks (bench.py) -------------------------------------- */
+/* When enabled, CUDA events bracket every J^T J p apply and PCG vector update
+ * launched by mo_solve (on the session stream, also inside CUDA graphs). */
+int mo_set_profiling(mo_session s, int enable);
+/* kind: 0 = J^T J p apply, 1 = PCG vector update, 2 = build_normal, 3 = cost */
+int mo_profile_read(mo_session s, int kind, double* total_ms, int64_t* launches);
+int mo_profile_reset(mo_session s);
+int mo_session_stream(mo_session s, void** stream); /* cudaStream_t */
+/* Number of this library's kernels launched so far (host-side count). */
+int mo_kernel_launches(mo_session s, int64_t* n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MO_B200_H_ */

@@ -1,0 +1,379 @@
+// mo_codegen.cpp — plan-time translation of the reference's guarded register
+// programs (program.hpp:21-167) into CUDA C++ for NVRTC (sm_100a).
+//
+// Semantics reproduced per element exactly as run_program (program.hpp:89-167):
+//  * every register starts at 0 (regs.assign, :92);
+//  * a block whose guard register is 0 is skipped wholesale (:94-95);
+//  * loads follow EvalEnv::read (eval.hpp:41-55): grid reads outside the
+//    field's own shape return 0, slot reads index edge[slot];
+//  * InBounds tests the iteration domain (eval.hpp:57-61);
+//  * pow uses the shared pow_eval rounding rule (common.hpp:116-124);
+//  * each output is Real(0) plus its guarded roots in listed order (:159-166).
+// Modules are compiled with --fmad=false so add/mul round exactly like the
+// reference's x86 build (no contraction), which makes per-element outputs of
+// add/mul/select programs bitwise equal to the CPU reference.
+//
+// The per-element bodies are wrapped in hand-written kernel skeletons: 32x8
+// tiles with a grid-stride tile loop (grid sized to the SM count), fused
+// epilogues (PCG p'Ap reduction, LM damping, identity patch of build_normal),
+// and deterministic last-block reductions.
+#include <cstdio>
+#include <sstream>
+#include <string>
+
+#include "mo_codegen.hpp"
+
+namespace mo {
+
+namespace {
+
+std::string hexd(double v) {
+  char buf[64];
+  std::snprintf(buf, sizeof buf, "%a", v);
+  std::string s = buf;
+  if (s == "inf") return "(1.0/0.0)";
+  if (s == "-inf") return "(-1.0/0.0)";
+  if (s == "nan" || s == "-nan") return "(0.0/0.0)";
+  return s;
+}
+
+struct Gen {
+  const Plan& P;
+  bool f64;
+  std::ostringstream os;
+  int nprog = 0;
+
+  Gen(const Plan& p, bool d) : P(p), f64(d) {}
+
+  int slot_of(int op, int field) const {
+    const int U = int(P.unknowns.size()), A = int(P.arrays.size());
+    switch (op) {
+      case kLoadU: return field;
+      case kLoadP: return U + field;
+      case kLoadA: return 2 * U + field;
+      case kLoadC: return 2 * U + A + field;
+    }
+    return -1;
+  }
+  const Field& field_of(int op, int field) const {
+    check(field >= 0, Err::kShapeMismatch, "kernel reads a field that is not bound");
+    switch (op) {
+      case kLoadU:
+      case kLoadP:
+        check(size_t(field) < P.unknowns.size(), Err::kShapeMismatch, "kernel reads a field that is not bound");
+        return P.unknowns[size_t(field)];
+      case kLoadA:
+        check(size_t(field) < P.arrays.size(), Err::kShapeMismatch, "kernel reads a field that is not bound");
+        return P.arrays[size_t(field)];
+      default:
+        check(size_t(field) < P.computed.size(), Err::kShapeMismatch, "kernel reads a field that is not bound");
+        return P.computed[size_t(field)];
+    }
+  }
+
+  const char* fn(int sub) const {
+    static const char* f32n[] = {"sqrtf", "sinf", "cosf", "expf", "logf", "fabsf", "atanf"};
+    static const char* f64n[] = {"sqrt", "sin", "cos", "exp", "log", "fabs", "atan"};
+    check(sub <= kAtan, Err::kFormatError, "codegen: unknown unary function");
+    return f64 ? f64n[sub] : f32n[sub];
+  }
+
+  // Emit `__device__ void NAME(P, p0, p1, p2, vs, out)`.
+  std::string program(const Program& pg, bool graph) {
+    std::string name = "mo_prog_" + std::to_string(nprog++);
+    os << "__device__ __forceinline__ void " << name
+       << "(const mo_kparams& P, int p0, int p1, int p2, const int* vs, Real* out) {\n";
+    os << "  (void)P; (void)p0; (void)p1; (void)p2; (void)vs;\n";
+    for (uint32_t r = 0; r < pg.num_regs; ++r) os << "  Real r" << r << " = (Real)0;\n";
+    for (const Block& b : pg.blocks) {
+      std::string ind = "  ";
+      if (b.gid != 0) {
+        os << "  if (r" << pg.guard_regs[b.gid] << " != (Real)0) {\n";
+        ind = "    ";
+      }
+      for (uint32_t i = b.begin; i < b.end; ++i) os << ind << instr(pg.instrs[i], graph) << "\n";
+      if (b.gid != 0) os << "  }\n";
+    }
+    for (size_t o = 0; o < pg.outputs.size(); ++o) {
+      os << "  { Real acc = (Real)0;";
+      for (auto [gid, reg] : pg.outputs[o]) {
+        if (gid != 0)
+          os << " if (r" << pg.guard_regs[gid] << " != (Real)0) acc += r" << reg << ";";
+        else
+          os << " acc += r" << reg << ";";
+      }
+      os << " out[" << o << "] = acc; }\n";
+    }
+    os << "}\n";
+    return name;
+  }
+
+  std::string reg(int r) const { return "r" + std::to_string(r); }
+
+  std::string instr(const Instr& in, bool graph) {
+    std::ostringstream s;
+    s << reg(in.dst) << " = ";
+    switch (in.op) {
+      case kImm: s << "(Real)(" << hexd(in.imm) << ")"; break;
+      case kParam:
+        check(in.field >= 0 && size_t(in.field) < P.params.size(), Err::kShapeMismatch,
+              "kernel reads a parameter that is not declared");
+        s << "(Real)P.params[" << in.field << "]";
+        break;
+      case kIndex:
+        if (graph || in.field > 2) s << "(Real)0";  // graph env pix = {0,0,0}
+        else s << "(Real)p" << in.field;
+        break;
+      case kLoadU:
+      case kLoadA:
+      case kLoadC:
+      case kLoadP: {
+        const Field& f = field_of(in.op, in.field);
+        check(in.channel >= 0 && in.channel < f.channels, Err::kShapeMismatch,
+              "kernel reads past the bound channel count");
+        int sl = slot_of(in.op, in.field);
+        if (in.graph) {
+          s << "mo_ldv<Real, " << f.channels << ">(P.v[" << sl << "], vs[" << in.slot << "], "
+            << in.channel << ")";
+        } else {
+          int nd = int(f.dom.dims.size());
+          s << "mo_ld<Real, " << (nd ? nd : 1) << ", " << f.channels << ">(P.v[" << sl << "], p0 + ("
+            << in.off[0] << "), p1 + (" << in.off[1] << "), p2 + (" << in.off[2] << "), "
+            << in.channel << ")";
+        }
+        break;
+      }
+      case kInB:
+        if (graph) s << "(Real)(" << (in.off[0] == 0 ? 1 : 0) << ")";
+        else
+          s << "(mo_inb(P, p0 + (" << in.off[0] << "), p1 + (" << in.off[1] << "), p2 + ("
+            << in.off[2] << ")) ? (Real)1 : (Real)0)";
+        break;
+      case kAdd: s << reg(in.a) << " + " << reg(in.b); break;
+      case kMul: s << reg(in.a) << " * " << reg(in.b); break;
+      case kPow: s << "mo_pow_eval<Real>(" << reg(in.a) << ", " << in.pnum << "LL, " << in.pden << "LL)"; break;
+      case kUn: s << fn(in.sub) << "(" << reg(in.a) << ")"; break;
+      case kCmp: {
+        static const char* ops[] = {"==", "!=", "<", "<=", ">", ">="};
+        check(in.sub <= kGe, Err::kFormatError, "codegen: unknown comparison");
+        s << "((" << reg(in.a) << " " << ops[in.sub] << " " << reg(in.b) << ") ? (Real)1 : (Real)0)";
+        break;
+      }
+      case kAnd:
+        s << "((" << reg(in.a) << " != (Real)0 && " << reg(in.b) << " != (Real)0) ? (Real)1 : (Real)0)";
+        break;
+      case kOr:
+        s << "((" << reg(in.a) << " != (Real)0 || " << reg(in.b) << " != (Real)0) ? (Real)1 : (Real)0)";
+        break;
+      case kNot: s << "((" << reg(in.a) << " == (Real)0) ? (Real)1 : (Real)0)"; break;
+      case kSel: s << "((" << reg(in.a) << " != (Real)0) ? " << reg(in.b) << " : " << reg(in.c) << ")"; break;
+      default: fail(Err::kFormatError, "codegen: unknown opcode");
+    }
+    s << ";";
+    return s.str();
+  }
+
+  static std::string kbegin(const std::string& kname) {
+    return "extern \"C\" __global__ void __launch_bounds__(MO_THREADS) " + kname +
+           "(const __grid_constant__ mo_kparams P) {\n";
+  }
+
+  // --------------------------------------------------------- grid kernels
+  void grid_cost(const std::string& pn, const std::string& kn) {
+    os << kbegin(kn)
+       << "  double acc = 0; bool bad = false;\n"
+          "  const int nt = mo_num_tiles(P);\n"
+          "  for (int t = blockIdx.x; t < nt; t += gridDim.x) {\n"
+          "    int p0, p1, p2;\n"
+          "    if (mo_tile_coord(P, t, p0, p1, p2)) {\n"
+          "      Real o[1];\n      "
+       << pn
+       << "(P, p0, p1, p2, nullptr, o);\n"
+          "      if (!mo_finite((double)o[0])) bad = true;\n"
+          "      acc += (double)o[0];\n"
+          "    }\n"
+          "  }\n"
+          "  if (bad) atomicOr(&P.state->nonfinite_kernel, 1);\n"
+          "  mo_reduce_epilogue<Real>(P.red, acc, 0.0, false);\n"
+          "}\n";
+  }
+
+  void grid_evalf(const std::string& pn, const std::string& kn, size_t nout) {
+    os << kbegin(kn) << "  bool bad = false;\n"
+       << "  const int nt = mo_num_tiles(P);\n"
+          "  for (int t = blockIdx.x; t < nt; t += gridDim.x) {\n"
+          "    int p0, p1, p2;\n"
+          "    if (mo_tile_coord(P, t, p0, p1, p2)) {\n"
+          "      const int e = mo_local_elem(P, p0, p1, p2);\n"
+          "      Real o["
+       << (nout ? nout : 1) << "];\n      " << pn << "(P, p0, p1, p2, nullptr, o);\n";
+    for (size_t k = 0; k < nout; ++k)
+      os << "      if (!mo_finite((double)o[" << k << "])) bad = true;\n"
+         << "      ((Real*)P.out0)[P.rowbase[" << k << "] + e] = o[" << k << "];\n";
+    os << "    }\n  }\n  if (bad) atomicOr(&P.state->nonfinite_kernel, 1);\n}\n";
+  }
+
+  // Per-element writes of `nout` outputs into strided buffers (computed arrays).
+  void grid_store(const std::string& pn, const std::string& kn, size_t nout) {
+    os << kbegin(kn) << "  bool bad = false;\n"
+       << "  const int nt = mo_num_tiles(P);\n"
+          "  for (int t = blockIdx.x; t < nt; t += gridDim.x) {\n"
+          "    int p0, p1, p2;\n"
+          "    if (mo_tile_coord(P, t, p0, p1, p2)) {\n"
+          "      const long long e = mo_local_elem(P, p0, p1, p2);\n"
+          "      Real o["
+       << (nout ? nout : 1) << "];\n      " << pn << "(P, p0, p1, p2, nullptr, o);\n";
+    for (size_t k = 0; k < nout; ++k)
+      os << "      if (!mo_finite((double)o[" << k << "])) bad = true;\n"
+         << "      ((Real*)P.out0)[e * " << nout << " + " << k << "] = o[" << k << "];\n";
+    os << "    }\n  }\n  if (bad) atomicOr(&P.state->nonfinite_kernel, 1);\n}\n";
+  }
+
+  void grid_exclude(const std::string& pn, const std::string& kn) {
+    os << kbegin(kn)
+       << "  const int nt = mo_num_tiles(P);\n"
+          "  for (int t = blockIdx.x; t < nt; t += gridDim.x) {\n"
+          "    int p0, p1, p2;\n"
+          "    if (mo_tile_coord(P, t, p0, p1, p2)) {\n"
+          "      const int e = mo_local_elem(P, p0, p1, p2);\n"
+          "      Real o[1];\n      "
+       << pn
+       << "(P, p0, p1, p2, nullptr, o);\n"
+          "      ((unsigned char*)P.out0)[e] = (o[0] != (Real)0) ? 1 : 0;\n"
+          "    }\n  }\n}\n";
+  }
+
+  // build_normal gather (solver.hpp:221-230) + fused identity patch (241-250).
+  void gather_bm(const GatherSet& g, const std::string& pn, const std::string& kn) {
+    const size_t K = g.chans.size();
+    os << kbegin(kn) << "  double cnt = 0; bool bad = false;\n"
+       << "  Real* B = (Real*)P.out0; Real* M = (Real*)P.out1;\n"
+          "  const int nt = mo_num_tiles(P);\n"
+          "  for (int t = blockIdx.x; t < nt; t += gridDim.x) {\n"
+          "    int p0, p1, p2;\n"
+          "    if (mo_tile_coord(P, t, p0, p1, p2)) {\n"
+          "      const long long e = mo_local_elem(P, p0, p1, p2);\n"
+          "      Real o["
+       << (K ? 2 * K : 1)
+       << "];\n"
+          "      const bool ex = P.mask && P.mask[e];\n"
+          "      if (ex) {\n"
+       << "        for (int k = 0; k < " << 2 * K << "; ++k) o[k] = (Real)0;\n"
+       << "      } else {\n        " << pn << "(P, p0, p1, p2, nullptr, o);\n"
+       << "        for (int k = 0; k < " << 2 * K << "; ++k) if (!mo_finite((double)o[k])) bad = true;\n"
+       << "      }\n";
+    for (size_t k = 0; k < K; ++k) {
+      int f = g.chans[k].first, ch = g.chans[k].second;
+      int C = P.unknowns[size_t(f)].channels;
+      os << "      { const long long col = P.ubase[" << f << "] + e * " << C << " + " << ch << ";\n"
+         << "        Real b = o[" << 2 * k << "], m = o[" << 2 * k + 1 << "];\n"
+         << "        if (P.flags & MO_F_PATCH) {\n"
+         << "          if (ex) { b = (Real)0; m = (Real)1; }\n"
+         << "          else if (m == (Real)0) { m = (Real)1; cnt += 1.0; }\n"
+         << "        }\n"
+         << "        B[col] = b; M[col] = m; }\n";
+    }
+    os << "    }\n  }\n  if (bad) atomicOr(&P.state->nonfinite_kernel, 1);\n"
+       << "  if (P.flags & MO_F_REDUCE) mo_reduce_epilogue<Real>(P.red, cnt, 0.0, false);\n}\n";
+  }
+
+  // Matrix-free normal apply gather (solver.hpp:257-265), with optional fused
+  // LM damping (401-405), excluded zeroing and p'Ap reduction (pcg.hpp:100-102).
+  void gather_jtj(const GatherSet& g, const std::string& pn, const std::string& kn) {
+    const size_t K = g.chans.size();
+    os << kbegin(kn) << "  if ((P.flags & MO_F_SKIPDONE) && P.state->done) return;\n"
+       << "  double acc = 0; bool bad = false;\n"
+       << "  Real* OUT = (Real*)P.out0; const Real* PV = (const Real*)P.in0; const Real* DAMP = (const Real*)P.in1;\n"
+          "  const int nt = mo_num_tiles(P);\n"
+          "  for (int t = blockIdx.x; t < nt; t += gridDim.x) {\n"
+          "    int p0, p1, p2;\n"
+          "    if (mo_tile_coord(P, t, p0, p1, p2)) {\n"
+          "      const long long e = mo_local_elem(P, p0, p1, p2);\n"
+          "      Real o["
+       << (K ? K : 1)
+       << "];\n"
+          "      const bool ex = P.mask && P.mask[e];\n"
+          "      if (ex) {\n"
+       << "        for (int k = 0; k < " << K << "; ++k) o[k] = (Real)0;\n"
+       << "      } else {\n        " << pn << "(P, p0, p1, p2, nullptr, o);\n"
+       << "        for (int k = 0; k < " << K << "; ++k) if (!mo_finite((double)o[k])) bad = true;\n"
+       << "      }\n";
+    for (size_t k = 0; k < K; ++k) {
+      int f = g.chans[k].first, ch = g.chans[k].second;
+      int C = P.unknowns[size_t(f)].channels;
+      os << "      { const long long col = P.ubase[" << f << "] + e * " << C << " + " << ch << ";\n"
+         << "        Real v = o[" << k << "];\n"
+         << "        if (P.flags & MO_F_DAMP) v = v + DAMP[col] * PV[col];\n"
+         << "        if ((P.flags & MO_F_ZEROEXCL) && P.colmask && P.colmask[col]) v = (Real)0;\n"
+         << "        OUT[col] = v;\n"
+         << "        if (P.flags & MO_F_REDUCE) acc += (double)(PV[col] * v); }\n";
+    }
+    os << "    }\n  }\n  if (bad) atomicOr(&P.state->nonfinite_kernel, 1);\n"
+       << "  if (P.flags & MO_F_REDUCE) mo_reduce_epilogue<Real>(P.red, acc, 0.0, false);\n}\n";
+  }
+
+  // --------------------------------------------------------- graph kernels
+  // One thread per hyperedge (exec.hpp:223-309); scatter outputs go to a
+  // per-edge contribution buffer that the deterministic vertex gather folds
+  // in edge order (mo_kernels.cu: mo_graph_gather).
+  void graph_kernel(const std::string& pn, const std::string& kn, size_t nout, int arity, int mode) {
+    // mode 0 = cost (reduce), 1 = evalf (row writes), 2 = contributions
+    os << kbegin(kn) << "  if ((P.flags & MO_F_SKIPDONE) && P.state->done) return;\n"
+       << "  double acc = 0; bool bad = false; (void)acc;\n"
+       << "  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < P.nedges;"
+          " e += (long long)gridDim.x * blockDim.x) {\n"
+       << "    int vs[" << (arity ? arity : 1) << "];\n";
+    for (int s = 0; s < arity; ++s) os << "    vs[" << s << "] = P.verts[e * " << arity << " + " << s << "];\n";
+    os << "    Real o[" << (nout ? nout : 1) << "];\n    " << pn << "(P, 0, 0, 0, vs, o);\n";
+    for (size_t k = 0; k < nout; ++k) {
+      os << "    if (!mo_finite((double)o[" << k << "])) bad = true;\n";
+      if (mode == 0) os << "    acc += (double)o[0];\n";
+      else if (mode == 1) os << "    ((Real*)P.out0)[P.rowbase[" << k << "] + e] = o[" << k << "];\n";
+      else os << "    ((Real*)P.out0)[e * " << nout << " + " << k << "] = o[" << k << "];\n";
+    }
+    os << "  }\n  if (bad) atomicOr(&P.state->nonfinite_kernel, 1);\n";
+    if (mode == 0) os << "  mo_reduce_epilogue<Real>(P.red, acc, 0.0, false);\n";
+    os << "}\n";
+  }
+
+  void run() {
+    for (size_t i = 0; i < P.grid_sets.size(); ++i) {
+      const GridSet& g = P.grid_sets[i];
+      grid_cost(program(g.cost, false), "mo_grid_cost_" + std::to_string(i));
+      grid_evalf(program(g.evalf, false), "mo_grid_evalf_" + std::to_string(i), g.evalf.outputs.size());
+    }
+    for (size_t i = 0; i < P.gather_sets.size(); ++i) {
+      const GatherSet& g = P.gather_sets[i];
+      gather_bm(g, program(g.bm, false), "mo_gather_bm_" + std::to_string(i));
+      gather_jtj(g, program(g.jtj, false), "mo_gather_jtj_" + std::to_string(i));
+    }
+    for (size_t i = 0; i < P.graph_sets.size(); ++i) {
+      const GraphSet& g = P.graph_sets[i];
+      int ar = P.graphs[size_t(g.graph)].second;
+      std::string s = std::to_string(i);
+      graph_kernel(program(g.cost, true), "mo_graph_cost_" + s, g.cost.outputs.size(), ar, 0);
+      graph_kernel(program(g.evalf, true), "mo_graph_evalf_" + s, g.evalf.outputs.size(), ar, 1);
+      graph_kernel(program(g.bm, true), "mo_graph_bm_" + s, g.bm.outputs.size(), ar, 2);
+      graph_kernel(program(g.jtj, true), "mo_graph_jtj_" + s, g.jtj.outputs.size(), ar, 2);
+    }
+    for (size_t i = 0; i < P.computed_kernels.size(); ++i) {
+      const ComputedKernel& ck = P.computed_kernels[i];
+      grid_store(program(ck.prog, false), "mo_computed_" + std::to_string(i), ck.prog.outputs.size());
+    }
+    for (size_t i = 0; i < P.exclude_kernels.size(); ++i)
+      grid_exclude(program(P.exclude_kernels[i].prog, false), "mo_exclude_" + std::to_string(i));
+  }
+};
+
+}  // namespace
+
+std::string generate_module(const Plan& P, bool f64, const std::string& prelude) {
+  Gen g(P, f64);
+  g.os << "// generated by mo_codegen.cpp — do not edit\n";
+  g.os << "typedef " << (f64 ? "double" : "float") << " Real;\n";
+  g.os << prelude << "\n";
+  g.run();
+  return g.os.str();
+}
+
+}  // namespace mo

@@ -1,0 +1,307 @@
+// mo_device.cuh — device-side definitions shared by the hand-written kernels
+// (mo_kernels.cu, compiled by nvcc into libmo_b200.so) and the per-element
+// kernels generated at plan time from the reference's KernelPrograms
+// (mo_codegen.cpp, compiled by NVRTC for sm_100a).  The file is embedded
+// verbatim into every generated module, so it must stay self-contained
+// (no standard headers).
+#ifndef MO_DEVICE_CUH_
+#define MO_DEVICE_CUH_
+
+#define MO_MAX_VIEWS 32
+#define MO_MAX_UNK 16
+#define MO_THREADS 256
+#define MO_TILE_X 32
+#define MO_TILE_Y 8
+
+// One bound field: channel-interleaved values over the field's own grid
+// domain (reference eval.hpp:15-21).  Shapes are GLOBAL extents; `row_lo` is
+// the global axis-0 row stored first in this (possibly strip-sharded) buffer.
+struct mo_view {
+  const void* p;
+  int ch;
+  int nd;
+  int s0, s1, s2;
+  int row_lo;
+};
+
+// Device-resident solver scalars.  Real-typed quantities are stored as double
+// (exact for float) and always recomputed in Real to follow pcg.hpp:63-130.
+struct mo_state {
+  double rz, pap, alpha, beta, stop, rz_next;
+  double tol_rel, tol_abs;
+  int done, iters, indefinite, nonfinite;
+  int use_precond, nonfinite_kernel;
+  int any_nonzero, pad0;
+  long long unconstrained;
+  double sums[8];
+  unsigned counters[8];
+};
+
+// Finalisation ops run by the last block of a reduction.
+enum {
+  MO_FIN_STORE = 0,      // sums[slot] = total (slot in fin_arg)
+  MO_FIN_PCG_INIT = 1,   // rz0, stop test          (pcg.hpp:88-95)
+  MO_FIN_PCG_ALPHA = 2,  // p'Ap checks, alpha      (pcg.hpp:100-110)
+  MO_FIN_PCG_BETA = 3,   // rz', stop test, beta    (pcg.hpp:116-124)
+  MO_FIN_UNCONSTRAINED = 4,
+  MO_FIN_STORE2 = 5,     // sums[slot], sums[slot+1] = pair totals
+};
+
+enum {
+  MO_F_DAMP = 1,       // jtj: out += damp * p              (solver.hpp:401-405)
+  MO_F_REDUCE = 2,     // kernel contributes to a reduction
+  MO_F_PATCH = 4,      // bm: identity patch + unconstrained (solver.hpp:241-250)
+  MO_F_ZEROEXCL = 8,   // jtj: zero excluded columns        (pcg.hpp:101)
+  MO_F_SKIPDONE = 16,  // return at once when the PCG has already stopped
+};
+
+// One deterministic reduction: partial slots [part_base, part_base+gridDim)
+// of [0, part_total); the last arriving block finalises with fin_op.
+struct mo_red {
+  double* partials;
+  unsigned* counter;
+  mo_state* state;
+  int part_base, part_total;
+  int fin_op, fin_arg;
+};
+
+struct mo_kparams {
+  mo_view v[MO_MAX_VIEWS];
+  const double* params;
+  int dnd, d0, d1, d2;  // iteration domain, global shape
+  int row0, row1;       // axis-0 rows this launch iterates (global)
+  int row_lo;           // first global row of the per-element storage
+  int flags;
+  void* out0;
+  void* out1;
+  const void* in0;  // p for damp / p'Ap
+  const void* in1;  // damp
+  const unsigned char* mask;     // per-element exclusion (uint8) or null
+  const unsigned char* colmask;  // per-column exclusion (uint8) or null
+  long long ubase[MO_MAX_UNK];   // local column base per unknown field
+  const long long* rowbase;      // evalf: residual row base per output
+  const int* verts;              // graph: int32 vertex table, edge-major
+  int arity;
+  long long nedges;
+  mo_red red;
+  mo_state* state;
+};
+
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ bool mo_finite(double x) { return x == x && fabs(x) <= 1.7976931348623157e308; }
+
+// pow_eval / ipow (reference common.hpp:102-124): one rounding rule everywhere.
+template <class Real>
+__device__ __forceinline__ Real mo_ipow(Real x, long long n) {
+  if (n < 0) return Real(1) / mo_ipow(x, -n);
+  Real r = Real(1);
+  while (n > 0) {
+    if (n & 1) r *= x;
+    x *= x;
+    n >>= 1;
+  }
+  return r;
+}
+__device__ __forceinline__ float mo_pow_(float x, float y) { return powf(x, y); }
+__device__ __forceinline__ double mo_pow_(double x, double y) { return pow(x, y); }
+__device__ __forceinline__ float mo_sqrt_(float x) { return sqrtf(x); }
+__device__ __forceinline__ double mo_sqrt_(double x) { return sqrt(x); }
+template <class Real>
+__device__ __forceinline__ Real mo_pow_eval(Real x, long long num, long long den) {
+  if (den == 1) {
+    if (num >= -32 && num <= 32) return mo_ipow(x, num);
+    return mo_pow_(x, Real(num));
+  }
+  if (den == 2) return mo_ipow(mo_sqrt_(x), num);
+  return mo_pow_(x, Real(num) / Real(den));
+}
+
+// Deterministic block sum (fixed shuffle tree, fixed warp order).
+__device__ __forceinline__ double mo_block_sum(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int tid = threadIdx.x + threadIdx.y * blockDim.x;
+  const int nw = (blockDim.x * blockDim.y + 31) >> 5;
+  if ((tid & 31) == 0) sh[tid >> 5] = v;
+  __syncthreads();
+  double t = 0;
+  if (tid < 32) {
+    t = tid < nw ? sh[tid] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+  }
+  __syncthreads();
+  return t;  // valid in thread 0
+}
+
+// Scalar finalisation: a single thread, after the reduction total is known.
+template <class Real>
+__device__ void mo_finalize(mo_state* st, int op, int arg, double total, double total2) {
+  switch (op) {
+    case MO_FIN_STORE: st->sums[arg] = total; break;
+    case MO_FIN_STORE2:
+      st->sums[arg] = total;
+      st->sums[arg + 1] = total2;
+      break;
+    case MO_FIN_UNCONSTRAINED: st->unconstrained = (long long)total; break;
+    case MO_FIN_PCG_INIT: {
+      Real rz = Real(total);
+      st->rz = double(rz);
+      if (!mo_finite(double(rz))) {
+        st->nonfinite = 1;
+        st->done = 1;
+        break;
+      }
+      Real tr = Real(st->tol_rel);
+      Real stop = tr * tr * rz;
+      Real ta = Real(st->tol_abs);
+      if (ta > stop) stop = ta;
+      st->stop = double(stop);
+      if (rz <= stop) st->done = 1;
+      break;
+    }
+    case MO_FIN_PCG_ALPHA: {
+      Real pap = Real(total);
+      st->pap = double(pap);
+      if (!mo_finite(double(pap))) {
+        st->nonfinite = 1;
+        st->done = 1;
+      } else if (pap <= Real(0)) {
+        st->indefinite = 1;
+        st->done = 1;
+      } else {
+        st->alpha = double(Real(st->rz) / pap);
+      }
+      break;
+    }
+    case MO_FIN_PCG_BETA: {
+      Real rzn = Real(total);
+      st->rz_next = double(rzn);
+      if (!mo_finite(double(rzn))) {
+        st->nonfinite = 1;
+        st->done = 1;
+        break;
+      }
+      st->iters += 1;
+      if (rzn <= Real(st->stop)) {
+        st->done = 1;
+        break;
+      }
+      st->beta = double(rzn / Real(st->rz));
+      st->rz = double(rzn);
+      break;
+    }
+  }
+}
+
+// Block epilogue of a (possibly multi-kernel) deterministic reduction: each
+// block writes its partial(s); the last block to arrive sums all partials in
+// index order (fixed assignment to threads, fixed tree) and finalises.
+// Must be called by every thread of the block.
+template <class Real>
+__device__ void mo_reduce_epilogue(const mo_red& P, double v, double v2, bool two) {
+  __shared__ double sh[32];
+  __shared__ bool am_last;
+  const int tid = threadIdx.x + threadIdx.y * blockDim.x;
+  const int nt = blockDim.x * blockDim.y;
+  const int bid = blockIdx.x;
+  double s = mo_block_sum(v, sh);
+  double s2 = two ? mo_block_sum(v2, sh) : 0.0;
+  if (tid == 0) {
+    P.partials[P.part_base + bid] = s;
+    if (two) P.partials[P.part_total + P.part_base + bid] = s2;
+    __threadfence();
+    unsigned t = atomicAdd(P.counter, 1u);
+    am_last = (t == unsigned(P.part_total - 1));
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  double a = 0, a2 = 0;
+  const volatile double* pp = P.partials;
+  for (int i = tid; i < P.part_total; i += nt) {
+    a += pp[i];
+    if (two) a2 += pp[P.part_total + i];
+  }
+  double tot = mo_block_sum(a, sh);
+  double tot2 = two ? mo_block_sum(a2, sh) : 0.0;
+  if (tid == 0) {
+    *P.counter = 0u;
+    mo_finalize<Real>(P.state, P.fin_op, P.fin_arg, tot, tot2);
+  }
+}
+
+// Grid-stride tile iteration for a grid domain (reference exec.hpp:151-214:
+// one program run per element; here one thread per element of a 32x8 tile,
+// fastest axis on threadIdx.x).  Returns the number of tiles.
+__device__ __forceinline__ int mo_num_tiles(const mo_kparams& P) {
+  const int rows = P.row1 - P.row0;
+  if (rows <= 0) return 0;
+  if (P.dnd == 1) return (rows + MO_THREADS - 1) / MO_THREADS;
+  const int fx = P.dnd == 2 ? P.d1 : P.d2;
+  const int ntx = (fx + MO_TILE_X - 1) / MO_TILE_X;
+  const int nty = P.dnd == 2 ? (rows + MO_TILE_Y - 1) / MO_TILE_Y : rows * ((P.d1 + MO_TILE_Y - 1) / MO_TILE_Y);
+  return ntx * nty;
+}
+
+// Coordinates (global) of this thread's element in tile t; false if outside.
+__device__ __forceinline__ bool mo_tile_coord(const mo_kparams& P, int t, int& p0, int& p1, int& p2) {
+  const int tid = threadIdx.x + threadIdx.y * blockDim.x;
+  if (P.dnd == 1) {
+    p0 = P.row0 + t * MO_THREADS + tid;
+    p1 = 0;
+    p2 = 0;
+    return p0 < P.row1;
+  }
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  if (P.dnd == 2) {
+    const int ntx = (P.d1 + MO_TILE_X - 1) / MO_TILE_X;
+    const int bx = t % ntx, by = t / ntx;
+    p0 = P.row0 + by * MO_TILE_Y + ty;
+    p1 = bx * MO_TILE_X + tx;
+    p2 = 0;
+    return p0 < P.row1 && p1 < P.d1;
+  }
+  const int ntx = (P.d2 + MO_TILE_X - 1) / MO_TILE_X;
+  const int nty = (P.d1 + MO_TILE_Y - 1) / MO_TILE_Y;
+  const int bx = t % ntx;
+  const int r = t / ntx;
+  const int by = r % nty;
+  p0 = P.row0 + r / nty;
+  p1 = by * MO_TILE_Y + ty;
+  p2 = bx * MO_TILE_X + tx;
+  return p0 < P.row1 && p1 < P.d1 && p2 < P.d2;
+}
+
+// Local (storage) element index of a global coordinate on the iteration domain.
+__device__ __forceinline__ int mo_local_elem(const mo_kparams& P, int p0, int p1, int p2) {
+  if (P.dnd == 1) return p0 - P.row_lo;
+  if (P.dnd == 2) return (p0 - P.row_lo) * P.d1 + p1;
+  return ((p0 - P.row_lo) * P.d1 + p1) * P.d2 + p2;
+}
+
+// InBounds against the iteration domain (eval.hpp:57-61).
+__device__ __forceinline__ bool mo_inb(const mo_kparams& P, int c0, int c1, int c2) {
+  if ((unsigned)c0 >= (unsigned)P.d0) return false;
+  if (P.dnd >= 2 && (unsigned)c1 >= (unsigned)P.d1) return false;
+  if (P.dnd >= 3 && (unsigned)c2 >= (unsigned)P.d2) return false;
+  return true;
+}
+
+// Grid read with the OOB->0 rule against the FIELD's own shape (eval.hpp:41-55).
+template <class Real, int ND, int C>
+__device__ __forceinline__ Real mo_ld(const mo_view& v, int c0, int c1, int c2, int ch) {
+  if ((unsigned)c0 >= (unsigned)v.s0) return Real(0);
+  if (ND >= 2 && (unsigned)c1 >= (unsigned)v.s1) return Real(0);
+  if (ND >= 3 && (unsigned)c2 >= (unsigned)v.s2) return Real(0);
+  int e = c0 - v.row_lo;
+  if (ND >= 2) e = e * v.s1 + c1;
+  if (ND >= 3) e = e * v.s2 + c2;
+  return __ldg(reinterpret_cast<const Real*>(v.p) + (long long)e * C + ch);
+}
+
+// Slot read (eval.hpp:43-45): vertex validated on the host before any launch.
+template <class Real, int C>
+__device__ __forceinline__ Real mo_ldv(const mo_view& v, int vert, int ch) {
+  return __ldg(reinterpret_cast<const Real*>(v.p) + (long long)vert * C + ch);
+}
+
+#endif  // MO_DEVICE_CUH_

@@ -1,0 +1,231 @@
+// mo_kernels.cuh — hand-written sm_100a kernels of the solver loop: Jacobi PCG
+// vector updates with fused deterministic reductions (pcg.hpp:63-130), LM
+// bookkeeping (solver.hpp:427-501), the build_normal identity patch
+// (solver.hpp:241-250), exclusion column masks (solver.hpp:137-157) and the
+// deterministic vertex-centric graph gather that replaces the reference's
+// atomic scatter (exec.hpp:265-282).
+//
+// Vector kernels are grid-stride over columns with a FIXED grid, so the
+// assignment of columns to threads (and therefore every reduction) is
+// reproducible run to run.  Column i of every vector is excluded iff
+// colmask[i] != 0 (the reference's per-column `excluded_`).
+#pragma once
+
+#include "mo_device.cuh"
+
+namespace mo {
+
+__device__ __forceinline__ bool ex_at(const unsigned char* cm, long long i) { return cm && cm[i]; }
+
+// delta = 0; r = b; z = r/m; p = z; rz = r'z   (pcg.hpp:75-97)
+template <class Real>
+__global__ void __launch_bounds__(MO_THREADS)
+k_pcg_init(mo_red R, long long n, const unsigned char* cm, const Real* __restrict__ b,
+           const Real* __restrict__ md, Real* __restrict__ delta, Real* __restrict__ r,
+           Real* __restrict__ p, int precond) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    R.state->done = 0;
+    R.state->iters = 0;
+    R.state->indefinite = 0;
+    R.state->nonfinite = 0;
+  }
+  double acc = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const bool ex = ex_at(cm, i);
+    const Real ri = ex ? Real(0) : b[i];
+    const Real zi = ex ? Real(0) : (precond ? ri / md[i] : ri);
+    delta[i] = Real(0);
+    r[i] = ri;
+    p[i] = zi;
+    acc += double(ri * zi);
+  }
+  mo_reduce_epilogue<Real>(R, acc, 0.0, false);
+}
+
+// delta += alpha p; r -= alpha Ap; z = r/m; rz' = r'z   (pcg.hpp:111-118)
+template <class Real>
+__global__ void __launch_bounds__(MO_THREADS)
+k_pcg_update(mo_red R, long long n, const unsigned char* cm, const Real* __restrict__ md,
+             Real* __restrict__ delta, Real* __restrict__ r, const Real* __restrict__ p,
+             const Real* __restrict__ ap, int precond) {
+  if (R.state->done) return;
+  const Real alpha = Real(R.state->alpha);
+  double acc = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    if (ex_at(cm, i)) {
+      delta[i] = Real(0);
+      r[i] = Real(0);
+      continue;
+    }
+    const Real d = delta[i] + alpha * p[i];
+    const Real ri = r[i] - alpha * ap[i];
+    const Real zi = precond ? ri / md[i] : ri;
+    delta[i] = d;
+    r[i] = ri;
+    acc += double(ri * zi);
+  }
+  mo_reduce_epilogue<Real>(R, acc, 0.0, false);
+}
+
+// p = z + beta p with z = r/m recomputed   (pcg.hpp:124-126)
+template <class Real>
+__global__ void __launch_bounds__(MO_THREADS)
+k_pcg_p(const mo_state* st, long long n, const unsigned char* cm, const Real* __restrict__ md,
+        const Real* __restrict__ r, Real* __restrict__ p, int precond) {
+  if (st->done) return;
+  const Real beta = Real(st->beta);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    if (ex_at(cm, i)) {
+      p[i] = Real(0);
+      continue;
+    }
+    const Real zi = precond ? r[i] / md[i] : r[i];
+    p[i] = zi + beta * p[i];
+  }
+}
+
+// Unfused apply epilogue (plans with graph scatters): LM damping, excluded
+// zeroing, p'Ap -> alpha.
+template <class Real>
+__global__ void __launch_bounds__(MO_THREADS)
+k_apply_finish(mo_red R, long long n, const unsigned char* cm, const Real* __restrict__ p,
+               const Real* __restrict__ damp, Real* __restrict__ ap, int flags) {
+  if ((flags & MO_F_REDUCE) && R.state->done) return;
+  double acc = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    Real v = ap[i];
+    if (flags & MO_F_DAMP) v = v + damp[i] * p[i];
+    if ((flags & MO_F_ZEROEXCL) && ex_at(cm, i)) v = Real(0);
+    ap[i] = v;
+    acc += double(p[i] * v);
+  }
+  if (flags & MO_F_REDUCE) mo_reduce_epilogue<Real>(R, acc, 0.0, false);
+}
+
+// Identity rows for excluded columns, m==0 -> 1 (solver.hpp:241-250).
+template <class Real>
+__global__ void __launch_bounds__(MO_THREADS)
+k_bm_patch(mo_red R, long long n, const unsigned char* cm, Real* __restrict__ b, Real* __restrict__ m) {
+  double cnt = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    if (ex_at(cm, i)) {
+      b[i] = Real(0);
+      m[i] = Real(1);
+    } else if (m[i] == Real(0)) {
+      cnt += 1.0;
+      m[i] = Real(1);
+    }
+  }
+  mo_reduce_epilogue<Real>(R, cnt, 0.0, false);
+}
+
+// Per-column exclusion from a per-element mask (solver.hpp:149-157).
+__global__ void __launch_bounds__(MO_THREADS)
+k_colmask(long long nelem, int C, const unsigned char* __restrict__ mask, unsigned char* __restrict__ cm) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nelem;
+       e += (long long)gridDim.x * blockDim.x) {
+    const unsigned char v = mask[e];
+    for (int c = 0; c < C; ++c) cm[e * C + c] = v;
+  }
+}
+
+// LM: base_diag = clamp(m/2, dmin, dmax) in double (solver.hpp:427-429).
+template <class Real>
+__global__ void __launch_bounds__(MO_THREADS)
+k_lm_base_diag(long long n, const Real* __restrict__ m, double* __restrict__ bd, double dmin, double dmax) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double v = double(m[i]) / 2.0;
+    bd[i] = v < dmin ? dmin : (dmax < v ? dmax : v);
+  }
+}
+
+// LM: damp = excluded ? 0 : 2/mu * base_diag; md = m + damp (solver.hpp:433-438).
+template <class Real>
+__global__ void __launch_bounds__(MO_THREADS)
+k_lm_damp(long long n, const unsigned char* cm, const Real* __restrict__ m, const double* __restrict__ bd,
+          Real* __restrict__ damp, Real* __restrict__ md, double mu) {
+  const double s = 2.0 / mu;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const Real d = ex_at(cm, i) ? Real(0) : Real(s * bd[i]);
+    damp[i] = d;
+    md[i] = m[i] + d;
+  }
+}
+
+// x_trial = excluded ? x : x + delta; flags any delta != 0 (solver.hpp:448-449, 486-492).
+// in_place (GN, commit unconditional unless cost_old / PCG were non-finite).
+template <class Real>
+__global__ void __launch_bounds__(MO_THREADS)
+k_xtrial(mo_state* st, long long n, const unsigned char* cm, Real* __restrict__ x,
+         const Real* __restrict__ delta, Real* __restrict__ xt, int in_place, int cost_slot) {
+  if (in_place && (st->nonfinite || !mo_finite(st->sums[cost_slot]))) return;
+  bool nz = false;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const Real d = delta[i];
+    if (d != Real(0)) nz = true;
+    const Real xi = x[i];
+    const Real v = ex_at(cm, i) ? xi : xi + d;
+    if (in_place) x[i] = v;
+    else xt[i] = v;
+  }
+  if (__syncthreads_or(nz) && threadIdx.x == 0) atomicOr(&st->any_nonzero, 1);
+}
+
+// LM predicted decrease pieces in double (solver.hpp:468-473):
+// sums[arg] = sum b*delta, sums[arg+1] = sum (0.5*delta)*JtJdelta.
+template <class Real>
+__global__ void __launch_bounds__(MO_THREADS)
+k_lm_predicted(mo_red R, long long n, const Real* __restrict__ b, const Real* __restrict__ delta,
+               const Real* __restrict__ ap) {
+  double s1 = 0, s2 = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    s1 += double(b[i]) * double(delta[i]);
+    s2 += 0.5 * double(delta[i]) * double(ap[i]);
+  }
+  mo_reduce_epilogue<Real>(R, s1, s2, true);
+}
+
+// Deterministic graph scatter (replaces exec.hpp:265-282's sequential `+=` /
+// parallel atomics).  One thread per target vertex v of one domain; incident
+// edges are visited in ascending edge order and, within an edge, outputs in
+// program order — exactly the per-column accumulation order of the
+// reference's sequential executor, without any floating-point atomics.
+struct mo_gather_out {
+  int slot;     // edge slot the output scatters through
+  int sel;      // 0 -> dst0, 1 -> dst1 (bm: b/m)
+  int C;        // channels of the target field
+  int active;   // target field lives on this launch's domain
+  long long cbase;  // ubase[field] + channel
+};
+
+template <class Real>
+__global__ void __launch_bounds__(MO_THREADS)
+k_graph_gather(long long nverts, const int* __restrict__ vptr, const int* __restrict__ vedge,
+               const int* __restrict__ verts, int arity, const Real* __restrict__ contrib, int NO,
+               const mo_gather_out* __restrict__ outs, Real* dst0, Real* dst1) {
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < nverts;
+       v += (long long)gridDim.x * blockDim.x) {
+    const int j0 = vptr[v], j1 = vptr[v + 1];
+    for (int j = j0; j < j1; ++j) {
+      const long long e = vedge[j];
+      for (int k = 0; k < NO; ++k) {
+        const mo_gather_out o = outs[k];
+        if (!o.active || verts[e * arity + o.slot] != int(v)) continue;
+        Real* d = o.sel ? dst1 : dst0;
+        const long long col = o.cbase + v * o.C;
+        d[col] = d[col] + contrib[e * NO + k];
+      }
+    }
+  }
+}
+
+}  // namespace mo

@@ -1,0 +1,1055 @@
+// mo_session.cu — device-resident solver session: the B200 replacement of
+// minopt::Solver<Real> (solver.hpp:80-635) and its executor/PCG layers
+// (exec.hpp, pcg.hpp).  One session = one device, one stream, all vectors in
+// HBM in the reference column layout.
+//
+// Per nonlinear iteration (solver.hpp:415-509) the host issues:
+//   refresh    computed arrays + exclusion masks            (125-168)
+//   cost       generated cost kernels, deterministic reduce (174-193)
+//   normal     generated b/m gather (+ graph gather, patch) (220-251)
+//   PCG        init + linear_iters x {apply+p'Ap, update+r'z, p} (pcg.hpp:63-130),
+//              captured once into a CUDA graph, device-side scalars/stop flags
+//   step       x_trial / in-place GN step, trial cost, LM predicted decrease
+// and synchronises once to read the scalar state for the trace row.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <limits>
+#include <string>
+
+#include "mo_codegen.hpp"
+#include "mo_jit.hpp"
+#include "mo_kernels.cuh"
+#include "mo_session.hpp"
+
+namespace mo {
+
+const char* device_prelude();
+
+#define CK(x)                                                                        \
+  do {                                                                               \
+    cudaError_t e_ = (x);                                                            \
+    if (e_ != cudaSuccess) fail(Err::kCuda, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+namespace {
+
+constexpr int kPartCap = 1 << 18;
+enum { SLOT_COST = 0, SLOT_PRED = 2 };
+
+template <class T>
+T* dalloc(size_t n) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  CK(cudaMalloc(&p, n * sizeof(T)));
+  return static_cast<T*>(p);
+}
+
+int vgrid(long long n, int nsm) {
+  long long g = (n + MO_THREADS - 1) / MO_THREADS;
+  long long cap = (long long)nsm * 8;
+  if (g > cap) g = cap;
+  return int(std::max<long long>(g, 1));
+}
+
+}  // namespace
+
+template <class Real>
+class Session final : public SessionBase {
+ public:
+  Session(const Plan& plan, int device) : P_(plan), dev_(device) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      fail(Err::kNoDevice, "no CUDA device available (the B200 path has no CPU fallback)");
+    check(device >= 0 && device < ndev, Err::kNoDevice, "device index out of range");
+    CK(cudaSetDevice(dev_));
+    CK(cudaDeviceGetAttribute(&nsm_, cudaDevAttrMultiProcessorCount, dev_));
+    CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+    cfg_ = P_.cfg;
+    if (cfg_.pcg_rel_tol < 0) cfg_.pcg_rel_tol = cfg_.precision == 0 ? 1e-4 : 1e-8;
+
+    // JIT the plan's per-element kernels (plan time; cached on disk).
+    std::string src = generate_module(P_, sizeof(Real) == 8, device_prelude());
+    mod_.load(compile_cubin(src, "mo_plan.cu"));
+
+    const size_t n = size_t(P_.num_cols);
+    x_ = dalloc<Real>(n);
+    xt_ = dalloc<Real>(n);
+    b_ = dalloc<Real>(n);
+    m_ = dalloc<Real>(n);
+    md_ = dalloc<Real>(n);
+    damp_ = dalloc<Real>(n);
+    delta_ = dalloc<Real>(n);
+    r_ = dalloc<Real>(n);
+    p_ = dalloc<Real>(n);
+    ap_ = dalloc<Real>(n);
+    vtmp_ = dalloc<Real>(n);
+    otmp_ = dalloc<Real>(n);
+    bd_ = dalloc<double>(n);
+    CK(cudaMemsetAsync(damp_, 0, n * sizeof(Real), st_));
+    CK(cudaMemsetAsync(x_, 0, n * sizeof(Real), st_));
+    arr_.resize(P_.arrays.size(), nullptr);
+    arr_n_.assign(P_.arrays.size(), -1);
+    for (size_t i = 0; i < P_.arrays.size(); ++i)
+      arr_[i] = dalloc<Real>(size_t(P_.extent_of(P_.arrays[i].dom) * P_.arrays[i].channels));
+    comp_.resize(P_.computed.size(), nullptr);
+    for (size_t i = 0; i < P_.computed.size(); ++i)
+      comp_[i] = dalloc<Real>(size_t(P_.extent_of(P_.computed[i].dom) * P_.computed[i].channels));
+    masks_.resize(P_.exclude_kernels.size(), nullptr);
+    for (size_t i = 0; i < P_.exclude_kernels.size(); ++i)
+      masks_[i] = dalloc<unsigned char>(size_t(P_.extent_of(P_.exclude_kernels[i].dom)));
+    if (!P_.exclude_kernels.empty()) colmask_ = dalloc<unsigned char>(n);
+    params_d_ = dalloc<double>(std::max<size_t>(P_.params.size(), 1));
+    state_ = dalloc<mo_state>(1);
+    CK(cudaMallocHost(&state_h_, sizeof(mo_state)));
+    std::memset(state_h_, 0, sizeof(mo_state));
+    state_h_->tol_rel = cfg_.pcg_rel_tol;
+    state_h_->tol_abs = cfg_.pcg_abs_tol;
+    state_h_->use_precond = cfg_.use_preconditioner;
+    CK(cudaMemcpyAsync(state_, state_h_, sizeof(mo_state), cudaMemcpyHostToDevice, st_));
+    partials_ = dalloc<double>(2 * size_t(kPartCap));
+    graphs_.resize(P_.graphs.size());
+    gsets_.resize(P_.graph_sets.size());
+    grid_rowbase_.resize(P_.grid_sets.size(), nullptr);
+    for (size_t i = 0; i < P_.grid_sets.size(); ++i)
+      grid_rowbase_[i] = dalloc<long long>(P_.grid_sets[i].templates.size());
+    for (size_t i = 0; i < P_.graph_sets.size(); ++i) setup_graph_set(int(i));
+    CK(cudaStreamSynchronize(st_));
+  }
+
+  ~Session() override {
+    cudaSetDevice(dev_);
+    cudaStreamSynchronize(st_);
+    for (auto& kv : pcg_exec_) cudaGraphExecDestroy(kv.second);
+    for (void* p : owned_) cudaFree(p);
+    for (Real* p : {x_, xt_, b_, m_, md_, damp_, delta_, r_, p_, ap_, vtmp_, otmp_, resid_}) cudaFree(p);
+    cudaFree(bd_);
+    for (Real* p : arr_) cudaFree(p);
+    for (Real* p : comp_) cudaFree(p);
+    for (unsigned char* p : masks_) cudaFree(p);
+    cudaFree(colmask_);
+    cudaFree(params_d_);
+    cudaFree(state_);
+    cudaFree(partials_);
+    cudaFreeHost(state_h_);
+    for (auto& g : graphs_) cudaFree(g.d_verts);
+    for (auto& gs : gsets_) {
+      cudaFree(gs.contrib);
+      cudaFree(gs.rowbase);
+      for (auto& d : gs.doms) {
+        cudaFree(d.vptr);
+        cudaFree(d.vedge);
+        cudaFree(d.outs_bm);
+        cudaFree(d.outs_jtj);
+      }
+    }
+    for (auto& pe : prof_) {
+      for (auto& ev : pe.ev) {
+        cudaEventDestroy(ev.first);
+        cudaEventDestroy(ev.second);
+      }
+    }
+    cudaStreamDestroy(st_);
+  }
+
+  // ------------------------------------------------------------ binding
+  void bind_x(const void* x, int64_t n, bool device) override {
+    check(n == P_.num_cols, Err::kBindError, "unknown vector size does not match the plan layout");
+    CK(cudaSetDevice(dev_));
+    CK(cudaMemcpyAsync(x_, x, size_t(n) * sizeof(Real), device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st_));
+    CK(cudaStreamSynchronize(st_));
+    x_bound_ = true;
+  }
+  void bind_array(int i, const void* d, int64_t n, bool device) override {
+    check(i >= 0 && size_t(i) < P_.arrays.size(), Err::kBindError, "array count does not match the declaration");
+    const ArrayFieldSize want = array_size(i);
+    check(n == want, Err::kBindError, "array '" + P_.arrays[size_t(i)].name + "' has the wrong size");
+    CK(cudaSetDevice(dev_));
+    CK(cudaMemcpyAsync(arr_[size_t(i)], d, size_t(n) * sizeof(Real), device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st_));
+    CK(cudaStreamSynchronize(st_));
+    arr_n_[size_t(i)] = n;
+  }
+  void bind_params(const double* p, int64_t n) override {
+    check(size_t(n) == P_.params.size(), Err::kBindError, "parameter count does not match the declaration");
+    CK(cudaSetDevice(dev_));
+    if (n) CK(cudaMemcpyAsync(params_d_, p, size_t(n) * sizeof(double), cudaMemcpyHostToDevice, st_));
+    CK(cudaStreamSynchronize(st_));
+    params_bound_ = true;
+  }
+  void bind_graph(int i, const uint64_t* verts, int64_t n, int arity) override {
+    check(i >= 0 && size_t(i) < P_.graphs.size(), Err::kBindError, "graph count does not match the declaration");
+    GraphData& g = graphs_[size_t(i)];
+    g.arity = arity;
+    g.verts.assign(verts, verts + n);
+    g.bound = true;
+    g.dirty = true;
+  }
+
+  // refresh(): solver.hpp:125-168
+  void refresh() override {
+    CK(cudaSetDevice(dev_));
+    validate();
+    upload_graphs();
+    for (const ComputedKernel& ck : P_.computed_kernels) {
+      mo_kparams kp = kp_grid(ck.dom, x_, nullptr);
+      kp.out0 = comp_[size_t(ck.index)];
+      launch_grid("mo_computed_" + std::to_string(&ck - P_.computed_kernels.data()), ck.dom, kp);
+    }
+    for (size_t i = 0; i < P_.exclude_kernels.size(); ++i) {
+      const ExcludeKernel& ek = P_.exclude_kernels[i];
+      mo_kparams kp = kp_grid(ek.dom, x_, nullptr);
+      kp.out0 = masks_[i];
+      launch_grid("mo_exclude_" + std::to_string(i), ek.dom, kp);
+    }
+    if (colmask_) {
+      CK(cudaMemsetAsync(colmask_, 0, size_t(P_.num_cols), st_));
+      for (size_t i = 0; i < P_.exclude_kernels.size(); ++i)
+        for (size_t f = 0; f < P_.unknowns.size(); ++f) {
+          if (!(P_.unknowns[f].dom == P_.exclude_kernels[i].dom)) continue;
+          long long ne = P_.extent_of(P_.unknowns[f].dom);
+          k_colmask<<<vgrid(ne, nsm_), MO_THREADS, 0, st_>>>(ne, P_.unknowns[f].channels, masks_[i],
+                                                           colmask_ + P_.ubase[f]);
+          ++launches_;
+        }
+    }
+    // Residual row offsets (graph sizes may change through callbacks).
+    rowbase_.assign(P_.residuals.size(), 0);
+    int64_t row = 0;
+    for (size_t t = 0; t < P_.residuals.size(); ++t) {
+      rowbase_[t] = row;
+      const Residual& r = P_.residuals[t];
+      row += r.graph ? graphs_[size_t(r.graph_idx)].E : P_.extent_of(r.dom);
+    }
+    rows_ = row;
+    for (size_t i = 0; i < P_.grid_sets.size(); ++i) {
+      std::vector<long long> rb;
+      for (int t : P_.grid_sets[i].templates) rb.push_back(rowbase_[size_t(t)]);
+      CK(cudaMemcpyAsync(grid_rowbase_[i], rb.data(), rb.size() * sizeof(long long), cudaMemcpyHostToDevice, st_));
+      CK(cudaStreamSynchronize(st_));
+    }
+    for (size_t i = 0; i < P_.graph_sets.size(); ++i) {
+      std::vector<long long> rb;
+      for (int t : P_.graph_sets[i].templates) rb.push_back(rowbase_[size_t(t)]);
+      CK(cudaMemcpyAsync(gsets_[i].rowbase, rb.data(), rb.size() * sizeof(long long), cudaMemcpyHostToDevice, st_));
+      CK(cudaStreamSynchronize(st_));
+    }
+    refreshed_ = true;
+  }
+
+  int64_t num_cols() const override { return P_.num_cols; }
+  int64_t num_rows() override {
+    ensure_refreshed();
+    return rows_;
+  }
+  void excluded(uint8_t* out, int64_t n) override {
+    ensure_refreshed();
+    check(n == P_.num_cols, Err::kShapeMismatch, "excluded(): size mismatch");
+    if (!colmask_) {
+      std::memset(out, 0, size_t(n));
+      return;
+    }
+    CK(cudaMemcpyAsync(out, colmask_, size_t(n), cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+  }
+
+  // ------------------------------------------------------------ routines
+  double cost() override {
+    ensure_refreshed();
+    cost_at(x_, SLOT_COST);
+    sync_state();
+    return state_h_->sums[SLOT_COST];
+  }
+
+  void residuals(void* out, int64_t n) override {
+    ensure_refreshed();
+    check(n == rows_, Err::kShapeMismatch, "residual vector size does not match the instance count");
+    if (size_t(n) > resid_cap_) {
+      cudaFree(resid_);
+      resid_ = dalloc<Real>(size_t(n));
+      resid_cap_ = size_t(n);
+    }
+    for (size_t i = 0; i < P_.grid_sets.size(); ++i) {
+      mo_kparams kp = kp_grid(P_.grid_sets[i].dom, x_, nullptr);
+      kp.out0 = resid_;
+      kp.rowbase = grid_rowbase_[i];
+      launch_grid("mo_grid_evalf_" + std::to_string(i), P_.grid_sets[i].dom, kp);
+    }
+    for (size_t i = 0; i < P_.graph_sets.size(); ++i) {
+      mo_kparams kp = kp_graph(int(i), x_, nullptr);
+      kp.out0 = resid_;
+      kp.rowbase = gsets_[i].rowbase;
+      launch_edges("mo_graph_evalf_" + std::to_string(i), int(i), kp);
+    }
+    if (n) CK(cudaMemcpyAsync(out, resid_, size_t(n) * sizeof(Real), cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+  }
+
+  void build_normal() override {
+    ensure_refreshed();
+    normal_device();
+    sync_state();
+    unconstrained_ = state_h_->unconstrained;
+  }
+  void get_rhs(void* out, int64_t n) override { download(b_, out, n); }
+  void get_precond(void* out, int64_t n) override { download(m_, out, n); }
+
+  void apply_jtj(const void* v, void* out, int64_t n, bool device) override {
+    ensure_refreshed();
+    check(n == P_.num_cols, Err::kShapeMismatch, "apply_jtj(): vector size mismatch");
+    if (device) {
+      apply(static_cast<const Real*>(v), static_cast<Real*>(out), 0);
+      CK(cudaStreamSynchronize(st_));
+      return;
+    }
+    if (n) CK(cudaMemcpyAsync(vtmp_, v, size_t(n) * sizeof(Real), cudaMemcpyHostToDevice, st_));
+    apply(vtmp_, otmp_, 0);
+    download(otmp_, out, n);
+  }
+
+  void get_x(void* out, int64_t n) override { download(x_, out, n); }
+  bool saw_nonfinite() override {
+    sync_state();
+    return state_h_->nonfinite_kernel != 0;
+  }
+
+  // ------------------------------------------------------------ solve
+  SolveResult solve(IterCallback cb, void* user) override {
+    using clock = std::chrono::steady_clock;
+    CK(cudaSetDevice(dev_));
+    const bool lm = cfg_.method == 1;
+    SolveResult res;
+    double mu = cfg_.lm_radius0, nu = 2.0;
+    auto t_prev = clock::now();
+    auto take_ms = [&] {
+      auto now = clock::now();
+      double ms = std::chrono::duration<double, std::milli>(now - t_prev).count();
+      t_prev = now;
+      return ms;
+    };
+    auto finish = [&] {
+      sync_state();
+      res.nonfinite_kernels = state_h_->nonfinite_kernel != 0;
+      res.unconstrained = unconstrained_;
+    };
+
+    for (int it = 0; it < cfg_.nonlinear_iters; ++it) {
+      refresh();
+      cost_at(x_, SLOT_COST);
+      sync_state();
+      const double cost_old = state_h_->sums[SLOT_COST];
+      if (!std::isfinite(cost_old)) {
+        res.trace.push_back({it, cost_old, false, lm ? mu : 0.0, 0, take_ms()});
+        res.reason = 3;
+        res.final_cost = cost_old;
+        finish();
+        return res;
+      }
+      normal_device();
+      if (lm) {
+        long long n = P_.num_cols;
+        k_lm_base_diag<Real><<<vgrid(n, nsm_), MO_THREADS, 0, st_>>>(n, m_, bd_, cfg_.lm_diag_min, cfg_.lm_diag_max);
+        ++launches_;
+      }
+      double cost_after = cost_old;
+      bool stepped = false;
+      while (!stepped) {
+        const long long n = P_.num_cols;
+        if (lm) {
+          k_lm_damp<Real><<<vgrid(n, nsm_), MO_THREADS, 0, st_>>>(n, colmask_, m_, bd_, damp_, md_, mu);
+          ++launches_;
+        }
+        run_pcg(lm);
+        CK(cudaMemsetAsync(&state_->any_nonzero, 0, sizeof(int), st_));
+        if (lm) {
+          k_xtrial<Real><<<vgrid(n, nsm_), MO_THREADS, 0, st_>>>(state_, n, colmask_, x_, delta_, xt_, 0, SLOT_COST);
+          ++launches_;
+          cost_at(xt_, SLOT_COST + 1);
+          apply(delta_, ap_, 0);  // undamped model curvature (solver.hpp:467)
+          mo_red R = red(0, vgrid(n, nsm_), MO_FIN_STORE2, SLOT_PRED);
+          k_lm_predicted<Real><<<vgrid(n, nsm_), MO_THREADS, 0, st_>>>(R, n, b_, delta_, ap_);
+          ++launches_;
+        } else {
+          // GN: the step is unconditional (solver.hpp:452); committed in place
+          // unless cost_old or the PCG recurrence went non-finite.
+          k_xtrial<Real><<<vgrid(n, nsm_), MO_THREADS, 0, st_>>>(state_, n, colmask_, x_, delta_, xt_, 1, SLOT_COST);
+          ++launches_;
+          cost_at(x_, SLOT_COST + 1);
+        }
+        sync_state();
+        collect_profile();
+        const mo_state S = *state_h_;
+        unconstrained_ = S.unconstrained;
+        res.indefinite_operator |= S.indefinite != 0;
+        if (S.nonfinite && !lm) {
+          res.reason = 3;
+          res.final_cost = cost_old;
+          res.trace.push_back({it, cost_old, false, 0.0, S.iters, take_ms()});
+          finish();
+          return res;
+        }
+        const double cost_new = S.nonfinite ? std::numeric_limits<double>::infinity() : S.sums[SLOT_COST + 1];
+        if (!lm) {
+          res.trace.push_back({it, cost_new, true, 0.0, S.iters, take_ms()});
+          if (!std::isfinite(cost_new)) {
+            res.reason = 3;
+            res.final_cost = cost_new;
+            finish();
+            return res;
+          }
+          cost_after = cost_new;
+          stepped = true;
+          break;
+        }
+        double predicted = 0.0 - S.sums[SLOT_PRED + 1];
+        predicted += S.sums[SLOT_PRED];
+        double rho = predicted > 0 ? (cost_old - cost_new) / predicted : -1.0;
+        if (std::isfinite(cost_new) && predicted > 0 && rho > cfg_.lm_min_decrease) {
+          CK(cudaMemcpyAsync(x_, xt_, size_t(n) * sizeof(Real), cudaMemcpyDeviceToDevice, st_));
+          double shrink = std::max(1.0 / 3.0, 1.0 - std::pow(2.0 * rho - 1.0, 3));
+          res.trace.push_back({it, cost_new, true, mu, S.iters, take_ms()});
+          mu = std::clamp(mu / shrink, cfg_.lm_radius_min, cfg_.lm_radius_max);
+          nu = 2.0;
+          cost_after = cost_new;
+          stepped = true;
+        } else {
+          res.trace.push_back({it, cost_new, false, mu, S.iters, take_ms()});
+          const bool zero_step = S.any_nonzero == 0;
+          mu /= nu;
+          nu *= 2.0;
+          if (zero_step || mu < cfg_.lm_radius_min) {
+            res.reason = 2;
+            res.final_cost = cost_old;
+            finish();
+            return res;
+          }
+        }
+      }
+      if (cb) {
+        CK(cudaStreamSynchronize(st_));
+        cb(it, user);
+      }
+      double rel = (cost_old - cost_after) / std::max(cost_old, 1e-300);
+      if (rel >= 0 && rel < cfg_.cost_stop_tol) {
+        res.reason = 1;
+        break;
+      }
+    }
+    refresh();
+    res.final_cost = cost();
+    if (!std::isfinite(res.final_cost)) res.reason = 3;
+    finish();
+    return res;
+  }
+
+  // ------------------------------------------------------------ profiling
+  void set_profiling(bool on) override {
+    profiling_ = on;
+    invalidate_graphs();
+  }
+  void profile_read(int kind, double* ms, int64_t* n) override {
+    check(kind >= 0 && kind < 4, Err::kBindError, "profile kind out of range");
+    *ms = prof_[size_t(kind)].total_ms;
+    *n = prof_[size_t(kind)].count;
+  }
+  void profile_reset() override {
+    for (auto& p : prof_) {
+      p.total_ms = 0;
+      p.count = 0;
+    }
+  }
+  void* stream() override { return st_; }
+  int64_t launches() const override { return launches_; }
+
+ private:
+  using ArrayFieldSize = int64_t;
+  struct GraphData {
+    int arity = -1;
+    std::vector<uint64_t> verts;
+    int64_t E = 0;
+    bool bound = false, dirty = true;
+    int* d_verts = nullptr;
+    size_t cap = 0;
+  };
+  struct GatherDom {
+    Domain dom;
+    int64_t nverts = 0;
+    std::vector<int> slots;  // slots whose outputs target this domain
+    int* vptr = nullptr;
+    int* vedge = nullptr;
+    size_t vedge_cap = 0;
+    mo_gather_out* outs_bm = nullptr;
+    mo_gather_out* outs_jtj = nullptr;
+  };
+  struct GSet {
+    Real* contrib = nullptr;
+    size_t cap = 0;
+    long long* rowbase = nullptr;
+    std::vector<GatherDom> doms;
+    std::vector<int64_t> slot_bound;
+  };
+  struct Prof {
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+    size_t used = 0;
+    double total_ms = 0;
+    int64_t count = 0;
+  };
+
+  int64_t array_size(int i) const {
+    return P_.extent_of(P_.arrays[size_t(i)].dom) * P_.arrays[size_t(i)].channels;
+  }
+
+  void ensure_refreshed() {
+    if (!refreshed_) refresh();
+  }
+
+  // validate(): solver.hpp:529-546
+  void validate() {
+    check(x_bound_, Err::kBindError, "unknown vector size does not match the plan layout");
+    check(params_bound_ || P_.params.empty(), Err::kBindError, "parameter count does not match the declaration");
+    for (size_t i = 0; i < P_.arrays.size(); ++i)
+      check(arr_n_[i] == array_size(int(i)), Err::kBindError,
+            "array '" + P_.arrays[i].name + "' has the wrong size");
+    for (size_t i = 0; i < P_.graphs.size(); ++i) {
+      check(graphs_[i].bound, Err::kBindError, "graph count does not match the declaration");
+      check(graphs_[i].arity == P_.graphs[i].second, Err::kBindError,
+            "graph '" + P_.graphs[i].first + "' arity does not match the declaration");
+    }
+  }
+
+  void setup_graph_set(int gi) {
+    const GraphSet& g = P_.graph_sets[size_t(gi)];
+    GSet& gs = gsets_[size_t(gi)];
+    gs.rowbase = dalloc<long long>(std::max<size_t>(g.templates.size(), 1));
+    const int ar = P_.graphs[size_t(g.graph)].second;
+    // Vertex bounds per slot: fields read through the slot and scatter
+    // targets (exec.hpp:238-259).
+    gs.slot_bound.assign(size_t(std::max(ar, 1)), INT64_MAX);
+    for (const Program* pg : {&g.cost, &g.evalf, &g.bm, &g.jtj})
+      for (const Instr& in : pg->instrs) {
+        if (in.op != kLoadU && in.op != kLoadA && in.op != kLoadC && in.op != kLoadP) continue;
+        if (!in.graph) continue;
+        check(in.slot >= 0 && in.slot < ar, Err::kShapeMismatch, "kernel reads a slot beyond the edge arity");
+        const Field* f = in.op == kLoadA ? &P_.arrays[size_t(in.field)]
+                        : in.op == kLoadC ? &P_.computed[size_t(in.field)]
+                                          : &P_.unknowns[size_t(in.field)];
+        gs.slot_bound[size_t(in.slot)] = std::min(gs.slot_bound[size_t(in.slot)], P_.extent_of(f->dom));
+      }
+    for (const Scat& s : g.scats) {
+      check(s.slot >= 0 && s.slot < ar, Err::kShapeMismatch, "graph output scatters through a slot beyond the edge arity");
+      gs.slot_bound[size_t(s.slot)] =
+          std::min(gs.slot_bound[size_t(s.slot)], P_.extent_of(P_.unknowns[size_t(s.field)].dom));
+    }
+    // One gather launch per target domain.
+    for (const Scat& s : g.scats) {
+      const Domain& d = P_.unknowns[size_t(s.field)].dom;
+      GatherDom* gd = nullptr;
+      for (auto& x : gs.doms)
+        if (x.dom == d) gd = &x;
+      if (!gd) {
+        gs.doms.push_back({});
+        gd = &gs.doms.back();
+        gd->dom = d;
+        gd->nverts = P_.extent_of(d);
+      }
+      if (std::find(gd->slots.begin(), gd->slots.end(), s.slot) == gd->slots.end()) gd->slots.push_back(s.slot);
+    }
+    const size_t K = g.scats.size();
+    for (auto& gd : gs.doms) {
+      std::vector<mo_gather_out> obm(2 * K), ojtj(K);
+      for (size_t k = 0; k < K; ++k) {
+        const Scat& s = g.scats[k];
+        const UnknownLike u = unknown(s.field);
+        mo_gather_out o{};
+        o.slot = s.slot;
+        o.C = u.channels;
+        o.active = P_.unknowns[size_t(s.field)].dom == gd.dom;
+        o.cbase = P_.ubase[size_t(s.field)] + s.channel;
+        o.sel = 0;
+        ojtj[k] = o;
+        obm[2 * k] = o;
+        o.sel = 1;
+        obm[2 * k + 1] = o;
+      }
+      gd.outs_bm = dalloc<mo_gather_out>(2 * K);
+      gd.outs_jtj = dalloc<mo_gather_out>(K);
+      gd.vptr = dalloc<int>(size_t(gd.nverts) + 1);
+      if (K) {
+        CK(cudaMemcpyAsync(gd.outs_bm, obm.data(), obm.size() * sizeof(mo_gather_out), cudaMemcpyHostToDevice, st_));
+        CK(cudaMemcpyAsync(gd.outs_jtj, ojtj.data(), ojtj.size() * sizeof(mo_gather_out), cudaMemcpyHostToDevice, st_));
+      }
+      CK(cudaStreamSynchronize(st_));
+    }
+  }
+  struct UnknownLike {
+    int channels;
+  };
+  UnknownLike unknown(int f) const { return {P_.unknowns[size_t(f)].channels}; }
+
+  // Upload changed graphs: int32 vertex table, contribution buffers and the
+  // per-domain incidence CSR (edges ascending) of the deterministic gather.
+  void upload_graphs() {
+    for (size_t gi = 0; gi < graphs_.size(); ++gi) {
+      GraphData& g = graphs_[gi];
+      if (!g.dirty) continue;
+      g.E = g.arity > 0 ? int64_t(g.verts.size()) / g.arity : 0;
+      const size_t ne = g.verts.size();
+      if (ne > g.cap) {
+        cudaFree(g.d_verts);
+        g.d_verts = dalloc<int>(ne);
+        g.cap = ne;
+        invalidate_graphs();
+      }
+      // Vertex validation before any write (exec.hpp:255-259).
+      for (size_t si = 0; si < P_.graph_sets.size(); ++si) {
+        if (P_.graph_sets[si].graph != int(gi)) continue;
+        const GSet& gs = gsets_[si];
+        for (int64_t e = 0; e < g.E; ++e)
+          for (int s = 0; s < g.arity; ++s)
+            check(g.verts[size_t(e * g.arity + s)] < uint64_t(gs.slot_bound[size_t(s)]), Err::kIndexOutOfRange,
+                  "edge references a vertex beyond the bound extent");
+      }
+      std::vector<int> v32(ne);
+      for (size_t k = 0; k < ne; ++k) {
+        check(g.verts[k] < (uint64_t(1) << 31), Err::kIndexOutOfRange, "vertex index exceeds int32");
+        v32[k] = int(g.verts[k]);
+      }
+      if (ne) CK(cudaMemcpyAsync(g.d_verts, v32.data(), ne * sizeof(int), cudaMemcpyHostToDevice, st_));
+      for (size_t si = 0; si < P_.graph_sets.size(); ++si) {
+        const GraphSet& gset = P_.graph_sets[si];
+        if (gset.graph != int(gi)) continue;
+        GSet& gs = gsets_[si];
+        const size_t no = std::max<size_t>(gset.bm.outputs.size(), 1);
+        if (size_t(g.E) * no > gs.cap) {
+          cudaFree(gs.contrib);
+          gs.contrib = dalloc<Real>(size_t(g.E) * no);
+          gs.cap = size_t(g.E) * no;
+          invalidate_graphs();
+        }
+        for (auto& gd : gs.doms) {
+          std::vector<int> cnt(size_t(gd.nverts) + 1, 0), last(size_t(gd.nverts), -1);
+          for (int64_t e = 0; e < g.E; ++e)
+            for (int s : gd.slots) {
+              int v = v32[size_t(e * g.arity + s)];
+              if (last[size_t(v)] != int(e)) {
+                last[size_t(v)] = int(e);
+                cnt[size_t(v) + 1]++;
+              }
+            }
+          for (size_t v = 0; v < size_t(gd.nverts); ++v) cnt[v + 1] += cnt[v];
+          std::vector<int> vedge(static_cast<size_t>(cnt[static_cast<size_t>(gd.nverts)]));
+          std::vector<int> pos(cnt.begin(), cnt.end() - 1);
+          std::fill(last.begin(), last.end(), -1);
+          for (int64_t e = 0; e < g.E; ++e)
+            for (int s : gd.slots) {
+              int v = v32[size_t(e * g.arity + s)];
+              if (last[size_t(v)] != int(e)) {
+                last[size_t(v)] = int(e);
+                vedge[size_t(pos[size_t(v)]++)] = int(e);
+              }
+            }
+          if (vedge.size() > gd.vedge_cap) {
+            cudaFree(gd.vedge);
+            gd.vedge = dalloc<int>(vedge.size());
+            gd.vedge_cap = vedge.size();
+            invalidate_graphs();
+          }
+          CK(cudaMemcpyAsync(gd.vptr, cnt.data(), cnt.size() * sizeof(int), cudaMemcpyHostToDevice, st_));
+          if (!vedge.empty())
+            CK(cudaMemcpyAsync(gd.vedge, vedge.data(), vedge.size() * sizeof(int), cudaMemcpyHostToDevice, st_));
+        }
+      }
+      CK(cudaStreamSynchronize(st_));
+      invalidate_graphs();  // edge counts are baked into the captured PCG graph
+      g.dirty = false;
+    }
+  }
+
+  void invalidate_graphs() {
+    for (auto& kv : pcg_exec_) cudaGraphExecDestroy(kv.second);
+    pcg_exec_.clear();
+  }
+
+  // ------------------------------------------------------------ launches
+  mo_kparams kp_base(const Real* xv, const Real* pv) {
+    mo_kparams k;
+    std::memset(&k, 0, sizeof k);
+    const int U = int(P_.unknowns.size()), A = int(P_.arrays.size());
+    auto view = [&](const void* ptr, const Field& f) {
+      mo_view v{};
+      v.p = ptr;
+      v.ch = f.channels;
+      v.nd = int(f.dom.dims.size());
+      auto s = P_.shape_of(f.dom);
+      v.s0 = int(s[0]);
+      v.s1 = int(s[1]);
+      v.s2 = int(s[2]);
+      v.row_lo = 0;
+      return v;
+    };
+    for (int f = 0; f < U; ++f) {
+      k.v[f] = view(xv + P_.ubase[size_t(f)], P_.unknowns[size_t(f)]);
+      k.v[U + f] = view(pv ? pv + P_.ubase[size_t(f)] : nullptr, P_.unknowns[size_t(f)]);
+      k.ubase[f] = P_.ubase[size_t(f)];
+    }
+    for (int a = 0; a < A; ++a) k.v[2 * U + a] = view(arr_[size_t(a)], P_.arrays[size_t(a)]);
+    for (size_t c = 0; c < P_.computed.size(); ++c) k.v[2 * U + A + int(c)] = view(comp_[c], P_.computed[c]);
+    k.params = params_d_;
+    k.colmask = colmask_;
+    k.state = state_;
+    return k;
+  }
+  mo_kparams kp_grid(const Domain& d, const Real* xv, const Real* pv) {
+    mo_kparams k = kp_base(xv, pv);
+    auto s = P_.shape_of(d);
+    k.dnd = std::max<int>(1, int(d.dims.size()));
+    k.d0 = int(s[0]);
+    k.d1 = int(s[1]);
+    k.d2 = int(s[2]);
+    k.row0 = 0;
+    k.row1 = int(s[0]);
+    k.row_lo = 0;
+    for (size_t i = 0; i < P_.exclude_kernels.size(); ++i)
+      if (P_.exclude_kernels[i].dom == d) k.mask = masks_[i];
+    return k;
+  }
+  mo_kparams kp_graph(int gi, const Real* xv, const Real* pv) {
+    mo_kparams k = kp_base(xv, pv);
+    const GraphData& g = graphs_[size_t(P_.graph_sets[size_t(gi)].graph)];
+    k.dnd = 1;  // graph env: default DomainInfo (shape {1,1,1}, nd 1)
+    k.d0 = k.d1 = k.d2 = 1;
+    k.verts = g.d_verts;
+    k.arity = g.arity;
+    k.nedges = g.E;
+    return k;
+  }
+
+  int tiles_of(const Domain& d) const {
+    auto s = P_.shape_of(d);
+    const int nd = std::max<int>(1, int(d.dims.size()));
+    long long rows = s[0];
+    if (rows <= 0) return 0;
+    if (nd == 1) return int((rows + MO_THREADS - 1) / MO_THREADS);
+    if (nd == 2) return int(((s[1] + MO_TILE_X - 1) / MO_TILE_X) * ((rows + MO_TILE_Y - 1) / MO_TILE_Y));
+    return int(((s[2] + MO_TILE_X - 1) / MO_TILE_X) * rows * ((s[1] + MO_TILE_Y - 1) / MO_TILE_Y));
+  }
+  int occupancy(const void* f) {
+    auto it = occ_.find(f);
+    if (it != occ_.end()) return it->second;
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, f, MO_THREADS, 0) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = 2;
+    }
+    occ_[f] = n;
+    return n;
+  }
+  int grid_blocks(const std::string& name, const Domain& d) {
+    const void* f = mod_.kernel(name);
+    long long g = std::min<long long>(tiles_of(d), (long long)nsm_ * occupancy(f));
+    return int(std::max<long long>(g, 1));
+  }
+  int edge_blocks(const std::string& name, int gi) {
+    const void* f = mod_.kernel(name);
+    long long E = graphs_[size_t(P_.graph_sets[size_t(gi)].graph)].E;
+    long long g = std::min<long long>((E + MO_THREADS - 1) / MO_THREADS, (long long)nsm_ * occupancy(f));
+    return int(std::max<long long>(g, 1));
+  }
+  void launch_grid(const std::string& name, const Domain& d, const mo_kparams& kp, int grid = 0) {
+    const void* f = mod_.kernel(name);
+    if (grid <= 0) grid = grid_blocks(name, d);
+    dim3 block = d.dims.size() <= 1 ? dim3(MO_THREADS, 1, 1) : dim3(MO_TILE_X, MO_TILE_Y, 1);
+    void* args[] = {const_cast<mo_kparams*>(&kp)};
+    CK(cudaLaunchKernel(f, dim3(grid), block, args, 0, st_));
+    ++launches_;
+  }
+  void launch_edges(const std::string& name, int gi, const mo_kparams& kp, int grid = 0) {
+    const void* f = mod_.kernel(name);
+    if (grid <= 0) grid = edge_blocks(name, gi);
+    void* args[] = {const_cast<mo_kparams*>(&kp)};
+    CK(cudaLaunchKernel(f, dim3(grid), dim3(MO_THREADS), args, 0, st_));
+    ++launches_;
+  }
+  mo_red red(int base, int total, int op, int arg) {
+    check(total <= kPartCap, Err::kInternal, "reduction exceeds the partial buffer");
+    mo_red R;
+    R.partials = partials_;
+    R.counter = &state_->counters[0];
+    R.state = state_;
+    R.part_base = base;
+    R.part_total = total;
+    R.fin_op = op;
+    R.fin_arg = arg;
+    return R;
+  }
+
+  void gather_graph(int gi, bool bm, Real* dst0, Real* dst1) {
+    const GraphSet& g = P_.graph_sets[size_t(gi)];
+    GSet& gs = gsets_[size_t(gi)];
+    const GraphData& gd0 = graphs_[size_t(g.graph)];
+    const int NO = int(bm ? g.bm.outputs.size() : g.jtj.outputs.size());
+    if (NO == 0) return;
+    for (auto& gd : gs.doms) {
+      k_graph_gather<Real><<<vgrid(gd.nverts, nsm_), MO_THREADS, 0, st_>>>(
+          gd.nverts, gd.vptr, gd.vedge, gd0.d_verts, gd0.arity, gs.contrib, NO, bm ? gd.outs_bm : gd.outs_jtj,
+          dst0, dst1);
+      ++launches_;
+    }
+  }
+
+  // cost_at (solver.hpp:176-193) into state->sums[slot].
+  void cost_at(const Real* xv, int slot) {
+    int total = 0;
+    std::vector<int> grids;
+    for (size_t i = 0; i < P_.grid_sets.size(); ++i) {
+      grids.push_back(grid_blocks("mo_grid_cost_" + std::to_string(i), P_.grid_sets[i].dom));
+      total += grids.back();
+    }
+    for (size_t i = 0; i < P_.graph_sets.size(); ++i) {
+      grids.push_back(edge_blocks("mo_graph_cost_" + std::to_string(i), int(i)));
+      total += grids.back();
+    }
+    if (total == 0) {
+      CK(cudaMemsetAsync(&state_->sums[slot], 0, sizeof(double), st_));
+      return;
+    }
+    int base = 0, gi = 0;
+    for (size_t i = 0; i < P_.grid_sets.size(); ++i, ++gi) {
+      mo_kparams kp = kp_grid(P_.grid_sets[i].dom, xv, nullptr);
+      kp.red = red(base, total, MO_FIN_STORE, slot);
+      launch_grid("mo_grid_cost_" + std::to_string(i), P_.grid_sets[i].dom, kp, grids[size_t(gi)]);
+      base += grids[size_t(gi)];
+    }
+    for (size_t i = 0; i < P_.graph_sets.size(); ++i, ++gi) {
+      mo_kparams kp = kp_graph(int(i), xv, nullptr);
+      kp.red = red(base, total, MO_FIN_STORE, slot);
+      launch_edges("mo_graph_cost_" + std::to_string(i), int(i), kp, grids[size_t(gi)]);
+      base += grids[size_t(gi)];
+    }
+  }
+
+  // build_normal (solver.hpp:220-251) on the device.
+  void normal_device() {
+    prof_begin(2);
+    const bool fused = P_.graph_sets.empty();
+    const long long n = P_.num_cols;
+    std::vector<int> grids;
+    int total = 0;
+    for (size_t i = 0; i < P_.gather_sets.size(); ++i) {
+      grids.push_back(grid_blocks("mo_gather_bm_" + std::to_string(i), P_.gather_sets[i].dom));
+      total += grids.back();
+    }
+    if (!fused) total = vgrid(n, nsm_);
+    int base = 0;
+    for (size_t i = 0; i < P_.gather_sets.size(); ++i) {
+      mo_kparams kp = kp_grid(P_.gather_sets[i].dom, x_, nullptr);
+      kp.out0 = b_;
+      kp.out1 = m_;
+      kp.flags = fused ? (MO_F_PATCH | MO_F_REDUCE) : 0;
+      kp.red = red(base, total, MO_FIN_UNCONSTRAINED, 0);
+      launch_grid("mo_gather_bm_" + std::to_string(i), P_.gather_sets[i].dom, kp, grids[i]);
+      base += grids[i];
+    }
+    if (!fused) {
+      for (size_t i = 0; i < P_.graph_sets.size(); ++i) {
+        mo_kparams kp = kp_graph(int(i), x_, nullptr);
+        kp.out0 = gsets_[i].contrib;
+        launch_edges("mo_graph_bm_" + std::to_string(i), int(i), kp);
+        gather_graph(int(i), true, b_, m_);
+      }
+      k_bm_patch<Real><<<vgrid(n, nsm_), MO_THREADS, 0, st_>>>(red(0, vgrid(n, nsm_), MO_FIN_UNCONSTRAINED, 0), n,
+                                                                colmask_, b_, m_);
+      ++launches_;
+    } else if (P_.gather_sets.empty()) {
+      CK(cudaMemsetAsync(&state_->unconstrained, 0, sizeof(long long), st_));
+    }
+    prof_end(2);
+  }
+
+  // out = 2 J^T J pv (+ damp pv), optionally zeroing excluded columns and
+  // reducing p'Ap into alpha (flags: MO_F_DAMP | MO_F_REDUCE | MO_F_ZEROEXCL).
+  void apply(const Real* pv, Real* out, int flags) {
+    const bool fused = P_.graph_sets.empty();
+    const long long n = P_.num_cols;
+    std::vector<int> grids;
+    int total = 0;
+    for (size_t i = 0; i < P_.gather_sets.size(); ++i) {
+      grids.push_back(grid_blocks("mo_gather_jtj_" + std::to_string(i), P_.gather_sets[i].dom));
+      total += grids.back();
+    }
+    if (!fused) total = vgrid(n, nsm_);
+    int base = 0;
+    for (size_t i = 0; i < P_.gather_sets.size(); ++i) {
+      mo_kparams kp = kp_grid(P_.gather_sets[i].dom, x_, pv);
+      kp.out0 = out;
+      kp.in0 = pv;
+      kp.in1 = damp_;
+      kp.flags = fused ? flags : (flags & MO_F_SKIPDONE);
+      kp.red = red(base, total, MO_FIN_PCG_ALPHA, 0);
+      launch_grid("mo_gather_jtj_" + std::to_string(i), P_.gather_sets[i].dom, kp, grids[i]);
+      base += grids[i];
+    }
+    if (!fused) {
+      for (size_t i = 0; i < P_.graph_sets.size(); ++i) {
+        mo_kparams kp = kp_graph(int(i), x_, pv);
+        kp.out0 = gsets_[i].contrib;
+        kp.flags = flags & MO_F_SKIPDONE;
+        launch_edges("mo_graph_jtj_" + std::to_string(i), int(i), kp);
+        gather_graph(int(i), false, out, nullptr);
+      }
+      if (flags & (MO_F_DAMP | MO_F_REDUCE | MO_F_ZEROEXCL)) {
+        k_apply_finish<Real><<<vgrid(n, nsm_), MO_THREADS, 0, st_>>>(red(0, vgrid(n, nsm_), MO_FIN_PCG_ALPHA, 0), n,
+                                                                     colmask_, pv, damp_, out, flags);
+        ++launches_;
+      }
+    }
+  }
+
+  // Jacobi PCG (pcg.hpp:63-130) as a captured CUDA graph.
+  void pcg_body(bool lm) {
+    const long long n = P_.num_cols;
+    const int vg = vgrid(n, nsm_);
+    const Real* mdv = lm ? md_ : m_;
+    const int pre = cfg_.use_preconditioner ? 1 : 0;
+    k_pcg_init<Real><<<vg, MO_THREADS, 0, st_>>>(red(0, vg, MO_FIN_PCG_INIT, 0), n, colmask_, b_, mdv, delta_, r_, p_, pre);
+    ++launches_;
+    const int flags = MO_F_REDUCE | MO_F_ZEROEXCL | MO_F_SKIPDONE | (lm ? MO_F_DAMP : 0);
+    for (int k = 0; k < cfg_.linear_iters; ++k) {
+      prof_begin(0);
+      apply(p_, ap_, flags);
+      prof_end(0);
+      prof_begin(1);
+      k_pcg_update<Real><<<vg, MO_THREADS, 0, st_>>>(red(0, vg, MO_FIN_PCG_BETA, 0), n, colmask_, mdv, delta_, r_, p_, ap_, pre);
+      k_pcg_p<Real><<<vg, MO_THREADS, 0, st_>>>(state_, n, colmask_, mdv, r_, p_, pre);
+      launches_ += 2;
+      prof_end(1);
+    }
+  }
+
+  void run_pcg(bool lm) {
+    if (P_.num_cols == 0) {
+      // Nothing to solve: an empty r'z is exactly 0 <= stop (pcg.hpp:95).
+      CK(cudaMemcpyAsync(&state_->done, &zero_flags_, sizeof(int) * 4, cudaMemcpyHostToDevice, st_));
+      return;
+    }
+    static const bool nograph = std::getenv("MO_B200_NOGRAPH") != nullptr;
+    if (nograph) {
+      prof_reset_slots();
+      pcg_body(lm);
+      return;
+    }
+    auto it = pcg_exec_.find(lm);
+    if (it == pcg_exec_.end()) {
+      prof_reset_slots();
+      int64_t before = launches_;
+      cudaGraph_t graph;
+      CK(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+      pcg_body(lm);
+      CK(cudaStreamEndCapture(st_, &graph));
+      cudaGraphExec_t exec;
+      CK(cudaGraphInstantiate(&exec, graph, 0));
+      cudaGraphDestroy(graph);
+      pcg_nodes_[lm] = launches_ - before;
+      launches_ = before;
+      it = pcg_exec_.emplace(lm, exec).first;
+    }
+    CK(cudaGraphLaunch(it->second, st_));
+    launches_ += pcg_nodes_[lm];
+    prof_pending_ = true;
+  }
+
+  // ------------------------------------------------------------ profiling
+  void prof_reset_slots() {
+    for (auto& p : prof_) p.used = 0;
+  }
+  void prof_begin(int kind) {
+    if (!profiling_) return;
+    Prof& p = prof_[size_t(kind)];
+    if (p.used == p.ev.size()) {
+      cudaEvent_t a, b;
+      CK(cudaEventCreate(&a));
+      CK(cudaEventCreate(&b));
+      p.ev.push_back({a, b});
+    }
+    CK(cudaEventRecord(p.ev[p.used].first, st_));
+  }
+  void prof_end(int kind) {
+    if (!profiling_) return;
+    Prof& p = prof_[size_t(kind)];
+    CK(cudaEventRecord(p.ev[p.used].second, st_));
+    p.used++;
+    prof_pending_ = true;
+  }
+  void collect_profile() {
+    if (!profiling_ || !prof_pending_) return;
+    for (size_t k = 0; k < prof_.size(); ++k) {
+      Prof& p = prof_[k];
+      for (size_t i = 0; i < p.used; ++i) {
+        float ms = 0;
+        if (cudaEventElapsedTime(&ms, p.ev[i].first, p.ev[i].second) == cudaSuccess) {
+          p.total_ms += ms;
+          p.count++;
+        } else {
+          cudaGetLastError();
+        }
+      }
+      if (k == 2) p.used = 0;  // build_normal events are re-recorded every iteration
+    }
+    prof_pending_ = false;
+  }
+
+  void sync_state() {
+    CK(cudaMemcpyAsync(state_h_, state_, sizeof(mo_state), cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+  }
+  void download(const Real* src, void* out, int64_t n) {
+    check(n == P_.num_cols, Err::kShapeMismatch, "vector size mismatch");
+    if (n) CK(cudaMemcpyAsync(out, src, size_t(n) * sizeof(Real), cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+  }
+
+  Plan P_;
+  Config cfg_;
+  int dev_ = 0, nsm_ = 148;
+  cudaStream_t st_ = nullptr;
+  Module mod_;
+  Real *x_ = nullptr, *xt_ = nullptr, *b_ = nullptr, *m_ = nullptr, *md_ = nullptr, *damp_ = nullptr;
+  Real *delta_ = nullptr, *r_ = nullptr, *p_ = nullptr, *ap_ = nullptr, *vtmp_ = nullptr, *otmp_ = nullptr;
+  Real* resid_ = nullptr;
+  size_t resid_cap_ = 0;
+  double* bd_ = nullptr;
+  std::vector<Real*> arr_, comp_;
+  std::vector<int64_t> arr_n_;
+  std::vector<unsigned char*> masks_;
+  unsigned char* colmask_ = nullptr;
+  double* params_d_ = nullptr;
+  mo_state* state_ = nullptr;
+  mo_state* state_h_ = nullptr;
+  double* partials_ = nullptr;
+  std::vector<GraphData> graphs_;
+  std::vector<GSet> gsets_;
+  std::vector<long long*> grid_rowbase_;
+  std::vector<int64_t> rowbase_;
+  int64_t rows_ = 0;
+  int64_t unconstrained_ = 0;
+  bool x_bound_ = false, params_bound_ = false, refreshed_ = false;
+  std::map<const void*, int> occ_;
+  std::map<bool, cudaGraphExec_t> pcg_exec_;
+  std::map<bool, int64_t> pcg_nodes_;
+  std::vector<void*> owned_;
+  int64_t launches_ = 0;
+  bool profiling_ = false, prof_pending_ = false;
+  std::vector<Prof> prof_ = std::vector<Prof>(4);
+  int zero_flags_[4] = {1, 0, 0, 0};
+};
+
+std::unique_ptr<SessionBase> make_session(const Plan& plan, int device) {
+  if (plan.cfg.precision == 0) return std::make_unique<Session<float>>(plan, device);
+  return std::make_unique<Session<double>>(plan, device);
+}
+
+}  // namespace mo

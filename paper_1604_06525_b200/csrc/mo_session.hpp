@@ -1,0 +1,62 @@
+// mo_session.hpp — precision-erased interface of a bound solver session
+// (the device counterpart of minopt::Solver<Real>, solver.hpp:80-635).
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <vector>
+
+#include "mo_plan.hpp"
+
+namespace mo {
+
+struct IterRow {
+  int iter = 0;
+  double cost = 0;
+  bool accepted = true;
+  double radius = 0;
+  int pcg_iters = 0;
+  double wall_ms = 0;
+};
+
+struct SolveResult {
+  double final_cost = 0;
+  int reason = 0;  // StopReason (solver.hpp:40-46)
+  std::vector<IterRow> trace;
+  bool nonfinite_kernels = false;
+  bool indefinite_operator = false;
+  int64_t unconstrained = 0;
+};
+
+using IterCallback = void (*)(int iter, void* user);
+
+class SessionBase {
+ public:
+  virtual ~SessionBase() = default;
+  virtual void bind_x(const void* x, int64_t n, bool device) = 0;
+  virtual void bind_array(int i, const void* data, int64_t n, bool device) = 0;
+  virtual void bind_params(const double* p, int64_t n) = 0;
+  virtual void bind_graph(int i, const uint64_t* verts, int64_t n, int arity) = 0;
+  virtual void refresh() = 0;
+  virtual int64_t num_cols() const = 0;
+  virtual int64_t num_rows() = 0;
+  virtual void excluded(uint8_t* out, int64_t n) = 0;
+  virtual double cost() = 0;
+  virtual void residuals(void* out, int64_t n) = 0;
+  virtual void build_normal() = 0;
+  virtual void get_rhs(void* out, int64_t n) = 0;
+  virtual void get_precond(void* out, int64_t n) = 0;
+  virtual void apply_jtj(const void* v, void* out, int64_t n, bool device) = 0;
+  virtual SolveResult solve(IterCallback cb, void* user) = 0;
+  virtual void get_x(void* out, int64_t n) = 0;
+  virtual bool saw_nonfinite() = 0;
+  virtual void set_profiling(bool on) = 0;
+  virtual void profile_read(int kind, double* ms, int64_t* n) = 0;
+  virtual void profile_reset() = 0;
+  virtual void* stream() = 0;
+  virtual int64_t launches() const = 0;
+};
+
+std::unique_ptr<SessionBase> make_session(const Plan& plan, int device);
+
+}  // namespace mo

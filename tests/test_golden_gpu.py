@@ -1,0 +1,100 @@
+"""GPU parity against the reference's own golden outputs (tests/golden/*.npz,
+produced by the unmodified reference through oracle/_ref/ref_driver).
+
+Tolerances (BASELINE.json north_star): per-element J^T F, J^T J p, M and
+residuals within 1e-10 relative in fp64 and 1e-5 in fp32 (with an absolute
+floor tied to ||ref||_inf for stencils with cancellation); cost trajectories
+within 1e-4 relative in fp32 (1e-8 in fp64); identical stop reasons, trace
+lengths, accept/reject sequences and PCG iteration counts.
+"""
+import numpy as np
+import pytest
+
+from helpers import Golden, assert_close_vec, golden_names, rel_close
+from paper_1604_06525_b200 import Solver
+
+pytestmark = pytest.mark.gpu
+
+NAMES = golden_names()
+
+
+def tol(prec):
+    return dict(vec=1e-10, cost=1e-12, traj=1e-8, x=1e-7) if prec == "f64" else \
+        dict(vec=1e-5, cost=2e-5, traj=1e-4, x=1e-3)
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_golden_case(name):
+    g = Golden(name)
+    t = tol(g.prec)
+    data = g.data()
+    s = Solver(g.plan(), data)
+    assert s.num_cols() == int(g.ref("num_cols")[0])
+    assert s.num_rows() == int(g.ref("num_rows")[0])
+    np.testing.assert_array_equal(s.excluded(), g.ref("excluded"))
+    for cmd in g.cmds:
+        if cmd == "cost":
+            c = s.cost()
+            assert rel_close(c, float(g.ref("cost")[0]), t["cost"]), (c, g.ref("cost"))
+        elif cmd == "residuals":
+            assert_close_vec(s.residuals(), g.ref("residuals"), t["vec"], "residuals")
+        elif cmd == "normal":
+            s.build_normal()
+            assert_close_vec(s.rhs(), g.ref("b"), t["vec"], "b = -2 J^T F")
+            assert_close_vec(s.precond(), g.ref("m"), t["vec"], "m = diag(2 J^T J)")
+        elif cmd == "jtj":
+            assert_close_vec(s.apply_jtj(g.z["v"].astype(g.dtype)), g.ref("jtj"), t["vec"], "2 J^T J v")
+        elif cmd == "solve":
+            r = s.solve()
+            assert int(r.reason) == int(g.ref("reason")[0])
+            assert len(r.trace) == len(g.ref("trace_iter"))
+            assert [int(x.accepted) for x in r.trace] == list(g.ref("trace_accepted"))
+            assert [x.iter for x in r.trace] == list(g.ref("trace_iter"))
+            assert [x.pcg_iters for x in r.trace] == list(g.ref("trace_pcg"))
+            for row, rc, rr in zip(r.trace, g.ref("trace_cost"), g.ref("trace_radius")):
+                assert rel_close(row.cost, rc, t["traj"]), (row.cost, rc)
+                assert rel_close(row.radius, rr, t["traj"]), (row.radius, rr)
+            assert rel_close(r.final_cost, float(g.ref("final_cost")[0]), t["traj"]), (r.final_cost, g.ref("final_cost"))
+            assert r.unconstrained == int(g.ref("unconstrained")[0])
+            assert r.nonfinite_kernels == bool(g.ref("nonfinite_kernels")[0])
+            assert r.indefinite_operator == bool(g.ref("indefinite")[0])
+            assert_close_vec(data.x, g.ref("x_final"), t["x"], "x after solve")
+
+
+def test_exclusion_keeps_negative_zero_bitwise():
+    """test_solver.cpp:206-234: x0 = -0.0 survives a solve bit for bit."""
+    g = Golden("exclude")
+    data = g.data()
+    s = Solver(g.plan(), data)
+    s.solve()
+    assert np.signbit(data.x[0]) and data.x[0] == 0.0
+    np.testing.assert_array_equal(data.x.view(np.uint64)[:1], g.ref("x_final").view(np.uint64)[:1])
+
+
+def test_lm_stall_leaves_x_bitwise():
+    """test_solver.cpp:323-344."""
+    g = Golden("lm_flat")
+    data = g.data()
+    x0 = data.x.copy()
+    s = Solver(g.plan(), data)
+    r = s.solve()
+    assert r.reason == 2 and r.final_cost == 25.0 and len(r.trace) == 1 and not r.trace[0].accepted
+    np.testing.assert_array_equal(data.x.view(np.uint64), x0.view(np.uint64))
+    assert r.unconstrained == 2
+
+
+@pytest.mark.parametrize("name", ["chain", "dense", "ops", "cfg_poisson_f32", "cfg_arap_mesh_f64"])
+def test_kernels_bitwise_deterministic(name):
+    """Run-to-run determinism: fixed grids + fixed-order reductions."""
+    g = Golden(name)
+    outs = []
+    for _ in range(2):
+        data = g.data()
+        s = Solver(g.plan(), data)
+        s.build_normal()
+        v = g.z["v"].astype(g.dtype) if "v" in g.z else np.ones(s.num_cols(), g.dtype)
+        r = s.solve()
+        outs.append((s.rhs(), s.apply_jtj(v), data.x.copy(), r.final_cost))
+    for a, b in zip(outs[0][:3], outs[1][:3]):
+        np.testing.assert_array_equal(a.view(np.uint8), b.view(np.uint8))
+    assert outs[0][3] == outs[1][3]
