@@ -120,6 +120,11 @@ int mo_plan_num_cols(mo_plan p, int64_t* n);
 /* Generate + NVRTC-compile the plan's sm_100a module into the kernel cache
  * (no GPU needed); sessions then load it without compiling. */
 int mo_plan_precompile(mo_plan p, int precision);
+/* exact != 0: compile the per-element kernels without FMA contraction so
+ * their add/mul round exactly like the reference's CPU build (bitwise
+ * per-element parity); default 0 lets nvcc contract a*b+c into FMA
+ * (results within the fp32 1e-5 / fp64 1e-10 tolerances). */
+int mo_plan_set_exact(mo_plan p, int exact);
 int mo_plan_counts(mo_plan p, int* n_params, int* n_arrays, int* n_graphs, int* n_unknowns);
 int mo_plan_array_size(mo_plan p, int i, int64_t* n_scalars);
 int mo_plan_graph_arity(mo_plan p, int i, int* arity);

@@ -24,6 +24,7 @@ int main(int argc, char** argv) {
   std::string energy, out;
   std::vector<std::pair<std::string, long long>> dims;
   SolveConfig cfg;
+  cfg.force_evalj = true;  // ship per-template Jacobian lanes for the two-phase apply
   bool f32 = false;
   for (int i = 1; i < argc; ++i) {
     std::string k = argv[i];

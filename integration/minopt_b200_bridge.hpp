@@ -24,6 +24,8 @@
 //   residuals N       / residual grid ND dims... | residual graph G
 //   ubase N cols... ; num_cols V
 //   grid_sets N       / grid_set ND dims... NT t...   + programs cost, evalf
+//                       [+ evalj NT / jtemplate T GUARD NL (out f c o0 o1 o2)...
+//                          + program evalj]   (plans built with force_evalj)
 //   gather_sets N     / gather_set ND dims... NCH (f c)...   + programs bm, jtj
 //   graph_sets N      / graph_set G NT t... NS (slot f c)... + cost, evalf, bm, jtj
 //   computed_kernels N/ computed_kernel IDX ND dims...   + program prog
@@ -138,6 +140,19 @@ inline std::string export_plan_text(const CompiledPlan& P) {
     os << '\n';
     put_program(os, "cost", g.cost);
     put_program(os, "evalf", g.evalf);
+    if (P.has_evalj) {
+      // Per-template Jacobian lanes (plan.hpp:59-72, 244-264): the device's
+      // two-phase J^T J p evaluates these once per element.
+      os << "evalj " << g.jtemplates.size() << '\n';
+      for (const auto& jt : g.jtemplates) {
+        os << "jtemplate " << jt.tmpl << ' ' << jt.guard_out << ' ' << jt.lanes.size();
+        for (const JLane& l : jt.lanes)
+          os << ' ' << l.out << ' ' << l.field << ' ' << l.channel << ' ' << l.off[0] << ' ' << l.off[1]
+             << ' ' << l.off[2];
+        os << '\n';
+      }
+      put_program(os, "evalj", g.evalj);
+    }
   }
   os << "gather_sets " << P.gather_sets.size() << '\n';
   for (const GatherKernels& g : P.gather_sets) {
@@ -180,3 +195,148 @@ inline std::string export_plan_text(const CompiledPlan& P) {
 }
 
 }  // namespace minopt::b200
+
+#ifdef MINOPT_B200_WITH_SOLVER
+// ---------------------------------------------------------------------------
+// Drop-in device solver: same constructor and routine signatures as
+// minopt::Solver<Real> (solver.hpp:80-635), executing on the GPU through the
+// C ABI of libmo_b200.so.  Switching a caller from minopt::Solver<double> to
+// minopt::b200::Solver<double> is the whole integration.
+#include <cstring>
+#include <functional>
+#include <span>
+
+#include "mo_b200.h"
+#include "minopt/solver.hpp"
+
+namespace minopt::b200 {
+
+[[noreturn]] inline void rethrow(int rc) {
+  Err code = Err::kInternal;
+  if (rc >= 1 && rc <= int(Err::kInternal) + 1) code = Err(rc - 1);
+  throw Error(code, std::string("mo_b200: ") + mo_last_error());
+}
+inline void ok(int rc) {
+  if (rc != MO_OK) rethrow(rc);
+}
+
+template <class Real>
+class Solver {
+ public:
+  Solver(const CompiledPlan& plan, SolveData<Real>& data, int device = 0) : data_(data) {
+    // The device's two-phase J^T J p wants the per-template Jacobian lanes;
+    // re-plan with force_evalj when the caller's plan lacks them (the other
+    // programs are unchanged by it).
+    std::string text;
+    if (plan.has_evalj) {
+      text = export_plan_text(plan);
+    } else {
+      SolveConfig c = plan.cfg;
+      c.force_evalj = true;
+      text = export_plan_text(minopt::plan(plan.spec, c));
+    }
+    ok(mo_plan_parse(text.data(), text.size(), &plan_));
+    mo_solve_config c{};
+    ok(mo_plan_get_config(plan_, &c));
+    c.precision = sizeof(Real) == 4 ? MO_F32 : MO_F64;
+    ok(mo_plan_set_config(plan_, &c));
+    ok(mo_session_create(plan_, device, &s_));
+    bind();
+    ok(mo_refresh(s_));
+  }
+  ~Solver() {
+    mo_session_destroy(s_);
+    mo_plan_destroy(plan_);
+  }
+  Solver(const Solver&) = delete;
+  Solver& operator=(const Solver&) = delete;
+
+  int64_t num_cols() const {
+    int64_t n = 0;
+    ok(mo_num_cols(s_, &n));
+    return n;
+  }
+  int64_t num_rows() const {
+    int64_t n = 0;
+    ok(mo_num_rows(s_, &n));
+    return n;
+  }
+  std::span<const uint8_t> excluded() {
+    excl_.resize(size_t(num_cols()));
+    ok(mo_get_excluded(s_, excl_.data(), int64_t(excl_.size())));
+    return excl_;
+  }
+  double cost() {
+    double v = 0;
+    ok(mo_cost(s_, &v));
+    return v;
+  }
+  void residuals(std::span<Real> f) { ok(mo_residuals(s_, f.data(), int64_t(f.size()))); }
+  void build_normal() {
+    ok(mo_build_normal(s_));
+    b_.resize(size_t(num_cols()));
+    m_.resize(size_t(num_cols()));
+    ok(mo_get_rhs(s_, b_.data(), int64_t(b_.size())));
+    ok(mo_get_precond(s_, m_.data(), int64_t(m_.size())));
+  }
+  std::span<const Real> rhs() const { return b_; }
+  std::span<const Real> precond() const { return m_; }
+  void apply_jtj(std::span<const Real> v, std::span<Real> out) {
+    check(v.size() == out.size(), Err::kShapeMismatch, "apply_jtj(): size mismatch");
+    ok(mo_apply_jtj(s_, v.data(), out.data(), int64_t(v.size())));
+  }
+  bool saw_nonfinite_kernel() const {
+    int v = 0;
+    ok(mo_saw_nonfinite(s_, &v));
+    return v != 0;
+  }
+
+  SolveResult solve(const std::function<void(int, SolveData<Real>&)>& callback = {}) {
+    cb_ = &callback;
+    mo_solve_result r{};
+    ok(mo_solve(s_, callback ? &Solver::trampoline : nullptr, this, &r));
+    data_.x.resize(size_t(num_cols()));
+    ok(mo_get_x(s_, data_.x.data(), int64_t(data_.x.size())));
+    SolveResult out;
+    out.final_cost = r.final_cost;
+    out.reason = StopReason(r.reason);
+    out.nonfinite_kernels = r.nonfinite_kernels != 0;
+    out.indefinite_operator = r.indefinite_operator != 0;
+    out.unconstrained = r.unconstrained;
+    for (int i = 0; i < r.n_trace; ++i) {
+      const mo_iter_row& t = r.trace[i];
+      out.trace.push_back({t.iter, t.cost, t.accepted != 0, t.radius, t.pcg_iters, t.wall_ms});
+    }
+    return out;
+  }
+
+ private:
+  void bind() {
+    ok(mo_bind_x(s_, data_.x.data(), int64_t(data_.x.size())));
+    for (size_t i = 0; i < data_.arrays.size(); ++i)
+      ok(mo_bind_array(s_, int(i), data_.arrays[i].data(), int64_t(data_.arrays[i].size())));
+    ok(mo_bind_params(s_, data_.params.data(), int64_t(data_.params.size())));
+    for (size_t i = 0; i < data_.graphs.size(); ++i)
+      ok(mo_bind_graph(s_, int(i), data_.graphs[i].verts.data(), int64_t(data_.graphs[i].verts.size()),
+                       data_.graphs[i].arity));
+  }
+  // Callbacks observe and may mutate SolveData between iterations
+  // (solver.hpp:503): download x, call, re-upload everything.
+  static void trampoline(int iter, mo_session, void* user) {
+    auto* self = static_cast<Solver*>(user);
+    self->data_.x.resize(size_t(self->num_cols()));
+    ok(mo_get_x(self->s_, self->data_.x.data(), int64_t(self->data_.x.size())));
+    (*self->cb_)(iter, self->data_);
+    self->bind();
+  }
+
+  SolveData<Real>& data_;
+  mo_plan plan_ = nullptr;
+  mo_session s_ = nullptr;
+  std::vector<Real> b_, m_;
+  std::vector<uint8_t> excl_;
+  const std::function<void(int, SolveData<Real>&)>* cb_ = nullptr;
+};
+
+}  // namespace minopt::b200
+#endif  // MINOPT_B200_WITH_SOLVER

@@ -53,6 +53,7 @@ SIGNATURES = {
     "mo_plan_set_config": (c_int, [c_void_p, ctypes.POINTER(SolveConfigC)]),
     "mo_plan_num_cols": (c_int, [c_void_p, ctypes.POINTER(c_int64)]),
     "mo_plan_precompile": (c_int, [c_void_p, c_int]),
+    "mo_plan_set_exact": (c_int, [c_void_p, c_int]),
     "mo_plan_counts": (c_int, [c_void_p] + [ctypes.POINTER(c_int)] * 4),
     "mo_plan_array_size": (c_int, [c_void_p, c_int, ctypes.POINTER(c_int64)]),
     "mo_plan_graph_arity": (c_int, [c_void_p, c_int, ctypes.POINTER(c_int)]),

@@ -177,7 +177,14 @@ int mo_plan_set_config(mo_plan p, const mo_solve_config* cfg) {
 int mo_plan_precompile(mo_plan p, int precision) {
   return guard([&] {
     need(p, "plan");
-    mo::compile_cubin(mo::generate_module(p->plan, precision != 0, mo::device_prelude()), "mo_plan.cu");
+    mo::compile_cubin(mo::generate_module(p->plan, precision != 0, mo::device_prelude()), "mo_plan.cu", p->plan.exact);
+  });
+}
+
+int mo_plan_set_exact(mo_plan p, int exact) {
+  return guard([&] {
+    need(p, "plan");
+    p->plan.exact = exact != 0;
   });
 }
 

@@ -17,7 +17,9 @@
 // tiles with a grid-stride tile loop (grid sized to the SM count), fused
 // epilogues (PCG p'Ap reduction, LM damping, identity patch of build_normal),
 // and deterministic last-block reductions.
+#include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <sstream>
 #include <string>
 
@@ -26,6 +28,8 @@
 namespace mo {
 
 namespace {
+
+constexpr int kTileX = 32, kTileY = 8, kThreads = 256;  // = MO_TILE_X/Y, MO_THREADS
 
 std::string hexd(double v) {
   char buf[64];
@@ -78,10 +82,25 @@ struct Gen {
     return f64 ? f64n[sub] : f32n[sub];
   }
 
-  // Emit `__device__ void NAME(P, p0, p1, p2, vs, out)`.
-  std::string program(const Program& pg, bool graph) {
+  // Emit `template <bool I> __device__ void NAME(P, p0, p1, p2, vs, out)`.
+  // I = true is the interior-tile variant: reads of fields living on the
+  // iteration domain skip the OOB test and InBounds folds to 1, valid when
+  // the tile is at least `reach` elements from every border; the compiler
+  // then drops the guards and can hoist every load (same values, bit for bit).
+  const Domain* iter_dom = nullptr;
+  int reach = 0;
+  std::string program(const Program& pg, bool graph, const Domain* dom = nullptr) {
     std::string name = "mo_prog_" + std::to_string(nprog++);
-    os << "__device__ __forceinline__ void " << name
+    iter_dom = graph ? nullptr : dom;
+    reach = 0;
+    for (const Instr& in : pg.instrs) {
+      bool counts = in.op == kInB;
+      if ((in.op == kLoadU || in.op == kLoadA || in.op == kLoadC || in.op == kLoadP) && !in.graph)
+        counts = iter_dom && field_of(in.op, in.field).dom == *iter_dom;
+      if (counts)
+        for (int a = 0; a < 3; ++a) reach = std::max(reach, std::abs(int(in.off[a])));
+    }
+    os << "template <bool I> __device__ __forceinline__ void " << name
        << "(const mo_kparams& P, int p0, int p1, int p2, const int* vs, Real* out) {\n";
     os << "  (void)P; (void)p0; (void)p1; (void)p2; (void)vs;\n";
     for (uint32_t r = 0; r < pg.num_regs; ++r) os << "  Real r" << r << " = (Real)0;\n";
@@ -137,7 +156,9 @@ struct Gen {
             << in.channel << ")";
         } else {
           int nd = int(f.dom.dims.size());
-          s << "mo_ld<Real, " << (nd ? nd : 1) << ", " << f.channels << ">(P.v[" << sl << "], p0 + ("
+          const bool same = iter_dom && f.dom == *iter_dom;
+          s << "mo_ld<Real, " << (nd ? nd : 1) << ", " << f.channels << ", " << (same ? "I" : "false")
+            << ">(P.v[" << sl << "], p0 + ("
             << in.off[0] << "), p1 + (" << in.off[1] << "), p2 + (" << in.off[2] << "), "
             << in.channel << ")";
         }
@@ -146,8 +167,8 @@ struct Gen {
       case kInB:
         if (graph) s << "(Real)(" << (in.off[0] == 0 ? 1 : 0) << ")";
         else
-          s << "(mo_inb(P, p0 + (" << in.off[0] << "), p1 + (" << in.off[1] << "), p2 + ("
-            << in.off[2] << ")) ? (Real)1 : (Real)0)";
+          s << "((I || mo_inb(P, p0 + (" << in.off[0] << "), p1 + (" << in.off[1] << "), p2 + ("
+            << in.off[2] << "))) ? (Real)1 : (Real)0)";
         break;
       case kAdd: s << reg(in.a) << " + " << reg(in.b); break;
       case kMul: s << reg(in.a) << " * " << reg(in.b); break;
@@ -173,6 +194,11 @@ struct Gen {
     return s.str();
   }
 
+  static std::string call(const std::string& pn) {
+    return "if (it) " + pn + "<true>(P, p0, p1, p2, nullptr, o); else " + pn +
+           "<false>(P, p0, p1, p2, nullptr, o);";
+  }
+
   static std::string kbegin(const std::string& kname) {
     return "extern \"C\" __global__ void __launch_bounds__(MO_THREADS) " + kname +
            "(const __grid_constant__ mo_kparams P) {\n";
@@ -184,11 +210,11 @@ struct Gen {
        << "  double acc = 0; bool bad = false;\n"
           "  const int nt = mo_num_tiles(P);\n"
           "  for (int t = blockIdx.x; t < nt; t += gridDim.x) {\n"
+       << "    const bool it = mo_tile_interior(P, t, " << reach << ");\n"
           "    int p0, p1, p2;\n"
           "    if (mo_tile_coord(P, t, p0, p1, p2)) {\n"
           "      Real o[1];\n      "
-       << pn
-       << "(P, p0, p1, p2, nullptr, o);\n"
+       << call(pn) << "\n"
           "      if (!mo_finite((double)o[0])) bad = true;\n"
           "      acc += (double)o[0];\n"
           "    }\n"
@@ -202,11 +228,12 @@ struct Gen {
     os << kbegin(kn) << "  bool bad = false;\n"
        << "  const int nt = mo_num_tiles(P);\n"
           "  for (int t = blockIdx.x; t < nt; t += gridDim.x) {\n"
+       << "    const bool it = mo_tile_interior(P, t, " << reach << ");\n"
           "    int p0, p1, p2;\n"
           "    if (mo_tile_coord(P, t, p0, p1, p2)) {\n"
           "      const int e = mo_local_elem(P, p0, p1, p2);\n"
           "      Real o["
-       << (nout ? nout : 1) << "];\n      " << pn << "(P, p0, p1, p2, nullptr, o);\n";
+       << (nout ? nout : 1) << "];\n      " << call(pn) << "\n";
     for (size_t k = 0; k < nout; ++k)
       os << "      if (!mo_finite((double)o[" << k << "])) bad = true;\n"
          << "      ((Real*)P.out0)[P.rowbase[" << k << "] + e] = o[" << k << "];\n";
@@ -218,11 +245,12 @@ struct Gen {
     os << kbegin(kn) << "  bool bad = false;\n"
        << "  const int nt = mo_num_tiles(P);\n"
           "  for (int t = blockIdx.x; t < nt; t += gridDim.x) {\n"
+       << "    const bool it = mo_tile_interior(P, t, " << reach << ");\n"
           "    int p0, p1, p2;\n"
           "    if (mo_tile_coord(P, t, p0, p1, p2)) {\n"
           "      const long long e = mo_local_elem(P, p0, p1, p2);\n"
           "      Real o["
-       << (nout ? nout : 1) << "];\n      " << pn << "(P, p0, p1, p2, nullptr, o);\n";
+       << (nout ? nout : 1) << "];\n      " << call(pn) << "\n";
     for (size_t k = 0; k < nout; ++k)
       os << "      if (!mo_finite((double)o[" << k << "])) bad = true;\n"
          << "      ((Real*)P.out0)[e * " << nout << " + " << k << "] = o[" << k << "];\n";
@@ -233,12 +261,12 @@ struct Gen {
     os << kbegin(kn)
        << "  const int nt = mo_num_tiles(P);\n"
           "  for (int t = blockIdx.x; t < nt; t += gridDim.x) {\n"
+       << "    const bool it = mo_tile_interior(P, t, " << reach << ");\n"
           "    int p0, p1, p2;\n"
           "    if (mo_tile_coord(P, t, p0, p1, p2)) {\n"
           "      const int e = mo_local_elem(P, p0, p1, p2);\n"
           "      Real o[1];\n      "
-       << pn
-       << "(P, p0, p1, p2, nullptr, o);\n"
+       << call(pn) << "\n"
           "      ((unsigned char*)P.out0)[e] = (o[0] != (Real)0) ? 1 : 0;\n"
           "    }\n  }\n}\n";
   }
@@ -250,6 +278,7 @@ struct Gen {
        << "  Real* B = (Real*)P.out0; Real* M = (Real*)P.out1;\n"
           "  const int nt = mo_num_tiles(P);\n"
           "  for (int t = blockIdx.x; t < nt; t += gridDim.x) {\n"
+       << "    const bool it = mo_tile_interior(P, t, " << reach << ");\n"
           "    int p0, p1, p2;\n"
           "    if (mo_tile_coord(P, t, p0, p1, p2)) {\n"
           "      const long long e = mo_local_elem(P, p0, p1, p2);\n"
@@ -259,7 +288,7 @@ struct Gen {
           "      const bool ex = P.mask && P.mask[e];\n"
           "      if (ex) {\n"
        << "        for (int k = 0; k < " << 2 * K << "; ++k) o[k] = (Real)0;\n"
-       << "      } else {\n        " << pn << "(P, p0, p1, p2, nullptr, o);\n"
+       << "      } else {\n        " << call(pn) << "\n"
        << "        for (int k = 0; k < " << 2 * K << "; ++k) if (!mo_finite((double)o[k])) bad = true;\n"
        << "      }\n";
     for (size_t k = 0; k < K; ++k) {
@@ -286,6 +315,7 @@ struct Gen {
        << "  Real* OUT = (Real*)P.out0; const Real* PV = (const Real*)P.in0; const Real* DAMP = (const Real*)P.in1;\n"
           "  const int nt = mo_num_tiles(P);\n"
           "  for (int t = blockIdx.x; t < nt; t += gridDim.x) {\n"
+       << "    const bool it = mo_tile_interior(P, t, " << reach << ");\n"
           "    int p0, p1, p2;\n"
           "    if (mo_tile_coord(P, t, p0, p1, p2)) {\n"
           "      const long long e = mo_local_elem(P, p0, p1, p2);\n"
@@ -295,7 +325,7 @@ struct Gen {
           "      const bool ex = P.mask && P.mask[e];\n"
           "      if (ex) {\n"
        << "        for (int k = 0; k < " << K << "; ++k) o[k] = (Real)0;\n"
-       << "      } else {\n        " << pn << "(P, p0, p1, p2, nullptr, o);\n"
+       << "      } else {\n        " << call(pn) << "\n"
        << "        for (int k = 0; k < " << K << "; ++k) if (!mo_finite((double)o[k])) bad = true;\n"
        << "      }\n";
     for (size_t k = 0; k < K; ++k) {
@@ -312,6 +342,128 @@ struct Gen {
        << "  if (P.flags & MO_F_REDUCE) mo_reduce_epilogue<Real>(P.red, acc, 0.0, false);\n}\n";
   }
 
+  // Two-phase matrix-free normal apply (the fast path; exact mode keeps the
+  // gather program above).  Mathematically identical to the reference gather
+  // (transform.hpp:238-260): jtj_c(q) = 2 sum_t sum_{lanes l of t on (f,c)}
+  // d_l(q - o_l) * Jp_t(q - o_l) with Jp_t(e) = sum_{l in t} d_l(e) p(e + o_l)
+  // and d_l the per-template partials of the reference's evalj program
+  // (plan.hpp:244-264; already guarded by the implicit bound guard).
+  // Phase 1 evaluates evalj ONCE per element of the tile plus an H-halo and
+  // stores c_l(e) = d_l(e) Jp_t(e) in shared memory; phase 2 gathers.  This
+  // removes the gather program's per-neighbour recomputation of every shifted
+  // residual instance (ARAP: 114 vs 386 instructions per element).
+  // Returns false (no kernel) when the domain is 3-D or no lanes exist.
+  struct TwoPhase {
+    bool ok = false;
+    int H = 0, reach = 0, nlanes = 0;
+    size_t smem = 0;
+  };
+
+  TwoPhase gather_jtj2(const GatherSet& g, int gi) {
+    TwoPhase tp;
+    const GridSet* S = nullptr;
+    for (const GridSet& s : P.grid_sets)
+      if (s.dom == g.dom && s.has_evalj) S = &s;
+    const int nd = int(g.dom.dims.size());
+    if (!S || nd < 1 || nd > 2) return tp;
+    struct L {
+      int t, out, f, c, o0, o1;
+    };
+    std::vector<L> lanes;
+    for (size_t t = 0; t < S->jtemplates.size(); ++t)
+      for (const Lane& ln : S->jtemplates[t].lanes) {
+        if (ln.off[2] != 0 || (nd == 1 && ln.off[1] != 0)) return tp;
+        lanes.push_back({int(t), ln.out, ln.field, ln.channel, ln.off[0], ln.off[1]});
+      }
+    if (lanes.empty()) return tp;
+    int H = 0;
+    for (const L& l : lanes) H = std::max({H, std::abs(l.o0), std::abs(l.o1)});
+    const std::string pe = program(S->evalj, false, &g.dom);
+    const int R = H + std::max(reach, H);
+    const int NO = int(S->evalj.outputs.size());
+    const int WX = nd == 2 ? kTileX + 2 * H : kThreads + 2 * H;
+    const int WY = nd == 2 ? kTileY + 2 * H : 1;
+    const int NE = WX * WY;
+    const int SY = nd == 2 ? WX : 1;  // shared-memory stride of axis 0
+    const int NL = int(lanes.size());
+    const int U = int(P.unknowns.size());
+    const std::string sfx = std::to_string(gi);
+    // Phase-1 body for one haloed element k at (p0, p1).
+    os << "template <bool I> __device__ __forceinline__ void mo_lanes_" << sfx
+       << "(const mo_kparams& P, int p0, int p1, int k, Real* CL) {\n"
+       << "  Real d[" << NO << "];\n  " << pe << "<I>(P, p0, p1, 0, nullptr, d);\n";
+    for (size_t t = 0; t < S->jtemplates.size(); ++t) {
+      os << "  { Real jp = (Real)0;\n";
+      for (const L& l : lanes) {
+        if (l.t != int(t)) continue;
+        const Field& f = P.unknowns[size_t(l.f)];
+        os << "    jp += d[" << l.out << "] * mo_ld<Real, " << nd << ", " << f.channels << ", I>(P.v[" << U + l.f
+           << "], p0 + (" << l.o0 << "), p1 + (" << l.o1 << "), 0, " << l.c << ");\n";
+      }
+      for (int li = 0; li < NL; ++li)
+        if (lanes[size_t(li)].t == int(t))
+          os << "    CL[" << li * NE << " + k] = d[" << lanes[size_t(li)].out << "] * jp;\n";
+      os << "  }\n";
+    }
+    os << "}\n";
+    const std::string kn = "mo_gather_jtj2_" + sfx;
+    os << "extern \"C\" __global__ void __launch_bounds__(MO_THREADS) " << kn
+       << "(const __grid_constant__ mo_kparams P) {\n"
+       << "  if ((P.flags & MO_F_SKIPDONE) && P.state->done) return;\n"
+       << "  extern __shared__ __align__(16) unsigned char mo_smem[];\n"
+       << "  Real* CL = reinterpret_cast<Real*>(mo_smem);  // [" << NL << " lanes][" << NE << " elements]\n"
+       << "  double acc = 0; bool bad = false;\n"
+       << "  Real* OUT = (Real*)P.out0; const Real* PV = (const Real*)P.in0; const Real* DAMP = (const Real*)P.in1;\n"
+       << "  const int tid = threadIdx.x + threadIdx.y * blockDim.x;\n"
+       << "  const int nt = mo_num_tiles(P);\n"
+       << "  for (int t = blockIdx.x; t < nt; t += gridDim.x) {\n"
+       << "    const bool it = mo_tile_interior(P, t, " << R << ");\n";
+    if (nd == 2)
+      os << "    const int ntx = (P.d1 + MO_TILE_X - 1) / MO_TILE_X;\n"
+         << "    const int r0 = P.row0 + (t / ntx) * MO_TILE_Y - " << H << ", c0 = (t % ntx) * MO_TILE_X - " << H
+         << ";\n"
+         << "    for (int k = tid; k < " << NE << "; k += MO_THREADS) {\n"
+         << "      const int q0 = r0 + k / " << WX << ", q1 = c0 + k % " << WX << ";\n";
+    else
+      os << "    const int r0 = P.row0 + t * MO_THREADS - " << H << ", c0 = 0; (void)c0;\n"
+         << "    for (int k = tid; k < " << NE << "; k += MO_THREADS) {\n"
+         << "      const int q0 = r0 + k, q1 = 0;\n";
+    os << "      if (it) mo_lanes_" << sfx << "<true>(P, q0, q1, k, CL); else mo_lanes_" << sfx
+       << "<false>(P, q0, q1, k, CL);\n"
+       << "    }\n    __syncthreads();\n"
+       << "    int p0, p1, p2;\n"
+       << "    if (mo_tile_coord(P, t, p0, p1, p2)) {\n"
+       << "      const long long e = mo_local_elem(P, p0, p1, p2);\n"
+       << "      const int hb = (p0 - r0) * " << SY << (nd == 2 ? " + (p1 - c0)" : "") << ";\n"
+       << "      const bool ex = P.mask && P.mask[e];\n";
+    for (size_t k = 0; k < g.chans.size(); ++k) {
+      const int f = g.chans[k].first, ch = g.chans[k].second;
+      const int C = P.unknowns[size_t(f)].channels;
+      os << "      { Real s = (Real)0;\n";
+      for (int li = 0; li < NL; ++li) {
+        const L& l = lanes[size_t(li)];
+        if (l.f != f || l.c != ch) continue;
+        os << "        s += CL[" << li * NE << " + hb - (" << l.o0 * SY + (nd == 2 ? l.o1 : 0) << ")];\n";
+      }
+      os << "        Real v = ex ? (Real)0 : (Real)2 * s;\n"
+         << "        if (!mo_finite((double)v)) bad = true;\n"
+         << "        const long long col = P.ubase[" << f << "] + e * " << C << " + " << ch << ";\n"
+         << "        if (P.flags & MO_F_DAMP) v = v + DAMP[col] * PV[col];\n"
+         << "        if ((P.flags & MO_F_ZEROEXCL) && P.colmask && P.colmask[col]) v = (Real)0;\n"
+         << "        OUT[col] = v;\n"
+         << "        if (P.flags & MO_F_REDUCE) acc += (double)(PV[col] * v); }\n";
+    }
+    os << "    }\n    __syncthreads();\n  }\n"
+       << "  if (bad) atomicOr(&P.state->nonfinite_kernel, 1);\n"
+       << "  if (P.flags & MO_F_REDUCE) mo_reduce_epilogue<Real>(P.red, acc, 0.0, false);\n}\n";
+    tp.ok = true;
+    tp.H = H;
+    tp.reach = R;
+    tp.nlanes = NL;
+    tp.smem = size_t(NL) * size_t(NE) * (f64 ? 8 : 4);
+    return tp;
+  }
+
   // --------------------------------------------------------- graph kernels
   // One thread per hyperedge (exec.hpp:223-309); scatter outputs go to a
   // per-edge contribution buffer that the deterministic vertex gather folds
@@ -324,7 +476,7 @@ struct Gen {
           " e += (long long)gridDim.x * blockDim.x) {\n"
        << "    int vs[" << (arity ? arity : 1) << "];\n";
     for (int s = 0; s < arity; ++s) os << "    vs[" << s << "] = P.verts[e * " << arity << " + " << s << "];\n";
-    os << "    Real o[" << (nout ? nout : 1) << "];\n    " << pn << "(P, 0, 0, 0, vs, o);\n";
+    os << "    Real o[" << (nout ? nout : 1) << "];\n    " << pn << "<false>(P, 0, 0, 0, vs, o);\n";
     for (size_t k = 0; k < nout; ++k) {
       os << "    if (!mo_finite((double)o[" << k << "])) bad = true;\n";
       if (mode == 0) os << "    acc += (double)o[0];\n";
@@ -336,16 +488,20 @@ struct Gen {
     os << "}\n";
   }
 
+  ModuleInfo info;
+
   void run() {
     for (size_t i = 0; i < P.grid_sets.size(); ++i) {
       const GridSet& g = P.grid_sets[i];
-      grid_cost(program(g.cost, false), "mo_grid_cost_" + std::to_string(i));
-      grid_evalf(program(g.evalf, false), "mo_grid_evalf_" + std::to_string(i), g.evalf.outputs.size());
+      grid_cost(program(g.cost, false, &g.dom), "mo_grid_cost_" + std::to_string(i));
+      grid_evalf(program(g.evalf, false, &g.dom), "mo_grid_evalf_" + std::to_string(i), g.evalf.outputs.size());
     }
     for (size_t i = 0; i < P.gather_sets.size(); ++i) {
       const GatherSet& g = P.gather_sets[i];
-      gather_bm(g, program(g.bm, false), "mo_gather_bm_" + std::to_string(i));
-      gather_jtj(g, program(g.jtj, false), "mo_gather_jtj_" + std::to_string(i));
+      gather_bm(g, program(g.bm, false, &g.dom), "mo_gather_bm_" + std::to_string(i));
+      gather_jtj(g, program(g.jtj, false, &g.dom), "mo_gather_jtj_" + std::to_string(i));
+      TwoPhase tp = gather_jtj2(g, int(i));
+      info.jtj2.push_back({tp.ok, tp.smem, tp.nlanes, tp.H});
     }
     for (size_t i = 0; i < P.graph_sets.size(); ++i) {
       const GraphSet& g = P.graph_sets[i];
@@ -358,21 +514,22 @@ struct Gen {
     }
     for (size_t i = 0; i < P.computed_kernels.size(); ++i) {
       const ComputedKernel& ck = P.computed_kernels[i];
-      grid_store(program(ck.prog, false), "mo_computed_" + std::to_string(i), ck.prog.outputs.size());
+      grid_store(program(ck.prog, false, &ck.dom), "mo_computed_" + std::to_string(i), ck.prog.outputs.size());
     }
     for (size_t i = 0; i < P.exclude_kernels.size(); ++i)
-      grid_exclude(program(P.exclude_kernels[i].prog, false), "mo_exclude_" + std::to_string(i));
+      grid_exclude(program(P.exclude_kernels[i].prog, false, &P.exclude_kernels[i].dom), "mo_exclude_" + std::to_string(i));
   }
 };
 
 }  // namespace
 
-std::string generate_module(const Plan& P, bool f64, const std::string& prelude) {
+std::string generate_module(const Plan& P, bool f64, const std::string& prelude, ModuleInfo* info) {
   Gen g(P, f64);
   g.os << "// generated by mo_codegen.cpp — do not edit\n";
   g.os << "typedef " << (f64 ? "double" : "float") << " Real;\n";
   g.os << prelude << "\n";
   g.run();
+  if (info) *info = g.info;
   return g.os.str();
 }
 

@@ -286,12 +286,36 @@ __device__ __forceinline__ bool mo_inb(const mo_kparams& P, int c0, int c1, int 
   return true;
 }
 
+// Is tile t at least R elements away from every border of the iteration
+// domain?  Then every InBounds(off) with |off| <= R is true and every read of
+// a field living on the iteration domain is in shape (uniform per block).
+__device__ __forceinline__ bool mo_tile_interior(const mo_kparams& P, int t, int R) {
+  if (P.dnd == 1) {
+    const int lo = P.row0 + t * MO_THREADS;
+    return lo - R >= 0 && lo + MO_THREADS - 1 + R < P.d0;
+  }
+  if (P.dnd == 2) {
+    const int ntx = (P.d1 + MO_TILE_X - 1) / MO_TILE_X;
+    const int r0 = P.row0 + (t / ntx) * MO_TILE_Y, c0 = (t % ntx) * MO_TILE_X;
+    return r0 - R >= 0 && r0 + MO_TILE_Y - 1 + R < P.d0 && c0 - R >= 0 && c0 + MO_TILE_X - 1 + R < P.d1;
+  }
+  const int ntx = (P.d2 + MO_TILE_X - 1) / MO_TILE_X;
+  const int nty = (P.d1 + MO_TILE_Y - 1) / MO_TILE_Y;
+  const int r = t / ntx;
+  const int p0 = P.row0 + r / nty, y0 = (r % nty) * MO_TILE_Y, x0 = (t % ntx) * MO_TILE_X;
+  return p0 - R >= 0 && p0 + R < P.d0 && y0 - R >= 0 && y0 + MO_TILE_Y - 1 + R < P.d1 && x0 - R >= 0 &&
+         x0 + MO_TILE_X - 1 + R < P.d2;
+}
+
 // Grid read with the OOB->0 rule against the FIELD's own shape (eval.hpp:41-55).
-template <class Real, int ND, int C>
+// UNCHECKED: caller proved the coordinate in shape (interior tile).
+template <class Real, int ND, int C, bool UNCHECKED = false>
 __device__ __forceinline__ Real mo_ld(const mo_view& v, int c0, int c1, int c2, int ch) {
-  if ((unsigned)c0 >= (unsigned)v.s0) return Real(0);
-  if (ND >= 2 && (unsigned)c1 >= (unsigned)v.s1) return Real(0);
-  if (ND >= 3 && (unsigned)c2 >= (unsigned)v.s2) return Real(0);
+  if (!UNCHECKED) {
+    if ((unsigned)c0 >= (unsigned)v.s0) return Real(0);
+    if (ND >= 2 && (unsigned)c1 >= (unsigned)v.s1) return Real(0);
+    if (ND >= 3 && (unsigned)c2 >= (unsigned)v.s2) return Real(0);
+  }
   int e = c0 - v.row_lo;
   if (ND >= 2) e = e * v.s1 + c1;
   if (ND >= 3) e = e * v.s2 + c2;

@@ -56,16 +56,18 @@ void mkdirs(const std::string& path) {
   }
 }
 
-const char* kOpts[] = {"-arch=sm_100a", "--fmad=false", "-std=c++17", "-lineinfo",
+const char* kOpts[] = {"-arch=sm_100a", "-std=c++17", "-lineinfo",
                        "-default-device", "--extra-device-vectorization"};
 
 }  // namespace
 
-std::vector<char> compile_cubin(const std::string& src, const std::string& name, std::string* log_out) {
+std::vector<char> compile_cubin(const std::string& src, const std::string& name, bool exact, std::string* log_out) {
+  std::vector<const char*> opts(std::begin(kOpts), std::end(kOpts));
+  opts.push_back(exact ? "--fmad=false" : "--fmad=true");
   int maj = 0, min = 0;
   nvrtcVersion(&maj, &min);
   std::string key = src;
-  for (const char* o : kOpts) key += o;
+  for (const char* o : opts) key += o;
   key += std::to_string(maj) + "." + std::to_string(min);
   char hex[32];
   std::snprintf(hex, sizeof hex, "%016llx", (unsigned long long)fnv1a(key));
@@ -81,7 +83,7 @@ std::vector<char> compile_cubin(const std::string& src, const std::string& name,
   nvrtcProgram prog;
   check(nvrtcCreateProgram(&prog, src.c_str(), name.c_str(), 0, nullptr, nullptr) == NVRTC_SUCCESS,
         Err::kInternal, "nvrtcCreateProgram failed");
-  nvrtcResult r = nvrtcCompileProgram(prog, int(sizeof(kOpts) / sizeof(kOpts[0])), kOpts);
+  nvrtcResult r = nvrtcCompileProgram(prog, int(opts.size()), opts.data());
   size_t logsz = 0;
   nvrtcGetProgramLogSize(prog, &logsz);
   std::string log(logsz, '\0');

@@ -11,7 +11,9 @@ namespace mo {
 
 // Compile CUDA C++ to an sm_100a cubin (cached on disk under $MO_B200_CACHE or
 // ~/.cache/mo_b200).  Works without a GPU.
-std::vector<char> compile_cubin(const std::string& src, const std::string& name,
+// exact = true compiles with --fmad=false (no FMA contraction: add/mul round
+// exactly like the reference's x86 build); false allows contraction.
+std::vector<char> compile_cubin(const std::string& src, const std::string& name, bool exact,
                                 std::string* log = nullptr);
 
 class Module {

@@ -43,7 +43,46 @@ k_pcg_init(mo_red R, long long n, const unsigned char* cm, const Real* __restric
   mo_reduce_epilogue<Real>(R, acc, 0.0, false);
 }
 
+// 4-wide vector access (16-byte for float, 2 x 16-byte for double).  Column
+// vectors come from cudaMalloc (256-byte aligned) and are indexed from 0.
+template <class Real>
+struct V4 {
+  Real a[4];
+};
+__device__ __forceinline__ V4<float> ld4(const float* p) {
+  const float4 t = *reinterpret_cast<const float4*>(p);
+  return {{t.x, t.y, t.z, t.w}};
+}
+__device__ __forceinline__ V4<double> ld4(const double* p) {
+  const double2 t0 = reinterpret_cast<const double2*>(p)[0], t1 = reinterpret_cast<const double2*>(p)[1];
+  return {{t0.x, t0.y, t1.x, t1.y}};
+}
+__device__ __forceinline__ void st4(float* p, const V4<float>& v) {
+  *reinterpret_cast<float4*>(p) = make_float4(v.a[0], v.a[1], v.a[2], v.a[3]);
+}
+__device__ __forceinline__ void st4(double* p, const V4<double>& v) {
+  reinterpret_cast<double2*>(p)[0] = make_double2(v.a[0], v.a[1]);
+  reinterpret_cast<double2*>(p)[1] = make_double2(v.a[2], v.a[3]);
+}
+__device__ __forceinline__ uchar4 ldm4(const unsigned char* cm, long long i) {
+  return cm ? *reinterpret_cast<const uchar4*>(cm + i) : make_uchar4(0, 0, 0, 0);
+}
+
 // delta += alpha p; r -= alpha Ap; z = r/m; rz' = r'z   (pcg.hpp:111-118)
+template <class Real>
+__device__ __forceinline__ double pcg_update1(Real alpha, bool ex, Real& d, Real& r, Real p, Real ap, Real md,
+                                              int precond) {
+  if (ex) {
+    d = Real(0);
+    r = Real(0);
+    return 0.0;
+  }
+  d = d + alpha * p;
+  r = r - alpha * ap;
+  const Real z = precond ? r / md : r;
+  return double(r * z);
+}
+
 template <class Real>
 __global__ void __launch_bounds__(MO_THREADS)
 k_pcg_update(mo_red R, long long n, const unsigned char* cm, const Real* __restrict__ md,
@@ -52,39 +91,52 @@ k_pcg_update(mo_red R, long long n, const unsigned char* cm, const Real* __restr
   if (R.state->done) return;
   const Real alpha = Real(R.state->alpha);
   double acc = 0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    if (ex_at(cm, i)) {
-      delta[i] = Real(0);
-      r[i] = Real(0);
-      continue;
-    }
-    const Real d = delta[i] + alpha * p[i];
-    const Real ri = r[i] - alpha * ap[i];
-    const Real zi = precond ? ri / md[i] : ri;
-    delta[i] = d;
-    r[i] = ri;
-    acc += double(ri * zi);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long n4 = n >> 2;
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n4; v += stride) {
+    const long long i = v << 2;
+    V4<Real> D = ld4(delta + i), Rr = ld4(r + i);
+    const V4<Real> Pp = ld4(p + i), A = ld4(ap + i), M = ld4(md + i);
+    const uchar4 e = ldm4(cm, i);
+    const bool ex[4] = {e.x != 0, e.y != 0, e.z != 0, e.w != 0};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc += pcg_update1(alpha, ex[k], D.a[k], Rr.a[k], Pp.a[k], A.a[k], M.a[k], precond);
+    st4(delta + i, D);
+    st4(r + i, Rr);
   }
+  for (long long i = (n4 << 2) + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride)
+    acc += pcg_update1(alpha, ex_at(cm, i), delta[i], r[i], p[i], ap[i], md[i], precond);
   mo_reduce_epilogue<Real>(R, acc, 0.0, false);
 }
 
 // p = z + beta p with z = r/m recomputed   (pcg.hpp:124-126)
+template <class Real>
+__device__ __forceinline__ Real pcg_p1(Real beta, bool ex, Real r, Real md, Real p, int precond) {
+  if (ex) return Real(0);
+  const Real z = precond ? r / md : r;
+  return z + beta * p;
+}
+
 template <class Real>
 __global__ void __launch_bounds__(MO_THREADS)
 k_pcg_p(const mo_state* st, long long n, const unsigned char* cm, const Real* __restrict__ md,
         const Real* __restrict__ r, Real* __restrict__ p, int precond) {
   if (st->done) return;
   const Real beta = Real(st->beta);
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    if (ex_at(cm, i)) {
-      p[i] = Real(0);
-      continue;
-    }
-    const Real zi = precond ? r[i] / md[i] : r[i];
-    p[i] = zi + beta * p[i];
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long n4 = n >> 2;
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n4; v += stride) {
+    const long long i = v << 2;
+    const V4<Real> Rr = ld4(r + i), M = ld4(md + i);
+    V4<Real> Pp = ld4(p + i);
+    const uchar4 e = ldm4(cm, i);
+    const bool ex[4] = {e.x != 0, e.y != 0, e.z != 0, e.w != 0};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) Pp.a[k] = pcg_p1(beta, ex[k], Rr.a[k], M.a[k], Pp.a[k], precond);
+    st4(p + i, Pp);
   }
+  for (long long i = (n4 << 2) + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride)
+    p[i] = pcg_p1(beta, ex_at(cm, i), r[i], md[i], p[i], precond);
 }
 
 // Unfused apply epilogue (plans with graph scatters): LM damping, excluded

@@ -17,6 +17,14 @@ struct Lexer {
     if (!(is >> w)) fail(Err::kTruncatedFile, "moplan: unexpected end of input");
     return w;
   }
+  std::string peek() {
+    auto pos = is.tellg();
+    std::string w;
+    is >> w;
+    is.clear();
+    is.seekg(pos);
+    return w;
+  }
   void expect(const char* kw) {
     std::string w = word();
     check(w == kw, Err::kFormatError, std::string("moplan: expected '") + kw + "', got '" + w + "'");
@@ -206,6 +214,33 @@ Plan parse_plan(const std::string& text) {
     for (long long t = 0; t < nt; ++t) g.templates.push_back(int(L.integer()));
     g.cost = L.program("cost");
     g.evalf = L.program("evalf");
+    if (L.peek() == "evalj") {
+      L.expect("evalj");
+      long long njt = L.integer();
+      for (long long k = 0; k < njt; ++k) {
+        L.expect("jtemplate");
+        JTemplate jt;
+        jt.tmpl = int(L.integer());
+        jt.guard_out = int(L.integer());
+        long long nl = L.integer();
+        for (long long l = 0; l < nl; ++l) {
+          Lane ln;
+          ln.out = int(L.integer());
+          ln.field = int(L.integer());
+          ln.channel = int(L.integer());
+          for (int a = 0; a < 3; ++a) ln.off[a] = int(L.integer());
+          jt.lanes.push_back(ln);
+        }
+        g.jtemplates.push_back(std::move(jt));
+      }
+      g.evalj = L.program("evalj");
+      g.has_evalj = true;
+      for (const JTemplate& jt : g.jtemplates)
+        for (const Lane& ln : jt.lanes)
+          check(ln.out >= 0 && size_t(ln.out) < g.evalj.outputs.size() && ln.field >= 0 &&
+                    size_t(ln.field) < P.unknowns.size(),
+                Err::kFormatError, "moplan: bad Jacobian lane");
+    }
     P.grid_sets.push_back(std::move(g));
   }
   L.expect("gather_sets");

@@ -95,10 +95,24 @@ struct Residual {
   int graph_idx = -1;
 };
 
+// One materialized-Jacobian lane (plan.hpp:50-56): evalj output `out` is
+// d r_t / d x[field, channel](e + off).
+struct Lane {
+  int out = 0, field = 0, channel = 0;
+  int off[3] = {0, 0, 0};
+};
+struct JTemplate {
+  int tmpl = 0, guard_out = 0;
+  std::vector<Lane> lanes;
+};
+
 struct GridSet {
   Domain dom;
   std::vector<int> templates;
   Program cost, evalf;
+  bool has_evalj = false;  // plan exported with force_evalj (two-phase apply)
+  std::vector<JTemplate> jtemplates;
+  Program evalj;
 };
 struct GatherSet {
   Domain dom;
@@ -138,6 +152,7 @@ struct Plan {
   std::vector<GraphSet> graph_sets;
   std::vector<ComputedKernel> computed_kernels;
   std::vector<ExcludeKernel> exclude_kernels;
+  bool exact = false;  // compile without FMA contraction (bitwise-faithful mode)
 
   std::array<int64_t, 3> shape_of(const Domain& d) const {
     std::array<int64_t, 3> s{1, 1, 1};

@@ -74,8 +74,8 @@ class Session final : public SessionBase {
     if (cfg_.pcg_rel_tol < 0) cfg_.pcg_rel_tol = cfg_.precision == 0 ? 1e-4 : 1e-8;
 
     // JIT the plan's per-element kernels (plan time; cached on disk).
-    std::string src = generate_module(P_, sizeof(Real) == 8, device_prelude());
-    mod_.load(compile_cubin(src, "mo_plan.cu"));
+    std::string src = generate_module(P_, sizeof(Real) == 8, device_prelude(), &minfo_);
+    mod_.load(compile_cubin(src, "mo_plan.cu", P_.exact));
 
     const size_t n = size_t(P_.num_cols);
     x_ = dalloc<Real>(n);
@@ -737,20 +737,22 @@ class Session final : public SessionBase {
     if (nd == 2) return int(((s[1] + MO_TILE_X - 1) / MO_TILE_X) * ((rows + MO_TILE_Y - 1) / MO_TILE_Y));
     return int(((s[2] + MO_TILE_X - 1) / MO_TILE_X) * rows * ((s[1] + MO_TILE_Y - 1) / MO_TILE_Y));
   }
-  int occupancy(const void* f) {
+  int occupancy(const void* f, size_t smem = 0) {
     auto it = occ_.find(f);
     if (it != occ_.end()) return it->second;
+    if (smem > 48 * 1024)
+      CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, f, MO_THREADS, 0) != cudaSuccess || n <= 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, f, MO_THREADS, smem) != cudaSuccess || n <= 0) {
       cudaGetLastError();
-      n = 2;
+      n = 1;
     }
     occ_[f] = n;
     return n;
   }
-  int grid_blocks(const std::string& name, const Domain& d) {
+  int grid_blocks(const std::string& name, const Domain& d, size_t smem = 0) {
     const void* f = mod_.kernel(name);
-    long long g = std::min<long long>(tiles_of(d), (long long)nsm_ * occupancy(f));
+    long long g = std::min<long long>(tiles_of(d), (long long)nsm_ * occupancy(f, smem));
     return int(std::max<long long>(g, 1));
   }
   int edge_blocks(const std::string& name, int gi) {
@@ -759,14 +761,21 @@ class Session final : public SessionBase {
     long long g = std::min<long long>((E + MO_THREADS - 1) / MO_THREADS, (long long)nsm_ * occupancy(f));
     return int(std::max<long long>(g, 1));
   }
-  void launch_grid(const std::string& name, const Domain& d, const mo_kparams& kp, int grid = 0) {
+  void launch_grid(const std::string& name, const Domain& d, const mo_kparams& kp, int grid = 0, size_t smem = 0) {
     const void* f = mod_.kernel(name);
-    if (grid <= 0) grid = grid_blocks(name, d);
+    if (grid <= 0) grid = grid_blocks(name, d, smem);
     dim3 block = d.dims.size() <= 1 ? dim3(MO_THREADS, 1, 1) : dim3(MO_TILE_X, MO_TILE_Y, 1);
     void* args[] = {const_cast<mo_kparams*>(&kp)};
-    CK(cudaLaunchKernel(f, dim3(grid), block, args, 0, st_));
+    CK(cudaLaunchKernel(f, dim3(grid), block, args, smem, st_));
     ++launches_;
   }
+  // Fast-path apply kernel of gather set i: the two-phase evalj kernel unless
+  // the plan asked for exact (reference-program) execution.
+  bool two_phase(size_t i) const { return !P_.exact && i < minfo_.jtj2.size() && minfo_.jtj2[i].ok; }
+  std::string jtj_kernel(size_t i) const {
+    return (two_phase(i) ? "mo_gather_jtj2_" : "mo_gather_jtj_") + std::to_string(i);
+  }
+  size_t jtj_smem(size_t i) const { return two_phase(i) ? minfo_.jtj2[i].smem : 0; }
   void launch_edges(const std::string& name, int gi, const mo_kparams& kp, int grid = 0) {
     const void* f = mod_.kernel(name);
     if (grid <= 0) grid = edge_blocks(name, gi);
@@ -878,7 +887,7 @@ class Session final : public SessionBase {
     std::vector<int> grids;
     int total = 0;
     for (size_t i = 0; i < P_.gather_sets.size(); ++i) {
-      grids.push_back(grid_blocks("mo_gather_jtj_" + std::to_string(i), P_.gather_sets[i].dom));
+      grids.push_back(grid_blocks(jtj_kernel(i), P_.gather_sets[i].dom, jtj_smem(i)));
       total += grids.back();
     }
     if (!fused) total = vgrid(n, nsm_);
@@ -890,7 +899,7 @@ class Session final : public SessionBase {
       kp.in1 = damp_;
       kp.flags = fused ? flags : (flags & MO_F_SKIPDONE);
       kp.red = red(base, total, MO_FIN_PCG_ALPHA, 0);
-      launch_grid("mo_gather_jtj_" + std::to_string(i), P_.gather_sets[i].dom, kp, grids[i]);
+      launch_grid(jtj_kernel(i), P_.gather_sets[i].dom, kp, grids[i], jtj_smem(i));
       base += grids[i];
     }
     if (!fused) {
@@ -963,6 +972,13 @@ class Session final : public SessionBase {
   }
 
   // ------------------------------------------------------------ profiling
+  // Inside stream capture an event record must be an external event node to
+  // be timed; outside capture it is a plain record.
+  unsigned capture_flags() {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(st_, &cs));
+    return cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
+  }
   void prof_reset_slots() {
     for (auto& p : prof_) p.used = 0;
   }
@@ -975,12 +991,12 @@ class Session final : public SessionBase {
       CK(cudaEventCreate(&b));
       p.ev.push_back({a, b});
     }
-    CK(cudaEventRecord(p.ev[p.used].first, st_));
+    CK(cudaEventRecordWithFlags(p.ev[p.used].first, st_, capture_flags()));
   }
   void prof_end(int kind) {
     if (!profiling_) return;
     Prof& p = prof_[size_t(kind)];
-    CK(cudaEventRecord(p.ev[p.used].second, st_));
+    CK(cudaEventRecordWithFlags(p.ev[p.used].second, st_, capture_flags()));
     p.used++;
     prof_pending_ = true;
   }
@@ -1038,6 +1054,7 @@ class Session final : public SessionBase {
   int64_t unconstrained_ = 0;
   bool x_bound_ = false, params_bound_ = false, refreshed_ = false;
   std::map<const void*, int> occ_;
+  ModuleInfo minfo_;
   std::map<bool, cudaGraphExec_t> pcg_exec_;
   std::map<bool, int64_t> pcg_nodes_;
   std::vector<void*> owned_;

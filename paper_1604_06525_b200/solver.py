@@ -132,11 +132,15 @@ class SolveResult:  # solver.hpp:58-74
 class CompiledPlan:
     """A parsed moplan (the reference's CompiledPlan, plan.hpp:125-137)."""
 
-    def __init__(self, text: str, cfg: Optional[SolveConfig] = None, dims: Optional[dict] = None):
+    def __init__(self, text: str, cfg: Optional[SolveConfig] = None, dims: Optional[dict] = None,
+                 exact: bool = False):
         h = ctypes.c_void_p()
         b = text.encode()
         call("mo_plan_parse", b, len(b), ctypes.byref(h))
         self._h = h
+        self.exact = bool(exact)
+        if exact:
+            call("mo_plan_set_exact", self._h, 1)
         for name, extent in (dims or {}).items():
             call("mo_plan_set_dim", self._h, name.encode(), int(extent))
         if cfg is not None:
@@ -178,17 +182,20 @@ class CompiledPlan:
             self._h = None
 
 
-def plan(text: str, cfg: Optional[SolveConfig] = None, dims: Optional[dict] = None) -> CompiledPlan:
-    """plan(spec, cfg) over an exported moplan text (plan.hpp:189)."""
-    return CompiledPlan(text, cfg, dims)
+def plan(text: str, cfg: Optional[SolveConfig] = None, dims: Optional[dict] = None,
+         exact: bool = False) -> CompiledPlan:
+    """plan(spec, cfg) over an exported moplan text (plan.hpp:189).  exact=True
+    compiles the per-element kernels without FMA contraction (bitwise mode)."""
+    return CompiledPlan(text, cfg, dims, exact)
 
 
-def load_plan(name_or_path: str, cfg: Optional[SolveConfig] = None, dims: Optional[dict] = None) -> CompiledPlan:
+def load_plan(name_or_path: str, cfg: Optional[SolveConfig] = None, dims: Optional[dict] = None,
+              exact: bool = False) -> CompiledPlan:
     path = name_or_path
     if not os.path.exists(path):
         path = os.path.join(PLAN_DIR, name_or_path + ".moplan")
     with open(path) as f:
-        return CompiledPlan(f.read(), cfg, dims)
+        return CompiledPlan(f.read(), cfg, dims, exact)
 
 
 def _as(a, dtype):

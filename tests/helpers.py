@@ -36,8 +36,8 @@ class Golden:
         self.cfg = cfg_from(self.cfg_dict, self.prec)
         self.cmds = str(self.z["cmds"]).split(",")
 
-    def plan(self):
-        return load_plan(os.path.join(GOLDEN, self.name + ".moplan"), self.cfg)
+    def plan(self, exact=False):
+        return load_plan(os.path.join(GOLDEN, self.name + ".moplan"), self.cfg, exact=exact)
 
     def data(self):
         z = self.z

@@ -81,9 +81,8 @@ def test_callback_mutates_arrays():
 def test_callback_grows_graph():
     """test_solver.cpp:432-453."""
     text = open(f"{__import__('helpers').GOLDEN}/graph.moplan").read()
-    text = text.replace("dim N 2", "dim N 3")
     from paper_1604_06525_b200 import plan as mkplan
-    p = mkplan(text, SolveConfig(nonlinear_iters=2))
+    p = mkplan(text, SolveConfig(nonlinear_iters=2), dims={"N": 3})
     # energy P(a) - P(b): consistent system; grow from one edge to two
     data = SolveData(x=np.array([1.0, 0.0, 0.0]), graphs=[EdgeTable(2, np.array([0, 1], np.uint64))])
     s = Solver(p, data)

@@ -23,12 +23,13 @@ def tol(prec):
         dict(vec=1e-5, cost=2e-5, traj=1e-4, x=1e-3)
 
 
+@pytest.mark.parametrize("exact", [False, True], ids=["fma", "exact"])
 @pytest.mark.parametrize("name", NAMES)
-def test_golden_case(name):
+def test_golden_case(name, exact):
     g = Golden(name)
     t = tol(g.prec)
     data = g.data()
-    s = Solver(g.plan(), data)
+    s = Solver(g.plan(exact), data)
     assert s.num_cols() == int(g.ref("num_cols")[0])
     assert s.num_rows() == int(g.ref("num_rows")[0])
     np.testing.assert_array_equal(s.excluded(), g.ref("excluded"))
@@ -59,6 +60,23 @@ def test_golden_case(name):
             assert r.nonfinite_kernels == bool(g.ref("nonfinite_kernels")[0])
             assert r.indefinite_operator == bool(g.ref("indefinite")[0])
             assert_close_vec(data.x, g.ref("x_final"), t["x"], "x after solve")
+
+
+@pytest.mark.parametrize("name", ["cfg_poisson_f64", "cfg_poisson_f32", "chain", "dense", "volume", "tri_graph"])
+def test_exact_mode_per_element_bitwise(name):
+    """Programs without transcendental calls, compiled without FMA contraction,
+    reproduce the reference's per-element outputs bit for bit."""
+    g = Golden(name)
+    s = Solver(g.plan(exact=True), g.data())
+    for cmd in g.cmds:
+        if cmd == "residuals":
+            np.testing.assert_array_equal(s.residuals().view(np.uint8), g.ref("residuals").astype(g.dtype).view(np.uint8))
+        elif cmd == "normal":
+            s.build_normal()
+            np.testing.assert_array_equal(s.rhs(), g.ref("b"))
+            np.testing.assert_array_equal(s.precond(), g.ref("m"))
+        elif cmd == "jtj":
+            np.testing.assert_array_equal(s.apply_jtj(g.z["v"].astype(g.dtype)), g.ref("jtj"))
 
 
 def test_exclusion_keeps_negative_zero_bitwise():
