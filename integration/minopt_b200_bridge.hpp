@@ -24,7 +24,7 @@
 //   residuals N       / residual grid ND dims... | residual graph G
 //   ubase N cols... ; num_cols V
 //   grid_sets N       / grid_set ND dims... NT t...   + programs cost, evalf
-//                       [+ evalj NT / jtemplate T GUARD NL (out f c o0 o1 o2)...
+//                       [+ evalj NT / jtemplate T GUARD ORIGIN NL (out f c o0 o1 o2)...
 //                          + program evalj]   (plans built with force_evalj)
 //   gather_sets N     / gather_set ND dims... NCH (f c)...   + programs bm, jtj
 //   graph_sets N      / graph_set G NT t... NS (slot f c)... + cost, evalf, bm, jtj
@@ -36,6 +36,8 @@
 // end), NG `g` lines (guard register), NO `o` lines (nroots (gid reg)...).
 #pragma once
 
+#include <algorithm>
+#include <array>
 #include <cstdio>
 #include <sstream>
 #include <string>
@@ -145,7 +147,12 @@ inline std::string export_plan_text(const CompiledPlan& P) {
       // two-phase J^T J p evaluates these once per element.
       os << "evalj " << g.jtemplates.size() << '\n';
       for (const auto& jt : g.jtemplates) {
-        os << "jtemplate " << jt.tmpl << ' ' << jt.guard_out << ' ' << jt.lanes.size();
+        // ORIGIN: the template reads at its own pixel, so a shifted instance
+        // whose centre leaves the domain is guarded off (transform.hpp:177-198);
+        // the bound guard itself folds that test away at the origin.
+        const auto& offs = P.transformed.residuals[size_t(jt.tmpl)].offsets;
+        const bool origin = std::find(offs.begin(), offs.end(), std::array<int16_t, 3>{0, 0, 0}) != offs.end();
+        os << "jtemplate " << jt.tmpl << ' ' << jt.guard_out << ' ' << int(origin) << ' ' << jt.lanes.size();
         for (const JLane& l : jt.lanes)
           os << ' ' << l.out << ' ' << l.field << ' ' << l.channel << ' ' << l.off[0] << ' ' << l.off[1]
              << ' ' << l.off[2];

@@ -406,6 +406,7 @@ int moo_create(const char* text, size_t len, int f64, moo** out) {
         expect(&L, "jtemplate");
         (void)geti(&L);
         (void)geti(&L);
+        (void)geti(&L);
         int nl = (int)geti(&L);
         for (int q = 0; q < 6 * nl; ++q) (void)geti(&L);
       }

@@ -101,8 +101,10 @@ struct Gen {
         for (int a = 0; a < 3; ++a) reach = std::max(reach, std::abs(int(in.off[a])));
     }
     os << "template <bool I> __device__ __forceinline__ void " << name
-       << "(const mo_kparams& P, int p0, int p1, int p2, const int* vs, Real* out) {\n";
-    os << "  (void)P; (void)p0; (void)p1; (void)p2; (void)vs;\n";
+       << "(const mo_kparams& P, int p0, int p1, int p2, int eb, const int* vs, Real* out) {\n";
+    os << "  (void)P; (void)p0; (void)p1; (void)p2; (void)eb; (void)vs;\n"
+       << "  const int ms0 = P.dnd == 3 ? P.d1 * P.d2 : (P.dnd == 2 ? P.d1 : 1), ms1 = P.dnd == 3 ? P.d2 : 1;\n"
+       << "  (void)ms0; (void)ms1;\n";
     for (uint32_t r = 0; r < pg.num_regs; ++r) os << "  Real r" << r << " = (Real)0;\n";
     for (const Block& b : pg.blocks) {
       std::string ind = "  ";
@@ -128,6 +130,15 @@ struct Gen {
   }
 
   std::string reg(int r) const { return "r" + std::to_string(r); }
+
+  // Interior-tile read of a field on the iteration domain: one shared element
+  // index `eb` plus a constant stencil offset (strides ms0/ms1 are uniform).
+  static std::string ldi(int C, int sl, int o0, int o1, int o2, int ch) {
+    std::ostringstream s;
+    s << "mo_ldi<Real, " << C << ">(P.v[" << sl << "], eb + (" << o0 << ") * ms0 + (" << o1 << ") * ms1 + (" << o2
+      << "), " << ch << ")";
+    return s.str();
+  }
 
   std::string instr(const Instr& in, bool graph) {
     std::ostringstream s;
@@ -157,10 +168,10 @@ struct Gen {
         } else {
           int nd = int(f.dom.dims.size());
           const bool same = iter_dom && f.dom == *iter_dom;
-          s << "mo_ld<Real, " << (nd ? nd : 1) << ", " << f.channels << ", " << (same ? "I" : "false")
-            << ">(P.v[" << sl << "], p0 + ("
-            << in.off[0] << "), p1 + (" << in.off[1] << "), p2 + (" << in.off[2] << "), "
-            << in.channel << ")";
+          if (same) s << "(I ? " << ldi(f.channels, sl, in.off[0], in.off[1], in.off[2], in.channel) << " : ";
+          s << "mo_ld<Real, " << (nd ? nd : 1) << ", " << f.channels << ", false>(P.v[" << sl << "], p0 + ("
+            << in.off[0] << "), p1 + (" << in.off[1] << "), p2 + (" << in.off[2] << "), " << in.channel << ")";
+          if (same) s << ")";
         }
         break;
       }
@@ -195,8 +206,8 @@ struct Gen {
   }
 
   static std::string call(const std::string& pn) {
-    return "if (it) " + pn + "<true>(P, p0, p1, p2, nullptr, o); else " + pn +
-           "<false>(P, p0, p1, p2, nullptr, o);";
+    return "if (it) " + pn + "<true>(P, p0, p1, p2, mo_local_elem(P, p0, p1, p2), nullptr, o); else " + pn +
+           "<false>(P, p0, p1, p2, 0, nullptr, o);";
   }
 
   static std::string kbegin(const std::string& kname) {
@@ -381,28 +392,45 @@ struct Gen {
     const std::string pe = program(S->evalj, false, &g.dom);
     const int R = H + std::max(reach, H);
     const int NO = int(S->evalj.outputs.size());
-    const int WX = nd == 2 ? kTileX + 2 * H : kThreads + 2 * H;
+    const int WX = nd == 2 ? kTileX + 2 * H : kThreads + 2 * H;  // haloed tile (lane contributions)
     const int WY = nd == 2 ? kTileY + 2 * H : 1;
     const int NE = WX * WY;
     const int SY = nd == 2 ? WX : 1;  // shared-memory stride of axis 0
+    const int PX = WX + 2 * H;        // p staging region: tile + 2H halo
+    const int PY = nd == 2 ? WY + 2 * H : 1;
+    const int NPE = PX * PY;
+    const int PSY = nd == 2 ? PX : 1;
     const int NL = int(lanes.size());
-    const int U = int(P.unknowns.size());
+    const int NS = int(g.chans.size());  // staged p channels = this domain's columns
+    auto sidx = [&](int f, int c) {
+      for (int s = 0; s < NS; ++s)
+        if (g.chans[size_t(s)].first == f && g.chans[size_t(s)].second == c) return s;
+      return -1;
+    };
+    for (const L& l : lanes)
+      if (sidx(l.f, l.c) < 0) return tp;
     const std::string sfx = std::to_string(gi);
-    // Phase-1 body for one haloed element k at (p0, p1).
+    // Phase-1 body for one haloed element k at (p0, p1); kp = its position in
+    // the p staging region.  Lane reads of p come from shared memory.
     os << "template <bool I> __device__ __forceinline__ void mo_lanes_" << sfx
-       << "(const mo_kparams& P, int p0, int p1, int k, Real* CL) {\n"
-       << "  Real d[" << NO << "];\n  " << pe << "<I>(P, p0, p1, 0, nullptr, d);\n";
+       << "(const mo_kparams& P, int p0, int p1, int k, int kp, const Real* PT, Real* CL) {\n"
+       << "  const int eb = I ? mo_local_elem(P, p0, p1, 0) : 0;\n"
+       << "  const bool inside = I || mo_inb(P, p0, p1, 0);\n"
+       << "  Real d[" << NO << "];\n  " << pe << "<I>(P, p0, p1, 0, eb, nullptr, d);\n";
     for (size_t t = 0; t < S->jtemplates.size(); ++t) {
       os << "  { Real jp = (Real)0;\n";
       for (const L& l : lanes) {
         if (l.t != int(t)) continue;
-        const Field& f = P.unknowns[size_t(l.f)];
-        os << "    jp += d[" << l.out << "] * mo_ld<Real, " << nd << ", " << f.channels << ", I>(P.v[" << U + l.f
-           << "], p0 + (" << l.o0 << "), p1 + (" << l.o1 << "), 0, " << l.c << ");\n";
+        os << "    jp += d[" << l.out << "] * PT[" << sidx(l.f, l.c) * NPE << " + kp + (" << l.o0 * PSY + (nd == 2 ? l.o1 : 0)
+           << ")];\n";
       }
+      // An instance centred outside the domain exists only for templates that
+      // never read their own pixel (transform.hpp:177-198 shifted guard).
+      const bool origin = S->jtemplates[t].origin;
       for (int li = 0; li < NL; ++li)
         if (lanes[size_t(li)].t == int(t))
-          os << "    CL[" << li * NE << " + k] = d[" << lanes[size_t(li)].out << "] * jp;\n";
+          os << "    CL[" << li * NE << " + k] = " << (origin ? "!inside ? (Real)0 : " : "") << "d["
+             << lanes[size_t(li)].out << "] * jp;\n";
       os << "  }\n";
     }
     os << "}\n";
@@ -412,29 +440,67 @@ struct Gen {
        << "  if ((P.flags & MO_F_SKIPDONE) && P.state->done) return;\n"
        << "  extern __shared__ __align__(16) unsigned char mo_smem[];\n"
        << "  Real* CL = reinterpret_cast<Real*>(mo_smem);  // [" << NL << " lanes][" << NE << " elements]\n"
+       << "  Real* PT = CL + " << NL * NE << ";              // [" << NS << " channels][" << NPE << " staged p]\n"
        << "  double acc = 0; bool bad = false;\n"
        << "  Real* OUT = (Real*)P.out0; const Real* PV = (const Real*)P.in0; const Real* DAMP = (const Real*)P.in1;\n"
+       << "  const Real* RV = (const Real*)P.in2; const Real* MD = (const Real*)P.in3; Real* PN = (Real*)P.out2;\n"
+       << "  const bool pupd = (P.flags & MO_F_PUPD) != 0;\n"
+       << "  const Real beta = pupd ? Real(P.state->beta) : Real(0);\n"
+       << "  const int pre = P.state->use_precond;\n"
        << "  const int tid = threadIdx.x + threadIdx.y * blockDim.x;\n"
        << "  const int nt = mo_num_tiles(P);\n"
        << "  for (int t = blockIdx.x; t < nt; t += gridDim.x) {\n"
        << "    const bool it = mo_tile_interior(P, t, " << R << ");\n";
     if (nd == 2)
       os << "    const int ntx = (P.d1 + MO_TILE_X - 1) / MO_TILE_X;\n"
-         << "    const int r0 = P.row0 + (t / ntx) * MO_TILE_Y - " << H << ", c0 = (t % ntx) * MO_TILE_X - " << H
-         << ";\n"
-         << "    for (int k = tid; k < " << NE << "; k += MO_THREADS) {\n"
-         << "      const int q0 = r0 + k / " << WX << ", q1 = c0 + k % " << WX << ";\n";
+         << "    const int tr0 = P.row0 + (t / ntx) * MO_TILE_Y, tc0 = (t % ntx) * MO_TILE_X;\n";
     else
-      os << "    const int r0 = P.row0 + t * MO_THREADS - " << H << ", c0 = 0; (void)c0;\n"
-         << "    for (int k = tid; k < " << NE << "; k += MO_THREADS) {\n"
-         << "      const int q0 = r0 + k, q1 = 0;\n";
-    os << "      if (it) mo_lanes_" << sfx << "<true>(P, q0, q1, k, CL); else mo_lanes_" << sfx
-       << "<false>(P, q0, q1, k, CL);\n"
+      os << "    const int tr0 = P.row0 + t * MO_THREADS, tc0 = 0;\n";
+    // Stage p (with the fused PCG direction update) for the tile + 2H halo.
+    os << "    for (int k = tid; k < " << NPE << "; k += MO_THREADS) {\n";
+    if (nd == 2)
+      os << "      const int y = k / " << PX << ", x = k % " << PX << ";\n"
+         << "      const int q0 = tr0 - " << 2 * H << " + y, q1 = tc0 - " << 2 * H << " + x;\n"
+         << "      const bool in = (unsigned)q0 < (unsigned)P.d0 && (unsigned)q1 < (unsigned)P.d1;\n"
+         << "      const bool own = y >= " << 2 * H << " && y < " << 2 * H << " + MO_TILE_Y && x >= " << 2 * H << " && x < "
+         << 2 * H << " + MO_TILE_X && q0 < P.row1;\n";
+    else
+      os << "      const int q0 = tr0 - " << 2 * H << " + k, q1 = 0;\n"
+         << "      const bool in = (unsigned)q0 < (unsigned)P.d0;\n"
+         << "      const bool own = k >= " << 2 * H << " && k < " << 2 * H << " + MO_THREADS && q0 < P.row1;\n";
+    os << "      const long long el = in ? mo_local_elem(P, q0, q1, 0) : 0;\n";
+    for (int s = 0; s < NS; ++s) {
+      const int f = g.chans[size_t(s)].first, ch = g.chans[size_t(s)].second;
+      const int C = P.unknowns[size_t(f)].channels;
+      os << "      { Real v = (Real)0;\n"
+         << "        if (in) {\n"
+         << "          const long long col = P.ubase[" << f << "] + el * " << C << " + " << ch << ";\n"
+         << "          if (!pupd) v = PV[col];\n"
+         << "          else if (!(P.colmask && P.colmask[col])) { const Real z = pre ? RV[col] / MD[col] : RV[col]; v = z + beta * PV[col]; }\n"
+         << "          if (pupd && own) PN[col] = v;\n"
+         << "        }\n"
+         << "        PT[" << s * NPE << " + k] = v; }\n";
+    }
+    os << "    }\n    __syncthreads();\n";
+    // Phase 1: lanes for the tile + H halo.
+    os << "    for (int k = tid; k < " << NE << "; k += MO_THREADS) {\n";
+    if (nd == 2)
+      os << "      const int y = k / " << WX << ", x = k % " << WX << ";\n"
+         << "      const int q0 = tr0 - " << H << " + y, q1 = tc0 - " << H << " + x;\n"
+         << "      const int kp = (y + " << H << ") * " << PX << " + x + " << H << ";\n";
+    else
+      os << "      const int q0 = tr0 - " << H << " + k, q1 = 0;\n"
+         << "      const int kp = k + " << H << ";\n";
+    os << "      if (it) mo_lanes_" << sfx << "<true>(P, q0, q1, k, kp, PT, CL); else mo_lanes_" << sfx
+       << "<false>(P, q0, q1, k, kp, PT, CL);\n"
        << "    }\n    __syncthreads();\n"
        << "    int p0, p1, p2;\n"
        << "    if (mo_tile_coord(P, t, p0, p1, p2)) {\n"
        << "      const long long e = mo_local_elem(P, p0, p1, p2);\n"
-       << "      const int hb = (p0 - r0) * " << SY << (nd == 2 ? " + (p1 - c0)" : "") << ";\n"
+       << "      const int hb = (p0 - tr0 + " << H << ") * " << SY << (nd == 2 ? " + (p1 - tc0 + " + std::to_string(H) + ")" : "")
+       << ";\n"
+       << "      const int pb = (p0 - tr0 + " << 2 * H << ") * " << PSY
+       << (nd == 2 ? " + (p1 - tc0 + " + std::to_string(2 * H) + ")" : "") << ";\n"
        << "      const bool ex = P.mask && P.mask[e];\n";
     for (size_t k = 0; k < g.chans.size(); ++k) {
       const int f = g.chans[k].first, ch = g.chans[k].second;
@@ -448,10 +514,11 @@ struct Gen {
       os << "        Real v = ex ? (Real)0 : (Real)2 * s;\n"
          << "        if (!mo_finite((double)v)) bad = true;\n"
          << "        const long long col = P.ubase[" << f << "] + e * " << C << " + " << ch << ";\n"
-         << "        if (P.flags & MO_F_DAMP) v = v + DAMP[col] * PV[col];\n"
+         << "        const Real pv = PT[" << int(k) * NPE << " + pb];\n"
+         << "        if (P.flags & MO_F_DAMP) v = v + DAMP[col] * pv;\n"
          << "        if ((P.flags & MO_F_ZEROEXCL) && P.colmask && P.colmask[col]) v = (Real)0;\n"
          << "        OUT[col] = v;\n"
-         << "        if (P.flags & MO_F_REDUCE) acc += (double)(PV[col] * v); }\n";
+         << "        if (P.flags & MO_F_REDUCE) acc += (double)(pv * v); }\n";
     }
     os << "    }\n    __syncthreads();\n  }\n"
        << "  if (bad) atomicOr(&P.state->nonfinite_kernel, 1);\n"
@@ -460,7 +527,7 @@ struct Gen {
     tp.H = H;
     tp.reach = R;
     tp.nlanes = NL;
-    tp.smem = size_t(NL) * size_t(NE) * (f64 ? 8 : 4);
+    tp.smem = (size_t(NL) * size_t(NE) + size_t(NS) * size_t(NPE)) * (f64 ? 8 : 4);
     return tp;
   }
 
@@ -476,7 +543,7 @@ struct Gen {
           " e += (long long)gridDim.x * blockDim.x) {\n"
        << "    int vs[" << (arity ? arity : 1) << "];\n";
     for (int s = 0; s < arity; ++s) os << "    vs[" << s << "] = P.verts[e * " << arity << " + " << s << "];\n";
-    os << "    Real o[" << (nout ? nout : 1) << "];\n    " << pn << "<false>(P, 0, 0, 0, vs, o);\n";
+    os << "    Real o[" << (nout ? nout : 1) << "];\n    " << pn << "<false>(P, 0, 0, 0, 0, vs, o);\n";
     for (size_t k = 0; k < nout; ++k) {
       os << "    if (!mo_finite((double)o[" << k << "])) bad = true;\n";
       if (mode == 0) os << "    acc += (double)o[0];\n";

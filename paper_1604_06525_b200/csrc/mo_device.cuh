@@ -53,6 +53,7 @@ enum {
   MO_F_PATCH = 4,      // bm: identity patch + unconstrained (solver.hpp:241-250)
   MO_F_ZEROEXCL = 8,   // jtj: zero excluded columns        (pcg.hpp:101)
   MO_F_SKIPDONE = 16,  // return at once when the PCG has already stopped
+  MO_F_PUPD = 32,      // two-phase apply: p = z + beta p_old fused into staging (pcg.hpp:124-126)
 };
 
 // One deterministic reduction: partial slots [part_base, part_base+gridDim)
@@ -74,8 +75,11 @@ struct mo_kparams {
   int flags;
   void* out0;
   void* out1;
-  const void* in0;  // p for damp / p'Ap
+  const void* in0;  // p for damp / p'Ap (PUPD: p_old)
   const void* in1;  // damp
+  const void* in2;  // PUPD: r
+  const void* in3;  // PUPD: m (+damp) preconditioner
+  void* out2;       // PUPD: p_new
   const unsigned char* mask;     // per-element exclusion (uint8) or null
   const unsigned char* colmask;  // per-column exclusion (uint8) or null
   long long ubase[MO_MAX_UNK];   // local column base per unknown field
@@ -216,10 +220,29 @@ __device__ void mo_reduce_epilogue(const mo_red& P, double v, double v2, bool tw
   if (!am_last) return;
   __threadfence();
   double a = 0, a2 = 0;
-  const volatile double* pp = P.partials;
-  for (int i = tid; i < P.part_total; i += nt) {
-    a += pp[i];
-    if (two) a2 += pp[P.part_total + i];
+  // Fixed thread->partial assignment; loads batched 4 deep (L2, bypassing L1)
+  // so the last block's sum costs ~one L2 round trip, not one per partial.
+  int i = tid;
+  for (; i + 3 * nt < P.part_total; i += 4 * nt) {
+    const double x0 = __ldcg(P.partials + i), x1 = __ldcg(P.partials + i + nt);
+    const double x2 = __ldcg(P.partials + i + 2 * nt), x3 = __ldcg(P.partials + i + 3 * nt);
+    a += x0;
+    a += x1;
+    a += x2;
+    a += x3;
+    if (two) {
+      const double y0 = __ldcg(P.partials + P.part_total + i), y1 = __ldcg(P.partials + P.part_total + i + nt);
+      const double y2 = __ldcg(P.partials + P.part_total + i + 2 * nt);
+      const double y3 = __ldcg(P.partials + P.part_total + i + 3 * nt);
+      a2 += y0;
+      a2 += y1;
+      a2 += y2;
+      a2 += y3;
+    }
+  }
+  for (; i < P.part_total; i += nt) {
+    a += __ldcg(P.partials + i);
+    if (two) a2 += __ldcg(P.partials + P.part_total + i);
   }
   double tot = mo_block_sum(a, sh);
   double tot2 = two ? mo_block_sum(a2, sh) : 0.0;
@@ -319,6 +342,13 @@ __device__ __forceinline__ Real mo_ld(const mo_view& v, int c0, int c1, int c2, 
   int e = c0 - v.row_lo;
   if (ND >= 2) e = e * v.s1 + c1;
   if (ND >= 3) e = e * v.s2 + c2;
+  return __ldg(reinterpret_cast<const Real*>(v.p) + (long long)e * C + ch);
+}
+
+// Interior read by precomputed local element index (field on the iteration
+// domain, coordinate proven in shape).
+template <class Real, int C>
+__device__ __forceinline__ Real mo_ldi(const mo_view& v, int e, int ch) {
   return __ldg(reinterpret_cast<const Real*>(v.p) + (long long)e * C + ch);
 }
 

@@ -222,6 +222,7 @@ Plan parse_plan(const std::string& text) {
         JTemplate jt;
         jt.tmpl = int(L.integer());
         jt.guard_out = int(L.integer());
+        jt.origin = L.integer() != 0;
         long long nl = L.integer();
         for (long long l = 0; l < nl; ++l) {
           Lane ln;

@@ -103,6 +103,8 @@ struct Lane {
 };
 struct JTemplate {
   int tmpl = 0, guard_out = 0;
+  bool origin = true;  // template reads its own pixel: instances centred
+                       // outside the domain are guarded off
   std::vector<Lane> lanes;
 };
 

@@ -52,7 +52,7 @@ T* dalloc(size_t n) {
 
 int vgrid(long long n, int nsm) {
   long long g = (n + MO_THREADS - 1) / MO_THREADS;
-  long long cap = (long long)nsm * 8;
+  long long cap = (long long)nsm * 4;  // one wave at <=64 regs x 256 threads
   if (g > cap) g = cap;
   return int(std::max<long long>(g, 1));
 }
@@ -87,6 +87,7 @@ class Session final : public SessionBase {
     delta_ = dalloc<Real>(n);
     r_ = dalloc<Real>(n);
     p_ = dalloc<Real>(n);
+    p2_ = dalloc<Real>(n);
     ap_ = dalloc<Real>(n);
     vtmp_ = dalloc<Real>(n);
     otmp_ = dalloc<Real>(n);
@@ -127,7 +128,7 @@ class Session final : public SessionBase {
     cudaStreamSynchronize(st_);
     for (auto& kv : pcg_exec_) cudaGraphExecDestroy(kv.second);
     for (void* p : owned_) cudaFree(p);
-    for (Real* p : {x_, xt_, b_, m_, md_, damp_, delta_, r_, p_, ap_, vtmp_, otmp_, resid_}) cudaFree(p);
+    for (Real* p : {x_, xt_, b_, m_, md_, damp_, delta_, r_, p_, p2_, ap_, vtmp_, otmp_, resid_}) cudaFree(p);
     cudaFree(bd_);
     for (Real* p : arr_) cudaFree(p);
     for (Real* p : comp_) cudaFree(p);
@@ -226,6 +227,11 @@ class Session final : public SessionBase {
       row += r.graph ? graphs_[size_t(r.graph_idx)].E : P_.extent_of(r.dom);
     }
     rows_ = row;
+    if (rowbase_ == rowbase_dev_) {  // unchanged since the last upload
+      refreshed_ = true;
+      return;
+    }
+    rowbase_dev_ = rowbase_;
     for (size_t i = 0; i < P_.grid_sets.size(); ++i) {
       std::vector<long long> rb;
       for (int t : P_.grid_sets[i].templates) rb.push_back(rowbase_[size_t(t)]);
@@ -881,7 +887,10 @@ class Session final : public SessionBase {
 
   // out = 2 J^T J pv (+ damp pv), optionally zeroing excluded columns and
   // reducing p'Ap into alpha (flags: MO_F_DAMP | MO_F_REDUCE | MO_F_ZEROEXCL).
-  void apply(const Real* pv, Real* out, int flags) {
+  // (MO_F_PUPD: pv is p_old; the two-phase kernels stage p = z + beta p_old
+  //  from rvec/mdvec and write it to pnew.)
+  void apply(const Real* pv, Real* out, int flags, const Real* rvec = nullptr, const Real* mdvec = nullptr,
+             Real* pnew = nullptr) {
     const bool fused = P_.graph_sets.empty();
     const long long n = P_.num_cols;
     std::vector<int> grids;
@@ -897,6 +906,9 @@ class Session final : public SessionBase {
       kp.out0 = out;
       kp.in0 = pv;
       kp.in1 = damp_;
+      kp.in2 = rvec;
+      kp.in3 = mdvec;
+      kp.out2 = pnew;
       kp.flags = fused ? flags : (flags & MO_F_SKIPDONE);
       kp.red = red(base, total, MO_FIN_PCG_ALPHA, 0);
       launch_grid(jtj_kernel(i), P_.gather_sets[i].dom, kp, grids[i], jtj_smem(i));
@@ -918,6 +930,15 @@ class Session final : public SessionBase {
     }
   }
 
+  // Every column is produced by a two-phase apply kernel (no graph scatters):
+  // the PCG direction update can then be fused into the apply's p staging.
+  bool fused_pcg() const {
+    if (!P_.graph_sets.empty() || P_.gather_sets.empty()) return false;
+    for (size_t i = 0; i < P_.gather_sets.size(); ++i)
+      if (!two_phase(i)) return false;
+    return true;
+  }
+
   // Jacobi PCG (pcg.hpp:63-130) as a captured CUDA graph.
   void pcg_body(bool lm) {
     const long long n = P_.num_cols;
@@ -927,6 +948,25 @@ class Session final : public SessionBase {
     k_pcg_init<Real><<<vg, MO_THREADS, 0, st_>>>(red(0, vg, MO_FIN_PCG_INIT, 0), n, colmask_, b_, mdv, delta_, r_, p_, pre);
     ++launches_;
     const int flags = MO_F_REDUCE | MO_F_ZEROEXCL | MO_F_SKIPDONE | (lm ? MO_F_DAMP : 0);
+    if (fused_pcg()) {
+      // Two kernels per iteration: {p = z + beta p_old staged in the apply,
+      // J^T J p, p'Ap -> alpha} and {delta, r update, r'z -> beta}.  p
+      // ping-pongs between p_ and p2_ so no block overwrites a halo another
+      // block still reads.
+      Real* pb[2] = {p_, p2_};
+      for (int k = 0; k < cfg_.linear_iters; ++k) {
+        Real* pk = pb[k & 1];
+        prof_begin(0);
+        if (k == 0) apply(p_, ap_, flags);
+        else apply(pb[(k - 1) & 1], ap_, flags | MO_F_PUPD, r_, mdv, pk);
+        prof_end(0);
+        prof_begin(1);
+        k_pcg_update<Real><<<vg, MO_THREADS, 0, st_>>>(red(0, vg, MO_FIN_PCG_BETA, 0), n, colmask_, mdv, delta_, r_, pk, ap_, pre);
+        ++launches_;
+        prof_end(1);
+      }
+      return;
+    }
     for (int k = 0; k < cfg_.linear_iters; ++k) {
       prof_begin(0);
       apply(p_, ap_, flags);
@@ -1034,7 +1074,8 @@ class Session final : public SessionBase {
   cudaStream_t st_ = nullptr;
   Module mod_;
   Real *x_ = nullptr, *xt_ = nullptr, *b_ = nullptr, *m_ = nullptr, *md_ = nullptr, *damp_ = nullptr;
-  Real *delta_ = nullptr, *r_ = nullptr, *p_ = nullptr, *ap_ = nullptr, *vtmp_ = nullptr, *otmp_ = nullptr;
+  Real *delta_ = nullptr, *r_ = nullptr, *p_ = nullptr, *p2_ = nullptr, *ap_ = nullptr, *vtmp_ = nullptr,
+       *otmp_ = nullptr;
   Real* resid_ = nullptr;
   size_t resid_cap_ = 0;
   double* bd_ = nullptr;
@@ -1049,7 +1090,7 @@ class Session final : public SessionBase {
   std::vector<GraphData> graphs_;
   std::vector<GSet> gsets_;
   std::vector<long long*> grid_rowbase_;
-  std::vector<int64_t> rowbase_;
+  std::vector<int64_t> rowbase_, rowbase_dev_;
   int64_t rows_ = 0;
   int64_t unconstrained_ = 0;
   bool x_bound_ = false, params_bound_ = false, refreshed_ = false;
