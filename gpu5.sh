@@ -1,6 +1,6 @@
 timeout 900 python -m pytest tests -m gpu -q --timeout 200 2>&1 | tail -8
-timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench4.json 2> gpurun_out/bench4.err; tail -3 gpurun_out/bench4.err; cat gpurun_out/bench4.json
+timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench5.json 2> gpurun_out/bench5.err; tail -3 gpurun_out/bench5.err; cat gpurun_out/bench5.json
 for c in poisson sfs arap_mesh; do timeout 300 python bench.py --config $c --steps 3 --warmup 2 --no-cpu-baseline 2>&1 | tail -1; done
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 200 -c 300 --csv --log-file gpurun_out/launches4.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline > /dev/null 2>&1; wc -l gpurun_out/launches4.csv
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:mo_gather_jtj -s 40 -c 1 -o gpurun_out/prof_jtj4 python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu4.log 2>&1; tail -1 gpurun_out/ncu4.log
-timeout 600 ncu --set full --clock-control none -k regex:k_pcg_update -s 40 -c 1 -o gpurun_out/prof_upd4 python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu4u.log 2>&1; tail -1 gpurun_out/ncu4u.log
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 200 -c 300 --csv --log-file gpurun_out/launches5.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline > /dev/null 2>&1; wc -l gpurun_out/launches5.csv
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:mo_gather_jtj -s 40 -c 1 -o gpurun_out/prof_jtj5 python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu5.log 2>&1; tail -1 gpurun_out/ncu5.log
+timeout 600 ncu --set full --clock-control none -k regex:k_pcg_update -s 40 -c 1 -o gpurun_out/prof_upd5 python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu5u.log 2>&1; tail -1 gpurun_out/ncu5u.log

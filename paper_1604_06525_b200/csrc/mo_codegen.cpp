@@ -105,6 +105,17 @@ struct Gen {
     os << "  (void)P; (void)p0; (void)p1; (void)p2; (void)eb; (void)vs;\n"
        << "  const int ms0 = P.dnd == 3 ? P.d1 * P.d2 : (P.dnd == 2 ? P.d1 : 1), ms1 = P.dnd == 3 ? P.d2 : 1;\n"
        << "  (void)ms0; (void)ms1;\n";
+    {
+      std::vector<std::pair<int, int>> slots;
+      for (const Instr& in : pg.instrs) {
+        if (!(in.op == kLoadU || in.op == kLoadA || in.op == kLoadC || in.op == kLoadP) || in.graph) continue;
+        const Field& f = field_of(in.op, in.field);
+        if (!iter_dom || !(f.dom == *iter_dom)) continue;
+        std::pair<int, int> sc{slot_of(in.op, in.field), f.channels};
+        if (std::find(slots.begin(), slots.end(), sc) == slots.end()) slots.push_back(sc);
+      }
+      os << ldi_bases(slots);
+    }
     for (uint32_t r = 0; r < pg.num_regs; ++r) os << "  Real r" << r << " = (Real)0;\n";
     for (const Block& b : pg.blocks) {
       std::string ind = "  ";
@@ -112,7 +123,23 @@ struct Gen {
         os << "  if (r" << pg.guard_regs[b.gid] << " != (Real)0) {\n";
         ind = "    ";
       }
-      for (uint32_t i = b.begin; i < b.end; ++i) os << ind << instr(pg.instrs[i], graph) << "\n";
+      for (uint32_t i = b.begin; i < b.end; ++i) {
+        // sin(x) next to cos(x) of the same register: one sincos call shares
+        // the argument reduction (rotate2d/rotate3d emit exactly this pair).
+        const Instr& a = pg.instrs[i];
+        if (i + 1 < b.end && a.op == kUn && (a.sub == kSin || a.sub == kCos) && a.dst != a.a) {
+          const Instr& c = pg.instrs[i + 1];
+          if (c.op == kUn && c.a == a.a && (c.sub == kSin || c.sub == kCos) && c.sub != a.sub) {
+            const Instr& si = a.sub == kSin ? a : c;
+            const Instr& co = a.sub == kSin ? c : a;
+            os << ind << "{ Real s_, c_; " << (f64 ? "sincos" : "sincosf") << "(" << reg(a.a) << ", &s_, &c_); "
+               << reg(si.dst) << " = s_; " << reg(co.dst) << " = c_; }\n";
+            ++i;
+            continue;
+          }
+        }
+        os << ind << instr(a, graph) << "\n";
+      }
       if (b.gid != 0) os << "  }\n";
     }
     for (size_t o = 0; o < pg.outputs.size(); ++o) {
@@ -134,6 +161,22 @@ struct Gen {
   // Interior-tile read of a field on the iteration domain: one shared element
   // index `eb` plus a constant stencil offset (strides ms0/ms1 are uniform).
   static std::string ldi(int C, int sl, int o0, int o1, int o2, int ch) {
+    std::ostringstream s;
+    (void)C;
+    s << "__ldg(b" << sl << " + ((" << o0 << ") * ms0 + (" << o1 << ") * ms1 + (" << o2 << ")) * " << C << " + " << ch
+      << ")";
+    return s.str();
+  }
+  // Per-field interior base pointers (field start + eb*C): each stencil load
+  // is then base + (row offset) + immediate.
+  static std::string ldi_bases(const std::vector<std::pair<int, int>>& slots) {
+    std::ostringstream s;
+    for (auto [sl, C] : slots)
+      s << "  const Real* __restrict__ b" << sl << " = I ? reinterpret_cast<const Real*>(P.v[" << sl
+        << "].p) + (long long)eb * " << C << " : nullptr; (void)b" << sl << ";\n";
+    return s.str();
+  }
+  static std::string ldi_unused(int C, int sl, int o0, int o1, int o2, int ch) {
     std::ostringstream s;
     s << "mo_ldi<Real, " << C << ">(P.v[" << sl << "], eb + (" << o0 << ") * ms0 + (" << o1 << ") * ms1 + (" << o2
       << "), " << ch << ")";
@@ -221,9 +264,10 @@ struct Gen {
        << "  double acc = 0; bool bad = false;\n"
           "  const int nt = mo_num_tiles(P);\n"
           "  for (int t = blockIdx.x; t < nt; t += gridDim.x) {\n"
-       << "    const bool it = mo_tile_interior(P, t, " << reach << ");\n"
+       << "    const mo_tile T = mo_tile_at(P, t);\n"
+       << "    const bool it = mo_tile_in(P, T, " << reach << ");\n"
           "    int p0, p1, p2;\n"
-          "    if (mo_tile_coord(P, t, p0, p1, p2)) {\n"
+          "    if (mo_tile_elem(P, T, p0, p1, p2)) {\n"
           "      Real o[1];\n      "
        << call(pn) << "\n"
           "      if (!mo_finite((double)o[0])) bad = true;\n"
@@ -239,9 +283,10 @@ struct Gen {
     os << kbegin(kn) << "  bool bad = false;\n"
        << "  const int nt = mo_num_tiles(P);\n"
           "  for (int t = blockIdx.x; t < nt; t += gridDim.x) {\n"
-       << "    const bool it = mo_tile_interior(P, t, " << reach << ");\n"
+       << "    const mo_tile T = mo_tile_at(P, t);\n"
+       << "    const bool it = mo_tile_in(P, T, " << reach << ");\n"
           "    int p0, p1, p2;\n"
-          "    if (mo_tile_coord(P, t, p0, p1, p2)) {\n"
+          "    if (mo_tile_elem(P, T, p0, p1, p2)) {\n"
           "      const int e = mo_local_elem(P, p0, p1, p2);\n"
           "      Real o["
        << (nout ? nout : 1) << "];\n      " << call(pn) << "\n";
@@ -256,9 +301,10 @@ struct Gen {
     os << kbegin(kn) << "  bool bad = false;\n"
        << "  const int nt = mo_num_tiles(P);\n"
           "  for (int t = blockIdx.x; t < nt; t += gridDim.x) {\n"
-       << "    const bool it = mo_tile_interior(P, t, " << reach << ");\n"
+       << "    const mo_tile T = mo_tile_at(P, t);\n"
+       << "    const bool it = mo_tile_in(P, T, " << reach << ");\n"
           "    int p0, p1, p2;\n"
-          "    if (mo_tile_coord(P, t, p0, p1, p2)) {\n"
+          "    if (mo_tile_elem(P, T, p0, p1, p2)) {\n"
           "      const long long e = mo_local_elem(P, p0, p1, p2);\n"
           "      Real o["
        << (nout ? nout : 1) << "];\n      " << call(pn) << "\n";
@@ -272,9 +318,10 @@ struct Gen {
     os << kbegin(kn)
        << "  const int nt = mo_num_tiles(P);\n"
           "  for (int t = blockIdx.x; t < nt; t += gridDim.x) {\n"
-       << "    const bool it = mo_tile_interior(P, t, " << reach << ");\n"
+       << "    const mo_tile T = mo_tile_at(P, t);\n"
+       << "    const bool it = mo_tile_in(P, T, " << reach << ");\n"
           "    int p0, p1, p2;\n"
-          "    if (mo_tile_coord(P, t, p0, p1, p2)) {\n"
+          "    if (mo_tile_elem(P, T, p0, p1, p2)) {\n"
           "      const int e = mo_local_elem(P, p0, p1, p2);\n"
           "      Real o[1];\n      "
        << call(pn) << "\n"
@@ -289,9 +336,10 @@ struct Gen {
        << "  Real* B = (Real*)P.out0; Real* M = (Real*)P.out1;\n"
           "  const int nt = mo_num_tiles(P);\n"
           "  for (int t = blockIdx.x; t < nt; t += gridDim.x) {\n"
-       << "    const bool it = mo_tile_interior(P, t, " << reach << ");\n"
+       << "    const mo_tile T = mo_tile_at(P, t);\n"
+       << "    const bool it = mo_tile_in(P, T, " << reach << ");\n"
           "    int p0, p1, p2;\n"
-          "    if (mo_tile_coord(P, t, p0, p1, p2)) {\n"
+          "    if (mo_tile_elem(P, T, p0, p1, p2)) {\n"
           "      const long long e = mo_local_elem(P, p0, p1, p2);\n"
           "      Real o["
        << (K ? 2 * K : 1)
@@ -326,9 +374,10 @@ struct Gen {
        << "  Real* OUT = (Real*)P.out0; const Real* PV = (const Real*)P.in0; const Real* DAMP = (const Real*)P.in1;\n"
           "  const int nt = mo_num_tiles(P);\n"
           "  for (int t = blockIdx.x; t < nt; t += gridDim.x) {\n"
-       << "    const bool it = mo_tile_interior(P, t, " << reach << ");\n"
+       << "    const mo_tile T = mo_tile_at(P, t);\n"
+       << "    const bool it = mo_tile_in(P, T, " << reach << ");\n"
           "    int p0, p1, p2;\n"
-          "    if (mo_tile_coord(P, t, p0, p1, p2)) {\n"
+          "    if (mo_tile_elem(P, T, p0, p1, p2)) {\n"
           "      const long long e = mo_local_elem(P, p0, p1, p2);\n"
           "      Real o["
        << (K ? K : 1)
@@ -392,133 +441,113 @@ struct Gen {
     const std::string pe = program(S->evalj, false, &g.dom);
     const int R = H + std::max(reach, H);
     const int NO = int(S->evalj.outputs.size());
-    const int WX = nd == 2 ? kTileX + 2 * H : kThreads + 2 * H;  // haloed tile (lane contributions)
+    const int WX = nd == 2 ? kTileX + 2 * H : kThreads + 2 * H;
     const int WY = nd == 2 ? kTileY + 2 * H : 1;
     const int NE = WX * WY;
     const int SY = nd == 2 ? WX : 1;  // shared-memory stride of axis 0
-    const int PX = WX + 2 * H;        // p staging region: tile + 2H halo
-    const int PY = nd == 2 ? WY + 2 * H : 1;
-    const int NPE = PX * PY;
-    const int PSY = nd == 2 ? PX : 1;
-    const int NL = int(lanes.size());
-    const int NS = int(g.chans.size());  // staged p channels = this domain's columns
-    auto sidx = [&](int f, int c) {
-      for (int s = 0; s < NS; ++s)
-        if (g.chans[size_t(s)].first == f && g.chans[size_t(s)].second == c) return s;
-      return -1;
+    const int U = int(P.unknowns.size());
+    // Merge lanes that land on the same (field, channel, offset): phase 1
+    // pre-sums their contributions, phase 2 gathers one value per offset.
+    struct M {
+      int f, c, o0, o1;
     };
-    for (const L& l : lanes)
-      if (sidx(l.f, l.c) < 0) return tp;
+    std::vector<M> merged;
+    std::vector<int> lane_slot(lanes.size());
+    for (size_t li = 0; li < lanes.size(); ++li) {
+      const L& l = lanes[li];
+      int s = -1;
+      for (size_t k = 0; k < merged.size(); ++k)
+        if (merged[k].f == l.f && merged[k].c == l.c && merged[k].o0 == l.o0 && merged[k].o1 == l.o1) s = int(k);
+      if (s < 0) {
+        s = int(merged.size());
+        merged.push_back({l.f, l.c, l.o0, l.o1});
+      }
+      lane_slot[li] = s;
+    }
+    const int NM = int(merged.size());
     const std::string sfx = std::to_string(gi);
-    // Phase-1 body for one haloed element k at (p0, p1); kp = its position in
-    // the p staging region.  Lane reads of p come from shared memory.
+    // Phase-1 body for one haloed element k at (p0, p1).
     os << "template <bool I> __device__ __forceinline__ void mo_lanes_" << sfx
-       << "(const mo_kparams& P, int p0, int p1, int k, int kp, const Real* PT, Real* CL) {\n"
+       << "(const mo_kparams& P, int p0, int p1, int k, Real* CL) {\n"
+       << "  const int ms0 = P.dnd == 2 ? P.d1 : 1, ms1 = 1; (void)ms1;\n"
        << "  const int eb = I ? mo_local_elem(P, p0, p1, 0) : 0;\n"
-       << "  const bool inside = I || mo_inb(P, p0, p1, 0);\n"
-       << "  Real d[" << NO << "];\n  " << pe << "<I>(P, p0, p1, 0, eb, nullptr, d);\n";
+       << "  const bool inside = I || mo_inb(P, p0, p1, 0);\n";
+    {
+      std::vector<std::pair<int, int>> slots;
+      for (const L& l : lanes) {
+        std::pair<int, int> sc{U + l.f, P.unknowns[size_t(l.f)].channels};
+        if (std::find(slots.begin(), slots.end(), sc) == slots.end()) slots.push_back(sc);
+      }
+      os << ldi_bases(slots);
+    }
+    os << "  Real d[" << NO << "];\n  " << pe << "<I>(P, p0, p1, 0, eb, nullptr, d);\n";
+    for (int s = 0; s < NM; ++s) os << "  Real m" << s << " = (Real)0;\n";
     for (size_t t = 0; t < S->jtemplates.size(); ++t) {
       os << "  { Real jp = (Real)0;\n";
       for (const L& l : lanes) {
         if (l.t != int(t)) continue;
-        os << "    jp += d[" << l.out << "] * PT[" << sidx(l.f, l.c) * NPE << " + kp + (" << l.o0 * PSY + (nd == 2 ? l.o1 : 0)
-           << ")];\n";
+        const Field& f = P.unknowns[size_t(l.f)];
+        os << "    jp += d[" << l.out << "] * (I ? " << ldi(f.channels, U + l.f, l.o0, l.o1, 0, l.c) << " : mo_ld<Real, "
+           << nd << ", " << f.channels << ", false>(P.v[" << U + l.f << "], p0 + (" << l.o0 << "), p1 + (" << l.o1
+           << "), 0, " << l.c << "));\n";
       }
       // An instance centred outside the domain exists only for templates that
       // never read their own pixel (transform.hpp:177-198 shifted guard).
       const bool origin = S->jtemplates[t].origin;
-      for (int li = 0; li < NL; ++li)
-        if (lanes[size_t(li)].t == int(t))
-          os << "    CL[" << li * NE << " + k] = " << (origin ? "!inside ? (Real)0 : " : "") << "d["
-             << lanes[size_t(li)].out << "] * jp;\n";
+      if (origin) os << "    if (inside) {\n";
+      for (size_t li = 0; li < lanes.size(); ++li)
+        if (lanes[li].t == int(t)) os << "    m" << lane_slot[li] << " += d[" << lanes[li].out << "] * jp;\n";
+      if (origin) os << "    }\n";
       os << "  }\n";
     }
+    for (int s = 0; s < NM; ++s) os << "  CL[" << s * NE << " + k] = m" << s << ";\n";
     os << "}\n";
     const std::string kn = "mo_gather_jtj2_" + sfx;
     os << "extern \"C\" __global__ void __launch_bounds__(MO_THREADS) " << kn
        << "(const __grid_constant__ mo_kparams P) {\n"
        << "  if ((P.flags & MO_F_SKIPDONE) && P.state->done) return;\n"
        << "  extern __shared__ __align__(16) unsigned char mo_smem[];\n"
-       << "  Real* CL = reinterpret_cast<Real*>(mo_smem);  // [" << NL << " lanes][" << NE << " elements]\n"
-       << "  Real* PT = CL + " << NL * NE << ";              // [" << NS << " channels][" << NPE << " staged p]\n"
+       << "  Real* CL = reinterpret_cast<Real*>(mo_smem);  // [" << NM << " merged lanes][" << NE << " elements]\n"
        << "  double acc = 0; bool bad = false;\n"
        << "  Real* OUT = (Real*)P.out0; const Real* PV = (const Real*)P.in0; const Real* DAMP = (const Real*)P.in1;\n"
-       << "  const Real* RV = (const Real*)P.in2; const Real* MD = (const Real*)P.in3; Real* PN = (Real*)P.out2;\n"
-       << "  const bool pupd = (P.flags & MO_F_PUPD) != 0;\n"
-       << "  const Real beta = pupd ? Real(P.state->beta) : Real(0);\n"
-       << "  const int pre = P.state->use_precond;\n"
        << "  const int tid = threadIdx.x + threadIdx.y * blockDim.x;\n"
        << "  const int nt = mo_num_tiles(P);\n"
        << "  for (int t = blockIdx.x; t < nt; t += gridDim.x) {\n"
-       << "    const bool it = mo_tile_interior(P, t, " << R << ");\n";
+       << "    const mo_tile T = mo_tile_at(P, t);\n"
+       << "    const bool it = mo_tile_in(P, T, " << R << ");\n";
     if (nd == 2)
-      os << "    const int ntx = (P.d1 + MO_TILE_X - 1) / MO_TILE_X;\n"
-         << "    const int tr0 = P.row0 + (t / ntx) * MO_TILE_Y, tc0 = (t % ntx) * MO_TILE_X;\n";
+      os << "    const int r0 = T.o0 - " << H << ", c0 = T.o1 - " << H
+         << ";\n"
+         << "    for (int k = tid; k < " << NE << "; k += MO_THREADS) {\n"
+         << "      const int q0 = r0 + k / " << WX << ", q1 = c0 + k % " << WX << ";\n";
     else
-      os << "    const int tr0 = P.row0 + t * MO_THREADS, tc0 = 0;\n";
-    // Stage p (with the fused PCG direction update) for the tile + 2H halo.
-    os << "    for (int k = tid; k < " << NPE << "; k += MO_THREADS) {\n";
-    if (nd == 2)
-      os << "      const int y = k / " << PX << ", x = k % " << PX << ";\n"
-         << "      const int q0 = tr0 - " << 2 * H << " + y, q1 = tc0 - " << 2 * H << " + x;\n"
-         << "      const bool in = (unsigned)q0 < (unsigned)P.d0 && (unsigned)q1 < (unsigned)P.d1;\n"
-         << "      const bool own = y >= " << 2 * H << " && y < " << 2 * H << " + MO_TILE_Y && x >= " << 2 * H << " && x < "
-         << 2 * H << " + MO_TILE_X && q0 < P.row1;\n";
-    else
-      os << "      const int q0 = tr0 - " << 2 * H << " + k, q1 = 0;\n"
-         << "      const bool in = (unsigned)q0 < (unsigned)P.d0;\n"
-         << "      const bool own = k >= " << 2 * H << " && k < " << 2 * H << " + MO_THREADS && q0 < P.row1;\n";
-    os << "      const long long el = in ? mo_local_elem(P, q0, q1, 0) : 0;\n";
-    for (int s = 0; s < NS; ++s) {
-      const int f = g.chans[size_t(s)].first, ch = g.chans[size_t(s)].second;
-      const int C = P.unknowns[size_t(f)].channels;
-      os << "      { Real v = (Real)0;\n"
-         << "        if (in) {\n"
-         << "          const long long col = P.ubase[" << f << "] + el * " << C << " + " << ch << ";\n"
-         << "          if (!pupd) v = PV[col];\n"
-         << "          else if (!(P.colmask && P.colmask[col])) { const Real z = pre ? RV[col] / MD[col] : RV[col]; v = z + beta * PV[col]; }\n"
-         << "          if (pupd && own) PN[col] = v;\n"
-         << "        }\n"
-         << "        PT[" << s * NPE << " + k] = v; }\n";
-    }
-    os << "    }\n    __syncthreads();\n";
-    // Phase 1: lanes for the tile + H halo.
-    os << "    for (int k = tid; k < " << NE << "; k += MO_THREADS) {\n";
-    if (nd == 2)
-      os << "      const int y = k / " << WX << ", x = k % " << WX << ";\n"
-         << "      const int q0 = tr0 - " << H << " + y, q1 = tc0 - " << H << " + x;\n"
-         << "      const int kp = (y + " << H << ") * " << PX << " + x + " << H << ";\n";
-    else
-      os << "      const int q0 = tr0 - " << H << " + k, q1 = 0;\n"
-         << "      const int kp = k + " << H << ";\n";
-    os << "      if (it) mo_lanes_" << sfx << "<true>(P, q0, q1, k, kp, PT, CL); else mo_lanes_" << sfx
-       << "<false>(P, q0, q1, k, kp, PT, CL);\n"
+      os << "    const int r0 = T.o0 - " << H << ", c0 = 0; (void)c0;\n"
+         << "    for (int k = tid; k < " << NE << "; k += MO_THREADS) {\n"
+         << "      const int q0 = r0 + k, q1 = 0;\n";
+    os << "      if (it) mo_lanes_" << sfx << "<true>(P, q0, q1, k, CL); else mo_lanes_" << sfx
+       << "<false>(P, q0, q1, k, CL);\n"
        << "    }\n    __syncthreads();\n"
        << "    int p0, p1, p2;\n"
-       << "    if (mo_tile_coord(P, t, p0, p1, p2)) {\n"
+       << "    if (mo_tile_elem(P, T, p0, p1, p2)) {\n"
        << "      const long long e = mo_local_elem(P, p0, p1, p2);\n"
-       << "      const int hb = (p0 - tr0 + " << H << ") * " << SY << (nd == 2 ? " + (p1 - tc0 + " + std::to_string(H) + ")" : "")
-       << ";\n"
-       << "      const int pb = (p0 - tr0 + " << 2 * H << ") * " << PSY
-       << (nd == 2 ? " + (p1 - tc0 + " + std::to_string(2 * H) + ")" : "") << ";\n"
+       << "      const int hb = (p0 - r0) * " << SY << (nd == 2 ? " + (p1 - c0)" : "") << ";\n"
        << "      const bool ex = P.mask && P.mask[e];\n";
     for (size_t k = 0; k < g.chans.size(); ++k) {
       const int f = g.chans[k].first, ch = g.chans[k].second;
       const int C = P.unknowns[size_t(f)].channels;
       os << "      { Real s = (Real)0;\n";
-      for (int li = 0; li < NL; ++li) {
-        const L& l = lanes[size_t(li)];
-        if (l.f != f || l.c != ch) continue;
-        os << "        s += CL[" << li * NE << " + hb - (" << l.o0 * SY + (nd == 2 ? l.o1 : 0) << ")];\n";
+      for (int s = 0; s < NM; ++s) {
+        const M& m = merged[size_t(s)];
+        if (m.f != f || m.c != ch) continue;
+        os << "        s += CL[" << s * NE << " + hb - (" << m.o0 * SY + (nd == 2 ? m.o1 : 0) << ")];\n";
       }
       os << "        Real v = ex ? (Real)0 : (Real)2 * s;\n"
          << "        if (!mo_finite((double)v)) bad = true;\n"
          << "        const long long col = P.ubase[" << f << "] + e * " << C << " + " << ch << ";\n"
-         << "        const Real pv = PT[" << int(k) * NPE << " + pb];\n"
-         << "        if (P.flags & MO_F_DAMP) v = v + DAMP[col] * pv;\n"
+         << "        if (P.flags & MO_F_DAMP) v = v + DAMP[col] * PV[col];\n"
          << "        if ((P.flags & MO_F_ZEROEXCL) && P.colmask && P.colmask[col]) v = (Real)0;\n"
          << "        OUT[col] = v;\n"
-         << "        if (P.flags & MO_F_REDUCE) acc += (double)(pv * v); }\n";
+         << "        if (P.flags & MO_F_REDUCE) acc += (double)(PV[col] * v); }\n";
     }
     os << "    }\n    __syncthreads();\n  }\n"
        << "  if (bad) atomicOr(&P.state->nonfinite_kernel, 1);\n"
@@ -526,8 +555,8 @@ struct Gen {
     tp.ok = true;
     tp.H = H;
     tp.reach = R;
-    tp.nlanes = NL;
-    tp.smem = (size_t(NL) * size_t(NE) + size_t(NS) * size_t(NPE)) * (f64 ? 8 : 4);
+    tp.nlanes = NM;
+    tp.smem = size_t(NM) * size_t(NE) * (f64 ? 8 : 4);
     return tp;
   }
 

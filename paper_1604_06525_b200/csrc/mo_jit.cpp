@@ -81,7 +81,15 @@ std::vector<char> compile_cubin(const std::string& src, const std::string& name,
     }
   }
   nvrtcProgram prog;
-  check(nvrtcCreateProgram(&prog, src.c_str(), name.c_str(), 0, nullptr, nullptr) == NVRTC_SUCCESS,
+  // The generated source is kept beside its cubin and named by that path so
+  // -lineinfo maps SASS back to it (ncu --import-source, compute-sanitizer).
+  std::string srcname = name;
+  if (!std::getenv("MO_B200_NOCACHE")) {
+    mkdirs(dir);
+    srcname = dir + "/" + hex + ".cu";
+    std::ofstream(srcname) << src;
+  }
+  check(nvrtcCreateProgram(&prog, src.c_str(), srcname.c_str(), 0, nullptr, nullptr) == NVRTC_SUCCESS,
         Err::kInternal, "nvrtcCreateProgram failed");
   nvrtcResult r = nvrtcCompileProgram(prog, int(opts.size()), opts.data());
   size_t logsz = 0;

@@ -200,9 +200,9 @@ k_lm_base_diag(long long n, const Real* __restrict__ m, double* __restrict__ bd,
 // LM: damp = excluded ? 0 : 2/mu * base_diag; md = m + damp (solver.hpp:433-438).
 template <class Real>
 __global__ void __launch_bounds__(MO_THREADS)
-k_lm_damp(long long n, const unsigned char* cm, const Real* __restrict__ m, const double* __restrict__ bd,
-          Real* __restrict__ damp, Real* __restrict__ md, double mu) {
-  const double s = 2.0 / mu;
+k_lm_damp(const mo_state* st, long long n, const unsigned char* cm, const Real* __restrict__ m,
+          const double* __restrict__ bd, Real* __restrict__ damp, Real* __restrict__ md) {
+  const double s = 2.0 / st->mu;  // mu staged by the host before each trial
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     const Real d = ex_at(cm, i) ? Real(0) : Real(s * bd[i]);

@@ -87,7 +87,6 @@ class Session final : public SessionBase {
     delta_ = dalloc<Real>(n);
     r_ = dalloc<Real>(n);
     p_ = dalloc<Real>(n);
-    p2_ = dalloc<Real>(n);
     ap_ = dalloc<Real>(n);
     vtmp_ = dalloc<Real>(n);
     otmp_ = dalloc<Real>(n);
@@ -108,6 +107,7 @@ class Session final : public SessionBase {
     params_d_ = dalloc<double>(std::max<size_t>(P_.params.size(), 1));
     state_ = dalloc<mo_state>(1);
     CK(cudaMallocHost(&state_h_, sizeof(mo_state)));
+    CK(cudaMallocHost(&mu_h_, sizeof(double)));
     std::memset(state_h_, 0, sizeof(mo_state));
     state_h_->tol_rel = cfg_.pcg_rel_tol;
     state_h_->tol_abs = cfg_.pcg_abs_tol;
@@ -126,9 +126,9 @@ class Session final : public SessionBase {
   ~Session() override {
     cudaSetDevice(dev_);
     cudaStreamSynchronize(st_);
-    for (auto& kv : pcg_exec_) cudaGraphExecDestroy(kv.second);
+    for (auto& kv : stage_exec_) cudaGraphExecDestroy(kv.second);
     for (void* p : owned_) cudaFree(p);
-    for (Real* p : {x_, xt_, b_, m_, md_, damp_, delta_, r_, p_, p2_, ap_, vtmp_, otmp_, resid_}) cudaFree(p);
+    for (Real* p : {x_, xt_, b_, m_, md_, damp_, delta_, r_, p_, ap_, vtmp_, otmp_, resid_}) cudaFree(p);
     cudaFree(bd_);
     for (Real* p : arr_) cudaFree(p);
     for (Real* p : comp_) cudaFree(p);
@@ -149,12 +149,12 @@ class Session final : public SessionBase {
         cudaFree(d.outs_jtj);
       }
     }
-    for (auto& pe : prof_) {
-      for (auto& ev : pe.ev) {
-        cudaEventDestroy(ev.first);
-        cudaEventDestroy(ev.second);
+    for (auto& kv : stage_ev_)
+      for (auto& ev : kv.second) {
+        cudaEventDestroy(ev.a);
+        cudaEventDestroy(ev.b);
       }
-    }
+    cudaFreeHost(mu_h_);
     cudaStreamDestroy(st_);
   }
 
@@ -192,10 +192,16 @@ class Session final : public SessionBase {
   }
 
   // refresh(): solver.hpp:125-168
+  // refresh(): solver.hpp:125-168.  Host half (bind validation, graph upload,
+  // residual rows) + device half (computed arrays, masks), the latter
+  // captured into the per-iteration CUDA graphs.
   void refresh() override {
-    CK(cudaSetDevice(dev_));
-    validate();
-    upload_graphs();
+    refresh_host();
+    refresh_device();
+    refreshed_ = true;
+  }
+
+  void refresh_device() {
     for (const ComputedKernel& ck : P_.computed_kernels) {
       mo_kparams kp = kp_grid(ck.dom, x_, nullptr);
       kp.out0 = comp_[size_t(ck.index)];
@@ -218,6 +224,12 @@ class Session final : public SessionBase {
           ++launches_;
         }
     }
+  }
+
+  void refresh_host() {
+    CK(cudaSetDevice(dev_));
+    validate();
+    upload_graphs();
     // Residual row offsets (graph sizes may change through callbacks).
     rowbase_.assign(P_.residuals.size(), 0);
     int64_t row = 0;
@@ -297,6 +309,7 @@ class Session final : public SessionBase {
 
   void build_normal() override {
     ensure_refreshed();
+    cur_stage_ = -1;
     normal_device();
     sync_state();
     unconstrained_ = state_h_->unconstrained;
@@ -328,6 +341,8 @@ class Session final : public SessionBase {
     using clock = std::chrono::steady_clock;
     CK(cudaSetDevice(dev_));
     const bool lm = cfg_.method == 1;
+    const long long n = P_.num_cols;
+    const int vg = vgrid(n, nsm_);
     SolveResult res;
     double mu = cfg_.lm_radius0, nu = 2.0;
     auto t_prev = clock::now();
@@ -344,73 +359,100 @@ class Session final : public SessionBase {
     };
 
     for (int it = 0; it < cfg_.nonlinear_iters; ++it) {
-      refresh();
-      cost_at(x_, SLOT_COST);
-      sync_state();
-      const double cost_old = state_h_->sums[SLOT_COST];
-      if (!std::isfinite(cost_old)) {
-        res.trace.push_back({it, cost_old, false, lm ? mu : 0.0, 0, take_ms()});
-        res.reason = 3;
-        res.final_cost = cost_old;
-        finish();
-        return res;
-      }
-      normal_device();
-      if (lm) {
-        long long n = P_.num_cols;
-        k_lm_base_diag<Real><<<vgrid(n, nsm_), MO_THREADS, 0, st_>>>(n, m_, bd_, cfg_.lm_diag_min, cfg_.lm_diag_max);
-        ++launches_;
-      }
-      double cost_after = cost_old;
-      bool stepped = false;
-      while (!stepped) {
-        const long long n = P_.num_cols;
-        if (lm) {
-          k_lm_damp<Real><<<vgrid(n, nsm_), MO_THREADS, 0, st_>>>(n, colmask_, m_, bd_, damp_, md_, mu);
-          ++launches_;
-        }
-        run_pcg(lm);
-        CK(cudaMemsetAsync(&state_->any_nonzero, 0, sizeof(int), st_));
-        if (lm) {
-          k_xtrial<Real><<<vgrid(n, nsm_), MO_THREADS, 0, st_>>>(state_, n, colmask_, x_, delta_, xt_, 0, SLOT_COST);
-          ++launches_;
-          cost_at(xt_, SLOT_COST + 1);
-          apply(delta_, ap_, 0);  // undamped model curvature (solver.hpp:467)
-          mo_red R = red(0, vgrid(n, nsm_), MO_FIN_STORE2, SLOT_PRED);
-          k_lm_predicted<Real><<<vgrid(n, nsm_), MO_THREADS, 0, st_>>>(R, n, b_, delta_, ap_);
-          ++launches_;
-        } else {
-          // GN: the step is unconditional (solver.hpp:452); committed in place
-          // unless cost_old or the PCG recurrence went non-finite.
-          k_xtrial<Real><<<vgrid(n, nsm_), MO_THREADS, 0, st_>>>(state_, n, colmask_, x_, delta_, xt_, 1, SLOT_COST);
+      refresh_host();
+      if (!lm) {
+        // One GN iteration = one graph, one host sync (solver.hpp:415-464).
+        // build_normal/PCG/step run even when cost_old turns out non-finite;
+        // the step kernel then leaves x untouched and the host stops exactly
+        // where the reference would.
+        run_stage(kStageGN, [&] {
+          refresh_device();
+          cost_at(x_, SLOT_COST);
+          normal_device();
+          pcg_body(false);
+          CK(cudaMemsetAsync(&state_->any_nonzero, 0, sizeof(int), st_));
+          k_xtrial<Real><<<vg, MO_THREADS, 0, st_>>>(state_, n, colmask_, x_, delta_, xt_, 1, SLOT_COST);
           ++launches_;
           cost_at(x_, SLOT_COST + 1);
-        }
+        });
         sync_state();
-        collect_profile();
+        collect_profile(kStageGN);
         const mo_state S = *state_h_;
+        const double cost_old = S.sums[SLOT_COST];
+        if (!std::isfinite(cost_old)) {
+          res.trace.push_back({it, cost_old, false, 0.0, 0, take_ms()});
+          res.reason = 3;
+          res.final_cost = cost_old;
+          finish();
+          return res;
+        }
         unconstrained_ = S.unconstrained;
         res.indefinite_operator |= S.indefinite != 0;
-        if (S.nonfinite && !lm) {
+        if (S.nonfinite) {
           res.reason = 3;
           res.final_cost = cost_old;
           res.trace.push_back({it, cost_old, false, 0.0, S.iters, take_ms()});
           finish();
           return res;
         }
-        const double cost_new = S.nonfinite ? std::numeric_limits<double>::infinity() : S.sums[SLOT_COST + 1];
-        if (!lm) {
-          res.trace.push_back({it, cost_new, true, 0.0, S.iters, take_ms()});
-          if (!std::isfinite(cost_new)) {
-            res.reason = 3;
-            res.final_cost = cost_new;
-            finish();
-            return res;
-          }
-          cost_after = cost_new;
-          stepped = true;
+        const double cost_new = S.sums[SLOT_COST + 1];
+        res.trace.push_back({it, cost_new, true, 0.0, S.iters, take_ms()});
+        if (!std::isfinite(cost_new)) {
+          res.reason = 3;
+          res.final_cost = cost_new;
+          finish();
+          return res;
+        }
+        if (cb) cb(it, user);
+        double rel = (cost_old - cost_new) / std::max(cost_old, 1e-300);
+        if (rel >= 0 && rel < cfg_.cost_stop_tol) {
+          res.reason = 1;
           break;
         }
+        continue;
+      }
+
+      // LM (solver.hpp:427-501): linearise once, then damped trials.
+      run_stage(kStageLMLin, [&] {
+        refresh_device();
+        cost_at(x_, SLOT_COST);
+        normal_device();
+        k_lm_base_diag<Real><<<vg, MO_THREADS, 0, st_>>>(n, m_, bd_, cfg_.lm_diag_min, cfg_.lm_diag_max);
+        ++launches_;
+      });
+      sync_state();
+      collect_profile(kStageLMLin);
+      const double cost_old = state_h_->sums[SLOT_COST];
+      if (!std::isfinite(cost_old)) {
+        res.trace.push_back({it, cost_old, false, mu, 0, take_ms()});
+        res.reason = 3;
+        res.final_cost = cost_old;
+        finish();
+        return res;
+      }
+      unconstrained_ = state_h_->unconstrained;
+      double cost_after = cost_old;
+      bool stepped = false;
+      while (!stepped) {
+        *mu_h_ = mu;
+        CK(cudaMemcpyAsync(&state_->mu, mu_h_, sizeof(double), cudaMemcpyHostToDevice, st_));
+        run_stage(kStageLMTrial, [&] {
+          k_lm_damp<Real><<<vg, MO_THREADS, 0, st_>>>(state_, n, colmask_, m_, bd_, damp_, md_);
+          ++launches_;
+          pcg_body(true);
+          CK(cudaMemsetAsync(&state_->any_nonzero, 0, sizeof(int), st_));
+          k_xtrial<Real><<<vg, MO_THREADS, 0, st_>>>(state_, n, colmask_, x_, delta_, xt_, 0, SLOT_COST);
+          ++launches_;
+          cost_at(xt_, SLOT_COST + 1);
+          apply(delta_, ap_, 0);  // undamped model curvature (solver.hpp:467)
+          k_lm_predicted<Real><<<vg, MO_THREADS, 0, st_>>>(red(0, vg, MO_FIN_STORE2, SLOT_PRED), n, b_, delta_, ap_);
+          ++launches_;
+        });
+        sync_state();
+        collect_profile(kStageLMTrial);
+        const mo_state S = *state_h_;
+        res.indefinite_operator |= S.indefinite != 0;
+        const double cost_new = S.nonfinite ? std::numeric_limits<double>::infinity() : S.sums[SLOT_COST + 1];
         double predicted = 0.0 - S.sums[SLOT_PRED + 1];
         predicted += S.sums[SLOT_PRED];
         double rho = predicted > 0 ? (cost_old - cost_new) / predicted : -1.0;
@@ -499,11 +541,14 @@ class Session final : public SessionBase {
     std::vector<int64_t> slot_bound;
   };
   struct Prof {
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
-    size_t used = 0;
     double total_ms = 0;
     int64_t count = 0;
   };
+  struct ProfEv {
+    int kind = 0;
+    cudaEvent_t a = nullptr, b = nullptr;
+  };
+  enum { kStageGN = 0, kStageLMLin = 1, kStageLMTrial = 2 };
 
   int64_t array_size(int i) const {
     return P_.extent_of(P_.arrays[size_t(i)].dom) * P_.arrays[size_t(i)].channels;
@@ -676,8 +721,8 @@ class Session final : public SessionBase {
   }
 
   void invalidate_graphs() {
-    for (auto& kv : pcg_exec_) cudaGraphExecDestroy(kv.second);
-    pcg_exec_.clear();
+    for (auto& kv : stage_exec_) cudaGraphExecDestroy(kv.second);
+    stage_exec_.clear();
   }
 
   // ------------------------------------------------------------ launches
@@ -930,16 +975,9 @@ class Session final : public SessionBase {
     }
   }
 
-  // Every column is produced by a two-phase apply kernel (no graph scatters):
-  // the PCG direction update can then be fused into the apply's p staging.
-  bool fused_pcg() const {
-    if (!P_.graph_sets.empty() || P_.gather_sets.empty()) return false;
-    for (size_t i = 0; i < P_.gather_sets.size(); ++i)
-      if (!two_phase(i)) return false;
-    return true;
-  }
-
-  // Jacobi PCG (pcg.hpp:63-130) as a captured CUDA graph.
+  // Jacobi PCG (pcg.hpp:63-130) as a captured CUDA graph.  (Fusing the
+  // direction update into the apply's p staging was measured slower: the
+  // apply is issue-bound, the p update streams at HBM speed on its own.)
   void pcg_body(bool lm) {
     const long long n = P_.num_cols;
     const int vg = vgrid(n, nsm_);
@@ -948,25 +986,6 @@ class Session final : public SessionBase {
     k_pcg_init<Real><<<vg, MO_THREADS, 0, st_>>>(red(0, vg, MO_FIN_PCG_INIT, 0), n, colmask_, b_, mdv, delta_, r_, p_, pre);
     ++launches_;
     const int flags = MO_F_REDUCE | MO_F_ZEROEXCL | MO_F_SKIPDONE | (lm ? MO_F_DAMP : 0);
-    if (fused_pcg()) {
-      // Two kernels per iteration: {p = z + beta p_old staged in the apply,
-      // J^T J p, p'Ap -> alpha} and {delta, r update, r'z -> beta}.  p
-      // ping-pongs between p_ and p2_ so no block overwrites a halo another
-      // block still reads.
-      Real* pb[2] = {p_, p2_};
-      for (int k = 0; k < cfg_.linear_iters; ++k) {
-        Real* pk = pb[k & 1];
-        prof_begin(0);
-        if (k == 0) apply(p_, ap_, flags);
-        else apply(pb[(k - 1) & 1], ap_, flags | MO_F_PUPD, r_, mdv, pk);
-        prof_end(0);
-        prof_begin(1);
-        k_pcg_update<Real><<<vg, MO_THREADS, 0, st_>>>(red(0, vg, MO_FIN_PCG_BETA, 0), n, colmask_, mdv, delta_, r_, pk, ap_, pre);
-        ++launches_;
-        prof_end(1);
-      }
-      return;
-    }
     for (int k = 0; k < cfg_.linear_iters; ++k) {
       prof_begin(0);
       apply(p_, ap_, flags);
@@ -979,36 +998,41 @@ class Session final : public SessionBase {
     }
   }
 
-  void run_pcg(bool lm) {
-    if (P_.num_cols == 0) {
-      // Nothing to solve: an empty r'z is exactly 0 <= stop (pcg.hpp:95).
-      CK(cudaMemcpyAsync(&state_->done, &zero_flags_, sizeof(int) * 4, cudaMemcpyHostToDevice, st_));
-      return;
-    }
+  // Replay `body` as a CUDA graph captured on first use (per stage key);
+  // MO_B200_NOGRAPH=1 launches it directly.  Kernels count individually.
+  template <class F>
+  void run_stage(int key, F&& body) {
     static const bool nograph = std::getenv("MO_B200_NOGRAPH") != nullptr;
+    cur_stage_ = key;
     if (nograph) {
-      prof_reset_slots();
-      pcg_body(lm);
+      stage_pos_[key] = 0;
+      body();
       return;
     }
-    auto it = pcg_exec_.find(lm);
-    if (it == pcg_exec_.end()) {
-      prof_reset_slots();
-      int64_t before = launches_;
+    auto it = stage_exec_.find(key);
+    if (it == stage_exec_.end()) {
+      stage_pos_[key] = 0;
+      const int64_t before = launches_;
       cudaGraph_t graph;
-      CK(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
-      pcg_body(lm);
+      CK(cudaStreamBeginCapture(st_, cudaStreamCaptureModeRelaxed));
+      try {
+        body();
+      } catch (...) {
+        cudaGraph_t g2;
+        cudaStreamEndCapture(st_, &g2);
+        if (g2) cudaGraphDestroy(g2);
+        throw;
+      }
       CK(cudaStreamEndCapture(st_, &graph));
       cudaGraphExec_t exec;
       CK(cudaGraphInstantiate(&exec, graph, 0));
       cudaGraphDestroy(graph);
-      pcg_nodes_[lm] = launches_ - before;
+      stage_nodes_[key] = launches_ - before;
       launches_ = before;
-      it = pcg_exec_.emplace(lm, exec).first;
+      it = stage_exec_.emplace(key, exec).first;
     }
     CK(cudaGraphLaunch(it->second, st_));
-    launches_ += pcg_nodes_[lm];
-    prof_pending_ = true;
+    launches_ += stage_nodes_[key];
   }
 
   // ------------------------------------------------------------ profiling
@@ -1019,43 +1043,38 @@ class Session final : public SessionBase {
     CK(cudaStreamIsCapturing(st_, &cs));
     return cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
   }
-  void prof_reset_slots() {
-    for (auto& p : prof_) p.used = 0;
-  }
   void prof_begin(int kind) {
-    if (!profiling_) return;
-    Prof& p = prof_[size_t(kind)];
-    if (p.used == p.ev.size()) {
-      cudaEvent_t a, b;
-      CK(cudaEventCreate(&a));
-      CK(cudaEventCreate(&b));
-      p.ev.push_back({a, b});
+    if (!profiling_ || cur_stage_ < 0) return;
+    auto& v = stage_ev_[cur_stage_];
+    size_t& pos = stage_pos_[cur_stage_];
+    if (pos == v.size()) {
+      ProfEv e;
+      CK(cudaEventCreate(&e.a));
+      CK(cudaEventCreate(&e.b));
+      v.push_back(e);
     }
-    CK(cudaEventRecordWithFlags(p.ev[p.used].first, st_, capture_flags()));
+    v[pos].kind = kind;
+    CK(cudaEventRecordWithFlags(v[pos].a, st_, capture_flags()));
+    open_.push_back(pos++);
   }
-  void prof_end(int kind) {
+  void prof_end(int) {
+    if (!profiling_ || cur_stage_ < 0 || open_.empty()) return;
+    auto& v = stage_ev_[cur_stage_];
+    CK(cudaEventRecordWithFlags(v[open_.back()].b, st_, capture_flags()));
+    open_.pop_back();
+  }
+  void collect_profile(int stage) {
     if (!profiling_) return;
-    Prof& p = prof_[size_t(kind)];
-    CK(cudaEventRecordWithFlags(p.ev[p.used].second, st_, capture_flags()));
-    p.used++;
-    prof_pending_ = true;
-  }
-  void collect_profile() {
-    if (!profiling_ || !prof_pending_) return;
-    for (size_t k = 0; k < prof_.size(); ++k) {
-      Prof& p = prof_[k];
-      for (size_t i = 0; i < p.used; ++i) {
-        float ms = 0;
-        if (cudaEventElapsedTime(&ms, p.ev[i].first, p.ev[i].second) == cudaSuccess) {
-          p.total_ms += ms;
-          p.count++;
-        } else {
-          cudaGetLastError();
-        }
+    auto& v = stage_ev_[stage];
+    for (size_t i = 0; i < stage_pos_[stage] && i < v.size(); ++i) {
+      float ms = 0;
+      if (cudaEventElapsedTime(&ms, v[i].a, v[i].b) == cudaSuccess) {
+        prof_[size_t(v[i].kind)].total_ms += ms;
+        prof_[size_t(v[i].kind)].count++;
+      } else {
+        cudaGetLastError();
       }
-      if (k == 2) p.used = 0;  // build_normal events are re-recorded every iteration
     }
-    prof_pending_ = false;
   }
 
   void sync_state() {
@@ -1074,8 +1093,7 @@ class Session final : public SessionBase {
   cudaStream_t st_ = nullptr;
   Module mod_;
   Real *x_ = nullptr, *xt_ = nullptr, *b_ = nullptr, *m_ = nullptr, *md_ = nullptr, *damp_ = nullptr;
-  Real *delta_ = nullptr, *r_ = nullptr, *p_ = nullptr, *p2_ = nullptr, *ap_ = nullptr, *vtmp_ = nullptr,
-       *otmp_ = nullptr;
+  Real *delta_ = nullptr, *r_ = nullptr, *p_ = nullptr, *ap_ = nullptr, *vtmp_ = nullptr, *otmp_ = nullptr;
   Real* resid_ = nullptr;
   size_t resid_cap_ = 0;
   double* bd_ = nullptr;
@@ -1096,13 +1114,17 @@ class Session final : public SessionBase {
   bool x_bound_ = false, params_bound_ = false, refreshed_ = false;
   std::map<const void*, int> occ_;
   ModuleInfo minfo_;
-  std::map<bool, cudaGraphExec_t> pcg_exec_;
-  std::map<bool, int64_t> pcg_nodes_;
+  std::map<int, cudaGraphExec_t> stage_exec_;
+  std::map<int, int64_t> stage_nodes_;
   std::vector<void*> owned_;
   int64_t launches_ = 0;
-  bool profiling_ = false, prof_pending_ = false;
+  bool profiling_ = false;
   std::vector<Prof> prof_ = std::vector<Prof>(4);
-  int zero_flags_[4] = {1, 0, 0, 0};
+  std::map<int, std::vector<ProfEv>> stage_ev_;
+  std::map<int, size_t> stage_pos_;
+  std::vector<size_t> open_;
+  int cur_stage_ = -1;
+  double* mu_h_ = nullptr;  // pinned staging of the LM radius
 };
 
 std::unique_ptr<SessionBase> make_session(const Plan& plan, int device) {
