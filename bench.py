@@ -199,10 +199,6 @@ def run_ours(args):
         restore()
         s.solve()
 
-    s.set_profiling(True)
-    restore()
-    s.solve()  # capture the profiled PCG graph outside the timed region
-    s.profile_reset()
     launches0 = s.kernel_launches()
     times = []
     if world > 1:
@@ -227,6 +223,17 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.barrier()
         step_ms = float(t.item())
+    # Kernel durations for the roofline: the same solves with CUDA events
+    # recorded around every J^T J p apply and PCG update on the session stream
+    # (event nodes inside the captured graphs), kept out of the headline timing.
+    s.set_profiling(True)
+    restore()
+    s.solve()  # capture the profiled graphs
+    s.profile_reset()
+    for _ in range(max(2, args.steps)):
+        restore()
+        s.solve()
+    torch.cuda.synchronize()
     apply_ms, apply_n = s.profile(0)
     upd_ms, upd_n = s.profile(1)
     s.set_profiling(False)

@@ -162,6 +162,28 @@ int mo_solve(mo_session s, mo_iter_cb cb, void* user, mo_solve_result* out); /* 
 int mo_get_x(mo_session s, void* out, int64_t n);
 int mo_saw_nonfinite(mo_session s, int* out);               /* :110 */
 
+/* ---- strip sharding (multi-GPU; no reference counterpart) --
+ * A grid plan (one grid domain, no graphs) is split into contiguous strips
+ * of axis-0 rows, one session per strip.  Each strip stores its rows plus
+ * mo_plan_halo_rows() halo rows on each side (clipped at the domain edge);
+ * binds take the strip's LOCAL data [lo, hi) (mo_session_local_layout).
+ * Per PCG iteration the p halo is exchanged and the two dot products are
+ * reduced in fixed rank order, so every strip takes identical steps. */
+typedef struct mo_comm_s* mo_comm;
+typedef struct mo_world_s* mo_world;
+int mo_plan_halo_rows(mo_plan p, int* rows);
+/* NCCL transport, one process per GPU: rank 0 creates the id, every rank passes it. */
+int mo_nccl_unique_id(void* out, size_t len /* >= 128 */);
+int mo_comm_create_nccl(const void* id, size_t len, int rank, int world, int device, mo_comm* out);
+/* Single-process transport: `world` strip sessions on one device, each driven
+ * from its own host thread (halo copies + fixed-order gathers). */
+int mo_world_create_local(int world, int device, mo_world* out);
+int mo_comm_create_local(mo_world w, int rank, mo_comm* out);
+void mo_world_destroy(mo_world w);
+void mo_comm_destroy(mo_comm c);
+int mo_session_create_shard(mo_plan p, int device, mo_comm c, int64_t row0, int64_t row1, mo_session* out);
+int mo_session_local_layout(mo_session s, int64_t* lo, int64_t* hi, int64_t* row0, int64_t* row1);
+
 /* ---- measurement hooks (bench.py) -------------------------------------- */
 /* When enabled, CUDA events bracket every J^T J p apply and PCG vector update
  * launched by mo_solve (on the session stream, also inside CUDA graphs). */

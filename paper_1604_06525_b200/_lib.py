@@ -80,6 +80,15 @@ SIGNATURES = {
     "mo_solve": (c_int, [c_void_p, ITER_CB, c_void_p, ctypes.POINTER(SolveResultC)]),
     "mo_get_x": (c_int, [c_void_p, c_void_p, c_int64]),
     "mo_saw_nonfinite": (c_int, [c_void_p, ctypes.POINTER(c_int)]),
+    "mo_plan_halo_rows": (c_int, [c_void_p, ctypes.POINTER(c_int)]),
+    "mo_nccl_unique_id": (c_int, [c_void_p, c_size_t]),
+    "mo_comm_create_nccl": (c_int, [c_void_p, c_size_t, c_int, c_int, c_int, ctypes.POINTER(c_void_p)]),
+    "mo_world_create_local": (c_int, [c_int, c_int, ctypes.POINTER(c_void_p)]),
+    "mo_comm_create_local": (c_int, [c_void_p, c_int, ctypes.POINTER(c_void_p)]),
+    "mo_world_destroy": (None, [c_void_p]),
+    "mo_comm_destroy": (None, [c_void_p]),
+    "mo_session_create_shard": (c_int, [c_void_p, c_int, c_void_p, c_int64, c_int64, ctypes.POINTER(c_void_p)]),
+    "mo_session_local_layout": (c_int, [c_void_p] + [ctypes.POINTER(c_int64)] * 4),
     "mo_set_profiling": (c_int, [c_void_p, c_int]),
     "mo_profile_read": (c_int, [c_void_p, c_int, ctypes.POINTER(c_double), ctypes.POINTER(c_int64)]),
     "mo_profile_reset": (c_int, [c_void_p]),

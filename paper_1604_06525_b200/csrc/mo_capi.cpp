@@ -9,6 +9,7 @@
 
 #include "../../include/mo_b200.h"
 #include "mo_codegen.hpp"
+#include "mo_comm.hpp"
 #include "mo_jit.hpp"
 #include "mo_plan.hpp"
 #include "mo_session.hpp"
@@ -24,6 +25,12 @@ const char* device_prelude() {
 
 struct mo_plan_s {
   mo::Plan plan;
+};
+struct mo_world_s {
+  std::shared_ptr<mo::LocalWorld> w;
+};
+struct mo_comm_s {
+  std::unique_ptr<mo::Comm> c;
 };
 struct mo_session_s {
   std::unique_ptr<mo::SessionBase> impl;
@@ -289,6 +296,71 @@ int mo_solve(mo_session s, mo_iter_cb cb, void* user, mo_solve_result* out) {
     out->n_trace = int(s->trace.size());
     out->trace = s->trace.data();
   });
+}
+
+int mo_plan_halo_rows(mo_plan p, int* rows) {
+  return guard([&] {
+    need(p, "plan");
+    need(rows, "output");
+    *rows = mo::halo_rows(p->plan);
+  });
+}
+
+int mo_nccl_unique_id(void* out, size_t len) {
+  return guard([&] {
+    need(out, "output");
+    mo::check(len >= 128, mo::Err::kBindError, "NCCL unique id needs 128 bytes");
+    mo::nccl_unique_id(out);
+  });
+}
+
+int mo_comm_create_nccl(const void* id, size_t len, int rank, int world, int device, mo_comm* out) {
+  return guard([&] {
+    need(id, "id");
+    need(out, "output");
+    mo::check(len >= 128, mo::Err::kBindError, "NCCL unique id needs 128 bytes");
+    auto c = std::make_unique<mo_comm_s>();
+    c->c = mo::make_nccl_comm(id, rank, world, device);
+    *out = c.release();
+  });
+}
+
+int mo_world_create_local(int world, int device, mo_world* out) {
+  return guard([&] {
+    need(out, "output");
+    auto w = std::make_unique<mo_world_s>();
+    w->w = mo::make_local_world(world, device);
+    *out = w.release();
+  });
+}
+
+int mo_comm_create_local(mo_world w, int rank, mo_comm* out) {
+  return guard([&] {
+    need(w, "world");
+    need(out, "output");
+    auto c = std::make_unique<mo_comm_s>();
+    c->c = mo::make_local_comm(w->w, rank);
+    *out = c.release();
+  });
+}
+
+void mo_world_destroy(mo_world w) { delete w; }
+void mo_comm_destroy(mo_comm c) { delete c; }
+
+int mo_session_create_shard(mo_plan p, int device, mo_comm c, int64_t row0, int64_t row1, mo_session* out) {
+  return guard([&] {
+    need(p, "plan");
+    need(c, "communicator");
+    need(out, "output");
+    auto s = std::make_unique<mo_session_s>();
+    s->impl = mo::make_shard_session(p->plan, device, c->c.get(), row0, row1);
+    *out = s.release();
+  });
+}
+
+int mo_session_local_layout(mo_session s, int64_t* lo, int64_t* hi, int64_t* row0, int64_t* row1) {
+  SESSION_CALL(need(lo, "output"); need(hi, "output"); need(row0, "output"); need(row1, "output");
+               s->impl->local_layout(lo, hi, row0, row1));
 }
 
 int mo_set_profiling(mo_session s, int enable) { SESSION_CALL(s->impl->set_profiling(enable != 0)); }

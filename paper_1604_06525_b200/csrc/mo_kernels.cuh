@@ -15,7 +15,41 @@
 
 namespace mo {
 
-__device__ __forceinline__ bool ex_at(const unsigned char* cm, long long i) { return cm && cm[i]; }
+// colmask bit 0: excluded column (solver.hpp:149-157).  Bit 1: halo column of
+// a strip shard — owned by a neighbour, never updated or reduced here.
+__device__ __forceinline__ bool ex_at(const unsigned char* cm, long long i) { return cm && (cm[i] & 1); }
+__device__ __forceinline__ bool halo_at(const unsigned char* cm, long long i) { return cm && (cm[i] & 2); }
+
+// Strip shards: fixed rank-order sum of the gathered partials, then the same
+// finalisation every rank (pcg.hpp scalar logic via mo_finalize).
+template <class Real>
+__global__ void k_global_fin(mo_state* st, const double* rb, int world, int op, int arg) {
+  if (threadIdx.x != 0) return;
+  if ((op == MO_FIN_PCG_ALPHA || op == MO_FIN_PCG_BETA) && st->done) return;
+  double t = 0, t2 = 0;
+  for (int r = 0; r < world; ++r) {
+    t += rb[2 * r];
+    t2 += rb[2 * r + 1];
+  }
+  mo_finalize<Real>(st, op, arg, t, t2);
+}
+__global__ void k_flags_out(mo_state* st) {
+  st->sums[4] = double(st->nonfinite_kernel);
+  st->sums[5] = double(st->any_nonzero);
+}
+__global__ void k_flags_in(mo_state* st, const double* rb, int world) {
+  int nf = 0, nz = 0;
+  for (int r = 0; r < world; ++r) {
+    nf |= rb[2 * r] != 0.0;
+    nz |= rb[2 * r + 1] != 0.0;
+  }
+  st->nonfinite_kernel = nf;
+  st->any_nonzero = nz;
+}
+__global__ void k_or_bits(unsigned char* p, long long n, unsigned char bits) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] |= bits;
+}
 
 // delta = 0; r = b; z = r/m; p = z; rz = r'z   (pcg.hpp:75-97)
 template <class Real>
@@ -32,6 +66,7 @@ k_pcg_init(mo_red R, long long n, const unsigned char* cm, const Real* __restric
   double acc = 0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
+    if (halo_at(cm, i)) continue;
     const bool ex = ex_at(cm, i);
     const Real ri = ex ? Real(0) : b[i];
     const Real zi = ex ? Real(0) : (precond ? ri / md[i] : ri);
@@ -70,9 +105,10 @@ __device__ __forceinline__ uchar4 ldm4(const unsigned char* cm, long long i) {
 
 // delta += alpha p; r -= alpha Ap; z = r/m; rz' = r'z   (pcg.hpp:111-118)
 template <class Real>
-__device__ __forceinline__ double pcg_update1(Real alpha, bool ex, Real& d, Real& r, Real p, Real ap, Real md,
+__device__ __forceinline__ double pcg_update1(Real alpha, unsigned char m, Real& d, Real& r, Real p, Real ap, Real md,
                                               int precond) {
-  if (ex) {
+  if (m & 2) return 0.0;  // halo column: a neighbour's
+  if (m & 1) {
     d = Real(0);
     r = Real(0);
     return 0.0;
@@ -98,21 +134,22 @@ k_pcg_update(mo_red R, long long n, const unsigned char* cm, const Real* __restr
     V4<Real> D = ld4(delta + i), Rr = ld4(r + i);
     const V4<Real> Pp = ld4(p + i), A = ld4(ap + i), M = ld4(md + i);
     const uchar4 e = ldm4(cm, i);
-    const bool ex[4] = {e.x != 0, e.y != 0, e.z != 0, e.w != 0};
+    const unsigned char ex[4] = {e.x, e.y, e.z, e.w};
 #pragma unroll
     for (int k = 0; k < 4; ++k) acc += pcg_update1(alpha, ex[k], D.a[k], Rr.a[k], Pp.a[k], A.a[k], M.a[k], precond);
     st4(delta + i, D);
     st4(r + i, Rr);
   }
   for (long long i = (n4 << 2) + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride)
-    acc += pcg_update1(alpha, ex_at(cm, i), delta[i], r[i], p[i], ap[i], md[i], precond);
+    acc += pcg_update1(alpha, cm ? cm[i] : (unsigned char)0, delta[i], r[i], p[i], ap[i], md[i], precond);
   mo_reduce_epilogue<Real>(R, acc, 0.0, false);
 }
 
 // p = z + beta p with z = r/m recomputed   (pcg.hpp:124-126)
 template <class Real>
-__device__ __forceinline__ Real pcg_p1(Real beta, bool ex, Real r, Real md, Real p, int precond) {
-  if (ex) return Real(0);
+__device__ __forceinline__ Real pcg_p1(Real beta, unsigned char m, Real r, Real md, Real p, int precond) {
+  if (m & 2) return p;  // halo column: refreshed by the exchange
+  if (m & 1) return Real(0);
   const Real z = precond ? r / md : r;
   return z + beta * p;
 }
@@ -130,13 +167,13 @@ k_pcg_p(const mo_state* st, long long n, const unsigned char* cm, const Real* __
     const V4<Real> Rr = ld4(r + i), M = ld4(md + i);
     V4<Real> Pp = ld4(p + i);
     const uchar4 e = ldm4(cm, i);
-    const bool ex[4] = {e.x != 0, e.y != 0, e.z != 0, e.w != 0};
+    const unsigned char ex[4] = {e.x, e.y, e.z, e.w};
 #pragma unroll
     for (int k = 0; k < 4; ++k) Pp.a[k] = pcg_p1(beta, ex[k], Rr.a[k], M.a[k], Pp.a[k], precond);
     st4(p + i, Pp);
   }
   for (long long i = (n4 << 2) + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride)
-    p[i] = pcg_p1(beta, ex_at(cm, i), r[i], md[i], p[i], precond);
+    p[i] = pcg_p1(beta, cm ? cm[i] : (unsigned char)0, r[i], md[i], p[i], precond);
 }
 
 // Unfused apply epilogue (plans with graph scatters): LM damping, excluded
@@ -165,6 +202,7 @@ k_bm_patch(mo_red R, long long n, const unsigned char* cm, Real* __restrict__ b,
   double cnt = 0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
+    if (halo_at(cm, i)) continue;
     if (ex_at(cm, i)) {
       b[i] = Real(0);
       m[i] = Real(1);
@@ -205,6 +243,7 @@ k_lm_damp(const mo_state* st, long long n, const unsigned char* cm, const Real* 
   const double s = 2.0 / st->mu;  // mu staged by the host before each trial
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
+    if (halo_at(cm, i)) continue;
     const Real d = ex_at(cm, i) ? Real(0) : Real(s * bd[i]);
     damp[i] = d;
     md[i] = m[i] + d;
@@ -221,6 +260,7 @@ k_xtrial(mo_state* st, long long n, const unsigned char* cm, Real* __restrict__ 
   bool nz = false;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
+    if (halo_at(cm, i)) continue;  // refreshed by the halo exchange
     const Real d = delta[i];
     if (d != Real(0)) nz = true;
     const Real xi = x[i];
@@ -235,11 +275,12 @@ k_xtrial(mo_state* st, long long n, const unsigned char* cm, Real* __restrict__ 
 // sums[arg] = sum b*delta, sums[arg+1] = sum (0.5*delta)*JtJdelta.
 template <class Real>
 __global__ void __launch_bounds__(MO_THREADS)
-k_lm_predicted(mo_red R, long long n, const Real* __restrict__ b, const Real* __restrict__ delta,
+k_lm_predicted(mo_red R, long long n, const unsigned char* cm, const Real* __restrict__ b, const Real* __restrict__ delta,
                const Real* __restrict__ ap) {
   double s1 = 0, s2 = 0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
+    if (halo_at(cm, i)) continue;
     s1 += double(b[i]) * double(delta[i]);
     s2 += 0.5 * double(delta[i]) * double(ap[i]);
   }

@@ -25,6 +25,7 @@
 #include "mo_codegen.hpp"
 #include "mo_jit.hpp"
 #include "mo_kernels.cuh"
+#include "mo_comm.hpp"
 #include "mo_session.hpp"
 
 namespace mo {
@@ -62,7 +63,14 @@ int vgrid(long long n, int nsm) {
 template <class Real>
 class Session final : public SessionBase {
  public:
-  Session(const Plan& plan, int device) : P_(plan), dev_(device) {
+  // comm != nullptr: strip shard owning axis-0 rows [row0, row1) of the
+  // plan's single grid domain.  Fields are stored for rows
+  // [lo, hi) = owned rows plus halo_rows(P) on each side (clipped); kernels
+  // keep GLOBAL coordinates, so InBounds / index() / OOB semantics are those
+  // of the unsharded problem.
+  Session(const Plan& plan, int device, Comm* comm = nullptr, int64_t row0 = 0, int64_t row1 = -1)
+      : P_(plan), dev_(device), comm_(comm) {
+    if (comm_) setup_shard(row0, row1);
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
       fail(Err::kNoDevice, "no CUDA device available (the B200 path has no CPU fallback)");
@@ -96,14 +104,21 @@ class Session final : public SessionBase {
     arr_.resize(P_.arrays.size(), nullptr);
     arr_n_.assign(P_.arrays.size(), -1);
     for (size_t i = 0; i < P_.arrays.size(); ++i)
-      arr_[i] = dalloc<Real>(size_t(P_.extent_of(P_.arrays[i].dom) * P_.arrays[i].channels));
+      arr_[i] = dalloc<Real>(size_t(lext(P_.arrays[i].dom) * P_.arrays[i].channels));
     comp_.resize(P_.computed.size(), nullptr);
     for (size_t i = 0; i < P_.computed.size(); ++i)
-      comp_[i] = dalloc<Real>(size_t(P_.extent_of(P_.computed[i].dom) * P_.computed[i].channels));
+      comp_[i] = dalloc<Real>(size_t(lext(P_.computed[i].dom) * P_.computed[i].channels));
     masks_.resize(P_.exclude_kernels.size(), nullptr);
     for (size_t i = 0; i < P_.exclude_kernels.size(); ++i)
-      masks_[i] = dalloc<unsigned char>(size_t(P_.extent_of(P_.exclude_kernels[i].dom)));
-    if (!P_.exclude_kernels.empty()) colmask_ = dalloc<unsigned char>(n);
+    {
+      masks_[i] = dalloc<unsigned char>(size_t(lext(P_.exclude_kernels[i].dom)));
+      CK(cudaMemsetAsync(masks_[i], 0, size_t(lext(P_.exclude_kernels[i].dom)), st_));
+    }
+    if (!P_.exclude_kernels.empty() || comm_) {
+      colmask_ = dalloc<unsigned char>(n);
+      CK(cudaMemsetAsync(colmask_, 0, n, st_));
+    }
+    if (comm_) rankbuf_ = dalloc<double>(size_t(comm_->world) * 64);
     params_d_ = dalloc<double>(std::max<size_t>(P_.params.size(), 1));
     state_ = dalloc<mo_state>(1);
     CK(cudaMallocHost(&state_h_, sizeof(mo_state)));
@@ -137,6 +152,7 @@ class Session final : public SessionBase {
     cudaFree(params_d_);
     cudaFree(state_);
     cudaFree(partials_);
+    cudaFree(rankbuf_);
     cudaFreeHost(state_h_);
     for (auto& g : graphs_) cudaFree(g.d_verts);
     for (auto& gs : gsets_) {
@@ -207,6 +223,7 @@ class Session final : public SessionBase {
       kp.out0 = comp_[size_t(ck.index)];
       launch_grid("mo_computed_" + std::to_string(&ck - P_.computed_kernels.data()), ck.dom, kp);
     }
+    exchange_computed();
     for (size_t i = 0; i < P_.exclude_kernels.size(); ++i) {
       const ExcludeKernel& ek = P_.exclude_kernels[i];
       mo_kparams kp = kp_grid(ek.dom, x_, nullptr);
@@ -218,11 +235,12 @@ class Session final : public SessionBase {
       for (size_t i = 0; i < P_.exclude_kernels.size(); ++i)
         for (size_t f = 0; f < P_.unknowns.size(); ++f) {
           if (!(P_.unknowns[f].dom == P_.exclude_kernels[i].dom)) continue;
-          long long ne = P_.extent_of(P_.unknowns[f].dom);
+          long long ne = lext(P_.unknowns[f].dom);
           k_colmask<<<vgrid(ne, nsm_), MO_THREADS, 0, st_>>>(ne, P_.unknowns[f].channels, masks_[i],
                                                            colmask_ + P_.ubase[f]);
           ++launches_;
         }
+      if (sh_.on) mark_halo_cols();  // bit 1: halo column, skipped by vector kernels
     }
   }
 
@@ -353,6 +371,7 @@ class Session final : public SessionBase {
       return ms;
     };
     auto finish = [&] {
+      reduce_flags();
       sync_state();
       res.nonfinite_kernels = state_h_->nonfinite_kernel != 0;
       res.unconstrained = unconstrained_;
@@ -373,7 +392,9 @@ class Session final : public SessionBase {
           CK(cudaMemsetAsync(&state_->any_nonzero, 0, sizeof(int), st_));
           k_xtrial<Real><<<vg, MO_THREADS, 0, st_>>>(state_, n, colmask_, x_, delta_, xt_, 1, SLOT_COST);
           ++launches_;
+          exchange_cols(x_);
           cost_at(x_, SLOT_COST + 1);
+          reduce_flags();
         });
         sync_state();
         collect_profile(kStageGN);
@@ -443,10 +464,15 @@ class Session final : public SessionBase {
           CK(cudaMemsetAsync(&state_->any_nonzero, 0, sizeof(int), st_));
           k_xtrial<Real><<<vg, MO_THREADS, 0, st_>>>(state_, n, colmask_, x_, delta_, xt_, 0, SLOT_COST);
           ++launches_;
+          exchange_cols(xt_);
           cost_at(xt_, SLOT_COST + 1);
+          exchange_cols(delta_);
           apply(delta_, ap_, 0);  // undamped model curvature (solver.hpp:467)
-          k_lm_predicted<Real><<<vg, MO_THREADS, 0, st_>>>(red(0, vg, MO_FIN_STORE2, SLOT_PRED), n, b_, delta_, ap_);
+          k_lm_predicted<Real><<<vg, MO_THREADS, 0, st_>>>(red(0, vg, MO_FIN_STORE2, SLOT_PRED), n, colmask_, b_,
+                                                           delta_, ap_);
           ++launches_;
+          reduce_done(MO_FIN_STORE2, SLOT_PRED);
+          reduce_flags();
         });
         sync_state();
         collect_profile(kStageLMTrial);
@@ -550,8 +576,118 @@ class Session final : public SessionBase {
   };
   enum { kStageGN = 0, kStageLMLin = 1, kStageLMTrial = 2 };
 
+  // ------------------------------------------------------------ sharding
+  struct Shard {
+    bool on = false;
+    Domain dom;
+    int64_t d0 = 0, S = 1;  // axis-0 extent, elements per row
+    int64_t row0 = 0, row1 = 0, lo = 0, hi = 0;
+    int R = 0;
+  };
+
+  void setup_shard(int64_t row0, int64_t row1) {
+    check(P_.graph_sets.empty(), Err::kBindError, "strip sharding supports grid energies only");
+    const Domain* D = nullptr;
+    auto same = [&](const Domain& d) {
+      if (!D) D = &d;
+      check(d == *D, Err::kBindError, "strip sharding needs every field on one grid domain");
+    };
+    for (const Field& f : P_.unknowns) same(f.dom);
+    for (const Field& f : P_.arrays) same(f.dom);
+    for (const Field& f : P_.computed) same(f.dom);
+    for (const GridSet& g : P_.grid_sets) same(g.dom);
+    for (const GatherSet& g : P_.gather_sets) same(g.dom);
+    for (const ExcludeKernel& e : P_.exclude_kernels) same(e.dom);
+    check(D && !D->dims.empty(), Err::kBindError, "strip sharding needs a grid domain");
+    sh_.dom = *D;
+    sh_.d0 = P_.shape_of(*D)[0];
+    sh_.S = P_.extent_of(*D) / std::max<int64_t>(sh_.d0, 1);
+    if (row1 < 0) row1 = sh_.d0;
+    check(row0 >= 0 && row0 < row1 && row1 <= sh_.d0, Err::kBindError, "strip rows out of range");
+    sh_.R = halo_rows(P_);
+    check(comm_->world == 1 || row1 - row0 >= sh_.R, Err::kBindError, "strip thinner than the halo");
+    sh_.row0 = row0;
+    sh_.row1 = row1;
+    sh_.lo = std::max<int64_t>(0, row0 - sh_.R);
+    sh_.hi = std::min<int64_t>(sh_.d0, row1 + sh_.R);
+    sh_.on = true;
+    int64_t col = 0;  // local column layout: each field's [lo, hi) rows, field-major
+    for (size_t f = 0; f < P_.unknowns.size(); ++f) {
+      P_.ubase[f] = col;
+      col += lext(P_.unknowns[f].dom) * P_.unknowns[f].channels;
+    }
+    P_.num_cols = col;
+  }
+  // Local (stored) element count of a domain.
+  int64_t lext(const Domain& d) const {
+    return sh_.on && d == sh_.dom ? (sh_.hi - sh_.lo) * sh_.S : P_.extent_of(d);
+  }
+  HaloSeg seg(void* base, size_t row_bytes) const {
+    HaloSeg s;
+    s.base = static_cast<char*>(base);
+    s.row_bytes = row_bytes;
+    s.top = int(sh_.row0 - sh_.lo);
+    s.owned = int(sh_.row1 - sh_.row0);
+    s.bottom = int(sh_.hi - sh_.row1);
+    s.send_up = int(std::min<int64_t>(sh_.d0, sh_.row0 + sh_.R) - sh_.row0);
+    s.send_down = int(std::min<int64_t>(sh_.R, sh_.row1));
+    if (comm_->rank == 0) s.send_up = 0;
+    if (comm_->rank == comm_->world - 1) s.send_down = 0;
+    return s;
+  }
+  // Halo rows of a column-layout vector (p, x, x_trial, delta).
+  void exchange_cols(Real* v) {
+    if (!sh_.on) return;
+    std::vector<HaloSeg> segs;
+    for (size_t f = 0; f < P_.unknowns.size(); ++f)
+      segs.push_back(seg(v + P_.ubase[f], size_t(sh_.S) * size_t(P_.unknowns[f].channels) * sizeof(Real)));
+    comm_->halo(segs, st_);
+  }
+  void exchange_computed() {
+    if (!sh_.on || comp_.empty()) return;
+    std::vector<HaloSeg> segs;
+    for (size_t c = 0; c < comp_.size(); ++c)
+      segs.push_back(seg(comp_[c], size_t(sh_.S) * size_t(P_.computed[c].channels) * sizeof(Real)));
+    comm_->halo(segs, st_);
+  }
+  // After the kernels of one reduction: every rank's partial is gathered in
+  // rank order and finalised identically everywhere (deterministic).
+  void reduce_done(int op, int arg) {
+    if (!sh_.on) return;
+    comm_->allgather(&state_->sums[4], rankbuf_, 2, st_);
+    k_global_fin<Real><<<1, 32, 0, st_>>>(state_, rankbuf_, comm_->world, op, arg);
+    ++launches_;
+  }
+  void reduce_flags() {
+    if (!sh_.on) return;
+    k_flags_out<<<1, 1, 0, st_>>>(state_);
+    comm_->allgather(&state_->sums[4], rankbuf_, 2, st_);
+    k_flags_in<<<1, 1, 0, st_>>>(state_, rankbuf_, comm_->world);
+    launches_ += 2;
+  }
+  void mark_halo_cols() {
+    for (size_t f = 0; f < P_.unknowns.size(); ++f) {
+      const long long rowc = sh_.S * P_.unknowns[f].channels;
+      const long long top = (sh_.row0 - sh_.lo) * rowc, own = (sh_.row1 - sh_.row0) * rowc;
+      const long long bot = (sh_.hi - sh_.row1) * rowc;
+      unsigned char* base = colmask_ + P_.ubase[f];
+      if (top) k_or_bits<<<vgrid(top, nsm_), MO_THREADS, 0, st_>>>(base, top, 2);
+      if (bot) k_or_bits<<<vgrid(bot, nsm_), MO_THREADS, 0, st_>>>(base + top + own, bot, 2);
+      launches_ += (top ? 1 : 0) + (bot ? 1 : 0);
+    }
+  }
+
+ public:
+  void local_layout(int64_t* lo, int64_t* hi, int64_t* row0, int64_t* row1) const override {
+    *lo = sh_.on ? sh_.lo : 0;
+    *hi = sh_.on ? sh_.hi : 0;
+    *row0 = sh_.on ? sh_.row0 : 0;
+    *row1 = sh_.on ? sh_.row1 : 0;
+  }
+
+ private:
   int64_t array_size(int i) const {
-    return P_.extent_of(P_.arrays[size_t(i)].dom) * P_.arrays[size_t(i)].channels;
+    return lext(P_.arrays[size_t(i)].dom) * P_.arrays[size_t(i)].channels;
   }
 
   void ensure_refreshed() {
@@ -739,7 +875,7 @@ class Session final : public SessionBase {
       v.s0 = int(s[0]);
       v.s1 = int(s[1]);
       v.s2 = int(s[2]);
-      v.row_lo = 0;
+      v.row_lo = sh_.on ? int(sh_.lo) : 0;
       return v;
     };
     for (int f = 0; f < U; ++f) {
@@ -761,9 +897,9 @@ class Session final : public SessionBase {
     k.d0 = int(s[0]);
     k.d1 = int(s[1]);
     k.d2 = int(s[2]);
-    k.row0 = 0;
-    k.row1 = int(s[0]);
-    k.row_lo = 0;
+    k.row0 = sh_.on ? int(sh_.row0) : 0;
+    k.row1 = sh_.on ? int(sh_.row1) : int(s[0]);
+    k.row_lo = sh_.on ? int(sh_.lo) : 0;
     for (size_t i = 0; i < P_.exclude_kernels.size(); ++i)
       if (P_.exclude_kernels[i].dom == d) k.mask = masks_[i];
     return k;
@@ -842,8 +978,10 @@ class Session final : public SessionBase {
     R.state = state_;
     R.part_base = base;
     R.part_total = total;
-    R.fin_op = op;
-    R.fin_arg = arg;
+    // Shard mode: kernels only produce this rank's partial (sums[4..5]);
+    // reduce_done() gathers and finalises.
+    R.fin_op = sh_.on ? MO_FIN_STORE2 : op;
+    R.fin_arg = sh_.on ? 4 : arg;
     return R;
   }
 
@@ -874,7 +1012,8 @@ class Session final : public SessionBase {
       total += grids.back();
     }
     if (total == 0) {
-      CK(cudaMemsetAsync(&state_->sums[slot], 0, sizeof(double), st_));
+      CK(cudaMemsetAsync(&state_->sums[sh_.on ? 4 : slot], 0, sizeof(double) * (sh_.on ? 2 : 1), st_));
+      reduce_done(MO_FIN_STORE, slot);
       return;
     }
     int base = 0, gi = 0;
@@ -890,6 +1029,7 @@ class Session final : public SessionBase {
       launch_edges("mo_graph_cost_" + std::to_string(i), int(i), kp, grids[size_t(gi)]);
       base += grids[size_t(gi)];
     }
+    reduce_done(MO_FIN_STORE, slot);
   }
 
   // build_normal (solver.hpp:220-251) on the device.
@@ -926,6 +1066,8 @@ class Session final : public SessionBase {
       ++launches_;
     } else if (P_.gather_sets.empty()) {
       CK(cudaMemsetAsync(&state_->unconstrained, 0, sizeof(long long), st_));
+    } else {
+      reduce_done(MO_FIN_UNCONSTRAINED, 0);
     }
     prof_end(2);
   }
@@ -959,6 +1101,7 @@ class Session final : public SessionBase {
       launch_grid(jtj_kernel(i), P_.gather_sets[i].dom, kp, grids[i], jtj_smem(i));
       base += grids[i];
     }
+    if (fused && (flags & MO_F_REDUCE)) reduce_done(MO_FIN_PCG_ALPHA, 0);
     if (!fused) {
       for (size_t i = 0; i < P_.graph_sets.size(); ++i) {
         mo_kparams kp = kp_graph(int(i), x_, pv);
@@ -985,6 +1128,8 @@ class Session final : public SessionBase {
     const int pre = cfg_.use_preconditioner ? 1 : 0;
     k_pcg_init<Real><<<vg, MO_THREADS, 0, st_>>>(red(0, vg, MO_FIN_PCG_INIT, 0), n, colmask_, b_, mdv, delta_, r_, p_, pre);
     ++launches_;
+    reduce_done(MO_FIN_PCG_INIT, 0);
+    exchange_cols(p_);  // strips: neighbours' p rows for the stencil apply
     const int flags = MO_F_REDUCE | MO_F_ZEROEXCL | MO_F_SKIPDONE | (lm ? MO_F_DAMP : 0);
     for (int k = 0; k < cfg_.linear_iters; ++k) {
       prof_begin(0);
@@ -992,8 +1137,11 @@ class Session final : public SessionBase {
       prof_end(0);
       prof_begin(1);
       k_pcg_update<Real><<<vg, MO_THREADS, 0, st_>>>(red(0, vg, MO_FIN_PCG_BETA, 0), n, colmask_, mdv, delta_, r_, p_, ap_, pre);
+      ++launches_;
+      reduce_done(MO_FIN_PCG_BETA, 0);
       k_pcg_p<Real><<<vg, MO_THREADS, 0, st_>>>(state_, n, colmask_, mdv, r_, p_, pre);
-      launches_ += 2;
+      ++launches_;
+      exchange_cols(p_);
       prof_end(1);
     }
   }
@@ -1004,7 +1152,7 @@ class Session final : public SessionBase {
   void run_stage(int key, F&& body) {
     static const bool nograph = std::getenv("MO_B200_NOGRAPH") != nullptr;
     cur_stage_ = key;
-    if (nograph) {
+    if (nograph || sh_.on) {  // strips: the local transport uses host barriers
       stage_pos_[key] = 0;
       body();
       return;
@@ -1111,6 +1259,9 @@ class Session final : public SessionBase {
   std::vector<int64_t> rowbase_, rowbase_dev_;
   int64_t rows_ = 0;
   int64_t unconstrained_ = 0;
+  Comm* comm_ = nullptr;      // strip-shard communicator (not owned)
+  Shard sh_;
+  double* rankbuf_ = nullptr;  // gathered per-rank partials
   bool x_bound_ = false, params_bound_ = false, refreshed_ = false;
   std::map<const void*, int> occ_;
   ModuleInfo minfo_;
@@ -1130,6 +1281,39 @@ class Session final : public SessionBase {
 std::unique_ptr<SessionBase> make_session(const Plan& plan, int device) {
   if (plan.cfg.precision == 0) return std::make_unique<Session<float>>(plan, device);
   return std::make_unique<Session<double>>(plan, device);
+}
+
+std::unique_ptr<SessionBase> make_shard_session(const Plan& plan, int device, Comm* comm, int64_t row0,
+                                                int64_t row1) {
+  check(comm != nullptr, Err::kBindError, "shard session needs a communicator");
+  if (plan.cfg.precision == 0) return std::make_unique<Session<float>>(plan, device, comm, row0, row1);
+  return std::make_unique<Session<double>>(plan, device, comm, row0, row1);
+}
+
+int halo_rows(const Plan& P) {
+  int reach = 0, H = 0;
+  auto scan = [&](const Program& pg) {
+    for (const Instr& in : pg.instrs) {
+      const bool load = in.op == kLoadU || in.op == kLoadA || in.op == kLoadC || in.op == kLoadP;
+      if ((load && !in.graph) || in.op == kInB) reach = std::max(reach, std::abs(int(in.off[0])));
+    }
+  };
+  for (const GridSet& g : P.grid_sets) {
+    scan(g.cost);
+    scan(g.evalf);
+    if (g.has_evalj) {
+      scan(g.evalj);
+      for (const JTemplate& jt : g.jtemplates)
+        for (const Lane& l : jt.lanes) H = std::max(H, std::abs(l.off[0]));
+    }
+  }
+  for (const GatherSet& g : P.gather_sets) {
+    scan(g.bm);
+    scan(g.jtj);
+  }
+  for (const ComputedKernel& c : P.computed_kernels) scan(c.prog);
+  for (const ExcludeKernel& e : P.exclude_kernels) scan(e.prog);
+  return reach + H;
 }
 
 }  // namespace mo

@@ -55,8 +55,18 @@ class SessionBase {
   virtual void profile_reset() = 0;
   virtual void* stream() = 0;
   virtual int64_t launches() const = 0;
+  // Strip shards: stored rows [lo, hi), owned rows [row0, row1) (all 0 when unsharded).
+  virtual void local_layout(int64_t* lo, int64_t* hi, int64_t* row0, int64_t* row1) const = 0;
 };
 
+class Comm;
 std::unique_ptr<SessionBase> make_session(const Plan& plan, int device);
+// Strip shard owning rows [row0, row1) of the plan's grid domain; `comm` must
+// outlive the session.
+std::unique_ptr<SessionBase> make_shard_session(const Plan& plan, int device, Comm* comm, int64_t row0,
+                                                int64_t row1);
+// Halo rows a strip needs on each side (max axis-0 reach of every program +
+// the two-phase apply's lane halo).
+int halo_rows(const Plan& plan);
 
 }  // namespace mo

@@ -1,0 +1,191 @@
+"""Strip sharding of grid plans across GPUs (the reference has
+no multi-device path).
+
+The plan's single grid domain is split into contiguous strips of axis-0 rows
+(the slowest axis of the reference's row-major layout, problem.hpp:131-136).
+A strip stores its owned rows plus `halo` rows on each side; the device
+kernels keep global coordinates, so InBounds / index() / OOB reads behave as
+in the unsharded problem.  Per PCG iteration the p halo is exchanged and the
+p'Ap / r'z partials are gathered and summed in rank order, so every strip
+takes the same alpha/beta.
+
+    # one process per GPU (torchrun), NCCL underneath:
+    s = ShardedSolver(plan, global_data, rank, world, device)
+    res = s.solve(); x = s.gather_x()
+    # all strips on one GPU (tests, the single-device fake of SURVEY.md §4):
+    g = LocalShardGroup(plan, global_data, world=3); res = g.solve(); x = g.gather_x()
+"""
+import ctypes
+import threading
+from dataclasses import dataclass
+from typing import List
+
+import numpy as np
+
+from . import planinfo
+from ._lib import call, lib
+from .solver import CompiledPlan, EdgeTable, SolveData, Solver
+
+
+def strip_rows(d0: int, world: int, rank: int):
+    """Balanced contiguous partition of [0, d0) into `world` strips."""
+    return (d0 * rank) // world, (d0 * (rank + 1)) // world
+
+
+@dataclass
+class Layout:
+    d0: int              # axis-0 extent of the grid domain
+    S: int               # elements per axis-0 row
+    unknown_ch: List[int]
+    array_ch: List[int]
+    halo: int
+
+
+def layout(plan: CompiledPlan) -> Layout:
+    info = planinfo.parse(plan.text)
+    dims = dict(info.dims)
+    dims.update(plan.dims)
+    names = list(info.dims.keys())
+
+    def shape(dd):
+        return [dims[names[i]] for i in dd]
+
+    doms = [tuple(f[2]) for f in info.fields["U"] + info.fields["A"] + info.fields["C"]]
+    if not doms or len(set(doms)) != 1:
+        raise ValueError("strip sharding needs every field on one grid domain")
+    shp = shape(doms[0])
+    h = ctypes.c_int()
+    call("mo_plan_halo_rows", plan._h, ctypes.byref(h))
+    return Layout(shp[0], int(np.prod(shp[1:])) if len(shp) > 1 else 1,
+                  [f[1] for f in info.fields["U"]], [f[1] for f in info.fields["A"]], h.value)
+
+
+def _rows_of(vec, d0, row_elems, lo, hi):
+    return vec.reshape(d0, row_elems)[lo:hi].reshape(-1)
+
+
+def local_data(plan: CompiledPlan, data: SolveData, row0: int, row1: int) -> SolveData:
+    """The strip's SolveData: rows [lo, hi) of every field (halos included)."""
+    L = layout(plan)
+    lo, hi = max(0, row0 - L.halo), min(L.d0, row1 + L.halo)
+    x, off, parts = np.asarray(data.x), 0, []
+    for C in L.unknown_ch:
+        n = L.d0 * L.S * C
+        parts.append(_rows_of(x[off:off + n], L.d0, L.S * C, lo, hi))
+        off += n
+    arrays = [_rows_of(np.asarray(a), L.d0, L.S * C, lo, hi) for a, C in zip(data.arrays, L.array_ch)]
+    return SolveData(x=np.concatenate(parts) if parts else x[:0], arrays=arrays, params=list(data.params),
+                     graphs=[EdgeTable(g.arity, g.verts) for g in data.graphs])
+
+
+def owned_x(plan: CompiledPlan, xloc: np.ndarray, row0: int, row1: int) -> List[np.ndarray]:
+    """Per unknown field, the strip's owned rows of its local x."""
+    L = layout(plan)
+    lo, hi = max(0, row0 - L.halo), min(L.d0, row1 + L.halo)
+    out, off = [], 0
+    for C in L.unknown_ch:
+        n = (hi - lo) * L.S * C
+        out.append(xloc[off:off + n].reshape(hi - lo, L.S * C)[row0 - lo:row1 - lo].reshape(-1))
+        off += n
+    return out
+
+
+def assemble_x(plan: CompiledPlan, owned: List[List[np.ndarray]]) -> np.ndarray:
+    """Global x (reference column layout) from every strip's owned rows (rank order)."""
+    L = layout(plan)
+    return np.concatenate([np.concatenate([o[f] for o in owned]) for f in range(len(L.unknown_ch))])
+
+
+class LocalShardGroup:
+    """`world` strip sessions of one plan on one GPU, driven from one host
+    thread each (the LocalComm transport): the single-device fake that tests
+    the exact partition / halo / reduction schedule the NCCL path runs."""
+
+    def __init__(self, plan: CompiledPlan, data: SolveData, world: int, device: int = 0):
+        self.plan, self.world = plan, world
+        L = layout(plan)
+        self._w = ctypes.c_void_p()
+        call("mo_world_create_local", int(world), int(device), ctypes.byref(self._w))
+        self.comms, self.rows = [], []
+        for r in range(world):
+            c = ctypes.c_void_p()
+            call("mo_comm_create_local", self._w, r, ctypes.byref(c))
+            self.comms.append(c)
+            self.rows.append(strip_rows(L.d0, world, r))
+        # Construction refreshes (collective halo exchanges): one thread per strip.
+        self.solvers = list(range(world))
+        self.solvers = self._parallel(
+            lambda r: Solver(plan, local_data(plan, data, *self.rows[r]), device, comm=self.comms[r], rows=self.rows[r]))
+
+    def _parallel(self, fn):
+        out, err = [None] * self.world, []
+
+        def run(r):
+            try:
+                out[r] = fn(self.solvers[r])  # (ints during construction)
+            except Exception as e:  # pragma: no cover - surfaced below
+                err.append(e)
+
+        ts = [threading.Thread(target=run, args=(r,)) for r in range(self.world)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        if err:
+            raise err[0]
+        return out
+
+    def solve(self):
+        return self._parallel(lambda s: s.solve())
+
+    def cost(self):
+        return self._parallel(lambda s: s.cost())
+
+    def gather_x(self):
+        return assemble_x(self.plan, [owned_x(self.plan, s.get_x(), *rw) for s, rw in zip(self.solvers, self.rows)])
+
+    def close(self):
+        for s in self.solvers:
+            s.__del__()
+        self.solvers = []
+        for c in self.comms:
+            lib.mo_comm_destroy(c)
+        self.comms = []
+        if self._w:
+            lib.mo_world_destroy(self._w)
+            self._w = None
+
+    def __del__(self):
+        if getattr(self, "_w", None):
+            self.close()
+
+
+class ShardedSolver:
+    """One strip per process (torchrun, one GPU per rank): the NCCL unique id
+    is broadcast with torch.distributed, halos and partials then travel over
+    NCCL on the session's stream."""
+
+    def __init__(self, plan: CompiledPlan, data: SolveData, rank: int, world: int, device: int):
+        import torch.distributed as dist
+        self.plan, self.rank, self.world = plan, rank, world
+        L = layout(plan)
+        uid = (ctypes.c_char * 128)()
+        if rank == 0:
+            call("mo_nccl_unique_id", uid, 128)
+        box = [bytes(uid)]
+        dist.broadcast_object_list(box, src=0)
+        uid = (ctypes.c_char * 128).from_buffer_copy(box[0])
+        self._c = ctypes.c_void_p()
+        call("mo_comm_create_nccl", uid, 128, rank, world, device, ctypes.byref(self._c))
+        self.rows = strip_rows(L.d0, world, rank)
+        self.solver = Solver(plan, local_data(plan, data, *self.rows), device, comm=self._c, rows=self.rows)
+
+    def solve(self):
+        return self.solver.solve()
+
+    def gather_x(self):
+        import torch.distributed as dist
+        mine = owned_x(self.plan, self.solver.get_x(), *self.rows)
+        allp = [None] * self.world
+        dist.all_gather_object(allp, mine)
+        return assemble_x(self.plan, allp)

@@ -138,6 +138,8 @@ class CompiledPlan:
         b = text.encode()
         call("mo_plan_parse", b, len(b), ctypes.byref(h))
         self._h = h
+        self.text = text
+        self.dims = dict(dims or {})
         self.exact = bool(exact)
         if exact:
             call("mo_plan_set_exact", self._h, 1)
@@ -205,12 +207,19 @@ def _as(a, dtype):
 class Solver:
     """minopt::Solver<Real> (solver.hpp:80-635) over the device session."""
 
-    def __init__(self, plan_: CompiledPlan, data: SolveData, device: int = 0):
+    def __init__(self, plan_: CompiledPlan, data: SolveData, device: int = 0, comm=None, rows=None):
+        """comm/rows: strip shard owning axis-0 rows [rows[0], rows[1]) of the
+        plan's grid domain (see sharded.py); `data` is then the strip's LOCAL
+        data (its stored rows [lo, hi), halos included)."""
         self.plan = plan_
         self.data = data
         self.dtype = plan_.real_dtype
+        self._comm = comm
         h = ctypes.c_void_p()
-        call("mo_session_create", plan_._h, int(device), ctypes.byref(h))
+        if comm is None:
+            call("mo_session_create", plan_._h, int(device), ctypes.byref(h))
+        else:
+            call("mo_session_create_shard", plan_._h, int(device), comm, int(rows[0]), int(rows[1]), ctypes.byref(h))
         self._h = h
         self._bind_all()
         call("mo_refresh", self._h)

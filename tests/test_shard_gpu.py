@@ -1,0 +1,69 @@
+"""Strip sharding on one GPU (the single-device multi-strip fake of SURVEY.md
+§4/§8e): N strip sessions exchange halos and gather partials through the
+LocalComm transport, running exactly the schedule the NCCL path runs.  The
+sharded solve must reproduce the unsharded one (fixed PCG iterations); only
+the summation order of the dot products differs."""
+import numpy as np
+import pytest
+
+from paper_1604_06525_b200 import Method, Precision, SolveConfig, Solver, load_plan, workloads
+from paper_1604_06525_b200.sharded import LocalShardGroup
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    "poisson": (lambda: workloads.poisson(40, 24), "gn"),
+    "arap_warp": (lambda: workloads.arap_warp(48, 20, nhandles=6), "gn"),
+    "sfs": (lambda: workloads.sfs(36, 20), "lm"),
+}
+
+
+def cfg(method, prec):
+    return SolveConfig(method=Method.kLevenbergMarquardt if method == "lm" else Method.kGaussNewton,
+                       precision=Precision.kF64 if prec == "f64" else Precision.kF32,
+                       nonlinear_iters=3, linear_iters=8, pcg_rel_tol=0.0)
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("name", list(CASES))
+def test_strips_match_unsharded(name, world, prec):
+    make, method = CASES[name]
+    prob = make()
+    dt = np.float64 if prec == "f64" else np.float32
+    c = cfg(method, prec)
+    ref_data = prob.data(dt)
+    ref = Solver(load_plan(prob.name, c, prob.dims), ref_data).solve()
+
+    g = LocalShardGroup(load_plan(prob.name, c, prob.dims), prob.data(dt), world)
+    try:
+        results = g.solve()
+        x = g.gather_x()
+    finally:
+        g.close()
+    tol = 1e-9 if prec == "f64" else 2e-4
+    for r in results:  # every strip takes the same steps
+        assert [t.accepted for t in r.trace] == [t.accepted for t in ref.trace]
+        assert [t.pcg_iters for t in r.trace] == [t.pcg_iters for t in ref.trace]
+        for a, b in zip(r.trace, ref.trace):
+            assert abs(a.cost - b.cost) <= tol * abs(b.cost), (a.cost, b.cost)
+        assert abs(r.final_cost - ref.final_cost) <= tol * abs(ref.final_cost)
+        assert r.unconstrained == ref.unconstrained
+    scale = np.max(np.abs(ref_data.x))
+    np.testing.assert_allclose(x, ref_data.x, rtol=tol * 10, atol=tol * 10 * scale)
+
+
+def test_single_strip_equals_unsharded_bitwise():
+    """world=1: the shard path with no neighbours is the unsharded algorithm."""
+    prob = workloads.poisson(32, 16)
+    c = cfg("gn", "f64")
+    ref_data = prob.data(np.float64)
+    ref = Solver(load_plan(prob.name, c, prob.dims), ref_data).solve()
+    g = LocalShardGroup(load_plan(prob.name, c, prob.dims), prob.data(np.float64), 1)
+    try:
+        r = g.solve()[0]
+        x = g.gather_x()
+    finally:
+        g.close()
+    assert [t.cost for t in r.trace] == [t.cost for t in ref.trace]
+    np.testing.assert_array_equal(x, ref_data.x)
