@@ -53,6 +53,35 @@ def test_strips_match_unsharded(name, world, prec):
     np.testing.assert_allclose(x, ref_data.x, rtol=tol * 10, atol=tol * 10 * scale)
 
 
+def test_nccl_transport_world1():
+    """The NCCL transport (dlopen'ed libnccl, unique id via torch.distributed,
+    all-gather on the session stream) on the one GPU available: world 1."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_1604_06525_b200.sharded import ShardedSolver
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        prob = workloads.poisson(32, 16)
+        c = cfg("gn", "f64")
+        ref_data = prob.data(np.float64)
+        ref = Solver(load_plan(prob.name, c, prob.dims), ref_data).solve()
+        sh = ShardedSolver(load_plan(prob.name, c, prob.dims), prob.data(np.float64), 0, 1, 0)
+        r = sh.solve()
+        x = sh.gather_x()
+        assert [t.cost for t in r.trace] == [t.cost for t in ref.trace]
+        np.testing.assert_array_equal(x, ref_data.x)
+    finally:
+        dist.destroy_process_group()
+
+
 def test_single_strip_equals_unsharded_bitwise():
     """world=1: the shard path with no neighbours is the unsharded algorithm."""
     prob = workloads.poisson(32, 16)
