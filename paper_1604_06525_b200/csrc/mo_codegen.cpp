@@ -564,6 +564,61 @@ struct Gen {
   // One thread per hyperedge (exec.hpp:223-309); scatter outputs go to a
   // per-edge contribution buffer that the deterministic vertex gather folds
   // in edge order (mo_kernels.cu: mo_graph_gather).
+  // Deterministic vertex-centric scatter (replaces exec_graph's sequential
+  // `+=` / parallel atomics, exec.hpp:265-282): one thread per target vertex
+  // v re-evaluates the edge program of every incident edge (CSR, ascending
+  // edge order) and accumulates, in registers, the outputs whose slot is v.
+  // Per column that is the grid-written value followed by the edges in order
+  // and the outputs in program order: the reference's sequential order.
+  void vertex_kernel(const GraphSet& g, const Domain& dom, const std::string& pn, const std::string& kn, int arity,
+                     bool bm) {
+    const size_t K = g.scats.size();
+    const size_t NO = bm ? 2 * K : K;
+    struct Col {
+      int vec, f, ch;
+    };
+    std::vector<Col> cols;
+    std::vector<int> cidx(NO, -1);
+    for (size_t o = 0; o < NO; ++o) {
+      const Scat& sc = g.scats[bm ? o / 2 : o];
+      if (!(P.unknowns[size_t(sc.field)].dom == dom)) continue;
+      Col c{bm ? int(o % 2) : 0, sc.field, sc.channel};
+      int k = -1;
+      for (size_t j = 0; j < cols.size(); ++j)
+        if (cols[j].vec == c.vec && cols[j].f == c.f && cols[j].ch == c.ch) k = int(j);
+      if (k < 0) {
+        k = int(cols.size());
+        cols.push_back(c);
+      }
+      cidx[o] = k;
+    }
+    os << kbegin(kn) << "  if ((P.flags & MO_F_SKIPDONE) && P.state->done) return;\n"
+       << "  bool bad = false;\n"
+       << "  Real* D0 = (Real*)P.out0; Real* D1 = (Real*)P.out1; (void)D1;\n"
+       << "  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < P.nverts;"
+          " v += (long long)gridDim.x * blockDim.x) {\n";
+    auto colexpr = [&](const Col& c) {
+      return std::string(c.vec ? "D1" : "D0") + "[P.ubase[" + std::to_string(c.f) + "] + v * " +
+             std::to_string(P.unknowns[size_t(c.f)].channels) + " + " + std::to_string(c.ch) + "]";
+    };
+    for (size_t j = 0; j < cols.size(); ++j) os << "    Real a" << j << " = " << colexpr(cols[j]) << ";\n";
+    os << "    const int j1 = P.vptr[v + 1];\n"
+       << "    for (int j = P.vptr[v]; j < j1; ++j) {\n"
+       << "      const long long e = P.vedge[j];\n"
+       << "      int vs[" << (arity ? arity : 1) << "];\n";
+    for (int s2 = 0; s2 < arity; ++s2) os << "      vs[" << s2 << "] = P.verts[e * " << arity << " + " << s2 << "];\n";
+    os << "      Real o[" << (NO ? NO : 1) << "];\n      " << pn << "<false>(P, 0, 0, 0, 0, vs, o);\n";
+    for (size_t o = 0; o < NO; ++o) {
+      os << "      if (!mo_finite((double)o[" << o << "])) bad = true;\n";
+      if (cidx[o] < 0) continue;
+      const Scat& sc = g.scats[bm ? o / 2 : o];
+      os << "      if (vs[" << sc.slot << "] == (int)v) a" << cidx[o] << " += o[" << o << "];\n";
+    }
+    os << "    }\n";
+    for (size_t j = 0; j < cols.size(); ++j) os << "    " << colexpr(cols[j]) << " = a" << j << ";\n";
+    os << "  }\n  if (bad) atomicOr(&P.state->nonfinite_kernel, 1);\n}\n";
+  }
+
   void graph_kernel(const std::string& pn, const std::string& kn, size_t nout, int arity, int mode) {
     // mode 0 = cost (reduce), 1 = evalf (row writes), 2 = contributions
     os << kbegin(kn) << "  if ((P.flags & MO_F_SKIPDONE) && P.state->done) return;\n"
@@ -607,6 +662,19 @@ struct Gen {
       graph_kernel(program(g.evalf, true), "mo_graph_evalf_" + s, g.evalf.outputs.size(), ar, 1);
       graph_kernel(program(g.bm, true), "mo_graph_bm_" + s, g.bm.outputs.size(), ar, 2);
       graph_kernel(program(g.jtj, true), "mo_graph_jtj_" + s, g.jtj.outputs.size(), ar, 2);
+      // Vertex-centric recompute kernels, one per scatter-target domain (in
+      // the session's GatherDom order: first appearance over the scats).
+      std::vector<Domain> doms;
+      for (const Scat& sc : g.scats) {
+        const Domain& d = P.unknowns[size_t(sc.field)].dom;
+        if (std::find(doms.begin(), doms.end(), d) == doms.end()) doms.push_back(d);
+      }
+      const std::string pj = program(g.jtj, true), pb = program(g.bm, true);
+      for (size_t di = 0; di < doms.size(); ++di) {
+        vertex_kernel(g, doms[di], pj, "mo_graph_vjtj_" + s + "_" + std::to_string(di), ar, false);
+        vertex_kernel(g, doms[di], pb, "mo_graph_vbm_" + s + "_" + std::to_string(di), ar, true);
+      }
+      info.vertex_kernels.push_back(true);
     }
     for (size_t i = 0; i < P.computed_kernels.size(); ++i) {
       const ComputedKernel& ck = P.computed_kernels[i];

@@ -16,6 +16,7 @@ struct ModuleInfo {
     int nlanes = 0, halo = 0;
   };
   std::vector<TwoPhase> jtj2;  // per gather set
+  std::vector<bool> vertex_kernels;  // per graph set: mo_graph_v{jtj,bm}_<g>_<dom> exist
 };
 
 // Full NVRTC translation unit for one plan and precision.  `prelude` is the

@@ -88,6 +88,9 @@ struct mo_kparams {
   const int* verts;              // graph: int32 vertex table, edge-major
   int arity;
   long long nedges;
+  const int* vptr;               // graph vertex kernels: incident-edge CSR of one domain
+  const int* vedge;
+  long long nverts;
   mo_red red;
   mo_state* state;
 };

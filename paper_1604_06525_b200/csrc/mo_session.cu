@@ -985,6 +985,29 @@ class Session final : public SessionBase {
     return R;
   }
 
+  // Vertex-centric recompute kernels (generated per scatter-target domain).
+  bool vertex_path(size_t gi) const {
+    static const bool off = std::getenv("MO_B200_EDGE_SCATTER") != nullptr;
+    return !off && gi < minfo_.vertex_kernels.size() && minfo_.vertex_kernels[gi];
+  }
+  void launch_vertex(const char* prefix, int gi, mo_kparams kp, Real* dst0, Real* dst1) {
+    GSet& gs = gsets_[size_t(gi)];
+    for (size_t di = 0; di < gs.doms.size(); ++di) {
+      const GatherDom& gd = gs.doms[di];
+      kp.out0 = dst0;
+      kp.out1 = dst1;
+      kp.vptr = gd.vptr;
+      kp.vedge = gd.vedge;
+      kp.nverts = gd.nverts;
+      const std::string name = prefix + std::to_string(gi) + "_" + std::to_string(di);
+      const void* f = mod_.kernel(name);
+      long long g = std::min<long long>((gd.nverts + MO_THREADS - 1) / MO_THREADS, (long long)nsm_ * occupancy(f));
+      void* args[] = {&kp};
+      CK(cudaLaunchKernel(f, dim3(unsigned(std::max<long long>(g, 1))), dim3(MO_THREADS), args, 0, st_));
+      ++launches_;
+    }
+  }
+
   void gather_graph(int gi, bool bm, Real* dst0, Real* dst1) {
     const GraphSet& g = P_.graph_sets[size_t(gi)];
     GSet& gs = gsets_[size_t(gi)];
@@ -1057,6 +1080,10 @@ class Session final : public SessionBase {
     if (!fused) {
       for (size_t i = 0; i < P_.graph_sets.size(); ++i) {
         mo_kparams kp = kp_graph(int(i), x_, nullptr);
+        if (vertex_path(i)) {
+          launch_vertex("mo_graph_vbm_", int(i), kp, b_, m_);
+          continue;
+        }
         kp.out0 = gsets_[i].contrib;
         launch_edges("mo_graph_bm_" + std::to_string(i), int(i), kp);
         gather_graph(int(i), true, b_, m_);
@@ -1105,8 +1132,12 @@ class Session final : public SessionBase {
     if (!fused) {
       for (size_t i = 0; i < P_.graph_sets.size(); ++i) {
         mo_kparams kp = kp_graph(int(i), x_, pv);
-        kp.out0 = gsets_[i].contrib;
         kp.flags = flags & MO_F_SKIPDONE;
+        if (vertex_path(i)) {
+          launch_vertex("mo_graph_vjtj_", int(i), kp, out, nullptr);
+          continue;
+        }
+        kp.out0 = gsets_[i].contrib;
         launch_edges("mo_graph_jtj_" + std::to_string(i), int(i), kp);
         gather_graph(int(i), false, out, nullptr);
       }
