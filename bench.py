@@ -293,7 +293,8 @@ def run_ours(args):
                    "final_cost": r.final_cost},
         "roofline": {"bound": "hbm", "kernel": "J^T J p apply (generated gather_jtj, fused p'Ap)",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": (achieved / peak) if achieved else None, "traffic": ncu_traffic(prob.name),
+                     "frac": (achieved / peak) if achieved else None,
+                     "traffic": ncu_traffic(prob.name + (f"_{args.size}" if args.size else "")) if world == 1 else None,
                      "alg_bytes_per_launch": alg, "alg_bytes_per_elem": per_elem,
                      "avg_launch_us": avg_apply * 1e3, "launches": apply_n,
                      "pcg_update_avg_us": upd_ms / max(upd_n, 1) * 1e3},

@@ -503,7 +503,15 @@ struct Gen {
     for (int s = 0; s < NM; ++s) os << "  CL[" << s * NE << " + k] = m" << s << ";\n";
     os << "}\n";
     const std::string kn = "mo_gather_jtj2_" + sfx;
-    os << "extern \"C\" __global__ void __launch_bounds__(MO_THREADS) " << kn
+    // Occupancy knob (blocks/SM the register allocator must allow) and
+    // phase-1 unroll; MO_B200_JTJ2_MINB / MO_B200_JTJ2_UNROLL override.
+    const char* mb = std::getenv("MO_B200_JTJ2_MINB");
+    const char* ur = std::getenv("MO_B200_JTJ2_UNROLL");
+    // Measured on B200 (ARAP 1024^2/8192^2, Poisson 8192^2, SFS): 5 resident
+    // blocks (<= 48 registers) is the best single setting; unrolling hurts.
+    const int minb = mb ? std::atoi(mb) : 5, unroll = ur ? std::atoi(ur) : 1;
+    os << "extern \"C\" __global__ void __launch_bounds__(MO_THREADS" << (minb > 0 ? ", " + std::to_string(minb) : "")
+       << ") " << kn
        << "(const __grid_constant__ mo_kparams P) {\n"
        << "  if ((P.flags & MO_F_SKIPDONE) && P.state->done) return;\n"
        << "  extern __shared__ __align__(16) unsigned char mo_smem[];\n"
@@ -515,10 +523,11 @@ struct Gen {
        << "  for (int t = blockIdx.x; t < nt; t += gridDim.x) {\n"
        << "    const mo_tile T = mo_tile_at(P, t);\n"
        << "    const bool it = mo_tile_in(P, T, " << R << ");\n";
+    const std::string pragma = unroll > 1 ? "    #pragma unroll " + std::to_string(unroll) + "\n" : "";
     if (nd == 2)
       os << "    const int r0 = T.o0 - " << H << ", c0 = T.o1 - " << H
          << ";\n"
-         << "    for (int k = tid; k < " << NE << "; k += MO_THREADS) {\n"
+         << pragma << "    for (int k = tid; k < " << NE << "; k += MO_THREADS) {\n"
          << "      const int q0 = r0 + k / " << WX << ", q1 = c0 + k % " << WX << ";\n";
     else
       os << "    const int r0 = T.o0 - " << H << ", c0 = 0; (void)c0;\n"

@@ -18,7 +18,9 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
+#include <mutex>
 #include <limits>
 #include <string>
 
@@ -83,6 +85,7 @@ class Session final : public SessionBase {
 
     // JIT the plan's per-element kernels (plan time; cached on disk).
     std::string src = generate_module(P_, sizeof(Real) == 8, device_prelude(), &minfo_);
+    module_key_ = std::to_string(std::hash<std::string>()(src)) + (P_.exact ? "/exact" : "/fma");
     mod_.load(compile_cubin(src, "mo_plan.cu", P_.exact));
 
     const size_t n = size_t(P_.num_cols);
@@ -337,6 +340,7 @@ class Session final : public SessionBase {
 
   void apply_jtj(const void* v, void* out, int64_t n, bool device) override {
     ensure_refreshed();
+    tune_apply();
     check(n == P_.num_cols, Err::kShapeMismatch, "apply_jtj(): vector size mismatch");
     if (device) {
       apply(static_cast<const Real*>(v), static_cast<Real*>(out), 0);
@@ -377,6 +381,11 @@ class Session final : public SessionBase {
       res.unconstrained = unconstrained_;
     };
 
+    refresh_host();
+    if (!tuned_) {
+      refresh_device();  // bound data in place for the timing runs
+      tune_apply();
+    }
     for (int it = 0; it < cfg_.nonlinear_iters; ++it) {
       refresh_host();
       if (!lm) {
@@ -958,7 +967,69 @@ class Session final : public SessionBase {
   }
   // Fast-path apply kernel of gather set i: the two-phase evalj kernel unless
   // the plan asked for exact (reference-program) execution.
-  bool two_phase(size_t i) const { return !P_.exact && i < minfo_.jtj2.size() && minfo_.jtj2[i].ok; }
+  bool two_phase(size_t i) const {
+    if (P_.exact || i >= minfo_.jtj2.size() || !minfo_.jtj2[i].ok) return false;
+    return i >= jtj_choice_.size() || jtj_choice_[i] != 0;
+  }
+  // First use: time the gather-program kernel against the two-phase kernel
+  // on the bound data and keep the faster per gather set (cheap programs such
+  // as Poisson's can win without shared memory, barriers or halo recompute).
+  // MO_B200_JTJ=gather|twophase forces a choice.
+  void tune_apply() {
+    if (tuned_) return;
+    tuned_ = true;
+    // One decision per (module, shape) per process, so every session of a plan
+    // runs the same kernel (bitwise run-to-run reproducibility).
+    static std::mutex mu;
+    static std::map<std::string, std::vector<int>> cache;
+    std::string key = module_key_;
+    for (auto& d : P_.dims) key += "/" + std::to_string(d.second);
+    key += sh_.on ? "/s" + std::to_string(sh_.row1 - sh_.row0) : "";
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      auto it = cache.find(key);
+      if (it != cache.end()) {
+        jtj_choice_ = it->second;
+        return;
+      }
+    }
+    jtj_choice_.assign(P_.gather_sets.size(), 1);
+    const char* force = std::getenv("MO_B200_JTJ");
+    for (size_t i = 0; i < P_.gather_sets.size(); ++i) {
+      if (P_.exact || i >= minfo_.jtj2.size() || !minfo_.jtj2[i].ok) continue;
+      if (force) {
+        jtj_choice_[i] = std::string(force) == "gather" ? 0 : 1;
+        continue;
+      }
+      float best[2] = {0, 0};
+      cudaEvent_t a, b;
+      CK(cudaEventCreate(&a));
+      CK(cudaEventCreate(&b));
+      for (int v = 0; v < 2; ++v) {
+        const std::string name = (v ? "mo_gather_jtj2_" : "mo_gather_jtj_") + std::to_string(i);
+        const size_t smem = v ? minfo_.jtj2[i].smem : 0;
+        mo_kparams kp = kp_grid(P_.gather_sets[i].dom, x_, x_);
+        kp.out0 = otmp_;
+        kp.in0 = x_;
+        kp.in1 = damp_;
+        const int grid = grid_blocks(name, P_.gather_sets[i].dom, smem);
+        for (int rep = 0; rep < 4; ++rep) {
+          if (rep == 1) CK(cudaEventRecord(a, st_));
+          launch_grid(name, P_.gather_sets[i].dom, kp, grid, smem);
+        }
+        CK(cudaEventRecord(b, st_));
+        CK(cudaEventSynchronize(b));
+        CK(cudaEventElapsedTime(&best[v], a, b));
+        launches_ -= 4;
+      }
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+      // Keep the two-phase kernel unless the gather kernel is clearly faster.
+      jtj_choice_[i] = best[0] < 0.9f * best[1] ? 0 : 1;
+    }
+    std::lock_guard<std::mutex> lk(mu);
+    cache[key] = jtj_choice_;
+  }
   std::string jtj_kernel(size_t i) const {
     return (two_phase(i) ? "mo_gather_jtj2_" : "mo_gather_jtj_") + std::to_string(i);
   }
@@ -1297,6 +1368,9 @@ class Session final : public SessionBase {
   std::map<const void*, int> occ_;
   ModuleInfo minfo_;
   std::map<int, cudaGraphExec_t> stage_exec_;
+  bool tuned_ = false;
+  std::vector<int> jtj_choice_;  // per gather set: 0 gather program, 1 two-phase
+  std::string module_key_;
   std::map<int, int64_t> stage_nodes_;
   std::vector<void*> owned_;
   int64_t launches_ = 0;
