@@ -207,9 +207,18 @@ def run_ours(args):
     def restore():
         call("mo_bind_x_device", s._h, ctypes.c_void_p(x0.data_ptr()), n)
 
+    from paper_1604_06525_b200 import _lib
+
+    def solve_resident():
+        # mo_solve alone: x stays in HBM (Solver.solve() would also download
+        # x into data.x, which belongs to the e2e measurement, not `value`).
+        res = _lib.SolveResultC()
+        call("mo_solve", s._h, _lib.ITER_CB(), None, ctypes.byref(res))
+        return res
+
     for _ in range(args.warmup):
         restore()
-        s.solve()
+        solve_resident()
 
     launches0 = s.kernel_launches()
     times = []
@@ -223,7 +232,7 @@ def run_ours(args):
                 flush.zero_()  # L2 flush between timed steps
                 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 ev0.record(st)
-            r = s.solve()
+            r = solve_resident()
             ev1.record(st)
             ev1.synchronize()
             times.append(ev0.elapsed_time(ev1))
@@ -240,11 +249,11 @@ def run_ours(args):
     # (event nodes inside the captured graphs), kept out of the headline timing.
     s.set_profiling(True)
     restore()
-    s.solve()  # capture the profiled graphs
+    solve_resident()  # capture the profiled graphs
     s.profile_reset()
     for _ in range(max(2, args.steps)):
         restore()
-        s.solve()
+        solve_resident()
     torch.cuda.synchronize()
     apply_ms, apply_n = s.profile(0)
     upd_ms, upd_n = s.profile(1)
@@ -261,7 +270,7 @@ def run_ours(args):
         call("mo_bind_x", s._h, ctypes.c_void_p(pin_x.data_ptr()), n)
         for i, a in enumerate(pin_arr):
             call("mo_bind_array", s._h, i, ctypes.c_void_p(a.data_ptr()), a.numel())
-        s.solve()
+        solve_resident()  # the C-ABI call; x comes back through mo_get_x below
         call("mo_get_x", s._h, ctypes.c_void_p(pin_out.data_ptr()), n)
         e2e.append((time.perf_counter() - t0) * 1e3)
     h2d = int(pin_x.numel() * pin_x.element_size() + sum(a.numel() * a.element_size() for a in pin_arr))

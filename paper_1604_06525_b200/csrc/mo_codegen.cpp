@@ -42,6 +42,14 @@ std::string hexd(double v) {
 }
 
 struct Gen {
+  // Merged-lane (field, channel, o0, o1) and lane lists shared by the
+  // two-phase apply generators.
+  struct MLane {
+    int f, c, o0, o1;
+  };
+  struct LaneG {
+    int t, out, f, c, o0, o1;
+  };
   const Plan& P;
   bool f64;
   std::ostringstream os;
@@ -89,22 +97,53 @@ struct Gen {
   // then drops the guards and can hoist every load (same values, bit for bit).
   const Domain* iter_dom = nullptr;
   int reach = 0;
-  std::string program(const Program& pg, bool graph, const Domain* dom = nullptr) {
-    std::string name = "mo_prog_" + std::to_string(nprog++);
-    iter_dom = graph ? nullptr : dom;
-    reach = 0;
+  // Shared-memory staged fields (TMA apply): slot -> (byte offset of the
+  // field's row ring in dynamic smem, channels).  In sm_mode, reads of these
+  // fields come from the ring: row ri[o0 + st_rx], column lx + o1.
+  bool sm_mode = false;
+  int st_rx = 0, st_win = 0;
+  std::vector<std::pair<int, std::pair<long long, int>>> staged;
+  const std::pair<long long, int>* staged_of(int sl) const {
+    for (auto& x : staged)
+      if (x.first == sl) return &x.second;
+    return nullptr;
+  }
+  int reach_of(const Program& pg, const Domain* dom) {
+    int r = 0;
     for (const Instr& in : pg.instrs) {
       bool counts = in.op == kInB;
       if ((in.op == kLoadU || in.op == kLoadA || in.op == kLoadC || in.op == kLoadP) && !in.graph)
-        counts = iter_dom && field_of(in.op, in.field).dom == *iter_dom;
+        counts = dom && field_of(in.op, in.field).dom == *dom;
       if (counts)
-        for (int a = 0; a < 3; ++a) reach = std::max(reach, std::abs(int(in.off[a])));
+        for (int a = 0; a < 3; ++a) r = std::max(r, std::abs(int(in.off[a])));
     }
-    os << "template <bool I> __device__ __forceinline__ void " << name
-       << "(const mo_kparams& P, int p0, int p1, int p2, int eb, const int* vs, Real* out) {\n";
-    os << "  (void)P; (void)p0; (void)p1; (void)p2; (void)eb; (void)vs;\n"
-       << "  const int ms0 = P.dnd == 3 ? P.d1 * P.d2 : (P.dnd == 2 ? P.d1 : 1), ms1 = P.dnd == 3 ? P.d2 : 1;\n"
-       << "  (void)ms0; (void)ms1;\n";
+    return r;
+  }
+  static constexpr int MO_MAX_TMAPS_HOST = 12;  // = MO_MAX_TMAPS (mo_device.cuh)
+  std::string program(const Program& pg, bool graph, const Domain* dom = nullptr, bool sm = false) {
+    std::string name = "mo_prog_" + std::to_string(nprog++);
+    iter_dom = graph ? nullptr : dom;
+    sm_mode = sm && !graph;
+    reach = reach_of(pg, iter_dom);
+    if (sm_mode)
+      os << "template <bool I> __device__ __forceinline__ void " << name
+         << "(const mo_kparams& P, int p0, int p1, int p2, const int* ri, int lx, Real* out) {\n"
+         << "  (void)P; (void)p0; (void)p1; (void)p2; (void)ri; (void)lx; const int eb = 0; (void)eb;\n";
+    else
+      os << "template <bool I> __device__ __forceinline__ void " << name
+         << "(const mo_kparams& P, int p0, int p1, int p2, int eb, const int* vs, Real* out) {\n"
+         << "  (void)P; (void)p0; (void)p1; (void)p2; (void)eb; (void)vs;\n";
+    if (iter_dom) {
+      // Strides of the iteration domain are plan constants (the plan fixes the
+      // global dims), so every interior stencil read is base + immediate.
+      const auto sh = P.shape_of(*iter_dom);
+      const size_t nd = iter_dom->dims.size();
+      const long long m0 = nd == 3 ? sh[1] * sh[2] : (nd == 2 ? sh[1] : 1), m1 = nd == 3 ? sh[2] : 1;
+      os << "  constexpr int ms0 = " << m0 << ", ms1 = " << m1 << ";\n  (void)ms0; (void)ms1;\n";
+    } else {
+      os << "  const int ms0 = P.dnd == 3 ? P.d1 * P.d2 : (P.dnd == 2 ? P.d1 : 1), ms1 = P.dnd == 3 ? P.d2 : 1;\n"
+         << "  (void)ms0; (void)ms1;\n";
+    }
     {
       std::vector<std::pair<int, int>> slots;
       for (const Instr& in : pg.instrs) {
@@ -114,7 +153,7 @@ struct Gen {
         std::pair<int, int> sc{slot_of(in.op, in.field), f.channels};
         if (std::find(slots.begin(), slots.end(), sc) == slots.end()) slots.push_back(sc);
       }
-      os << ldi_bases(slots);
+      if (!sm_mode) os << ldi_bases(slots);
     }
     for (uint32_t r = 0; r < pg.num_regs; ++r) os << "  Real r" << r << " = (Real)0;\n";
     for (const Block& b : pg.blocks) {
@@ -167,6 +206,15 @@ struct Gen {
       << ")";
     return s.str();
   }
+  // Staged read: field ring in dynamic smem, row ri[o0 + rx], column lx + o1.
+  std::string smx(int sl, int o0, int o1, int ch) const {
+    const auto* st = staged_of(sl);
+    std::ostringstream s;
+    const int C = st->second;
+    s << "reinterpret_cast<const Real*>(mo_dsm + " << st->first << ")[ri[" << o0 + st_rx << "] * " << st_win * C
+      << " + (lx + (" << o1 << ")) * " << C << " + " << ch << "]";
+    return s.str();
+  }
   // Per-field interior base pointers (field start + eb*C): each stencil load
   // is then base + (row offset) + immediate.
   static std::string ldi_bases(const std::vector<std::pair<int, int>>& slots) {
@@ -191,7 +239,8 @@ struct Gen {
       case kParam:
         check(in.field >= 0 && size_t(in.field) < P.params.size(), Err::kShapeMismatch,
               "kernel reads a parameter that is not declared");
-        s << "(Real)P.params[" << in.field << "]";
+        if (in.field < 16) s << "(Real)P.pv[" << in.field << "]";  // MO_MAX_PARAMS
+        else s << "(Real)P.params[" << in.field << "]";
         break;
       case kIndex:
         if (graph || in.field > 2) s << "(Real)0";  // graph env pix = {0,0,0}
@@ -211,10 +260,14 @@ struct Gen {
         } else {
           int nd = int(f.dom.dims.size());
           const bool same = iter_dom && f.dom == *iter_dom;
-          if (same) s << "(I ? " << ldi(f.channels, sl, in.off[0], in.off[1], in.off[2], in.channel) << " : ";
+          if (same && sm_mode && staged_of(sl)) {
+            s << smx(sl, in.off[0], in.off[1], in.channel);
+            break;
+          }
+          if (same && !sm_mode) s << "(I ? " << ldi(f.channels, sl, in.off[0], in.off[1], in.off[2], in.channel) << " : ";
           s << "mo_ld<Real, " << (nd ? nd : 1) << ", " << f.channels << ", false>(P.v[" << sl << "], p0 + ("
             << in.off[0] << "), p1 + (" << in.off[1] << "), p2 + (" << in.off[2] << "), " << in.channel << ")";
-          if (same) s << ")";
+          if (same && !sm_mode) s << ")";
         }
         break;
       }
@@ -468,8 +521,8 @@ struct Gen {
     const std::string sfx = std::to_string(gi);
     // Phase-1 body for one haloed element k at (p0, p1).
     os << "template <bool I> __device__ __forceinline__ void mo_lanes_" << sfx
-       << "(const mo_kparams& P, int p0, int p1, int k, Real* CL) {\n"
-       << "  const int ms0 = P.dnd == 2 ? P.d1 : 1, ms1 = 1; (void)ms1;\n"
+       << "(const mo_kparams& P, int p0, int p1, int k, Real* CL, int ls) {\n"
+       << "  constexpr int ms0 = " << (nd == 2 ? P.shape_of(g.dom)[1] : 1) << ", ms1 = 1; (void)ms1;\n"
        << "  const int eb = I ? mo_local_elem(P, p0, p1, 0) : 0;\n"
        << "  const bool inside = I || mo_inb(P, p0, p1, 0);\n";
     {
@@ -500,7 +553,7 @@ struct Gen {
       if (origin) os << "    }\n";
       os << "  }\n";
     }
-    for (int s = 0; s < NM; ++s) os << "  CL[" << s * NE << " + k] = m" << s << ";\n";
+    for (int s = 0; s < NM; ++s) os << "  CL[" << s << " * ls + k] = m" << s << ";\n";
     os << "}\n";
     const std::string kn = "mo_gather_jtj2_" + sfx;
     // Occupancy knob (blocks/SM the register allocator must allow) and
@@ -533,8 +586,8 @@ struct Gen {
       os << "    const int r0 = T.o0 - " << H << ", c0 = 0; (void)c0;\n"
          << "    for (int k = tid; k < " << NE << "; k += MO_THREADS) {\n"
          << "      const int q0 = r0 + k, q1 = 0;\n";
-    os << "      if (it) mo_lanes_" << sfx << "<true>(P, q0, q1, k, CL); else mo_lanes_" << sfx
-       << "<false>(P, q0, q1, k, CL);\n"
+    os << "      if (it) mo_lanes_" << sfx << "<true>(P, q0, q1, k, CL, " << NE << "); else mo_lanes_" << sfx
+       << "<false>(P, q0, q1, k, CL, " << NE << ");\n"
        << "    }\n    __syncthreads();\n"
        << "    int p0, p1, p2;\n"
        << "    if (mo_tile_elem(P, T, p0, p1, p2)) {\n"
@@ -566,8 +619,371 @@ struct Gen {
     tp.reach = R;
     tp.nlanes = NM;
     tp.smem = size_t(NM) * size_t(NE) * (f64 ? 8 : 4);
+    if (nd == 2) {
+      gather_jtj3(g, gi, H, std::max(reach, H), NM, merged_off(merged));
+      std::vector<LaneG> lg;
+      for (const L& l : lanes) lg.push_back({l.t, l.out, l.f, l.c, l.o0, l.o1});
+      gather_jtj4(g, gi, *S, lg, lane_slot, merged_off(merged), H);
+    }
     return tp;
   }
+
+  // TMA-staged row-streaming apply (2-D domains): gather_jtj3's band/ring
+  // schedule, with every field the phase-1 body reads (x, arrays, computed on
+  // the iteration domain and p) streamed into shared-memory row rings by TMA
+  // 8 rows at a time, NBUF blocks deep, completion tracked by mbarriers.
+  // Phase 1 then reads only shared memory (immediate offsets, no 64-bit
+  // address arithmetic, no L1TEX misses on its critical path) and the loads
+  // of the next rows overlap the current rows' arithmetic.  TMA zero-fills
+  // out-of-bounds box elements, which is the reference's OOB->0 read rule
+  // (eval.hpp:47-51), so border bands run the same code.
+  void gather_jtj4(const GatherSet& g, int gi, const GridSet& S, const std::vector<LaneG>& lanes,
+                   const std::vector<int>& lane_slot, const std::vector<MLane>& merged, int H) {
+    if (f64_disabled_tma()) return;
+    const std::string sfx = std::to_string(gi);
+    const auto sh = P.shape_of(g.dom);
+    const long long D0 = sh[0], D1 = sh[1];
+    const int BW = 32 - 2 * H;
+    if (BW < 8) return;
+    const int U = int(P.unknowns.size());
+    const int RX = std::max(reach_of(S.evalj, &g.dom), H);
+    if (RX > 4) return;  // two 8-row blocks cover one step's input rows
+    // TMA needs a 16-byte aligned box start: the window starts at the
+    // aligned column cs <= c0 - H - RX (shift sh = c0 - H - RX - cs < AU).
+    const int AU = f64 ? 2 : 4;
+    const int WIN = (32 + 2 * RX + AU - 1 + AU - 1) / AU * AU;
+    const int NBUF = std::getenv("MO_B200_JTJ4_NBUF") ? std::max(3, std::atoi(std::getenv("MO_B200_JTJ4_NBUF"))) : 3;
+    const int NEED = 1 + (2 * RX + 7) / 8;
+    const int RING = 8 + 2 * H;  // two barriers per step
+    const int LS = RING * 32;
+    const int NM = int(merged.size());
+    const int RB = f64 ? 8 : 4;
+    // Staged slots: same-domain fields evalj reads + the lanes' p fields.
+    std::vector<std::pair<int, int>> slots;  // (slot, channels)
+    auto add = [&](int sl, int C) {
+      for (auto& x : slots)
+        if (x.first == sl) return;
+      slots.push_back({sl, C});
+    };
+    for (const Instr& in : S.evalj.instrs) {
+      if (!(in.op == kLoadU || in.op == kLoadA || in.op == kLoadC || in.op == kLoadP) || in.graph) continue;
+      const Field& f = field_of(in.op, in.field);
+      if (f.dom == g.dom) add(slot_of(in.op, in.field), f.channels);
+    }
+    for (const LaneG& l : lanes) add(U + l.f, P.unknowns[size_t(l.f)].channels);
+    if (slots.empty() || int(slots.size()) > MO_MAX_TMAPS_HOST) return;
+    for (auto& x : slots)
+      if (WIN * x.second > 256) return;  // TMA box inner extent limit
+    // Dynamic smem layout: CL ring | field rings (128-B aligned) | mbarriers.
+    long long off = (long long)NM * LS * RB;
+    off = (off + 127) / 128 * 128;
+    staged.clear();
+    long long tx = 0;
+    std::vector<long long> boxbytes;
+    for (auto& x : slots) {
+      staged.push_back({x.first, {off, x.second}});
+      const long long bb = 8LL * WIN * x.second * RB;
+      boxbytes.push_back(bb);
+      tx += bb;
+      off += (long long)NBUF * bb;
+    }
+    const long long mbar_off = off;
+    off += 8LL * NBUF;
+    st_rx = RX;
+    st_win = WIN;
+    const std::string pe = program(S.evalj, false, &g.dom, true);
+    const int NO = int(S.evalj.outputs.size());
+    // Phase-1 body from shared memory.
+    os << "template <bool I> __device__ __forceinline__ void mo_lanes4_" << sfx
+       << "(const mo_kparams& P, int p0, int p1, int k, Real* CL, const int* ri, int lx) {\n"
+       << "  const bool inside = I || mo_inb(P, p0, p1, 0);\n"
+       << "  Real d[" << NO << "];\n  " << pe << "<I>(P, p0, p1, 0, ri, lx, d);\n";
+    for (int si = 0; si < NM; ++si) os << "  Real m" << si << " = (Real)0;\n";
+    for (size_t t = 0; t < S.jtemplates.size(); ++t) {
+      os << "  { Real jp = (Real)0;\n";
+      for (const LaneG& l : lanes)
+        if (l.t == int(t)) os << "    jp += d[" << l.out << "] * " << smx(U + l.f, l.o0, l.o1, l.c) << ";\n";
+      const bool origin = S.jtemplates[t].origin;
+      if (origin) os << "    if (inside) {\n";
+      for (size_t li = 0; li < lanes.size(); ++li)
+        if (lanes[li].t == int(t)) os << "    m" << lane_slot[li] << " += d[" << lanes[li].out << "] * jp;\n";
+      if (origin) os << "    }\n";
+      os << "  }\n";
+    }
+    for (int si = 0; si < NM; ++si) os << "  CL[" << si * LS << " + k] = m" << si << ";\n";
+    os << "}\n";
+    sm_mode = false;
+
+    const std::string kn = "mo_gather_jtj4_" + sfx;
+    const char* mb = std::getenv("MO_B200_JTJ4_MINB");
+    const int minb = mb ? std::atoi(mb) : 4;
+    os << "extern \"C\" __global__ void __launch_bounds__(MO_THREADS" << (minb > 0 ? ", " + std::to_string(minb) : "")
+       << ") " << kn << "(const __grid_constant__ mo_kparams P, const __grid_constant__ mo_tmaps T) {\n"
+       << "  if ((P.flags & MO_F_SKIPDONE) && P.state->done) return;\n"
+       << "  Real* CL = reinterpret_cast<Real*>(mo_dsm);  // [" << NM << " merged lanes][" << RING << " rows][32]\n"
+       << "  unsigned long long* MB = reinterpret_cast<unsigned long long*>(mo_dsm + " << mbar_off << ");\n"
+       << "  double acc = 0; bool bad = false;\n"
+       << "  const int tid = threadIdx.x + threadIdx.y * blockDim.x;\n"
+       << "  const int w = tid >> 5, l = tid & 31;\n"
+       << "  constexpr int NB = " << NB(D1, BW) << ", BW = " << BW << ", H = " << H << ", RX = " << RX << ";\n"
+       << "  constexpr int D0 = " << D0 << ", D1 = " << D1 << ", RING = " << RING << ", NBUF = " << NBUF
+       << ", NEED = " << NEED << ";\n"
+       << "  if (tid == 0) {\n"
+       << "    for (int i = 0; i < NBUF; ++i) mo_mbar_init(MB + i, 1);\n"
+       << "    mo_mbar_fence_init();\n"
+       << "  }\n"
+       << "  __syncthreads();\n"
+       << "  const int CH = P.chunk;\n"
+       << "  const int nch = (P.row1 - P.row0 + CH - 1) / CH;\n"
+       << "  const int items = NB * nch;\n"
+       << "  int slot0 = 0;        // ring slot of the item's input block 0\n"
+       << "  unsigned ph = 0;      // per-slot mbarrier phase parity (bit per slot)\n"
+       << "  // input row block j of an item = global rows [y0 - H - RX + 8j, +8), window columns from cs\n";
+    // Issue code is emitted inline at both sites: the tensor maps must be
+    // addressed in kernel-parameter space (a helper that is not inlined
+    // would see a local copy, which TMA rejects).
+    std::ostringstream is;
+    is << "{ int slot_ = slot0 + (JJ); while (slot_ >= NBUF) slot_ -= NBUF;\n"
+       << "  mo_mbar_expect_tx(MB + slot_, " << tx << "u);\n"
+       << "  const int r_ = y0 - H - RX + 8 * (JJ) - P.row_lo;\n";
+    for (size_t i = 0; i < slots.size(); ++i)
+      is << "  mo_tma_load_2d(mo_dsm + " << staged[i].second.first << " + slot_ * " << boxbytes[i] << ", &T.m[" << i
+         << "], cs * " << slots[i].second << ", r_, MB + slot_);\n";
+    is << "}\n";
+    auto issue = [&](const std::string& j) {
+      std::string t = is.str();
+      for (size_t p = t.find("JJ"); p != std::string::npos; p = t.find("JJ", p)) t.replace(p, 2, j);
+      return t;
+    };
+    os << "  for (int t = blockIdx.x; t < items; t += gridDim.x) {\n"
+       << "    const int ci = t / NB, c0 = (t - ci * NB) * BW;\n"
+       << "    const int y0 = P.row0 + ci * CH, y1 = min(y0 + CH, P.row1);\n"
+       << "    const bool it = y0 - H - RX >= 0 && y1 + H - 1 + RX < D0 && c0 - H - RX >= 0 && c0 - H + 31 + RX < D1;\n"
+       << "    const int q1 = c0 - H + l;\n"
+       << "    const int sh = (c0 - H - RX) & " << AU - 1 << ", cs = c0 - H - RX - sh;  // 16-byte aligned window start\n"
+       << "    const int nsteps = (y1 - y0 + 2 * H + 7) >> 3;\n"
+       << "    const int nblk = (y1 - y0 + 2 * H + 2 * RX + 7) >> 3;\n"
+       << "    if (tid == 0) {\n"
+       << "      mo_fence_proxy_async();\n"
+       << "      for (int j = 0; j < NBUF && j < nblk; ++j) " << issue("j")
+       << "    }\n"
+       << "    // Per-warp ring bookkeeping, advanced incrementally (no divisions):\n"
+       << "    // ss = ring slot of input block s; cr = CL ring row of phase-1 row 8s + w.\n"
+       << "    int ss = slot0, cr = w;\n"
+       << "    // Output columns of this lane (phase 2): 32-bit column indices.\n"
+       << "    const bool lane_out = l >= H && l < 32 - H && q1 < D1;\n"
+       << "    for (int s = 0; s < nsteps; ++s) {\n"
+       << "      // Wait for the newest input block this step needs (each block is\n"
+       << "      // waited exactly once; earlier ones were waited by earlier steps).\n"
+       << "      for (int j = (s == 0 ? 0 : s + NEED - 1); j < s + NEED && j < nblk; ++j) {\n"
+       << "        int q = ss + (j - s); if (q >= NBUF) q -= NBUF;\n"
+       << "        mo_mbar_wait(MB + q, (ph >> q) & 1u);\n"
+       << "        ph ^= 1u << q;\n"
+       << "      }\n"
+       << "      const int rr = 8 * s + w;  // phase-1 row relative to y0 - H\n"
+       << "      const int q0 = y0 - H + rr;\n"
+       << "      if (q0 < y1 + H) {\n"
+       << "        int ri[" << 2 * RX + 1 << "];\n"
+       << "        #pragma unroll\n"
+       << "        for (int o = 0; o < " << 2 * RX + 1 << "; ++o) {\n"
+       << "          const int rel = w + o;  // input row q0 + o - RX, relative to block s\n"
+       << "          int b = ss + (rel >> 3); if (b >= NBUF) b -= NBUF;\n"
+       << "          ri[o] = b * 8 + (rel & 7);\n"
+       << "        }\n"
+       << "        const int k = cr * 32 + l;\n"
+       << "        if (it) mo_lanes4_" << sfx << "<true>(P, q0, q1, k, CL, ri, l + RX + sh); else mo_lanes4_" << sfx
+       << "<false>(P, q0, q1, k, CL, ri, l + RX + sh);\n"
+       << "      }\n"
+       << "      __syncthreads();\n"
+       << "      if (tid == 0 && s + NBUF < nblk) {\n"
+       << "        mo_fence_proxy_async();\n"
+       << "        " << issue("s + NBUF")
+       << "      }\n"
+       << "      const int y = q0 - H;\n"
+       << "      if (y >= y0 && y < y1 && lane_out) {\n"
+       << "        const int e = (y - P.row_lo) * D1 + q1;\n"
+       << "        const bool ex = P.mask && P.mask[e];\n";
+    // CL ring row of output-row minus o0, for o0 in [-H, H]: cr - H - o0 (mod RING).
+    for (int o = -H; o <= H; ++o)
+      os << "        int sl" << (o < 0 ? "m" : "p") << std::abs(o) << " = cr - " << H + o << "; if (sl"
+         << (o < 0 ? "m" : "p") << std::abs(o) << " < 0) sl" << (o < 0 ? "m" : "p") << std::abs(o) << " += RING; sl"
+         << (o < 0 ? "m" : "p") << std::abs(o) << " = sl" << (o < 0 ? "m" : "p") << std::abs(o) << " * 32 + l;\n";
+    epilogue4(g, merged, LS, "        ");
+    os << "      }\n"
+       << "      __syncthreads();  // CL ring rows are rewritten by the next step's phase 1\n"
+       << "      ss = ss + 1 == NBUF ? 0 : ss + 1;\n"
+       << "      cr += 8; if (cr >= RING) cr -= RING;\n"
+       << "    }\n"
+       << "    slot0 += nblk; slot0 %= NBUF;\n"
+       << "  }\n"
+       << "  if (bad) atomicOr(&P.state->nonfinite_kernel, 1);\n"
+       << "  if (P.flags & MO_F_REDUCE) mo_reduce_epilogue<Real>(P.red, acc, 0.0, false);\n}\n";
+    ModuleInfo::Tma ti;
+    ti.ok = true;
+    ti.smem = size_t(off);
+    ti.halo = H;
+    ti.band = BW;
+    ti.rx = RX;
+    ti.win = WIN;
+    for (auto& x : slots) ti.slots.push_back({x.first, x.second});
+    tma_info = ti;
+    staged.clear();
+  }
+  static long long NB(long long D1, int BW) { return (D1 + BW - 1) / BW; }
+  bool f64_disabled_tma() const { return std::getenv("MO_B200_NO_TMA") != nullptr; }
+  ModuleInfo::Tma tma_info;
+
+  // Phase-2 epilogue of the TMA kernel.  Columns are 32-bit (num_cols < 2^31
+  // is checked on the host).  The per-column exclusion mask of a column of a
+  // field on this domain equals the element mask (k_colmask), so ZEROEXCL
+  // reuses `ex` instead of re-reading colmask.
+  void epilogue4(const GatherSet& g, const std::vector<MLane>& merged, int LS, const std::string& ind) {
+    os << ind << "Real* const OUT = (Real*)P.out0; const Real* const PV = (const Real*)P.in0;\n"
+       << ind << "const Real* const DAMP = (const Real*)P.in1; (void)DAMP;\n"
+       << ind << "const int fl = P.flags;\n";
+    for (size_t k = 0; k < g.chans.size(); ++k) {
+      const int f = g.chans[k].first, ch = g.chans[k].second;
+      const int C = P.unknowns[size_t(f)].channels;
+      os << ind << "{ Real s = (Real)0;\n";
+      for (size_t si = 0; si < merged.size(); ++si) {
+        const MLane& m = merged[si];
+        if (m.f != f || m.c != ch) continue;
+        os << ind << "  s += CL[" << si * LS << " + sl" << (m.o0 < 0 ? "m" : "p") << std::abs(m.o0) << " - (" << m.o1
+           << ")];\n";
+      }
+      os << ind << "  Real v = ex ? (Real)0 : (Real)2 * s;\n"
+         << ind << "  if (!(v == v && (v < (Real)0 ? -v : v) <= (Real)MO_REAL_MAX)) bad = true;\n"
+         << ind << "  const int col = (int)P.ubase[" << f << "] + e * " << C << " + " << ch << ";\n"
+         << ind << "  const Real pc = PV[col];\n"
+         << ind << "  if (fl & MO_F_DAMP) v = v + DAMP[col] * pc;\n"
+         << ind << "  if ((fl & MO_F_ZEROEXCL) && ex) v = (Real)0;\n"
+         << ind << "  OUT[col] = v;\n"
+         << ind << "  if (fl & MO_F_REDUCE) acc += (double)(pc * v); }\n";
+    }
+  }
+
+  // Phase-2 gather + apply epilogue of the streaming kernels: out(f,c)(q) =
+  // 2 sum_s CL[s][q - o_s], LM damping, excluded zeroing, p'Ap partial.
+  void epilogue(const GatherSet& g, const std::vector<MLane>& merged, int LS, const std::string& ind) {
+    for (size_t k = 0; k < g.chans.size(); ++k) {
+      const int f = g.chans[k].first, ch = g.chans[k].second;
+      const int C = P.unknowns[size_t(f)].channels;
+      os << ind << "{ Real s = (Real)0;\n";
+      for (size_t si = 0; si < merged.size(); ++si) {
+        const MLane& m = merged[si];
+        if (m.f != f || m.c != ch) continue;
+        os << ind << "  s += CL[" << si * LS << " + sl" << (m.o0 < 0 ? "m" : "p") << std::abs(m.o0) << " - (" << m.o1
+           << ")];\n";
+      }
+      os << ind << "  Real v = ex ? (Real)0 : (Real)2 * s;\n"
+         << ind << "  if (!(v == v && (v < (Real)0 ? -v : v) <= (Real)MO_REAL_MAX)) bad = true;\n"
+         << ind << "  const long long col = P.ubase[" << f << "] + e * " << C << " + " << ch << ";\n"
+         << ind << "  const Real pc = PV[col];\n"
+         << ind << "  if (P.flags & MO_F_DAMP) v = v + DAMP[col] * pc;\n"
+         << ind << "  if ((P.flags & MO_F_ZEROEXCL) && P.colmask && P.colmask[col]) v = (Real)0;\n"
+         << ind << "  OUT[col] = v;\n"
+         << ind << "  if (P.flags & MO_F_REDUCE) acc += (double)(pc * v); }\n";
+    }
+  }
+
+  template <class V>
+  static std::vector<MLane> merged_off(const V& m) {
+    std::vector<MLane> r;
+    for (const auto& x : m) r.push_back({x.f, x.c, x.o0, x.o1});
+    return r;
+  }
+
+  // Row-streaming two-phase apply for 2-D domains (same mathematics as
+  // gather_jtj2, transform.hpp:238-260).  A work item is a band of
+  // BW = 32 - 2H output columns by `P.chunk` output rows.  Each warp owns one
+  // row of 32 phase-1 elements (columns c0-H .. c0-H+31) per step of 8 rows;
+  // the block walks down the band and keeps the last RING = 16 + 2H phase-1
+  // rows of merged-lane contributions in a shared-memory ring, so every
+  // residual instance is evaluated once per item except the 2H halo rows at
+  // the chunk ends and the 2H halo columns of the band (vs. the 32x8 tile's
+  // 1.33x for H = 1).  One barrier per step: phase 1 of step s+1 writes ring
+  // rows [8s+8, 8s+16) while lagging warps may still read [8s-2H, 8s+8).
+  void gather_jtj3(const GatherSet& g, int gi, int H, int RR, int NM, const std::vector<MLane>& merged) {
+    const std::string sfx = std::to_string(gi);
+    const auto sh = P.shape_of(g.dom);
+    const long long D0 = sh[0], D1 = sh[1];
+    const int BW = 32 - 2 * H;
+    if (BW < 8) return;
+    const int RING = 16 + 2 * H;
+    const long long NB = (D1 + BW - 1) / BW;
+    const int LS = RING * 32;
+    const std::string kn = "mo_gather_jtj3_" + sfx;
+    const char* mb = std::getenv("MO_B200_JTJ3_MINB");
+    const int minb = mb ? std::atoi(mb) : 4;
+    os << "extern \"C\" __global__ void __launch_bounds__(MO_THREADS" << (minb > 0 ? ", " + std::to_string(minb) : "")
+       << ") " << kn << "(const __grid_constant__ mo_kparams P) {\n"
+       << "  if ((P.flags & MO_F_SKIPDONE) && P.state->done) return;\n"
+       << "  extern __shared__ __align__(16) unsigned char mo_smem[];\n"
+       << "  Real* CL = reinterpret_cast<Real*>(mo_smem);  // [" << NM << " merged lanes][" << RING << " rows][32]\n"
+       << "  double acc = 0; bool bad = false;\n"
+       << "  Real* OUT = (Real*)P.out0; const Real* PV = (const Real*)P.in0; const Real* DAMP = (const Real*)P.in1;\n"
+       << "  const int tid = threadIdx.x + threadIdx.y * blockDim.x;\n"
+       << "  const int w = tid >> 5, l = tid & 31;\n"
+       << "  constexpr int NB = " << NB << ", BW = " << BW << ", H = " << H << ", RR = " << RR << ";\n"
+       << "  constexpr int D0 = " << D0 << ", D1 = " << D1 << ", RING = " << RING << ";\n"
+       << "  const int CH = P.chunk;\n"
+       << "  const int nch = (P.row1 - P.row0 + CH - 1) / CH;\n"
+       << "  const int items = NB * nch;\n"
+       << "  for (int t = blockIdx.x; t < items; t += gridDim.x) {\n"
+       << "    const int ci = t / NB, c0 = (t - ci * NB) * BW;\n"
+       << "    const int y0 = P.row0 + ci * CH, y1 = min(y0 + CH, P.row1);\n"
+       << "    const bool it = y0 - H - RR >= 0 && y1 + H - 1 + RR < D0 && c0 - H - RR >= 0 && c0 - H + 31 + RR < D1;\n"
+       << "    const int q1 = c0 - H + l;\n"
+       << "    const int nsteps = (y1 - y0 + 2 * H + 7) >> 3;\n"
+       << "    for (int s = 0; s < nsteps; ++s) {\n"
+       << "      const int rr = 8 * s + w;  // phase-1 row relative to y0 - H\n"
+       << "      const int q0 = y0 - H + rr;\n"
+       << "      if (q0 < y1 + H) {\n"
+       << "        const int k = (rr % RING) * 32 + l;\n"
+       << "        if (it) mo_lanes_" << sfx << "<true>(P, q0, q1, k, CL, " << LS << "); else mo_lanes_" << sfx
+       << "<false>(P, q0, q1, k, CL, " << LS << ");\n"
+       << "      }\n"
+       << "      __syncthreads();\n"
+       << "      const int y = q0 - H;\n"
+       << "      if (y >= y0 && y < y1 && l >= H && l < 32 - H && q1 < D1) {\n"
+       << "        const int rrel = rr - H;\n"
+       << "        const long long e = (long long)(y - P.row_lo) * D1 + q1;\n"
+       << "        const bool ex = P.mask && P.mask[e];\n";
+    // ring row slot of output row minus o0, for every o0 in [-H, H]
+    for (int o = -H; o <= H; ++o)
+      os << "        const int sl" << (o < 0 ? "m" : "p") << std::abs(o) << " = ((rrel - (" << o << ")) % RING) * 32 + l;\n";
+    for (size_t k = 0; k < g.chans.size(); ++k) {
+      const int f = g.chans[k].first, ch = g.chans[k].second;
+      const int C = P.unknowns[size_t(f)].channels;
+      os << "        { Real s = (Real)0;\n";
+      for (int si = 0; si < NM; ++si) {
+        const MLane& m = merged[size_t(si)];
+        if (m.f != f || m.c != ch) continue;
+        os << "          s += CL[" << si * LS << " + sl" << (m.o0 < 0 ? "m" : "p") << std::abs(m.o0) << " - (" << m.o1
+           << ")];\n";
+      }
+      os << "          Real v = ex ? (Real)0 : (Real)2 * s;\n"
+         << "          if (!mo_finite((double)v)) bad = true;\n"
+         << "          const long long col = P.ubase[" << f << "] + e * " << C << " + " << ch << ";\n"
+         << "          if (P.flags & MO_F_DAMP) v = v + DAMP[col] * PV[col];\n"
+         << "          if ((P.flags & MO_F_ZEROEXCL) && P.colmask && P.colmask[col]) v = (Real)0;\n"
+         << "          OUT[col] = v;\n"
+         << "          if (P.flags & MO_F_REDUCE) acc += (double)(PV[col] * v); }\n";
+    }
+    os << "      }\n    }\n    __syncthreads();\n  }\n"
+       << "  if (bad) atomicOr(&P.state->nonfinite_kernel, 1);\n"
+       << "  if (P.flags & MO_F_REDUCE) mo_reduce_epilogue<Real>(P.red, acc, 0.0, false);\n}\n";
+    ModuleInfo::Stream st;
+    st.ok = true;
+    st.smem = size_t(NM) * size_t(LS) * (f64 ? 8 : 4);
+    st.halo = H;
+    st.ring = RING;
+    st.band = BW;
+    stream_info = st;
+    stream_gi = gi;
+  }
+  ModuleInfo::Stream stream_info;
+  int stream_gi = -1;
 
   // --------------------------------------------------------- graph kernels
   // One thread per hyperedge (exec.hpp:223-309); scatter outputs go to a
@@ -660,8 +1076,12 @@ struct Gen {
       const GatherSet& g = P.gather_sets[i];
       gather_bm(g, program(g.bm, false, &g.dom), "mo_gather_bm_" + std::to_string(i));
       gather_jtj(g, program(g.jtj, false, &g.dom), "mo_gather_jtj_" + std::to_string(i));
+      stream_info = ModuleInfo::Stream{};
+      tma_info = ModuleInfo::Tma{};
       TwoPhase tp = gather_jtj2(g, int(i));
       info.jtj2.push_back({tp.ok, tp.smem, tp.nlanes, tp.H});
+      info.jtj3.push_back(stream_info);
+      info.jtj4.push_back(tma_info);
     }
     for (size_t i = 0; i < P.graph_sets.size(); ++i) {
       const GraphSet& g = P.graph_sets[i];
@@ -700,7 +1120,9 @@ std::string generate_module(const Plan& P, bool f64, const std::string& prelude,
   Gen g(P, f64);
   g.os << "// generated by mo_codegen.cpp — do not edit\n";
   g.os << "typedef " << (f64 ? "double" : "float") << " Real;\n";
+  g.os << "#define MO_REAL_MAX " << (f64 ? "1.7976931348623157e308" : "3.40282347e38f") << "\n";
   g.os << prelude << "\n";
+  g.os << "extern __shared__ __align__(128) unsigned char mo_dsm[];\n";
   g.run();
   if (info) *info = g.info;
   return g.os.str();

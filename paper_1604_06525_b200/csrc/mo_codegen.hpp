@@ -15,7 +15,26 @@ struct ModuleInfo {
     size_t smem = 0;       // dynamic shared memory per block (bytes)
     int nlanes = 0, halo = 0;
   };
+  // Row-streaming two-phase apply (mo_gather_jtj3_<i>, 2-D domains): one
+  // block walks a band of 32 - 2*halo columns down `chunk` rows, keeping a
+  // ring of `ring` phase-1 rows in shared memory.
+  struct Stream {
+    bool ok = false;
+    size_t smem = 0;
+    int halo = 0, ring = 0, band = 0;
+  };
+  // TMA-staged streaming apply (mo_gather_jtj4_<i>): kernel parameter 2 is a
+  // mo_tmaps with one 2-D tensor map per staged slot, in `slots` order, over
+  // the field as [rows][D1 * C] with box [8][win * C].
+  struct Tma {
+    bool ok = false;
+    size_t smem = 0;
+    int halo = 0, band = 0, rx = 0, win = 0;
+    std::vector<std::pair<int, int>> slots;  // (view slot, channels)
+  };
   std::vector<TwoPhase> jtj2;  // per gather set
+  std::vector<Stream> jtj3;    // per gather set
+  std::vector<Tma> jtj4;       // per gather set
   std::vector<bool> vertex_kernels;  // per graph set: mo_graph_v{jtj,bm}_<g>_<dom> exist
 };
 

@@ -67,9 +67,11 @@ struct mo_red {
   int fin_op, fin_arg;
 };
 
+#define MO_MAX_PARAMS 16
 struct mo_kparams {
   mo_view v[MO_MAX_VIEWS];
   const double* params;
+  double pv[MO_MAX_PARAMS];  // parameter values (constant bank); params[] beyond MO_MAX_PARAMS
   int dnd, d0, d1, d2;  // iteration domain, global shape
   int row0, row1;       // axis-0 rows this launch iterates (global)
   int row_lo;           // first global row of the per-element storage
@@ -87,6 +89,7 @@ struct mo_kparams {
   const long long* rowbase;      // evalf: residual row base per output
   const int* verts;              // graph: int32 vertex table, edge-major
   int arity;
+  int chunk;                     // jtj3: rows per work item (chunk + 2*halo is a multiple of 8)
   long long nedges;
   const int* vptr;               // graph vertex kernels: incident-edge CSR of one domain
   const int* vedge;
@@ -94,6 +97,57 @@ struct mo_kparams {
   mo_red red;
   mo_state* state;
 };
+
+// TMA tensor maps of the fields a staged apply kernel streams into shared
+// memory (second __grid_constant__ kernel parameter).  Same 128-byte, 64-byte
+// aligned layout as the driver's CUtensorMap.
+#define MO_MAX_TMAPS 12
+struct __align__(64) mo_tmap {
+  unsigned long long w[16];
+};
+struct mo_tmaps {
+  mo_tmap m[MO_MAX_TMAPS];
+};
+
+// ---------------------------------------------------------------- TMA / mbarrier
+__device__ __forceinline__ unsigned mo_smem_addr(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mo_mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mo_smem_addr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mo_mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// One arrival that also announces `bytes` of TMA transactions for this phase.
+__device__ __forceinline__ void mo_mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mo_smem_addr(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mo_mbar_wait(unsigned long long* b, unsigned parity) {
+  unsigned ok = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(mo_smem_addr(b)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+// Generic-proxy reads of a ring slot are ordered before the async-proxy
+// (TMA) writes that refill it.
+__device__ __forceinline__ void mo_fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// 2-D tiled TMA load: box at (c_inner, c_outer) of tensor map `m` into smem
+// `dst`, completing `bytes` on barrier `b`.  Out-of-bounds box elements are
+// zero-filled, which is exactly the reference's OOB->0 read (eval.hpp:47-51).
+__device__ __forceinline__ void mo_tma_load_2d(void* dst, const mo_tmap* m, int c_inner, int c_outer,
+                                               unsigned long long* b) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(mo_smem_addr(dst)), "l"(reinterpret_cast<unsigned long long>(m)), "r"(c_inner), "r"(c_outer),
+      "r"(mo_smem_addr(b))
+      : "memory");
+}
 
 // ---------------------------------------------------------------- helpers
 __device__ __forceinline__ bool mo_finite(double x) { return x == x && fabs(x) <= 1.7976931348623157e308; }

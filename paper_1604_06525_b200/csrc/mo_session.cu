@@ -11,6 +11,7 @@
 //              captured once into a CUDA graph, device-side scalars/stop flags
 //   step       x_trial / in-place GN step, trial cost, LM predicted decrease
 // and synchronises once to read the scalar state for the trace row.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -199,6 +200,11 @@ class Session final : public SessionBase {
     CK(cudaSetDevice(dev_));
     if (n) CK(cudaMemcpyAsync(params_d_, p, size_t(n) * sizeof(double), cudaMemcpyHostToDevice, st_));
     CK(cudaStreamSynchronize(st_));
+    // Kernels read parameters from their (graph-captured) launch arguments:
+    // new values invalidate the captured stage graphs.
+    std::vector<double> nv(p, p + n);
+    if (params_bound_ && nv != params_h_) invalidate_graphs();
+    params_h_ = nv;
     params_bound_ = true;
   }
   void bind_graph(int i, const uint64_t* verts, int64_t n, int arity) override {
@@ -895,6 +901,7 @@ class Session final : public SessionBase {
     for (int a = 0; a < A; ++a) k.v[2 * U + a] = view(arr_[size_t(a)], P_.arrays[size_t(a)]);
     for (size_t c = 0; c < P_.computed.size(); ++c) k.v[2 * U + A + int(c)] = view(comp_[c], P_.computed[c]);
     k.params = params_d_;
+    for (size_t i = 0; i < params_h_.size() && i < MO_MAX_PARAMS; ++i) k.pv[i] = params_h_[i];
     k.colmask = colmask_;
     k.state = state_;
     return k;
@@ -965,16 +972,90 @@ class Session final : public SessionBase {
     CK(cudaLaunchKernel(f, dim3(grid), block, args, smem, st_));
     ++launches_;
   }
-  // Fast-path apply kernel of gather set i: the two-phase evalj kernel unless
-  // the plan asked for exact (reference-program) execution.
-  bool two_phase(size_t i) const {
-    if (P_.exact || i >= minfo_.jtj2.size() || !minfo_.jtj2[i].ok) return false;
-    return i >= jtj_choice_.size() || jtj_choice_[i] != 0;
+  // Apply kernel variants of gather set i: 0 = the reference's gather program
+  // (exact mode always uses it), 1 = two-phase 32x8 tiles, 2 = row-streaming
+  // two-phase bands (2-D domains).
+  bool variant_ok(size_t i, int v) const {
+    if (v == 0) return true;
+    if (P_.exact) return false;
+    if (v == 1) return i < minfo_.jtj2.size() && minfo_.jtj2[i].ok;
+    if (v == 2) return i < minfo_.jtj3.size() && minfo_.jtj3[i].ok;
+    return i < minfo_.jtj4.size() && minfo_.jtj4[i].ok && tma_capable(i);
   }
-  // First use: time the gather-program kernel against the two-phase kernel
-  // on the bound data and keep the faster per gather set (cheap programs such
-  // as Poisson's can win without shared memory, barriers or halo recompute).
-  // MO_B200_JTJ=gather|twophase forces a choice.
+  int variant(size_t i) const {
+    if (i < jtj_choice_.size() && variant_ok(i, jtj_choice_[i])) return jtj_choice_[i];
+    for (int v : {3, 2, 1}) if (variant_ok(i, v)) return v;
+    return 0;
+  }
+  static const char* variant_prefix(int v) {
+    static const char* n[] = {"mo_gather_jtj_", "mo_gather_jtj2_", "mo_gather_jtj3_", "mo_gather_jtj4_"};
+    return n[v];
+  }
+
+  // ---- TMA tensor maps for the staged apply (variant 3)
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn encoder() {
+    static EncodeFn fn = [] {
+      void* f = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+          q != cudaDriverEntryPointSuccess)
+        f = nullptr;
+      cudaGetLastError();
+      return reinterpret_cast<EncodeFn>(f);
+    }();
+    return fn;
+  }
+  // Rows stored per buffer of a grid field (strip shards keep their halo rows).
+  long long stored_rows(const Domain& d) const {
+    return sh_.on && d == sh_.dom ? (long long)(sh_.hi - sh_.lo) : (long long)P_.shape_of(d)[0];
+  }
+  // Every staged field must be addressable by TMA: 16-byte aligned base
+  // (column-layout fields start at ubase[f]) and 16-byte multiple row pitch.
+  bool tma_capable(size_t i) const {
+    if (!encoder() || std::getenv("MO_B200_NO_TMA")) return false;
+    if (P_.num_cols >= (1LL << 31)) return false;  // 32-bit column indices in the epilogue
+    const auto sh = P_.shape_of(P_.gather_sets[i].dom);
+    const int U = int(P_.unknowns.size());
+    for (auto [sl, C] : minfo_.jtj4[i].slots) {
+      if ((sh[1] * C * (long long)sizeof(Real)) % 16) return false;
+      if (sl < 2 * U && (P_.ubase[size_t(sl % U)] * (long long)sizeof(Real)) % 16) return false;
+    }
+    return true;
+  }
+  const mo_tmaps& tmaps_for(size_t i, const mo_kparams& kp) {
+    const auto& ti = minfo_.jtj4[i];
+    std::string key = std::to_string(i);
+    for (auto [sl, C] : ti.slots) key += "/" + std::to_string(reinterpret_cast<uintptr_t>(kp.v[sl].p));
+    auto it = tmaps_.find(key);
+    if (it != tmaps_.end()) return it->second;
+    mo_tmaps T;
+    std::memset(&T, 0, sizeof T);
+    const auto sh = P_.shape_of(P_.gather_sets[i].dom);
+    const long long rows = stored_rows(P_.gather_sets[i].dom);
+    for (size_t k = 0; k < ti.slots.size(); ++k) {
+      const int C = ti.slots[k].second;
+      const void* ptr = kp.v[ti.slots[k].first].p;
+      check(ptr != nullptr, Err::kInternal, "TMA apply: staged field is not bound");
+      const cuuint64_t dims[2] = {cuuint64_t(sh[1] * C), cuuint64_t(rows)};
+      const cuuint64_t strides[1] = {cuuint64_t(sh[1] * C * (long long)sizeof(Real))};
+      const cuuint32_t box[2] = {cuuint32_t(ti.win * C), 8u};
+      const cuuint32_t estr[2] = {1u, 1u};
+      CUresult r = encoder()(reinterpret_cast<CUtensorMap*>(&T.m[k]),
+                             sizeof(Real) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                             const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      check(r == CUDA_SUCCESS, Err::kCuda, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+    }
+    return tmaps_.emplace(key, T).first->second;
+  }
+  // First use: time every available variant on the bound data and keep the
+  // fastest per gather set (cheap programs such as Poisson's can win without
+  // shared memory, barriers or halo recompute).  MO_B200_JTJ=gather|twophase|
+  // stream forces a choice.
   void tune_apply() {
     if (tuned_) return;
     tuned_ = true;
@@ -993,47 +1074,108 @@ class Session final : public SessionBase {
         return;
       }
     }
-    jtj_choice_.assign(P_.gather_sets.size(), 1);
+    jtj_choice_.assign(P_.gather_sets.size(), 0);
     const char* force = std::getenv("MO_B200_JTJ");
     for (size_t i = 0; i < P_.gather_sets.size(); ++i) {
-      if (P_.exact || i >= minfo_.jtj2.size() || !minfo_.jtj2[i].ok) continue;
-      if (force) {
-        jtj_choice_[i] = std::string(force) == "gather" ? 0 : 1;
-        continue;
+      jtj_choice_[i] = -1;
+      const int want = !force ? -1
+                       : std::string(force) == "gather" ? 0
+                       : std::string(force) == "twophase" ? 1
+                       : std::string(force) == "stream" ? 2
+                                                         : 3;
+      if (want >= 0) {
+        jtj_choice_[i] = variant_ok(i, want) ? want : -1;
+        if (jtj_choice_[i] >= 0) continue;
       }
-      float best[2] = {0, 0};
+      float best = 0;
+      int bestv = 0;
       cudaEvent_t a, b;
       CK(cudaEventCreate(&a));
       CK(cudaEventCreate(&b));
-      for (int v = 0; v < 2; ++v) {
-        const std::string name = (v ? "mo_gather_jtj2_" : "mo_gather_jtj_") + std::to_string(i);
-        const size_t smem = v ? minfo_.jtj2[i].smem : 0;
-        mo_kparams kp = kp_grid(P_.gather_sets[i].dom, x_, x_);
-        kp.out0 = otmp_;
-        kp.in0 = x_;
-        kp.in1 = damp_;
-        const int grid = grid_blocks(name, P_.gather_sets[i].dom, smem);
+      for (int v = 0; v < 4; ++v) {
+        if (!variant_ok(i, v)) continue;
+        jtj_choice_[i] = v;
+        mo_kparams kp = kp_apply(i, x_, otmp_, 0);
+        const int grid = jtj_grid(i);
         for (int rep = 0; rep < 4; ++rep) {
           if (rep == 1) CK(cudaEventRecord(a, st_));
-          launch_grid(name, P_.gather_sets[i].dom, kp, grid, smem);
+          launch_apply(i, kp, grid);
         }
         CK(cudaEventRecord(b, st_));
         CK(cudaEventSynchronize(b));
-        CK(cudaEventElapsedTime(&best[v], a, b));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, a, b));
         launches_ -= 4;
+        if (v == 0 || ms < best) {
+          best = ms;
+          bestv = v;
+        }
       }
       cudaEventDestroy(a);
       cudaEventDestroy(b);
-      // Keep the two-phase kernel unless the gather kernel is clearly faster.
-      jtj_choice_[i] = best[0] < 0.9f * best[1] ? 0 : 1;
+      jtj_choice_[i] = bestv;
     }
     std::lock_guard<std::mutex> lk(mu);
     cache[key] = jtj_choice_;
   }
-  std::string jtj_kernel(size_t i) const {
-    return (two_phase(i) ? "mo_gather_jtj2_" : "mo_gather_jtj_") + std::to_string(i);
+  std::string jtj_kernel(size_t i) const { return variant_prefix(variant(i)) + std::to_string(i); }
+  size_t jtj_smem(size_t i) const {
+    const int v = variant(i);
+    return v == 1 ? minfo_.jtj2[i].smem : v == 2 ? minfo_.jtj3[i].smem : v == 3 ? minfo_.jtj4[i].smem : 0;
   }
-  size_t jtj_smem(size_t i) const { return two_phase(i) ? minfo_.jtj2[i].smem : 0; }
+  int jtj_halo(size_t i) const { return variant(i) == 3 ? minfo_.jtj4[i].halo : minfo_.jtj3[i].halo; }
+  int jtj_band(size_t i) const { return variant(i) == 3 ? minfo_.jtj4[i].band : minfo_.jtj3[i].band; }
+  // Launch the apply kernel of gather set i (variant 3 also takes the tensor maps).
+  void launch_apply(size_t i, const mo_kparams& kp, int grid) {
+    if (variant(i) != 3) {
+      launch_grid(jtj_kernel(i), P_.gather_sets[i].dom, kp, grid, jtj_smem(i));
+      return;
+    }
+    const void* f = mod_.kernel(jtj_kernel(i));
+    const size_t smem = jtj_smem(i);
+    occupancy(f, smem);  // sets the dynamic smem attribute once
+    const mo_tmaps& T = tmaps_for(i, kp);
+    void* args[] = {const_cast<mo_kparams*>(&kp), const_cast<mo_tmaps*>(&T)};
+    CK(cudaLaunchKernel(f, dim3(grid), dim3(MO_TILE_X, MO_TILE_Y, 1), args, smem, st_));
+    ++launches_;
+  }
+  // Rows per streaming work item: chunk + 2H a multiple of 8, as long as the
+  // item count still fills ~2 waves of resident blocks.
+  int jtj3_chunk(size_t i) {
+    const auto sh = P_.shape_of(P_.gather_sets[i].dom);
+    const long long rows = sh_.on ? sh_.row1 - sh_.row0 : sh[0];
+    const int halo = jtj_halo(i), band = jtj_band(i);
+    const long long nb = (sh[1] + band - 1) / band;
+    const long long want = 2LL * nsm_ * occupancy(mod_.kernel(jtj_kernel(i)), jtj_smem(i));
+    int best = 8 - 2 * halo;
+    for (int m = 1; m <= 16; ++m) {
+      const int ch = 8 * m - 2 * halo;
+      if (ch <= 0) continue;
+      if (best <= 0) best = ch;
+      if (nb * ((rows + ch - 1) / ch) >= want) best = ch;
+    }
+    return std::max(best, 1);
+  }
+  int jtj_grid(size_t i) {
+    if (variant(i) < 2) return grid_blocks(jtj_kernel(i), P_.gather_sets[i].dom, jtj_smem(i));
+    const auto sh = P_.shape_of(P_.gather_sets[i].dom);
+    const long long rows = sh_.on ? sh_.row1 - sh_.row0 : sh[0];
+    const int band = jtj_band(i);
+    const long long nb = (sh[1] + band - 1) / band;
+    const int ch = jtj3_chunk(i);
+    const long long items = nb * ((rows + ch - 1) / ch);
+    const long long cap = (long long)nsm_ * occupancy(mod_.kernel(jtj_kernel(i)), jtj_smem(i));
+    return int(std::max<long long>(1, std::min(items, cap)));
+  }
+  mo_kparams kp_apply(size_t i, const Real* pv, Real* out, int flags) {
+    mo_kparams kp = kp_grid(P_.gather_sets[i].dom, x_, pv);
+    kp.out0 = out;
+    kp.in0 = pv;
+    kp.in1 = damp_;
+    kp.flags = flags;
+    if (variant(i) >= 2) kp.chunk = jtj3_chunk(i);
+    return kp;
+  }
   void launch_edges(const std::string& name, int gi, const mo_kparams& kp, int grid = 0) {
     const void* f = mod_.kernel(name);
     if (grid <= 0) grid = edge_blocks(name, gi);
@@ -1181,22 +1323,18 @@ class Session final : public SessionBase {
     std::vector<int> grids;
     int total = 0;
     for (size_t i = 0; i < P_.gather_sets.size(); ++i) {
-      grids.push_back(grid_blocks(jtj_kernel(i), P_.gather_sets[i].dom, jtj_smem(i)));
+      grids.push_back(jtj_grid(i));
       total += grids.back();
     }
     if (!fused) total = vgrid(n, nsm_);
     int base = 0;
     for (size_t i = 0; i < P_.gather_sets.size(); ++i) {
-      mo_kparams kp = kp_grid(P_.gather_sets[i].dom, x_, pv);
-      kp.out0 = out;
-      kp.in0 = pv;
-      kp.in1 = damp_;
+      mo_kparams kp = kp_apply(i, pv, out, fused ? flags : (flags & MO_F_SKIPDONE));
       kp.in2 = rvec;
       kp.in3 = mdvec;
       kp.out2 = pnew;
-      kp.flags = fused ? flags : (flags & MO_F_SKIPDONE);
       kp.red = red(base, total, MO_FIN_PCG_ALPHA, 0);
-      launch_grid(jtj_kernel(i), P_.gather_sets[i].dom, kp, grids[i], jtj_smem(i));
+      launch_apply(i, kp, grids[i]);
       base += grids[i];
     }
     if (fused && (flags & MO_F_REDUCE)) reduce_done(MO_FIN_PCG_ALPHA, 0);
@@ -1352,6 +1490,7 @@ class Session final : public SessionBase {
   std::vector<unsigned char*> masks_;
   unsigned char* colmask_ = nullptr;
   double* params_d_ = nullptr;
+  std::vector<double> params_h_;
   mo_state* state_ = nullptr;
   mo_state* state_h_ = nullptr;
   double* partials_ = nullptr;
@@ -1369,7 +1508,8 @@ class Session final : public SessionBase {
   ModuleInfo minfo_;
   std::map<int, cudaGraphExec_t> stage_exec_;
   bool tuned_ = false;
-  std::vector<int> jtj_choice_;  // per gather set: 0 gather program, 1 two-phase
+  std::vector<int> jtj_choice_;  // per gather set: 0 gather program, 1 two-phase tiles, 2 streaming, 3 TMA streaming
+  std::map<std::string, mo_tmaps> tmaps_;  // per (gather set, staged buffers)
   std::string module_key_;
   std::map<int, int64_t> stage_nodes_;
   std::vector<void*> owned_;
