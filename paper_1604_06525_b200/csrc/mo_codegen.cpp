@@ -722,7 +722,8 @@ struct Gen {
        << "  if ((P.flags & MO_F_SKIPDONE) && P.state->done) return;\n"
        << "  Real* CL = reinterpret_cast<Real*>(mo_dsm);  // [" << NM << " merged lanes][" << RING << " rows][32]\n"
        << "  unsigned long long* MB = reinterpret_cast<unsigned long long*>(mo_dsm + " << mbar_off << ");\n"
-       << "  double acc = 0; bool bad = false;\n"
+       << "  double acc = 0;\n"
+       << "  unsigned em = 0;  // max exponent field of the outputs: all ones <=> a non-finite output\n"
        << "  const int tid = threadIdx.x + threadIdx.y * blockDim.x;\n"
        << "  const int w = tid >> 5, l = tid & 31;\n"
        << "  constexpr int NB = " << NB(D1, BW) << ", BW = " << BW << ", H = " << H << ", RX = " << RX << ";\n"
@@ -775,8 +776,15 @@ struct Gen {
        << "    for (int s = 0; s < nsteps; ++s) {\n"
        << "      // Wait for the newest input block this step needs (each block is\n"
        << "      // waited exactly once; earlier ones were waited by earlier steps).\n"
-       << "      for (int j = (s == 0 ? 0 : s + NEED - 1); j < s + NEED && j < nblk; ++j) {\n"
-       << "        int q = ss + (j - s); if (q >= NBUF) q -= NBUF;\n"
+       << "      if (s == 0) {\n"
+       << "        for (int j = 0; j < NEED - 1 && j < nblk; ++j) {\n"
+       << "          int q = ss + j; if (q >= NBUF) q -= NBUF;\n"
+       << "          mo_mbar_wait(MB + q, (ph >> q) & 1u);\n"
+       << "          ph ^= 1u << q;\n"
+       << "        }\n"
+       << "      }\n"
+       << "      if (s + NEED - 1 < nblk) {\n"
+       << "        int q = ss + NEED - 1; if (q >= NBUF) q -= NBUF;\n"
        << "        mo_mbar_wait(MB + q, (ph >> q) & 1u);\n"
        << "        ph ^= 1u << q;\n"
        << "      }\n"
@@ -795,10 +803,6 @@ struct Gen {
        << "<false>(P, q0, q1, k, CL, ri, l + RX + sh);\n"
        << "      }\n"
        << "      __syncthreads();\n"
-       << "      if (tid == 0 && s + NBUF < nblk) {\n"
-       << "        mo_fence_proxy_async();\n"
-       << "        " << issue("s + NBUF")
-       << "      }\n"
        << "      const int y = q0 - H;\n"
        << "      if (y >= y0 && y < y1 && lane_out) {\n"
        << "        const int e = (y - P.row_lo) * D1 + q1;\n"
@@ -811,12 +815,17 @@ struct Gen {
     epilogue4(g, merged, LS, "        ");
     os << "      }\n"
        << "      __syncthreads();  // CL ring rows are rewritten by the next step's phase 1\n"
+       << "      // Input block s (read by phase 1 and, for p, by phase 2) is free now.\n"
+       << "      if (tid == 0 && s + NBUF < nblk) {\n"
+       << "        mo_fence_proxy_async();\n"
+       << "        " << issue("s + NBUF")
+       << "      }\n"
        << "      ss = ss + 1 == NBUF ? 0 : ss + 1;\n"
        << "      cr += 8; if (cr >= RING) cr -= RING;\n"
        << "    }\n"
        << "    slot0 += nblk; slot0 %= NBUF;\n"
        << "  }\n"
-       << "  if (bad) atomicOr(&P.state->nonfinite_kernel, 1);\n"
+       << "  if (em == MO_EXP_MASK) atomicOr(&P.state->nonfinite_kernel, 1);\n"
        << "  if (P.flags & MO_F_REDUCE) mo_reduce_epilogue<Real>(P.red, acc, 0.0, false);\n}\n";
     ModuleInfo::Tma ti;
     ti.ok = true;
@@ -838,9 +847,21 @@ struct Gen {
   // field on this domain equals the element mask (k_colmask), so ZEROEXCL
   // reuses `ex` instead of re-reading colmask.
   void epilogue4(const GatherSet& g, const std::vector<MLane>& merged, int LS, const std::string& ind) {
-    os << ind << "Real* const OUT = (Real*)P.out0; const Real* const PV = (const Real*)P.in0;\n"
+    const int U = int(P.unknowns.size());
+    os << ind << "Real* const OUT = (Real*)P.out0; const Real* const PV = (const Real*)P.in0; (void)PV;\n"
        << ind << "const Real* const DAMP = (const Real*)P.in1; (void)DAMP;\n"
-       << ind << "const int fl = P.flags;\n";
+       << ind << "const int fl = P.flags;\n"
+       << ind << "// staged p of the output row (input row y = block s row w - H + RX)\n"
+       << ind << "int rp = ss + ((w - H + RX) >> 3); if (rp >= NBUF) rp -= NBUF; rp = rp * 8 + ((w - H + RX) & 7);\n"
+       << ind << "const int lx = l + RX + sh; (void)lx;\n";
+    std::vector<int> fields;
+    for (auto& fc : g.chans)
+      if (std::find(fields.begin(), fields.end(), fc.first) == fields.end()) fields.push_back(fc.first);
+    for (int f : fields) {
+      const int C = P.unknowns[size_t(f)].channels;
+      os << ind << "const int cb" << f << " = (int)P.ubase[" << f << "] + e * " << C << ";\n"
+         << ind << "Real* const o" << f << " = OUT + cb" << f << ";\n";
+    }
     for (size_t k = 0; k < g.chans.size(); ++k) {
       const int f = g.chans[k].first, ch = g.chans[k].second;
       const int C = P.unknowns[size_t(f)].channels;
@@ -852,12 +873,15 @@ struct Gen {
            << ")];\n";
       }
       os << ind << "  Real v = ex ? (Real)0 : (Real)2 * s;\n"
-         << ind << "  if (!(v == v && (v < (Real)0 ? -v : v) <= (Real)MO_REAL_MAX)) bad = true;\n"
-         << ind << "  const int col = (int)P.ubase[" << f << "] + e * " << C << " + " << ch << ";\n"
-         << ind << "  const Real pc = PV[col];\n"
-         << ind << "  if (fl & MO_F_DAMP) v = v + DAMP[col] * pc;\n"
+         << ind << "  em = max(em, MO_EXP_BITS(v));\n";
+      if (const auto* st = staged_of(U + f))
+        os << ind << "  const Real pc = reinterpret_cast<const Real*>(mo_dsm + " << st->first << ")[rp * " << st_win * C
+           << " + lx * " << C << " + " << ch << "];\n";
+      else
+        os << ind << "  const Real pc = PV[cb" << f << " + " << ch << "];\n";
+      os << ind << "  if (fl & MO_F_DAMP) v = v + DAMP[cb" << f << " + " << ch << "] * pc;\n"
          << ind << "  if ((fl & MO_F_ZEROEXCL) && ex) v = (Real)0;\n"
-         << ind << "  OUT[col] = v;\n"
+         << ind << "  o" << f << "[" << ch << "] = v;\n"
          << ind << "  if (fl & MO_F_REDUCE) acc += (double)(pc * v); }\n";
     }
   }
@@ -1121,6 +1145,11 @@ std::string generate_module(const Plan& P, bool f64, const std::string& prelude,
   g.os << "// generated by mo_codegen.cpp — do not edit\n";
   g.os << "typedef " << (f64 ? "double" : "float") << " Real;\n";
   g.os << "#define MO_REAL_MAX " << (f64 ? "1.7976931348623157e308" : "3.40282347e38f") << "\n";
+  // Exponent field of a Real (as unsigned): all ones <=> inf or nan.
+  if (f64)
+    g.os << "#define MO_EXP_BITS(v) ((unsigned)(__double_as_longlong(v) >> 32) & 0x7ff00000u)\n#define MO_EXP_MASK 0x7ff00000u\n";
+  else
+    g.os << "#define MO_EXP_BITS(v) (__float_as_uint(v) & 0x7f800000u)\n#define MO_EXP_MASK 0x7f800000u\n";
   g.os << prelude << "\n";
   g.os << "extern __shared__ __align__(128) unsigned char mo_dsm[];\n";
   g.run();

@@ -1139,20 +1139,28 @@ class Session final : public SessionBase {
     CK(cudaLaunchKernel(f, dim3(grid), dim3(MO_TILE_X, MO_TILE_Y, 1), args, smem, st_));
     ++launches_;
   }
-  // Rows per streaming work item: chunk + 2H a multiple of 8, as long as the
-  // item count still fills ~2 waves of resident blocks.
+  // Rows per streaming work item (chunk + 2H a multiple of 8).  Work items
+  // are dealt to a fixed grid of resident blocks, so the apply takes
+  // ceil(items / grid) rounds of ceil((chunk + 2H) / 8) row steps: pick the
+  // chunk minimising that (plus a per-item pipeline fill), larger on ties.
   int jtj3_chunk(size_t i) {
     const auto sh = P_.shape_of(P_.gather_sets[i].dom);
     const long long rows = sh_.on ? sh_.row1 - sh_.row0 : sh[0];
     const int halo = jtj_halo(i), band = jtj_band(i);
     const long long nb = (sh[1] + band - 1) / band;
-    const long long want = 2LL * nsm_ * occupancy(mod_.kernel(jtj_kernel(i)), jtj_smem(i));
-    int best = 8 - 2 * halo;
+    const long long grid = (long long)nsm_ * occupancy(mod_.kernel(jtj_kernel(i)), jtj_smem(i));
+    int best = 0;
+    double best_cost = 1e300;
     for (int m = 1; m <= 16; ++m) {
       const int ch = 8 * m - 2 * halo;
       if (ch <= 0) continue;
-      if (best <= 0) best = ch;
-      if (nb * ((rows + ch - 1) / ch) >= want) best = ch;
+      const long long items = nb * ((rows + ch - 1) / ch);
+      const long long rounds = (items + grid - 1) / grid;
+      const double cost = double(rounds) * (m + 0.5);
+      if (cost <= best_cost) {
+        best_cost = cost;
+        best = ch;
+      }
     }
     return std::max(best, 1);
   }
@@ -1376,6 +1384,8 @@ class Session final : public SessionBase {
       apply(p_, ap_, flags);
       prof_end(0);
       prof_begin(1);
+      // (A cooperative single-kernel update + direction with a grid barrier
+      // was measured slower on B200 than this pair at every config size.)
       k_pcg_update<Real><<<vg, MO_THREADS, 0, st_>>>(red(0, vg, MO_FIN_PCG_BETA, 0), n, colmask_, mdv, delta_, r_, p_, ap_, pre);
       ++launches_;
       reduce_done(MO_FIN_PCG_BETA, 0);
