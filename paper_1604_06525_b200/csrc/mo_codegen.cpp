@@ -624,6 +624,7 @@ struct Gen {
       std::vector<LaneG> lg;
       for (const L& l : lanes) lg.push_back({l.t, l.out, l.f, l.c, l.o0, l.o1});
       gather_jtj4(g, gi, *S, lg, lane_slot, merged_off(merged), H);
+      gather_jtj5(g, gi, *S, lg, lane_slot, merged_off(merged), H);
     }
     return tp;
   }
@@ -838,6 +839,272 @@ struct Gen {
     tma_info = ti;
     staged.clear();
   }
+  // Warp-streaming TMA apply (2-D domains).  A block is NW warps side by
+  // side: warp w owns the band of BW = 32 - 2H output columns starting at
+  // c0 + w*BW and walks a chunk of rows on its own.  Per phase-1 row every lane
+  // evaluates the evalj template partials of its element ONCE (from the
+  // TMA-fed shared-memory input ring), forms the NM merged-lane contributions
+  // and routes them to their output pixels without shared memory: the column
+  // offset o1 through a warp shuffle, the row offset o0 into one of 2H+1
+  // rolling register accumulators (out(q) = sum_s c_s(q - o_s), gather_jtj2's
+  // sum).  Row q0 - H is complete after row q0 and is written at once.  No
+  // block barrier per row: input blocks of R rows are refilled by whichever
+  // warp releases a slot last (shared-memory arrival counter), consumers wait
+  // on the slot's mbarrier.  One TMA box per field and input block, so the
+  // block window (NW*BW + 2H + 2RX, aligned) must fit 256/C columns.
+  void gather_jtj5(const GatherSet& g, int gi, const GridSet& S, const std::vector<LaneG>& lanes,
+                   const std::vector<int>& lane_slot, const std::vector<MLane>& merged, int H) {
+    if (f64_disabled_tma()) return;
+    const std::string sfx = std::to_string(gi);
+    const auto sh = P.shape_of(g.dom);
+    const long long D0 = sh[0], D1 = sh[1];
+    const int BW = 32 - 2 * H;
+    if (BW < 8) return;
+    const int U = int(P.unknowns.size());
+    const int RX = std::max(reach_of(S.evalj, &g.dom), H);
+    const int AU = f64 ? 2 : 4;
+    const int R = 2;                               // rows per input block
+    const int NBUF = 2 + (2 * RX + R - 1) / R;     // blocks a row needs + one in flight
+    const int NM = int(merged.size());
+    const int RB = f64 ? 8 : 4;
+    std::vector<std::pair<int, int>> slots;  // (slot, channels)
+    auto add = [&](int sl, int C) {
+      for (auto& x : slots)
+        if (x.first == sl) return;
+      slots.push_back({sl, C});
+    };
+    for (const Instr& in : S.evalj.instrs) {
+      if (!(in.op == kLoadU || in.op == kLoadA || in.op == kLoadC || in.op == kLoadP) || in.graph) continue;
+      const Field& f = field_of(in.op, in.field);
+      if (f.dom == g.dom) add(slot_of(in.op, in.field), f.channels);
+    }
+    for (const LaneG& l : lanes) add(U + l.f, P.unknowns[size_t(l.f)].channels);
+    for (auto& fc : g.chans) add(U + fc.first, P.unknowns[size_t(fc.first)].channels);
+    if (slots.empty() || int(slots.size()) > MO_MAX_TMAPS_HOST) return;
+    int cmax = 1;
+    for (auto& x : slots) cmax = std::max(cmax, x.second);
+    // widest block whose window fits one TMA box row (<= 256 elements)
+    int NW = 0, WIN = 0;
+    // WIN unit: 16-byte aligned box starts (AU) and R-row slots that are
+    // whole multiples of 128 bytes (R * WIN * RB % 128 == 0 for any C).
+    const int WU = std::max(AU, 128 / (R * RB));
+    for (int nw = 4; nw >= 1; --nw) {
+      const int win = (nw * BW + 2 * H + 2 * RX + AU - 1 + WU - 1) / WU * WU;
+      if (win * cmax <= 256) {
+        NW = nw;
+        WIN = win;
+        break;
+      }
+    }
+    if (!NW) return;
+    // Dynamic smem: field rings [NBUF*R rows][WIN*C] (128-B aligned) | mbarriers | counters.
+    long long off = 0;
+    staged.clear();
+    long long tx = 0;
+    std::vector<long long> boxbytes;
+    for (auto& x : slots) {
+      staged.push_back({x.first, {off, x.second}});
+      const long long bb = (long long)R * WIN * x.second * RB;
+      boxbytes.push_back(bb);  // a multiple of 128 bytes (WIN rounding): TMA destinations are 128-byte aligned
+      tx += bb;
+      off += (long long)NBUF * bb;
+    }
+    const long long mbar_off = off;
+    off += 8LL * NBUF;
+    const long long cnt_off = off;
+    off += 4LL * NBUF;
+    st_rx = RX;
+    st_win = WIN;
+    const std::string pe = program(S.evalj, false, &g.dom, true);
+    const int NO = int(S.evalj.outputs.size());
+    os << "template <bool I> __device__ __forceinline__ void mo_lanes5_" << sfx
+       << "(const mo_kparams& P, int p0, int p1, const int* ri, int lx, Real* c) {\n"
+       << "  const bool inside = I || mo_inb(P, p0, p1, 0);\n"
+       << "  Real d[" << NO << "];\n  " << pe << "<I>(P, p0, p1, 0, ri, lx, d);\n";
+    for (int si = 0; si < NM; ++si) os << "  Real m" << si << " = (Real)0;\n";
+    for (size_t t = 0; t < S.jtemplates.size(); ++t) {
+      os << "  { Real jp = (Real)0;\n";
+      for (const LaneG& l : lanes)
+        if (l.t == int(t)) os << "    jp += d[" << l.out << "] * " << smx(U + l.f, l.o0, l.o1, l.c) << ";\n";
+      const bool origin = S.jtemplates[t].origin;
+      if (origin) os << "    if (inside) {\n";
+      for (size_t li = 0; li < lanes.size(); ++li)
+        if (lanes[li].t == int(t)) os << "    m" << lane_slot[li] << " += d[" << lanes[li].out << "] * jp;\n";
+      if (origin) os << "    }\n";
+      os << "  }\n";
+    }
+    for (int si = 0; si < NM; ++si) os << "  c[" << si << "] = m" << si << ";\n";
+    os << "}\n";
+    sm_mode = false;
+
+    const int K = int(g.chans.size());
+    const int NA = 2 * H + 1;
+    const std::string kn = "mo_gather_jtj5_" + sfx;
+    const char* mb = std::getenv("MO_B200_JTJ5_MINB");
+    const int minb = mb ? std::atoi(mb) : 0;
+    std::ostringstream is;  // TMA issue of input block JJ (inline: tensor maps in param space)
+    is << "{ int slot_ = slot0 + (JJ); while (slot_ >= NBUF) slot_ -= NBUF;\n"
+       << "  mo_mbar_expect_tx(MB + slot_, " << tx << "u);\n"
+       << "  const int r_ = y0 - H - RX + R * (JJ) - P.row_lo;\n";
+    for (size_t i = 0; i < slots.size(); ++i)
+      is << "  mo_tma_load_2d(mo_dsm + " << staged[i].second.first << " + slot_ * " << boxbytes[i] << ", &T.m[" << i
+         << "], cs * " << slots[i].second << ", r_, MB + slot_);\n";
+    is << "}\n";
+    auto issue = [&](const std::string& j) {
+      std::string t = is.str();
+      for (size_t p = t.find("JJ"); p != std::string::npos; p = t.find("JJ", p)) t.replace(p, 2, j);
+      return t;
+    };
+    os << "extern \"C\" __global__ void __launch_bounds__(" << 32 * NW << (minb > 0 ? ", " + std::to_string(minb) : "")
+       << ") " << kn << "(const __grid_constant__ mo_kparams P, const __grid_constant__ mo_tmaps T) {\n"
+       << "  if ((P.flags & MO_F_SKIPDONE) && P.state->done) return;\n"
+       << "  unsigned long long* MB = reinterpret_cast<unsigned long long*>(mo_dsm + " << mbar_off << ");\n"
+       << "  unsigned* CNT = reinterpret_cast<unsigned*>(mo_dsm + " << cnt_off << ");\n"
+       << "  double acc = 0;\n"
+       << "  unsigned em = 0;\n"
+       << "  const int tid = threadIdx.x + threadIdx.y * blockDim.x;\n"
+       << "  const int w = tid >> 5, l = tid & 31;\n"
+       << "  constexpr int NW = " << NW << ", BW = " << BW << ", H = " << H << ", RX = " << RX << ", R = " << R
+       << ", NBUF = " << NBUF << ";\n"
+       << "  constexpr int D0 = " << D0 << ", D1 = " << D1 << ", NBG = " << (D1 + NW * BW - 1) / (NW * BW) << ";\n"
+       << "  if (tid == 0) {\n"
+       << "    for (int i = 0; i < NBUF; ++i) { mo_mbar_init(MB + i, 1); CNT[i] = 0u; }\n"
+       << "    mo_mbar_fence_init();\n"
+       << "  }\n"
+       << "  __syncthreads();\n"
+       << "  Real* const OUT = (Real*)P.out0; const Real* const DAMP = (const Real*)P.in1; (void)DAMP;\n"
+       << "  const int fl = P.flags;\n"
+       << "  const int CH = P.chunk;\n"
+       << "  const int nch = (P.row1 - P.row0 + CH - 1) / CH;\n"
+       << "  const int items = NBG * nch;\n"
+       << "  int slot0 = 0;    // ring slot of the item's input block 0\n"
+       << "  unsigned ph = 0;  // per-slot mbarrier parity\n"
+       << "  for (int t = blockIdx.x; t < items; t += gridDim.x) {\n"
+       << "    const int ci = t / NBG, c0 = (t - ci * NBG) * (NW * BW);\n"
+       << "    const int y0 = P.row0 + ci * CH, y1 = min(y0 + CH, P.row1);\n"
+       << "    const bool it = y0 - H - RX >= 0 && y1 + H - 1 + RX < D0 && c0 - H - RX >= 0 && c0 + NW * BW + H - 1 + RX < D1;\n"
+       << "    const int sh = (c0 - H - RX) & " << AU - 1 << ", cs = c0 - H - RX - sh;\n"
+       << "    const int nrows = y1 - y0 + 2 * H;              // phase-1 rows\n"
+       << "    const int nblk = (nrows + 2 * RX + R - 1) / R;  // input blocks\n"
+       << "    if (tid == 0) {\n"
+       << "      mo_fence_proxy_async();\n"
+       << "      for (int j = 0; j < NBUF && j < nblk; ++j) " << issue("j")
+       << "    }\n"
+       << "    const int q1 = c0 + w * BW - H + l;\n"
+       << "    const int lx = w * BW + l + RX + sh;  // window column of this lane's element\n"
+       << "    const bool lane_out = l >= H && l < 32 - H && q1 < D1;\n";
+    for (int k = 0; k < K; ++k)
+      for (int a = 0; a < NA; ++a) os << "    Real A" << k << "_" << a << " = (Real)0;\n";
+    os << "    int sb = slot0;  // ring slot of input block k / R\n"
+       << "    for (int k = 0; k < nrows; ++k) {\n"
+       << "      const int kr = k & (R - 1);\n"
+       << "      // newest input block this row needs: (k + 2RX) / R (each waited once)\n"
+       << "      if (k == 0) {\n"
+       << "        for (int j = 0; j <= (2 * RX) / R && j < nblk; ++j) {\n"
+       << "          int q = sb + j; while (q >= NBUF) q -= NBUF;\n"
+       << "          mo_mbar_wait(MB + q, (ph >> q) & 1u); ph ^= 1u << q;\n"
+       << "        }\n"
+       << "      } else if (((k + 2 * RX) & (R - 1)) == 0 && (k + 2 * RX) / R < nblk) {\n"
+       << "        int q = sb + (kr + 2 * RX) / R; while (q >= NBUF) q -= NBUF;\n"
+       << "        mo_mbar_wait(MB + q, (ph >> q) & 1u); ph ^= 1u << q;\n"
+       << "      }\n"
+       << "      int ri[" << 2 * RX + 1 << "];\n"
+       << "      #pragma unroll\n"
+       << "      for (int o = 0; o < " << 2 * RX + 1 << "; ++o) {\n"
+       << "        int b = sb + (kr + o) / R; while (b >= NBUF) b -= NBUF;\n"
+       << "        ri[o] = b * R + ((kr + o) & (R - 1));\n"
+       << "      }\n"
+       << "      const int q0 = y0 - H + k;\n"
+       << "      Real c[" << NM << "];\n"
+       << "      if (it) mo_lanes5_" << sfx << "<true>(P, q0, q1, ri, lx, c); else mo_lanes5_" << sfx
+       << "<false>(P, q0, q1, ri, lx, c);\n";
+    // route contributions: value from lane l - o1, into accumulator of row q0 + o0 (slot H + o0)
+    for (int si = 0; si < NM; ++si) {
+      const MLane& m = merged[size_t(si)];
+      int kk = -1;
+      for (int k = 0; k < K; ++k)
+        if (g.chans[size_t(k)].first == m.f && g.chans[size_t(k)].second == m.c) kk = k;
+      if (kk < 0) continue;
+      std::string v = "c[" + std::to_string(si) + "]";
+      if (m.o1 > 0) v = "__shfl_up_sync(0xffffffffu, " + v + ", " + std::to_string(m.o1) + ")";
+      if (m.o1 < 0) v = "__shfl_down_sync(0xffffffffu, " + v + ", " + std::to_string(-m.o1) + ")";
+      os << "      A" << kk << "_" << H + m.o0 << " += " << v << ";\n";
+    }
+    // output row q0 - H is complete
+    os << "      const int y = q0 - H;\n"
+       << "      if (k >= 2 * H && y < y1 && lane_out) {\n"
+       << "        const int e = (y - P.row_lo) * D1 + q1;\n"
+       << "        const bool ex = P.mask && P.mask[e];\n"
+       << "        // staged p of the output pixel: input row k - H + RX\n"
+       << "        int rp = sb + (kr - H + RX) / R; while (rp >= NBUF) rp -= NBUF; rp = rp * R + ((kr - H + RX) & (R - 1));\n";
+    {
+      std::vector<int> fields;
+      for (auto& fc : g.chans)
+        if (std::find(fields.begin(), fields.end(), fc.first) == fields.end()) fields.push_back(fc.first);
+      for (int f : fields) {
+        const int C = P.unknowns[size_t(f)].channels;
+        os << "        const int cb" << f << " = (int)P.ubase[" << f << "] + e * " << C << ";\n";
+      }
+      for (int k = 0; k < K; ++k) {
+        const int f = g.chans[size_t(k)].first, ch = g.chans[size_t(k)].second;
+        const int C = P.unknowns[size_t(f)].channels;
+        const auto* st = staged_of(U + f);
+        os << "        { Real v = ex ? (Real)0 : (Real)2 * A" << k << "_0;\n"
+           << "          em = max(em, MO_EXP_BITS(v));\n"
+           << "          const Real pc = reinterpret_cast<const Real*>(mo_dsm + " << st->first << ")[rp * " << WIN * C
+           << " + lx * " << C << " + " << ch << "];\n"
+           << "          if (fl & MO_F_DAMP) v = v + DAMP[cb" << f << " + " << ch << "] * pc;\n"
+           << "          if ((fl & MO_F_ZEROEXCL) && ex) v = (Real)0;\n"
+           << "          OUT[cb" << f << " + " << ch << "] = v;\n"
+           << "          if (fl & MO_F_REDUCE) acc += (double)(pc * v); }\n";
+      }
+    }
+    os << "      }\n";
+    for (int k = 0; k < K; ++k) {
+      for (int a = 0; a + 1 < NA; ++a) os << "      A" << k << "_" << a << " = A" << k << "_" << a + 1 << ";\n";
+      os << "      A" << k << "_" << NA - 1 << " = (Real)0;\n";
+    }
+    os << "      // release input block k / R after its last row (and everything at the end)\n"
+       << "      const bool last = k + 1 == nrows;\n"
+       << "      if (kr == R - 1 || last) {\n"
+       << "        const int jlo = k / R, jhi = last ? nblk - 1 : k / R;\n"
+       << "        __syncwarp();\n"
+       << "        if (l == 0) {\n"
+       << "          __threadfence_block();\n"
+       << "          for (int j = jlo; j <= jhi; ++j) {\n"
+       << "            int q = slot0 + j; while (q >= NBUF) q -= NBUF;\n"
+       << "            if (atomicAdd(CNT + q, 1u) == NW - 1) {\n"
+       << "              CNT[q] = 0u;\n"
+       << "              if (j + NBUF < nblk) {\n"
+       << "                mo_fence_proxy_async();\n"
+       << "                " << issue("j + NBUF")
+       << "              }\n"
+       << "            }\n"
+       << "          }\n"
+       << "        }\n"
+       << "        if (kr == R - 1) { sb = sb + 1 == NBUF ? 0 : sb + 1; }\n"
+       << "      }\n"
+       << "    }\n"
+       << "    __syncthreads();  // every warp is done with this item's ring slots\n"
+       << "    slot0 = (slot0 + nblk) % NBUF;\n"
+       << "  }\n"
+       << "  if (em == MO_EXP_MASK) atomicOr(&P.state->nonfinite_kernel, 1);\n"
+       << "  if (P.flags & MO_F_REDUCE) mo_reduce_epilogue<Real>(P.red, acc, 0.0, false);\n}\n";
+    ModuleInfo::Tma ti;
+    ti.ok = true;
+    ti.smem = size_t(off);
+    ti.halo = H;
+    ti.band = NW * BW;
+    ti.rx = RX;
+    ti.win = WIN;
+    ti.rows = R;
+    ti.threads = 32 * NW;
+    for (auto& x : slots) ti.slots.push_back({x.first, x.second});
+    tma5_info = ti;
+    staged.clear();
+  }
+  ModuleInfo::Tma tma5_info;
+
   static long long NB(long long D1, int BW) { return (D1 + BW - 1) / BW; }
   bool f64_disabled_tma() const { return std::getenv("MO_B200_NO_TMA") != nullptr; }
   ModuleInfo::Tma tma_info;
@@ -1102,10 +1369,12 @@ struct Gen {
       gather_jtj(g, program(g.jtj, false, &g.dom), "mo_gather_jtj_" + std::to_string(i));
       stream_info = ModuleInfo::Stream{};
       tma_info = ModuleInfo::Tma{};
+      tma5_info = ModuleInfo::Tma{};
       TwoPhase tp = gather_jtj2(g, int(i));
       info.jtj2.push_back({tp.ok, tp.smem, tp.nlanes, tp.H});
       info.jtj3.push_back(stream_info);
       info.jtj4.push_back(tma_info);
+      info.jtj5.push_back(tma5_info);
     }
     for (size_t i = 0; i < P.graph_sets.size(); ++i) {
       const GraphSet& g = P.graph_sets[i];

@@ -30,11 +30,13 @@ struct ModuleInfo {
     bool ok = false;
     size_t smem = 0;
     int halo = 0, band = 0, rx = 0, win = 0;
+    int rows = 8, threads = 256;             // box rows; block size
     std::vector<std::pair<int, int>> slots;  // (view slot, channels)
   };
   std::vector<TwoPhase> jtj2;  // per gather set
   std::vector<Stream> jtj3;    // per gather set
   std::vector<Tma> jtj4;       // per gather set
+  std::vector<Tma> jtj5;       // per gather set: warp-streaming (box rows = rows)
   std::vector<bool> vertex_kernels;  // per graph set: mo_graph_v{jtj,bm}_<g>_<dom> exist
 };
 

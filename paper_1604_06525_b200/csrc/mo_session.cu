@@ -54,9 +54,9 @@ T* dalloc(size_t n) {
   return static_cast<T*>(p);
 }
 
-int vgrid(long long n, int nsm) {
+int vgrid(long long n, int nsm, int per_sm = 4) {
   long long g = (n + MO_THREADS - 1) / MO_THREADS;
-  long long cap = (long long)nsm * 4;  // one wave at <=64 regs x 256 threads
+  long long cap = (long long)nsm * per_sm;  // one wave (4 x 256 threads at <= 64 regs)
   if (g > cap) g = cap;
   return int(std::max<long long>(g, 1));
 }
@@ -93,13 +93,22 @@ class Session final : public SessionBase {
     x_ = dalloc<Real>(n);
     xt_ = dalloc<Real>(n);
     b_ = dalloc<Real>(n);
-    m_ = dalloc<Real>(n);
-    md_ = dalloc<Real>(n);
     damp_ = dalloc<Real>(n);
-    delta_ = dalloc<Real>(n);
-    r_ = dalloc<Real>(n);
-    p_ = dalloc<Real>(n);
-    ap_ = dalloc<Real>(n);
+    // The PCG working set (every vector the inner loop touches 20x per
+    // nonlinear iteration) lives in one arena.  (An L2 access-policy window
+    // over it was measured to make no difference on B200.)
+    {
+      const size_t vn = (n * sizeof(Real) + 255) / 256 * 256;
+      char* base = static_cast<char*>(static_cast<void*>(dalloc<unsigned char>(6 * vn)));
+      arena_ = base;
+      arena_bytes_ = 6 * vn;
+      p_ = reinterpret_cast<Real*>(base);
+      ap_ = reinterpret_cast<Real*>(base + vn);
+      r_ = reinterpret_cast<Real*>(base + 2 * vn);
+      delta_ = reinterpret_cast<Real*>(base + 3 * vn);
+      m_ = reinterpret_cast<Real*>(base + 4 * vn);
+      md_ = reinterpret_cast<Real*>(base + 5 * vn);
+    }
     vtmp_ = dalloc<Real>(n);
     otmp_ = dalloc<Real>(n);
     bd_ = dalloc<double>(n);
@@ -147,7 +156,8 @@ class Session final : public SessionBase {
     cudaStreamSynchronize(st_);
     for (auto& kv : stage_exec_) cudaGraphExecDestroy(kv.second);
     for (void* p : owned_) cudaFree(p);
-    for (Real* p : {x_, xt_, b_, m_, md_, damp_, delta_, r_, p_, ap_, vtmp_, otmp_, resid_}) cudaFree(p);
+    for (Real* p : {x_, xt_, b_, damp_, vtmp_, otmp_, resid_}) cudaFree(p);
+    cudaFree(arena_);
     cudaFree(bd_);
     for (Real* p : arr_) cudaFree(p);
     for (Real* p : comp_) cudaFree(p);
@@ -876,6 +886,9 @@ class Session final : public SessionBase {
     stage_exec_.clear();
   }
 
+  void* arena_ = nullptr;
+  size_t arena_bytes_ = 0;
+
   // ------------------------------------------------------------ launches
   mo_kparams kp_base(const Real* xv, const Real* pv) {
     mo_kparams k;
@@ -974,25 +987,34 @@ class Session final : public SessionBase {
   }
   // Apply kernel variants of gather set i: 0 = the reference's gather program
   // (exact mode always uses it), 1 = two-phase 32x8 tiles, 2 = row-streaming
-  // two-phase bands (2-D domains).
+  // two-phase bands, 3 = TMA-staged row-streaming bands (block-wide 8-row
+  // steps), 4 = TMA-staged warp-streaming bands (2-D domains).
+  static constexpr int kVariants = 5;
+  const ModuleInfo::Tma* tma_info(size_t i, int v) const {
+    if (v == 3 && i < minfo_.jtj4.size()) return &minfo_.jtj4[i];
+    if (v == 4 && i < minfo_.jtj5.size()) return &minfo_.jtj5[i];
+    return nullptr;
+  }
   bool variant_ok(size_t i, int v) const {
     if (v == 0) return true;
     if (P_.exact) return false;
     if (v == 1) return i < minfo_.jtj2.size() && minfo_.jtj2[i].ok;
     if (v == 2) return i < minfo_.jtj3.size() && minfo_.jtj3[i].ok;
-    return i < minfo_.jtj4.size() && minfo_.jtj4[i].ok && tma_capable(i);
+    const ModuleInfo::Tma* t = tma_info(i, v);
+    return t && t->ok && tma_capable(i, *t);
   }
   int variant(size_t i) const {
     if (i < jtj_choice_.size() && variant_ok(i, jtj_choice_[i])) return jtj_choice_[i];
-    for (int v : {3, 2, 1}) if (variant_ok(i, v)) return v;
+    for (int v : {4, 3, 2, 1}) if (variant_ok(i, v)) return v;
     return 0;
   }
   static const char* variant_prefix(int v) {
-    static const char* n[] = {"mo_gather_jtj_", "mo_gather_jtj2_", "mo_gather_jtj3_", "mo_gather_jtj4_"};
+    static const char* n[] = {"mo_gather_jtj_", "mo_gather_jtj2_", "mo_gather_jtj3_", "mo_gather_jtj4_",
+                              "mo_gather_jtj5_"};
     return n[v];
   }
 
-  // ---- TMA tensor maps for the staged apply (variant 3)
+  // ---- TMA tensor maps for the staged applies (variants 3, 4)
   using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -1014,20 +1036,20 @@ class Session final : public SessionBase {
   }
   // Every staged field must be addressable by TMA: 16-byte aligned base
   // (column-layout fields start at ubase[f]) and 16-byte multiple row pitch.
-  bool tma_capable(size_t i) const {
+  bool tma_capable(size_t i, const ModuleInfo::Tma& t) const {
     if (!encoder() || std::getenv("MO_B200_NO_TMA")) return false;
     if (P_.num_cols >= (1LL << 31)) return false;  // 32-bit column indices in the epilogue
     const auto sh = P_.shape_of(P_.gather_sets[i].dom);
     const int U = int(P_.unknowns.size());
-    for (auto [sl, C] : minfo_.jtj4[i].slots) {
+    for (auto [sl, C] : t.slots) {
       if ((sh[1] * C * (long long)sizeof(Real)) % 16) return false;
       if (sl < 2 * U && (P_.ubase[size_t(sl % U)] * (long long)sizeof(Real)) % 16) return false;
     }
     return true;
   }
-  const mo_tmaps& tmaps_for(size_t i, const mo_kparams& kp) {
-    const auto& ti = minfo_.jtj4[i];
-    std::string key = std::to_string(i);
+  const mo_tmaps& tmaps_for(size_t i, int v, const mo_kparams& kp) {
+    const ModuleInfo::Tma& ti = *tma_info(i, v);
+    std::string key = std::to_string(i) + "/" + std::to_string(v);
     for (auto [sl, C] : ti.slots) key += "/" + std::to_string(reinterpret_cast<uintptr_t>(kp.v[sl].p));
     auto it = tmaps_.find(key);
     if (it != tmaps_.end()) return it->second;
@@ -1041,7 +1063,7 @@ class Session final : public SessionBase {
       check(ptr != nullptr, Err::kInternal, "TMA apply: staged field is not bound");
       const cuuint64_t dims[2] = {cuuint64_t(sh[1] * C), cuuint64_t(rows)};
       const cuuint64_t strides[1] = {cuuint64_t(sh[1] * C * (long long)sizeof(Real))};
-      const cuuint32_t box[2] = {cuuint32_t(ti.win * C), 8u};
+      const cuuint32_t box[2] = {cuuint32_t(ti.win * C), cuuint32_t(ti.rows)};
       const cuuint32_t estr[2] = {1u, 1u};
       CUresult r = encoder()(reinterpret_cast<CUtensorMap*>(&T.m[k]),
                              sizeof(Real) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
@@ -1065,7 +1087,8 @@ class Session final : public SessionBase {
     static std::map<std::string, std::vector<int>> cache;
     std::string key = module_key_;
     for (auto& d : P_.dims) key += "/" + std::to_string(d.second);
-    key += sh_.on ? "/s" + std::to_string(sh_.row1 - sh_.row0) : "";
+    // A strip that owns the whole domain shares the unsharded decision.
+    if (sh_.on && sh_.row1 - sh_.row0 != sh_.d0) key += "/s" + std::to_string(sh_.row1 - sh_.row0);
     {
       std::lock_guard<std::mutex> lk(mu);
       auto it = cache.find(key);
@@ -1078,11 +1101,13 @@ class Session final : public SessionBase {
     const char* force = std::getenv("MO_B200_JTJ");
     for (size_t i = 0; i < P_.gather_sets.size(); ++i) {
       jtj_choice_[i] = -1;
+      const std::string fs = force ? force : "";
       const int want = !force ? -1
-                       : std::string(force) == "gather" ? 0
-                       : std::string(force) == "twophase" ? 1
-                       : std::string(force) == "stream" ? 2
-                                                         : 3;
+                       : fs == "gather" ? 0
+                       : fs == "twophase" ? 1
+                       : fs == "stream" ? 2
+                       : fs == "tma" ? 3
+                                     : 4;
       if (want >= 0) {
         jtj_choice_[i] = variant_ok(i, want) ? want : -1;
         if (jtj_choice_[i] >= 0) continue;
@@ -1092,7 +1117,7 @@ class Session final : public SessionBase {
       cudaEvent_t a, b;
       CK(cudaEventCreate(&a));
       CK(cudaEventCreate(&b));
-      for (int v = 0; v < 4; ++v) {
+      for (int v = 0; v < kVariants; ++v) {
         if (!variant_ok(i, v)) continue;
         jtj_choice_[i] = v;
         mo_kparams kp = kp_apply(i, x_, otmp_, 0);
@@ -1121,42 +1146,72 @@ class Session final : public SessionBase {
   std::string jtj_kernel(size_t i) const { return variant_prefix(variant(i)) + std::to_string(i); }
   size_t jtj_smem(size_t i) const {
     const int v = variant(i);
-    return v == 1 ? minfo_.jtj2[i].smem : v == 2 ? minfo_.jtj3[i].smem : v == 3 ? minfo_.jtj4[i].smem : 0;
+    if (const ModuleInfo::Tma* t = tma_info(i, v)) return t->smem;
+    return v == 1 ? minfo_.jtj2[i].smem : v == 2 ? minfo_.jtj3[i].smem : 0;
   }
-  int jtj_halo(size_t i) const { return variant(i) == 3 ? minfo_.jtj4[i].halo : minfo_.jtj3[i].halo; }
-  int jtj_band(size_t i) const { return variant(i) == 3 ? minfo_.jtj4[i].band : minfo_.jtj3[i].band; }
-  // Launch the apply kernel of gather set i (variant 3 also takes the tensor maps).
+  int jtj_threads(size_t i) const {
+    const ModuleInfo::Tma* t = tma_info(i, variant(i));
+    return t ? t->threads : MO_THREADS;
+  }
+  int jtj_halo(size_t i) const {
+    const ModuleInfo::Tma* t = tma_info(i, variant(i));
+    return t ? t->halo : minfo_.jtj3[i].halo;
+  }
+  int jtj_band(size_t i) const {
+    const ModuleInfo::Tma* t = tma_info(i, variant(i));
+    return t ? t->band : minfo_.jtj3[i].band;
+  }
+  int jtj_occupancy(size_t i) {
+    const void* f = mod_.kernel(jtj_kernel(i));
+    const size_t smem = jtj_smem(i);
+    const int threads = jtj_threads(i);
+    auto it = occ_.find(f);
+    if (it != occ_.end()) return it->second;
+    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, f, threads, smem) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = 1;
+    }
+    occ_[f] = n;
+    return n;
+  }
+  // Launch the apply kernel of gather set i (variants 3, 4 also take the tensor maps).
   void launch_apply(size_t i, const mo_kparams& kp, int grid) {
-    if (variant(i) != 3) {
+    const int v = variant(i);
+    if (v < 3) {
       launch_grid(jtj_kernel(i), P_.gather_sets[i].dom, kp, grid, jtj_smem(i));
       return;
     }
     const void* f = mod_.kernel(jtj_kernel(i));
     const size_t smem = jtj_smem(i);
-    occupancy(f, smem);  // sets the dynamic smem attribute once
-    const mo_tmaps& T = tmaps_for(i, kp);
+    jtj_occupancy(i);  // sets the dynamic smem attribute once
+    const mo_tmaps& T = tmaps_for(i, v, kp);
     void* args[] = {const_cast<mo_kparams*>(&kp), const_cast<mo_tmaps*>(&T)};
-    CK(cudaLaunchKernel(f, dim3(grid), dim3(MO_TILE_X, MO_TILE_Y, 1), args, smem, st_));
+    const dim3 block = v == 3 ? dim3(MO_TILE_X, MO_TILE_Y, 1) : dim3(unsigned(jtj_threads(i)), 1, 1);
+    CK(cudaLaunchKernel(f, dim3(grid), block, args, smem, st_));
     ++launches_;
   }
-  // Rows per streaming work item (chunk + 2H a multiple of 8).  Work items
-  // are dealt to a fixed grid of resident blocks, so the apply takes
-  // ceil(items / grid) rounds of ceil((chunk + 2H) / 8) row steps: pick the
-  // chunk minimising that (plus a per-item pipeline fill), larger on ties.
+  // Rows per work item of the streaming variants.  Work items are dealt to a
+  // fixed grid of resident blocks, so an apply takes ceil(items / grid)
+  // rounds of (chunk + 2H) phase-1 rows (variants 2-3 step 8 rows at a time,
+  // chunk + 2H a multiple of 8): pick the chunk minimising that plus a
+  // per-item pipeline fill, the larger one on ties.
   int jtj3_chunk(size_t i) {
     const auto sh = P_.shape_of(P_.gather_sets[i].dom);
     const long long rows = sh_.on ? sh_.row1 - sh_.row0 : sh[0];
     const int halo = jtj_halo(i), band = jtj_band(i);
     const long long nb = (sh[1] + band - 1) / band;
-    const long long grid = (long long)nsm_ * occupancy(mod_.kernel(jtj_kernel(i)), jtj_smem(i));
+    const long long grid = (long long)nsm_ * jtj_occupancy(i);
+    const bool rowwise = variant(i) == 4;
     int best = 0;
     double best_cost = 1e300;
-    for (int m = 1; m <= 16; ++m) {
-      const int ch = 8 * m - 2 * halo;
+    for (int m = 1; m <= (rowwise ? 256 : 16); ++m) {
+      const int ch = rowwise ? m : 8 * m - 2 * halo;
       if (ch <= 0) continue;
       const long long items = nb * ((rows + ch - 1) / ch);
       const long long rounds = (items + grid - 1) / grid;
-      const double cost = double(rounds) * (m + 0.5);
+      const double cost = rowwise ? double(rounds) * (ch + 2 * halo + 4) : double(rounds) * (m + 0.5);
       if (cost <= best_cost) {
         best_cost = cost;
         best = ch;
@@ -1172,7 +1227,7 @@ class Session final : public SessionBase {
     const long long nb = (sh[1] + band - 1) / band;
     const int ch = jtj3_chunk(i);
     const long long items = nb * ((rows + ch - 1) / ch);
-    const long long cap = (long long)nsm_ * occupancy(mod_.kernel(jtj_kernel(i)), jtj_smem(i));
+    const long long cap = (long long)nsm_ * jtj_occupancy(i);
     return int(std::max<long long>(1, std::min(items, cap)));
   }
   mo_kparams kp_apply(size_t i, const Real* pv, Real* out, int flags) {
