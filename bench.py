@@ -122,12 +122,15 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
-def ncu_traffic(config):
-    """dram bytes per J^T J p launch from the committed ncu summary, if any."""
+def ncu_traffic(config, kernel):
+    """dram bytes per J^T J p launch from the committed ncu summary of this
+    round (profiles/ncu_summary.json, one `ncu --set full` capture of the
+    same kernel on the same workload), if any."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
-            return json.load(f)[config]["jtj"]["dram_bytes"]
+            e = json.load(f)[config]["jtj"]
+        return e["dram_bytes"] if e.get("kernel") == kernel else None
     except Exception:
         return None
 
@@ -300,10 +303,11 @@ def run_ours(args):
                    "parallelism": f"{world} axis-0 strips (NCCL halo + fixed-order reductions)" if world > 1 else "1 GPU",
                    "l2": "flushed between timed steps (256 MiB write)", "step": f"solve() = {NL} iterations",
                    "final_cost": r.final_cost},
-        "roofline": {"bound": "hbm", "kernel": "J^T J p apply (generated gather_jtj, fused p'Ap)",
+        "roofline": {"bound": "hbm", "kernel": f"J^T J p apply ({s.apply_kernel(0)}, fused p'Ap)",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None,
-                     "traffic": ncu_traffic(prob.name + (f"_{args.size}" if args.size else "")) if world == 1 else None,
+                     "traffic": ncu_traffic(prob.name + (f"_{args.size}" if args.size else ""), s.apply_kernel(0))
+                     if world == 1 else None,
                      "alg_bytes_per_launch": alg, "alg_bytes_per_elem": per_elem,
                      "avg_launch_us": avg_apply * 1e3, "launches": apply_n,
                      "pcg_update_avg_us": upd_ms / max(upd_n, 1) * 1e3},

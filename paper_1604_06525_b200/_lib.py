@@ -94,6 +94,7 @@ SIGNATURES = {
     "mo_profile_reset": (c_int, [c_void_p]),
     "mo_session_stream": (c_int, [c_void_p, ctypes.POINTER(c_void_p)]),
     "mo_kernel_launches": (c_int, [c_void_p, ctypes.POINTER(c_int64)]),
+    "mo_apply_kernel": (c_int, [c_void_p, c_int, ctypes.c_char_p, ctypes.c_size_t]),
 }
 
 for _name, (_res, _args) in SIGNATURES.items():

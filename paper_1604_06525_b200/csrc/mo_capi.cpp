@@ -370,5 +370,10 @@ int mo_profile_read(mo_session s, int kind, double* ms, int64_t* n) {
 int mo_profile_reset(mo_session s) { SESSION_CALL(s->impl->profile_reset()); }
 int mo_session_stream(mo_session s, void** st) { SESSION_CALL(need(st, "output"); *st = s->impl->stream()); }
 int mo_kernel_launches(mo_session s, int64_t* n) { SESSION_CALL(need(n, "output"); *n = s->impl->launches()); }
+int mo_apply_kernel(mo_session s, int gather_set, char* name, size_t len) {
+  SESSION_CALL(need(name, "output"); const std::string k = s->impl->apply_kernel(gather_set);
+               mo::check(len > k.size(), mo::Err::kShapeMismatch, "name buffer too small");
+               std::memcpy(name, k.c_str(), k.size() + 1));
+}
 
 }  // extern "C"

@@ -563,6 +563,12 @@ class Session final : public SessionBase {
   }
   void* stream() override { return st_; }
   int64_t launches() const override { return launches_; }
+  std::string apply_kernel(int i) override {
+    check(i >= 0 && size_t(i) < P_.gather_sets.size(), Err::kIndexOutOfRange, "no such gather set");
+    ensure_refreshed();
+    tune_apply();
+    return jtj_kernel(size_t(i));
+  }
 
  private:
   using ArrayFieldSize = int64_t;

@@ -1,6 +1,7 @@
 // mo_session.hpp — precision-erased interface of a bound solver session
 // (the device counterpart of minopt::Solver<Real>, solver.hpp:80-635).
 #pragma once
+#include <string>
 
 #include <cstdint>
 #include <memory>
@@ -55,6 +56,7 @@ class SessionBase {
   virtual void profile_reset() = 0;
   virtual void* stream() = 0;
   virtual int64_t launches() const = 0;
+  virtual std::string apply_kernel(int gather_set) = 0;
   // Strip shards: stored rows [lo, hi), owned rows [row0, row1) (all 0 when unsharded).
   virtual void local_layout(int64_t* lo, int64_t* hi, int64_t* row0, int64_t* row1) const = 0;
 };

@@ -355,6 +355,12 @@ class Solver:
     def profile_reset(self):
         call("mo_profile_reset", self._h)
 
+    def apply_kernel(self, gather_set: int = 0) -> str:
+        """Name of the J^T J p kernel the session runs for a gather set."""
+        buf = ctypes.create_string_buffer(128)
+        call("mo_apply_kernel", self._h, int(gather_set), buf, 128)
+        return buf.value.decode()
+
     def kernel_launches(self) -> int:
         n = ctypes.c_int64()
         call("mo_kernel_launches", self._h, ctypes.byref(n))
