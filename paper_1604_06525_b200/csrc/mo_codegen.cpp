@@ -863,8 +863,9 @@ struct Gen {
     const int U = int(P.unknowns.size());
     const int RX = std::max(reach_of(S.evalj, &g.dom), H);
     const int AU = f64 ? 2 : 4;
-    const int R = 2;                               // rows per input block
-    const int NBUF = 2 + (2 * RX + R - 1) / R;     // blocks a row needs + one in flight
+    const int R = 1;  // rows per input block (TMA box); the ring holds NBUF rows
+    int NBUF = 1;
+    while (NBUF < 2 * RX + 2) NBUF *= 2;  // rows a phase-1 row reads + one in flight, power of two
     const int NM = int(merged.size());
     const int RB = f64 ? 8 : 4;
     std::vector<std::pair<int, int>> slots;  // (slot, channels)
@@ -943,7 +944,7 @@ struct Gen {
     const char* mb = std::getenv("MO_B200_JTJ5_MINB");
     const int minb = mb ? std::atoi(mb) : 0;
     std::ostringstream is;  // TMA issue of input block JJ (inline: tensor maps in param space)
-    is << "{ int slot_ = slot0 + (JJ); while (slot_ >= NBUF) slot_ -= NBUF;\n"
+    is << "{ const int slot_ = (slot0 + (JJ)) & (NBUF - 1);\n"
        << "  mo_mbar_expect_tx(MB + slot_, " << tx << "u);\n"
        << "  const int r_ = y0 - H - RX + R * (JJ) - P.row_lo;\n";
     for (size_t i = 0; i < slots.size(); ++i)
@@ -995,25 +996,22 @@ struct Gen {
        << "    const bool lane_out = l >= H && l < 32 - H && q1 < D1;\n";
     for (int k = 0; k < K; ++k)
       for (int a = 0; a < NA; ++a) os << "    Real A" << k << "_" << a << " = (Real)0;\n";
-    os << "    int sb = slot0;  // ring slot of input block k / R\n"
-       << "    for (int k = 0; k < nrows; ++k) {\n"
-       << "      const int kr = k & (R - 1);\n"
-       << "      // newest input block this row needs: (k + 2RX) / R (each waited once)\n"
+    os << "    int sb = slot0;  // ring slot of input row k (one row per block)\n"
+       << "    int e = (y0 - 2 * H - P.row_lo) * D1 + q1;  // element of output row y0 - 2H + k\n"
+       << "    for (int k = 0; k < nrows; ++k, e += D1) {\n"
+       << "      // newest input row this phase-1 row needs: k + 2RX (each waited once)\n"
        << "      if (k == 0) {\n"
-       << "        for (int j = 0; j <= (2 * RX) / R && j < nblk; ++j) {\n"
-       << "          int q = sb + j; while (q >= NBUF) q -= NBUF;\n"
+       << "        for (int j = 0; j <= 2 * RX && j < nblk; ++j) {\n"
+       << "          const int q = (sb + j) & (NBUF - 1);\n"
        << "          mo_mbar_wait(MB + q, (ph >> q) & 1u); ph ^= 1u << q;\n"
        << "        }\n"
-       << "      } else if (((k + 2 * RX) & (R - 1)) == 0 && (k + 2 * RX) / R < nblk) {\n"
-       << "        int q = sb + (kr + 2 * RX) / R; while (q >= NBUF) q -= NBUF;\n"
+       << "      } else if (k + 2 * RX < nblk) {\n"
+       << "        const int q = (sb + 2 * RX) & (NBUF - 1);\n"
        << "        mo_mbar_wait(MB + q, (ph >> q) & 1u); ph ^= 1u << q;\n"
        << "      }\n"
        << "      int ri[" << 2 * RX + 1 << "];\n"
        << "      #pragma unroll\n"
-       << "      for (int o = 0; o < " << 2 * RX + 1 << "; ++o) {\n"
-       << "        int b = sb + (kr + o) / R; while (b >= NBUF) b -= NBUF;\n"
-       << "        ri[o] = b * R + ((kr + o) & (R - 1));\n"
-       << "      }\n"
+       << "      for (int o = 0; o < " << 2 * RX + 1 << "; ++o) ri[o] = (sb + o) & (NBUF - 1);\n"
        << "      const int q0 = y0 - H + k;\n"
        << "      Real c[" << NM << "];\n"
        << "      if (it) mo_lanes5_" << sfx << "<true>(P, q0, q1, ri, lx, c); else mo_lanes5_" << sfx
@@ -1033,17 +1031,17 @@ struct Gen {
     // output row q0 - H is complete
     os << "      const int y = q0 - H;\n"
        << "      if (k >= 2 * H && y < y1 && lane_out) {\n"
-       << "        const int e = (y - P.row_lo) * D1 + q1;\n"
        << "        const bool ex = P.mask && P.mask[e];\n"
-       << "        // staged p of the output pixel: input row k - H + RX\n"
-       << "        int rp = sb + (kr - H + RX) / R; while (rp >= NBUF) rp -= NBUF; rp = rp * R + ((kr - H + RX) & (R - 1));\n";
+       << "        const int rp = (sb + RX - H) & (NBUF - 1);  // staged p of the output pixel: input row k - H + RX\n"
+       << "        Real pa = (Real)0;  // this pixel's p'Ap terms (products in Real, as pcg.hpp:43)\n";
     {
       std::vector<int> fields;
       for (auto& fc : g.chans)
         if (std::find(fields.begin(), fields.end(), fc.first) == fields.end()) fields.push_back(fc.first);
       for (int f : fields) {
         const int C = P.unknowns[size_t(f)].channels;
-        os << "        const int cb" << f << " = (int)P.ubase[" << f << "] + e * " << C << ";\n";
+        os << "        const int cb" << f << " = (int)P.ubase[" << f << "] + e * " << C << ";\n"
+           << "        Real* const o" << f << " = OUT + cb" << f << ";\n";
       }
       for (int k = 0; k < K; ++k) {
         const int f = g.chans[size_t(k)].first, ch = g.chans[size_t(k)].second;
@@ -1055,38 +1053,36 @@ struct Gen {
            << " + lx * " << C << " + " << ch << "];\n"
            << "          if (fl & MO_F_DAMP) v = v + DAMP[cb" << f << " + " << ch << "] * pc;\n"
            << "          if ((fl & MO_F_ZEROEXCL) && ex) v = (Real)0;\n"
-           << "          OUT[cb" << f << " + " << ch << "] = v;\n"
-           << "          if (fl & MO_F_REDUCE) acc += (double)(pc * v); }\n";
+           << "          o" << f << "[" << ch << "] = v;\n"
+           << "          pa += pc * v; }\n";
       }
+      os << "        if (fl & MO_F_REDUCE) acc += (double)pa;\n";
     }
     os << "      }\n";
     for (int k = 0; k < K; ++k) {
       for (int a = 0; a + 1 < NA; ++a) os << "      A" << k << "_" << a << " = A" << k << "_" << a + 1 << ";\n";
       os << "      A" << k << "_" << NA - 1 << " = (Real)0;\n";
     }
-    os << "      // release input block k / R after its last row (and everything at the end)\n"
-       << "      const bool last = k + 1 == nrows;\n"
-       << "      if (kr == R - 1 || last) {\n"
-       << "        const int jlo = k / R, jhi = last ? nblk - 1 : k / R;\n"
-       << "        __syncwarp();\n"
-       << "        if (l == 0) {\n"
-       << "          __threadfence_block();\n"
-       << "          for (int j = jlo; j <= jhi; ++j) {\n"
-       << "            int q = slot0 + j; while (q >= NBUF) q -= NBUF;\n"
-       << "            if (atomicAdd(CNT + q, 1u) == NW - 1) {\n"
-       << "              CNT[q] = 0u;\n"
-       << "              if (j + NBUF < nblk) {\n"
-       << "                mo_fence_proxy_async();\n"
-       << "                " << issue("j + NBUF")
-       << "              }\n"
+    os << "      // release input row k (and every remaining row after the last one)\n"
+       << "      const int jhi = k + 1 == nrows ? nblk - 1 : k;\n"
+       << "      __syncwarp();\n"
+       << "      if (l == 0) {\n"
+       << "        __threadfence_block();\n"
+       << "        for (int j = k; j <= jhi; ++j) {\n"
+       << "          const int q = (slot0 + j) & (NBUF - 1);\n"
+       << "          if (atomicAdd(CNT + q, 1u) == NW - 1) {\n"
+       << "            CNT[q] = 0u;\n"
+       << "            if (j + NBUF < nblk) {\n"
+       << "              mo_fence_proxy_async();\n"
+       << "              " << issue("j + NBUF")
        << "            }\n"
        << "          }\n"
        << "        }\n"
-       << "        if (kr == R - 1) { sb = sb + 1 == NBUF ? 0 : sb + 1; }\n"
        << "      }\n"
+       << "      sb = (sb + 1) & (NBUF - 1);\n"
        << "    }\n"
        << "    __syncthreads();  // every warp is done with this item's ring slots\n"
-       << "    slot0 = (slot0 + nblk) % NBUF;\n"
+       << "    slot0 = (slot0 + nblk) & (NBUF - 1);\n"
        << "  }\n"
        << "  if (em == MO_EXP_MASK) atomicOr(&P.state->nonfinite_kernel, 1);\n"
        << "  if (P.flags & MO_F_REDUCE) mo_reduce_epilogue<Real>(P.red, acc, 0.0, false);\n}\n";
@@ -1120,7 +1116,8 @@ struct Gen {
        << ind << "const int fl = P.flags;\n"
        << ind << "// staged p of the output row (input row y = block s row w - H + RX)\n"
        << ind << "int rp = ss + ((w - H + RX) >> 3); if (rp >= NBUF) rp -= NBUF; rp = rp * 8 + ((w - H + RX) & 7);\n"
-       << ind << "const int lx = l + RX + sh; (void)lx;\n";
+       << ind << "const int lx = l + RX + sh; (void)lx;\n"
+       << ind << "Real pa = (Real)0;  // this pixel's p'Ap terms (products in Real, as pcg.hpp:43)\n";
     std::vector<int> fields;
     for (auto& fc : g.chans)
       if (std::find(fields.begin(), fields.end(), fc.first) == fields.end()) fields.push_back(fc.first);
@@ -1149,8 +1146,9 @@ struct Gen {
       os << ind << "  if (fl & MO_F_DAMP) v = v + DAMP[cb" << f << " + " << ch << "] * pc;\n"
          << ind << "  if ((fl & MO_F_ZEROEXCL) && ex) v = (Real)0;\n"
          << ind << "  o" << f << "[" << ch << "] = v;\n"
-         << ind << "  if (fl & MO_F_REDUCE) acc += (double)(pc * v); }\n";
+         << ind << "  pa += pc * v; }\n";
     }
+    os << ind << "if (fl & MO_F_REDUCE) acc += (double)pa;\n";
   }
 
   // Phase-2 gather + apply epilogue of the streaming kernels: out(f,c)(q) =
