@@ -308,7 +308,7 @@ struct Gen {
 
   static std::string kbegin(const std::string& kname) {
     return "extern \"C\" __global__ void __launch_bounds__(MO_THREADS) " + kname +
-           "(const __grid_constant__ mo_kparams P) {\n";
+           "(const __grid_constant__ mo_kparams P) {\n  MO_PDL_ENTRY();\n";
   }
 
   // --------------------------------------------------------- grid kernels
@@ -566,6 +566,7 @@ struct Gen {
     os << "extern \"C\" __global__ void __launch_bounds__(MO_THREADS" << (minb > 0 ? ", " + std::to_string(minb) : "")
        << ") " << kn
        << "(const __grid_constant__ mo_kparams P) {\n"
+       << "  MO_PDL_ENTRY();\n"
        << "  if ((P.flags & MO_F_SKIPDONE) && P.state->done) return;\n"
        << "  extern __shared__ __align__(16) unsigned char mo_smem[];\n"
        << "  Real* CL = reinterpret_cast<Real*>(mo_smem);  // [" << NM << " merged lanes][" << NE << " elements]\n"
@@ -720,6 +721,7 @@ struct Gen {
     const int minb = mb ? std::atoi(mb) : 4;
     os << "extern \"C\" __global__ void __launch_bounds__(MO_THREADS" << (minb > 0 ? ", " + std::to_string(minb) : "")
        << ") " << kn << "(const __grid_constant__ mo_kparams P, const __grid_constant__ mo_tmaps T) {\n"
+       << "  MO_PDL_ENTRY();\n"
        << "  if ((P.flags & MO_F_SKIPDONE) && P.state->done) return;\n"
        << "  Real* CL = reinterpret_cast<Real*>(mo_dsm);  // [" << NM << " merged lanes][" << RING << " rows][32]\n"
        << "  unsigned long long* MB = reinterpret_cast<unsigned long long*>(mo_dsm + " << mbar_off << ");\n"
@@ -958,6 +960,7 @@ struct Gen {
     };
     os << "extern \"C\" __global__ void __launch_bounds__(" << 32 * NW << (minb > 0 ? ", " + std::to_string(minb) : "")
        << ") " << kn << "(const __grid_constant__ mo_kparams P, const __grid_constant__ mo_tmaps T) {\n"
+       << "  MO_PDL_ENTRY();\n"
        << "  if ((P.flags & MO_F_SKIPDONE) && P.state->done) return;\n"
        << "  unsigned long long* MB = reinterpret_cast<unsigned long long*>(mo_dsm + " << mbar_off << ");\n"
        << "  unsigned* CNT = reinterpret_cast<unsigned*>(mo_dsm + " << cnt_off << ");\n"
@@ -1206,6 +1209,7 @@ struct Gen {
     const int minb = mb ? std::atoi(mb) : 4;
     os << "extern \"C\" __global__ void __launch_bounds__(MO_THREADS" << (minb > 0 ? ", " + std::to_string(minb) : "")
        << ") " << kn << "(const __grid_constant__ mo_kparams P) {\n"
+       << "  MO_PDL_ENTRY();\n"
        << "  if ((P.flags & MO_F_SKIPDONE) && P.state->done) return;\n"
        << "  extern __shared__ __align__(16) unsigned char mo_smem[];\n"
        << "  Real* CL = reinterpret_cast<Real*>(mo_smem);  // [" << NM << " merged lanes][" << RING << " rows][32]\n"

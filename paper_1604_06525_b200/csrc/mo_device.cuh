@@ -109,6 +109,12 @@ struct mo_tmaps {
   mo_tmap m[MO_MAX_TMAPS];
 };
 
+// Programmatic dependent launch: every kernel first waits for its stream
+// predecessor to complete (memory visible), then lets its own successor be
+// scheduled, so block launch and ramp-up of kernel N+1 overlap kernel N's
+// tail.  Harmless when launched without the PDL attribute.
+#define MO_PDL_ENTRY() asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory")
+
 // ---------------------------------------------------------------- TMA / mbarrier
 __device__ __forceinline__ unsigned mo_smem_addr(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);

@@ -24,6 +24,7 @@ __device__ __forceinline__ bool halo_at(const unsigned char* cm, long long i) { 
 // finalisation every rank (pcg.hpp scalar logic via mo_finalize).
 template <class Real>
 __global__ void k_global_fin(mo_state* st, const double* rb, int world, int op, int arg) {
+  MO_PDL_ENTRY();
   if (threadIdx.x != 0) return;
   if ((op == MO_FIN_PCG_ALPHA || op == MO_FIN_PCG_BETA) && st->done) return;
   double t = 0, t2 = 0;
@@ -34,10 +35,12 @@ __global__ void k_global_fin(mo_state* st, const double* rb, int world, int op, 
   mo_finalize<Real>(st, op, arg, t, t2);
 }
 __global__ void k_flags_out(mo_state* st) {
+  MO_PDL_ENTRY();
   st->sums[4] = double(st->nonfinite_kernel);
   st->sums[5] = double(st->any_nonzero);
 }
 __global__ void k_flags_in(mo_state* st, const double* rb, int world) {
+  MO_PDL_ENTRY();
   int nf = 0, nz = 0;
   for (int r = 0; r < world; ++r) {
     nf |= rb[2 * r] != 0.0;
@@ -47,8 +50,19 @@ __global__ void k_flags_in(mo_state* st, const double* rb, int world) {
   st->any_nonzero = nz;
 }
 __global__ void k_or_bits(unsigned char* p, long long n, unsigned char bits) {
+  MO_PDL_ENTRY();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     p[i] |= bits;
+}
+
+// Jacobi z = r / m (pcg.hpp:79, 117, 124), bitwise.  r == +-0 with m > 0
+// gives r itself (the IEEE quotient): a zero numerator otherwise sends every
+// column through the division's slow path (FCHK), and the residual of a
+// matrix-free solve is exactly zero on most of the domain while it spreads
+// from the data terms (measured: the slow path was ~40% of k_pcg_update).
+template <class Real>
+__device__ __forceinline__ Real mo_precond_div(Real r, Real m) {
+  return (r == Real(0) && m > Real(0)) ? r : r / m;
 }
 
 // delta = 0; r = b; z = r/m; p = z; rz = r'z   (pcg.hpp:75-97)
@@ -57,6 +71,7 @@ __global__ void __launch_bounds__(MO_THREADS)
 k_pcg_init(mo_red R, long long n, const unsigned char* cm, const Real* __restrict__ b,
            const Real* __restrict__ md, Real* __restrict__ delta, Real* __restrict__ r,
            Real* __restrict__ p, int precond) {
+  MO_PDL_ENTRY();
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     R.state->done = 0;
     R.state->iters = 0;
@@ -69,7 +84,7 @@ k_pcg_init(mo_red R, long long n, const unsigned char* cm, const Real* __restric
     if (halo_at(cm, i)) continue;
     const bool ex = ex_at(cm, i);
     const Real ri = ex ? Real(0) : b[i];
-    const Real zi = ex ? Real(0) : (precond ? ri / md[i] : ri);
+    const Real zi = ex ? Real(0) : (precond ? mo_precond_div(ri, md[i]) : ri);
     delta[i] = Real(0);
     r[i] = ri;
     p[i] = zi;
@@ -115,7 +130,7 @@ __device__ __forceinline__ double pcg_update1(Real alpha, unsigned char m, Real&
   }
   d = d + alpha * p;
   r = r - alpha * ap;
-  const Real z = precond ? r / md : r;
+  const Real z = precond ? mo_precond_div(r, md) : r;
   return double(r * z);
 }
 
@@ -124,6 +139,7 @@ __global__ void __launch_bounds__(MO_THREADS)
 k_pcg_update(mo_red R, long long n, const unsigned char* cm, const Real* __restrict__ md,
              Real* __restrict__ delta, Real* __restrict__ r, const Real* __restrict__ p,
              const Real* __restrict__ ap, int precond) {
+  MO_PDL_ENTRY();
   if (R.state->done) return;
   const Real alpha = Real(R.state->alpha);
   double acc = 0;
@@ -150,7 +166,7 @@ template <class Real>
 __device__ __forceinline__ Real pcg_p1(Real beta, unsigned char m, Real r, Real md, Real p, int precond) {
   if (m & 2) return p;  // halo column: refreshed by the exchange
   if (m & 1) return Real(0);
-  const Real z = precond ? r / md : r;
+  const Real z = precond ? mo_precond_div(r, md) : r;
   return z + beta * p;
 }
 
@@ -158,6 +174,7 @@ template <class Real>
 __global__ void __launch_bounds__(MO_THREADS)
 k_pcg_p(const mo_state* st, long long n, const unsigned char* cm, const Real* __restrict__ md,
         const Real* __restrict__ r, Real* __restrict__ p, int precond) {
+  MO_PDL_ENTRY();
   if (st->done) return;
   const Real beta = Real(st->beta);
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -182,6 +199,7 @@ template <class Real>
 __global__ void __launch_bounds__(MO_THREADS)
 k_apply_finish(mo_red R, long long n, const unsigned char* cm, const Real* __restrict__ p,
                const Real* __restrict__ damp, Real* __restrict__ ap, int flags) {
+  MO_PDL_ENTRY();
   if ((flags & MO_F_REDUCE) && R.state->done) return;
   double acc = 0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -199,6 +217,7 @@ k_apply_finish(mo_red R, long long n, const unsigned char* cm, const Real* __res
 template <class Real>
 __global__ void __launch_bounds__(MO_THREADS)
 k_bm_patch(mo_red R, long long n, const unsigned char* cm, Real* __restrict__ b, Real* __restrict__ m) {
+  MO_PDL_ENTRY();
   double cnt = 0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
@@ -217,6 +236,7 @@ k_bm_patch(mo_red R, long long n, const unsigned char* cm, Real* __restrict__ b,
 // Per-column exclusion from a per-element mask (solver.hpp:149-157).
 __global__ void __launch_bounds__(MO_THREADS)
 k_colmask(long long nelem, int C, const unsigned char* __restrict__ mask, unsigned char* __restrict__ cm) {
+  MO_PDL_ENTRY();
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nelem;
        e += (long long)gridDim.x * blockDim.x) {
     const unsigned char v = mask[e];
@@ -228,6 +248,7 @@ k_colmask(long long nelem, int C, const unsigned char* __restrict__ mask, unsign
 template <class Real>
 __global__ void __launch_bounds__(MO_THREADS)
 k_lm_base_diag(long long n, const Real* __restrict__ m, double* __restrict__ bd, double dmin, double dmax) {
+  MO_PDL_ENTRY();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     double v = double(m[i]) / 2.0;
@@ -240,6 +261,7 @@ template <class Real>
 __global__ void __launch_bounds__(MO_THREADS)
 k_lm_damp(const mo_state* st, long long n, const unsigned char* cm, const Real* __restrict__ m,
           const double* __restrict__ bd, Real* __restrict__ damp, Real* __restrict__ md) {
+  MO_PDL_ENTRY();
   const double s = 2.0 / st->mu;  // mu staged by the host before each trial
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
@@ -256,6 +278,7 @@ template <class Real>
 __global__ void __launch_bounds__(MO_THREADS)
 k_xtrial(mo_state* st, long long n, const unsigned char* cm, Real* __restrict__ x,
          const Real* __restrict__ delta, Real* __restrict__ xt, int in_place, int cost_slot) {
+  MO_PDL_ENTRY();
   if (in_place && (st->nonfinite || !mo_finite(st->sums[cost_slot]))) return;
   bool nz = false;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -277,6 +300,7 @@ template <class Real>
 __global__ void __launch_bounds__(MO_THREADS)
 k_lm_predicted(mo_red R, long long n, const unsigned char* cm, const Real* __restrict__ b, const Real* __restrict__ delta,
                const Real* __restrict__ ap) {
+  MO_PDL_ENTRY();
   double s1 = 0, s2 = 0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
@@ -305,6 +329,7 @@ __global__ void __launch_bounds__(MO_THREADS)
 k_graph_gather(long long nverts, const int* __restrict__ vptr, const int* __restrict__ vedge,
                const int* __restrict__ verts, int arity, const Real* __restrict__ contrib, int NO,
                const mo_gather_out* __restrict__ outs, Real* dst0, Real* dst1) {
+  MO_PDL_ENTRY();
   for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < nverts;
        v += (long long)gridDim.x * blockDim.x) {
     const int j0 = vptr[v], j1 = vptr[v + 1];

@@ -255,7 +255,7 @@ class Session final : public SessionBase {
         for (size_t f = 0; f < P_.unknowns.size(); ++f) {
           if (!(P_.unknowns[f].dom == P_.exclude_kernels[i].dom)) continue;
           long long ne = lext(P_.unknowns[f].dom);
-          k_colmask<<<vgrid(ne, nsm_), MO_THREADS, 0, st_>>>(ne, P_.unknowns[f].channels, masks_[i],
+          kl(k_colmask, dim3(vgrid(ne, nsm_)), dim3(MO_THREADS), ne, P_.unknowns[f].channels, masks_[i],
                                                            colmask_ + P_.ubase[f]);
           ++launches_;
         }
@@ -415,7 +415,7 @@ class Session final : public SessionBase {
           normal_device();
           pcg_body(false);
           CK(cudaMemsetAsync(&state_->any_nonzero, 0, sizeof(int), st_));
-          k_xtrial<Real><<<vg, MO_THREADS, 0, st_>>>(state_, n, colmask_, x_, delta_, xt_, 1, SLOT_COST);
+          kl(k_xtrial<Real>, dim3(vg), dim3(MO_THREADS), state_, n, colmask_, x_, delta_, xt_, 1, SLOT_COST);
           ++launches_;
           exchange_cols(x_);
           cost_at(x_, SLOT_COST + 1);
@@ -463,7 +463,7 @@ class Session final : public SessionBase {
         refresh_device();
         cost_at(x_, SLOT_COST);
         normal_device();
-        k_lm_base_diag<Real><<<vg, MO_THREADS, 0, st_>>>(n, m_, bd_, cfg_.lm_diag_min, cfg_.lm_diag_max);
+        kl(k_lm_base_diag<Real>, dim3(vg), dim3(MO_THREADS), n, m_, bd_, cfg_.lm_diag_min, cfg_.lm_diag_max);
         ++launches_;
       });
       sync_state();
@@ -483,17 +483,17 @@ class Session final : public SessionBase {
         *mu_h_ = mu;
         CK(cudaMemcpyAsync(&state_->mu, mu_h_, sizeof(double), cudaMemcpyHostToDevice, st_));
         run_stage(kStageLMTrial, [&] {
-          k_lm_damp<Real><<<vg, MO_THREADS, 0, st_>>>(state_, n, colmask_, m_, bd_, damp_, md_);
+          kl(k_lm_damp<Real>, dim3(vg), dim3(MO_THREADS), state_, n, colmask_, m_, bd_, damp_, md_);
           ++launches_;
           pcg_body(true);
           CK(cudaMemsetAsync(&state_->any_nonzero, 0, sizeof(int), st_));
-          k_xtrial<Real><<<vg, MO_THREADS, 0, st_>>>(state_, n, colmask_, x_, delta_, xt_, 0, SLOT_COST);
+          kl(k_xtrial<Real>, dim3(vg), dim3(MO_THREADS), state_, n, colmask_, x_, delta_, xt_, 0, SLOT_COST);
           ++launches_;
           exchange_cols(xt_);
           cost_at(xt_, SLOT_COST + 1);
           exchange_cols(delta_);
           apply(delta_, ap_, 0);  // undamped model curvature (solver.hpp:467)
-          k_lm_predicted<Real><<<vg, MO_THREADS, 0, st_>>>(red(0, vg, MO_FIN_STORE2, SLOT_PRED), n, colmask_, b_,
+          kl(k_lm_predicted<Real>, dim3(vg), dim3(MO_THREADS), red(0, vg, MO_FIN_STORE2, SLOT_PRED), n, colmask_, b_,
                                                            delta_, ap_);
           ++launches_;
           reduce_done(MO_FIN_STORE2, SLOT_PRED);
@@ -686,14 +686,14 @@ class Session final : public SessionBase {
   void reduce_done(int op, int arg) {
     if (!sh_.on) return;
     comm_->allgather(&state_->sums[4], rankbuf_, 2, st_);
-    k_global_fin<Real><<<1, 32, 0, st_>>>(state_, rankbuf_, comm_->world, op, arg);
+    kl(k_global_fin<Real>, dim3(1), dim3(32), state_, rankbuf_, comm_->world, op, arg);
     ++launches_;
   }
   void reduce_flags() {
     if (!sh_.on) return;
-    k_flags_out<<<1, 1, 0, st_>>>(state_);
+    kl(k_flags_out, dim3(1), dim3(1), state_);
     comm_->allgather(&state_->sums[4], rankbuf_, 2, st_);
-    k_flags_in<<<1, 1, 0, st_>>>(state_, rankbuf_, comm_->world);
+    kl(k_flags_in, dim3(1), dim3(1), state_, rankbuf_, comm_->world);
     launches_ += 2;
   }
   void mark_halo_cols() {
@@ -702,8 +702,8 @@ class Session final : public SessionBase {
       const long long top = (sh_.row0 - sh_.lo) * rowc, own = (sh_.row1 - sh_.row0) * rowc;
       const long long bot = (sh_.hi - sh_.row1) * rowc;
       unsigned char* base = colmask_ + P_.ubase[f];
-      if (top) k_or_bits<<<vgrid(top, nsm_), MO_THREADS, 0, st_>>>(base, top, 2);
-      if (bot) k_or_bits<<<vgrid(bot, nsm_), MO_THREADS, 0, st_>>>(base + top + own, bot, 2);
+      if (top) kl(k_or_bits, dim3(vgrid(top, nsm_)), dim3(MO_THREADS), base, top, 2);
+      if (bot) kl(k_or_bits, dim3(vgrid(bot, nsm_)), dim3(MO_THREADS), base + top + own, bot, 2);
       launches_ += (top ? 1 : 0) + (bot ? 1 : 0);
     }
   }
@@ -896,6 +896,37 @@ class Session final : public SessionBase {
   size_t arena_bytes_ = 0;
 
   // ------------------------------------------------------------ launches
+  // Every kernel of the solver goes through kl()/klc().  MO_B200_PDL=1 adds
+  // the programmatic-stream-serialization attribute (MO_PDL_ENTRY in each
+  // kernel makes that safe) so kernel N+1 is scheduled while kernel N drains;
+  // measured 3-8% slower on B200 for these single-wave kernels, so off.
+  static bool pdl_on() {
+    static const bool on = std::getenv("MO_B200_PDL") != nullptr;
+    return on;
+  }
+  cudaLaunchConfig_t launch_cfg(dim3 grid, dim3 block, size_t smem, cudaLaunchAttribute* at) const {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = grid;
+    lc.blockDim = block;
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st_;
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = pdl_on() ? 1 : 0;
+    return lc;
+  }
+  template <class... K, class... A>
+  void kl(void (*k)(K...), dim3 grid, dim3 block, A&&... a) {
+    cudaLaunchAttribute at[1];
+    cudaLaunchConfig_t lc = launch_cfg(grid, block, 0, at);
+    CK(cudaLaunchKernelEx(&lc, k, std::forward<A>(a)...));
+  }
+  void klc(const void* f, dim3 grid, dim3 block, void** args, size_t smem) {
+    cudaLaunchAttribute at[1];
+    cudaLaunchConfig_t lc = launch_cfg(grid, block, smem, at);
+    CK(cudaLaunchKernelExC(&lc, f, args));
+  }
   mo_kparams kp_base(const Real* xv, const Real* pv) {
     mo_kparams k;
     std::memset(&k, 0, sizeof k);
@@ -988,7 +1019,7 @@ class Session final : public SessionBase {
     if (grid <= 0) grid = grid_blocks(name, d, smem);
     dim3 block = d.dims.size() <= 1 ? dim3(MO_THREADS, 1, 1) : dim3(MO_TILE_X, MO_TILE_Y, 1);
     void* args[] = {const_cast<mo_kparams*>(&kp)};
-    CK(cudaLaunchKernel(f, dim3(grid), block, args, smem, st_));
+    klc(f, dim3(grid), block, args, smem);
     ++launches_;
   }
   // Apply kernel variants of gather set i: 0 = the reference's gather program
@@ -1195,7 +1226,7 @@ class Session final : public SessionBase {
     const mo_tmaps& T = tmaps_for(i, v, kp);
     void* args[] = {const_cast<mo_kparams*>(&kp), const_cast<mo_tmaps*>(&T)};
     const dim3 block = v == 3 ? dim3(MO_TILE_X, MO_TILE_Y, 1) : dim3(unsigned(jtj_threads(i)), 1, 1);
-    CK(cudaLaunchKernel(f, dim3(grid), block, args, smem, st_));
+    klc(f, dim3(grid), block, args, smem);
     ++launches_;
   }
   // Rows per work item of the streaming variants.  Work items are dealt to a
@@ -1249,7 +1280,7 @@ class Session final : public SessionBase {
     const void* f = mod_.kernel(name);
     if (grid <= 0) grid = edge_blocks(name, gi);
     void* args[] = {const_cast<mo_kparams*>(&kp)};
-    CK(cudaLaunchKernel(f, dim3(grid), dim3(MO_THREADS), args, 0, st_));
+    klc(f, dim3(grid), dim3(MO_THREADS), args, 0);
     ++launches_;
   }
   mo_red red(int base, int total, int op, int arg) {
@@ -1285,7 +1316,7 @@ class Session final : public SessionBase {
       const void* f = mod_.kernel(name);
       long long g = std::min<long long>((gd.nverts + MO_THREADS - 1) / MO_THREADS, (long long)nsm_ * occupancy(f));
       void* args[] = {&kp};
-      CK(cudaLaunchKernel(f, dim3(unsigned(std::max<long long>(g, 1))), dim3(MO_THREADS), args, 0, st_));
+      klc(f, dim3(unsigned(std::max<long long>(g, 1))), dim3(MO_THREADS), args, 0);
       ++launches_;
     }
   }
@@ -1297,7 +1328,7 @@ class Session final : public SessionBase {
     const int NO = int(bm ? g.bm.outputs.size() : g.jtj.outputs.size());
     if (NO == 0) return;
     for (auto& gd : gs.doms) {
-      k_graph_gather<Real><<<vgrid(gd.nverts, nsm_), MO_THREADS, 0, st_>>>(
+      kl(k_graph_gather<Real>, dim3(vgrid(gd.nverts, nsm_)), dim3(MO_THREADS), 
           gd.nverts, gd.vptr, gd.vedge, gd0.d_verts, gd0.arity, gs.contrib, NO, bm ? gd.outs_bm : gd.outs_jtj,
           dst0, dst1);
       ++launches_;
@@ -1370,7 +1401,7 @@ class Session final : public SessionBase {
         launch_edges("mo_graph_bm_" + std::to_string(i), int(i), kp);
         gather_graph(int(i), true, b_, m_);
       }
-      k_bm_patch<Real><<<vgrid(n, nsm_), MO_THREADS, 0, st_>>>(red(0, vgrid(n, nsm_), MO_FIN_UNCONSTRAINED, 0), n,
+      kl(k_bm_patch<Real>, dim3(vgrid(n, nsm_)), dim3(MO_THREADS), red(0, vgrid(n, nsm_), MO_FIN_UNCONSTRAINED, 0), n,
                                                                 colmask_, b_, m_);
       ++launches_;
     } else if (P_.gather_sets.empty()) {
@@ -1420,7 +1451,7 @@ class Session final : public SessionBase {
         gather_graph(int(i), false, out, nullptr);
       }
       if (flags & (MO_F_DAMP | MO_F_REDUCE | MO_F_ZEROEXCL)) {
-        k_apply_finish<Real><<<vgrid(n, nsm_), MO_THREADS, 0, st_>>>(red(0, vgrid(n, nsm_), MO_FIN_PCG_ALPHA, 0), n,
+        kl(k_apply_finish<Real>, dim3(vgrid(n, nsm_)), dim3(MO_THREADS), red(0, vgrid(n, nsm_), MO_FIN_PCG_ALPHA, 0), n,
                                                                      colmask_, pv, damp_, out, flags);
         ++launches_;
       }
@@ -1435,7 +1466,7 @@ class Session final : public SessionBase {
     const int vg = vgrid(n, nsm_);
     const Real* mdv = lm ? md_ : m_;
     const int pre = cfg_.use_preconditioner ? 1 : 0;
-    k_pcg_init<Real><<<vg, MO_THREADS, 0, st_>>>(red(0, vg, MO_FIN_PCG_INIT, 0), n, colmask_, b_, mdv, delta_, r_, p_, pre);
+    kl(k_pcg_init<Real>, dim3(vg), dim3(MO_THREADS), red(0, vg, MO_FIN_PCG_INIT, 0), n, colmask_, b_, mdv, delta_, r_, p_, pre);
     ++launches_;
     reduce_done(MO_FIN_PCG_INIT, 0);
     exchange_cols(p_);  // strips: neighbours' p rows for the stencil apply
@@ -1447,10 +1478,10 @@ class Session final : public SessionBase {
       prof_begin(1);
       // (A cooperative single-kernel update + direction with a grid barrier
       // was measured slower on B200 than this pair at every config size.)
-      k_pcg_update<Real><<<vg, MO_THREADS, 0, st_>>>(red(0, vg, MO_FIN_PCG_BETA, 0), n, colmask_, mdv, delta_, r_, p_, ap_, pre);
+      kl(k_pcg_update<Real>, dim3(vg), dim3(MO_THREADS), red(0, vg, MO_FIN_PCG_BETA, 0), n, colmask_, mdv, delta_, r_, p_, ap_, pre);
       ++launches_;
       reduce_done(MO_FIN_PCG_BETA, 0);
-      k_pcg_p<Real><<<vg, MO_THREADS, 0, st_>>>(state_, n, colmask_, mdv, r_, p_, pre);
+      kl(k_pcg_p<Real>, dim3(vg), dim3(MO_THREADS), state_, n, colmask_, mdv, r_, p_, pre);
       ++launches_;
       exchange_cols(p_);
       prof_end(1);
