@@ -1122,7 +1122,8 @@ class Session final : public SessionBase {
     // runs the same kernel (bitwise run-to-run reproducibility).
     static std::mutex mu;
     static std::map<std::string, std::vector<int>> cache;
-    std::string key = module_key_;
+    const char* force = std::getenv("MO_B200_JTJ");
+    std::string key = module_key_ + (force ? std::string("/force:") + force : "");
     for (auto& d : P_.dims) key += "/" + std::to_string(d.second);
     // A strip that owns the whole domain shares the unsharded decision.
     if (sh_.on && sh_.row1 - sh_.row0 != sh_.d0) key += "/s" + std::to_string(sh_.row1 - sh_.row0);
@@ -1135,7 +1136,6 @@ class Session final : public SessionBase {
       }
     }
     jtj_choice_.assign(P_.gather_sets.size(), 0);
-    const char* force = std::getenv("MO_B200_JTJ");
     for (size_t i = 0; i < P_.gather_sets.size(); ++i) {
       jtj_choice_[i] = -1;
       const std::string fs = force ? force : "";

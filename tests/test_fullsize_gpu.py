@@ -1,0 +1,97 @@
+"""Full-size parity (BASELINE.json configs at their own sizes) against the
+UNMODIFIED reference (oracle/_ref/ref_driver, all host threads) on identical
+seeded inputs, for every J^T J p kernel variant the session can run.
+
+The small golden cases pin the semantics; these check that the row-streaming
+/ TMA kernels, their work-item decomposition and ring bookkeeping are right
+where they actually run (1024^2 ARAP: many bands and chunks, interior and
+border items), per element within the north_star tolerances.  The
+reference's own J^T J v is exact ground truth here, computed on the box's
+CPU in ~1 s.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from helpers import assert_close_vec
+from oracle import pyoracle
+from paper_1604_06525_b200 import Method, Precision, SolveConfig, Solver, load_plan, workloads
+
+pytestmark = pytest.mark.gpu
+
+VARIANTS = ["gather", "twophase", "stream", "tma", "warp"]
+PREFIX = {"gather": "mo_gather_jtj_", "twophase": "mo_gather_jtj2_", "stream": "mo_gather_jtj3_",
+          "tma": "mo_gather_jtj4_", "warp": "mo_gather_jtj5_"}
+THREADS = os.cpu_count() or 1
+
+
+def _cfg(prob, prec, nl=2, lin=10):
+    return SolveConfig(method=Method.kLevenbergMarquardt if prob.method == "lm" else Method.kGaussNewton,
+                       precision=Precision.kF32 if prec == "f32" else Precision.kF64,
+                       nonlinear_iters=nl, linear_iters=lin, pcg_rel_tol=0.0, pcg_abs_tol=0.0, cost_stop_tol=0.0)
+
+
+@pytest.fixture(scope="module")
+def arap1024():
+    prob = workloads.arap_warp(1024, 1024)
+    data = prob.data(np.float32)
+    v = (workloads.uniform(99, data.x.size) - 0.5).astype(np.float32)
+    ref = pyoracle.run_ref(prob.energy, data, ["cost", "normal", "jtj"], dims=prob.dims, prec="f32",
+                           exec_mode="par", threads=THREADS, v=v)
+    return prob, v, ref
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_arap_1024_apply_matches_reference(arap1024, variant, monkeypatch):
+    prob, v, ref = arap1024
+    monkeypatch.setenv("MO_B200_JTJ", variant)
+    s = Solver(load_plan(prob.name, _cfg(prob, "f32"), prob.dims), prob.data(np.float32))
+    k = s.apply_kernel(0)
+    if not k.startswith(PREFIX[variant]):
+        pytest.skip(f"{variant} not available here (runs {k})")
+    assert_close_vec(s.apply_jtj(v), ref["jtj"], 1e-5, f"2 J^T J v, 1024^2 ARAP [{k}]")
+    assert abs(s.cost() - float(ref["cost"][0])) <= 2e-5 * abs(float(ref["cost"][0]))
+    s.build_normal()
+    assert_close_vec(s.rhs(), ref["b"], 1e-5, "b")
+    assert_close_vec(s.precond(), ref["m"], 1e-5, "m")
+
+
+def test_arap_1024_variants_agree_on_a_solve(monkeypatch):
+    """Whole GN solves at full size: every variant's trajectory within the
+    north_star 1e-4 of the reference's, identical PCG iteration counts."""
+    prob = workloads.arap_warp(1024, 1024)
+    data = prob.data(np.float32)
+    ref = pyoracle.run_ref(prob.energy, data, ["solve"], dims=prob.dims, prec="f32", nl=2, lin=10, rel=0.0,
+                           abs_tol=0.0, cost_stop=0.0, exec_mode="par", threads=THREADS)
+    ran = 0
+    for variant in VARIANTS:
+        monkeypatch.setenv("MO_B200_JTJ", variant)
+        s = Solver(load_plan(prob.name, _cfg(prob, "f32"), prob.dims), prob.data(np.float32))
+        if not s.apply_kernel(0).startswith(PREFIX[variant]):
+            continue
+        r = s.solve()
+        ran += 1
+        assert [t.pcg_iters for t in r.trace] == list(ref["trace_pcg"])
+        for row, rc in zip(r.trace, ref["trace_cost"]):
+            assert abs(row.cost - rc) <= 1e-4 * abs(rc), (variant, row.cost, rc)
+        assert abs(r.final_cost - float(ref["final_cost"][0])) <= 1e-4 * abs(float(ref["final_cost"][0]))
+    assert ran >= 3
+
+
+@pytest.mark.parametrize("name,make,prec", [
+    ("sfs", lambda: workloads.sfs(640, 480), "f32"),
+    ("poisson", lambda: workloads.poisson(512, 512), "f64"),
+])
+def test_other_configs_apply_matches_reference(name, make, prec):
+    prob = make()
+    dt = np.float32 if prec == "f32" else np.float64
+    data = prob.data(dt)
+    v = (workloads.uniform(98, data.x.size) - 0.5).astype(dt)
+    ref = pyoracle.run_ref(prob.energy, data, ["normal", "jtj"], dims=prob.dims, prec=prec, exec_mode="par",
+                           threads=THREADS, v=v)
+    s = Solver(load_plan(prob.name, _cfg(prob, prec), prob.dims), prob.data(dt))
+    tol = 1e-5 if prec == "f32" else 1e-10
+    assert_close_vec(s.apply_jtj(v), ref["jtj"], tol, f"2 J^T J v {name} [{s.apply_kernel(0)}]")
+    s.build_normal()
+    assert_close_vec(s.rhs(), ref["b"], tol, "b")

@@ -116,3 +116,32 @@ def test_kernels_bitwise_deterministic(name):
     for a, b in zip(outs[0][:3], outs[1][:3]):
         np.testing.assert_array_equal(a.view(np.uint8), b.view(np.uint8))
     assert outs[0][3] == outs[1][3]
+
+
+VARIANTS = ["gather", "twophase", "stream", "tma", "warp"]
+PREFIX = {"gather": "mo_gather_jtj_", "twophase": "mo_gather_jtj2_", "stream": "mo_gather_jtj3_",
+          "tma": "mo_gather_jtj4_", "warp": "mo_gather_jtj5_"}
+GRID = [n for n in NAMES if n.startswith("cfg_") and "mesh" not in n]
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("name", GRID)
+def test_apply_variant_parity(name, variant, monkeypatch):
+    """Every J^T J p kernel variant (forced with MO_B200_JTJ; the session
+    normally autotunes among them) against the reference's 2 J^T J v and its
+    full solve trajectory."""
+    monkeypatch.setenv("MO_B200_JTJ", variant)
+    g = Golden(name)
+    t = tol(g.prec)
+    s = Solver(g.plan(False), g.data())
+    k = s.apply_kernel(0)
+    if not k.startswith(PREFIX[variant]):
+        pytest.skip(f"{variant} not generated for {name} (runs {k})")
+    assert_close_vec(s.apply_jtj(g.z["v"].astype(g.dtype)), g.ref("jtj"), t["vec"], f"2 J^T J v [{k}]")
+    r = s.solve()
+    assert int(r.reason) == int(g.ref("reason")[0])
+    assert [x.pcg_iters for x in r.trace] == list(g.ref("trace_pcg"))
+    assert [int(x.accepted) for x in r.trace] == list(g.ref("trace_accepted"))
+    for row, rc in zip(r.trace, g.ref("trace_cost")):
+        assert rel_close(row.cost, rc, t["traj"]), (k, row.cost, rc)
+    assert rel_close(r.final_cost, float(g.ref("final_cost")[0]), t["traj"]), (k, r.final_cost)
