@@ -1288,8 +1288,14 @@ struct Gen {
   // edge order) and accumulates, in registers, the outputs whose slot is v.
   // Per column that is the grid-written value followed by the edges in order
   // and the outputs in program order: the reference's sequential order.
+  // fused != nullptr (J^T J p only): the kernel also evaluates the grid gather
+  // program `fused` of the same (1-D vertex) domain for its vertex first -
+  // exactly what exec_grid writes before the graph scatters add
+  // (solver.hpp:257-265) - and finishes the apply in the same pass: LM
+  // damping, excluded zeroing and the p'Ap partial (the k_apply_finish
+  // epilogue), so one launch replaces gather + vertex gather + finish.
   void vertex_kernel(const GraphSet& g, const Domain& dom, const std::string& pn, const std::string& kn, int arity,
-                     bool bm) {
+                     bool bm, const GatherSet* gs = nullptr, const std::string& fused = "") {
     const size_t K = g.scats.size();
     const size_t NO = bm ? 2 * K : K;
     struct Col {
@@ -1311,7 +1317,7 @@ struct Gen {
       cidx[o] = k;
     }
     os << kbegin(kn) << "  if ((P.flags & MO_F_SKIPDONE) && P.state->done) return;\n"
-       << "  bool bad = false;\n"
+       << "  bool bad = false; double acc = 0; (void)acc;\n"
        << "  Real* D0 = (Real*)P.out0; Real* D1 = (Real*)P.out1; (void)D1;\n"
        << "  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < P.nverts;"
           " v += (long long)gridDim.x * blockDim.x) {\n";
@@ -1319,7 +1325,23 @@ struct Gen {
       return std::string(c.vec ? "D1" : "D0") + "[P.ubase[" + std::to_string(c.f) + "] + v * " +
              std::to_string(P.unknowns[size_t(c.f)].channels) + " + " + std::to_string(c.ch) + "]";
     };
-    for (size_t j = 0; j < cols.size(); ++j) os << "    Real a" << j << " = " << colexpr(cols[j]) << ";\n";
+    if (gs) {
+      // grid gather outputs of this vertex (element v of the 1-D domain)
+      const size_t K = gs->chans.size();
+      os << "    const bool gex = P.mask && P.mask[v];\n"
+         << "    Real go[" << (K ? K : 1) << "];\n"
+         << "    if (gex) { for (int k = 0; k < " << K << "; ++k) go[k] = (Real)0; }\n"
+         << "    else { " << fused << "<false>(P, (int)v, 0, 0, 0, nullptr, go);\n"
+         << "      for (int k = 0; k < " << K << "; ++k) if (!mo_finite((double)go[k])) bad = true; }\n";
+      for (size_t j = 0; j < cols.size(); ++j) {
+        int k = -1;
+        for (size_t q = 0; q < K; ++q)
+          if (gs->chans[q].first == cols[j].f && gs->chans[q].second == cols[j].ch) k = int(q);
+        os << "    Real a" << j << " = " << (k >= 0 ? "go[" + std::to_string(k) + "]" : std::string("(Real)0")) << ";\n";
+      }
+    } else {
+      for (size_t j = 0; j < cols.size(); ++j) os << "    Real a" << j << " = " << colexpr(cols[j]) << ";\n";
+    }
     os << "    const int j1 = P.vptr[v + 1];\n"
        << "    for (int j = P.vptr[v]; j < j1; ++j) {\n"
        << "      const long long e = P.vedge[j];\n"
@@ -1333,6 +1355,23 @@ struct Gen {
       os << "      if (vs[" << sc.slot << "] == (int)v) a" << cidx[o] << " += o[" << o << "];\n";
     }
     os << "    }\n";
+    if (gs) {
+      // k_apply_finish epilogue per owned column (solver.hpp:401-405, pcg.hpp:100-102)
+      os << "    const Real* PV = (const Real*)P.in0; const Real* DAMP = (const Real*)P.in1;\n";
+      for (size_t j = 0; j < cols.size(); ++j) {
+        const std::string col = "P.ubase[" + std::to_string(cols[j].f) + "] + v * " +
+                                std::to_string(P.unknowns[size_t(cols[j].f)].channels) + " + " +
+                                std::to_string(cols[j].ch);
+        os << "    { const long long col = " << col << "; Real x = a" << j << ";\n"
+           << "      if (P.flags & MO_F_DAMP) x = x + DAMP[col] * PV[col];\n"
+           << "      if ((P.flags & MO_F_ZEROEXCL) && P.colmask && (P.colmask[col] & 1)) x = (Real)0;\n"
+           << "      D0[col] = x;\n"
+           << "      if (P.flags & MO_F_REDUCE) acc += (double)(PV[col] * x); }\n";
+      }
+      os << "  }\n  if (bad) atomicOr(&P.state->nonfinite_kernel, 1);\n"
+         << "  if (P.flags & MO_F_REDUCE) mo_reduce_epilogue<Real>(P.red, acc, 0.0, false);\n}\n";
+      return;
+    }
     for (size_t j = 0; j < cols.size(); ++j) os << "    " << colexpr(cols[j]) << " = a" << j << ";\n";
     os << "  }\n  if (bad) atomicOr(&P.state->nonfinite_kernel, 1);\n}\n";
   }
@@ -1399,6 +1438,27 @@ struct Gen {
         vertex_kernel(g, doms[di], pb, "mo_graph_vbm_" + s + "_" + std::to_string(di), ar, true);
       }
       info.vertex_kernels.push_back(true);
+      // One-pass apply: a single graph set scattering into one 1-D domain that
+      // also holds the only gather set and every unknown column.
+      bool one = P.graph_sets.size() == 1 && doms.size() == 1 && P.gather_sets.size() == 1 &&
+                 P.gather_sets[0].dom == doms[0] && doms[0].dims.size() == 1;
+      for (const Field& f : P.unknowns) one = one && f.dom == doms[0];
+      if (one) {
+        std::vector<std::pair<int, int>> need;
+        for (size_t f = 0; f < P.unknowns.size(); ++f)
+          for (int c = 0; c < P.unknowns[f].channels; ++c) need.push_back({int(f), c});
+        for (auto fc : need) {  // every unknown column is a scatter target, so the kernel owns it
+          bool hit = false;
+          for (const Scat& sc : g.scats) hit = hit || (sc.field == fc.first && sc.channel == fc.second);
+          one = one && hit;
+        }
+      }
+      if (one) {
+        const GatherSet& gs0 = P.gather_sets[0];
+        const std::string pgj = program(gs0.jtj, false, &gs0.dom);
+        vertex_kernel(g, doms[0], pj, "mo_graph_vjtjf_" + s, ar, false, &gs0, pgj);
+        info.fused_vertex_apply = true;
+      }
     }
     for (size_t i = 0; i < P.computed_kernels.size(); ++i) {
       const ComputedKernel& ck = P.computed_kernels[i];

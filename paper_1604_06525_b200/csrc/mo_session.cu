@@ -1298,6 +1298,37 @@ class Session final : public SessionBase {
     return R;
   }
 
+  // One-pass graph apply (mo_graph_vjtjf_0): grid gather program, incident
+  // edges in order and the apply epilogue per vertex, one launch.
+  bool vertex_apply_one_pass() const {
+    static const bool off = std::getenv("MO_B200_NO_VFUSE") != nullptr;
+    return !off && minfo_.fused_vertex_apply && !sh_.on && vertex_path(0);
+  }
+  void apply_vertex_fused(const Real* pv, Real* out, int flags) {
+    GSet& gs = gsets_[0];
+    const GatherDom& gd = gs.doms[0];
+    mo_kparams kp = kp_grid(P_.gather_sets[0].dom, x_, pv);  // grid env (InBounds, mask) of the vertex domain
+    const GraphData& g = graphs_[size_t(P_.graph_sets[0].graph)];
+    kp.verts = g.d_verts;
+    kp.arity = g.arity;
+    kp.nedges = g.E;
+    kp.vptr = gd.vptr;
+    kp.vedge = gd.vedge;
+    kp.nverts = gd.nverts;
+    kp.out0 = out;
+    kp.in0 = pv;
+    kp.in1 = damp_;
+    kp.flags = flags;
+    const void* f = mod_.kernel("mo_graph_vjtjf_0");
+    const int grid = int(std::max<long long>(
+        1, std::min<long long>((gd.nverts + MO_THREADS - 1) / MO_THREADS, (long long)nsm_ * occupancy(f))));
+    kp.red = red(0, grid, MO_FIN_PCG_ALPHA, 0);
+    void* args[] = {&kp};
+    klc(f, dim3(grid), dim3(MO_THREADS), args, 0);
+    ++launches_;
+    if (flags & MO_F_REDUCE) reduce_done(MO_FIN_PCG_ALPHA, 0);
+  }
+
   // Vertex-centric recompute kernels (generated per scatter-target domain).
   bool vertex_path(size_t gi) const {
     static const bool off = std::getenv("MO_B200_EDGE_SCATTER") != nullptr;
@@ -1418,6 +1449,10 @@ class Session final : public SessionBase {
   //  from rvec/mdvec and write it to pnew.)
   void apply(const Real* pv, Real* out, int flags, const Real* rvec = nullptr, const Real* mdvec = nullptr,
              Real* pnew = nullptr) {
+    if (vertex_apply_one_pass()) {
+      apply_vertex_fused(pv, out, flags);
+      return;
+    }
     const bool fused = P_.graph_sets.empty();
     const long long n = P_.num_cols;
     std::vector<int> grids;
