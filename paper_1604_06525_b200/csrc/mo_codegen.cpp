@@ -1104,6 +1104,177 @@ struct Gen {
   }
   ModuleInfo::Tma tma5_info;
 
+  // TMA-staged gather program (2-D domains): the reference's own J^T J p
+  // gather program (transform.hpp:238-260, run_program semantics) per output
+  // pixel, with every field it reads streamed into shared-memory row rings by
+  // TMA (8-row blocks, NBUF deep, mbarrier completion) instead of read through
+  // L1.  For cheap stencils (Poisson) this beats the two-phase schemes: no
+  // phase-1 halo, no contribution ring, one barrier per 8-row step.  Work
+  // item: a band of 32 output columns (one per lane) by `chunk` rows; each of
+  // the 8 warps owns one output row per step.
+  void gather_jtj6(const GatherSet& g, int gi) {
+    if (f64_disabled_tma()) return;
+    const auto sh = P.shape_of(g.dom);
+    if (g.dom.dims.size() != 2) return;
+    const long long D0 = sh[0], D1 = sh[1];
+    const int U = int(P.unknowns.size());
+    const int RG = reach_of(g.jtj, &g.dom);
+    if (RG > 4) return;
+    const int AU = f64 ? 2 : 4;
+    const int WIN = (32 + 2 * RG + AU - 1 + AU - 1) / AU * AU;
+    // (3 to 8 ring slots measured the same on Poisson 512^2 / 8192^2: the
+    // kernel is instruction-bound, not waiting on TMA.)
+    const int NBUF = std::getenv("MO_B200_JTJ6_NBUF") ? std::max(3, std::atoi(std::getenv("MO_B200_JTJ6_NBUF"))) : 3;
+    const int NEED = 1 + (2 * RG + 7) / 8;
+    const int RB = f64 ? 8 : 4;
+    std::vector<std::pair<int, int>> slots;
+    auto add = [&](int sl, int C) {
+      for (auto& x : slots)
+        if (x.first == sl) return;
+      slots.push_back({sl, C});
+    };
+    for (const Instr& in : g.jtj.instrs) {
+      if (!(in.op == kLoadU || in.op == kLoadA || in.op == kLoadC || in.op == kLoadP) || in.graph) continue;
+      const Field& f = field_of(in.op, in.field);
+      if (f.dom == g.dom) add(slot_of(in.op, in.field), f.channels);
+    }
+    for (auto& fc : g.chans) add(U + fc.first, P.unknowns[size_t(fc.first)].channels);
+    if (slots.empty() || int(slots.size()) > MO_MAX_TMAPS_HOST) return;
+    for (auto& x : slots)
+      if (WIN * x.second > 256) return;
+    long long off = 0;
+    staged.clear();
+    long long tx = 0;
+    std::vector<long long> boxbytes;
+    for (auto& x : slots) {
+      staged.push_back({x.first, {off, x.second}});
+      const long long bb = 8LL * WIN * x.second * RB;
+      boxbytes.push_back(bb);
+      tx += bb;
+      off += ((long long)NBUF * bb + 127) / 128 * 128;
+    }
+    const long long mbar_off = off;
+    off += 8LL * NBUF;
+    st_rx = RG;
+    st_win = WIN;
+    const std::string pn = program(g.jtj, false, &g.dom, true);
+    sm_mode = false;
+    const std::string sfx = std::to_string(gi);
+    const std::string kn = "mo_gather_jtj6_" + sfx;
+    std::ostringstream is;
+    is << "{ int slot_ = slot0 + (JJ); while (slot_ >= NBUF) slot_ -= NBUF;\n"
+       << "  mo_mbar_expect_tx(MB + slot_, " << tx << "u);\n"
+       << "  const int r_ = y0 - RG + 8 * (JJ) - P.row_lo;\n";
+    for (size_t i = 0; i < slots.size(); ++i)
+      is << "  mo_tma_load_2d(mo_dsm + " << staged[i].second.first << " + slot_ * " << boxbytes[i] << ", &T.m[" << i
+         << "], cs * " << slots[i].second << ", r_, MB + slot_);\n";
+    is << "}\n";
+    auto issue = [&](const std::string& j) {
+      std::string t = is.str();
+      for (size_t p = t.find("JJ"); p != std::string::npos; p = t.find("JJ", p)) t.replace(p, 2, j);
+      return t;
+    };
+    const size_t K = g.chans.size();
+    os << "extern \"C\" __global__ void __launch_bounds__(MO_THREADS) " << kn
+       << "(const __grid_constant__ mo_kparams P, const __grid_constant__ mo_tmaps T) {\n"
+       << "  MO_PDL_ENTRY();\n"
+       << "  if ((P.flags & MO_F_SKIPDONE) && P.state->done) return;\n"
+       << "  unsigned long long* MB = reinterpret_cast<unsigned long long*>(mo_dsm + " << mbar_off << ");\n"
+       << "  double acc = 0;\n"
+       << "  bool bad = false;\n"
+       << "  const int tid = threadIdx.x + threadIdx.y * blockDim.x;\n"
+       << "  const int w = tid >> 5, l = tid & 31;\n"
+       << "  constexpr int RG = " << RG << ", NBUF = " << NBUF << ", NEED = " << NEED << ";\n"
+       << "  constexpr int D0 = " << D0 << ", D1 = " << D1 << ", NB = " << (D1 + 31) / 32 << ";\n"
+       << "  if (tid == 0) {\n"
+       << "    for (int i = 0; i < NBUF; ++i) mo_mbar_init(MB + i, 1);\n"
+       << "    mo_mbar_fence_init();\n"
+       << "  }\n"
+       << "  __syncthreads();\n"
+       << "  Real* const OUT = (Real*)P.out0; const Real* const DAMP = (const Real*)P.in1; (void)DAMP;\n"
+       << "  const int fl = P.flags;\n"
+       << "  const int CH = P.chunk;\n"
+       << "  const int nch = (P.row1 - P.row0 + CH - 1) / CH;\n"
+       << "  const int items = NB * nch;\n"
+       << "  int slot0 = 0;\n"
+       << "  unsigned ph = 0;\n"
+       << "  for (int t = blockIdx.x; t < items; t += gridDim.x) {\n"
+       << "    const int ci = t / NB, c0 = (t - ci * NB) * 32;\n"
+       << "    const int y0 = P.row0 + ci * CH, y1 = min(y0 + CH, P.row1);\n"
+       << "    const bool it = y0 - RG >= 0 && y1 - 1 + RG < D0 && c0 - RG >= 0 && c0 + 31 + RG < D1;\n"
+       << "    const int sh = (c0 - RG) & " << AU - 1 << ", cs = c0 - RG - sh;\n"
+       << "    const int nsteps = (y1 - y0 + 7) >> 3;\n"
+       << "    const int nblk = (y1 - y0 + 2 * RG + 7) >> 3;\n"
+       << "    if (tid == 0) {\n"
+       << "      mo_fence_proxy_async();\n"
+       << "      for (int j = 0; j < NBUF && j < nblk; ++j) " << issue("j")
+       << "    }\n"
+       << "    const int q1 = c0 + l;\n"
+       << "    const int lx = l + RG + sh;\n"
+       << "    int ss = slot0;\n"
+       << "    for (int s = 0; s < nsteps; ++s) {\n"
+       << "      if (s == 0) {\n"
+       << "        for (int j = 0; j < NEED - 1 && j < nblk; ++j) { int q = ss + j; while (q >= NBUF) q -= NBUF;"
+          " mo_mbar_wait(MB + q, (ph >> q) & 1u); ph ^= 1u << q; }\n"
+       << "      }\n"
+       << "      if (s + NEED - 1 < nblk) { int q = ss + NEED - 1; while (q >= NBUF) q -= NBUF;"
+          " mo_mbar_wait(MB + q, (ph >> q) & 1u); ph ^= 1u << q; }\n"
+       << "      const int y = y0 + 8 * s + w;\n"
+       << "      if (y < y1 && q1 < D1) {\n"
+       << "        int ri[" << 2 * RG + 1 << "];\n"
+       << "        #pragma unroll\n"
+       << "        for (int o = 0; o < " << 2 * RG + 1 << "; ++o) {\n"
+       << "          const int rel = w + o;  // input row y + o - RG, relative to block s\n"
+       << "          int b = ss + (rel >> 3); if (b >= NBUF) b -= NBUF;\n"
+       << "          ri[o] = b * 8 + (rel & 7);\n"
+       << "        }\n"
+       << "        const int e = (y - P.row_lo) * D1 + q1;\n"
+       << "        const bool ex = P.mask && P.mask[e];\n"
+       << "        Real o[" << (K ? K : 1) << "];\n"
+       << "        if (ex) { for (int k = 0; k < " << K << "; ++k) o[k] = (Real)0; }\n"
+       << "        else { if (it) " << pn << "<true>(P, y, q1, 0, ri, lx, o); else " << pn
+       << "<false>(P, y, q1, 0, ri, lx, o);\n"
+       << "          for (int k = 0; k < " << K << "; ++k) if (!mo_finite((double)o[k])) bad = true; }\n"
+       << "        Real pa = (Real)0;\n";
+    for (size_t k = 0; k < K; ++k) {
+      const int f = g.chans[k].first, ch = g.chans[k].second;
+      const int C = P.unknowns[size_t(f)].channels;
+      const auto* st = staged_of(U + f);
+      os << "        { const int col = (int)P.ubase[" << f << "] + e * " << C << " + " << ch << ";\n"
+         << "          Real v = o[" << k << "];\n"
+         << "          const Real pc = reinterpret_cast<const Real*>(mo_dsm + " << st->first << ")[ri[" << RG << "] * "
+         << WIN * C << " + lx * " << C << " + " << ch << "];\n"
+         << "          if (fl & MO_F_DAMP) v = v + DAMP[col] * pc;\n"
+         << "          if ((fl & MO_F_ZEROEXCL) && P.colmask && (P.colmask[col] & 1)) v = (Real)0;\n"
+         << "          OUT[col] = v;\n"
+         << "          pa += pc * v; }\n";
+    }
+    os << "        if (fl & MO_F_REDUCE) acc += (double)pa;\n"
+       << "      }\n"
+       << "      __syncthreads();  // every warp is done with input block s\n"
+       << "      if (tid == 0 && s + NBUF < nblk) {\n"
+       << "        mo_fence_proxy_async();\n"
+       << "        " << issue("s + NBUF")
+       << "      }\n"
+       << "      ss = ss + 1 == NBUF ? 0 : ss + 1;\n"
+       << "    }\n"
+       << "    slot0 = (slot0 + nblk) % NBUF;\n"
+       << "  }\n"
+       << "  if (bad) atomicOr(&P.state->nonfinite_kernel, 1);\n"
+       << "  if (P.flags & MO_F_REDUCE) mo_reduce_epilogue<Real>(P.red, acc, 0.0, false);\n}\n";
+    ModuleInfo::Tma ti;
+    ti.ok = true;
+    ti.smem = size_t(off);
+    ti.halo = 0;
+    ti.band = 32;
+    ti.rx = RG;
+    ti.win = WIN;
+    for (auto& x : slots) ti.slots.push_back({x.first, x.second});
+    tma6_info = ti;
+    staged.clear();
+  }
+  ModuleInfo::Tma tma6_info;
+
   static long long NB(long long D1, int BW) { return (D1 + BW - 1) / BW; }
   bool f64_disabled_tma() const { return std::getenv("MO_B200_NO_TMA") != nullptr; }
   ModuleInfo::Tma tma_info;
@@ -1408,6 +1579,8 @@ struct Gen {
       const GatherSet& g = P.gather_sets[i];
       gather_bm(g, program(g.bm, false, &g.dom), "mo_gather_bm_" + std::to_string(i));
       gather_jtj(g, program(g.jtj, false, &g.dom), "mo_gather_jtj_" + std::to_string(i));
+      tma6_info = ModuleInfo::Tma{};
+      gather_jtj6(g, int(i));
       stream_info = ModuleInfo::Stream{};
       tma_info = ModuleInfo::Tma{};
       tma5_info = ModuleInfo::Tma{};
@@ -1416,6 +1589,7 @@ struct Gen {
       info.jtj3.push_back(stream_info);
       info.jtj4.push_back(tma_info);
       info.jtj5.push_back(tma5_info);
+      info.jtj6.push_back(tma6_info);
     }
     for (size_t i = 0; i < P.graph_sets.size(); ++i) {
       const GraphSet& g = P.graph_sets[i];

@@ -1025,11 +1025,13 @@ class Session final : public SessionBase {
   // Apply kernel variants of gather set i: 0 = the reference's gather program
   // (exact mode always uses it), 1 = two-phase 32x8 tiles, 2 = row-streaming
   // two-phase bands, 3 = TMA-staged row-streaming bands (block-wide 8-row
-  // steps), 4 = TMA-staged warp-streaming bands (2-D domains).
-  static constexpr int kVariants = 5;
+  // steps), 4 = TMA-staged warp-streaming bands, 5 = TMA-staged gather
+  // program (2-D domains).
+  static constexpr int kVariants = 6;
   const ModuleInfo::Tma* tma_info(size_t i, int v) const {
     if (v == 3 && i < minfo_.jtj4.size()) return &minfo_.jtj4[i];
     if (v == 4 && i < minfo_.jtj5.size()) return &minfo_.jtj5[i];
+    if (v == 5 && i < minfo_.jtj6.size()) return &minfo_.jtj6[i];
     return nullptr;
   }
   bool variant_ok(size_t i, int v) const {
@@ -1046,8 +1048,8 @@ class Session final : public SessionBase {
     return 0;
   }
   static const char* variant_prefix(int v) {
-    static const char* n[] = {"mo_gather_jtj_", "mo_gather_jtj2_", "mo_gather_jtj3_", "mo_gather_jtj4_",
-                              "mo_gather_jtj5_"};
+    static const char* n[] = {"mo_gather_jtj_",  "mo_gather_jtj2_", "mo_gather_jtj3_",
+                              "mo_gather_jtj4_", "mo_gather_jtj5_", "mo_gather_jtj6_"};
     return n[v];
   }
 
@@ -1144,7 +1146,8 @@ class Session final : public SessionBase {
                        : fs == "twophase" ? 1
                        : fs == "stream" ? 2
                        : fs == "tma" ? 3
-                                     : 4;
+                       : fs == "warp" ? 4
+                                      : 5;
       if (want >= 0) {
         jtj_choice_[i] = variant_ok(i, want) ? want : -1;
         if (jtj_choice_[i] >= 0) continue;
@@ -1225,7 +1228,7 @@ class Session final : public SessionBase {
     jtj_occupancy(i);  // sets the dynamic smem attribute once
     const mo_tmaps& T = tmaps_for(i, v, kp);
     void* args[] = {const_cast<mo_kparams*>(&kp), const_cast<mo_tmaps*>(&T)};
-    const dim3 block = v == 3 ? dim3(MO_TILE_X, MO_TILE_Y, 1) : dim3(unsigned(jtj_threads(i)), 1, 1);
+    const dim3 block = v == 4 ? dim3(unsigned(jtj_threads(i)), 1, 1) : dim3(MO_TILE_X, MO_TILE_Y, 1);
     klc(f, dim3(grid), block, args, smem);
     ++launches_;
   }
