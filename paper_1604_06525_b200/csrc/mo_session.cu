@@ -1502,6 +1502,13 @@ class Session final : public SessionBase {
   void pcg_body(bool lm) {
     const long long n = P_.num_cols;
     const int vg = vgrid(n, nsm_);
+    // Update / direction kernels: one wave of 4 blocks per SM while a thread
+    // has few float4 groups (small grids are latency-bound), 16 blocks per SM
+    // (several waves) for large ones; both measured on B200 (1024^2 vs 8192^2
+    // ARAP).  MO_B200_VEC_PER_SM overrides.
+    static const int vper_env = std::getenv("MO_B200_VEC_PER_SM") ? std::atoi(std::getenv("MO_B200_VEC_PER_SM")) : 0;
+    const int vper = vper_env > 0 ? vper_env : (n / 4 > 8LL * nsm_ * 4 * MO_THREADS ? 16 : 4);
+    const int vgu = vgrid(n, nsm_, vper);
     const Real* mdv = lm ? md_ : m_;
     const int pre = cfg_.use_preconditioner ? 1 : 0;
     kl(k_pcg_init<Real>, dim3(vg), dim3(MO_THREADS), red(0, vg, MO_FIN_PCG_INIT, 0), n, colmask_, b_, mdv, delta_, r_, p_, pre);
@@ -1516,10 +1523,10 @@ class Session final : public SessionBase {
       prof_begin(1);
       // (A cooperative single-kernel update + direction with a grid barrier
       // was measured slower on B200 than this pair at every config size.)
-      kl(k_pcg_update<Real>, dim3(vg), dim3(MO_THREADS), red(0, vg, MO_FIN_PCG_BETA, 0), n, colmask_, mdv, delta_, r_, p_, ap_, pre);
+      kl(k_pcg_update<Real>, dim3(vgu), dim3(MO_THREADS), red(0, vgu, MO_FIN_PCG_BETA, 0), n, colmask_, mdv, delta_, r_, p_, ap_, pre);
       ++launches_;
       reduce_done(MO_FIN_PCG_BETA, 0);
-      kl(k_pcg_p<Real>, dim3(vg), dim3(MO_THREADS), state_, n, colmask_, mdv, r_, p_, pre);
+      kl(k_pcg_p<Real>, dim3(vgu), dim3(MO_THREADS), state_, n, colmask_, mdv, r_, p_, pre);
       ++launches_;
       exchange_cols(p_);
       prof_end(1);
