@@ -1238,6 +1238,8 @@ class Session final : public SessionBase {
   // chunk + 2H a multiple of 8): pick the chunk minimising that plus a
   // per-item pipeline fill, the larger one on ties.
   int jtj3_chunk(size_t i) {
+    static const int force = std::getenv("MO_B200_CHUNK") ? std::atoi(std::getenv("MO_B200_CHUNK")) : 0;
+    if (force > 0) return force;
     const auto sh = P_.shape_of(P_.gather_sets[i].dom);
     const long long rows = sh_.on ? sh_.row1 - sh_.row0 : sh[0];
     const int halo = jtj_halo(i), band = jtj_band(i);
