@@ -385,8 +385,14 @@ struct Gen {
   // build_normal gather (solver.hpp:221-230) + fused identity patch (241-250).
   void gather_bm(const GatherSet& g, const std::string& pn, const std::string& kn) {
     const size_t K = g.chans.size();
-    os << kbegin(kn) << "  double cnt = 0; bool bad = false;\n"
+    os << kbegin(kn) << "  double cnt = 0, rz = 0; bool bad = false;\n"
        << "  Real* B = (Real*)P.out0; Real* M = (Real*)P.out1;\n"
+       << "  Real* PP = (Real*)P.out2; Real* DL = (Real*)P.out3; Real* RR = (Real*)P.out4;\n"
+       << "  const bool pinit = (P.flags & MO_F_PCGINIT) != 0;\n"
+       << "  const int pre = P.state->use_precond;\n"
+       << "  if (pinit && blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0) {\n"
+       << "    P.state->done = 0; P.state->iters = 0; P.state->indefinite = 0; P.state->nonfinite = 0;\n"
+       << "  }\n"
           "  const int nt = mo_num_tiles(P);\n"
           "  for (int t = blockIdx.x; t < nt; t += gridDim.x) {\n"
        << "    const mo_tile T = mo_tile_at(P, t);\n"
@@ -412,10 +418,16 @@ struct Gen {
          << "          if (ex) { b = (Real)0; m = (Real)1; }\n"
          << "          else if (m == (Real)0) { m = (Real)1; cnt += 1.0; }\n"
          << "        }\n"
-         << "        B[col] = b; M[col] = m; }\n";
+         << "        B[col] = b; M[col] = m;\n"
+         << "        if (pinit) {  // k_pcg_init (pcg.hpp:75-97) on the patched b, m\n"
+         << "          const bool xc = P.colmask && (P.colmask[col] & 1);\n"
+         << "          const Real ri = xc ? (Real)0 : b;\n"
+         << "          const Real zi = xc ? (Real)0 : (pre ? ((ri == (Real)0 && m > (Real)0) ? ri : ri / m) : ri);\n"
+         << "          DL[col] = (Real)0; RR[col] = ri; PP[col] = zi; rz += (double)(ri * zi);\n"
+         << "        } }\n";
     }
     os << "    }\n  }\n  if (bad) atomicOr(&P.state->nonfinite_kernel, 1);\n"
-       << "  if (P.flags & MO_F_REDUCE) mo_reduce_epilogue<Real>(P.red, cnt, 0.0, false);\n}\n";
+       << "  if (P.flags & MO_F_REDUCE) mo_reduce_epilogue<Real>(P.red, cnt, rz, pinit);\n}\n";
   }
 
   // Matrix-free normal apply gather (solver.hpp:257-265), with optional fused

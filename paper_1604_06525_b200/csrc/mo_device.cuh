@@ -46,6 +46,7 @@ enum {
   MO_FIN_PCG_BETA = 3,   // rz', stop test, beta    (pcg.hpp:116-124)
   MO_FIN_UNCONSTRAINED = 4,
   MO_FIN_STORE2 = 5,     // sums[slot], sums[slot+1] = pair totals
+  MO_FIN_BM_INIT = 6,    // unconstrained count + rz0 / stop test (fused bm + pcg init)
 };
 
 enum {
@@ -55,6 +56,7 @@ enum {
   MO_F_ZEROEXCL = 8,   // jtj: zero excluded columns        (pcg.hpp:101)
   MO_F_SKIPDONE = 16,  // return at once when the PCG has already stopped
   MO_F_PUPD = 32,      // two-phase apply: p = z + beta p_old fused into staging (pcg.hpp:124-126)
+  MO_F_PCGINIT = 64,   // bm: also delta = 0, r = b, p = z = b/m, rz0 (pcg.hpp:75-97)
 };
 
 // One deterministic reduction: partial slots [part_base, part_base+gridDim)
@@ -82,7 +84,9 @@ struct mo_kparams {
   const void* in1;  // damp
   const void* in2;  // PUPD: r
   const void* in3;  // PUPD: m (+damp) preconditioner
-  void* out2;       // PUPD: p_new
+  void* out2;       // PUPD: p_new; PCGINIT: p
+  void* out3;       // PCGINIT: delta
+  void* out4;       // PCGINIT: r
   const unsigned char* mask;     // per-element exclusion (uint8) or null
   const unsigned char* colmask;  // per-column exclusion (uint8) or null
   long long ubase[MO_MAX_UNK];   // local column base per unknown field
@@ -210,6 +214,10 @@ __device__ void mo_finalize(mo_state* st, int op, int arg, double total, double 
       st->sums[arg + 1] = total2;
       break;
     case MO_FIN_UNCONSTRAINED: st->unconstrained = (long long)total; break;
+    case MO_FIN_BM_INIT:
+      st->unconstrained = (long long)total;
+      total = total2;
+      [[fallthrough]];
     case MO_FIN_PCG_INIT: {
       Real rz = Real(total);
       st->rz = double(rz);

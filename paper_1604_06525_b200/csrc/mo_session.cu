@@ -236,13 +236,22 @@ class Session final : public SessionBase {
     refreshed_ = true;
   }
 
-  void refresh_device() {
+  // Do the exclusion programs read the unknowns (or computed arrays)?  If
+  // not, the masks only change when arrays are re-bound.
+  bool exclude_reads_x() const {
+    for (const ExcludeKernel& ek : P_.exclude_kernels)
+      for (const Instr& in : ek.prog.instrs)
+        if (in.op == kLoadU || in.op == kLoadC || in.op == kLoadP) return true;
+    return false;
+  }
+  void refresh_device(bool masks = true) {
     for (const ComputedKernel& ck : P_.computed_kernels) {
       mo_kparams kp = kp_grid(ck.dom, x_, nullptr);
       kp.out0 = comp_[size_t(ck.index)];
       launch_grid("mo_computed_" + std::to_string(&ck - P_.computed_kernels.data()), ck.dom, kp);
     }
     exchange_computed();
+    if (!masks) return;
     for (size_t i = 0; i < P_.exclude_kernels.size(); ++i) {
       const ExcludeKernel& ek = P_.exclude_kernels[i];
       mo_kparams kp = kp_grid(ek.dom, x_, nullptr);
@@ -414,14 +423,17 @@ class Session final : public SessionBase {
         // could rebind data): reuse it instead of re-evaluating the cost.
         const bool reuse_cost = it > 0 && !cb && P_.computed.empty() && !std::getenv("MO_B200_NO_COST_REUSE");
         run_stage(reuse_cost ? kStageGNNext : kStageGN, [&] {
-          refresh_device();
+          // (with reuse_cost no array can have changed since iteration 0, so
+          // masks that do not depend on x are still current)
+          refresh_device(!reuse_cost || exclude_reads_x());
           if (reuse_cost)
             CK(cudaMemcpyAsync(&state_->sums[SLOT_COST], &state_->sums[SLOT_COST + 1], sizeof(double),
                                cudaMemcpyDeviceToDevice, st_));
           else
             cost_at(x_, SLOT_COST);
-          normal_device();
-          pcg_body(false);
+          const bool fi = bm_init_ok();
+          normal_device(fi);
+          pcg_body(false, fi);
           CK(cudaMemsetAsync(&state_->any_nonzero, 0, sizeof(int), st_));
           kl(k_xtrial<Real>, dim3(vg), dim3(MO_THREADS), state_, n, colmask_, x_, delta_, xt_, 1, SLOT_COST);
           ++launches_;
@@ -1424,7 +1436,18 @@ class Session final : public SessionBase {
   }
 
   // build_normal (solver.hpp:220-251) on the device.
-  void normal_device() {
+  // GN: the bm gather kernels can also start the PCG (k_pcg_init's work on
+  // the patched b, m), when they write every column (no graph scatters,
+  // unsharded, every unknown channel is an output of exactly one gather set).
+  bool bm_init_ok() const {
+    static const bool off = std::getenv("MO_B200_NO_BMINIT") != nullptr;
+    if (off || sh_.on || !P_.graph_sets.empty() || P_.gather_sets.empty()) return false;
+    size_t outs = 0, chans = 0;
+    for (const GatherSet& g : P_.gather_sets) outs += g.chans.size();
+    for (const Field& f : P_.unknowns) chans += size_t(f.channels);
+    return outs == chans;
+  }
+  void normal_device(bool pcg_init = false) {
     prof_begin(2);
     const bool fused = P_.graph_sets.empty();
     const long long n = P_.num_cols;
@@ -1442,6 +1465,13 @@ class Session final : public SessionBase {
       kp.out1 = m_;
       kp.flags = fused ? (MO_F_PATCH | MO_F_REDUCE) : 0;
       kp.red = red(base, total, MO_FIN_UNCONSTRAINED, 0);
+      if (pcg_init) {
+        kp.flags |= MO_F_PCGINIT;
+        kp.red = red(base, total, MO_FIN_BM_INIT, 0);
+        kp.out2 = p_;
+        kp.out3 = delta_;
+        kp.out4 = r_;
+      }
       launch_grid("mo_gather_bm_" + std::to_string(i), P_.gather_sets[i].dom, kp, grids[i]);
       base += grids[i];
     }
@@ -1520,7 +1550,7 @@ class Session final : public SessionBase {
   // Jacobi PCG (pcg.hpp:63-130) as a captured CUDA graph.  (Fusing the
   // direction update into the apply's p staging was measured slower: the
   // apply is issue-bound, the p update streams at HBM speed on its own.)
-  void pcg_body(bool lm) {
+  void pcg_body(bool lm, bool init_done = false) {
     const long long n = P_.num_cols;
     const int vg = vgrid(n, nsm_);
     // Update / direction kernels: one wave of 4 blocks per SM while a thread
@@ -1532,9 +1562,12 @@ class Session final : public SessionBase {
     const int vgu = vgrid(n, nsm_, vper);
     const Real* mdv = lm ? md_ : m_;
     const int pre = cfg_.use_preconditioner ? 1 : 0;
-    kl(k_pcg_init<Real>, dim3(vg), dim3(MO_THREADS), red(0, vg, MO_FIN_PCG_INIT, 0), n, colmask_, b_, mdv, delta_, r_, p_, pre);
-    ++launches_;
-    reduce_done(MO_FIN_PCG_INIT, 0);
+    if (!init_done) {
+      kl(k_pcg_init<Real>, dim3(vg), dim3(MO_THREADS), red(0, vg, MO_FIN_PCG_INIT, 0), n, colmask_, b_, mdv, delta_, r_,
+         p_, pre);
+      ++launches_;
+      reduce_done(MO_FIN_PCG_INIT, 0);
+    }
     exchange_cols(p_);  // strips: neighbours' p rows for the stencil apply
     const int flags = MO_F_REDUCE | MO_F_ZEROEXCL | MO_F_SKIPDONE | (lm ? MO_F_DAMP : 0);
     for (int k = 0; k < cfg_.linear_iters; ++k) {
