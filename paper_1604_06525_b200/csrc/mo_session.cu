@@ -1437,11 +1437,12 @@ class Session final : public SessionBase {
 
   // build_normal (solver.hpp:220-251) on the device.
   // GN: the bm gather kernels can also start the PCG (k_pcg_init's work on
-  // the patched b, m), when they write every column (no graph scatters,
-  // unsharded, every unknown channel is an output of exactly one gather set).
+  // the patched b, m), when they write every column (no graph scatters, every
+  // unknown channel an output of exactly one gather set).  On a strip the
+  // kernels cover the owned rows only; halo p arrives by the exchange.
   bool bm_init_ok() const {
     static const bool off = std::getenv("MO_B200_NO_BMINIT") != nullptr;
-    if (off || sh_.on || !P_.graph_sets.empty() || P_.gather_sets.empty()) return false;
+    if (off || !P_.graph_sets.empty() || P_.gather_sets.empty()) return false;
     size_t outs = 0, chans = 0;
     for (const GatherSet& g : P_.gather_sets) outs += g.chans.size();
     for (const Field& f : P_.unknowns) chans += size_t(f.channels);
@@ -1492,7 +1493,7 @@ class Session final : public SessionBase {
     } else if (P_.gather_sets.empty()) {
       CK(cudaMemsetAsync(&state_->unconstrained, 0, sizeof(long long), st_));
     } else {
-      reduce_done(MO_FIN_UNCONSTRAINED, 0);
+      reduce_done(pcg_init ? MO_FIN_BM_INIT : MO_FIN_UNCONSTRAINED, 0);
     }
     prof_end(2);
   }
