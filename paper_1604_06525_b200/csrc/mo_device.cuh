@@ -114,10 +114,14 @@ struct mo_tmaps {
 };
 
 // Programmatic dependent launch: every kernel first waits for its stream
-// predecessor to complete (memory visible), then lets its own successor be
-// scheduled, so block launch and ramp-up of kernel N+1 overlap kernel N's
-// tail.  Harmless when launched without the PDL attribute.
+// predecessor to complete (memory visible); the successor is triggered
+// implicitly when this grid exits.  Harmless without the PDL attribute.
+// (MO_PDL_EARLY: trigger at entry instead - measured slower.)
+#ifndef MO_PDL_EARLY
+#define MO_PDL_ENTRY() asm volatile("griddepcontrol.wait;" ::: "memory")
+#else
 #define MO_PDL_ENTRY() asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory")
+#endif
 
 // ---------------------------------------------------------------- TMA / mbarrier
 __device__ __forceinline__ unsigned mo_smem_addr(const void* p) {
