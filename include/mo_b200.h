@@ -195,7 +195,7 @@ int mo_session_stream(mo_session s, void** stream); /* cudaStream_t */
 /* Number of this library's kernels launched so far (host-side count). */
 int mo_kernel_launches(mo_session s, int64_t* n);
 /* Name of the J^T J p kernel gather set i runs (autotuned on first use;
- * MO_B200_JTJ=gather|twophase|stream|tma|warp|gprog forces it). */
+ * MO_B200_JTJ=gather|twophase|stream|tma|warp|gprog|tma4 forces it). */
 int mo_apply_kernel(mo_session s, int gather_set, char* name, size_t len);
 
 #ifdef __cplusplus

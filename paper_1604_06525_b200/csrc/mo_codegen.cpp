@@ -637,6 +637,7 @@ struct Gen {
       std::vector<LaneG> lg;
       for (const L& l : lanes) lg.push_back({l.t, l.out, l.f, l.c, l.o0, l.o1});
       gather_jtj4(g, gi, *S, lg, lane_slot, merged_off(merged), H);
+      gather_jtj4(g, gi, *S, lg, lane_slot, merged_off(merged), H, 4);
       gather_jtj5(g, gi, *S, lg, lane_slot, merged_off(merged), H);
     }
     return tp;
@@ -651,8 +652,12 @@ struct Gen {
   // of the next rows overlap the current rows' arithmetic.  TMA zero-fills
   // out-of-bounds box elements, which is the reference's OOB->0 read rule
   // (eval.hpp:47-51), so border bands run the same code.
+  // RS = rows per step = warps per block (8: mo_gather_jtj4_<gi>, 4:
+  // mo_gather_jtj7_<gi>, twice the resident blocks for small grids).
   void gather_jtj4(const GatherSet& g, int gi, const GridSet& S, const std::vector<LaneG>& lanes,
-                   const std::vector<int>& lane_slot, const std::vector<MLane>& merged, int H) {
+                   const std::vector<int>& lane_slot, const std::vector<MLane>& merged, int H, int RS = 8) {
+    const int LRS = RS == 8 ? 3 : 2;
+    const std::string LN = RS == 8 ? "mo_lanes4_" : "mo_lanes7_";
     if (f64_disabled_tma()) return;
     const std::string sfx = std::to_string(gi);
     const auto sh = P.shape_of(g.dom);
@@ -661,14 +666,14 @@ struct Gen {
     if (BW < 8) return;
     const int U = int(P.unknowns.size());
     const int RX = std::max(reach_of(S.evalj, &g.dom), H);
-    if (RX > 4) return;  // two 8-row blocks cover one step's input rows
+    if (2 * RX > RS) return;  // two RS-row blocks cover one step's input rows
     // TMA needs a 16-byte aligned box start: the window starts at the
     // aligned column cs <= c0 - H - RX (shift sh = c0 - H - RX - cs < AU).
     const int AU = f64 ? 2 : 4;
     const int WIN = (32 + 2 * RX + AU - 1 + AU - 1) / AU * AU;
     const int NBUF = std::getenv("MO_B200_JTJ4_NBUF") ? std::max(3, std::atoi(std::getenv("MO_B200_JTJ4_NBUF"))) : 3;
-    const int NEED = 1 + (2 * RX + 7) / 8;
-    const int RING = 8 + 2 * H;  // two barriers per step
+    const int NEED = 1 + (2 * RX + RS - 1) / RS;
+    const int RING = RS + 2 * H;  // two barriers per step
     const int LS = RING * 32;
     const int NM = int(merged.size());
     const int RB = f64 ? 8 : 4;
@@ -696,7 +701,8 @@ struct Gen {
     std::vector<long long> boxbytes;
     for (auto& x : slots) {
       staged.push_back({x.first, {off, x.second}});
-      const long long bb = 8LL * WIN * x.second * RB;
+      const long long bb = (long long)RS * WIN * x.second * RB;
+      if (bb % 128) return;  // ring rows are contiguous across 128-byte aligned slots
       boxbytes.push_back(bb);
       tx += bb;
       off += (long long)NBUF * bb;
@@ -708,7 +714,7 @@ struct Gen {
     const std::string pe = program(S.evalj, false, &g.dom, true);
     const int NO = int(S.evalj.outputs.size());
     // Phase-1 body from shared memory.
-    os << "template <bool I> __device__ __forceinline__ void mo_lanes4_" << sfx
+    os << "template <bool I> __device__ __forceinline__ void " << LN << sfx
        << "(const mo_kparams& P, int p0, int p1, int k, Real* CL, const int* ri, int lx) {\n"
        << "  const bool inside = I || mo_inb(P, p0, p1, 0);\n"
        << "  Real d[" << NO << "];\n  " << pe << "<I>(P, p0, p1, 0, ri, lx, d);\n";
@@ -728,10 +734,10 @@ struct Gen {
     os << "}\n";
     sm_mode = false;
 
-    const std::string kn = "mo_gather_jtj4_" + sfx;
+    const std::string kn = (RS == 8 ? "mo_gather_jtj4_" : "mo_gather_jtj7_") + sfx;
     const char* mb = std::getenv("MO_B200_JTJ4_MINB");
-    const int minb = mb ? std::atoi(mb) : 4;
-    os << "extern \"C\" __global__ void __launch_bounds__(MO_THREADS" << (minb > 0 ? ", " + std::to_string(minb) : "")
+    const int minb = mb ? std::atoi(mb) : 32 / RS;
+    os << "extern \"C\" __global__ void __launch_bounds__(" << 32 * RS << (minb > 0 ? ", " + std::to_string(minb) : "")
        << ") " << kn << "(const __grid_constant__ mo_kparams P, const __grid_constant__ mo_tmaps T) {\n"
        << "  MO_PDL_ENTRY();\n"
        << "  if ((P.flags & MO_F_SKIPDONE) && P.state->done) return;\n"
@@ -761,7 +767,7 @@ struct Gen {
     std::ostringstream is;
     is << "{ int slot_ = slot0 + (JJ); while (slot_ >= NBUF) slot_ -= NBUF;\n"
        << "  mo_mbar_expect_tx(MB + slot_, " << tx << "u);\n"
-       << "  const int r_ = y0 - H - RX + 8 * (JJ) - P.row_lo;\n";
+       << "  const int r_ = y0 - H - RX + " << RS << " * (JJ) - P.row_lo;\n";
     for (size_t i = 0; i < slots.size(); ++i)
       is << "  mo_tma_load_2d(mo_dsm + " << staged[i].second.first << " + slot_ * " << boxbytes[i] << ", &T.m[" << i
          << "], cs * " << slots[i].second << ", r_, MB + slot_);\n";
@@ -777,8 +783,8 @@ struct Gen {
        << "    const bool it = y0 - H - RX >= 0 && y1 + H - 1 + RX < D0 && c0 - H - RX >= 0 && c0 - H + 31 + RX < D1;\n"
        << "    const int q1 = c0 - H + l;\n"
        << "    const int sh = (c0 - H - RX) & " << AU - 1 << ", cs = c0 - H - RX - sh;  // 16-byte aligned window start\n"
-       << "    const int nsteps = (y1 - y0 + 2 * H + 7) >> 3;\n"
-       << "    const int nblk = (y1 - y0 + 2 * H + 2 * RX + 7) >> 3;\n"
+       << "    const int nsteps = (y1 - y0 + 2 * H + " << RS - 1 << ") >> " << LRS << ";\n"
+       << "    const int nblk = (y1 - y0 + 2 * H + 2 * RX + " << RS - 1 << ") >> " << LRS << ";\n"
        << "    if (tid == 0) {\n"
        << "      mo_fence_proxy_async();\n"
        << "      for (int j = 0; j < NBUF && j < nblk; ++j) " << issue("j")
@@ -803,18 +809,18 @@ struct Gen {
        << "        mo_mbar_wait(MB + q, (ph >> q) & 1u);\n"
        << "        ph ^= 1u << q;\n"
        << "      }\n"
-       << "      const int rr = 8 * s + w;  // phase-1 row relative to y0 - H\n"
+       << "      const int rr = " << RS << " * s + w;  // phase-1 row relative to y0 - H\n"
        << "      const int q0 = y0 - H + rr;\n"
        << "      if (q0 < y1 + H) {\n"
        << "        int ri[" << 2 * RX + 1 << "];\n"
        << "        #pragma unroll\n"
        << "        for (int o = 0; o < " << 2 * RX + 1 << "; ++o) {\n"
        << "          const int rel = w + o;  // input row q0 + o - RX, relative to block s\n"
-       << "          int b = ss + (rel >> 3); if (b >= NBUF) b -= NBUF;\n"
-       << "          ri[o] = b * 8 + (rel & 7);\n"
+       << "          int b = ss + (rel >> " << LRS << "); if (b >= NBUF) b -= NBUF;\n"
+       << "          ri[o] = b * " << RS << " + (rel & " << RS - 1 << ");\n"
        << "        }\n"
        << "        const int k = cr * 32 + l;\n"
-       << "        if (it) mo_lanes4_" << sfx << "<true>(P, q0, q1, k, CL, ri, l + RX + sh); else mo_lanes4_" << sfx
+       << "        if (it) " << LN << sfx << "<true>(P, q0, q1, k, CL, ri, l + RX + sh); else " << LN << sfx
        << "<false>(P, q0, q1, k, CL, ri, l + RX + sh);\n"
        << "      }\n"
        << "      __syncthreads();\n"
@@ -827,7 +833,7 @@ struct Gen {
       os << "        int sl" << (o < 0 ? "m" : "p") << std::abs(o) << " = cr - " << H + o << "; if (sl"
          << (o < 0 ? "m" : "p") << std::abs(o) << " < 0) sl" << (o < 0 ? "m" : "p") << std::abs(o) << " += RING; sl"
          << (o < 0 ? "m" : "p") << std::abs(o) << " = sl" << (o < 0 ? "m" : "p") << std::abs(o) << " * 32 + l;\n";
-    epilogue4(g, merged, LS, "        ");
+    epilogue4(g, merged, LS, "        ", RS);
     os << "      }\n"
        << "      __syncthreads();  // CL ring rows are rewritten by the next step's phase 1\n"
        << "      // Input block s (read by phase 1 and, for p, by phase 2) is free now.\n"
@@ -836,7 +842,7 @@ struct Gen {
        << "        " << issue("s + NBUF")
        << "      }\n"
        << "      ss = ss + 1 == NBUF ? 0 : ss + 1;\n"
-       << "      cr += 8; if (cr >= RING) cr -= RING;\n"
+       << "      cr += " << RS << "; if (cr >= RING) cr -= RING;\n"
        << "    }\n"
        << "    slot0 += nblk; slot0 %= NBUF;\n"
        << "  }\n"
@@ -849,8 +855,10 @@ struct Gen {
     ti.band = BW;
     ti.rx = RX;
     ti.win = WIN;
+    ti.rows = RS;
+    ti.threads = 32 * RS;
     for (auto& x : slots) ti.slots.push_back({x.first, x.second});
-    tma_info = ti;
+    (RS == 8 ? tma_info : tma7_info) = ti;
     staged.clear();
   }
   // Warp-streaming TMA apply (2-D domains).  A block is NW warps side by
@@ -1289,19 +1297,21 @@ struct Gen {
 
   static long long NB(long long D1, int BW) { return (D1 + BW - 1) / BW; }
   bool f64_disabled_tma() const { return std::getenv("MO_B200_NO_TMA") != nullptr; }
-  ModuleInfo::Tma tma_info;
+  ModuleInfo::Tma tma_info, tma7_info;
 
   // Phase-2 epilogue of the TMA kernel.  Columns are 32-bit (num_cols < 2^31
   // is checked on the host).  The per-column exclusion mask of a column of a
   // field on this domain equals the element mask (k_colmask), so ZEROEXCL
   // reuses `ex` instead of re-reading colmask.
-  void epilogue4(const GatherSet& g, const std::vector<MLane>& merged, int LS, const std::string& ind) {
+  void epilogue4(const GatherSet& g, const std::vector<MLane>& merged, int LS, const std::string& ind, int RS = 8) {
+    const int LRS = RS == 8 ? 3 : 2;
     const int U = int(P.unknowns.size());
     os << ind << "Real* const OUT = (Real*)P.out0; const Real* const PV = (const Real*)P.in0; (void)PV;\n"
        << ind << "const Real* const DAMP = (const Real*)P.in1; (void)DAMP;\n"
        << ind << "const int fl = P.flags;\n"
        << ind << "// staged p of the output row (input row y = block s row w - H + RX)\n"
-       << ind << "int rp = ss + ((w - H + RX) >> 3); if (rp >= NBUF) rp -= NBUF; rp = rp * 8 + ((w - H + RX) & 7);\n"
+       << ind << "int rp = ss + ((w - H + RX) >> " << LRS << "); if (rp >= NBUF) rp -= NBUF; rp = rp * " << RS
+       << " + ((w - H + RX) & " << RS - 1 << ");\n"
        << ind << "const int lx = l + RX + sh; (void)lx;\n"
        << ind << "Real pa = (Real)0;  // this pixel's p'Ap terms (products in Real, as pcg.hpp:43)\n";
     std::vector<int> fields;
@@ -1595,6 +1605,7 @@ struct Gen {
       gather_jtj6(g, int(i));
       stream_info = ModuleInfo::Stream{};
       tma_info = ModuleInfo::Tma{};
+      tma7_info = ModuleInfo::Tma{};
       tma5_info = ModuleInfo::Tma{};
       TwoPhase tp = gather_jtj2(g, int(i));
       info.jtj2.push_back({tp.ok, tp.smem, tp.nlanes, tp.H});
@@ -1602,6 +1613,7 @@ struct Gen {
       info.jtj4.push_back(tma_info);
       info.jtj5.push_back(tma5_info);
       info.jtj6.push_back(tma6_info);
+      info.jtj7.push_back(tma7_info);
     }
     for (size_t i = 0; i < P.graph_sets.size(); ++i) {
       const GraphSet& g = P.graph_sets[i];

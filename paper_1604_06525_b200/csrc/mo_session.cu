@@ -1050,9 +1050,10 @@ class Session final : public SessionBase {
   // two-phase bands, 3 = TMA-staged row-streaming bands (block-wide 8-row
   // steps), 4 = TMA-staged warp-streaming bands, 5 = TMA-staged gather
   // program (2-D domains).
-  static constexpr int kVariants = 6;
+  static constexpr int kVariants = 7;
   const ModuleInfo::Tma* tma_info(size_t i, int v) const {
     if (v == 3 && i < minfo_.jtj4.size()) return &minfo_.jtj4[i];
+    if (v == 6 && i < minfo_.jtj7.size()) return &minfo_.jtj7[i];
     if (v == 4 && i < minfo_.jtj5.size()) return &minfo_.jtj5[i];
     if (v == 5 && i < minfo_.jtj6.size()) return &minfo_.jtj6[i];
     return nullptr;
@@ -1067,12 +1068,12 @@ class Session final : public SessionBase {
   }
   int variant(size_t i) const {
     if (i < jtj_choice_.size() && variant_ok(i, jtj_choice_[i])) return jtj_choice_[i];
-    for (int v : {4, 3, 2, 1}) if (variant_ok(i, v)) return v;
+    for (int v : {3, 6, 5, 4, 2, 1}) if (variant_ok(i, v)) return v;
     return 0;
   }
   static const char* variant_prefix(int v) {
     static const char* n[] = {"mo_gather_jtj_",  "mo_gather_jtj2_", "mo_gather_jtj3_",
-                              "mo_gather_jtj4_", "mo_gather_jtj5_", "mo_gather_jtj6_"};
+                              "mo_gather_jtj4_", "mo_gather_jtj5_", "mo_gather_jtj6_", "mo_gather_jtj7_"};
     return n[v];
   }
 
@@ -1170,7 +1171,8 @@ class Session final : public SessionBase {
                        : fs == "stream" ? 2
                        : fs == "tma" ? 3
                        : fs == "warp" ? 4
-                                      : 5;
+                       : fs == "gprog" ? 5
+                                       : 6;
       if (want >= 0) {
         jtj_choice_[i] = variant_ok(i, want) ? want : -1;
         if (jtj_choice_[i] >= 0) continue;
@@ -1206,7 +1208,7 @@ class Session final : public SessionBase {
       cudaEventDestroy(a);
       cudaEventDestroy(b);
       int bestv = 0;
-      for (int v : {3, 5, 4, 2, 1, 0})
+      for (int v : {3, 6, 5, 4, 2, 1, 0})
         if (t[v] <= 1.05f * best) {
           bestv = v;
           break;
@@ -1261,7 +1263,7 @@ class Session final : public SessionBase {
     jtj_occupancy(i);  // sets the dynamic smem attribute once
     const mo_tmaps& T = tmaps_for(i, v, kp);
     void* args[] = {const_cast<mo_kparams*>(&kp), const_cast<mo_tmaps*>(&T)};
-    const dim3 block = v == 4 ? dim3(unsigned(jtj_threads(i)), 1, 1) : dim3(MO_TILE_X, MO_TILE_Y, 1);
+    const dim3 block = v == 4 ? dim3(unsigned(jtj_threads(i)), 1, 1) : dim3(32, unsigned(jtj_threads(i) / 32), 1);
     klc(f, dim3(grid), block, args, smem);
     ++launches_;
   }
@@ -1279,10 +1281,12 @@ class Session final : public SessionBase {
     const long long nb = (sh[1] + band - 1) / band;
     const long long grid = (long long)nsm_ * jtj_occupancy(i);
     const bool rowwise = variant(i) == 4;
+    const ModuleInfo::Tma* ti = tma_info(i, variant(i));
+    const int step = ti && variant(i) != 4 ? ti->rows : 8;  // rows per step of the block-stepped variants
     int best = 0;
     double best_cost = 1e300;
-    for (int m = 1; m <= (rowwise ? 256 : 16); ++m) {
-      const int ch = rowwise ? m : 8 * m - 2 * halo;
+    for (int m = 1; m <= (rowwise ? 256 : 128 / step); ++m) {
+      const int ch = rowwise ? m : step * m - 2 * halo;
       if (ch <= 0) continue;
       const long long items = nb * ((rows + ch - 1) / ch);
       const long long rounds = (items + grid - 1) / grid;

@@ -5,7 +5,7 @@
 # Results land in gpurun_out/; profiles/summarize.py turns them into profiles/.
 R=${ROUND:-r01}
 mkdir -p gpurun_out
-variant() { case "$1" in *jtj6_*) echo gprog;; *jtj5_*) echo warp;; *jtj4_*) echo tma;; *jtj3_*) echo stream;; *jtj2_*) echo twophase;; *) echo gather;; esac; }
+variant() { case "$1" in *jtj7_*) echo tma4;; *jtj6_*) echo gprog;; *jtj5_*) echo warp;; *jtj4_*) echo tma;; *jtj3_*) echo stream;; *jtj2_*) echo twophase;; *) echo gather;; esac; }
 while read -r tag args; do
   [ -z "$tag" ] && continue
   timeout 900 python bench.py $args --steps 5 --warmup 3 ${CPU:---no-cpu-baseline} > gpurun_out/${R}_${tag}_bench.json 2> gpurun_out/${R}_${tag}_bench.err

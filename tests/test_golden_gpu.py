@@ -118,9 +118,9 @@ def test_kernels_bitwise_deterministic(name):
     assert outs[0][3] == outs[1][3]
 
 
-VARIANTS = ["gather", "twophase", "stream", "tma", "warp", "gprog"]
+VARIANTS = ["gather", "twophase", "stream", "tma", "warp", "gprog", "tma4"]
 PREFIX = {"gather": "mo_gather_jtj_", "twophase": "mo_gather_jtj2_", "stream": "mo_gather_jtj3_",
-          "tma": "mo_gather_jtj4_", "warp": "mo_gather_jtj5_", "gprog": "mo_gather_jtj6_"}
+          "tma": "mo_gather_jtj4_", "warp": "mo_gather_jtj5_", "gprog": "mo_gather_jtj6_", "tma4": "mo_gather_jtj7_"}
 GRID = [n for n in NAMES if n.startswith("cfg_") and "mesh" not in n]
 
 
