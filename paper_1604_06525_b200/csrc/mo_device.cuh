@@ -55,7 +55,6 @@ enum {
   MO_F_PATCH = 4,      // bm: identity patch + unconstrained (solver.hpp:241-250)
   MO_F_ZEROEXCL = 8,   // jtj: zero excluded columns        (pcg.hpp:101)
   MO_F_SKIPDONE = 16,  // return at once when the PCG has already stopped
-  MO_F_PUPD = 32,      // two-phase apply: p = z + beta p_old fused into staging (pcg.hpp:124-126)
   MO_F_PCGINIT = 64,   // bm: also delta = 0, r = b, p = z = b/m, rz0 (pcg.hpp:75-97)
 };
 
@@ -80,11 +79,11 @@ struct mo_kparams {
   int flags;
   void* out0;
   void* out1;
-  const void* in0;  // p for damp / p'Ap (PUPD: p_old)
+  const void* in0;  // p for damp / p'Ap
   const void* in1;  // damp
-  const void* in2;  // PUPD: r
-  const void* in3;  // PUPD: m (+damp) preconditioner
-  void* out2;       // PUPD: p_new; PCGINIT: p
+  const void* in2;  // (unused)
+  const void* in3;  // (unused)
+  void* out2;       // PCGINIT: p
   void* out3;       // PCGINIT: delta
   void* out4;       // PCGINIT: r
   const unsigned char* mask;     // per-element exclusion (uint8) or null

@@ -1506,10 +1506,7 @@ class Session final : public SessionBase {
 
   // out = 2 J^T J pv (+ damp pv), optionally zeroing excluded columns and
   // reducing p'Ap into alpha (flags: MO_F_DAMP | MO_F_REDUCE | MO_F_ZEROEXCL).
-  // (MO_F_PUPD: pv is p_old; the two-phase kernels stage p = z + beta p_old
-  //  from rvec/mdvec and write it to pnew.)
-  void apply(const Real* pv, Real* out, int flags, const Real* rvec = nullptr, const Real* mdvec = nullptr,
-             Real* pnew = nullptr) {
+  void apply(const Real* pv, Real* out, int flags) {
     if (vertex_apply_one_pass()) {
       apply_vertex_fused(pv, out, flags);
       return;
@@ -1526,9 +1523,6 @@ class Session final : public SessionBase {
     int base = 0;
     for (size_t i = 0; i < P_.gather_sets.size(); ++i) {
       mo_kparams kp = kp_apply(i, pv, out, fused ? flags : (flags & MO_F_SKIPDONE));
-      kp.in2 = rvec;
-      kp.in3 = mdvec;
-      kp.out2 = pnew;
       kp.red = red(base, total, MO_FIN_PCG_ALPHA, 0);
       launch_apply(i, kp, grids[i]);
       base += grids[i];
