@@ -37,8 +37,8 @@ NL, LIN = 10, 20
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="arap_warp")
     ap.add_argument("--prec", default="f32", choices=["f32", "f64"])
@@ -87,7 +87,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -133,6 +133,24 @@ def ncu_traffic(config, kernel):
         return e["dram_bytes"] if e.get("kernel") == kernel else None
     except Exception:
         return None
+
+
+def jtf_roofline(info, rb, units, ms, n, peak, prob):
+    """J^T F + Jacobi (build_normal) kernel: algorithmic bytes of the bm
+    program per element (+ the PCG start it carries for GN grids: delta, r, p
+    writes) over its mean launch time."""
+    from paper_1604_06525_b200 import planinfo
+    if not n:
+        return None
+    per = planinfo.algorithmic_bytes_per_element(info, "gather_set", "bm", rb)
+    cols = sum(f[1] for f in info.fields["U"])  # unknown columns per element
+    fused = prob.method == "gn" and not prob.graphs
+    per_total = per + (3 * cols * rb if fused else 0)
+    avg_us = ms / n * 1e3
+    ach = per_total * units / (avg_us * 1e-6) / 1e9
+    return {"bound": "hbm", "kernel": "build_normal (b = -2 J^T F, m = diag 2 J^T J" +
+            (", + PCG start" if fused else "") + ")", "achieved": ach, "peak": peak, "unit": "GB/s",
+            "frac": ach / peak, "alg_bytes_per_elem": per_total, "avg_launch_us": avg_us, "launches": n}
 
 
 def cpu_reference(prob, prec, repeat, threads):
@@ -219,6 +237,7 @@ def run_ours(args):
         call("mo_solve", s._h, _lib.ITER_CB(), None, ctypes.byref(res))
         return res
 
+    clk = ClockSampler(local).__enter__()  # sampling runs through warm-up and the timed steps
     for _ in range(args.warmup):
         restore()
         solve_resident()
@@ -228,7 +247,7 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    if True:
         for _ in range(args.steps):
             restore()
             with torch.cuda.stream(st):
@@ -240,6 +259,7 @@ def run_ours(args):
             ev1.synchronize()
             times.append(ev0.elapsed_time(ev1))
     torch.cuda.synchronize()
+    clk.__exit__(None, None, None)
     launches = s.kernel_launches() - launches0
     step_ms = float(np.mean(times))
     if world > 1:
@@ -260,6 +280,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     apply_ms, apply_n = s.profile(0)
     upd_ms, upd_n = s.profile(1)
+    bm_ms, bm_n = s.profile(2)
     s.set_profiling(False)
 
     # e2e through the public API with pinned host buffers.
@@ -311,6 +332,7 @@ def run_ours(args):
                      "alg_bytes_per_launch": alg, "alg_bytes_per_elem": per_elem,
                      "avg_launch_us": avg_apply * 1e3, "launches": apply_n,
                      "pcg_update_avg_us": upd_ms / max(upd_n, 1) * 1e3},
+        "roofline_jtf": jtf_roofline(info, rb, units, bm_ms, bm_n, peak, prob),
         "e2e": {"value": float(np.median(e2e)) / NL, "unit": "ms/iter", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
