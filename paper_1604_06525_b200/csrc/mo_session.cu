@@ -1581,9 +1581,11 @@ class Session final : public SessionBase {
       kl(k_pcg_update<Real>, dim3(vgu), dim3(MO_THREADS), red(0, vgu, MO_FIN_PCG_BETA, 0), n, colmask_, mdv, delta_, r_, p_, ap_, pre);
       ++launches_;
       reduce_done(MO_FIN_PCG_BETA, 0);
-      kl(k_pcg_p<Real>, dim3(vgu), dim3(MO_THREADS), state_, n, colmask_, mdv, r_, p_, pre);
-      ++launches_;
-      exchange_cols(p_);
+      if (k + 1 < cfg_.linear_iters) {  // the last direction is never applied
+        kl(k_pcg_p<Real>, dim3(vgu), dim3(MO_THREADS), state_, n, colmask_, mdv, r_, p_, pre);
+        ++launches_;
+        exchange_cols(p_);
+      }
       prof_end(1);
     }
   }
