@@ -638,6 +638,7 @@ struct Gen {
       for (const L& l : lanes) lg.push_back({l.t, l.out, l.f, l.c, l.o0, l.o1});
       gather_jtj4(g, gi, *S, lg, lane_slot, merged_off(merged), H);
       gather_jtj4(g, gi, *S, lg, lane_slot, merged_off(merged), H, 4);
+      gather_jtj4(g, gi, *S, lg, lane_slot, merged_off(merged), H, 8, true);
       gather_jtj5(g, gi, *S, lg, lane_slot, merged_off(merged), H);
     }
     return tp;
@@ -654,10 +655,18 @@ struct Gen {
   // (eval.hpp:47-51), so border bands run the same code.
   // RS = rows per step = warps per block (8: mo_gather_jtj4_<gi>, 4:
   // mo_gather_jtj7_<gi>, twice the resident blocks for small grids).
+  // bm = true: the same schedule for build_normal (solver.hpp:220-251):
+  // phase 1 evaluates evalj AND evalf (residual values, one per template,
+  // plan.hpp:236-239) once per element and forms per merged lane the J^T F
+  // terms d_l r_t and the Jacobi terms d_l^2 (two contribution planes);
+  // phase 2 gathers b = -2 sum, m = 2 sum with the identity patch, the
+  // unconstrained count and the fused PCG start (mo_gather_bm4_<gi>).
   void gather_jtj4(const GatherSet& g, int gi, const GridSet& S, const std::vector<LaneG>& lanes,
-                   const std::vector<int>& lane_slot, const std::vector<MLane>& merged, int H, int RS = 8) {
+                   const std::vector<int>& lane_slot, const std::vector<MLane>& merged, int H, int RS = 8,
+                   bool bm = false) {
     const int LRS = RS == 8 ? 3 : 2;
-    const std::string LN = RS == 8 ? "mo_lanes4_" : "mo_lanes7_";
+    const std::string LN = bm ? "mo_lanesbm_" : RS == 8 ? "mo_lanes4_" : "mo_lanes7_";
+    if (bm && S.evalf.outputs.size() != S.jtemplates.size()) return;
     if (f64_disabled_tma()) return;
     const std::string sfx = std::to_string(gi);
     const auto sh = P.shape_of(g.dom);
@@ -665,7 +674,7 @@ struct Gen {
     const int BW = 32 - 2 * H;
     if (BW < 8) return;
     const int U = int(P.unknowns.size());
-    const int RX = std::max(reach_of(S.evalj, &g.dom), H);
+    const int RX = std::max(std::max(reach_of(S.evalj, &g.dom), bm ? reach_of(S.evalf, &g.dom) : 0), H);
     if (2 * RX > RS) return;  // two RS-row blocks cover one step's input rows
     // TMA needs a 16-byte aligned box start: the window starts at the
     // aligned column cs <= c0 - H - RX (shift sh = c0 - H - RX - cs < AU).
@@ -689,12 +698,21 @@ struct Gen {
       const Field& f = field_of(in.op, in.field);
       if (f.dom == g.dom) add(slot_of(in.op, in.field), f.channels);
     }
-    for (const LaneG& l : lanes) add(U + l.f, P.unknowns[size_t(l.f)].channels);
+    if (bm) {
+      for (const Instr& in : S.evalf.instrs) {
+        if (!(in.op == kLoadU || in.op == kLoadA || in.op == kLoadC || in.op == kLoadP) || in.graph) continue;
+        const Field& f = field_of(in.op, in.field);
+        if (f.dom == g.dom) add(slot_of(in.op, in.field), f.channels);
+      }
+    } else {
+      for (const LaneG& l : lanes) add(U + l.f, P.unknowns[size_t(l.f)].channels);
+    }
     if (slots.empty() || int(slots.size()) > MO_MAX_TMAPS_HOST) return;
     for (auto& x : slots)
       if (WIN * x.second > 256) return;  // TMA box inner extent limit
     // Dynamic smem layout: CL ring | field rings (128-B aligned) | mbarriers.
-    long long off = (long long)NM * LS * RB;
+    const int NPL = bm ? 2 * NM : NM;  // contribution planes
+    long long off = (long long)NPL * LS * RB;
     off = (off + 127) / 128 * 128;
     staged.clear();
     long long tx = 0;
@@ -712,12 +730,31 @@ struct Gen {
     st_rx = RX;
     st_win = WIN;
     const std::string pe = program(S.evalj, false, &g.dom, true);
+    const std::string pf = bm ? program(S.evalf, false, &g.dom, true) : std::string();
     const int NO = int(S.evalj.outputs.size());
+    const int NT = int(S.jtemplates.size());
     // Phase-1 body from shared memory.
     os << "template <bool I> __device__ __forceinline__ void " << LN << sfx
        << "(const mo_kparams& P, int p0, int p1, int k, Real* CL, const int* ri, int lx) {\n"
        << "  const bool inside = I || mo_inb(P, p0, p1, 0);\n"
        << "  Real d[" << NO << "];\n  " << pe << "<I>(P, p0, p1, 0, ri, lx, d);\n";
+    if (bm) {
+      os << "  Real fv[" << NT << "];\n  " << pf << "<I>(P, p0, p1, 0, ri, lx, fv);\n";
+      for (int si = 0; si < NM; ++si) os << "  Real mb" << si << " = (Real)0, mm" << si << " = (Real)0;\n";
+      for (int t = 0; t < NT; ++t) {
+        const bool origin = S.jtemplates[size_t(t)].origin;
+        os << "  {" << (origin ? " if (inside) {" : "") << "\n";
+        for (size_t li = 0; li < lanes.size(); ++li)
+          if (lanes[li].t == t)
+            os << "    mb" << lane_slot[li] << " += d[" << lanes[li].out << "] * fv[" << t << "]; mm" << lane_slot[li]
+               << " += d[" << lanes[li].out << "] * d[" << lanes[li].out << "];\n";
+        os << "  }" << (origin ? " }" : "") << "\n";
+      }
+      for (int si = 0; si < NM; ++si)
+        os << "  CL[" << si * LS << " + k] = mb" << si << "; CL[" << (NM + si) * LS << " + k] = mm" << si << ";\n";
+      os << "}\n";
+    }
+    if (!bm) {
     for (int si = 0; si < NM; ++si) os << "  Real m" << si << " = (Real)0;\n";
     for (size_t t = 0; t < S.jtemplates.size(); ++t) {
       os << "  { Real jp = (Real)0;\n";
@@ -732,17 +769,23 @@ struct Gen {
     }
     for (int si = 0; si < NM; ++si) os << "  CL[" << si * LS << " + k] = m" << si << ";\n";
     os << "}\n";
+    }
     sm_mode = false;
 
-    const std::string kn = (RS == 8 ? "mo_gather_jtj4_" : "mo_gather_jtj7_") + sfx;
+    const std::string kn = (bm ? "mo_gather_bm4_" : RS == 8 ? "mo_gather_jtj4_" : "mo_gather_jtj7_") + sfx;
     const char* mb = std::getenv("MO_B200_JTJ4_MINB");
     const int minb = mb ? std::atoi(mb) : 32 / RS;
     os << "extern \"C\" __global__ void __launch_bounds__(" << 32 * RS << (minb > 0 ? ", " + std::to_string(minb) : "")
        << ") " << kn << "(const __grid_constant__ mo_kparams P, const __grid_constant__ mo_tmaps T) {\n"
        << "  MO_PDL_ENTRY();\n"
        << "  if ((P.flags & MO_F_SKIPDONE) && P.state->done) return;\n"
-       << "  Real* CL = reinterpret_cast<Real*>(mo_dsm);  // [" << NM << " merged lanes][" << RING << " rows][32]\n"
-       << "  unsigned long long* MB = reinterpret_cast<unsigned long long*>(mo_dsm + " << mbar_off << ");\n"
+       << "  Real* CL = reinterpret_cast<Real*>(mo_dsm);  // [" << NPL << " planes][" << RING << " rows][32]\n"
+       << "  double cnt = 0, rz = 0; (void)cnt; (void)rz;\n";
+    if (bm)
+      os << "  if ((P.flags & MO_F_PCGINIT) && blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0) {\n"
+         << "    P.state->done = 0; P.state->iters = 0; P.state->indefinite = 0; P.state->nonfinite = 0;\n"
+         << "  }\n";
+    os << "  unsigned long long* MB = reinterpret_cast<unsigned long long*>(mo_dsm + " << mbar_off << ");\n"
        << "  double acc = 0;\n"
        << "  unsigned em = 0;  // max exponent field of the outputs: all ones <=> a non-finite output\n"
        << "  const int tid = threadIdx.x + threadIdx.y * blockDim.x;\n"
@@ -833,7 +876,8 @@ struct Gen {
       os << "        int sl" << (o < 0 ? "m" : "p") << std::abs(o) << " = cr - " << H + o << "; if (sl"
          << (o < 0 ? "m" : "p") << std::abs(o) << " < 0) sl" << (o < 0 ? "m" : "p") << std::abs(o) << " += RING; sl"
          << (o < 0 ? "m" : "p") << std::abs(o) << " = sl" << (o < 0 ? "m" : "p") << std::abs(o) << " * 32 + l;\n";
-    epilogue4(g, merged, LS, "        ", RS);
+    if (bm) epilogue_bm4(g, merged, LS, NM, "        ", RS);
+    else epilogue4(g, merged, LS, "        ", RS);
     os << "      }\n"
        << "      __syncthreads();  // CL ring rows are rewritten by the next step's phase 1\n"
        << "      // Input block s (read by phase 1 and, for p, by phase 2) is free now.\n"
@@ -846,8 +890,11 @@ struct Gen {
        << "    }\n"
        << "    slot0 += nblk; slot0 %= NBUF;\n"
        << "  }\n"
-       << "  if (em == MO_EXP_MASK) atomicOr(&P.state->nonfinite_kernel, 1);\n"
-       << "  if (P.flags & MO_F_REDUCE) mo_reduce_epilogue<Real>(P.red, acc, 0.0, false);\n}\n";
+       << "  if (em == MO_EXP_MASK) atomicOr(&P.state->nonfinite_kernel, 1);\n";
+    if (bm)
+      os << "  if (P.flags & MO_F_REDUCE) mo_reduce_epilogue<Real>(P.red, cnt, rz, (P.flags & MO_F_PCGINIT) != 0);\n}\n";
+    else
+      os << "  if (P.flags & MO_F_REDUCE) mo_reduce_epilogue<Real>(P.red, acc, 0.0, false);\n}\n";
     ModuleInfo::Tma ti;
     ti.ok = true;
     ti.smem = size_t(off);
@@ -858,7 +905,7 @@ struct Gen {
     ti.rows = RS;
     ti.threads = 32 * RS;
     for (auto& x : slots) ti.slots.push_back({x.first, x.second});
-    (RS == 8 ? tma_info : tma7_info) = ti;
+    (bm ? tmabm_info : RS == 8 ? tma_info : tma7_info) = ti;
     staged.clear();
   }
   // Warp-streaming TMA apply (2-D domains).  A block is NW warps side by
@@ -1297,7 +1344,7 @@ struct Gen {
 
   static long long NB(long long D1, int BW) { return (D1 + BW - 1) / BW; }
   bool f64_disabled_tma() const { return std::getenv("MO_B200_NO_TMA") != nullptr; }
-  ModuleInfo::Tma tma_info, tma7_info;
+  ModuleInfo::Tma tma_info, tma7_info, tmabm_info;
 
   // Phase-2 epilogue of the TMA kernel.  Columns are 32-bit (num_cols < 2^31
   // is checked on the host).  The per-column exclusion mask of a column of a
@@ -1345,6 +1392,42 @@ struct Gen {
          << ind << "  pa += pc * v; }\n";
     }
     os << ind << "if (fl & MO_F_REDUCE) acc += (double)pa;\n";
+  }
+
+  // Phase-2 epilogue of mo_gather_bm4: b = -2 sum_s cb_s(q - o_s),
+  // m = 2 sum_s cm_s(q - o_s); excluded -> b = m = 0, then the identity
+  // patch / unconstrained count (solver.hpp:241-250) and the fused PCG start
+  // (k_pcg_init on the patched b, m).
+  void epilogue_bm4(const GatherSet& g, const std::vector<MLane>& merged, int LS, int NM, const std::string& ind,
+                    int RS) {
+    (void)RS;
+    os << ind << "Real* const B = (Real*)P.out0; Real* const M = (Real*)P.out1;\n"
+       << ind << "Real* const PP = (Real*)P.out2; Real* const DL = (Real*)P.out3; Real* const RR = (Real*)P.out4;\n"
+       << ind << "const int fl = P.flags; const int pre = P.state->use_precond;\n";
+    for (size_t k = 0; k < g.chans.size(); ++k) {
+      const int f = g.chans[k].first, ch = g.chans[k].second;
+      const int C = P.unknowns[size_t(f)].channels;
+      os << ind << "{ Real sb = (Real)0, sm = (Real)0;\n";
+      for (size_t si = 0; si < merged.size(); ++si) {
+        const MLane& m = merged[si];
+        if (m.f != f || m.c != ch) continue;
+        const std::string sl = std::string("sl") + (m.o0 < 0 ? "m" : "p") + std::to_string(std::abs(m.o0));
+        os << ind << "  sb += CL[" << si * LS << " + " << sl << " - (" << m.o1 << ")]; sm += CL[" << (NM + si) * LS
+           << " + " << sl << " - (" << m.o1 << ")];\n";
+      }
+      os << ind << "  Real b = ex ? (Real)0 : (Real)-2 * sb, m = ex ? (Real)0 : (Real)2 * sm;\n"
+         << ind << "  em = max(em, max(MO_EXP_BITS(b), MO_EXP_BITS(m)));\n"
+         << ind << "  if (fl & MO_F_PATCH) {\n"
+         << ind << "    if (ex) { b = (Real)0; m = (Real)1; }\n"
+         << ind << "    else if (m == (Real)0) { m = (Real)1; cnt += 1.0; }\n"
+         << ind << "  }\n"
+         << ind << "  const int col = (int)P.ubase[" << f << "] + e * " << C << " + " << ch << ";\n"
+         << ind << "  B[col] = b; M[col] = m;\n"
+         << ind << "  if (fl & MO_F_PCGINIT) {\n"
+         << ind << "    const Real zi = ex ? (Real)0 : (pre ? ((b == (Real)0 && m > (Real)0) ? b : b / m) : b);\n"
+         << ind << "    DL[col] = (Real)0; RR[col] = b; PP[col] = zi; rz += (double)(b * zi);\n"
+         << ind << "  } }\n";
+    }
   }
 
   // Phase-2 gather + apply epilogue of the streaming kernels: out(f,c)(q) =
@@ -1606,6 +1689,7 @@ struct Gen {
       stream_info = ModuleInfo::Stream{};
       tma_info = ModuleInfo::Tma{};
       tma7_info = ModuleInfo::Tma{};
+      tmabm_info = ModuleInfo::Tma{};
       tma5_info = ModuleInfo::Tma{};
       TwoPhase tp = gather_jtj2(g, int(i));
       info.jtj2.push_back({tp.ok, tp.smem, tp.nlanes, tp.H});
@@ -1614,6 +1698,7 @@ struct Gen {
       info.jtj5.push_back(tma5_info);
       info.jtj6.push_back(tma6_info);
       info.jtj7.push_back(tma7_info);
+      info.bm4.push_back(tmabm_info);
     }
     for (size_t i = 0; i < P.graph_sets.size(); ++i) {
       const GraphSet& g = P.graph_sets[i];

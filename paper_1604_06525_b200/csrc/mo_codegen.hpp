@@ -39,6 +39,7 @@ struct ModuleInfo {
   std::vector<Tma> jtj5;       // per gather set: warp-streaming (box rows = rows)
   std::vector<Tma> jtj6;       // per gather set: TMA-staged gather program
   std::vector<Tma> jtj7;       // per gather set: variant 3 with 4-row steps (128 threads)
+  std::vector<Tma> bm4;        // per gather set: TMA two-phase build_normal (mo_gather_bm4_<i>)
   std::vector<bool> vertex_kernels;  // per graph set: mo_graph_v{jtj,bm}_<g>_<dom> exist
   bool fused_vertex_apply = false;   // mo_graph_vjtjf_0: grid gather + graph gather + finish in one pass
 };

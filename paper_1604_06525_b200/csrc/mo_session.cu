@@ -1051,7 +1051,9 @@ class Session final : public SessionBase {
   // steps), 4 = TMA-staged warp-streaming bands, 5 = TMA-staged gather
   // program (2-D domains).
   static constexpr int kVariants = 7;
+  static constexpr int kBm4 = 100;  // tma_info id of the TMA build_normal kernel
   const ModuleInfo::Tma* tma_info(size_t i, int v) const {
+    if (v == kBm4 && i < minfo_.bm4.size()) return &minfo_.bm4[i];
     if (v == 3 && i < minfo_.jtj4.size()) return &minfo_.jtj4[i];
     if (v == 6 && i < minfo_.jtj7.size()) return &minfo_.jtj7[i];
     if (v == 4 && i < minfo_.jtj5.size()) return &minfo_.jtj5[i];
@@ -1147,7 +1149,7 @@ class Session final : public SessionBase {
     // One decision per (module, shape) per process, so every session of a plan
     // runs the same kernel (bitwise run-to-run reproducibility).
     static std::mutex mu;
-    static std::map<std::string, std::vector<int>> cache;
+    static std::map<std::string, std::vector<int>> cache, bm_cache;
     const char* force = std::getenv("MO_B200_JTJ");
     std::string key = module_key_ + (force ? std::string("/force:") + force : "");
     for (auto& d : P_.dims) key += "/" + std::to_string(d.second);
@@ -1158,6 +1160,7 @@ class Session final : public SessionBase {
       auto it = cache.find(key);
       if (it != cache.end()) {
         jtj_choice_ = it->second;
+        bm_choice_ = bm_cache[key];
         return;
       }
     }
@@ -1215,8 +1218,39 @@ class Session final : public SessionBase {
         }
       jtj_choice_[i] = bestv;
     }
+    // build_normal: TMA two-phase kernel vs the reference's bm program.
+    bm_choice_.assign(P_.gather_sets.size(), 0);
+    const int stage = cur_stage_;
+    cur_stage_ = -1;  // no profiling events while tuning
+    const int64_t launched = launches_;
+    for (size_t i = 0; i < P_.gather_sets.size(); ++i) {
+      if (!bm4_avail(i)) continue;
+      float tb[2] = {1e30f, 1e30f};
+      cudaEvent_t a, b;
+      CK(cudaEventCreate(&a));
+      CK(cudaEventCreate(&b));
+      for (int v = 0; v < 2; ++v) {
+        bm_choice_[i] = v;
+        normal_device();  // warm-up
+        for (int round = 0; round < 3; ++round) {
+          CK(cudaEventRecord(a, st_));
+          for (int rep = 0; rep < 3; ++rep) normal_device();
+          CK(cudaEventRecord(b, st_));
+          CK(cudaEventSynchronize(b));
+          float ms = 0;
+          CK(cudaEventElapsedTime(&ms, a, b));
+          tb[v] = std::min(tb[v], ms);
+        }
+      }
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+      bm_choice_[i] = tb[1] < 0.95f * tb[0] ? 1 : 0;
+    }
+    launches_ = launched;
+    cur_stage_ = stage;
     std::lock_guard<std::mutex> lk(mu);
     cache[key] = jtj_choice_;
+    bm_cache[key] = bm_choice_;
   }
   std::string jtj_kernel(size_t i) const { return variant_prefix(variant(i)) + std::to_string(i); }
   size_t jtj_smem(size_t i) const {
@@ -1446,6 +1480,38 @@ class Session final : public SessionBase {
   // the patched b, m), when they write every column (no graph scatters, every
   // unknown channel an output of exactly one gather set).  On a strip the
   // kernels cover the owned rows only; halo p arrives by the exchange.
+  // TMA two-phase build_normal (mo_gather_bm4_<i>), fast mode only;
+  // MO_B200_NO_BM4=1 keeps the reference's bm gather program.
+  bool bm4_avail(size_t i) const {
+    if (std::getenv("MO_B200_NO_BM4") || P_.exact || i >= minfo_.bm4.size() || !minfo_.bm4[i].ok) return false;
+    return tma_capable(i, minfo_.bm4[i]);
+  }
+  // chosen by tune_apply (timed against the bm gather program; kept only
+  // when >5% faster: it wins on large grids, loses on small ones)
+  bool bm4_ok(size_t i) const { return i < bm_choice_.size() && bm_choice_[i] && bm4_avail(i); }
+  int bm4_grid(size_t i, int* chunk) {
+    const ModuleInfo::Tma& ti = minfo_.bm4[i];
+    const void* f = mod_.kernel("mo_gather_bm4_" + std::to_string(i));
+    const int occ = occupancy(f, ti.smem);
+    const auto sh = P_.shape_of(P_.gather_sets[i].dom);
+    const long long rows = sh_.on ? sh_.row1 - sh_.row0 : sh[0];
+    const long long nb = (sh[1] + ti.band - 1) / ti.band, grid = (long long)nsm_ * occ;
+    int best = 0;
+    double best_cost = 1e300;
+    for (int m = 1; m <= 16; ++m) {  // same round model as the apply (jtj3_chunk)
+      const int ch = 8 * m - 2 * ti.halo;
+      if (ch <= 0) continue;
+      const long long items = nb * ((rows + ch - 1) / ch);
+      const double cost = double((items + grid - 1) / grid) * (m + 0.5);
+      if (cost <= best_cost) {
+        best_cost = cost;
+        best = ch;
+      }
+    }
+    *chunk = std::max(best, 1);
+    const long long items = nb * ((rows + *chunk - 1) / *chunk);
+    return int(std::max<long long>(1, std::min(items, grid)));
+  }
   bool bm_init_ok() const {
     static const bool off = std::getenv("MO_B200_NO_BMINIT") != nullptr;
     if (off || !P_.graph_sets.empty() || P_.gather_sets.empty()) return false;
@@ -1458,16 +1524,24 @@ class Session final : public SessionBase {
     prof_begin(2);
     const bool fused = P_.graph_sets.empty();
     const long long n = P_.num_cols;
-    std::vector<int> grids;
+    std::vector<int> grids, chunks;
     int total = 0;
     for (size_t i = 0; i < P_.gather_sets.size(); ++i) {
-      grids.push_back(grid_blocks("mo_gather_bm_" + std::to_string(i), P_.gather_sets[i].dom));
+      if (bm4_ok(i)) {
+        int ch = 0;
+        grids.push_back(bm4_grid(i, &ch));
+        chunks.push_back(ch);
+      } else {
+        grids.push_back(grid_blocks("mo_gather_bm_" + std::to_string(i), P_.gather_sets[i].dom));
+        chunks.push_back(0);
+      }
       total += grids.back();
     }
     if (!fused) total = vgrid(n, nsm_);
     int base = 0;
     for (size_t i = 0; i < P_.gather_sets.size(); ++i) {
       mo_kparams kp = kp_grid(P_.gather_sets[i].dom, x_, nullptr);
+      kp.chunk = chunks[i];
       kp.out0 = b_;
       kp.out1 = m_;
       kp.flags = fused ? (MO_F_PATCH | MO_F_REDUCE) : 0;
@@ -1479,7 +1553,15 @@ class Session final : public SessionBase {
         kp.out3 = delta_;
         kp.out4 = r_;
       }
-      launch_grid("mo_gather_bm_" + std::to_string(i), P_.gather_sets[i].dom, kp, grids[i]);
+      if (chunks[i]) {  // TMA two-phase build_normal
+        const void* f = mod_.kernel("mo_gather_bm4_" + std::to_string(i));
+        const mo_tmaps& T = tmaps_for(i, kBm4, kp);
+        void* args[] = {&kp, const_cast<mo_tmaps*>(&T)};
+        klc(f, dim3(grids[i]), dim3(MO_TILE_X, MO_TILE_Y, 1), args, minfo_.bm4[i].smem);
+        ++launches_;
+      } else {
+        launch_grid("mo_gather_bm_" + std::to_string(i), P_.gather_sets[i].dom, kp, grids[i]);
+      }
       base += grids[i];
     }
     if (!fused) {
@@ -1712,6 +1794,7 @@ class Session final : public SessionBase {
   ModuleInfo minfo_;
   std::map<int, cudaGraphExec_t> stage_exec_;
   bool tuned_ = false;
+  std::vector<int> bm_choice_;   // per gather set: 1 = TMA two-phase build_normal
   std::vector<int> jtj_choice_;  // per gather set: 0 gather program, 1 two-phase tiles, 2 streaming, 3 TMA streaming
   std::map<std::string, mo_tmaps> tmaps_;  // per (gather set, staged buffers)
   std::string module_key_;
