@@ -36,6 +36,7 @@ struct mo_state {
   double sums[8];
   unsigned counters[8];
   double mu;  // LM trust-region radius of the current trial
+  double rzs[2];  // consumer-side reductions: rz of PCG iteration k in rzs[k & 1]
 };
 
 // Finalisation ops run by the last block of a reduction.
@@ -47,6 +48,7 @@ enum {
   MO_FIN_UNCONSTRAINED = 4,
   MO_FIN_STORE2 = 5,     // sums[slot], sums[slot+1] = pair totals
   MO_FIN_BM_INIT = 6,    // unconstrained count + rz0 / stop test (fused bm + pcg init)
+  MO_FIN_PARTIALS = 7,   // store the block partials only; the consuming kernel sums them
 };
 
 enum {
@@ -224,6 +226,7 @@ __device__ void mo_finalize(mo_state* st, int op, int arg, double total, double 
     case MO_FIN_PCG_INIT: {
       Real rz = Real(total);
       st->rz = double(rz);
+      st->rzs[0] = double(rz);
       if (!mo_finite(double(rz))) {
         st->nonfinite = 1;
         st->done = 1;
@@ -284,6 +287,13 @@ __device__ void mo_reduce_epilogue(const mo_red& P, double v, double v2, bool tw
   const int bid = blockIdx.x;
   double s = mo_block_sum(v, sh);
   double s2 = two ? mo_block_sum(v2, sh) : 0.0;
+  if (P.fin_op == MO_FIN_PARTIALS) {  // the next kernel sums (mo_sum_partials)
+    if (tid == 0) {
+      P.partials[P.part_base + bid] = s;
+      if (two) P.partials[P.part_total + P.part_base + bid] = s2;
+    }
+    return;
+  }
   if (tid == 0) {
     P.partials[P.part_base + bid] = s;
     if (two) P.partials[P.part_total + P.part_base + bid] = s2;
@@ -325,6 +335,64 @@ __device__ void mo_reduce_epilogue(const mo_red& P, double v, double v2, bool tw
     *P.counter = 0u;
     mo_finalize<Real>(P.state, P.fin_op, P.fin_arg, tot, tot2);
   }
+}
+
+// Consumer side of a MO_FIN_PARTIALS reduction: every block sums the n block
+// partials of the previous kernel in the same fixed order (the last-block
+// scheme's order), so all blocks obtain the bitwise same total without the
+// producer's atomic + last-block tail.  All threads call it; total in all.
+__device__ __forceinline__ double mo_sum_partials(const double* p, int n) {
+  __shared__ double sh[32];
+  __shared__ double tot;
+  const int tid = threadIdx.x + threadIdx.y * blockDim.x;
+  const int nt = blockDim.x * blockDim.y;
+  double a = 0;
+  int i = tid;
+  for (; i + 3 * nt < n; i += 4 * nt) {
+    const double x0 = __ldcg(p + i), x1 = __ldcg(p + i + nt), x2 = __ldcg(p + i + 2 * nt), x3 = __ldcg(p + i + 3 * nt);
+    a += x0;
+    a += x1;
+    a += x2;
+    a += x3;
+  }
+  for (; i < n; i += nt) a += __ldcg(p + i);
+  const double t = mo_block_sum(a, sh);
+  if (tid == 0) tot = t;
+  __syncthreads();
+  return tot;
+}
+// alpha from p'Ap (pcg.hpp:100-110); block 0 (writer) records the state.
+// Returns false when the PCG stops here (indefinite / non-finite).
+template <class Real>
+__device__ __forceinline__ bool mo_alpha_from(mo_state* st, double total, int k, bool writer, Real* alpha) {
+  const Real pap = Real(total);
+  if (!mo_finite(double(pap))) {
+    if (writer) { st->pap = double(pap); st->nonfinite = 1; st->done = 1; }
+    return false;
+  }
+  if (pap <= Real(0)) {
+    if (writer) { st->pap = double(pap); st->indefinite = 1; st->done = 1; }
+    return false;
+  }
+  *alpha = Real(st->rzs[k & 1]) / pap;
+  if (writer) { st->pap = double(pap); st->alpha = double(*alpha); }
+  return true;
+}
+// beta from r'z (pcg.hpp:116-124): rz of iteration k is rzs[k & 1], the new
+// one goes to rzs[(k + 1) & 1].  Returns false when the PCG stops here.
+template <class Real>
+__device__ __forceinline__ bool mo_beta_from(mo_state* st, double total, int k, bool writer, Real* beta) {
+  const Real rzn = Real(total);
+  if (!mo_finite(double(rzn))) {
+    if (writer) { st->rz_next = double(rzn); st->nonfinite = 1; st->done = 1; }
+    return false;
+  }
+  const bool stop = rzn <= Real(st->stop);
+  if (writer) { st->rz_next = double(rzn); st->iters += 1; if (stop) st->done = 1; }
+  if (stop) return false;
+  *beta = rzn / Real(st->rzs[k & 1]);
+  if (writer) { st->beta = double(*beta); st->rz = double(rzn); st->rzs[(k + 1) & 1] = double(rzn); }
+  return true;
 }
 
 // Grid-stride tile iteration for a grid domain (reference exec.hpp:151-214:

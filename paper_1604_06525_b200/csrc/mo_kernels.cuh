@@ -138,10 +138,17 @@ template <class Real>
 __global__ void __launch_bounds__(MO_THREADS)
 k_pcg_update(mo_red R, long long n, const unsigned char* cm, const Real* __restrict__ md,
              Real* __restrict__ delta, Real* __restrict__ r, const Real* __restrict__ p,
-             const Real* __restrict__ ap, int precond) {
+             const Real* __restrict__ ap, int precond, const double* pap_part, int pap_n, int k) {
   MO_PDL_ENTRY();
   if (R.state->done) return;
-  const Real alpha = Real(R.state->alpha);
+  Real alpha;
+  if (pap_part) {  // consumer-side p'Ap (the apply only stored block partials)
+    const double tot = mo_sum_partials(pap_part, pap_n);
+    const bool writer = blockIdx.x == 0 && threadIdx.x == 0;
+    if (!mo_alpha_from<Real>(R.state, tot, k, writer, &alpha)) return;
+  } else {
+    alpha = Real(R.state->alpha);
+  }
   double acc = 0;
   const long long stride = (long long)gridDim.x * blockDim.x;
   const long long n4 = n >> 2;
@@ -172,11 +179,18 @@ __device__ __forceinline__ Real pcg_p1(Real beta, unsigned char m, Real r, Real 
 
 template <class Real>
 __global__ void __launch_bounds__(MO_THREADS)
-k_pcg_p(const mo_state* st, long long n, const unsigned char* cm, const Real* __restrict__ md,
-        const Real* __restrict__ r, Real* __restrict__ p, int precond) {
+k_pcg_p(mo_state* st, long long n, const unsigned char* cm, const Real* __restrict__ md,
+        const Real* __restrict__ r, Real* __restrict__ p, int precond, const double* rz_part, int rz_n, int k) {
   MO_PDL_ENTRY();
   if (st->done) return;
-  const Real beta = Real(st->beta);
+  Real beta;
+  if (rz_part) {  // consumer-side r'z of the update kernel
+    const double tot = mo_sum_partials(rz_part, rz_n);
+    const bool writer = blockIdx.x == 0 && threadIdx.x == 0;
+    if (!mo_beta_from<Real>(st, tot, k, writer, &beta)) return;
+  } else {
+    beta = Real(st->beta);
+  }
   const long long stride = (long long)gridDim.x * blockDim.x;
   const long long n4 = n >> 2;
   for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n4; v += stride) {
@@ -191,6 +205,17 @@ k_pcg_p(const mo_state* st, long long n, const unsigned char* cm, const Real* __
   }
   for (long long i = (n4 << 2) + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride)
     p[i] = pcg_p1(beta, cm ? cm[i] : (unsigned char)0, r[i], md[i], p[i], precond);
+}
+
+// Last PCG iteration under consumer-side reductions: no direction update,
+// only the r'z bookkeeping (iteration count, stop / non-finite flags).
+template <class Real>
+__global__ void k_pcg_fin(mo_state* st, const double* rz_part, int rz_n, int k) {
+  MO_PDL_ENTRY();
+  if (st->done) return;
+  const double tot = mo_sum_partials(rz_part, rz_n);
+  Real beta;
+  if (threadIdx.x == 0) mo_beta_from<Real>(st, tot, k, true, &beta);
 }
 
 // Unfused apply epilogue (plans with graph scatters): LM damping, excluded

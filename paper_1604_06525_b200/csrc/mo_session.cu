@@ -142,6 +142,7 @@ class Session final : public SessionBase {
     state_h_->use_precond = cfg_.use_preconditioner;
     CK(cudaMemcpyAsync(state_, state_h_, sizeof(mo_state), cudaMemcpyHostToDevice, st_));
     partials_ = dalloc<double>(2 * size_t(kPartCap));
+    partials2_ = dalloc<double>(2 * size_t(kPartCap));
     graphs_.resize(P_.graphs.size());
     gsets_.resize(P_.graph_sets.size());
     grid_rowbase_.resize(P_.grid_sets.size(), nullptr);
@@ -166,6 +167,7 @@ class Session final : public SessionBase {
     cudaFree(params_d_);
     cudaFree(state_);
     cudaFree(partials_);
+    cudaFree(partials2_);
     cudaFree(rankbuf_);
     cudaFreeHost(state_h_);
     for (auto& g : graphs_) cudaFree(g.d_verts);
@@ -1622,14 +1624,15 @@ class Session final : public SessionBase {
       total += grids.back();
     }
     if (!fused) total = vgrid(n, nsm_);
+    apply_parts_ = total;
     int base = 0;
     for (size_t i = 0; i < P_.gather_sets.size(); ++i) {
       mo_kparams kp = kp_apply(i, pv, out, fused ? flags : (flags & MO_F_SKIPDONE));
-      kp.red = red(base, total, MO_FIN_PCG_ALPHA, 0);
+      kp.red = red(base, total, consumer_ && fused ? MO_FIN_PARTIALS : MO_FIN_PCG_ALPHA, 0);
       launch_apply(i, kp, grids[i]);
       base += grids[i];
     }
-    if (fused && (flags & MO_F_REDUCE)) reduce_done(MO_FIN_PCG_ALPHA, 0);
+    if (fused && (flags & MO_F_REDUCE) && !consumer_) reduce_done(MO_FIN_PCG_ALPHA, 0);
     if (!fused) {
       for (size_t i = 0; i < P_.graph_sets.size(); ++i) {
         mo_kparams kp = kp_graph(int(i), x_, pv);
@@ -1673,20 +1676,36 @@ class Session final : public SessionBase {
     }
     exchange_cols(p_);  // strips: neighbours' p rows for the stencil apply
     const int flags = MO_F_REDUCE | MO_F_ZEROEXCL | MO_F_SKIPDONE | (lm ? MO_F_DAMP : 0);
+    // Consumer-side reductions (unsharded grid plans): the apply and the
+    // update only store block partials; the next kernel sums them in every
+    // block (same fixed order, bitwise the same total) and derives alpha /
+    // beta itself, removing the atomic + last-block tail from the producers.
+    static const bool nocons = std::getenv("MO_B200_NO_CONSUMER") != nullptr;
+    const bool cons = !nocons && !sh_.on && P_.graph_sets.empty();
     for (int k = 0; k < cfg_.linear_iters; ++k) {
       prof_begin(0);
+      consumer_ = cons;
       apply(p_, ap_, flags);
+      consumer_ = false;
       prof_end(0);
       prof_begin(1);
       // (A cooperative single-kernel update + direction with a grid barrier
       // was measured slower on B200 than this pair at every config size.)
-      kl(k_pcg_update<Real>, dim3(vgu), dim3(MO_THREADS), red(0, vgu, MO_FIN_PCG_BETA, 0), n, colmask_, mdv, delta_, r_, p_, ap_, pre);
+      mo_red ru = red(0, vgu, cons ? MO_FIN_PARTIALS : MO_FIN_PCG_BETA, 0);
+      if (cons) ru.partials = partials2_;
+      const double* pap_part = cons ? partials_ : nullptr;
+      kl(k_pcg_update<Real>, dim3(vgu), dim3(MO_THREADS), ru, n, colmask_, mdv, delta_, r_, p_, ap_, pre, pap_part,
+         apply_parts_, k);
       ++launches_;
-      reduce_done(MO_FIN_PCG_BETA, 0);
+      if (!cons) reduce_done(MO_FIN_PCG_BETA, 0);
+      const double* rz_part = cons ? partials2_ : nullptr;
       if (k + 1 < cfg_.linear_iters) {  // the last direction is never applied
-        kl(k_pcg_p<Real>, dim3(vgu), dim3(MO_THREADS), state_, n, colmask_, mdv, r_, p_, pre);
+        kl(k_pcg_p<Real>, dim3(vgu), dim3(MO_THREADS), state_, n, colmask_, mdv, r_, p_, pre, rz_part, vgu, k);
         ++launches_;
         exchange_cols(p_);
+      } else if (cons) {  // bookkeeping of the last r'z
+        kl(k_pcg_fin<Real>, dim3(1), dim3(MO_THREADS), state_, rz_part, vgu, k);
+        ++launches_;
       }
       prof_end(1);
     }
@@ -1800,6 +1819,9 @@ class Session final : public SessionBase {
   mo_state* state_ = nullptr;
   mo_state* state_h_ = nullptr;
   double* partials_ = nullptr;
+  double* partials2_ = nullptr;   // r'z block partials (consumer-side reductions)
+  bool consumer_ = false;         // PCG applies store p'Ap block partials only
+  int apply_parts_ = 0;           // block partials of the last captured apply
   std::vector<GraphData> graphs_;
   std::vector<GSet> gsets_;
   std::vector<long long*> grid_rowbase_;
