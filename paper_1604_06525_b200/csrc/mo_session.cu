@@ -1420,11 +1420,12 @@ class Session final : public SessionBase {
     const void* f = mod_.kernel("mo_graph_vjtjf_0");
     const int grid = int(std::max<long long>(
         1, std::min<long long>((gd.nverts + MO_THREADS - 1) / MO_THREADS, (long long)nsm_ * occupancy(f))));
-    kp.red = red(0, grid, MO_FIN_PCG_ALPHA, 0);
+    kp.red = red(0, grid, consumer_ ? MO_FIN_PARTIALS : MO_FIN_PCG_ALPHA, 0);
+    apply_parts_ = grid;
     void* args[] = {&kp};
     klc(f, dim3(grid), dim3(MO_THREADS), args, 0);
     ++launches_;
-    if (flags & MO_F_REDUCE) reduce_done(MO_FIN_PCG_ALPHA, 0);
+    if ((flags & MO_F_REDUCE) && !consumer_) reduce_done(MO_FIN_PCG_ALPHA, 0);
   }
 
   // Vertex-centric recompute kernels (generated per scatter-target domain).
@@ -1681,7 +1682,7 @@ class Session final : public SessionBase {
     // block (same fixed order, bitwise the same total) and derives alpha /
     // beta itself, removing the atomic + last-block tail from the producers.
     static const bool nocons = std::getenv("MO_B200_NO_CONSUMER") != nullptr;
-    const bool cons = !nocons && !sh_.on && P_.graph_sets.empty();
+    const bool cons = !nocons && !sh_.on && (P_.graph_sets.empty() || vertex_apply_one_pass());
     for (int k = 0; k < cfg_.linear_iters; ++k) {
       prof_begin(0);
       consumer_ = cons;
