@@ -59,8 +59,9 @@ enum { MO_F32 = 0, MO_F64 = 1 };                         /* plan.hpp:16 Precisio
 /* StopReason, solver.hpp:40-46 */
 enum { MO_STOP_ITER_LIMIT = 0, MO_STOP_COST_TOL = 1, MO_STOP_STALLED = 2, MO_STOP_NONFINITE = 3 };
 
-/* SolveConfig (plan.hpp:19-38).  materialize/exec/force_evalj have no device
- * meaning (the device path is matrix-free) and are omitted. */
+/* SolveConfig (plan.hpp:19-38).  exec/force_evalj have no device meaning and
+ * are omitted; `materialize` is fixed at plan time (a Materialize::kJ plan
+ * carries no matrix-free J^T J programs) and is reported by mo_plan_materialize. */
 typedef struct mo_solve_config {
   int method;
   int precision;
@@ -125,6 +126,9 @@ int mo_plan_precompile(mo_plan p, int precision);
  * per-element parity); default 0 lets nvcc contract a*b+c into FMA
  * (results within the fp32 1e-5 / fp64 1e-10 tolerances). */
 int mo_plan_set_exact(mo_plan p, int exact);
+/* Materialize (plan.hpp:17) the plan was compiled for: 0 kNone, 1 kJ, 2 kJtJ
+ * (kJtJ sessions are refused with MO_ERR_BIND). */
+int mo_plan_materialize(mo_plan p, int* mode);
 int mo_plan_counts(mo_plan p, int* n_params, int* n_arrays, int* n_graphs, int* n_unknowns);
 int mo_plan_array_size(mo_plan p, int i, int64_t* n_scalars);
 int mo_plan_graph_arity(mo_plan p, int i, int* arity);
@@ -161,6 +165,17 @@ int mo_apply_jtj_device(mo_session s, const void* v, void* out);
 int mo_solve(mo_session s, mo_iter_cb cb, void* user, mo_solve_result* out); /* :389 */
 int mo_get_x(mo_session s, void* out, int64_t n);
 int mo_saw_nonfinite(mo_session s, int* out);               /* :110 */
+/* linearize (solver.hpp:291-377): evaluate the Jacobian lanes at x on the
+ * device (plans with Jacobian lanes: materialized or force_evalj).  In
+ * Materialize::kJ sessions mo_apply_jtj then computes 2 J^T (J v) in the
+ * reference's spmv / spmv_t order (solver.hpp:278-283); before the first
+ * linearize after a refresh it fails with MO_ERR_INTERNAL like the reference. */
+int mo_linearize(mo_session s);
+/* jacobian() (solver.hpp:378-381): the reference's CSR (rows template-major,
+ * columns ascending, repeated edge vertices merged).  Call mo_jacobian_size,
+ * then mo_get_jacobian with offs[rows + 1], col[nnz], val[nnz] (Real). */
+int mo_jacobian_size(mo_session s, int64_t* rows, int64_t* cols, int64_t* nnz);
+int mo_get_jacobian(mo_session s, int64_t* offs, int64_t* col, void* val, int64_t nnz);
 
 /* ---- strip sharding (multi-GPU; no reference counterpart) --
  * A grid plan (one grid domain, no graphs) is split into contiguous strips

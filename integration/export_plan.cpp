@@ -2,7 +2,8 @@
 // the moplan v1 interchange the B200 library executes.
 //
 //   export_plan --energy F.opt [--dim W=16 ...] [--prec f32|f64] [--method gn|lm]
-//               [--nl N] [--lin N] [--rel T] [--out plan.moplan]
+//               [--nl N] [--lin N] [--rel T] [--materialize none|j|jtj]
+//               [--out plan.moplan]
 //
 // Plan-time only (the reference's parse/lower/transform/schedule pipeline is
 // out of scope for the device path); built by
@@ -40,6 +41,10 @@ int main(int argc, char** argv) {
     else if (k == "--nl") cfg.nonlinear_iters = std::atoi(next().c_str());
     else if (k == "--lin") cfg.linear_iters = std::atoi(next().c_str());
     else if (k == "--rel") cfg.pcg_rel_tol = std::atof(next().c_str());
+    else if (k == "--materialize") {
+      std::string m = next();
+      cfg.materialize = m == "j" ? Materialize::kJ : m == "jtj" ? Materialize::kJtJ : Materialize::kNone;
+    } else if (k == "--force-evalj") cfg.force_evalj = true;
     else {
       std::fprintf(stderr, "unknown option %s\n", k.c_str());
       return 2;

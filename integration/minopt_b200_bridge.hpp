@@ -15,6 +15,7 @@
 //   moplan 1
 //   cfg <method> <precision> <nl> <lin> <rel> <abs> <precond> <r0> <rmin> <rmax>
 //       <dmin> <dmax> <eta> <cost_stop>
+//   [materialize M]   (1 = Materialize::kJ, 2 = kJtJ; absent = matrix-free)
 //   dims N            / dim NAME EXTENT
 //   params N          / param NAME
 //   unknowns N        / unknown NAME CH ND dims...
@@ -28,6 +29,7 @@
 //                          + program evalj]   (plans built with force_evalj)
 //   gather_sets N     / gather_set ND dims... NCH (f c)...   + programs bm, jtj
 //   graph_sets N      / graph_set G NT t... NS (slot f c)... + cost, evalf, bm, jtj
+//                       [+ gevalj NT / gjtemplate T NL (out f c slot)... + program evalj]
 //   computed_kernels N/ computed_kernel IDX ND dims...   + program prog
 //   exclude_kernels N / exclude_kernel ND dims...        + program prog
 //   end
@@ -79,12 +81,11 @@ inline void put_program(std::ostream& os, const char* name, const KernelProgram&
 
 }  // namespace bridge_detail
 
-// Serialise a matrix-free CompiledPlan.  Throws Err::kBindError for plans
-// compiled for the materialized modes (out of scope for the device path).
+// Serialise a CompiledPlan.  Materialized plans (Materialize::kJ / kJtJ,
+// plan.hpp:17) carry no gather J^T J programs (plan.hpp:210, 289, 331); the
+// device then applies its J (or H = 2 J^T J) assembled from the evalj lanes.
 inline std::string export_plan_text(const CompiledPlan& P) {
   using namespace bridge_detail;
-  check(P.cfg.materialize == Materialize::kNone, Err::kBindError,
-        "the B200 path executes matrix-free plans only");
   const ProblemSpec& s = P.spec;
   const SolveConfig& c = P.cfg;
   std::ostringstream os;
@@ -95,6 +96,7 @@ inline std::string export_plan_text(const CompiledPlan& P) {
      << ' ' << hexf(c.lm_radius_max) << ' ' << hexf(c.lm_diag_min) << ' '
      << hexf(c.lm_diag_max) << ' ' << hexf(c.lm_min_decrease) << ' ' << hexf(c.cost_stop_tol)
      << '\n';
+  if (c.materialize != Materialize::kNone) os << "materialize " << int(c.materialize) << '\n';
   os << "dims " << s.dims.size() << '\n';
   for (const DimDecl& d : s.dims) os << "dim " << d.name << ' ' << d.extent << '\n';
   os << "params " << s.params.size() << '\n';
@@ -182,6 +184,16 @@ inline std::string export_plan_text(const CompiledPlan& P) {
     put_program(os, "evalf", g.evalf);
     put_program(os, "bm", g.bm);
     put_program(os, "jtj", g.jtj);
+    if (P.has_evalj) {
+      // Per-template Jacobian lanes of the edge rows (plan.hpp:318-330).
+      os << "gevalj " << g.jtemplates.size() << '\n';
+      for (const auto& jt : g.jtemplates) {
+        os << "gjtemplate " << jt.tmpl << ' ' << jt.lanes.size();
+        for (const JLane& l : jt.lanes) os << ' ' << l.out << ' ' << l.field << ' ' << l.channel << ' ' << l.slot;
+        os << '\n';
+      }
+      put_program(os, "evalj", g.evalj);
+    }
   }
   os << "computed_kernels " << P.computed_kernels.size() << '\n';
   for (const ComputedKernels& ck : P.computed_kernels) {
@@ -215,6 +227,7 @@ inline std::string export_plan_text(const CompiledPlan& P) {
 
 #include "mo_b200.h"
 #include "minopt/solver.hpp"
+#include "minopt/sparse.hpp"
 
 namespace minopt::b200 {
 
@@ -297,6 +310,21 @@ class Solver {
     ok(mo_saw_nonfinite(s_, &v));
     return v != 0;
   }
+  // linearize() / jacobian() (solver.hpp:291-382): lanes evaluated on the
+  // device, the CSR assembled exactly as the reference assembles it.
+  void linearize() {
+    ok(mo_linearize(s_));
+    J_ = SparseCSR<Real>{};
+    int64_t rows = 0, cols = 0, nnz = 0;
+    ok(mo_jacobian_size(s_, &rows, &cols, &nnz));
+    J_.rows = rows;
+    J_.cols = cols;
+    J_.offs.resize(size_t(rows) + 1);
+    J_.col.resize(size_t(nnz));
+    J_.val.resize(size_t(nnz));
+    ok(mo_get_jacobian(s_, J_.offs.data(), J_.col.data(), J_.val.data(), nnz));
+  }
+  const SparseCSR<Real>& jacobian() const { return J_; }
 
   SolveResult solve(const std::function<void(int, SolveData<Real>&)>& callback = {}) {
     cb_ = &callback;
@@ -342,6 +370,7 @@ class Solver {
   mo_session s_ = nullptr;
   std::vector<Real> b_, m_;
   std::vector<uint8_t> excl_;
+  SparseCSR<Real> J_;
   const std::function<void(int, SolveData<Real>&)>* cb_ = nullptr;
 };
 

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <random>
 #include <vector>
 
 #define MINOPT_B200_WITH_SOLVER
@@ -62,6 +63,99 @@ static void two_pixel_values() {
   std::vector<double> v{1.0, 0.0}, out(2);
   s.apply_jtj(v, out);
   CHECK(out[0] == 4.0 && out[1] == -2.0);
+}
+
+// test_solver.cpp:39-77 (materialized part: force_evalj, linearize, jacobian)
+static void two_pixel_jacobian() {
+  SolveConfig cfg;
+  cfg.force_evalj = true;
+  CompiledPlan p = plan(compile_source(kChain), cfg);
+  SolveData<double> data = chain_data<double>({0.0, 0.0}, {1.0, 0.0});
+  Solver<double> s(p, data);
+  s.build_normal();
+  std::vector<double> v{1.0, 0.0}, out(2);
+  s.apply_jtj(v, out);
+  CHECK(out[0] == 4.0 && out[1] == -2.0);
+  s.linearize();
+  const SparseCSR<double>& j = s.jacobian();
+  CHECK(j.rows == 4);
+  CHECK(j.cols == 2);
+  CHECK((j.offs == std::vector<int64_t>{0, 1, 2, 4, 4}));
+  CHECK((j.col == std::vector<int64_t>{0, 1, 0, 1}));
+  CHECK((j.val == std::vector<double>{1.0, 1.0, 1.0, -1.0}));
+}
+
+// test_solver.cpp:103-153 (kJtJ is refused by the device path; kJ and the
+// matrix-free apply must agree, and deliver the same iterates)
+static void materialized_agrees() {
+  const char* src = R"(
+dim W 9
+unknown X [W]
+array A [W]
+energy sin(X(0)) - A(0)
+energy 0.5 * (X(0) - X(1))
+)";
+  std::mt19937 rng(41);
+  std::uniform_real_distribution<double> u(-1.0, 1.0);
+  std::vector<double> x0(9), a0(9);
+  for (auto& v : x0) v = u(rng);
+  for (auto& v : a0) v = u(rng);
+  auto make = [&](Materialize mode) {
+    SolveConfig cfg;
+    cfg.materialize = mode;
+    return plan(compile_source(src), cfg);
+  };
+  CompiledPlan pn = make(Materialize::kNone), pj = make(Materialize::kJ);
+  SolveData<double> dn = chain_data<double>(x0, a0), dj = chain_data<double>(x0, a0);
+  Solver<double> sn(pn, dn), sj(pj, dj);
+  bool threw = false;
+  std::vector<double> probe(9, 1.0), pout(9);
+  try {
+    sj.apply_jtj(probe, pout);  // solver.hpp:278: apply before linearize()
+  } catch (const Error&) {
+    threw = true;
+  }
+  CHECK(threw);
+  sj.linearize();
+  for (int trial = 0; trial < 10; ++trial) {
+    std::vector<double> v(9), on(9), oj(9);
+    for (auto& e : v) e = u(rng);
+    sn.apply_jtj(v, on);
+    sj.apply_jtj(v, oj);
+    for (int i = 0; i < 9; ++i) CHECK(std::fabs(oj[i] - on[i]) <= 1e-12);
+  }
+  SolveResult rn = sn.solve(), rj = sj.solve();
+  CHECK(approx(rn.final_cost, rj.final_cost, 1e-10));
+  for (int i = 0; i < 9; ++i) CHECK(std::fabs(dj.x[i] - dn.x[i]) <= 1e-8);
+  bool refused = false;
+  try {
+    CompiledPlan ph = make(Materialize::kJtJ);
+    SolveData<double> dh = chain_data<double>(x0, a0);
+    Solver<double> sh(ph, dh);
+  } catch (const Error& e) {
+    refused = e.code() == Err::kBindError;
+  }
+  CHECK(refused);
+}
+
+// test_solver.cpp:186-204
+static void degenerate_hyperedge() {
+  SolveConfig cfg;
+  cfg.materialize = Materialize::kJ;
+  CompiledPlan p = plan(compile_source("dim N 2\nunknown P [N]\ngraph G (a, b)\nenergy P(G.a) - P(G.b)"), cfg);
+  SolveData<double> data;
+  data.x = {5.0, 7.0};
+  data.graphs = {EdgeTable{2, {0, 0}}};
+  Solver<double> s(p, data);
+  s.linearize();
+  const SparseCSR<double>& j = s.jacobian();
+  CHECK(j.rows == 1);
+  CHECK((j.offs == std::vector<int64_t>{0, 1}));
+  CHECK((j.col == std::vector<int64_t>{0}));
+  CHECK(j.val.size() == 1 && j.val[0] == 0.0);
+  std::vector<double> v{1.0, 2.0}, out(2, 9.0);
+  s.apply_jtj(v, out);  // J = [0 0]: 2 J^T J v = 0
+  CHECK(out[0] == 0.0 && out[1] == 0.0);
 }
 
 // test_solver.cpp:79-101
@@ -261,6 +355,9 @@ static void no_energies() {
 int main() {
   using namespace dropin;
   two_pixel_values();
+  two_pixel_jacobian();
+  materialized_agrees();
+  degenerate_hyperedge();
   one_gn_step();
   graph_scatter();
   frozen_unknowns();

@@ -146,3 +146,15 @@ class Oracle:
         out = np.zeros(self.num_cols(), self.dtype)
         self._chk(self.lib.moo_get_x(self.h, out.ctypes.data_as(ctypes.c_void_p)))
         return out
+
+    def linearize(self):
+        """linearize() (solver.hpp:291-376); returns the CSR (offs, col, val)."""
+        self._chk(self.lib.moo_linearize(self.h))
+        rows, nnz = ctypes.c_int64(), ctypes.c_int64()
+        self._chk(self.lib.moo_jacobian(self.h, ctypes.byref(rows), ctypes.byref(nnz), None, None, None))
+        offs = np.zeros(rows.value + 1, np.int64)
+        col = np.zeros(nnz.value, np.int64)
+        val = np.zeros(nnz.value, self.dtype)
+        ptr = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+        self._chk(self.lib.moo_jacobian(self.h, ctypes.byref(rows), ctypes.byref(nnz), ptr(offs), ptr(col), ptr(val)))
+        return offs, col, val

@@ -50,11 +50,21 @@ typedef struct {
   Dom dom;
   int graph_idx;
 } Res;
+/* One template's Jacobian lanes (plan.hpp:47-72): grid lanes carry stencil
+ * offsets, graph lanes edge slots. */
+typedef struct {
+  int tmpl, guard, nl;
+  int *out, *f, *c, *slot;
+  int (*off)[3];
+} JTmpl;
 typedef struct {
   Dom dom;
   int nt;
   int tmpl[MOO_MAXT];
   Prog cost, evalf;
+  int njt;
+  JTmpl* jt;
+  Prog evalj;
 } GridSetO;
 typedef struct {
   Dom dom;
@@ -67,6 +77,9 @@ typedef struct {
   int tmpl[MOO_MAXT];
   int sslot[MOO_MAXOUT], sfield[MOO_MAXOUT], sch[MOO_MAXOUT];
   Prog cost, evalf, bm, jtj;
+  int njt;
+  JTmpl* jt;
+  Prog evalj;
 } GraphSetO;
 typedef struct {
   int index;
@@ -111,6 +124,13 @@ struct moo {
   int64_t rows, unconstrained;
   int nonfinite_seen;
   void* st;
+  /* materialized J (solver.hpp:278-376): 0 kNone, 1 kJ, 2 kJtJ */
+  int materialize, jvalid;
+  int64_t rows_seen;
+  int64_t* joffs; /* CSR of J: rows + 1 */
+  int64_t* jcol;
+  void* jval;
+  int64_t jnnz, jcap;
 };
 
 static char g_err[512];
@@ -189,7 +209,8 @@ static Prog getprog(Lex* L, const char* name, uint32_t* maxr) {
   p.nb = (int)geti(L);
   p.ng = (int)geti(L);
   p.no = (int)geti(L);
-  if (L->bad || p.ni < 0 || p.nb < 0 || p.ng < 1 || p.no < 0 || p.no > MOO_MAXOUT) {
+  if (L->bad || p.ni < 0 || p.nb < 0 || p.no < 0 || p.no > MOO_MAXOUT ||
+      (p.ng < 1 && (p.ni || p.nb || p.no))) { /* empty = not compiled by the plan */
     L->bad = 1;
     return p;
   }
@@ -221,7 +242,7 @@ static Prog getprog(Lex* L, const char* name, uint32_t* maxr) {
     p.blk[i].begin = (uint32_t)geti(L);
     p.blk[i].end = (uint32_t)geti(L);
   }
-  p.greg = (uint16_t*)calloc((size_t)p.ng, sizeof(uint16_t));
+  p.greg = (uint16_t*)calloc((size_t)(p.ng > 0 ? p.ng : 1), sizeof(uint16_t));
   for (int i = 0; i < p.ng; ++i) {
     expect(L, "g");
     p.greg[i] = (uint16_t)geti(L);
@@ -301,6 +322,25 @@ static void relayout(moo* o) {
 #define ATANF atan
 #include "mo_oracle_impl.h"
 
+static void jt_alloc(JTmpl* t) {
+  size_t n = (size_t)t->nl + 1;
+  t->out = (int*)calloc(n, sizeof(int));
+  t->f = (int*)calloc(n, sizeof(int));
+  t->c = (int*)calloc(n, sizeof(int));
+  t->slot = (int*)calloc(n, sizeof(int));
+  t->off = (int(*)[3])calloc(n, sizeof(int[3]));
+}
+static void jt_free(JTmpl* t, int n) {
+  for (int k = 0; t && k < n; ++k) {
+    free(t[k].out);
+    free(t[k].f);
+    free(t[k].c);
+    free(t[k].slot);
+    free(t[k].off);
+  }
+  free(t);
+}
+
 /* ------------------------------------------------------------ API */
 int moo_create(const char* text, size_t len, int f64, moo** out) {
   moo* o = (moo*)calloc(1, sizeof(moo));
@@ -324,6 +364,12 @@ int moo_create(const char* text, size_t len, int f64, moo** out) {
   o->cfg.lm_diag_max = getd(&L);
   o->cfg.lm_min_decrease = getd(&L);
   o->cfg.cost_stop_tol = getd(&L);
+  {
+    const char* save = L.p;
+    tok(&L, w, sizeof w);
+    if (strcmp(w, "materialize") == 0) o->materialize = (int)geti(&L);
+    else L.p = save;
+  }
   expect(&L, "dims");
   o->ndims = (int)geti(&L);
   for (int i = 0; i < o->ndims && i < 16; ++i) {
@@ -397,24 +443,32 @@ int moo_create(const char* text, size_t len, int f64, moo** out) {
     for (int t = 0; t < o->gs[i].nt; ++t) o->gs[i].tmpl[t] = (int)geti(&L);
     o->gs[i].cost = getprog(&L, "cost", &o->max_regs);
     o->gs[i].evalf = getprog(&L, "evalf", &o->max_regs);
-    /* optional Jacobian-lane section (force_evalj plans): not used here */
+    /* optional Jacobian-lane section (force_evalj / materialized plans) */
     const char* save = L.p;
     tok(&L, w, sizeof w);
     if (strcmp(w, "evalj") == 0) {
-      int njt = (int)geti(&L);
-      for (int k = 0; k < njt; ++k) {
+      GridSetO* g = &o->gs[i];
+      g->njt = (int)geti(&L);
+      g->jt = (JTmpl*)calloc((size_t)g->njt + 1, sizeof(JTmpl));
+      for (int k = 0; k < g->njt; ++k) {
         expect(&L, "jtemplate");
-        (void)geti(&L);
-        (void)geti(&L);
-        (void)geti(&L);
-        int nl = (int)geti(&L);
-        for (int q = 0; q < 6 * nl; ++q) (void)geti(&L);
+        JTmpl* t = &g->jt[k];
+        t->tmpl = (int)geti(&L);
+        t->guard = (int)geti(&L);
+        (void)geti(&L); /* origin flag: device-side only */
+        t->nl = (int)geti(&L);
+        jt_alloc(t);
+        for (int q = 0; q < t->nl; ++q) {
+          t->out[q] = (int)geti(&L);
+          t->f[q] = (int)geti(&L);
+          t->c[q] = (int)geti(&L);
+          for (int a = 0; a < 3; ++a) t->off[q][a] = (int)geti(&L);
+          t->slot[q] = -1;
+        }
       }
-      Prog ej = getprog(&L, "evalj", &o->max_regs);
-      freeprog(&ej);
+      g->evalj = getprog(&L, "evalj", &o->max_regs);
     } else {
       L.p = save;
-      L.bad = 0 || L.bad;
     }
   }
   expect(&L, "gather_sets");
@@ -449,6 +503,30 @@ int moo_create(const char* text, size_t len, int f64, moo** out) {
     o->hs[i].evalf = getprog(&L, "evalf", &o->max_regs);
     o->hs[i].bm = getprog(&L, "bm", &o->max_regs);
     o->hs[i].jtj = getprog(&L, "jtj", &o->max_regs);
+    const char* save = L.p;
+    tok(&L, w, sizeof w);
+    if (strcmp(w, "gevalj") == 0) {
+      GraphSetO* g = &o->hs[i];
+      g->njt = (int)geti(&L);
+      g->jt = (JTmpl*)calloc((size_t)g->njt + 1, sizeof(JTmpl));
+      for (int k = 0; k < g->njt; ++k) {
+        expect(&L, "gjtemplate");
+        JTmpl* t = &g->jt[k];
+        t->tmpl = (int)geti(&L);
+        t->guard = -1;
+        t->nl = (int)geti(&L);
+        jt_alloc(t);
+        for (int q = 0; q < t->nl; ++q) {
+          t->out[q] = (int)geti(&L);
+          t->f[q] = (int)geti(&L);
+          t->c[q] = (int)geti(&L);
+          t->slot[q] = (int)geti(&L);
+        }
+      }
+      g->evalj = getprog(&L, "evalj", &o->max_regs);
+    } else {
+      L.p = save;
+    }
   }
   expect(&L, "computed_kernels");
   o->nck = (int)geti(&L);
@@ -504,6 +582,17 @@ void moo_destroy(moo* o) {
     freeprog(&o->hs[i].bm);
     freeprog(&o->hs[i].jtj);
   }
+  for (int i = 0; i < o->ngs; ++i) {
+    jt_free(o->gs[i].jt, o->gs[i].njt);
+    if (o->gs[i].njt) freeprog(&o->gs[i].evalj);
+  }
+  for (int i = 0; i < o->nhs; ++i) {
+    jt_free(o->hs[i].jt, o->hs[i].njt);
+    if (o->hs[i].njt) freeprog(&o->hs[i].evalj);
+  }
+  free(o->joffs);
+  free(o->jcol);
+  free(o->jval);
   for (int i = 0; i < o->nck; ++i) freeprog(&o->ck[i].prog);
   for (int i = 0; i < o->nek; ++i) freeprog(&o->ek[i].prog);
   free(o->gs);
@@ -661,20 +750,32 @@ int moo_build_normal(moo* o, void* b, void* m) {
   return 0;
 }
 int moo_apply_jtj(moo* o, const void* v, void* out) {
-  if (o->f64) apply_jtj_d(o, (const double*)v, (double*)out);
-  else apply_jtj_f(o, (const float*)v, (float*)out);
-  return 0;
+  return o->f64 ? apply_jtj_d(o, (const double*)v, (double*)out) : apply_jtj_f(o, (const float*)v, (float*)out);
 }
 int moo_solve(moo* o, moo_result* r, int* ti, double* tc, int* ta, double* tr, int* tp) {
   int rc = validate(o);
   if (rc) return rc;
   if (o->f64) {
     ensure_elemcost_d(o);
-    solve_d(o, r, ti, tc, ta, tr, tp);
+    rc = solve_d(o, r, ti, tc, ta, tr, tp);
   } else {
     ensure_elemcost_f(o);
-    solve_f(o, r, ti, tc, ta, tr, tp);
+    rc = solve_f(o, r, ti, tc, ta, tr, tp);
   }
+  return rc;
+}
+int moo_linearize(moo* o) {
+  int rc = validate(o);
+  if (rc) return rc;
+  return o->f64 ? linearize_d(o) : linearize_f(o);
+}
+int moo_jacobian(moo* o, int64_t* rows, int64_t* nnz, int64_t* offs, int64_t* col, void* val) {
+  if (!o->jvalid) return err(E_BIND, "no Jacobian has been materialized");
+  *rows = o->rows;
+  *nnz = o->jnnz;
+  if (offs) memcpy(offs, o->joffs, (size_t)(o->rows + 1) * sizeof(int64_t));
+  if (col) memcpy(col, o->jcol, (size_t)o->jnnz * sizeof(int64_t));
+  if (val) memcpy(val, o->jval, (size_t)o->jnnz * RSZ(o));
   return 0;
 }
 int moo_get_x(moo* o, void* out) {

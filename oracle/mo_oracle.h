@@ -7,7 +7,8 @@
  *   EvalEnv      eval.hpp:41-61         exec_graph exec.hpp:223-309 (sequential order)
  *   pow_eval     common.hpp:102-124     pcg        pcg.hpp:63-130
  *   Solver       solver.hpp:125-515 (refresh, cost, residuals, build_normal,
- *                apply_jtj, solve GN/LM; no callbacks)
+ *                apply_jtj, linearize + Materialize::kJ, solve GN/LM; no callbacks)
+ *   SparseCSR    sparse.hpp (push checks, spmv, spmv_t)
  * Real is float or double per instance, like Solver<float>/Solver<double>.
  * Pinned against the unmodified reference's golden outputs by
  * tests/test_oracle_cpu.py.
@@ -53,5 +54,9 @@ int moo_apply_jtj(moo* o, const void* v, void* out);
 /* trace arrays sized >= 4096 rows by the caller */
 int moo_solve(moo* o, moo_result* r, int* t_iter, double* t_cost, int* t_acc, double* t_radius, int* t_pcg);
 int moo_get_x(moo* o, void* out);
+/* linearize (solver.hpp:291-376) / jacobian() CSR; Materialize::kJ plans then
+ * apply 2 J^T (J v) through spmv / spmv_t (sparse.hpp). */
+int moo_linearize(moo* o);
+int moo_jacobian(moo* o, int64_t* rows, int64_t* nnz, int64_t* offs, int64_t* col, void* val);
 
 #endif

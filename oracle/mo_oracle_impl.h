@@ -147,6 +147,8 @@ typedef struct {
   REAL* regs;
   REAL* outs;
   REAL* elemcost;
+  REAL* jtmp; /* materialized apply: J v (solver.hpp:280) */
+  int64_t jtmp_cap;
 } F(State);
 
 static void F(coord_of)(const int64_t* shape, int nd, int64_t e, int64_t* c) {
@@ -239,6 +241,7 @@ static void F(refresh)(moo* o) {
   F(State)* S = (F(State)*)o->st;
   F(Env) e;
   F(Out) outs[MOO_MAXOUT];
+  o->jvalid = 0; /* solver.hpp:167 */
   for (int i = 0; i < o->nck; ++i) {
     const CompK* ck = &o->ck[i];
     int tc = o->cmp[ck->index].ch;
@@ -350,11 +353,150 @@ static void F(build_normal)(moo* o) {
   }
 }
 
-/* apply_jtj, matrix-free branch (solver.hpp:255-277) */
-static void F(apply_jtj)(moo* o, const REAL* v, REAL* out) {
+/* linearize (solver.hpp:291-376): evalj lanes per template set, then the
+ * CSR of J with the SparseCSR push checks (sparse.hpp:30-37). */
+static int F(jpush)(moo* o, int64_t c, REAL v) {
+  if (c < 0 || c >= o->num_cols) return err(E_INDEX, "CSR column out of range");
+  int64_t r = o->rows_seen;
+  if (!(o->jnnz == o->joffs[r - 1] || o->jcol[o->jnnz - 1] < c))
+    return err(E_INTERNAL, "CSR row entries must arrive in increasing column order");
+  if (o->jnnz == o->jcap) {
+    o->jcap = o->jcap ? 2 * o->jcap : 1024;
+    o->jcol = (int64_t*)realloc(o->jcol, (size_t)o->jcap * sizeof(int64_t));
+    o->jval = realloc(o->jval, (size_t)o->jcap * sizeof(REAL));
+  }
+  o->jcol[o->jnnz] = c;
+  ((REAL*)o->jval)[o->jnnz] = v;
+  ++o->jnnz;
+  o->joffs[r] = o->jnnz;
+  return 0;
+}
+static int F(linearize)(moo* o) {
   F(State)* S = (F(State)*)o->st;
   F(Env) e;
   F(Out) outs[MOO_MAXOUT];
+  REAL* lg[MOO_MAXT] = {0};
+  REAL* lh[MOO_MAXT] = {0};
+  int rc = 0;
+  for (int i = 0; i < o->ngs; ++i) {
+    const GridSetO* g = &o->gs[i];
+    if (!g->njt) continue;
+    int64_t ext = dom_extent(o, &g->dom);
+    lg[i] = (REAL*)calloc((size_t)(g->evalj.no * ext) + 1, sizeof(REAL));
+    for (int l = 0; l < g->evalj.no; ++l) outs[l] = (F(Out)){lg[i], (int64_t)l * ext, 1, ext, -1};
+    F(env)(o, S->x, NULL, &g->dom, &e);
+    F(exec_grid)(o, &g->evalj, &e, outs, NULL);
+  }
+  for (int i = 0; i < o->nhs; ++i) {
+    const GraphSetO* g = &o->hs[i];
+    if (!g->njt) continue;
+    int64_t E = o->graphs[g->graph].E;
+    lh[i] = (REAL*)calloc((size_t)(g->evalj.no * E) + 1, sizeof(REAL));
+    for (int l = 0; l < g->evalj.no; ++l) outs[l] = (F(Out)){lh[i], (int64_t)l * E, 1, E, -1};
+    F(env)(o, S->x, NULL, NULL, &e);
+    F(exec_graph)(o, &g->evalj, &e, g->graph, outs);
+  }
+  free(o->joffs);
+  o->joffs = (int64_t*)calloc((size_t)o->rows + 1, sizeof(int64_t));
+  o->jnnz = 0;
+  o->rows_seen = 0;
+  for (int t = 0; t < o->nres && !rc; ++t) {
+    int found = 0;
+    for (int i = 0; i < o->ngs && !found; ++i) {
+      const GridSetO* g = &o->gs[i];
+      for (int k = 0; k < g->njt && !found; ++k) {
+        const JTmpl* jt = &g->jt[k];
+        if (jt->tmpl != t) continue;
+        found = 1;
+        int64_t sh[3], ext = dom_extent(o, &g->dom);
+        dom_shape(o, &g->dom, sh);
+        for (int64_t el = 0; el < ext && !rc; ++el) {
+          o->joffs[++o->rows_seen] = o->jnnz; /* begin_row */
+          if (lg[i][(int64_t)jt->guard * ext + el] == (REAL)0) continue;
+          for (int q = 0; q < jt->nl && !rc; ++q) {
+            int64_t lin = ((int64_t)jt->off[q][0] * sh[1] + jt->off[q][1]) * sh[2] + jt->off[q][2];
+            rc = F(jpush)(o, o->ubase[jt->f[q]] + (el + lin) * o->unk[jt->f[q]].ch + jt->c[q],
+                          lg[i][(int64_t)jt->out[q] * ext + el]);
+          }
+        }
+      }
+    }
+    for (int i = 0; i < o->nhs && !found; ++i) {
+      const GraphSetO* g = &o->hs[i];
+      for (int k = 0; k < g->njt && !found; ++k) {
+        const JTmpl* jt = &g->jt[k];
+        if (jt->tmpl != t) continue;
+        found = 1;
+        const Graph* G = &o->graphs[g->graph];
+        int64_t cols[MOO_MAXOUT];
+        REAL vals[MOO_MAXOUT];
+        for (int64_t ed = 0; ed < G->E && !rc; ++ed) {
+          o->joffs[++o->rows_seen] = o->jnnz;
+          int n = 0;
+          for (int q = 0; q < jt->nl; ++q) { /* stable insertion sort by column */
+            int64_t c = o->ubase[jt->f[q]] + (int64_t)G->verts[ed * G->arity + jt->slot[q]] * o->unk[jt->f[q]].ch +
+                        jt->c[q];
+            REAL v = lh[i][(int64_t)jt->out[q] * G->E + ed];
+            int j = n++;
+            while (j > 0 && cols[j - 1] > c) {
+              cols[j] = cols[j - 1];
+              vals[j] = vals[j - 1];
+              --j;
+            }
+            cols[j] = c;
+            vals[j] = v;
+          }
+          for (int q = 0; q < n && !rc;) { /* degenerate edges: merge columns */
+            int64_t c = cols[q];
+            REAL v = vals[q];
+            for (++q; q < n && cols[q] == c; ++q) v += vals[q];
+            rc = F(jpush)(o, c, v);
+          }
+        }
+      }
+    }
+    if (!found) rc = err(E_BIND, "plan was compiled without Jacobian kernels");
+  }
+  for (int i = 0; i < MOO_MAXT; ++i) {
+    free(lg[i]);
+    free(lh[i]);
+  }
+  o->jvalid = rc == 0;
+  return rc;
+}
+
+/* spmv / spmv_t (sparse.hpp): y = J v row by row; y = J^T x by row-ordered scatter */
+static void F(apply_materialized)(moo* o, const REAL* v, REAL* out) {
+  F(State)* S = (F(State)*)o->st;
+  const REAL* val = (const REAL*)o->jval;
+  for (int64_t r = 0; r < o->rows; ++r) {
+    REAL acc = (REAL)0;
+    for (int64_t k = o->joffs[r]; k < o->joffs[r + 1]; ++k) acc += val[k] * v[o->jcol[k]];
+    S->jtmp[r] = acc;
+  }
+  for (int64_t i = 0; i < o->num_cols; ++i) out[i] = (REAL)0;
+  for (int64_t r = 0; r < o->rows; ++r) {
+    REAL xr = S->jtmp[r];
+    for (int64_t k = o->joffs[r]; k < o->joffs[r + 1]; ++k) out[o->jcol[k]] += val[k] * xr;
+  }
+  for (int64_t i = 0; i < o->num_cols; ++i) out[i] *= (REAL)2;
+}
+
+/* apply_jtj (solver.hpp:255-285): matrix-free, or the materialized J */
+static int F(apply_jtj)(moo* o, const REAL* v, REAL* out) {
+  F(State)* S = (F(State)*)o->st;
+  F(Env) e;
+  F(Out) outs[MOO_MAXOUT];
+  if (o->materialize) {
+    if (!o->jvalid) return err(E_INTERNAL, "normal-matrix apply before linearize()");
+    if (o->rows > S->jtmp_cap) {
+      free(S->jtmp);
+      S->jtmp = (REAL*)calloc((size_t)o->rows, sizeof(REAL));
+      S->jtmp_cap = o->rows;
+    }
+    F(apply_materialized)(o, v, out);
+    return 0;
+  }
   for (int i = 0; i < o->nqs; ++i) {
     const GatherSetO* g = &o->qs[i];
     F(env)(o, S->x, v, &g->dom, &e);
@@ -369,6 +511,7 @@ static void F(apply_jtj)(moo* o, const REAL* v, REAL* out) {
       outs[k] = (F(Out)){out, o->ubase[g->sfield[k]] + g->sch[k], o->unk[g->sfield[k]].ch, 0, g->sslot[k]};
     F(exec_graph)(o, &g->jtj, &e, g->graph, outs);
   }
+  return 0;
 }
 
 static REAL F(dot)(const REAL* a, const REAL* b, int64_t n) {
@@ -457,8 +600,8 @@ static void F(pcg)(moo* o, int lm, int* iters, int* indefinite, int* nonfinite) 
   } while (0)
 
 /* solve (solver.hpp:389-515), no callbacks */
-static void F(solve)(moo* o, moo_result* res, int* t_iter, double* t_cost, int* t_acc, double* t_radius,
-                     int* t_pcg) {
+static int F(solve)(moo* o, moo_result* res, int* t_iter, double* t_cost, int* t_acc, double* t_radius,
+                    int* t_pcg) {
   F(State)* S = (F(State)*)o->st;
   const moo_config* c = &o->cfg;
   const int lm = c->method == 1;
@@ -477,6 +620,10 @@ static void F(solve)(moo* o, moo_result* res, int* t_iter, double* t_cost, int* 
       goto done;
     }
     F(build_normal)(o);
+    if (o->materialize) { /* solver.hpp:426 */
+      int rc = F(linearize)(o);
+      if (rc) return rc;
+    }
     if (lm)
       for (int64_t i = 0; i < n; ++i) {
         double v = (double)S->m[i] / 2.0;
@@ -564,6 +711,7 @@ done:
   res->n_trace = nt;
   res->nonfinite_kernels = o->nonfinite_seen;
   res->unconstrained = o->unconstrained;
+  return 0;
 }
 
 static void F(alloc)(moo* o) {
@@ -591,6 +739,7 @@ static void F(free_state)(moo* o) {
   REAL* vecs[] = {S->x, S->b, S->m, S->md, S->damp, S->delta, S->xt, S->aptmp, S->r, S->z, S->p, S->ap, S->regs, S->outs, S->elemcost};
   for (size_t k = 0; k < sizeof vecs / sizeof vecs[0]; ++k) free(vecs[k]);
   free(S->base_diag);
+  free(S->jtmp);
   for (int a = 0; a < MOO_MAXF; ++a) {
     free(S->arrays[a]);
     free(S->comp[a]);

@@ -68,7 +68,7 @@ def energy_path(stem_or_path, tmpdir=None):
 
 def run_ref(energy, data, cmds, dims=None, prec="f64", method="gn", nl=None, lin=None, rel=None,
             abs_tol=None, precond=True, radius0=None, cost_stop=None, exec_mode="seq", repeat=1,
-            v=None, threads=None, timeout=3600):
+            v=None, threads=None, timeout=3600, materialize=None, force_evalj=False):
     """Run the reference solver; `data` is a SolveData-like object (x, arrays,
     params, graphs).  Returns the output record dict (see ref_driver.cpp)."""
     if not ref_available():
@@ -97,6 +97,10 @@ def run_ref(energy, data, cmds, dims=None, prec="f64", method="gn", nl=None, lin
                 cmd += [flag, repr(float(val)) if isinstance(val, float) else str(val)]
         if not precond:
             cmd.append("--noprecond")
+        if materialize:
+            cmd += ["--materialize", materialize]
+        if force_evalj:
+            cmd.append("--force-evalj")
         env = dict(os.environ)
         if threads:
             env["MINOPT_THREADS"] = str(threads)

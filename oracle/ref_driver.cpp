@@ -15,8 +15,9 @@
 //   ref_driver --energy F.opt [--dim W=16 ...] --in IN.mob --out OUT.mob
 //              [--prec f32|f64] [--method gn|lm] [--nl N] [--lin N] [--rel T]
 //              [--abs T] [--noprecond] [--radius0 R] [--cost-stop T]
-//              [--exec seq|par] [--repeat N] --do cmd[,cmd...]
-//   cmds: cost residuals normal jtj solve time routines
+//              [--exec seq|par] [--repeat N] [--materialize none|j|jtj]
+//              [--force-evalj] --do cmd[,cmd...]
+//   cmds: cost residuals normal linearize jtj solve time routines
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -100,6 +101,10 @@ Args parse_args(int argc, char** argv) {
     else if (k == "--nl") a.cfg.nonlinear_iters = std::atoi(next().c_str());
     else if (k == "--lin") a.cfg.linear_iters = std::atoi(next().c_str());
     else if (k == "--rel") a.cfg.pcg_rel_tol = std::atof(next().c_str());
+    else if (k == "--materialize") {
+      std::string m = next();
+      a.cfg.materialize = m == "j" ? Materialize::kJ : m == "jtj" ? Materialize::kJtJ : Materialize::kNone;
+    } else if (k == "--force-evalj") a.cfg.force_evalj = true;
     else if (k == "--abs") a.cfg.pcg_abs_tol = std::atof(next().c_str());
     else if (k == "--noprecond") a.cfg.use_preconditioner = false;
     else if (k == "--radius0") a.cfg.lm_radius0 = std::atof(next().c_str());
@@ -187,6 +192,12 @@ int run(const Args& a, const CompiledPlan& P) {
         s.build_normal();
         mob_put(&w, "b", RD, s.rhs().data(), s.rhs().size());
         mob_put(&w, "m", RD, s.precond().data(), s.precond().size());
+      } else if (c == "linearize") {  // solver.hpp:291-381
+        s.linearize();
+        const SparseCSR<Real>& j = s.jacobian();
+        mob_put(&w, "j_offs", MOB_I64, j.offs.data(), j.offs.size());
+        mob_put(&w, "j_col", MOB_I64, j.col.data(), j.col.size());
+        mob_put(&w, "j_val", RD, j.val.data(), j.val.size());
       } else if (c == "jtj") {
         std::vector<Real> v = get_real<Real>(in, "v");
         std::vector<Real> out(static_cast<size_t>(ncols));

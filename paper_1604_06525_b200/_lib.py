@@ -95,6 +95,10 @@ SIGNATURES = {
     "mo_session_stream": (c_int, [c_void_p, ctypes.POINTER(c_void_p)]),
     "mo_kernel_launches": (c_int, [c_void_p, ctypes.POINTER(c_int64)]),
     "mo_apply_kernel": (c_int, [c_void_p, c_int, ctypes.c_char_p, ctypes.c_size_t]),
+    "mo_plan_materialize": (c_int, [c_void_p, ctypes.POINTER(c_int)]),
+    "mo_linearize": (c_int, [c_void_p]),
+    "mo_jacobian_size": (c_int, [c_void_p] + [ctypes.POINTER(c_int64)] * 3),
+    "mo_get_jacobian": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64]),
 }
 
 for _name, (_res, _args) in SIGNATURES.items():

@@ -37,6 +37,7 @@ struct mo_session_s {
   std::vector<mo_iter_row> trace;
   mo_iter_cb cb = nullptr;
   void* user = nullptr;
+  bool f32 = false;
 };
 
 namespace {
@@ -177,6 +178,7 @@ int mo_plan_set_config(mo_plan p, const mo_solve_config* cfg) {
               "trust-region radius bounds must bracket the initial radius");
     mo::check(k.lm_diag_min <= k.lm_diag_max && k.lm_diag_min >= 0, mo::Err::kBindError,
               "damping diagonal clamp must be an interval");
+    k.materialize = p->plan.cfg.materialize;  // fixed at plan time
     p->plan.cfg = k;
   });
 }
@@ -195,6 +197,13 @@ int mo_plan_set_exact(mo_plan p, int exact) {
   });
 }
 
+int mo_plan_materialize(mo_plan p, int* mode) {
+  return guard([&] {
+    need(p, "plan");
+    need(mode, "output");
+    *mode = p->plan.cfg.materialize;
+  });
+}
 int mo_plan_num_cols(mo_plan p, int64_t* n) {
   return guard([&] {
     need(p, "plan");
@@ -239,16 +248,17 @@ int mo_session_create(mo_plan p, int device, mo_session* out) {
     need(out, "output");
     auto s = std::make_unique<mo_session_s>();
     s->impl = mo::make_session(p->plan, device);
+    s->f32 = p->plan.cfg.precision == 0;
     *out = s.release();
   });
 }
 
 void mo_session_destroy(mo_session s) { delete s; }
 
-#define SESSION_CALL(body) \
-  return guard([&] {       \
-    need(s, "session");    \
-    body;                  \
+#define SESSION_CALL(...) \
+  return guard([&] {      \
+    need(s, "session");   \
+    __VA_ARGS__;          \
   })
 
 int mo_bind_x(mo_session s, const void* x, int64_t n) { SESSION_CALL(s->impl->bind_x(x, n, false)); }
@@ -354,6 +364,7 @@ int mo_session_create_shard(mo_plan p, int device, mo_comm c, int64_t row0, int6
     need(out, "output");
     auto s = std::make_unique<mo_session_s>();
     s->impl = mo::make_shard_session(p->plan, device, c->c.get(), row0, row1);
+    s->f32 = p->plan.cfg.precision == 0;
     *out = s.release();
   });
 }
@@ -370,6 +381,35 @@ int mo_profile_read(mo_session s, int kind, double* ms, int64_t* n) {
 int mo_profile_reset(mo_session s) { SESSION_CALL(s->impl->profile_reset()); }
 int mo_session_stream(mo_session s, void** st) { SESSION_CALL(need(st, "output"); *st = s->impl->stream()); }
 int mo_kernel_launches(mo_session s, int64_t* n) { SESSION_CALL(need(n, "output"); *n = s->impl->launches()); }
+int mo_linearize(mo_session s) { SESSION_CALL(s->impl->linearize()); }
+int mo_jacobian_size(mo_session s, int64_t* rows, int64_t* cols, int64_t* nnz) {
+  SESSION_CALL({
+    need(rows, "output");
+    need(cols, "output");
+    need(nnz, "output");
+    std::vector<int64_t> offs;
+    s->impl->jacobian(rows, cols, &offs, nullptr, nullptr);
+    *nnz = offs.empty() ? 0 : offs.back();
+  });
+}
+int mo_get_jacobian(mo_session s, int64_t* offs, int64_t* col, void* val, int64_t nnz) {
+  SESSION_CALL({
+    int64_t rows = 0, cols = 0;
+    std::vector<int64_t> o, c;
+    std::vector<double> v;
+    s->impl->jacobian(&rows, &cols, &o, &c, &v);
+    mo::check(nnz == int64_t(c.size()), mo::Err::kShapeMismatch, "jacobian(): nnz does not match mo_jacobian_size");
+    if (offs) std::memcpy(offs, o.data(), o.size() * sizeof(int64_t));
+    if (col && !c.empty()) std::memcpy(col, c.data(), c.size() * sizeof(int64_t));
+    if (val) {
+      if (s->f32)
+        for (size_t k = 0; k < v.size(); ++k) static_cast<float*>(val)[k] = float(v[k]);
+      else if (!v.empty())
+        std::memcpy(val, v.data(), v.size() * sizeof(double));
+    }
+  });
+}
+
 int mo_apply_kernel(mo_session s, int gather_set, char* name, size_t len) {
   SESSION_CALL(need(name, "output"); const std::string k = s->impl->apply_kernel(gather_set);
                mo::check(len > k.size(), mo::Err::kShapeMismatch, "name buffer too small");

@@ -1674,15 +1674,44 @@ struct Gen {
 
   ModuleInfo info;
 
+  // linearize (solver.hpp:291-322): evalj per element / edge, output l of
+  // element e -> out0[rowbase[l] + e] with rowbase[l] = l * extent (the
+  // reference's jlanes buffers), no exclusion mask (exec_grid(..., nullptr)).
+  void evalj_kernels() {
+    for (size_t i = 0; i < P.grid_sets.size(); ++i) {
+      const GridSet& g = P.grid_sets[i];
+      if (g.has_evalj)
+        grid_evalf(program(g.evalj, false, &g.dom), "mo_grid_evalj_" + std::to_string(i), g.evalj.outputs.size());
+    }
+    for (size_t i = 0; i < P.graph_sets.size(); ++i) {
+      const GraphSet& g = P.graph_sets[i];
+      if (g.has_evalj)
+        graph_kernel(program(g.evalj, true), "mo_graph_evalj_" + std::to_string(i), g.evalj.outputs.size(),
+                     P.graphs[size_t(g.graph)].second, 1);
+    }
+  }
+
   void run() {
+    const bool mat = P.cfg.materialize != 0;
     for (size_t i = 0; i < P.grid_sets.size(); ++i) {
       const GridSet& g = P.grid_sets[i];
       grid_cost(program(g.cost, false, &g.dom), "mo_grid_cost_" + std::to_string(i));
       grid_evalf(program(g.evalf, false, &g.dom), "mo_grid_evalf_" + std::to_string(i), g.evalf.outputs.size());
     }
+    if (mat) evalj_kernels();
     for (size_t i = 0; i < P.gather_sets.size(); ++i) {
       const GatherSet& g = P.gather_sets[i];
       gather_bm(g, program(g.bm, false, &g.dom), "mo_gather_bm_" + std::to_string(i));
+      if (mat) {  // no gather J^T J program: the apply runs from the materialized J
+        info.jtj2.push_back({});
+        info.jtj3.push_back({});
+        info.jtj4.push_back({});
+        info.jtj5.push_back({});
+        info.jtj6.push_back({});
+        info.jtj7.push_back({});
+        info.bm4.push_back({});
+        continue;
+      }
       gather_jtj(g, program(g.jtj, false, &g.dom), "mo_gather_jtj_" + std::to_string(i));
       tma6_info = ModuleInfo::Tma{};
       gather_jtj6(g, int(i));
@@ -1707,7 +1736,7 @@ struct Gen {
       graph_kernel(program(g.cost, true), "mo_graph_cost_" + s, g.cost.outputs.size(), ar, 0);
       graph_kernel(program(g.evalf, true), "mo_graph_evalf_" + s, g.evalf.outputs.size(), ar, 1);
       graph_kernel(program(g.bm, true), "mo_graph_bm_" + s, g.bm.outputs.size(), ar, 2);
-      graph_kernel(program(g.jtj, true), "mo_graph_jtj_" + s, g.jtj.outputs.size(), ar, 2);
+      if (!mat) graph_kernel(program(g.jtj, true), "mo_graph_jtj_" + s, g.jtj.outputs.size(), ar, 2);
       // Vertex-centric recompute kernels, one per scatter-target domain (in
       // the session's GatherDom order: first appearance over the scats).
       std::vector<Domain> doms;
@@ -1715,12 +1744,13 @@ struct Gen {
         const Domain& d = P.unknowns[size_t(sc.field)].dom;
         if (std::find(doms.begin(), doms.end(), d) == doms.end()) doms.push_back(d);
       }
-      const std::string pj = program(g.jtj, true), pb = program(g.bm, true);
+      const std::string pj = mat ? std::string() : program(g.jtj, true), pb = program(g.bm, true);
       for (size_t di = 0; di < doms.size(); ++di) {
-        vertex_kernel(g, doms[di], pj, "mo_graph_vjtj_" + s + "_" + std::to_string(di), ar, false);
+        if (!mat) vertex_kernel(g, doms[di], pj, "mo_graph_vjtj_" + s + "_" + std::to_string(di), ar, false);
         vertex_kernel(g, doms[di], pb, "mo_graph_vbm_" + s + "_" + std::to_string(di), ar, true);
       }
       info.vertex_kernels.push_back(true);
+      if (mat) continue;
       // One-pass apply: a single graph set scattering into one 1-D domain that
       // also holds the only gather set and every unknown column.
       bool one = P.graph_sets.size() == 1 && doms.size() == 1 && P.gather_sets.size() == 1 &&
@@ -1754,7 +1784,8 @@ struct Gen {
 
 }  // namespace
 
-std::string generate_module(const Plan& P, bool f64, const std::string& prelude, ModuleInfo* info) {
+std::string generate_module(const Plan& P, bool f64, const std::string& prelude, ModuleInfo* info,
+                            bool evalj_only) {
   Gen g(P, f64);
   g.os << "// generated by mo_codegen.cpp — do not edit\n";
   g.os << "typedef " << (f64 ? "double" : "float") << " Real;\n";
@@ -1766,7 +1797,10 @@ std::string generate_module(const Plan& P, bool f64, const std::string& prelude,
     g.os << "#define MO_EXP_BITS(v) (__float_as_uint(v) & 0x7f800000u)\n#define MO_EXP_MASK 0x7f800000u\n";
   g.os << prelude << "\n";
   g.os << "extern __shared__ __align__(128) unsigned char mo_dsm[];\n";
-  g.run();
+  if (evalj_only)
+    g.evalj_kernels();
+  else
+    g.run();
   if (info) *info = g.info;
   return g.os.str();
 }

@@ -45,7 +45,9 @@ struct ModuleInfo {
 };
 
 // Full NVRTC translation unit for one plan and precision.  `prelude` is the
-// text of mo_device.cuh.
+// text of mo_device.cuh.  evalj_only: just the linearize kernels
+// (mo_grid_evalj_<i>, mo_graph_evalj_<g>), compiled on demand for matrix-free
+// plans that also carry Jacobian lanes (force_evalj).
 std::string generate_module(const Plan& P, bool f64, const std::string& prelude,
-                            ModuleInfo* info = nullptr);
+                            ModuleInfo* info = nullptr, bool evalj_only = false);
 }  // namespace mo

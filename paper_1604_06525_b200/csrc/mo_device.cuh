@@ -31,7 +31,7 @@ struct mo_state {
   double tol_rel, tol_abs;
   int done, iters, indefinite, nonfinite;
   int use_precond, nonfinite_kernel;
-  int any_nonzero, pad0;
+  int any_nonzero, mat_bad;  // mat_bad: linearize's CSR checks (k_mat_check)
   long long unconstrained;
   double sums[8];
   unsigned counters[8];

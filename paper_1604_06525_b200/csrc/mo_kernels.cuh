@@ -371,4 +371,190 @@ k_graph_gather(long long nverts, const int* __restrict__ vptr, const int* __rest
   }
 }
 
+// ------------------------------------------------------------ materialized J
+// Materialize::kJ (solver.hpp:278-283, 291-376; sparse.hpp spmv / spmv_t).
+// J is kept as the reference keeps it before CSR assembly: one value lane
+// buffer per template set, [lane][row element] (jlanes_grid_ / jlanes_graph_),
+// plus these tables describing where each lane's column lies.  The apply is
+//   jtmp = J v          (k_mat_rows: one thread per row, entries in the CSR's
+//                        column order, acc = 0 then acc + val * v[col])
+//   out  = 2 J^T jtmp   (k_mat_cols: one thread per column, its entries in the
+//                        CSR's row order, i.e. spmv_t's scatter order)
+// with round-to-nearest intrinsics (no FMA contraction), so both products
+// round exactly like the reference's CPU loops.  A grid lane's column is
+// ubase + (e + lin) * C + ch with lin the lane offset linearised over the
+// domain shape, exactly linear_index(coord + off) (problem.hpp:131-136).
+#define MO_MAT_MAXL 32
+struct mo_mat_tmpl {
+  long long rowbase, nrows;  // rows [rowbase, rowbase + nrows); lane stride nrows
+  const void* buf;           // lane values, [out][nrows]
+  int kind;                  // 0 grid, 1 graph
+  int guard;                 // grid: boundary-guard lane (0 -> the row is empty)
+  int lane0, nlanes;         // into the lane table
+  const int* verts;          // graph: int32 edge-major vertex table
+  int arity;
+  const int* vptr;           // graph: vertex -> incident edges (unique, ascending)
+  const int* vedge;
+  long long nverts;
+};
+struct mo_mat_lane {
+  int out, field, ch, slot;
+  long long lin;  // grid: linearised stencil offset
+};
+struct mo_mat_centry {  // one source of entries of a (field, channel) column
+  int t, lane;          // grid: the lane; graph: -1 (scan the template's lanes per edge)
+};
+struct mo_mat_tables {
+  const mo_mat_tmpl* tm;
+  int ntm;
+  const mo_mat_lane* lanes;
+  const mo_mat_centry* ce;
+  const int* ceptr;  // per (field, channel) index cbase[f] + ch: [ceptr[k], ceptr[k+1])
+  long long ubase[MO_MAX_UNK];
+  int chans[MO_MAX_UNK];
+  int cbase[MO_MAX_UNK];
+  int nfields;
+  long long nrows, ncols;
+};
+
+__device__ __forceinline__ float mo_mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mo_mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float mo_add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double mo_add_rn(double a, double b) { return __dadd_rn(a, b); }
+
+__device__ __forceinline__ int mo_mat_find(const mo_mat_tables& T, long long r) {
+  int t = 0;
+  while (t + 1 < T.ntm && T.tm[t + 1].rowbase <= r) ++t;
+  return t;
+}
+
+// The reference's CSR assembly checks (sparse.hpp:30-37) on every non-empty
+// grid row: column inside the field (bit 0: kIndexOutOfRange; the reference
+// throws for columns outside [0, cols) and would silently read a neighbouring
+// field's column otherwise - the device refuses both) and strictly ascending
+// (bit 1: kInternal).
+template <class Real>
+__global__ void __launch_bounds__(MO_THREADS) k_mat_check(const __grid_constant__ mo_mat_tables T, mo_state* st) {
+  MO_PDL_ENTRY();
+  int bad = 0;
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < T.nrows;
+       r += (long long)gridDim.x * blockDim.x) {
+    const mo_mat_tmpl& M = T.tm[mo_mat_find(T, r)];
+    if (M.kind != 0) continue;
+    const long long e = r - M.rowbase;
+    if (static_cast<const Real*>(M.buf)[(long long)M.guard * M.nrows + e] == Real(0)) continue;
+    long long prev = -1;
+    for (int k = 0; k < M.nlanes; ++k) {
+      const mo_mat_lane L = T.lanes[M.lane0 + k];
+      const long long el = e + L.lin;
+      if (el < 0 || el >= M.nrows) {
+        bad |= 1;
+        continue;
+      }
+      const long long col = T.ubase[L.field] + el * T.chans[L.field] + L.ch;
+      if (col <= prev) bad |= 2;
+      prev = col;
+    }
+  }
+  if (bad) atomicOr(&st->mat_bad, bad);
+}
+
+template <class Real>
+__global__ void __launch_bounds__(MO_THREADS)
+k_mat_rows(const __grid_constant__ mo_mat_tables T, const mo_state* st, int skipdone, const Real* __restrict__ v,
+           Real* __restrict__ jtmp) {
+  MO_PDL_ENTRY();
+  if (skipdone && st->done) return;
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < T.nrows;
+       r += (long long)gridDim.x * blockDim.x) {
+    const mo_mat_tmpl& M = T.tm[mo_mat_find(T, r)];
+    const long long e = r - M.rowbase;
+    const Real* buf = static_cast<const Real*>(M.buf);
+    Real acc = Real(0);
+    if (M.kind == 0) {
+      if (buf[(long long)M.guard * M.nrows + e] != Real(0)) {
+        for (int k = 0; k < M.nlanes; ++k) {
+          const mo_mat_lane L = T.lanes[M.lane0 + k];
+          const long long el = e + L.lin;
+          if (el < 0 || el >= M.nrows) continue;  // (refused by k_mat_check)
+          const long long col = T.ubase[L.field] + el * T.chans[L.field] + L.ch;
+          acc = mo_add_rn(acc, mo_mul_rn(buf[(long long)L.out * M.nrows + e], v[col]));
+        }
+      }
+    } else {
+      // Edge row: entries sorted by column (stable: repeated vertices keep
+      // lane order) and merged (solver.hpp:350-366).
+      long long cols[MO_MAT_MAXL];
+      Real vals[MO_MAT_MAXL];
+      int n = 0;
+      for (int k = 0; k < M.nlanes; ++k) {
+        const mo_mat_lane L = T.lanes[M.lane0 + k];
+        const long long col = T.ubase[L.field] + (long long)M.verts[e * M.arity + L.slot] * T.chans[L.field] + L.ch;
+        const Real val = buf[(long long)L.out * M.nrows + e];
+        int j = n++;
+        while (j > 0 && cols[j - 1] > col) {
+          cols[j] = cols[j - 1];
+          vals[j] = vals[j - 1];
+          --j;
+        }
+        cols[j] = col;
+        vals[j] = val;
+      }
+      for (int k = 0; k < n;) {
+        const long long col = cols[k];
+        Real mv = vals[k];
+        for (++k; k < n && cols[k] == col; ++k) mv = mo_add_rn(mv, vals[k]);
+        acc = mo_add_rn(acc, mo_mul_rn(mv, v[col]));
+      }
+    }
+    jtmp[r] = acc;
+  }
+}
+
+template <class Real>
+__global__ void __launch_bounds__(MO_THREADS)
+k_mat_cols(const __grid_constant__ mo_mat_tables T, const mo_state* st, int skipdone, const Real* __restrict__ jtmp,
+           Real* __restrict__ out) {
+  MO_PDL_ENTRY();
+  if (skipdone && st->done) return;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < T.ncols;
+       q += (long long)gridDim.x * blockDim.x) {
+    int f = 0;
+    while (f + 1 < T.nfields && T.ubase[f + 1] <= q) ++f;
+    const long long rel = q - T.ubase[f];
+    const long long el = rel / T.chans[f];
+    const int ch = int(rel - el * T.chans[f]);
+    const int k = T.cbase[f] + ch;
+    Real y = Real(0);
+    for (int c = T.ceptr[k]; c < T.ceptr[k + 1]; ++c) {
+      const mo_mat_centry E = T.ce[c];
+      const mo_mat_tmpl& M = T.tm[E.t];
+      const Real* buf = static_cast<const Real*>(M.buf);
+      if (E.lane >= 0) {  // grid: the one row of this template holding q through the lane
+        const mo_mat_lane L = T.lanes[E.lane];
+        const long long e = el - L.lin;
+        if (e < 0 || e >= M.nrows) continue;
+        if (buf[(long long)M.guard * M.nrows + e] == Real(0)) continue;
+        y = mo_add_rn(y, mo_mul_rn(buf[(long long)L.out * M.nrows + e], jtmp[M.rowbase + e]));
+      } else {  // graph: incident edges in row order, the merged entry of q
+        if (el >= M.nverts) continue;
+        for (int j = M.vptr[el]; j < M.vptr[el + 1]; ++j) {
+          const int e = M.vedge[j];
+          bool has = false;
+          Real mv = Real(0);
+          for (int l = 0; l < M.nlanes; ++l) {
+            const mo_mat_lane L = T.lanes[M.lane0 + l];
+            if (L.field != f || L.ch != ch || M.verts[(long long)e * M.arity + L.slot] != el) continue;
+            const Real val = buf[(long long)L.out * M.nrows + e];
+            mv = has ? mo_add_rn(mv, val) : val;
+            has = true;
+          }
+          if (has) y = mo_add_rn(y, mo_mul_rn(mv, jtmp[M.rowbase + e]));
+        }
+      }
+    }
+    out[q] = mo_mul_rn(y, Real(2));
+  }
+}
+
 }  // namespace mo

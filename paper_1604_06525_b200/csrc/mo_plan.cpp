@@ -60,7 +60,10 @@ struct Lexer {
     Program p;
     p.num_regs = uint32_t(integer());
     long long ni = integer(), nb = integer(), ng = integer(), no = integer();
-    check(ni >= 0 && nb >= 0 && ng >= 1 && no >= 0, Err::kFormatError, "moplan: bad program header");
+    // (a program the plan did not compile - e.g. the gather J^T J of a
+    // materialized plan - is exported empty, without even the "always" guard)
+    check(ni >= 0 && nb >= 0 && no >= 0 && (ng >= 1 || (ni == 0 && nb == 0 && no == 0)), Err::kFormatError,
+          "moplan: bad program header");
     p.instrs.resize(size_t(ni));
     for (Instr& in : p.instrs) {
       expect("i");
@@ -145,6 +148,11 @@ Plan parse_plan(const std::string& text) {
   c.lm_diag_max = L.real();
   c.lm_min_decrease = L.real();
   c.cost_stop_tol = L.real();
+  if (L.peek() == "materialize") {
+    L.expect("materialize");
+    c.materialize = int(L.integer());
+    check(c.materialize >= 0 && c.materialize <= 2, Err::kFormatError, "moplan: bad materialize mode");
+  }
 
   L.expect("dims");
   long long nd = L.integer();
@@ -279,6 +287,34 @@ Plan parse_plan(const std::string& text) {
     g.evalf = L.program("evalf");
     g.bm = L.program("bm");
     g.jtj = L.program("jtj");
+    if (L.peek() == "gevalj") {
+      L.expect("gevalj");
+      long long njt = L.integer();
+      for (long long k = 0; k < njt; ++k) {
+        L.expect("gjtemplate");
+        JTemplate jt;
+        jt.tmpl = int(L.integer());
+        jt.guard_out = -1;
+        long long nl = L.integer();
+        for (long long l = 0; l < nl; ++l) {
+          Lane ln;
+          ln.out = int(L.integer());
+          ln.field = int(L.integer());
+          ln.channel = int(L.integer());
+          ln.slot = int(L.integer());
+          jt.lanes.push_back(ln);
+        }
+        g.jtemplates.push_back(std::move(jt));
+      }
+      g.evalj = L.program("evalj");
+      g.has_evalj = true;
+      for (const JTemplate& jt : g.jtemplates)
+        for (const Lane& ln : jt.lanes)
+          check(ln.out >= 0 && size_t(ln.out) < g.evalj.outputs.size() && ln.field >= 0 &&
+                    size_t(ln.field) < P.unknowns.size() && ln.slot >= 0 &&
+                    ln.slot < P.graphs[size_t(g.graph)].second,
+                Err::kFormatError, "moplan: bad graph Jacobian lane");
+    }
     P.graph_sets.push_back(std::move(g));
   }
   L.expect("computed_kernels");
@@ -307,13 +343,15 @@ Plan parse_plan(const std::string& text) {
   check(P.unknowns.size() <= 16, Err::kInternal, "moplan: more than 16 unknown fields");
   check(2 * P.unknowns.size() + P.arrays.size() + P.computed.size() <= 32, Err::kInternal,
         "moplan: more than 32 bound fields");
+  // (materialized plans compile no J^T J gather programs, plan.hpp:210)
+  const bool free = P.cfg.materialize == 0;
   for (const GatherSet& g : P.gather_sets) {
     check(g.bm.outputs.size() == 2 * g.chans.size(), Err::kFormatError, "moplan: bm outputs");
-    check(g.jtj.outputs.size() == g.chans.size(), Err::kFormatError, "moplan: jtj outputs");
+    check(!free || g.jtj.outputs.size() == g.chans.size(), Err::kFormatError, "moplan: jtj outputs");
   }
   for (const GraphSet& g : P.graph_sets) {
     check(g.bm.outputs.size() == 2 * g.scats.size(), Err::kFormatError, "moplan: graph bm outputs");
-    check(g.jtj.outputs.size() == g.scats.size(), Err::kFormatError, "moplan: graph jtj outputs");
+    check(!free || g.jtj.outputs.size() == g.scats.size(), Err::kFormatError, "moplan: graph jtj outputs");
     check(g.graph >= 0 && size_t(g.graph) < P.graphs.size(), Err::kFormatError, "moplan: graph index");
   }
   int64_t saved = P.num_cols;

@@ -87,6 +87,7 @@ struct Config {  // SolveConfig (plan.hpp:19-38), device-relevant members
   double lm_radius0 = 1e4, lm_radius_min = 1e-32, lm_radius_max = 1e16;
   double lm_diag_min = 1e-6, lm_diag_max = 1e32, lm_min_decrease = 1e-3;
   double cost_stop_tol = 0.0;
+  int materialize = 0;  // Materialize (plan.hpp:17): 0 none, 1 kJ, 2 kJtJ
 };
 
 struct Residual {
@@ -100,6 +101,7 @@ struct Residual {
 struct Lane {
   int out = 0, field = 0, channel = 0;
   int off[3] = {0, 0, 0};
+  int slot = -1;  // graph rows: edge slot of the column's vertex
 };
 struct JTemplate {
   int tmpl = 0, guard_out = 0;
@@ -129,6 +131,9 @@ struct GraphSet {
   std::vector<int> templates;
   std::vector<Scat> scats;
   Program cost, evalf, bm, jtj;
+  bool has_evalj = false;
+  std::vector<JTemplate> jtemplates;  // lanes carry slots (plan.hpp:318-330)
+  Program evalj;
 };
 struct ComputedKernel {
   int index = 0;

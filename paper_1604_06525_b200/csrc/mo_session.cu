@@ -83,6 +83,9 @@ class Session final : public SessionBase {
     CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
     cfg_ = P_.cfg;
     if (cfg_.pcg_rel_tol < 0) cfg_.pcg_rel_tol = cfg_.precision == 0 ? 1e-4 : 1e-8;
+    mat_ = P_.cfg.materialize;
+    check(mat_ != 2, Err::kBindError, "Materialize::kJtJ is not supported by the device path (kJ and kNone are)");
+    check(!mat_ || !comm_, Err::kBindError, "materialized plans cannot be strip-sharded");
 
     // JIT the plan's per-element kernels (plan time; cached on disk).
     std::string src = generate_module(P_, sizeof(Real) == 8, device_prelude(), &minfo_);
@@ -149,6 +152,14 @@ class Session final : public SessionBase {
     for (size_t i = 0; i < P_.grid_sets.size(); ++i)
       grid_rowbase_[i] = dalloc<long long>(P_.grid_sets[i].templates.size());
     for (size_t i = 0; i < P_.graph_sets.size(); ++i) setup_graph_set(int(i));
+    jl_grid_.assign(P_.grid_sets.size(), nullptr);
+    jl_rb_grid_.assign(P_.grid_sets.size(), nullptr);
+    jl_graph_.assign(P_.graph_sets.size(), nullptr);
+    jl_rb_graph_.assign(P_.graph_sets.size(), nullptr);
+    jl_graph_cap_.assign(P_.graph_sets.size(), 0);
+    mat_vptr_.assign(P_.graphs.size(), nullptr);
+    mat_vedge_.assign(P_.graphs.size(), nullptr);
+    mat_nverts_.assign(P_.graphs.size(), 0);
     CK(cudaStreamSynchronize(st_));
   }
 
@@ -181,6 +192,14 @@ class Session final : public SessionBase {
         cudaFree(d.outs_jtj);
       }
     }
+    for (Real* p : jl_grid_) cudaFree(p);
+    for (Real* p : jl_graph_) cudaFree(p);
+    for (long long* p : jl_rb_grid_) cudaFree(p);
+    for (long long* p : jl_rb_graph_) cudaFree(p);
+    for (int* p : mat_vptr_) cudaFree(p);
+    for (int* p : mat_vedge_) cudaFree(p);
+    for (void* p : mt_bufs_) cudaFree(p);
+    cudaFree(jtmp_);
     for (auto& kv : stage_ev_)
       for (auto& ev : kv.second) {
         cudaEventDestroy(ev.a);
@@ -236,6 +255,7 @@ class Session final : public SessionBase {
     refresh_host();
     refresh_device();
     refreshed_ = true;
+    jvalid_ = false;  // solver.hpp:167
   }
 
   // Do the exclusion programs read the unknowns (or computed arrays)?  If
@@ -287,6 +307,7 @@ class Session final : public SessionBase {
       row += r.graph ? graphs_[size_t(r.graph_idx)].E : P_.extent_of(r.dom);
     }
     rows_ = row;
+    if (mat_) mat_prepare();
     if (rowbase_ == rowbase_dev_) {  // unchanged since the last upload
       refreshed_ = true;
       return;
@@ -435,6 +456,7 @@ class Session final : public SessionBase {
             cost_at(x_, SLOT_COST);
           const bool fi = bm_init_ok();
           normal_device(fi);
+          if (mat_) linearize_device();  // solver.hpp:426
           pcg_body(false, fi);
           CK(cudaMemsetAsync(&state_->any_nonzero, 0, sizeof(int), st_));
           kl(k_xtrial<Real>, dim3(vg), dim3(MO_THREADS), state_, n, colmask_, x_, delta_, xt_, 1, SLOT_COST);
@@ -444,6 +466,10 @@ class Session final : public SessionBase {
           reduce_flags();
         });
         sync_state();
+        if (mat_) {  // (the replayed stage ran linearize)
+          check_mat_bad();
+          jvalid_ = true;
+        }
         collect_profile(reuse_cost ? kStageGNNext : kStageGN);
         const mo_state S = *state_h_;
         const double cost_old = S.sums[SLOT_COST];
@@ -485,10 +511,15 @@ class Session final : public SessionBase {
         refresh_device();
         cost_at(x_, SLOT_COST);
         normal_device();
+        if (mat_) linearize_device();  // solver.hpp:426
         kl(k_lm_base_diag<Real>, dim3(vg), dim3(MO_THREADS), n, m_, bd_, cfg_.lm_diag_min, cfg_.lm_diag_max);
         ++launches_;
       });
       sync_state();
+      if (mat_) {
+        check_mat_bad();
+        jvalid_ = true;
+      }
       collect_profile(kStageLMLin);
       const double cost_old = state_h_->sums[SLOT_COST];
       if (!std::isfinite(cost_old)) {
@@ -589,6 +620,7 @@ class Session final : public SessionBase {
     check(i >= 0 && size_t(i) < P_.gather_sets.size(), Err::kIndexOutOfRange, "no such gather set");
     ensure_refreshed();
     tune_apply();
+    if (mat_) return "k_mat_cols";
     if (vertex_apply_one_pass()) return "mo_graph_vjtjf_0";
     return jtj_kernel(size_t(i));
   }
@@ -907,6 +939,7 @@ class Session final : public SessionBase {
       CK(cudaStreamSynchronize(st_));
       invalidate_graphs();  // edge counts are baked into the captured PCG graph
       g.dirty = false;
+      mt_dirty_ = true;
     }
   }
 
@@ -917,6 +950,23 @@ class Session final : public SessionBase {
 
   void* arena_ = nullptr;
   size_t arena_bytes_ = 0;
+
+  // materialized J (linearize / Materialize::kJ)
+  int mat_ = 0;
+  bool jvalid_ = false, mt_dirty_ = true, mt_ok_ = false, csr_ok_ = false;
+  Module mod_evj_;
+  std::vector<Real*> jl_grid_, jl_graph_;
+  std::vector<long long*> jl_rb_grid_, jl_rb_graph_;
+  std::vector<size_t> jl_graph_cap_;
+  std::vector<int*> mat_vptr_, mat_vedge_;
+  std::vector<long long> mat_nverts_;
+  std::vector<int64_t> mt_rowbase_;
+  std::vector<void*> mt_bufs_;
+  mo_mat_tables mt_{};
+  Real* jtmp_ = nullptr;
+  size_t jtmp_cap_ = 0;
+  std::vector<int64_t> csr_offs_, csr_col_;
+  std::vector<Real> csr_val_;
 
   // ------------------------------------------------------------ launches
   // Every kernel of the solver goes through kl()/klc() with the
@@ -1177,6 +1227,7 @@ class Session final : public SessionBase {
   void tune_apply() {
     if (tuned_) return;
     tuned_ = true;
+    if (mat_) return;  // one apply: the materialized J
     // One decision per (module, shape) per process, so every session of a plan
     // runs the same kernel (bitwise run-to-run reproducibility).
     static std::mutex mu;
@@ -1612,6 +1663,10 @@ class Session final : public SessionBase {
   // out = 2 J^T J pv (+ damp pv), optionally zeroing excluded columns and
   // reducing p'Ap into alpha (flags: MO_F_DAMP | MO_F_REDUCE | MO_F_ZEROEXCL).
   void apply(const Real* pv, Real* out, int flags) {
+    if (mat_) {
+      mat_apply(pv, out, flags);
+      return;
+    }
     if (vertex_apply_one_pass()) {
       apply_vertex_fused(pv, out, flags);
       return;
@@ -1654,6 +1709,380 @@ class Session final : public SessionBase {
     }
   }
 
+  // ------------------------------------------------------------ materialized J
+  // linearize (solver.hpp:291-376) keeps J as the reference does before its
+  // CSR assembly: the evalj lanes, [lane][element] per template set.  In
+  // Materialize::kJ plans the apply is 2 J^T (J v) from those lanes
+  // (k_mat_rows / k_mat_cols, sparse.hpp spmv / spmv_t order); jacobian()
+  // assembles the reference's CSR on the host for callers that want it.
+  bool plan_has_evalj() const {
+    for (const GridSet& g : P_.grid_sets)
+      if (!g.templates.empty() && !g.has_evalj) return false;
+    for (const GraphSet& g : P_.graph_sets)
+      if (!g.templates.empty() && !g.has_evalj) return false;
+    return true;
+  }
+  const void* evj_kernel(const std::string& name) {
+    if (mat_) return mod_.kernel(name);
+    if (!mod_evj_.loaded())  // matrix-free plan with lanes: compile the linearize kernels on demand
+      mod_evj_.load(compile_cubin(generate_module(P_, sizeof(Real) == 8, device_prelude(), nullptr, true),
+                                  "mo_evalj.cu", P_.exact));
+    return mod_evj_.kernel(name);
+  }
+  // linear_index(coord + off) - linear_index(coord) (problem.hpp:131-136)
+  static long long lane_lin(const Lane& l, const std::array<int64_t, 3>& sh) {
+    return ((long long)l.off[0] * sh[1] + l.off[1]) * sh[2] + l.off[2];
+  }
+  void check_mat_bad() {
+    if (state_h_->mat_bad & 1) fail(Err::kIndexOutOfRange, "CSR column out of range");
+    if (state_h_->mat_bad & 2) fail(Err::kInternal, "CSR row entries must arrive in increasing column order");
+  }
+  static std::vector<long long> lane_rowbase(size_t nout, long long n) {
+    std::vector<long long> rb(std::max<size_t>(nout, 1));
+    for (size_t k = 0; k < rb.size(); ++k) rb[k] = (long long)k * n;
+    return rb;
+  }
+  // Lane buffers, row tables and per-graph incidence; rebuilt when the
+  // residual rows or the graphs change (never inside a captured stage).
+  void mat_prepare() {
+    if (!mt_dirty_ && mt_rowbase_ == rowbase_ && mt_ok_) return;
+    bool realloc = false;
+    for (size_t i = 0; i < P_.grid_sets.size(); ++i) {
+      const GridSet& g = P_.grid_sets[i];
+      if (g.jtemplates.empty() || jl_grid_[i]) continue;
+      const long long ext = P_.extent_of(g.dom);
+      const size_t no = g.evalj.outputs.size();
+      jl_grid_[i] = dalloc<Real>(std::max<size_t>(no * size_t(ext), 1));
+      const auto rb = lane_rowbase(no, ext);
+      jl_rb_grid_[i] = dalloc<long long>(rb.size());
+      CK(cudaMemcpyAsync(jl_rb_grid_[i], rb.data(), rb.size() * sizeof(long long), cudaMemcpyHostToDevice, st_));
+      realloc = true;
+    }
+    for (size_t i = 0; i < P_.graph_sets.size(); ++i) {
+      const GraphSet& g = P_.graph_sets[i];
+      if (g.jtemplates.empty()) continue;
+      const long long E = graphs_[size_t(g.graph)].E;
+      const size_t no = g.evalj.outputs.size(), need = std::max<size_t>(no * size_t(E), 1);
+      if (need > jl_graph_cap_[i]) {
+        cudaFree(jl_graph_[i]);
+        jl_graph_[i] = dalloc<Real>(need);
+        jl_graph_cap_[i] = need;
+      }
+      const auto rb = lane_rowbase(no, E);
+      if (!jl_rb_graph_[i]) jl_rb_graph_[i] = dalloc<long long>(rb.size());
+      CK(cudaMemcpyAsync(jl_rb_graph_[i], rb.data(), rb.size() * sizeof(long long), cudaMemcpyHostToDevice, st_));
+      realloc = true;
+    }
+    if (size_t(rows_) > jtmp_cap_) {
+      cudaFree(jtmp_);
+      jtmp_ = dalloc<Real>(size_t(rows_));
+      jtmp_cap_ = size_t(rows_);
+    }
+    // Per-graph vertex -> incident edges (each edge once, ascending): the
+    // row order of spmv_t for a vertex column.
+    for (size_t gi = 0; gi < graphs_.size(); ++gi) {
+      const GraphData& g = graphs_[gi];
+      long long nv = 0;
+      for (uint64_t v : g.verts) nv = std::max<long long>(nv, (long long)v + 1);
+      std::vector<int> cnt(size_t(nv) + 1, 0), last(size_t(nv), -1), vedge;
+      for (int64_t e = 0; e < g.E; ++e)
+        for (int k = 0; k < g.arity; ++k) {
+          const size_t v = size_t(g.verts[size_t(e * g.arity + k)]);
+          if (last[v] != int(e)) {
+            last[v] = int(e);
+            cnt[v + 1]++;
+          }
+        }
+      for (size_t v = 0; v < size_t(nv); ++v) cnt[v + 1] += cnt[v];
+      vedge.resize(size_t(cnt[size_t(nv)]));
+      std::vector<int> pos(cnt.begin(), cnt.end() - 1);
+      std::fill(last.begin(), last.end(), -1);
+      for (int64_t e = 0; e < g.E; ++e)
+        for (int k = 0; k < g.arity; ++k) {
+          const size_t v = size_t(g.verts[size_t(e * g.arity + k)]);
+          if (last[v] != int(e)) {
+            last[v] = int(e);
+            vedge[size_t(pos[v]++)] = int(e);
+          }
+        }
+      cudaFree(mat_vptr_[gi]);
+      cudaFree(mat_vedge_[gi]);
+      mat_vptr_[gi] = dalloc<int>(cnt.size());
+      mat_vedge_[gi] = dalloc<int>(std::max<size_t>(vedge.size(), 1));
+      CK(cudaMemcpyAsync(mat_vptr_[gi], cnt.data(), cnt.size() * sizeof(int), cudaMemcpyHostToDevice, st_));
+      if (!vedge.empty())
+        CK(cudaMemcpyAsync(mat_vedge_[gi], vedge.data(), vedge.size() * sizeof(int), cudaMemcpyHostToDevice, st_));
+      mat_nverts_[gi] = nv;
+      CK(cudaStreamSynchronize(st_));
+    }
+    // Row tables, one per residual template, in template (= row) order.
+    const size_t NT = P_.residuals.size();
+    std::vector<mo_mat_tmpl> tm(NT);
+    std::vector<bool> seen(NT, false);
+    std::vector<mo_mat_lane> lanes;
+    for (size_t i = 0; i < P_.grid_sets.size(); ++i) {
+      const GridSet& g = P_.grid_sets[i];
+      const auto sh = P_.shape_of(g.dom);
+      for (const JTemplate& jt : g.jtemplates) {
+        mo_mat_tmpl& M = tm[size_t(jt.tmpl)];
+        M = mo_mat_tmpl{};
+        M.rowbase = rowbase_[size_t(jt.tmpl)];
+        M.nrows = P_.extent_of(g.dom);
+        M.buf = jl_grid_[i];
+        M.kind = 0;
+        M.guard = jt.guard_out;
+        M.lane0 = int(lanes.size());
+        M.nlanes = int(jt.lanes.size());
+        for (const Lane& l : jt.lanes) {
+          check(P_.unknowns[size_t(l.field)].dom == g.dom, Err::kBindError,
+                "materialized J: an unknown read on a different domain than its residual's");
+          lanes.push_back({l.out, l.field, l.channel, -1, lane_lin(l, sh)});
+        }
+        seen[size_t(jt.tmpl)] = true;
+      }
+    }
+    for (size_t i = 0; i < P_.graph_sets.size(); ++i) {
+      const GraphSet& g = P_.graph_sets[i];
+      const GraphData& gd = graphs_[size_t(g.graph)];
+      for (const JTemplate& jt : g.jtemplates) {
+        check(jt.lanes.size() <= MO_MAT_MAXL, Err::kInternal, "materialized J: too many lanes per edge row");
+        mo_mat_tmpl& M = tm[size_t(jt.tmpl)];
+        M = mo_mat_tmpl{};
+        M.rowbase = rowbase_[size_t(jt.tmpl)];
+        M.nrows = gd.E;
+        M.buf = jl_graph_[i];
+        M.kind = 1;
+        M.guard = -1;
+        M.lane0 = int(lanes.size());
+        M.nlanes = int(jt.lanes.size());
+        M.verts = gd.d_verts;
+        M.arity = gd.arity;
+        M.vptr = mat_vptr_[size_t(g.graph)];
+        M.vedge = mat_vedge_[size_t(g.graph)];
+        M.nverts = mat_nverts_[size_t(g.graph)];
+        for (const Lane& l : jt.lanes) lanes.push_back({l.out, l.field, l.channel, l.slot, 0});
+        seen[size_t(jt.tmpl)] = true;
+      }
+    }
+    for (size_t t = 0; t < NT; ++t) check(seen[t], Err::kBindError, "plan was compiled without Jacobian kernels");
+    // Column entry lists per (field, channel): templates ascending; within a
+    // grid template the rows holding the column ascend as the offset descends.
+    std::vector<int> cbase(P_.unknowns.size() + 1, 0);
+    for (size_t f = 0; f < P_.unknowns.size(); ++f) cbase[f + 1] = cbase[f] + P_.unknowns[f].channels;
+    std::vector<std::vector<mo_mat_centry>> per(size_t(cbase.back()));
+    for (size_t t = 0; t < NT; ++t) {
+      const mo_mat_tmpl& M = tm[t];
+      std::vector<int> idx;
+      for (int k = 0; k < M.nlanes; ++k) idx.push_back(M.lane0 + k);
+      if (M.kind == 0) {
+        std::stable_sort(idx.begin(), idx.end(),
+                         [&](int a, int b) { return lanes[size_t(a)].lin > lanes[size_t(b)].lin; });
+        for (int k : idx) per[size_t(cbase[size_t(lanes[size_t(k)].field)] + lanes[size_t(k)].ch)].push_back({int(t), k});
+      } else {
+        for (int k : idx) {
+          auto& v = per[size_t(cbase[size_t(lanes[size_t(k)].field)] + lanes[size_t(k)].ch)];
+          if (v.empty() || v.back().t != int(t)) v.push_back({int(t), -1});
+        }
+      }
+    }
+    std::vector<mo_mat_centry> ce;
+    std::vector<int> ceptr{0};
+    for (auto& v : per) {
+      ce.insert(ce.end(), v.begin(), v.end());
+      ceptr.push_back(int(ce.size()));
+    }
+    for (void* p : mt_bufs_) cudaFree(p);
+    mt_bufs_.clear();
+    auto up = [&](const void* src, size_t bytes) {
+      void* d = dalloc<unsigned char>(std::max<size_t>(bytes, 1));
+      if (bytes) CK(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, st_));
+      mt_bufs_.push_back(d);
+      return d;
+    };
+    mt_ = mo_mat_tables{};
+    mt_.tm = static_cast<const mo_mat_tmpl*>(up(tm.data(), tm.size() * sizeof(mo_mat_tmpl)));
+    mt_.ntm = int(NT);
+    mt_.lanes = static_cast<const mo_mat_lane*>(up(lanes.data(), lanes.size() * sizeof(mo_mat_lane)));
+    mt_.ce = static_cast<const mo_mat_centry*>(up(ce.data(), ce.size() * sizeof(mo_mat_centry)));
+    mt_.ceptr = static_cast<const int*>(up(ceptr.data(), ceptr.size() * sizeof(int)));
+    for (size_t f = 0; f < P_.unknowns.size(); ++f) {
+      mt_.ubase[f] = P_.ubase[f];
+      mt_.chans[f] = P_.unknowns[f].channels;
+      mt_.cbase[f] = cbase[f];
+    }
+    mt_.nfields = int(P_.unknowns.size());
+    mt_.nrows = rows_;
+    mt_.ncols = P_.num_cols;
+    CK(cudaStreamSynchronize(st_));
+    if (realloc || mt_ok_) invalidate_graphs();  // captured stages hold the old pointers
+    mt_rowbase_ = rowbase_;
+    mt_dirty_ = false;
+    mt_ok_ = true;
+    jvalid_ = false;
+  }
+  void linearize_device() {
+    CK(cudaMemsetAsync(&state_->mat_bad, 0, sizeof(int), st_));
+    bool grid_rows = false;
+    for (size_t i = 0; i < P_.grid_sets.size(); ++i) {
+      const GridSet& g = P_.grid_sets[i];
+      if (g.jtemplates.empty()) continue;
+      mo_kparams kp = kp_grid(g.dom, x_, nullptr);
+      kp.out0 = jl_grid_[i];
+      kp.rowbase = jl_rb_grid_[i];
+      const void* f = evj_kernel("mo_grid_evalj_" + std::to_string(i));
+      const long long nb = std::min<long long>(tiles_of(g.dom), (long long)nsm_ * occupancy(f));
+      dim3 block = g.dom.dims.size() <= 1 ? dim3(MO_THREADS, 1, 1) : dim3(MO_TILE_X, MO_TILE_Y, 1);
+      void* args[] = {&kp};
+      klc(f, dim3(unsigned(std::max<long long>(nb, 1))), block, args, 0);
+      ++launches_;
+      grid_rows = true;
+    }
+    if (grid_rows && mt_ok_ && rows_ > 0) {
+      kl(k_mat_check<Real>, dim3(vgrid(rows_, nsm_)), dim3(MO_THREADS), mt_, state_);
+      ++launches_;
+    }
+    for (size_t i = 0; i < P_.graph_sets.size(); ++i) {
+      const GraphSet& g = P_.graph_sets[i];
+      if (g.jtemplates.empty() || graphs_[size_t(g.graph)].E == 0) continue;
+      mo_kparams kp = kp_graph(int(i), x_, nullptr);
+      kp.out0 = jl_graph_[i];
+      kp.rowbase = jl_rb_graph_[i];
+      const void* f = evj_kernel("mo_graph_evalj_" + std::to_string(i));
+      const long long nb =
+          std::min<long long>((graphs_[size_t(g.graph)].E + MO_THREADS - 1) / MO_THREADS, (long long)nsm_ * occupancy(f));
+      void* args[] = {&kp};
+      klc(f, dim3(unsigned(std::max<long long>(nb, 1))), dim3(MO_THREADS), args, 0);
+      ++launches_;
+    }
+    jvalid_ = true;
+  }
+  // apply_jtj, materialized branch (solver.hpp:278-283) + apply_damped's
+  // damping, exclusion and p'Ap (pcg.hpp:100-102) in k_apply_finish.
+  void mat_apply(const Real* pv, Real* out, int flags) {
+    check(jvalid_, Err::kInternal, "normal-matrix apply before linearize()");
+    const long long n = P_.num_cols;
+    const int skip = (flags & MO_F_SKIPDONE) ? 1 : 0;
+    if (rows_ > 0) {
+      kl(k_mat_rows<Real>, dim3(vgrid(rows_, nsm_)), dim3(MO_THREADS), mt_, static_cast<const mo_state*>(state_), skip,
+         pv, jtmp_);
+      ++launches_;
+    }
+    kl(k_mat_cols<Real>, dim3(vgrid(n, nsm_)), dim3(MO_THREADS), mt_, static_cast<const mo_state*>(state_), skip,
+       static_cast<const Real*>(jtmp_), out);
+    ++launches_;
+    apply_parts_ = vgrid(n, nsm_);
+    if (flags & (MO_F_DAMP | MO_F_REDUCE | MO_F_ZEROEXCL)) {
+      kl(k_apply_finish<Real>, dim3(vgrid(n, nsm_)), dim3(MO_THREADS), red(0, vgrid(n, nsm_), MO_FIN_PCG_ALPHA, 0), n,
+         colmask_, pv, damp_, out, flags);
+      ++launches_;
+    }
+  }
+
+ public:
+  void linearize() override {
+    ensure_refreshed();
+    check(plan_has_evalj(), Err::kBindError, "plan was compiled without Jacobian kernels");
+    cur_stage_ = -1;
+    mat_prepare();
+    linearize_device();
+    sync_state();
+    csr_ok_ = false;
+    if (state_h_->mat_bad) jvalid_ = false;
+    check_mat_bad();
+  }
+  void jacobian(int64_t* rows, int64_t* cols, std::vector<int64_t>* offs, std::vector<int64_t>* col,
+                std::vector<double>* val) override {
+    check(jvalid_, Err::kBindError, "no Jacobian has been materialized");
+    if (!csr_ok_) assemble_csr();
+    *rows = rows_;
+    *cols = P_.num_cols;
+    if (offs) *offs = csr_offs_;
+    if (col) *col = csr_col_;
+    if (val) val->assign(csr_val_.begin(), csr_val_.end());
+  }
+
+ private:
+  // The reference's CSR assembly (solver.hpp:323-369) over the device lanes.
+  void assemble_csr() {
+    std::vector<std::vector<Real>> hg(P_.grid_sets.size()), hr(P_.graph_sets.size());
+    for (size_t i = 0; i < P_.grid_sets.size(); ++i) {
+      const GridSet& g = P_.grid_sets[i];
+      if (g.jtemplates.empty()) continue;
+      hg[i].resize(g.evalj.outputs.size() * size_t(P_.extent_of(g.dom)));
+      if (!hg[i].empty())
+        CK(cudaMemcpyAsync(hg[i].data(), jl_grid_[i], hg[i].size() * sizeof(Real), cudaMemcpyDeviceToHost, st_));
+    }
+    for (size_t i = 0; i < P_.graph_sets.size(); ++i) {
+      const GraphSet& g = P_.graph_sets[i];
+      if (g.jtemplates.empty()) continue;
+      hr[i].resize(g.evalj.outputs.size() * size_t(graphs_[size_t(g.graph)].E));
+      if (!hr[i].empty())
+        CK(cudaMemcpyAsync(hr[i].data(), jl_graph_[i], hr[i].size() * sizeof(Real), cudaMemcpyDeviceToHost, st_));
+    }
+    CK(cudaStreamSynchronize(st_));
+    csr_offs_.assign(1, 0);
+    csr_col_.clear();
+    csr_val_.clear();
+    auto begin_row = [&] { csr_offs_.push_back(int64_t(csr_col_.size())); };
+    auto push = [&](int64_t c, Real v) {
+      csr_col_.push_back(c);
+      csr_val_.push_back(v);
+      csr_offs_.back() = int64_t(csr_col_.size());
+    };
+    for (size_t t = 0; t < P_.residuals.size(); ++t) {
+      bool done = false;
+      for (size_t i = 0; i < P_.grid_sets.size() && !done; ++i) {
+        const GridSet& g = P_.grid_sets[i];
+        for (const JTemplate& jt : g.jtemplates) {
+          if (size_t(jt.tmpl) != t) continue;
+          const auto sh = P_.shape_of(g.dom);
+          const int64_t ext = P_.extent_of(g.dom);
+          const std::vector<Real>& buf = hg[i];
+          for (int64_t e = 0; e < ext; ++e) {
+            begin_row();
+            if (buf[size_t(jt.guard_out) * size_t(ext) + size_t(e)] == Real(0)) continue;
+            for (const Lane& l : jt.lanes)
+              push(P_.ubase[size_t(l.field)] + (e + lane_lin(l, sh)) * P_.unknowns[size_t(l.field)].channels +
+                       l.channel,
+                   buf[size_t(l.out) * size_t(ext) + size_t(e)]);
+          }
+          done = true;
+          break;
+        }
+      }
+      for (size_t i = 0; i < P_.graph_sets.size() && !done; ++i) {
+        const GraphSet& g = P_.graph_sets[i];
+        for (const JTemplate& jt : g.jtemplates) {
+          if (size_t(jt.tmpl) != t) continue;
+          const GraphData& gd = graphs_[size_t(g.graph)];
+          const std::vector<Real>& buf = hr[i];
+          std::vector<std::pair<int64_t, Real>> row;
+          for (int64_t e = 0; e < gd.E; ++e) {
+            begin_row();
+            row.clear();
+            for (const Lane& l : jt.lanes)
+              row.emplace_back(P_.ubase[size_t(l.field)] +
+                                   int64_t(gd.verts[size_t(e * gd.arity + l.slot)]) *
+                                       P_.unknowns[size_t(l.field)].channels +
+                                   l.channel,
+                               buf[size_t(l.out) * size_t(gd.E) + size_t(e)]);
+            std::stable_sort(row.begin(), row.end(),
+                             [](const auto& x, const auto& y) { return x.first < y.first; });
+            for (size_t k = 0; k < row.size();) {
+              const int64_t c = row[k].first;
+              Real v = row[k].second;
+              for (++k; k < row.size() && row[k].first == c; ++k) v += row[k].second;
+              push(c, v);
+            }
+          }
+          done = true;
+          break;
+        }
+      }
+    }
+    csr_ok_ = true;
+  }
+
   // Jacobi PCG (pcg.hpp:63-130) as a captured CUDA graph.  (Fusing the
   // direction update into the apply's p staging was measured slower: the
   // apply is issue-bound, the p update streams at HBM speed on its own.)
@@ -1682,7 +2111,7 @@ class Session final : public SessionBase {
     // block (same fixed order, bitwise the same total) and derives alpha /
     // beta itself, removing the atomic + last-block tail from the producers.
     static const bool nocons = std::getenv("MO_B200_NO_CONSUMER") != nullptr;
-    const bool cons = !nocons && !sh_.on && (P_.graph_sets.empty() || vertex_apply_one_pass());
+    const bool cons = !nocons && !sh_.on && !mat_ && (P_.graph_sets.empty() || vertex_apply_one_pass());
     for (int k = 0; k < cfg_.linear_iters; ++k) {
       prof_begin(0);
       consumer_ = cons;

@@ -57,6 +57,11 @@ class SessionBase {
   virtual void* stream() = 0;
   virtual int64_t launches() const = 0;
   virtual std::string apply_kernel(int gather_set) = 0;
+  // linearize / jacobian (solver.hpp:291-382): evaluate the Jacobian lanes on
+  // the device; jacobian() assembles the reference's CSR from them (host).
+  virtual void linearize() = 0;
+  virtual void jacobian(int64_t* rows, int64_t* cols, std::vector<int64_t>* offs, std::vector<int64_t>* col,
+                        std::vector<double>* val) = 0;
   // Strip shards: stored rows [lo, hi), owned rows [row0, row1) (all 0 when unsharded).
   virtual void local_layout(int64_t* lo, int64_t* hi, int64_t* row0, int64_t* row1) const = 0;
 };

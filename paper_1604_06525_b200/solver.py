@@ -164,6 +164,13 @@ class CompiledPlan:
         call("mo_plan_num_cols", self._h, ctypes.byref(n))
         return n.value
 
+    @property
+    def materialize(self) -> int:
+        """Materialize mode compiled into the plan (plan.hpp:17): 0 none, 1 kJ, 2 kJtJ."""
+        m = ctypes.c_int()
+        call("mo_plan_materialize", self._h, ctypes.byref(m))
+        return m.value
+
     def array_size(self, i: int) -> int:
         n = ctypes.c_int64()
         call("mo_plan_array_size", self._h, i, ctypes.byref(n))
@@ -301,6 +308,22 @@ class Solver:
         res = np.empty(v.size, self.dtype) if out is None else out
         call("mo_apply_jtj", self._h, v.ctypes.data, res.ctypes.data, v.size)
         return res
+
+    def linearize(self) -> None:
+        """linearize() (solver.hpp:291-377): Jacobian lanes at x, on the device.
+        Materialize::kJ sessions apply 2 J^T J v from them afterwards."""
+        call("mo_linearize", self._h)
+
+    def jacobian(self):
+        """jacobian() (solver.hpp:378-381) as CSR arrays (offs, col, val) in the
+        reference's row and column order."""
+        rows, cols, nnz = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        call("mo_jacobian_size", self._h, ctypes.byref(rows), ctypes.byref(cols), ctypes.byref(nnz))
+        offs = np.empty(rows.value + 1, np.int64)
+        col = np.empty(nnz.value, np.int64)
+        val = np.empty(nnz.value, self.dtype)
+        call("mo_get_jacobian", self._h, offs.ctypes.data, col.ctypes.data, val.ctypes.data, nnz.value)
+        return offs, col, val
 
     def saw_nonfinite_kernel(self) -> bool:
         v = ctypes.c_int()

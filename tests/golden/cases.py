@@ -111,6 +111,19 @@ def unit_cases():
     C["tri_graph"] = dict(src=K_TRI, x=_r(71, 10), arrays=[_r(72, 5, 0, 1)],
                           graphs=[(3, [0, 1, 2, 1, 2, 3, 4, 0, 2, 2, 2, 4, 3, 3, 1])], cfg=dict(nl=3, lin=6),
                           cmds=["cost", "residuals", "normal", "jtj", "solve"], v=_r(73, 10))
+    # Materialize::kJ (solver.hpp:278-376) and force_evalj linearize / jacobian
+    # (test_solver.cpp:39-77, 103-153, 186-204)
+    lin = ["cost", "normal", "linearize", "jtj", "solve"]
+    C["mat_chain_lanes"] = dict(C["chain"], cfg=dict(nl=1, force_evalj=True), cmds=["normal", "jtj", "linearize"])
+    C["mat_sinchain"] = dict(C["sinchain"], cfg=dict(materialize="j"), cmds=lin)
+    C["mat_sinchain_lm"] = dict(C["sinchain"], cfg=dict(materialize="j", method="lm", nl=4), cmds=lin)
+    C["mat_graph_degenerate"] = dict(C["graph_degenerate"], cfg=dict(materialize="j"), cmds=["cost", "linearize", "jtj", "solve"])
+    C["mat_exclude"] = dict(C["exclude"], cfg=dict(nl=1, materialize="j"), cmds=lin)
+    C["mat_dense"] = dict(C["dense"], cfg=dict(nl=1, materialize="j"), cmds=lin)
+    C["mat_ops"] = dict(C["ops"], cfg=dict(nl=3, lin=8, materialize="j"), cmds=lin)
+    C["mat_ops_f32"] = dict(C["mat_ops"], prec="f32")
+    C["mat_volume"] = dict(C["volume"], cfg=dict(nl=2, materialize="j"), cmds=lin)
+    C["mat_tri_graph"] = dict(C["tri_graph"], cfg=dict(nl=3, lin=6, materialize="j"), cmds=lin)
     for c in C.values():
         c.setdefault("arrays", [])
         c.setdefault("params", [])
@@ -127,4 +140,9 @@ CONFIG_CASES = {
     "cfg_arap_warp": ("arap_warp", dict(W=24, H=20, nhandles=6), dict(nl=3, lin=10, rel=0.0)),
     "cfg_sfs": ("sfs", dict(W=24, H=18), dict(nl=3, lin=10, rel=0.0, method="lm")),
     "cfg_arap_mesh": ("arap_mesh", dict(n=8, nhandles=5), dict(nl=3, lin=10, rel=0.0)),
+    # Materialize::kJ instances
+    "cfg_poisson_mat": ("poisson", dict(W=24, H=20), dict(nl=3, lin=10, rel=0.0, materialize="j")),
+    "cfg_arap_warp_mat": ("arap_warp", dict(W=24, H=20, nhandles=6), dict(nl=3, lin=10, rel=0.0, materialize="j")),
+    "cfg_sfs_mat": ("sfs", dict(W=24, H=18), dict(nl=3, lin=10, rel=0.0, method="lm", materialize="j")),
+    "cfg_arap_mesh_mat": ("arap_mesh", dict(n=8, nhandles=5), dict(nl=3, lin=10, rel=0.0, materialize="j")),
 }

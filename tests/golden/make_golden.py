@@ -27,21 +27,24 @@ from paper_1604_06525_b200.solver import EdgeTable, SolveData  # noqa: E402
 EXPORT = os.path.join(ROOT, "integration", "_build", "export_plan")
 
 
-def export(src_or_path, dims=None):
+def export(src_or_path, dims=None, cfg=None):
     with tempfile.TemporaryDirectory() as td:
         path = pyoracle.energy_path(src_or_path, td)
         cmd = [EXPORT, "--energy", path]
+        if (cfg or {}).get("materialize"):
+            cmd += ["--materialize", cfg["materialize"]]
         for k, v in (dims or {}).items():
             cmd += ["--dim", f"{k}={v}"]
         return subprocess.run(cmd, check=True, capture_output=True, text=True).stdout
 
 
 def run_case(name, src, data, cfg, prec, cmds, v, dims=None, energy=None):
-    plan_text = export(energy or src, dims)
+    plan_text = export(energy or src, dims, cfg)
     with open(os.path.join(HERE, name + ".moplan"), "w") as f:
         f.write(plan_text)
     kw = dict(prec=prec, method=cfg.get("method", "gn"), nl=cfg.get("nl"), lin=cfg.get("lin"),
-              rel=cfg.get("rel"), radius0=cfg.get("radius0"), cost_stop=cfg.get("cost_stop"), v=v, dims=dims)
+              rel=cfg.get("rel"), radius0=cfg.get("radius0"), cost_stop=cfg.get("cost_stop"), v=v, dims=dims,
+              materialize=cfg.get("materialize"), force_evalj=cfg.get("force_evalj", False))
     out = pyoracle.run_ref(energy or src, data, cmds, **kw)
     rec = {"x": np.asarray(data.x, np.float64), "params": np.asarray(data.params, np.float64),
            "prec": np.array(prec), "cfg": np.array(json.dumps(cfg)), "cmds": np.array(",".join(cmds)),
@@ -61,7 +64,10 @@ def run_case(name, src, data, cfg, prec, cmds, v, dims=None, energy=None):
 
 
 def main():
+    only = set(sys.argv[1:])  # optional: regenerate just these case names
     for name, c in unit_cases().items():
+        if only and name not in only:
+            continue
         dt = np.float32 if c["prec"] == "f32" else np.float64
         data = SolveData(x=np.asarray(c["x"], dt), arrays=[np.asarray(a, dt) for a in c["arrays"]],
                          params=c["params"], graphs=[EdgeTable(a, np.asarray(v, np.uint64)) for a, v in c["graphs"]])
@@ -69,11 +75,15 @@ def main():
     for name, (wl, kw, cfg) in CONFIG_CASES.items():
         prob = workloads.CONFIGS[wl](**kw)
         for prec in ("f64", "f32"):
+            if only and f"{name}_{prec}" not in only:
+                continue
             dt = np.float32 if prec == "f32" else np.float64
             data = prob.data(dt)
             v = workloads.uniform(99, data.x.size) - 0.5
-            run_case(f"{name}_{prec}", None, data, cfg, prec, ["cost", "residuals", "normal", "jtj", "solve"],
-                     v.astype(dt), dims=prob.dims, energy=prob.energy)
+            cmds = ["cost", "residuals", "normal", "jtj", "solve"]
+            if cfg.get("materialize"):
+                cmds = ["cost", "residuals", "normal", "linearize", "jtj", "solve"]
+            run_case(f"{name}_{prec}", None, data, cfg, prec, cmds, v.astype(dt), dims=prob.dims, energy=prob.energy)
 
 
 if __name__ == "__main__":

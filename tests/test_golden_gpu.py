@@ -11,11 +11,15 @@ import numpy as np
 import pytest
 
 from helpers import Golden, assert_close_vec, golden_names, rel_close
-from paper_1604_06525_b200 import Solver
+from paper_1604_06525_b200 import MoError, Solver
 
 pytestmark = pytest.mark.gpu
 
 NAMES = golden_names()
+# transcendental-free programs: exact mode reproduces the reference bit for bit
+BITWISE = {"cfg_poisson_f64", "cfg_poisson_f32", "chain", "dense", "volume", "tri_graph", "mat_chain_lanes",
+           "mat_dense", "mat_volume", "mat_tri_graph", "mat_graph_degenerate", "mat_exclude",
+           "cfg_poisson_mat_f64", "cfg_poisson_mat_f32"}
 
 
 def tol(prec):
@@ -27,6 +31,19 @@ def tol(prec):
 @pytest.mark.parametrize("name", NAMES)
 def test_golden_case(name, exact):
     g = Golden(name)
+    err = g.ref("error")
+    if err is None:
+        run_golden(g, exact)
+        return
+    # The reference threw (e.g. linearize's CSR range check): the device must
+    # raise the same Err code from the same routine.
+    code = bytes(err).decode().split(":")[0]
+    with pytest.raises(MoError) as ei:
+        run_golden(g, exact)
+    assert ei.value.code == code, (str(ei.value), bytes(err).decode())
+
+
+def run_golden(g, exact):
     t = tol(g.prec)
     data = g.data()
     s = Solver(g.plan(exact), data)
@@ -34,6 +51,17 @@ def test_golden_case(name, exact):
     assert s.num_rows() == int(g.ref("num_rows")[0])
     np.testing.assert_array_equal(s.excluded(), g.ref("excluded"))
     for cmd in g.cmds:
+        if cmd == "linearize":
+            s.linearize()
+            offs, col, val = s.jacobian()
+            np.testing.assert_array_equal(offs, g.ref("j_offs"))
+            np.testing.assert_array_equal(col, g.ref("j_col"))
+            assert_close_vec(val, g.ref("j_val"), t["vec"], "J values")
+            if exact and g.name in BITWISE:
+                np.testing.assert_array_equal(val, g.ref("j_val"))
+            continue
+        if cmd == "jtj" and exact and g.name in BITWISE:
+            np.testing.assert_array_equal(s.apply_jtj(g.z["v"].astype(g.dtype)), g.ref("jtj"))
         if cmd == "cost":
             c = s.cost()
             assert rel_close(c, float(g.ref("cost")[0]), t["cost"]), (c, g.ref("cost"))
@@ -121,7 +149,7 @@ def test_kernels_bitwise_deterministic(name):
 VARIANTS = ["gather", "twophase", "stream", "tma", "warp", "gprog", "tma4"]
 PREFIX = {"gather": "mo_gather_jtj_", "twophase": "mo_gather_jtj2_", "stream": "mo_gather_jtj3_",
           "tma": "mo_gather_jtj4_", "warp": "mo_gather_jtj5_", "gprog": "mo_gather_jtj6_", "tma4": "mo_gather_jtj7_"}
-GRID = [n for n in NAMES if n.startswith("cfg_") and "mesh" not in n]
+GRID = [n for n in NAMES if n.startswith("cfg_") and "mesh" not in n and "_mat" not in n]
 
 
 @pytest.mark.parametrize("variant", VARIANTS)

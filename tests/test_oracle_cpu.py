@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 from helpers import Golden, golden_names
-from oracle.cref import Oracle
+from oracle.cref import Oracle, OracleError
 
 
 def bits_equal(a, b):
@@ -15,9 +15,23 @@ def bits_equal(a, b):
     return a.shape == b.shape and np.array_equal(a.view(np.uint8), b.view(np.uint8))
 
 
+ERR_RC = {"IndexOutOfRange": 11, "BindError": 15, "InternalError": 18}
+
+
 @pytest.mark.parametrize("name", golden_names())
 def test_oracle_reproduces_reference_bitwise(name):
     g = Golden(name)
+    err = g.ref("error")
+    if err is None:
+        run_oracle(g, name)
+        return
+    # the reference threw: the restatement raises the same Err code
+    with pytest.raises(OracleError) as ei:
+        run_oracle(g, name)
+    assert ei.value.rc == ERR_RC[bytes(err).decode().split(":")[0]], str(ei.value)
+
+
+def run_oracle(g, name):
     plan_text = open(f"{__import__('helpers').GOLDEN}/{name}.moplan").read()
     o = Oracle(plan_text, f64=g.prec == "f64", cfg=g.cfg)
     data = g.data()
@@ -33,6 +47,10 @@ def test_oracle_reproduces_reference_bitwise(name):
         elif cmd == "normal":
             b, m = o.build_normal()
             assert bits_equal(b, g.ref("b")) and bits_equal(m, g.ref("m"))
+        elif cmd == "linearize":
+            offs, col, val = o.linearize()
+            assert bits_equal(offs, g.ref("j_offs")) and bits_equal(col, g.ref("j_col"))
+            assert bits_equal(val, g.ref("j_val"))
         elif cmd == "jtj":
             assert bits_equal(o.apply_jtj(g.z["v"].astype(g.dtype)), g.ref("jtj"))
         elif cmd == "solve":
