@@ -126,8 +126,7 @@ int mo_plan_precompile(mo_plan p, int precision);
  * per-element parity); default 0 lets nvcc contract a*b+c into FMA
  * (results within the fp32 1e-5 / fp64 1e-10 tolerances). */
 int mo_plan_set_exact(mo_plan p, int exact);
-/* Materialize (plan.hpp:17) the plan was compiled for: 0 kNone, 1 kJ, 2 kJtJ
- * (kJtJ sessions are refused with MO_ERR_BIND). */
+/* Materialize (plan.hpp:17) the plan was compiled for: 0 kNone, 1 kJ, 2 kJtJ. */
 int mo_plan_materialize(mo_plan p, int* mode);
 int mo_plan_counts(mo_plan p, int* n_params, int* n_arrays, int* n_graphs, int* n_unknowns);
 int mo_plan_array_size(mo_plan p, int i, int64_t* n_scalars);
@@ -168,7 +167,8 @@ int mo_saw_nonfinite(mo_session s, int* out);               /* :110 */
 /* linearize (solver.hpp:291-377): evaluate the Jacobian lanes at x on the
  * device (plans with Jacobian lanes: materialized or force_evalj).  In
  * Materialize::kJ sessions mo_apply_jtj then computes 2 J^T (J v) in the
- * reference's spmv / spmv_t order (solver.hpp:278-283); before the first
+ * reference's spmv / spmv_t order (solver.hpp:278-283), in kJtJ sessions
+ * spmv(H, v) over the assembled H = 2 J^T J (solver.hpp:284); before the first
  * linearize after a refresh it fails with MO_ERR_INTERNAL like the reference. */
 int mo_linearize(mo_session s);
 /* jacobian() (solver.hpp:378-381): the reference's CSR (rows template-major,
@@ -176,6 +176,11 @@ int mo_linearize(mo_session s);
  * then mo_get_jacobian with offs[rows + 1], col[nnz], val[nnz] (Real). */
 int mo_jacobian_size(mo_session s, int64_t* rows, int64_t* cols, int64_t* nnz);
 int mo_get_jacobian(mo_session s, int64_t* offs, int64_t* col, void* val, int64_t nnz);
+/* normal_matrix() (solver.hpp:383-387): H = 2 J^T J of a Materialize::kJtJ
+ * session, assembled on the device by mo_linearize in the reference's
+ * transpose + spgemm order (sparse.hpp); offs[num_cols + 1], col/val[nnz]. */
+int mo_normal_matrix_size(mo_session s, int64_t* nnz);
+int mo_get_normal_matrix(mo_session s, int64_t* offs, int64_t* col, void* val, int64_t nnz);
 
 /* ---- strip sharding (multi-GPU; no reference counterpart) --
  * A grid plan (one grid domain, no graphs) is split into contiguous strips

@@ -325,6 +325,18 @@ class Solver {
     ok(mo_get_jacobian(s_, J_.offs.data(), J_.col.data(), J_.val.data(), nnz));
   }
   const SparseCSR<Real>& jacobian() const { return J_; }
+  // normal_matrix() (solver.hpp:383-387): kJtJ sessions
+  const SparseCSR<Real>& normal_matrix() {
+    int64_t nnz = 0;
+    ok(mo_normal_matrix_size(s_, &nnz));
+    H_ = SparseCSR<Real>{};
+    H_.rows = H_.cols = num_cols();
+    H_.offs.resize(size_t(H_.rows) + 1);
+    H_.col.resize(size_t(nnz));
+    H_.val.resize(size_t(nnz));
+    ok(mo_get_normal_matrix(s_, H_.offs.data(), H_.col.data(), H_.val.data(), nnz));
+    return H_;
+  }
 
   SolveResult solve(const std::function<void(int, SolveData<Real>&)>& callback = {}) {
     cb_ = &callback;
@@ -370,7 +382,7 @@ class Solver {
   mo_session s_ = nullptr;
   std::vector<Real> b_, m_;
   std::vector<uint8_t> excl_;
-  SparseCSR<Real> J_;
+  SparseCSR<Real> J_, H_;
   const std::function<void(int, SolveData<Real>&)>* cb_ = nullptr;
 };
 

@@ -85,8 +85,8 @@ static void two_pixel_jacobian() {
   CHECK((j.val == std::vector<double>{1.0, 1.0, 1.0, -1.0}));
 }
 
-// test_solver.cpp:103-153 (kJtJ is refused by the device path; kJ and the
-// matrix-free apply must agree, and deliver the same iterates)
+// test_solver.cpp:103-153: kJ, kJtJ and the matrix-free apply agree and
+// deliver the same iterates
 static void materialized_agrees() {
   const char* src = R"(
 dim W 9
@@ -105,9 +105,9 @@ energy 0.5 * (X(0) - X(1))
     cfg.materialize = mode;
     return plan(compile_source(src), cfg);
   };
-  CompiledPlan pn = make(Materialize::kNone), pj = make(Materialize::kJ);
-  SolveData<double> dn = chain_data<double>(x0, a0), dj = chain_data<double>(x0, a0);
-  Solver<double> sn(pn, dn), sj(pj, dj);
+  CompiledPlan pn = make(Materialize::kNone), pj = make(Materialize::kJ), ph = make(Materialize::kJtJ);
+  SolveData<double> dn = chain_data<double>(x0, a0), dj = chain_data<double>(x0, a0), dh = chain_data<double>(x0, a0);
+  Solver<double> sn(pn, dn), sj(pj, dj), sh(ph, dh);
   bool threw = false;
   std::vector<double> probe(9, 1.0), pout(9);
   try {
@@ -117,25 +117,27 @@ energy 0.5 * (X(0) - X(1))
   }
   CHECK(threw);
   sj.linearize();
+  sh.linearize();
   for (int trial = 0; trial < 10; ++trial) {
-    std::vector<double> v(9), on(9), oj(9);
+    std::vector<double> v(9), on(9), oj(9), oh(9);
     for (auto& e : v) e = u(rng);
     sn.apply_jtj(v, on);
     sj.apply_jtj(v, oj);
-    for (int i = 0; i < 9; ++i) CHECK(std::fabs(oj[i] - on[i]) <= 1e-12);
+    sh.apply_jtj(v, oh);
+    for (int i = 0; i < 9; ++i) {
+      CHECK(std::fabs(oj[i] - on[i]) <= 1e-12);
+      CHECK(std::fabs(oh[i] - on[i]) <= 1e-12);
+    }
   }
-  SolveResult rn = sn.solve(), rj = sj.solve();
+  const SparseCSR<double>& h = sh.normal_matrix();
+  CHECK(h.rows == 9 && h.offs.size() == 10 && h.nnz() == 25);  // tridiagonal 9x9
+  SolveResult rn = sn.solve(), rj = sj.solve(), rh = sh.solve();
   CHECK(approx(rn.final_cost, rj.final_cost, 1e-10));
-  for (int i = 0; i < 9; ++i) CHECK(std::fabs(dj.x[i] - dn.x[i]) <= 1e-8);
-  bool refused = false;
-  try {
-    CompiledPlan ph = make(Materialize::kJtJ);
-    SolveData<double> dh = chain_data<double>(x0, a0);
-    Solver<double> sh(ph, dh);
-  } catch (const Error& e) {
-    refused = e.code() == Err::kBindError;
+  CHECK(approx(rn.final_cost, rh.final_cost, 1e-10));
+  for (int i = 0; i < 9; ++i) {
+    CHECK(std::fabs(dj.x[i] - dn.x[i]) <= 1e-8);
+    CHECK(std::fabs(dh.x[i] - dn.x[i]) <= 1e-8);
   }
-  CHECK(refused);
 }
 
 // test_solver.cpp:186-204

@@ -158,3 +158,14 @@ class Oracle:
         ptr = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
         self._chk(self.lib.moo_jacobian(self.h, ctypes.byref(rows), ctypes.byref(nnz), ptr(offs), ptr(col), ptr(val)))
         return offs, col, val
+
+    def normal_matrix(self):
+        """normal_matrix() (solver.hpp:383-387) of a kJtJ plan: CSR (offs, col, val)."""
+        nnz = ctypes.c_int64()
+        self._chk(self.lib.moo_normal_matrix(self.h, ctypes.byref(nnz), None, None, None))
+        offs = np.zeros(self.num_cols() + 1, np.int64)
+        col = np.zeros(nnz.value, np.int64)
+        val = np.zeros(nnz.value, self.dtype)
+        ptr = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+        self._chk(self.lib.moo_normal_matrix(self.h, ctypes.byref(nnz), ptr(offs), ptr(col), ptr(val)))
+        return offs, col, val

@@ -131,6 +131,10 @@ struct moo {
   int64_t* jcol;
   void* jval;
   int64_t jnnz, jcap;
+  int64_t* hoffs; /* kJtJ: CSR of H = 2 J^T J */
+  int64_t* hcol;
+  void* hval;
+  int64_t hnnz;
 };
 
 static char g_err[512];
@@ -593,6 +597,9 @@ void moo_destroy(moo* o) {
   free(o->joffs);
   free(o->jcol);
   free(o->jval);
+  free(o->hoffs);
+  free(o->hcol);
+  free(o->hval);
   for (int i = 0; i < o->nck; ++i) freeprog(&o->ck[i].prog);
   for (int i = 0; i < o->nek; ++i) freeprog(&o->ek[i].prog);
   free(o->gs);
@@ -768,6 +775,14 @@ int moo_linearize(moo* o) {
   int rc = validate(o);
   if (rc) return rc;
   return o->f64 ? linearize_d(o) : linearize_f(o);
+}
+int moo_normal_matrix(moo* o, int64_t* nnz, int64_t* offs, int64_t* col, void* val) {
+  if (!o->jvalid || o->materialize != 2) return err(E_BIND, "no normal matrix has been assembled");
+  *nnz = o->hnnz;
+  if (offs) memcpy(offs, o->hoffs, (size_t)(o->num_cols + 1) * sizeof(int64_t));
+  if (col) memcpy(col, o->hcol, (size_t)o->hnnz * sizeof(int64_t));
+  if (val) memcpy(val, o->hval, (size_t)o->hnnz * RSZ(o));
+  return 0;
 }
 int moo_jacobian(moo* o, int64_t* rows, int64_t* nnz, int64_t* offs, int64_t* col, void* val) {
   if (!o->jvalid) return err(E_BIND, "no Jacobian has been materialized");

@@ -58,5 +58,7 @@ int moo_get_x(moo* o, void* out);
  * apply 2 J^T (J v) through spmv / spmv_t (sparse.hpp). */
 int moo_linearize(moo* o);
 int moo_jacobian(moo* o, int64_t* rows, int64_t* nnz, int64_t* offs, int64_t* col, void* val);
+/* normal_matrix() (solver.hpp:383-387): H = 2 J^T J of a kJtJ plan, CSR */
+int moo_normal_matrix(moo* o, int64_t* nnz, int64_t* offs, int64_t* col, void* val);
 
 #endif

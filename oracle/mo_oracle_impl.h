@@ -353,6 +353,78 @@ static void F(build_normal)(moo* o) {
   }
 }
 
+/* H = 2 J^T J (solver.hpp:370-374): transpose by counting sort, Gustavson
+ * spgemm with a dense accumulator (rows of J^T in order, touched columns
+ * sorted), scale_inplace (sparse.hpp). */
+static int F(cmp_i64)(const void* a, const void* b) {
+  int64_t x = *(const int64_t*)a, y = *(const int64_t*)b;
+  return x < y ? -1 : x > y;
+}
+static void F(assemble_h)(moo* o) {
+  const int64_t n = o->num_cols, nnz = o->jnnz;
+  const REAL* jv = (const REAL*)o->jval;
+  int64_t* toffs = (int64_t*)calloc((size_t)n + 1, sizeof(int64_t));
+  int64_t* tcol = (int64_t*)malloc((size_t)nnz * sizeof(int64_t) + 8);
+  REAL* tval = (REAL*)malloc((size_t)nnz * sizeof(REAL) + 8);
+  for (int64_t k = 0; k < nnz; ++k) ++toffs[o->jcol[k] + 1];
+  for (int64_t i = 0; i < n; ++i) toffs[i + 1] += toffs[i];
+  int64_t* cur = (int64_t*)malloc((size_t)n * sizeof(int64_t) + 8);
+  memcpy(cur, toffs, (size_t)n * sizeof(int64_t));
+  for (int64_t r = 0; r < o->rows; ++r)
+    for (int64_t k = o->joffs[r]; k < o->joffs[r + 1]; ++k) {
+      int64_t d = cur[o->jcol[k]]++;
+      tcol[d] = r;
+      tval[d] = jv[k];
+    }
+  REAL* acc = (REAL*)calloc((size_t)n + 1, sizeof(REAL));
+  char* used = (char*)calloc((size_t)n + 1, 1);
+  int64_t* touched = (int64_t*)malloc((size_t)n * sizeof(int64_t) + 8);
+  free(o->hoffs);
+  free(o->hcol);
+  free(o->hval);
+  o->hoffs = (int64_t*)calloc((size_t)n + 1, sizeof(int64_t));
+  int64_t cap = 1024, hn = 0;
+  o->hcol = (int64_t*)malloc((size_t)cap * sizeof(int64_t));
+  o->hval = malloc((size_t)cap * sizeof(REAL));
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t nt = 0;
+    for (int64_t ka = toffs[i]; ka < toffs[i + 1]; ++ka) {
+      int64_t mid = tcol[ka];
+      REAL av = tval[ka];
+      for (int64_t kb = o->joffs[mid]; kb < o->joffs[mid + 1]; ++kb) {
+        int64_t cc = o->jcol[kb];
+        if (!used[cc]) {
+          used[cc] = 1;
+          acc[cc] = (REAL)0;
+          touched[nt++] = cc;
+        }
+        acc[cc] += av * jv[kb];
+      }
+    }
+    qsort(touched, (size_t)nt, sizeof(int64_t), F(cmp_i64));
+    for (int64_t k = 0; k < nt; ++k) {
+      if (hn == cap) {
+        cap *= 2;
+        o->hcol = (int64_t*)realloc(o->hcol, (size_t)cap * sizeof(int64_t));
+        o->hval = realloc(o->hval, (size_t)cap * sizeof(REAL));
+      }
+      o->hcol[hn] = touched[k];
+      ((REAL*)o->hval)[hn] = acc[touched[k]] * (REAL)2;
+      ++hn;
+      used[touched[k]] = 0;
+    }
+    o->hoffs[i + 1] = hn;
+  }
+  o->hnnz = hn;
+  free(toffs);
+  free(tcol);
+  free(tval);
+  free(cur);
+  free(acc);
+  free(used);
+  free(touched);
+}
+
 /* linearize (solver.hpp:291-376): evalj lanes per template set, then the
  * CSR of J with the SparseCSR push checks (sparse.hpp:30-37). */
 static int F(jpush)(moo* o, int64_t c, REAL v) {
@@ -461,6 +533,7 @@ static int F(linearize)(moo* o) {
     free(lg[i]);
     free(lh[i]);
   }
+  if (!rc && o->materialize == 2) F(assemble_h)(o);
   o->jvalid = rc == 0;
   return rc;
 }
@@ -493,6 +566,15 @@ static int F(apply_jtj)(moo* o, const REAL* v, REAL* out) {
       free(S->jtmp);
       S->jtmp = (REAL*)calloc((size_t)o->rows, sizeof(REAL));
       S->jtmp_cap = o->rows;
+    }
+    if (o->materialize == 2) { /* spmv(H, v) */
+      const REAL* hv = (const REAL*)o->hval;
+      for (int64_t i = 0; i < o->num_cols; ++i) {
+        REAL acc = (REAL)0;
+        for (int64_t k = o->hoffs[i]; k < o->hoffs[i + 1]; ++k) acc += hv[k] * v[o->hcol[k]];
+        out[i] = acc;
+      }
+      return 0;
     }
     F(apply_materialized)(o, v, out);
     return 0;

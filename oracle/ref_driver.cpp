@@ -198,6 +198,12 @@ int run(const Args& a, const CompiledPlan& P) {
         mob_put(&w, "j_offs", MOB_I64, j.offs.data(), j.offs.size());
         mob_put(&w, "j_col", MOB_I64, j.col.data(), j.col.size());
         mob_put(&w, "j_val", RD, j.val.data(), j.val.size());
+        if (a.cfg.materialize == Materialize::kJtJ) {
+          const SparseCSR<Real>& h = s.normal_matrix();
+          mob_put(&w, "h_offs", MOB_I64, h.offs.data(), h.offs.size());
+          mob_put(&w, "h_col", MOB_I64, h.col.data(), h.col.size());
+          mob_put(&w, "h_val", RD, h.val.data(), h.val.size());
+        }
       } else if (c == "jtj") {
         std::vector<Real> v = get_real<Real>(in, "v");
         std::vector<Real> out(static_cast<size_t>(ncols));

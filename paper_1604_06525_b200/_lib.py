@@ -99,6 +99,8 @@ SIGNATURES = {
     "mo_linearize": (c_int, [c_void_p]),
     "mo_jacobian_size": (c_int, [c_void_p] + [ctypes.POINTER(c_int64)] * 3),
     "mo_get_jacobian": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64]),
+    "mo_normal_matrix_size": (c_int, [c_void_p, ctypes.POINTER(c_int64)]),
+    "mo_get_normal_matrix": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64]),
 }
 
 for _name, (_res, _args) in SIGNATURES.items():

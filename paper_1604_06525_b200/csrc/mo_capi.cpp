@@ -410,6 +410,32 @@ int mo_get_jacobian(mo_session s, int64_t* offs, int64_t* col, void* val, int64_
   });
 }
 
+int mo_normal_matrix_size(mo_session s, int64_t* nnz) {
+  SESSION_CALL({
+    need(nnz, "output");
+    std::vector<int64_t> o, c;
+    std::vector<double> v;
+    s->impl->normal_matrix(&o, &c, &v);
+    *nnz = int64_t(c.size());
+  });
+}
+int mo_get_normal_matrix(mo_session s, int64_t* offs, int64_t* col, void* val, int64_t nnz) {
+  SESSION_CALL({
+    std::vector<int64_t> o, c;
+    std::vector<double> v;
+    s->impl->normal_matrix(&o, &c, &v);
+    mo::check(nnz == int64_t(c.size()), mo::Err::kShapeMismatch, "normal_matrix(): nnz does not match");
+    if (offs) std::memcpy(offs, o.data(), o.size() * sizeof(int64_t));
+    if (col && !c.empty()) std::memcpy(col, c.data(), c.size() * sizeof(int64_t));
+    if (val) {
+      if (s->f32)
+        for (size_t k = 0; k < v.size(); ++k) static_cast<float*>(val)[k] = float(v[k]);
+      else if (!v.empty())
+        std::memcpy(val, v.data(), v.size() * sizeof(double));
+    }
+  });
+}
+
 int mo_apply_kernel(mo_session s, int gather_set, char* name, size_t len) {
   SESSION_CALL(need(name, "output"); const std::string k = s->impl->apply_kernel(gather_set);
                mo::check(len > k.size(), mo::Err::kShapeMismatch, "name buffer too small");

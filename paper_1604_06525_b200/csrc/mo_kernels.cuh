@@ -557,4 +557,139 @@ k_mat_cols(const __grid_constant__ mo_mat_tables T, const mo_state* st, int skip
   }
 }
 
+// Materialize::kJtJ (solver.hpp:370-374; sparse.hpp transpose + spgemm +
+// scale_inplace): row q of H = 2 J^T J, one thread per column q.  Rows r of
+// J holding q are visited in ascending order (transpose's row order), each
+// row's entries in column order, H[q][j] accumulating a * b from 0 exactly
+// as Gustavson's dense accumulator does; the row is then emitted in column
+// order (slot-major ELL: slot k of column q at k * ncols + q) and doubled.
+template <class Real>
+__device__ __forceinline__ void mo_h_acc(long long* cols, Real* vals, int& n, int K, long long j, Real p, int& bad) {
+  for (int k = 0; k < n; ++k)
+    if (cols[k] == j) {
+      vals[k] = mo_add_rn(vals[k], p);
+      return;
+    }
+  if (n == K) {
+    bad |= 4;
+    return;
+  }
+  cols[n] = j;
+  vals[n] = mo_add_rn(Real(0), p);
+  ++n;
+}
+#define MO_MAT_MAXK 64
+template <class Real>
+__global__ void __launch_bounds__(128)
+k_mat_hbuild(const __grid_constant__ mo_mat_tables T, mo_state* st, int K, long long* __restrict__ hcol,
+             Real* __restrict__ hval, int* __restrict__ hcnt) {
+  MO_PDL_ENTRY();
+  int bad = 0;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < T.ncols;
+       q += (long long)gridDim.x * blockDim.x) {
+    long long cols[MO_MAT_MAXK];
+    Real vals[MO_MAT_MAXK];
+    int n = 0;
+    int f = 0;
+    while (f + 1 < T.nfields && T.ubase[f + 1] <= q) ++f;
+    const long long rel = q - T.ubase[f];
+    const long long el = rel / T.chans[f];
+    const int ch = int(rel - el * T.chans[f]);
+    const int kk = T.cbase[f] + ch;
+    for (int c = T.ceptr[kk]; c < T.ceptr[kk + 1]; ++c) {
+      const mo_mat_centry E = T.ce[c];
+      const mo_mat_tmpl& M = T.tm[E.t];
+      const Real* buf = static_cast<const Real*>(M.buf);
+      if (E.lane >= 0) {
+        const mo_mat_lane L = T.lanes[E.lane];
+        const long long e = el - L.lin;
+        if (e < 0 || e >= M.nrows) continue;
+        if (buf[(long long)M.guard * M.nrows + e] == Real(0)) continue;
+        const Real a = buf[(long long)L.out * M.nrows + e];
+        for (int l = 0; l < M.nlanes; ++l) {
+          const mo_mat_lane B = T.lanes[M.lane0 + l];
+          const long long e2 = e + B.lin;
+          if (e2 < 0 || e2 >= M.nrows) continue;
+          mo_h_acc(cols, vals, n, K, T.ubase[B.field] + e2 * T.chans[B.field] + B.ch,
+                   mo_mul_rn(a, buf[(long long)B.out * M.nrows + e]), bad);
+        }
+      } else {
+        if (el >= M.nverts) continue;
+        for (int j = M.vptr[el]; j < M.vptr[el + 1]; ++j) {
+          const int e = M.vedge[j];
+          long long rc[MO_MAT_MAXL];
+          Real rv[MO_MAT_MAXL];
+          int rn = 0;
+          for (int l = 0; l < M.nlanes; ++l) {  // the row's entries, sorted (stable) and merged below
+            const mo_mat_lane B = T.lanes[M.lane0 + l];
+            const long long col =
+                T.ubase[B.field] + (long long)M.verts[(long long)e * M.arity + B.slot] * T.chans[B.field] + B.ch;
+            const Real val = buf[(long long)B.out * M.nrows + e];
+            int x = rn++;
+            while (x > 0 && rc[x - 1] > col) {
+              rc[x] = rc[x - 1];
+              rv[x] = rv[x - 1];
+              --x;
+            }
+            rc[x] = col;
+            rv[x] = val;
+          }
+          int w = 0;
+          for (int k = 0; k < rn;) {
+            const long long col = rc[k];
+            Real mv = rv[k];
+            for (++k; k < rn && rc[k] == col; ++k) mv = mo_add_rn(mv, rv[k]);
+            rc[w] = col;
+            rv[w] = mv;
+            ++w;
+          }
+          Real a = Real(0);
+          bool has = false;
+          for (int k = 0; k < w; ++k)
+            if (rc[k] == q) {
+              a = rv[k];
+              has = true;
+            }
+          if (!has) continue;
+          for (int k = 0; k < w; ++k) mo_h_acc(cols, vals, n, K, rc[k], mo_mul_rn(a, rv[k]), bad);
+        }
+      }
+    }
+    for (int k = 1; k < n; ++k) {  // emit in column order
+      const long long cc = cols[k];
+      const Real vv = vals[k];
+      int x = k;
+      while (x > 0 && cols[x - 1] > cc) {
+        cols[x] = cols[x - 1];
+        vals[x] = vals[x - 1];
+        --x;
+      }
+      cols[x] = cc;
+      vals[x] = vv;
+    }
+    hcnt[q] = n;
+    for (int k = 0; k < n; ++k) {  // slot-major ELL: coalesced in the apply
+      hcol[k * T.ncols + q] = cols[k];
+      hval[k * T.ncols + q] = mo_mul_rn(vals[k], Real(2));
+    }
+  }
+  if (bad) atomicOr(&st->mat_bad, bad);
+}
+
+// spmv(H, v) (sparse.hpp spmv): out[q] = sum over row q in column order.
+template <class Real>
+__global__ void __launch_bounds__(MO_THREADS)
+k_mat_happly(long long n, int K, const long long* __restrict__ hcol, const Real* __restrict__ hval,
+             const int* __restrict__ hcnt, const mo_state* st, int skipdone, const Real* __restrict__ v,
+             Real* __restrict__ out) {
+  MO_PDL_ENTRY();
+  if (skipdone && st->done) return;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n; q += (long long)gridDim.x * blockDim.x) {
+    Real acc = Real(0);
+    const int c = hcnt[q];
+    for (int k = 0; k < c; ++k) acc = mo_add_rn(acc, mo_mul_rn(hval[k * n + q], v[hcol[k * n + q]]));
+    out[q] = acc;
+  }
+}
+
 }  // namespace mo

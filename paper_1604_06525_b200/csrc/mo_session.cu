@@ -22,6 +22,8 @@
 #include <functional>
 #include <map>
 #include <mutex>
+#include <set>
+#include <tuple>
 #include <limits>
 #include <string>
 
@@ -84,7 +86,6 @@ class Session final : public SessionBase {
     cfg_ = P_.cfg;
     if (cfg_.pcg_rel_tol < 0) cfg_.pcg_rel_tol = cfg_.precision == 0 ? 1e-4 : 1e-8;
     mat_ = P_.cfg.materialize;
-    check(mat_ != 2, Err::kBindError, "Materialize::kJtJ is not supported by the device path (kJ and kNone are)");
     check(!mat_ || !comm_, Err::kBindError, "materialized plans cannot be strip-sharded");
 
     // JIT the plan's per-element kernels (plan time; cached on disk).
@@ -200,6 +201,9 @@ class Session final : public SessionBase {
     for (int* p : mat_vedge_) cudaFree(p);
     for (void* p : mt_bufs_) cudaFree(p);
     cudaFree(jtmp_);
+    cudaFree(hcol_);
+    cudaFree(hval_);
+    cudaFree(hcnt_);
     for (auto& kv : stage_ev_)
       for (auto& ev : kv.second) {
         cudaEventDestroy(ev.a);
@@ -965,6 +969,11 @@ class Session final : public SessionBase {
   mo_mat_tables mt_{};
   Real* jtmp_ = nullptr;
   size_t jtmp_cap_ = 0;
+  long long* hcol_ = nullptr;  // kJtJ: H = 2 J^T J, slot-major ELL
+  Real* hval_ = nullptr;
+  int* hcnt_ = nullptr;
+  int hK_ = 0;
+  size_t hn_ = 0;
   std::vector<int64_t> csr_offs_, csr_col_;
   std::vector<Real> csr_val_;
 
@@ -1736,6 +1745,33 @@ class Session final : public SessionBase {
   void check_mat_bad() {
     if (state_h_->mat_bad & 1) fail(Err::kIndexOutOfRange, "CSR column out of range");
     if (state_h_->mat_bad & 2) fail(Err::kInternal, "CSR row entries must arrive in increasing column order");
+    if (state_h_->mat_bad & 4) fail(Err::kInternal, "normal matrix row exceeds its assembled width");
+  }
+  // max over vertices of |union of the columns of the edge rows incident to it|
+  size_t graph_row_union(const std::vector<uint64_t>& verts, int64_t E, int arity, long long nv,
+                         const std::vector<const JTemplate*>& jts) const {
+    std::vector<int> deg(size_t(nv) + 1, 0), edge_of;
+    for (int64_t e = 0; e < E; ++e)
+      for (int k = 0; k < arity; ++k) deg[size_t(verts[size_t(e * arity + k)]) + 1] += 1;
+    for (size_t i = 0; i < size_t(nv); ++i) deg[i + 1] += deg[i];
+    edge_of.resize(size_t(deg[size_t(nv)]));
+    std::vector<int> pos(deg.begin(), deg.end() - 1);
+    for (int64_t e = 0; e < E; ++e)
+      for (int k = 0; k < arity; ++k) edge_of[size_t(pos[size_t(verts[size_t(e * arity + k)])]++)] = int(e);
+    size_t best = 0;
+    std::set<long long> cols;
+    for (size_t vtx = 0; vtx < size_t(nv); ++vtx) {
+      cols.clear();
+      for (int k = deg[vtx]; k < deg[vtx + 1]; ++k) {
+        const int64_t e = edge_of[size_t(k)];
+        for (const JTemplate* jt : jts)
+          for (const Lane& l : jt->lanes)
+            cols.insert(P_.ubase[size_t(l.field)] +
+                        (long long)verts[size_t(e * arity + l.slot)] * P_.unknowns[size_t(l.field)].channels + l.channel);
+      }
+      best = std::max(best, cols.size());
+    }
+    return best;
   }
   static std::vector<long long> lane_rowbase(size_t nout, long long n) {
     std::vector<long long> rb(std::max<size_t>(nout, 1));
@@ -1913,6 +1949,45 @@ class Session final : public SessionBase {
     mt_.nfields = int(P_.unknowns.size());
     mt_.nrows = rows_;
     mt_.ncols = P_.num_cols;
+    if (mat_ == 2) {  // ELL width of H = 2 J^T J: an upper bound on the row widths
+      std::vector<std::set<std::tuple<int, int, long long>>> S(size_t(cbase.back()));
+      for (size_t t = 0; t < NT; ++t) {
+        const mo_mat_tmpl& M = tm[t];
+        if (M.kind != 0) continue;
+        for (int a = 0; a < M.nlanes; ++a) {
+          const mo_mat_lane& A = lanes[size_t(M.lane0 + a)];
+          for (int b = 0; b < M.nlanes; ++b) {
+            const mo_mat_lane& B = lanes[size_t(M.lane0 + b)];
+            S[size_t(cbase[size_t(A.field)] + A.ch)].insert({B.field, B.ch, B.lin - A.lin});
+          }
+        }
+      }
+      size_t K = 0;
+      for (auto& x : S) K = std::max(K, x.size());
+      for (size_t gi = 0; gi < graphs_.size(); ++gi) {  // per vertex: columns of the incident rows
+        const GraphData& g = graphs_[gi];
+        std::vector<const JTemplate*> jts;
+        for (const GraphSet& gs : P_.graph_sets)
+          if (gs.graph == int(gi))
+            for (const JTemplate& jt : gs.jtemplates) jts.push_back(&jt);
+        if (jts.empty()) continue;
+        K += graph_row_union(g.verts, g.E, g.arity, mat_nverts_[gi], jts);
+      }
+      K = std::max<size_t>(K, 1);
+      check(K <= MO_MAT_MAXK, Err::kBindError, "normal matrix rows too wide for the device's assembled H (kJtJ)");
+      const size_t n = size_t(P_.num_cols);
+      if (int(K) != hK_ || n != hn_) {
+        cudaFree(hcol_);
+        cudaFree(hval_);
+        cudaFree(hcnt_);
+        hcol_ = dalloc<long long>(K * n + 1);
+        hval_ = dalloc<Real>(K * n + 1);
+        hcnt_ = dalloc<int>(n + 1);
+        hK_ = int(K);
+        hn_ = n;
+        realloc = true;
+      }
+    }
     CK(cudaStreamSynchronize(st_));
     if (realloc || mt_ok_) invalidate_graphs();  // captured stages hold the old pointers
     mt_rowbase_ = rowbase_;
@@ -1941,6 +2016,7 @@ class Session final : public SessionBase {
       kl(k_mat_check<Real>, dim3(vgrid(rows_, nsm_)), dim3(MO_THREADS), mt_, state_);
       ++launches_;
     }
+    bool pending_h = mat_ == 2;
     for (size_t i = 0; i < P_.graph_sets.size(); ++i) {
       const GraphSet& g = P_.graph_sets[i];
       if (g.jtemplates.empty() || graphs_[size_t(g.graph)].E == 0) continue;
@@ -1954,6 +2030,12 @@ class Session final : public SessionBase {
       klc(f, dim3(unsigned(std::max<long long>(nb, 1))), dim3(MO_THREADS), args, 0);
       ++launches_;
     }
+    if (pending_h && mt_ok_) {  // assemble H = 2 J^T J (solver.hpp:370-374)
+      const long long n = P_.num_cols;
+      kl(k_mat_hbuild<Real>, dim3(unsigned(std::max<long long>(1, std::min<long long>((n + 127) / 128, 8LL * nsm_)))),
+         dim3(128), mt_, state_, hK_, hcol_, hval_, hcnt_);
+      ++launches_;
+    }
     jvalid_ = true;
   }
   // apply_jtj, materialized branch (solver.hpp:278-283) + apply_damped's
@@ -1962,14 +2044,21 @@ class Session final : public SessionBase {
     check(jvalid_, Err::kInternal, "normal-matrix apply before linearize()");
     const long long n = P_.num_cols;
     const int skip = (flags & MO_F_SKIPDONE) ? 1 : 0;
-    if (rows_ > 0) {
-      kl(k_mat_rows<Real>, dim3(vgrid(rows_, nsm_)), dim3(MO_THREADS), mt_, static_cast<const mo_state*>(state_), skip,
-         pv, jtmp_);
+    if (mat_ == 2) {  // spmv(H, v) (solver.hpp:284)
+      kl(k_mat_happly<Real>, dim3(vgrid(n, nsm_)), dim3(MO_THREADS), n, hK_, static_cast<const long long*>(hcol_),
+         static_cast<const Real*>(hval_), static_cast<const int*>(hcnt_), static_cast<const mo_state*>(state_), skip, pv,
+         out);
+      ++launches_;
+    } else {
+      if (rows_ > 0) {
+        kl(k_mat_rows<Real>, dim3(vgrid(rows_, nsm_)), dim3(MO_THREADS), mt_, static_cast<const mo_state*>(state_),
+           skip, pv, jtmp_);
+        ++launches_;
+      }
+      kl(k_mat_cols<Real>, dim3(vgrid(n, nsm_)), dim3(MO_THREADS), mt_, static_cast<const mo_state*>(state_), skip,
+         static_cast<const Real*>(jtmp_), out);
       ++launches_;
     }
-    kl(k_mat_cols<Real>, dim3(vgrid(n, nsm_)), dim3(MO_THREADS), mt_, static_cast<const mo_state*>(state_), skip,
-       static_cast<const Real*>(jtmp_), out);
-    ++launches_;
     apply_parts_ = vgrid(n, nsm_);
     if (flags & (MO_F_DAMP | MO_F_REDUCE | MO_F_ZEROEXCL)) {
       kl(k_apply_finish<Real>, dim3(vgrid(n, nsm_)), dim3(MO_THREADS), red(0, vgrid(n, nsm_), MO_FIN_PCG_ALPHA, 0), n,
@@ -1999,6 +2088,30 @@ class Session final : public SessionBase {
     if (offs) *offs = csr_offs_;
     if (col) *col = csr_col_;
     if (val) val->assign(csr_val_.begin(), csr_val_.end());
+  }
+
+  void normal_matrix(std::vector<int64_t>* offs, std::vector<int64_t>* col, std::vector<double>* val) override {
+    check(jvalid_ && mat_ == 2, Err::kBindError, "no normal matrix has been assembled");
+    const size_t n = size_t(P_.num_cols), K = size_t(hK_);
+    std::vector<int> cnt(n);
+    std::vector<long long> hc(K * n);
+    std::vector<Real> hv(K * n);
+    if (n) {
+      CK(cudaMemcpyAsync(cnt.data(), hcnt_, n * sizeof(int), cudaMemcpyDeviceToHost, st_));
+      CK(cudaMemcpyAsync(hc.data(), hcol_, K * n * sizeof(long long), cudaMemcpyDeviceToHost, st_));
+      CK(cudaMemcpyAsync(hv.data(), hval_, K * n * sizeof(Real), cudaMemcpyDeviceToHost, st_));
+    }
+    CK(cudaStreamSynchronize(st_));
+    offs->assign(1, 0);
+    col->clear();
+    val->clear();
+    for (size_t q = 0; q < n; ++q) {
+      for (int k = 0; k < cnt[q]; ++k) {
+        col->push_back(hc[size_t(k) * n + q]);
+        val->push_back(double(hv[size_t(k) * n + q]));
+      }
+      offs->push_back(int64_t(col->size()));
+    }
   }
 
  private:

@@ -62,6 +62,8 @@ class SessionBase {
   virtual void linearize() = 0;
   virtual void jacobian(int64_t* rows, int64_t* cols, std::vector<int64_t>* offs, std::vector<int64_t>* col,
                         std::vector<double>* val) = 0;
+  // normal_matrix() (solver.hpp:383-387) of a Materialize::kJtJ session, CSR.
+  virtual void normal_matrix(std::vector<int64_t>* offs, std::vector<int64_t>* col, std::vector<double>* val) = 0;
   // Strip shards: stored rows [lo, hi), owned rows [row0, row1) (all 0 when unsharded).
   virtual void local_layout(int64_t* lo, int64_t* hi, int64_t* row0, int64_t* row1) const = 0;
 };

@@ -325,6 +325,16 @@ class Solver:
         call("mo_get_jacobian", self._h, offs.ctypes.data, col.ctypes.data, val.ctypes.data, nnz.value)
         return offs, col, val
 
+    def normal_matrix(self):
+        """normal_matrix() (solver.hpp:383-387) of a kJtJ session: CSR (offs, col, val)."""
+        nnz = ctypes.c_int64()
+        call("mo_normal_matrix_size", self._h, ctypes.byref(nnz))
+        offs = np.empty(self.num_cols() + 1, np.int64)
+        col = np.empty(nnz.value, np.int64)
+        val = np.empty(nnz.value, self.dtype)
+        call("mo_get_normal_matrix", self._h, offs.ctypes.data, col.ctypes.data, val.ctypes.data, nnz.value)
+        return offs, col, val
+
     def saw_nonfinite_kernel(self) -> bool:
         v = ctypes.c_int()
         call("mo_saw_nonfinite", self._h, ctypes.byref(v))

@@ -124,6 +124,12 @@ def unit_cases():
     C["mat_ops_f32"] = dict(C["mat_ops"], prec="f32")
     C["mat_volume"] = dict(C["volume"], cfg=dict(nl=2, materialize="j"), cmds=lin)
     C["mat_tri_graph"] = dict(C["tri_graph"], cfg=dict(nl=3, lin=6, materialize="j"), cmds=lin)
+    # Materialize::kJtJ (H = 2 J^T J assembled, solver.hpp:370-374)
+    for k in ("sinchain", "sinchain_lm", "graph_degenerate", "exclude", "dense", "ops", "ops_f32", "volume",
+              "tri_graph"):
+        c = dict(C["mat_" + k])
+        c["cfg"] = dict(c["cfg"], materialize="jtj")
+        C["math_" + k] = c
     for c in C.values():
         c.setdefault("arrays", [])
         c.setdefault("params", [])
@@ -145,4 +151,7 @@ CONFIG_CASES = {
     "cfg_arap_warp_mat": ("arap_warp", dict(W=24, H=20, nhandles=6), dict(nl=3, lin=10, rel=0.0, materialize="j")),
     "cfg_sfs_mat": ("sfs", dict(W=24, H=18), dict(nl=3, lin=10, rel=0.0, method="lm", materialize="j")),
     "cfg_arap_mesh_mat": ("arap_mesh", dict(n=8, nhandles=5), dict(nl=3, lin=10, rel=0.0, materialize="j")),
+    "cfg_poisson_math": ("poisson", dict(W=24, H=20), dict(nl=3, lin=10, rel=0.0, materialize="jtj")),
+    "cfg_arap_warp_math": ("arap_warp", dict(W=24, H=20, nhandles=6), dict(nl=3, lin=10, rel=0.0, materialize="jtj")),
+    "cfg_arap_mesh_math": ("arap_mesh", dict(n=8, nhandles=5), dict(nl=3, lin=10, rel=0.0, materialize="jtj")),
 }

@@ -19,7 +19,8 @@ NAMES = golden_names()
 # transcendental-free programs: exact mode reproduces the reference bit for bit
 BITWISE = {"cfg_poisson_f64", "cfg_poisson_f32", "chain", "dense", "volume", "tri_graph", "mat_chain_lanes",
            "mat_dense", "mat_volume", "mat_tri_graph", "mat_graph_degenerate", "mat_exclude",
-           "cfg_poisson_mat_f64", "cfg_poisson_mat_f32"}
+           "cfg_poisson_mat_f64", "cfg_poisson_mat_f32", "math_dense", "math_volume", "math_tri_graph",
+           "math_graph_degenerate", "math_exclude", "cfg_poisson_math_f64", "cfg_poisson_math_f32"}
 
 
 def tol(prec):
@@ -59,6 +60,13 @@ def run_golden(g, exact):
             assert_close_vec(val, g.ref("j_val"), t["vec"], "J values")
             if exact and g.name in BITWISE:
                 np.testing.assert_array_equal(val, g.ref("j_val"))
+            if g.ref("h_offs") is not None:  # kJtJ: the assembled H = 2 J^T J
+                ho, hc, hv = s.normal_matrix()
+                np.testing.assert_array_equal(ho, g.ref("h_offs"))
+                np.testing.assert_array_equal(hc, g.ref("h_col"))
+                assert_close_vec(hv, g.ref("h_val"), t["vec"], "H values")
+                if exact and g.name in BITWISE:
+                    np.testing.assert_array_equal(hv, g.ref("h_val"))
             continue
         if cmd == "jtj" and exact and g.name in BITWISE:
             np.testing.assert_array_equal(s.apply_jtj(g.z["v"].astype(g.dtype)), g.ref("jtj"))

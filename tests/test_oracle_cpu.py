@@ -51,6 +51,10 @@ def run_oracle(g, name):
             offs, col, val = o.linearize()
             assert bits_equal(offs, g.ref("j_offs")) and bits_equal(col, g.ref("j_col"))
             assert bits_equal(val, g.ref("j_val"))
+            if g.ref("h_offs") is not None:
+                ho, hc, hv = o.normal_matrix()
+                assert bits_equal(ho, g.ref("h_offs")) and bits_equal(hc, g.ref("h_col"))
+                assert bits_equal(hv, g.ref("h_val"))
         elif cmd == "jtj":
             assert bits_equal(o.apply_jtj(g.z["v"].astype(g.dtype)), g.ref("jtj"))
         elif cmd == "solve":
