@@ -415,7 +415,30 @@ struct mo_mat_tables {
   int cbase[MO_MAX_UNK];
   int nfields;
   long long nrows, ncols;
+  int ntl, nce, nk;  // table sizes: lanes, column entries, (field, channel) pairs
 };
+
+// Stage the (few-KB) tables in shared memory: every row / column walks them,
+// and from global memory those walks were the kernels' dominant issue cost.
+__device__ __forceinline__ mo_mat_tables mo_mat_stage(const mo_mat_tables& G) {
+  extern __shared__ __align__(16) unsigned char mo_mat_sm[];
+  mo_mat_tables T = G;
+  size_t off = 0;
+  auto copy = [&](const void* src, size_t bytes) -> const void* {
+    unsigned char* dst = mo_mat_sm + off;
+    const int tid = threadIdx.x + threadIdx.y * blockDim.x, nt = blockDim.x * blockDim.y;
+    for (size_t i = size_t(tid) * 4; i < bytes; i += size_t(nt) * 4)
+      *reinterpret_cast<unsigned*>(dst + i) = *reinterpret_cast<const unsigned*>(static_cast<const unsigned char*>(src) + i);
+    off += (bytes + 15) & ~size_t(15);
+    return dst;
+  };
+  T.tm = static_cast<const mo_mat_tmpl*>(copy(G.tm, sizeof(mo_mat_tmpl) * size_t(G.ntm)));
+  T.lanes = static_cast<const mo_mat_lane*>(copy(G.lanes, sizeof(mo_mat_lane) * size_t(G.ntl)));
+  T.ce = static_cast<const mo_mat_centry*>(copy(G.ce, sizeof(mo_mat_centry) * size_t(G.nce)));
+  T.ceptr = static_cast<const int*>(copy(G.ceptr, sizeof(int) * size_t(G.nk + 1)));
+  __syncthreads();
+  return T;
+}
 
 __device__ __forceinline__ float mo_mul_rn(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ double mo_mul_rn(double a, double b) { return __dmul_rn(a, b); }
@@ -434,12 +457,13 @@ __device__ __forceinline__ int mo_mat_find(const mo_mat_tables& T, long long r) 
 // field's column otherwise - the device refuses both) and strictly ascending
 // (bit 1: kInternal).
 template <class Real>
-__global__ void __launch_bounds__(MO_THREADS) k_mat_check(const __grid_constant__ mo_mat_tables T, mo_state* st) {
+__global__ void __launch_bounds__(MO_THREADS) k_mat_check(const __grid_constant__ mo_mat_tables G, mo_state* st) {
   MO_PDL_ENTRY();
+  const mo_mat_tables T = mo_mat_stage(G);
   int bad = 0;
   for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < T.nrows;
        r += (long long)gridDim.x * blockDim.x) {
-    const mo_mat_tmpl& M = T.tm[mo_mat_find(T, r)];
+    const mo_mat_tmpl M = T.tm[mo_mat_find(T, r)];
     if (M.kind != 0) continue;
     const long long e = r - M.rowbase;
     if (static_cast<const Real*>(M.buf)[(long long)M.guard * M.nrows + e] == Real(0)) continue;
@@ -459,26 +483,37 @@ __global__ void __launch_bounds__(MO_THREADS) k_mat_check(const __grid_constant_
   if (bad) atomicOr(&st->mat_bad, bad);
 }
 
+// gridDim.y = template: the block's template (and its lanes) are uniform,
+// read once; threads stride over the template's rows.
 template <class Real>
 __global__ void __launch_bounds__(MO_THREADS)
-k_mat_rows(const __grid_constant__ mo_mat_tables T, const mo_state* st, int skipdone, const Real* __restrict__ v,
+k_mat_rows(const __grid_constant__ mo_mat_tables G, const mo_state* st, int skipdone, const Real* __restrict__ v,
            Real* __restrict__ jtmp) {
   MO_PDL_ENTRY();
   if (skipdone && st->done) return;
-  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < T.nrows;
-       r += (long long)gridDim.x * blockDim.x) {
-    const mo_mat_tmpl& M = T.tm[mo_mat_find(T, r)];
-    const long long e = r - M.rowbase;
-    const Real* buf = static_cast<const Real*>(M.buf);
+  const mo_mat_tmpl M = G.tm[blockIdx.y];
+  const Real* __restrict__ buf = static_cast<const Real*>(M.buf);
+  __shared__ mo_mat_lane sl[MO_MAT_MAXL];
+  __shared__ long long sb[MO_MAT_MAXL];  // grid: column base of the lane, ubase + lin * C + ch
+  __shared__ int sc[MO_MAT_MAXL];        // channels of the lane's field
+  const int nl = M.nlanes < MO_MAT_MAXL ? M.nlanes : MO_MAT_MAXL;
+  if (threadIdx.x < nl) {
+    const mo_mat_lane L = G.lanes[M.lane0 + threadIdx.x];
+    sl[threadIdx.x] = L;
+    sc[threadIdx.x] = G.chans[L.field];
+    sb[threadIdx.x] = G.ubase[L.field] + L.lin * G.chans[L.field] + L.ch;
+  }
+  __syncthreads();
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < M.nrows;
+       e += (long long)gridDim.x * blockDim.x) {
     Real acc = Real(0);
     if (M.kind == 0) {
       if (buf[(long long)M.guard * M.nrows + e] != Real(0)) {
-        for (int k = 0; k < M.nlanes; ++k) {
-          const mo_mat_lane L = T.lanes[M.lane0 + k];
-          const long long el = e + L.lin;
+#pragma unroll 4
+        for (int k = 0; k < nl; ++k) {
+          const long long el = e + sl[k].lin;
           if (el < 0 || el >= M.nrows) continue;  // (refused by k_mat_check)
-          const long long col = T.ubase[L.field] + el * T.chans[L.field] + L.ch;
-          acc = mo_add_rn(acc, mo_mul_rn(buf[(long long)L.out * M.nrows + e], v[col]));
+          acc = mo_add_rn(acc, mo_mul_rn(buf[(long long)sl[k].out * M.nrows + e], v[sb[k] + e * sc[k]]));
         }
       }
     } else {
@@ -487,9 +522,9 @@ k_mat_rows(const __grid_constant__ mo_mat_tables T, const mo_state* st, int skip
       long long cols[MO_MAT_MAXL];
       Real vals[MO_MAT_MAXL];
       int n = 0;
-      for (int k = 0; k < M.nlanes; ++k) {
-        const mo_mat_lane L = T.lanes[M.lane0 + k];
-        const long long col = T.ubase[L.field] + (long long)M.verts[e * M.arity + L.slot] * T.chans[L.field] + L.ch;
+      for (int k = 0; k < nl; ++k) {
+        const mo_mat_lane L = sl[k];
+        const long long col = G.ubase[L.field] + (long long)M.verts[e * M.arity + L.slot] * sc[k] + L.ch;
         const Real val = buf[(long long)L.out * M.nrows + e];
         int j = n++;
         while (j > 0 && cols[j - 1] > col) {
@@ -507,43 +542,65 @@ k_mat_rows(const __grid_constant__ mo_mat_tables T, const mo_state* st, int skip
         acc = mo_add_rn(acc, mo_mul_rn(mv, v[col]));
       }
     }
-    jtmp[r] = acc;
+    jtmp[M.rowbase + e] = acc;
   }
 }
 
+// gridDim.y = (field, channel) pair: the block's column-entry list is uniform
+// and staged in shared memory; threads stride over the field's elements.
+#define MO_MAT_MAXCE 128
 template <class Real>
 __global__ void __launch_bounds__(MO_THREADS)
-k_mat_cols(const __grid_constant__ mo_mat_tables T, const mo_state* st, int skipdone, const Real* __restrict__ jtmp,
+k_mat_cols(const __grid_constant__ mo_mat_tables G, const mo_state* st, int skipdone, const Real* __restrict__ jtmp,
            Real* __restrict__ out) {
   MO_PDL_ENTRY();
   if (skipdone && st->done) return;
-  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < T.ncols;
-       q += (long long)gridDim.x * blockDim.x) {
-    int f = 0;
-    while (f + 1 < T.nfields && T.ubase[f + 1] <= q) ++f;
-    const long long rel = q - T.ubase[f];
-    const long long el = rel / T.chans[f];
-    const int ch = int(rel - el * T.chans[f]);
-    const int k = T.cbase[f] + ch;
+  const int k = blockIdx.y;
+  int f = 0;
+  while (f + 1 < G.nfields && G.cbase[f + 1] <= k) ++f;
+  const int ch = k - G.cbase[f], C = G.chans[f];
+  const long long nel = (f + 1 < G.nfields ? G.ubase[f + 1] : G.ncols) - G.ubase[f];
+  const long long ne = nel / C;
+  const int c0 = G.ceptr[k], nce = min(G.ceptr[k + 1] - c0, MO_MAT_MAXCE);
+  // per entry: template rows, lane value row, guard row, rowbase, lin (or graph template index)
+  __shared__ const Real* s_val[MO_MAT_MAXCE];
+  __shared__ const Real* s_grd[MO_MAT_MAXCE];
+  __shared__ long long s_rb[MO_MAT_MAXCE], s_lin[MO_MAT_MAXCE], s_n[MO_MAT_MAXCE];
+  __shared__ int s_t[MO_MAT_MAXCE];
+  for (int c = threadIdx.x; c < nce; c += blockDim.x) {
+    const mo_mat_centry E = G.ce[c0 + c];
+    const mo_mat_tmpl& M = G.tm[E.t];
+    const Real* buf = static_cast<const Real*>(M.buf);
+    s_t[c] = E.lane >= 0 ? -1 : E.t;
+    s_rb[c] = M.rowbase;
+    s_n[c] = M.nrows;
+    if (E.lane >= 0) {
+      const mo_mat_lane L = G.lanes[E.lane];
+      s_val[c] = buf + (long long)L.out * M.nrows;
+      s_grd[c] = buf + (long long)M.guard * M.nrows;
+      s_lin[c] = L.lin;
+    }
+  }
+  __syncthreads();
+  for (long long el = blockIdx.x * (long long)blockDim.x + threadIdx.x; el < ne;
+       el += (long long)gridDim.x * blockDim.x) {
     Real y = Real(0);
-    for (int c = T.ceptr[k]; c < T.ceptr[k + 1]; ++c) {
-      const mo_mat_centry E = T.ce[c];
-      const mo_mat_tmpl& M = T.tm[E.t];
-      const Real* buf = static_cast<const Real*>(M.buf);
-      if (E.lane >= 0) {  // grid: the one row of this template holding q through the lane
-        const mo_mat_lane L = T.lanes[E.lane];
-        const long long e = el - L.lin;
-        if (e < 0 || e >= M.nrows) continue;
-        if (buf[(long long)M.guard * M.nrows + e] == Real(0)) continue;
-        y = mo_add_rn(y, mo_mul_rn(buf[(long long)L.out * M.nrows + e], jtmp[M.rowbase + e]));
-      } else {  // graph: incident edges in row order, the merged entry of q
+    for (int c = 0; c < nce; ++c) {
+      if (s_t[c] < 0) {  // grid: the one row of this template holding the column through the lane
+        const long long e = el - s_lin[c];
+        if (e < 0 || e >= s_n[c]) continue;
+        if (s_grd[c][e] == Real(0)) continue;
+        y = mo_add_rn(y, mo_mul_rn(s_val[c][e], jtmp[s_rb[c] + e]));
+      } else {  // graph: incident edges in row order, the merged entry of the column
+        const mo_mat_tmpl& M = G.tm[s_t[c]];
+        const Real* buf = static_cast<const Real*>(M.buf);
         if (el >= M.nverts) continue;
         for (int j = M.vptr[el]; j < M.vptr[el + 1]; ++j) {
           const int e = M.vedge[j];
           bool has = false;
           Real mv = Real(0);
           for (int l = 0; l < M.nlanes; ++l) {
-            const mo_mat_lane L = T.lanes[M.lane0 + l];
+            const mo_mat_lane L = G.lanes[M.lane0 + l];
             if (L.field != f || L.ch != ch || M.verts[(long long)e * M.arity + L.slot] != el) continue;
             const Real val = buf[(long long)L.out * M.nrows + e];
             mv = has ? mo_add_rn(mv, val) : val;
@@ -553,7 +610,7 @@ k_mat_cols(const __grid_constant__ mo_mat_tables T, const mo_state* st, int skip
         }
       }
     }
-    out[q] = mo_mul_rn(y, Real(2));
+    out[G.ubase[f] + el * C + ch] = mo_mul_rn(y, Real(2));
   }
 }
 
@@ -581,9 +638,10 @@ __device__ __forceinline__ void mo_h_acc(long long* cols, Real* vals, int& n, in
 #define MO_MAT_MAXK 64
 template <class Real>
 __global__ void __launch_bounds__(128)
-k_mat_hbuild(const __grid_constant__ mo_mat_tables T, mo_state* st, int K, long long* __restrict__ hcol,
+k_mat_hbuild(const __grid_constant__ mo_mat_tables G, mo_state* st, int K, int* __restrict__ hcol,
              Real* __restrict__ hval, int* __restrict__ hcnt) {
   MO_PDL_ENTRY();
+  const mo_mat_tables T = mo_mat_stage(G);
   int bad = 0;
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < T.ncols;
        q += (long long)gridDim.x * blockDim.x) {
@@ -593,12 +651,12 @@ k_mat_hbuild(const __grid_constant__ mo_mat_tables T, mo_state* st, int K, long 
     int f = 0;
     while (f + 1 < T.nfields && T.ubase[f + 1] <= q) ++f;
     const long long rel = q - T.ubase[f];
-    const long long el = rel / T.chans[f];
+    const long long el = T.ncols < 2147483647LL ? (long long)(int(rel) / T.chans[f]) : rel / T.chans[f];
     const int ch = int(rel - el * T.chans[f]);
     const int kk = T.cbase[f] + ch;
     for (int c = T.ceptr[kk]; c < T.ceptr[kk + 1]; ++c) {
       const mo_mat_centry E = T.ce[c];
-      const mo_mat_tmpl& M = T.tm[E.t];
+      const mo_mat_tmpl M = T.tm[E.t];
       const Real* buf = static_cast<const Real*>(M.buf);
       if (E.lane >= 0) {
         const mo_mat_lane L = T.lanes[E.lane];
@@ -669,7 +727,7 @@ k_mat_hbuild(const __grid_constant__ mo_mat_tables T, mo_state* st, int K, long 
     }
     hcnt[q] = n;
     for (int k = 0; k < n; ++k) {  // slot-major ELL: coalesced in the apply
-      hcol[k * T.ncols + q] = cols[k];
+      hcol[k * T.ncols + q] = int(cols[k]);
       hval[k * T.ncols + q] = mo_mul_rn(vals[k], Real(2));
     }
   }
@@ -679,7 +737,7 @@ k_mat_hbuild(const __grid_constant__ mo_mat_tables T, mo_state* st, int K, long 
 // spmv(H, v) (sparse.hpp spmv): out[q] = sum over row q in column order.
 template <class Real>
 __global__ void __launch_bounds__(MO_THREADS)
-k_mat_happly(long long n, int K, const long long* __restrict__ hcol, const Real* __restrict__ hval,
+k_mat_happly(long long n, int K, const int* __restrict__ hcol, const Real* __restrict__ hval,
              const int* __restrict__ hcnt, const mo_state* st, int skipdone, const Real* __restrict__ v,
              Real* __restrict__ out) {
   MO_PDL_ENTRY();

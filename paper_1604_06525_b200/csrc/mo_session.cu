@@ -969,7 +969,9 @@ class Session final : public SessionBase {
   mo_mat_tables mt_{};
   Real* jtmp_ = nullptr;
   size_t jtmp_cap_ = 0;
-  long long* hcol_ = nullptr;  // kJtJ: H = 2 J^T J, slot-major ELL
+  size_t mt_smem_ = 0;         // staged table bytes (mo_mat_stage)
+  long long max_trows_ = 1, max_fel_ = 1;
+  int* hcol_ = nullptr;  // kJtJ: H = 2 J^T J, slot-major ELL (int32 columns)
   Real* hval_ = nullptr;
   int* hcnt_ = nullptr;
   int hK_ = 0;
@@ -1004,6 +1006,12 @@ class Session final : public SessionBase {
   void kl(void (*k)(K...), dim3 grid, dim3 block, A&&... a) {
     cudaLaunchAttribute at[1];
     cudaLaunchConfig_t lc = launch_cfg(grid, block, 0, at);
+    CK(cudaLaunchKernelEx(&lc, k, std::forward<A>(a)...));
+  }
+  template <class... K, class... A>
+  void kls(void (*k)(K...), dim3 grid, dim3 block, size_t smem, A&&... a) {
+    cudaLaunchAttribute at[1];
+    cudaLaunchConfig_t lc = launch_cfg(grid, block, smem, at);
     CK(cudaLaunchKernelEx(&lc, k, std::forward<A>(a)...));
   }
   void klc(const void* f, dim3 grid, dim3 block, void** args, size_t smem) {
@@ -1949,6 +1957,23 @@ class Session final : public SessionBase {
     mt_.nfields = int(P_.unknowns.size());
     mt_.nrows = rows_;
     mt_.ncols = P_.num_cols;
+    max_trows_ = 1;
+    for (const mo_mat_tmpl& M : tm) max_trows_ = std::max<long long>(max_trows_, M.nrows);
+    max_fel_ = 1;
+    for (size_t f = 0; f < P_.unknowns.size(); ++f) max_fel_ = std::max<long long>(max_fel_, P_.extent_of(P_.unknowns[f].dom));
+    for (const mo_mat_tmpl& M : tm) check(M.nlanes <= MO_MAT_MAXL, Err::kInternal, "materialized J: too many lanes per row");
+    for (size_t k = 0; k + 1 < ceptr.size(); ++k)
+      check(ceptr[k + 1] - ceptr[k] <= MO_MAT_MAXCE, Err::kInternal, "materialized J: too many rows per column");
+    mt_.ntl = int(lanes.size());
+    mt_.nce = int(ce.size());
+    mt_.nk = int(per.size());
+    auto r16 = [](size_t b) { return (b + 15) & ~size_t(15); };
+    mt_smem_ = r16(sizeof(mo_mat_tmpl) * NT) + r16(sizeof(mo_mat_lane) * lanes.size()) +
+               r16(sizeof(mo_mat_centry) * ce.size()) + r16(sizeof(int) * ceptr.size());
+    check(mt_smem_ <= 200 * 1024, Err::kBindError, "materialized J: lane tables exceed shared memory");
+    if (mt_smem_ > 48 * 1024)
+      for (const void* f : {(const void*)k_mat_check<Real>, (const void*)k_mat_hbuild<Real>})
+        CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(mt_smem_)));
     if (mat_ == 2) {  // ELL width of H = 2 J^T J: an upper bound on the row widths
       std::vector<std::set<std::tuple<int, int, long long>>> S(size_t(cbase.back()));
       for (size_t t = 0; t < NT; ++t) {
@@ -1980,7 +2005,8 @@ class Session final : public SessionBase {
         cudaFree(hcol_);
         cudaFree(hval_);
         cudaFree(hcnt_);
-        hcol_ = dalloc<long long>(K * n + 1);
+        check(P_.num_cols < (int64_t(1) << 31), Err::kBindError, "kJtJ: more than 2^31 columns");
+        hcol_ = dalloc<int>(K * n + 1);
         hval_ = dalloc<Real>(K * n + 1);
         hcnt_ = dalloc<int>(n + 1);
         hK_ = int(K);
@@ -1994,6 +2020,12 @@ class Session final : public SessionBase {
     mt_dirty_ = false;
     mt_ok_ = true;
     jvalid_ = false;
+  }
+  // (x blocks per row of the y extent: ~8 resident blocks per SM in total)
+  dim3 mat_grid(long long n, int ny) const {
+    const long long want = std::max<long long>(1, (8LL * nsm_ + ny - 1) / std::max(ny, 1));
+    return dim3(unsigned(std::max<long long>(1, std::min<long long>((n + MO_THREADS - 1) / MO_THREADS, want))),
+                unsigned(std::max(ny, 1)));
   }
   void linearize_device() {
     CK(cudaMemsetAsync(&state_->mat_bad, 0, sizeof(int), st_));
@@ -2013,7 +2045,7 @@ class Session final : public SessionBase {
       grid_rows = true;
     }
     if (grid_rows && mt_ok_ && rows_ > 0) {
-      kl(k_mat_check<Real>, dim3(vgrid(rows_, nsm_)), dim3(MO_THREADS), mt_, state_);
+      kls(k_mat_check<Real>, dim3(vgrid(rows_, nsm_, 8)), dim3(MO_THREADS), mt_smem_, mt_, state_);
       ++launches_;
     }
     bool pending_h = mat_ == 2;
@@ -2032,8 +2064,8 @@ class Session final : public SessionBase {
     }
     if (pending_h && mt_ok_) {  // assemble H = 2 J^T J (solver.hpp:370-374)
       const long long n = P_.num_cols;
-      kl(k_mat_hbuild<Real>, dim3(unsigned(std::max<long long>(1, std::min<long long>((n + 127) / 128, 8LL * nsm_)))),
-         dim3(128), mt_, state_, hK_, hcol_, hval_, hcnt_);
+      kls(k_mat_hbuild<Real>, dim3(unsigned(std::max<long long>(1, std::min<long long>((n + 127) / 128, 8LL * nsm_)))),
+          dim3(128), mt_smem_, mt_, state_, hK_, hcol_, hval_, hcnt_);
       ++launches_;
     }
     jvalid_ = true;
@@ -2045,18 +2077,18 @@ class Session final : public SessionBase {
     const long long n = P_.num_cols;
     const int skip = (flags & MO_F_SKIPDONE) ? 1 : 0;
     if (mat_ == 2) {  // spmv(H, v) (solver.hpp:284)
-      kl(k_mat_happly<Real>, dim3(vgrid(n, nsm_)), dim3(MO_THREADS), n, hK_, static_cast<const long long*>(hcol_),
+      kl(k_mat_happly<Real>, dim3(vgrid(n, nsm_, 8)), dim3(MO_THREADS), n, hK_, static_cast<const int*>(hcol_),
          static_cast<const Real*>(hval_), static_cast<const int*>(hcnt_), static_cast<const mo_state*>(state_), skip, pv,
          out);
       ++launches_;
     } else {
       if (rows_ > 0) {
-        kl(k_mat_rows<Real>, dim3(vgrid(rows_, nsm_)), dim3(MO_THREADS), mt_, static_cast<const mo_state*>(state_),
+        kl(k_mat_rows<Real>, mat_grid(max_trows_, mt_.ntm), dim3(MO_THREADS), mt_, static_cast<const mo_state*>(state_),
            skip, pv, jtmp_);
         ++launches_;
       }
-      kl(k_mat_cols<Real>, dim3(vgrid(n, nsm_)), dim3(MO_THREADS), mt_, static_cast<const mo_state*>(state_), skip,
-         static_cast<const Real*>(jtmp_), out);
+      kl(k_mat_cols<Real>, mat_grid(max_fel_, mt_.nk), dim3(MO_THREADS), mt_, static_cast<const mo_state*>(state_),
+         skip, static_cast<const Real*>(jtmp_), out);
       ++launches_;
     }
     apply_parts_ = vgrid(n, nsm_);
@@ -2094,11 +2126,11 @@ class Session final : public SessionBase {
     check(jvalid_ && mat_ == 2, Err::kBindError, "no normal matrix has been assembled");
     const size_t n = size_t(P_.num_cols), K = size_t(hK_);
     std::vector<int> cnt(n);
-    std::vector<long long> hc(K * n);
+    std::vector<int> hc(K * n);
     std::vector<Real> hv(K * n);
     if (n) {
       CK(cudaMemcpyAsync(cnt.data(), hcnt_, n * sizeof(int), cudaMemcpyDeviceToHost, st_));
-      CK(cudaMemcpyAsync(hc.data(), hcol_, K * n * sizeof(long long), cudaMemcpyDeviceToHost, st_));
+      CK(cudaMemcpyAsync(hc.data(), hcol_, K * n * sizeof(int), cudaMemcpyDeviceToHost, st_));
       CK(cudaMemcpyAsync(hv.data(), hval_, K * n * sizeof(Real), cudaMemcpyDeviceToHost, st_));
     }
     CK(cudaStreamSynchronize(st_));
