@@ -508,14 +508,24 @@ k_mat_rows(const __grid_constant__ mo_mat_tables G, const mo_state* st, int skip
        e += (long long)gridDim.x * blockDim.x) {
     Real acc = Real(0);
     if (M.kind == 0) {
-      if (buf[(long long)M.guard * M.nrows + e] != Real(0)) {
-#pragma unroll 4
-        for (int k = 0; k < nl; ++k) {
-          const long long el = e + sl[k].lin;
-          if (el < 0 || el >= M.nrows) continue;  // (refused by k_mat_check)
-          acc = mo_add_rn(acc, mo_mul_rn(buf[(long long)sl[k].out * M.nrows + e], v[sb[k] + e * sc[k]]));
+      // All loads of the row issue together (none depends on the guard).
+      const Real g = buf[(long long)M.guard * M.nrows + e];
+      for (int k0 = 0; k0 < nl; k0 += 4) {
+        Real a[4], b[4];
+        bool ok[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = k0 + u;
+          const long long el = e + (k < nl ? sl[k].lin : 0);
+          ok[u] = k < nl && el >= 0 && el < M.nrows;  // (out-of-field lanes are refused by k_mat_check)
+          a[u] = ok[u] ? buf[(long long)sl[k].out * M.nrows + e] : Real(0);
+          b[u] = ok[u] ? v[sb[k] + e * sc[k]] : Real(0);
         }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (ok[u]) acc = mo_add_rn(acc, mo_mul_rn(a[u], b[u]));
       }
+      if (g == Real(0)) acc = Real(0);  // boundary guard false: the row is empty
     } else {
       // Edge row: entries sorted by column (stable: repeated vertices keep
       // lane order) and merged (solver.hpp:350-366).
@@ -587,10 +597,25 @@ k_mat_cols(const __grid_constant__ mo_mat_tables G, const mo_state* st, int skip
     Real y = Real(0);
     for (int c = 0; c < nce; ++c) {
       if (s_t[c] < 0) {  // grid: the one row of this template holding the column through the lane
-        const long long e = el - s_lin[c];
-        if (e < 0 || e >= s_n[c]) continue;
-        if (s_grd[c][e] == Real(0)) continue;
-        y = mo_add_rn(y, mo_mul_rn(s_val[c][e], jtmp[s_rb[c] + e]));
+        // batch the consecutive grid entries' loads (independent of the guards)
+        Real g[4], a[4], b[4];
+        bool ok[4];
+        int m = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int cc = c + u;
+          const bool grid = cc < nce && s_t[cc] < 0 && (u == 0 || m == u);
+          const long long e = el - (grid ? s_lin[cc] : 0);
+          ok[u] = grid && e >= 0 && e < s_n[cc];
+          if (grid) m = u + 1;
+          g[u] = ok[u] ? s_grd[cc][e] : Real(0);
+          a[u] = ok[u] ? s_val[cc][e] : Real(0);
+          b[u] = ok[u] ? jtmp[s_rb[cc] + e] : Real(0);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (ok[u] && g[u] != Real(0)) y = mo_add_rn(y, mo_mul_rn(a[u], b[u]));
+        c += m - 1;
       } else {  // graph: incident edges in row order, the merged entry of the column
         const mo_mat_tmpl& M = G.tm[s_t[c]];
         const Real* buf = static_cast<const Real*>(M.buf);
