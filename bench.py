@@ -53,8 +53,10 @@ def make_problem(cfg_name, size=0, rows_mult=1):
         return workloads.arap_warp((size or 1024) * rows_mult, size or 1024)
     if cfg_name == "poisson":
         return workloads.poisson((size or 512) * rows_mult, size or 512)
+    if cfg_name == "arap_mesh" and rows_mult != 1:  # vertex strips: rows_mult x 448 rows of 448 vertices
+        return workloads.arap_mesh(size or 448, 64 * rows_mult, rows=(size or 448) * rows_mult)
     if rows_mult != 1:
-        raise SystemExit(f"{cfg_name}: multi-GPU strips are for the grid configs (arap_warp, poisson)")
+        raise SystemExit(f"{cfg_name}: multi-GPU strips are for arap_warp, poisson and arap_mesh")
     if cfg_name == "sfs":
         return workloads.sfs(size or 640, size or 480)
     if cfg_name == "arap_mesh":

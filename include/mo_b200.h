@@ -202,6 +202,12 @@ int mo_comm_create_local(mo_world w, int rank, mo_comm* out);
 void mo_world_destroy(mo_world w);
 void mo_comm_destroy(mo_comm c);
 int mo_session_create_shard(mo_plan p, int device, mo_comm c, int64_t row0, int64_t row1, mo_session* out);
+/* Graph energies (vertices = the domain's elements) shard the same way: a
+ * strip stores every edge with an endpoint in its rows, so `halo` must cover
+ * the graph's row bandwidth (max row distance within an edge; refused with
+ * MO_ERR_BIND otherwise).  halo <= mo_plan_halo_rows() means the plan's. */
+int mo_session_create_shard_halo(mo_plan p, int device, mo_comm c, int64_t row0, int64_t row1, int halo,
+                                 mo_session* out);
 int mo_session_local_layout(mo_session s, int64_t* lo, int64_t* hi, int64_t* row0, int64_t* row1);
 
 /* ---- measurement hooks (bench.py) -------------------------------------- */

@@ -88,6 +88,8 @@ SIGNATURES = {
     "mo_world_destroy": (None, [c_void_p]),
     "mo_comm_destroy": (None, [c_void_p]),
     "mo_session_create_shard": (c_int, [c_void_p, c_int, c_void_p, c_int64, c_int64, ctypes.POINTER(c_void_p)]),
+    "mo_session_create_shard_halo": (c_int, [c_void_p, c_int, c_void_p, c_int64, c_int64, c_int,
+                                             ctypes.POINTER(c_void_p)]),
     "mo_session_local_layout": (c_int, [c_void_p] + [ctypes.POINTER(c_int64)] * 4),
     "mo_set_profiling": (c_int, [c_void_p, c_int]),
     "mo_profile_read": (c_int, [c_void_p, c_int, ctypes.POINTER(c_double), ctypes.POINTER(c_int64)]),

@@ -369,6 +369,19 @@ int mo_session_create_shard(mo_plan p, int device, mo_comm c, int64_t row0, int6
   });
 }
 
+int mo_session_create_shard_halo(mo_plan p, int device, mo_comm c, int64_t row0, int64_t row1, int halo,
+                                 mo_session* out) {
+  return guard([&] {
+    need(p, "plan");
+    need(c, "communicator");
+    need(out, "output");
+    auto s = std::make_unique<mo_session_s>();
+    s->impl = mo::make_shard_session(p->plan, device, c->c.get(), row0, row1, halo);
+    s->f32 = p->plan.cfg.precision == 0;
+    *out = s.release();
+  });
+}
+
 int mo_session_local_layout(mo_session s, int64_t* lo, int64_t* hi, int64_t* row0, int64_t* row1) {
   SESSION_CALL(need(lo, "output"); need(hi, "output"); need(row0, "output"); need(row1, "output");
                s->impl->local_layout(lo, hi, row0, row1));

@@ -229,6 +229,7 @@ k_apply_finish(mo_red R, long long n, const unsigned char* cm, const Real* __res
   double acc = 0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
+    if (halo_at(cm, i)) continue;  // a strip's halo column: owned (and reduced) by a neighbour
     Real v = ap[i];
     if (flags & MO_F_DAMP) v = v + damp[i] * p[i];
     if ((flags & MO_F_ZEROEXCL) && ex_at(cm, i)) v = Real(0);

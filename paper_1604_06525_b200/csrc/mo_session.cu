@@ -73,9 +73,9 @@ class Session final : public SessionBase {
   // [lo, hi) = owned rows plus halo_rows(P) on each side (clipped); kernels
   // keep GLOBAL coordinates, so InBounds / index() / OOB semantics are those
   // of the unsharded problem.
-  Session(const Plan& plan, int device, Comm* comm = nullptr, int64_t row0 = 0, int64_t row1 = -1)
+  Session(const Plan& plan, int device, Comm* comm = nullptr, int64_t row0 = 0, int64_t row1 = -1, int halo = 0)
       : P_(plan), dev_(device), comm_(comm) {
-    if (comm_) setup_shard(row0, row1);
+    if (comm_) setup_shard(row0, row1, halo);
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
       fail(Err::kNoDevice, "no CUDA device available (the B200 path has no CPU fallback)");
@@ -634,7 +634,8 @@ class Session final : public SessionBase {
   struct GraphData {
     int arity = -1;
     std::vector<uint64_t> verts;
-    int64_t E = 0;
+    int64_t E = 0;      // edges stored (a strip: every edge touching its rows)
+    int64_t E_own = 0;  // of which this strip evaluates for cost (slot-0 vertex owned; stored first)
     bool bound = false, dirty = true;
     int* d_verts = nullptr;
     size_t cap = 0;
@@ -675,8 +676,10 @@ class Session final : public SessionBase {
     int R = 0;
   };
 
-  void setup_shard(int64_t row0, int64_t row1) {
-    check(P_.graph_sets.empty(), Err::kBindError, "strip sharding supports grid energies only");
+  // Graph energies shard too when their vertices are the elements of the one
+  // domain: a strip holds every edge with an endpoint in its rows; `halo`
+  // (>= the plan's) must cover the graph's row bandwidth (checked at upload).
+  void setup_shard(int64_t row0, int64_t row1, int halo) {
     const Domain* D = nullptr;
     auto same = [&](const Domain& d) {
       if (!D) D = &d;
@@ -694,7 +697,7 @@ class Session final : public SessionBase {
     sh_.S = P_.extent_of(*D) / std::max<int64_t>(sh_.d0, 1);
     if (row1 < 0) row1 = sh_.d0;
     check(row0 >= 0 && row0 < row1 && row1 <= sh_.d0, Err::kBindError, "strip rows out of range");
-    sh_.R = halo_rows(P_);
+    sh_.R = std::max(halo_rows(P_), halo);
     check(comm_->world == 1 || row1 - row0 >= sh_.R, Err::kBindError, "strip thinner than the halo");
     sh_.row0 = row0;
     sh_.row1 = row1;
@@ -831,7 +834,7 @@ class Session final : public SessionBase {
         gs.doms.push_back({});
         gd = &gs.doms.back();
         gd->dom = d;
-        gd->nverts = P_.extent_of(d);
+        gd->nverts = lext(d);  // (a strip: its stored rows, local vertex ids)
       }
       if (std::find(gd->slots.begin(), gd->slots.end(), s.slot) == gd->slots.end()) gd->slots.push_back(s.slot);
     }
@@ -895,7 +898,44 @@ class Session final : public SessionBase {
         check(g.verts[k] < (uint64_t(1) << 31), Err::kIndexOutOfRange, "vertex index exceeds int32");
         v32[k] = int(g.verts[k]);
       }
-      if (ne) CK(cudaMemcpyAsync(g.d_verts, v32.data(), ne * sizeof(int), cudaMemcpyHostToDevice, st_));
+      g.E_own = g.E;
+      std::vector<int> ord;  // local edges in global edge order (the gathers' accumulation order)
+      if (sh_.on) {  // strip: edges touching the owned rows, local vertex ids, owned edges first
+        const int64_t a = sh_.row0 * sh_.S, b = sh_.row1 * sh_.S, la = sh_.lo * sh_.S, lb = sh_.hi * sh_.S;
+        std::vector<int> own, other;
+        for (int64_t e = 0; e < g.E; ++e) {
+          bool touch = false;
+          for (int k = 0; k < g.arity; ++k) {
+            const int64_t v = v32[size_t(e * g.arity + k)];
+            touch = touch || (v >= a && v < b);
+          }
+          if (!touch) continue;
+          for (int k = 0; k < g.arity; ++k) {
+            const int64_t v = v32[size_t(e * g.arity + k)];
+            check(v >= la && v < lb, Err::kBindError, "graph edge spans more rows than the strip halo");
+          }
+          const int64_t v0 = v32[size_t(e * g.arity)];
+          (v0 >= a && v0 < b ? own : other).push_back(int(e));
+        }
+        std::vector<int> loc;
+        loc.reserve((own.size() + other.size()) * size_t(g.arity));
+        for (const std::vector<int>* lst : {&own, &other})
+          for (int e : *lst)
+            for (int k = 0; k < g.arity; ++k) loc.push_back(int(v32[size_t(e * g.arity + k)] - la));
+        v32.swap(loc);
+        g.E = int64_t(own.size() + other.size());
+        g.E_own = int64_t(own.size());
+        size_t i = 0, j = 0;
+        while (i < own.size() || j < other.size()) {
+          if (j == other.size() || (i < own.size() && own[i] < other[j])) ord.push_back(int(i++));
+          else ord.push_back(int(own.size() + j++));
+        }
+      } else {
+        ord.resize(size_t(g.E));
+        for (int64_t e = 0; e < g.E; ++e) ord[size_t(e)] = int(e);
+      }
+      const size_t nl = v32.size();
+      if (nl) CK(cudaMemcpyAsync(g.d_verts, v32.data(), nl * sizeof(int), cudaMemcpyHostToDevice, st_));
       for (size_t si = 0; si < P_.graph_sets.size(); ++si) {
         const GraphSet& gset = P_.graph_sets[si];
         if (gset.graph != int(gi)) continue;
@@ -909,7 +949,7 @@ class Session final : public SessionBase {
         }
         for (auto& gd : gs.doms) {
           std::vector<int> cnt(size_t(gd.nverts) + 1, 0), last(size_t(gd.nverts), -1);
-          for (int64_t e = 0; e < g.E; ++e)
+          for (int e : ord)
             for (int s : gd.slots) {
               int v = v32[size_t(e * g.arity + s)];
               if (last[size_t(v)] != int(e)) {
@@ -921,7 +961,7 @@ class Session final : public SessionBase {
           std::vector<int> vedge(static_cast<size_t>(cnt[static_cast<size_t>(gd.nverts)]));
           std::vector<int> pos(cnt.begin(), cnt.end() - 1);
           std::fill(last.begin(), last.end(), -1);
-          for (int64_t e = 0; e < g.E; ++e)
+          for (int e : ord)
             for (int s : gd.slots) {
               int v = v32[size_t(e * g.arity + s)];
               if (last[size_t(v)] != int(e)) {
@@ -1069,7 +1109,7 @@ class Session final : public SessionBase {
     k.d0 = k.d1 = k.d2 = 1;
     k.verts = g.d_verts;
     k.arity = g.arity;
-    k.nedges = g.E;
+    k.nedges = g.E_own;  // edge kernels (cost, residuals): the edges this strip owns
     return k;
   }
 
@@ -1102,7 +1142,7 @@ class Session final : public SessionBase {
   }
   int edge_blocks(const std::string& name, int gi) {
     const void* f = mod_.kernel(name);
-    long long E = graphs_[size_t(P_.graph_sets[size_t(gi)].graph)].E;
+    long long E = graphs_[size_t(P_.graph_sets[size_t(gi)].graph)].E_own;
     long long g = std::min<long long>((E + MO_THREADS - 1) / MO_THREADS, (long long)nsm_ * occupancy(f));
     return int(std::max<long long>(g, 1));
   }
@@ -1669,6 +1709,7 @@ class Session final : public SessionBase {
       kl(k_bm_patch<Real>, dim3(vgrid(n, nsm_)), dim3(MO_THREADS), red(0, vgrid(n, nsm_), MO_FIN_UNCONSTRAINED, 0), n,
                                                                 colmask_, b_, m_);
       ++launches_;
+      reduce_done(MO_FIN_UNCONSTRAINED, 0);  // (strips only)
     } else if (P_.gather_sets.empty()) {
       CK(cudaMemsetAsync(&state_->unconstrained, 0, sizeof(long long), st_));
     } else {
@@ -1722,6 +1763,7 @@ class Session final : public SessionBase {
         kl(k_apply_finish<Real>, dim3(vgrid(n, nsm_)), dim3(MO_THREADS), red(0, vgrid(n, nsm_), MO_FIN_PCG_ALPHA, 0), n,
                                                                      colmask_, pv, damp_, out, flags);
         ++launches_;
+        if (flags & MO_F_REDUCE) reduce_done(MO_FIN_PCG_ALPHA, 0);  // (strips only)
       }
     }
   }
@@ -2433,10 +2475,10 @@ std::unique_ptr<SessionBase> make_session(const Plan& plan, int device) {
 }
 
 std::unique_ptr<SessionBase> make_shard_session(const Plan& plan, int device, Comm* comm, int64_t row0,
-                                                int64_t row1) {
+                                                int64_t row1, int halo) {
   check(comm != nullptr, Err::kBindError, "shard session needs a communicator");
-  if (plan.cfg.precision == 0) return std::make_unique<Session<float>>(plan, device, comm, row0, row1);
-  return std::make_unique<Session<double>>(plan, device, comm, row0, row1);
+  if (plan.cfg.precision == 0) return std::make_unique<Session<float>>(plan, device, comm, row0, row1, halo);
+  return std::make_unique<Session<double>>(plan, device, comm, row0, row1, halo);
 }
 
 int halo_rows(const Plan& P) {

@@ -73,7 +73,7 @@ std::unique_ptr<SessionBase> make_session(const Plan& plan, int device);
 // Strip shard owning rows [row0, row1) of the plan's grid domain; `comm` must
 // outlive the session.
 std::unique_ptr<SessionBase> make_shard_session(const Plan& plan, int device, Comm* comm, int64_t row0,
-                                                int64_t row1);
+                                                int64_t row1, int halo = 0);
 // Halo rows a strip needs on each side (max axis-0 reach of every program +
 // the two-phase apply's lane halo).
 int halo_rows(const Plan& plan);

@@ -9,6 +9,11 @@ in the unsharded problem.  Per PCG iteration the p halo is exchanged and the
 p'Ap / r'z partials are gathered and summed in rank order, so every strip
 takes the same alpha/beta.
 
+Graph energies whose vertices are the domain's elements (the ARAP mesh) shard
+as vertex ranges: the halo is the graph's row bandwidth (graph_halo_rows), a
+strip keeps every edge touching its rows and counts only its own edges in
+the cost.
+
     # one process per GPU (torchrun), NCCL underneath:
     s = ShardedSolver(plan, global_data, rank, world, device)
     res = s.solve(); x = s.gather_x()
@@ -41,7 +46,19 @@ class Layout:
     halo: int
 
 
-def layout(plan: CompiledPlan) -> Layout:
+def graph_halo_rows(graphs, S: int) -> int:
+    """Row bandwidth of the bound graphs (max row distance between two vertices
+    of one edge, vertex v in row v // S): the halo a strip needs so that it
+    stores every endpoint of the edges touching its rows."""
+    h = 0
+    for g in graphs:
+        v = np.asarray(g.verts, np.int64).reshape(-1, g.arity) // S
+        if v.size:
+            h = max(h, int((v.max(axis=1) - v.min(axis=1)).max()))
+    return h
+
+
+def layout(plan: CompiledPlan, data: SolveData = None) -> Layout:
     info = planinfo.parse(plan.text)
     dims = dict(info.dims)
     dims.update(plan.dims)
@@ -56,8 +73,11 @@ def layout(plan: CompiledPlan) -> Layout:
     shp = shape(doms[0])
     h = ctypes.c_int()
     call("mo_plan_halo_rows", plan._h, ctypes.byref(h))
-    return Layout(shp[0], int(np.prod(shp[1:])) if len(shp) > 1 else 1,
-                  [f[1] for f in info.fields["U"]], [f[1] for f in info.fields["A"]], h.value)
+    S = int(np.prod(shp[1:])) if len(shp) > 1 else 1
+    halo = h.value
+    if data is not None and data.graphs:
+        halo = max(halo, graph_halo_rows(data.graphs, S))
+    return Layout(shp[0], S, [f[1] for f in info.fields["U"]], [f[1] for f in info.fields["A"]], halo)
 
 
 def _rows_of(vec, d0, row_elems, lo, hi):
@@ -65,8 +85,9 @@ def _rows_of(vec, d0, row_elems, lo, hi):
 
 
 def local_data(plan: CompiledPlan, data: SolveData, row0: int, row1: int) -> SolveData:
-    """The strip's SolveData: rows [lo, hi) of every field (halos included)."""
-    L = layout(plan)
+    """The strip's SolveData: rows [lo, hi) of every field (halos included).
+    Graphs stay global: the session keeps the edges touching its rows."""
+    L = layout(plan, data)
     lo, hi = max(0, row0 - L.halo), min(L.d0, row1 + L.halo)
     x, off, parts = np.asarray(data.x), 0, []
     for C in L.unknown_ch:
@@ -78,9 +99,11 @@ def local_data(plan: CompiledPlan, data: SolveData, row0: int, row1: int) -> Sol
                      graphs=[EdgeTable(g.arity, g.verts) for g in data.graphs])
 
 
-def owned_x(plan: CompiledPlan, xloc: np.ndarray, row0: int, row1: int) -> List[np.ndarray]:
+def owned_x(plan: CompiledPlan, xloc: np.ndarray, row0: int, row1: int, halo: int = None) -> List[np.ndarray]:
     """Per unknown field, the strip's owned rows of its local x."""
     L = layout(plan)
+    if halo is not None:
+        L.halo = halo
     lo, hi = max(0, row0 - L.halo), min(L.d0, row1 + L.halo)
     out, off = [], 0
     for C in L.unknown_ch:
@@ -103,7 +126,8 @@ class LocalShardGroup:
 
     def __init__(self, plan: CompiledPlan, data: SolveData, world: int, device: int = 0):
         self.plan, self.world = plan, world
-        L = layout(plan)
+        L = layout(plan, data)
+        self.halo = L.halo
         self._w = ctypes.c_void_p()
         call("mo_world_create_local", int(world), int(device), ctypes.byref(self._w))
         self.comms, self.rows = [], []
@@ -115,7 +139,8 @@ class LocalShardGroup:
         # Construction refreshes (collective halo exchanges): one thread per strip.
         self.solvers = list(range(world))
         self.solvers = self._parallel(
-            lambda r: Solver(plan, local_data(plan, data, *self.rows[r]), device, comm=self.comms[r], rows=self.rows[r]))
+            lambda r: Solver(plan, local_data(plan, data, *self.rows[r]), device, comm=self.comms[r], rows=self.rows[r],
+                             halo=self.halo))
 
     def _parallel(self, fn):
         out, err = [None] * self.world, []
@@ -142,7 +167,8 @@ class LocalShardGroup:
         return self._parallel(lambda s: s.cost())
 
     def gather_x(self):
-        return assemble_x(self.plan, [owned_x(self.plan, s.get_x(), *rw) for s, rw in zip(self.solvers, self.rows)])
+        return assemble_x(self.plan, [owned_x(self.plan, s.get_x(), *rw, halo=self.halo)
+                                      for s, rw in zip(self.solvers, self.rows)])
 
     def close(self):
         for s in self.solvers:
@@ -168,7 +194,8 @@ class ShardedSolver:
     def __init__(self, plan: CompiledPlan, data: SolveData, rank: int, world: int, device: int):
         import torch.distributed as dist
         self.plan, self.rank, self.world = plan, rank, world
-        L = layout(plan)
+        L = layout(plan, data)
+        self.halo = L.halo
         uid = (ctypes.c_char * 128)()
         if rank == 0:
             call("mo_nccl_unique_id", uid, 128)
@@ -178,14 +205,15 @@ class ShardedSolver:
         self._c = ctypes.c_void_p()
         call("mo_comm_create_nccl", uid, 128, rank, world, device, ctypes.byref(self._c))
         self.rows = strip_rows(L.d0, world, rank)
-        self.solver = Solver(plan, local_data(plan, data, *self.rows), device, comm=self._c, rows=self.rows)
+        self.solver = Solver(plan, local_data(plan, data, *self.rows), device, comm=self._c, rows=self.rows,
+                             halo=self.halo)
 
     def solve(self):
         return self.solver.solve()
 
     def gather_x(self):
         import torch.distributed as dist
-        mine = owned_x(self.plan, self.solver.get_x(), *self.rows)
+        mine = owned_x(self.plan, self.solver.get_x(), *self.rows, halo=self.halo)
         allp = [None] * self.world
         dist.all_gather_object(allp, mine)
         return assemble_x(self.plan, allp)

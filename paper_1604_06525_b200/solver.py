@@ -214,7 +214,7 @@ def _as(a, dtype):
 class Solver:
     """minopt::Solver<Real> (solver.hpp:80-635) over the device session."""
 
-    def __init__(self, plan_: CompiledPlan, data: SolveData, device: int = 0, comm=None, rows=None):
+    def __init__(self, plan_: CompiledPlan, data: SolveData, device: int = 0, comm=None, rows=None, halo=0):
         """comm/rows: strip shard owning axis-0 rows [rows[0], rows[1]) of the
         plan's grid domain (see sharded.py); `data` is then the strip's LOCAL
         data (its stored rows [lo, hi), halos included)."""
@@ -226,7 +226,8 @@ class Solver:
         if comm is None:
             call("mo_session_create", plan_._h, int(device), ctypes.byref(h))
         else:
-            call("mo_session_create_shard", plan_._h, int(device), comm, int(rows[0]), int(rows[1]), ctypes.byref(h))
+            call("mo_session_create_shard_halo", plan_._h, int(device), comm, int(rows[0]), int(rows[1]), int(halo),
+                 ctypes.byref(h))
         self._h = h
         self._bind_all()
         call("mo_refresh", self._h)

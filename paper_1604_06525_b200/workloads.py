@@ -106,9 +106,11 @@ def sfs(W: int = 640, H: int = 480) -> Problem:
     return Problem("sfs", {"W": W, "H": H}, X0, [D, Im], params, method="lm", energy="sfs")
 
 
-def grid_mesh_edges(n: int) -> np.ndarray:
-    """Both directions of every edge of an n x n grid mesh, vertex-major order."""
-    v = np.arange(n * n, dtype=np.uint64).reshape(n, n)
+def grid_mesh_edges(n: int, rows: int = 0) -> np.ndarray:
+    """Both directions of every edge of a rows x n grid mesh (rows = n by
+    default), vertex-major order."""
+    rows = rows or n
+    v = np.arange(rows * n, dtype=np.uint64).reshape(rows, n)
     right = np.stack([v[:, :-1], v[:, 1:]], axis=-1)
     down = np.stack([v[:-1, :], v[1:, :]], axis=-1)
     e = []
@@ -118,18 +120,20 @@ def grid_mesh_edges(n: int) -> np.ndarray:
     return np.concatenate(e).reshape(-1)
 
 
-def arap_mesh(n: int = 448, nhandles: int = 64) -> Problem:
-    """ARAP mesh deformation (Fig. 25) on an n x n grid mesh (n=448 gives
-    200,704 vertices and 801,024 directed edges).  Ur = (r, c, 0); Off0 = Ur;
-    Ang0 = 0; C = -1e6 except handles C = Ur + U[0,3)^3; w_fit = 10, w_reg = 1."""
-    N = n * n
-    r, c = np.meshgrid(np.arange(n, dtype=np.float64), np.arange(n, dtype=np.float64), indexing="ij")
+def arap_mesh(n: int = 448, nhandles: int = 64, rows: int = 0) -> Problem:
+    """ARAP mesh deformation (Fig. 25) on a rows x n grid mesh (rows = n by
+    default; n=448 gives 200,704 vertices and 801,024 directed edges).
+    Ur = (r, c, 0); Off0 = Ur; Ang0 = 0; C = -1e6 except handles
+    C = Ur + U[0,3)^3; w_fit = 10, w_reg = 1."""
+    rows = rows or n
+    N = rows * n
+    r, c = np.meshgrid(np.arange(rows, dtype=np.float64), np.arange(n, dtype=np.float64), indexing="ij")
     Ur = np.stack([r.reshape(-1), c.reshape(-1), np.zeros(N)], axis=1)
     C = np.full((N, 3), -1e6)
     h = _handles(21, nhandles, N)
     C[h] = Ur[h] + 3.0 * uniform(22, 3 * nhandles).reshape(nhandles, 3)
     x = np.concatenate([Ur.reshape(-1), np.zeros(3 * N)])
-    g = EdgeTable(2, grid_mesh_edges(n))
+    g = EdgeTable(2, grid_mesh_edges(n, rows))
     return Problem("arap_mesh", {"N": N}, x, [Ur.reshape(-1), C.reshape(-1)], [10.0, 1.0], [g],
                    energy="arap_mesh")
 

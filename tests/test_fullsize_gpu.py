@@ -155,3 +155,30 @@ def test_config5_strips_2048(name):
         for row, rc in zip(r.trace, ref["trace_cost"]):
             assert abs(row.cost - rc) <= 1e-4 * abs(rc), (name, row.cost, rc)
         assert abs(r.final_cost - float(ref["final_cost"][0])) <= 1e-4 * abs(float(ref["final_cost"][0]))
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_config4_mesh_vertex_strips(prec):
+    """Config 4 (ARAP mesh, 200,704 vertices, 801,024 edges) in 4 vertex
+    strips (halo = the mesh's row bandwidth, edges touching a strip stored
+    there, cost over the strip's own edges) against the reference's fp64 GN
+    trajectory: fp64 within 1e-8, fp32 within 1e-4 (the fp32 reference is
+    the outlier at this size)."""
+    from paper_1604_06525_b200.sharded import LocalShardGroup
+    prob = workloads.arap_mesh(448)
+    nl, lin = 2, 10
+    ref = pyoracle.run_ref(prob.energy, prob.data(np.float64), ["solve"], dims=prob.dims, prec="f64", nl=nl, lin=lin,
+                           rel=0.0, abs_tol=0.0, cost_stop=0.0, exec_mode="par", threads=THREADS)
+    dt = np.float64 if prec == "f64" else np.float32
+    g = LocalShardGroup(load_plan(prob.name, _cfg(prob, prec, nl, lin), prob.dims), prob.data(dt), 4)
+    try:
+        assert g.halo == 448
+        results = g.solve()
+    finally:
+        g.close()
+    tol = 1e-8 if prec == "f64" else 1e-4
+    for r in results:
+        assert [t.pcg_iters for t in r.trace] == list(ref["trace_pcg"])
+        for row, rc in zip(r.trace, ref["trace_cost"]):
+            assert abs(row.cost - rc) <= tol * abs(rc), (row.cost, rc)
+        assert abs(r.final_cost - float(ref["final_cost"][0])) <= tol * abs(float(ref["final_cost"][0]))

@@ -28,12 +28,12 @@ def _worker(rank, world, port, name, dims, q):
     try:
         prob = workloads.CONFIGS[name](**dims)
         plan = load_plan(prob.name, dims=prob.dims)
-        L = layout(plan)
         data = prob.data(np.float64)
+        L = layout(plan, data)
         rows = strip_rows(L.d0, world, rank)
         loc = local_data(plan, data, *rows)
         # halo rows of x must equal the neighbour's owned rows
-        mine = owned_x(plan, loc.x, *rows)
+        mine = owned_x(plan, loc.x, *rows, halo=L.halo)
         allp = [None] * world
         dist.all_gather_object(allp, {"rows": rows, "x": loc.x, "owned": mine})
         lo = max(0, rows[0] - L.halo)
@@ -53,7 +53,8 @@ def _worker(rank, world, port, name, dims, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name,dims", [("poisson", dict(W=20, H=12)), ("arap_warp", dict(W=18, H=10))])
+@pytest.mark.parametrize("name,dims", [("poisson", dict(W=20, H=12)), ("arap_warp", dict(W=18, H=10)),
+                                       ("arap_mesh", dict(n=9, nhandles=4))])
 def test_gloo_world2_partition_halo_gather(name, dims):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -68,7 +69,7 @@ def test_gloo_world2_partition_halo_gather(name, dims):
     assert all(r[1] for r in res), "halo rows differ from the neighbour's owned rows"
     assert all(r[2] for r in res), "all-gathered owned rows do not reassemble x"
     (r0, r1), (s0, s1) = res[0][3], res[1][3]
-    assert r0 == 0 and r1 == s0 and s1 == dims["W"]
+    assert r0 == 0 and r1 == s0 and s1 == dims.get("W", dims.get("n", 0) ** 2)
     assert res[0][4] >= 1
 
 
@@ -80,3 +81,13 @@ def test_strip_rows_cover_and_balance():
             assert all(a[1] == b[0] for a, b in zip(rows, rows[1:]))
             sizes = [b - a for a, b in rows]
             assert max(sizes) - min(sizes) <= 1
+
+
+def test_graph_halo_is_the_row_bandwidth():
+    from paper_1604_06525_b200 import EdgeTable
+    from paper_1604_06525_b200.sharded import graph_halo_rows
+    prob = workloads.arap_mesh(9, nhandles=4)  # 9x9 grid mesh, vertex = r * 9 + c
+    assert graph_halo_rows(prob.graphs, 1) == 9
+    assert graph_halo_rows([EdgeTable(3, np.array([0, 5, 2, 7, 7, 7], np.uint64))], 2) == 2
+    plan = load_plan(prob.name, dims=prob.dims)
+    assert layout(plan, prob.data(np.float64)).halo == 9

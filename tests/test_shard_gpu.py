@@ -15,6 +15,8 @@ CASES = {
     "poisson": (lambda: workloads.poisson(40, 24), "gn"),
     "arap_warp": (lambda: workloads.arap_warp(48, 20, nhandles=6), "gn"),
     "sfs": (lambda: workloads.sfs(36, 20), "lm"),
+    # graph energy: vertex strips, halo = the mesh's row bandwidth (§8f rank 3)
+    "arap_mesh": (lambda: workloads.arap_mesh(12, nhandles=5), "gn"),
 }
 
 
