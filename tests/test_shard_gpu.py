@@ -17,6 +17,7 @@ CASES = {
     "sfs": (lambda: workloads.sfs(36, 20), "lm"),
     # graph energy: vertex strips, halo = the mesh's row bandwidth (§8f rank 3)
     "arap_mesh": (lambda: workloads.arap_mesh(12, nhandles=5), "gn"),
+    "arap_mesh_lm": (lambda: workloads.arap_mesh(12, nhandles=5, rows=17), "lm"),
 }
 
 
