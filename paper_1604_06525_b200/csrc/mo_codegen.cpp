@@ -599,7 +599,12 @@ struct Gen {
       os << "    const int r0 = T.o0 - " << H << ", c0 = 0; (void)c0;\n"
          << "    for (int k = tid; k < " << NE << "; k += MO_THREADS) {\n"
          << "      const int q0 = r0 + k, q1 = 0;\n";
-    os << "      if (it) mo_lanes_" << sfx << "<true>(P, q0, q1, k, CL, " << NE << "); else mo_lanes_" << sfx
+    // (a strip stores rows [row0 - R, row1 + R): elements no owned output
+    // needs are not evaluated, so no read leaves the strip's storage)
+    os << "      if (q0 < P.row0 - " << H << " || q0 >= P.row1 + " << H << ") {\n"
+       << "        for (int s = 0; s < " << NM << "; ++s) CL[s * " << NE << " + k] = (Real)0;\n"
+       << "        continue;\n      }\n"
+       << "      if (it) mo_lanes_" << sfx << "<true>(P, q0, q1, k, CL, " << NE << "); else mo_lanes_" << sfx
        << "<false>(P, q0, q1, k, CL, " << NE << ");\n"
        << "    }\n    __syncthreads();\n"
        << "    int p0, p1, p2;\n"
