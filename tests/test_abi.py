@@ -67,3 +67,18 @@ def test_no_cpu_fallback_without_gpu():
     with pytest.raises(_lib.MoError) as e:
         Solver(p, SolveData(x=np.zeros(p.num_cols), arrays=[np.zeros(192), np.zeros(64)]))
     assert e.value.code == "NoDevice"
+
+
+@pytest.mark.parametrize("name,mode", [("poisson", 0), ("poisson_mat", 1), ("arap_warp_math", 2), ("arap_mesh_mat", 1),
+                                       ("arap_mesh_math", 2)])
+def test_materialize_mode_travels_with_the_plan(name, mode):
+    """Materialize (plan.hpp:17) is fixed at plan time: a kJ / kJtJ plan
+    carries no gather J^T J programs (empty in the interchange) and keeps its
+    mode across set_config."""
+    from paper_1604_06525_b200 import SolveConfig
+    p = load_plan(name)
+    assert p.materialize == mode
+    q = load_plan(name, SolveConfig(nonlinear_iters=3, linear_iters=5))
+    assert q.materialize == mode
+    text = open(os.path.join(PLAN_DIR, name + ".moplan")).read()
+    assert ("program jtj 0 0 0 0 0" in text) == (mode != 0)
