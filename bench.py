@@ -124,6 +124,30 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
+def compute_roofline(info, units, avg_apply_us, nsm=148):
+    """The J^T J p program's arithmetic (add / mul / pow / unary ops of the
+    reference's gather program per element, planinfo n_arith) against the
+    FP32 CUDA-core issue rate: 128 lanes x SMs x max SM clock, one op per
+    lane-cycle (an FMA would count its two ops as one issue).  SURVEY §8d:
+    SFS (~18.7 op/B) sits above the HBM ridge, so it is reported here too."""
+    ops = None
+    for hdr, progs in info.sections:
+        if hdr.startswith("gather_set") and "jtj" in progs:
+            ops = progs["jtj"].n_arith
+            break
+    if ops is None or not avg_apply_us:
+        return None
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mhz = float(json.load(f)["sm_max_mhz"])
+    except Exception:
+        mhz = 1965.0
+    peak = 128 * nsm * mhz * 1e6 / 1e12
+    ach = ops * units / (avg_apply_us * 1e-6) / 1e12
+    return {"bound": "fp32 issue", "achieved": ach, "peak": peak, "unit": "Top/s", "frac": ach / peak,
+            "ops_per_elem": ops, "peak_kind": "derived: 128 FP32 lanes x SMs x sm_max_mhz"}
+
+
 def ncu_traffic(config, kernel):
     """dram bytes per J^T J p launch from the committed ncu summary of this
     round (profiles/ncu_summary.json, one `ncu --set full` capture of the
@@ -358,6 +382,8 @@ def run_ours(args):
                      "avg_launch_us": avg_apply * 1e3, "launches": apply_n,
                      "pcg_update_avg_us": upd_ms / max(upd_n, 1) * 1e3},
         "roofline_jtf": jtf_roofline(info, rb, units, bm_ms, bm_n, peak, prob),
+        "roofline_compute": compute_roofline(info, units, avg_apply * 1e3 if apply_n else None,
+                                             torch.cuda.get_device_properties(dev).multi_processor_count),
         "e2e": {"value": float(np.median(e2e)) / NL, "unit": "ms/iter", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
