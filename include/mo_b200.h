@@ -210,6 +210,24 @@ int mo_session_create_shard_halo(mo_plan p, int device, mo_comm c, int64_t row0,
                                  mo_session* out);
 int mo_session_local_layout(mo_session s, int64_t* lo, int64_t* hi, int64_t* row0, int64_t* row1);
 
+/* ---- standalone Jacobi PCG: pcg<Real>(apply_a, b, m, delta, opt, ws,
+ * excluded) (pcg.hpp:59-130) with PcgOptions / PcgOutcome (pcg.hpp:12-24).
+ * The operator is the caller's: `apply(x, y, stream, user)` gets DEVICE
+ * pointers of n Reals and must leave y = A x complete on return or enqueued
+ * on `stream` (a cudaStream_t).  b, m, delta (out) and excluded (uint8, may
+ * be NULL) are host buffers.  Numerical failures are flags, never errors. */
+typedef struct mo_pcg_options {
+  int max_iters;
+  double tol_rel, tol_abs;
+  int use_preconditioner;
+} mo_pcg_options;
+typedef struct mo_pcg_outcome {
+  int iterations, indefinite, nonfinite;
+} mo_pcg_outcome;
+typedef void (*mo_apply_fn)(const void* x, void* y, void* stream, void* user);
+int mo_pcg(int device, int precision, int64_t n, mo_apply_fn apply, void* user, const void* b, const void* m,
+           void* delta, const mo_pcg_options* opt, const uint8_t* excluded, mo_pcg_outcome* out);
+
 /* ---- measurement hooks (bench.py) -------------------------------------- */
 /* When enabled, CUDA events bracket every J^T J p apply and PCG vector update
  * launched by mo_solve (on the session stream, also inside CUDA graphs). */

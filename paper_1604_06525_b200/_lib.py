@@ -41,6 +41,15 @@ class SolveResultC(ctypes.Structure):
 
 
 ITER_CB = ctypes.CFUNCTYPE(None, c_int, c_void_p, c_void_p)
+APPLY_FN = ctypes.CFUNCTYPE(None, c_void_p, c_void_p, c_void_p, c_void_p)
+
+
+class PcgOptionsC(ctypes.Structure):
+    _fields_ = [("max_iters", c_int), ("tol_rel", c_double), ("tol_abs", c_double), ("use_preconditioner", c_int)]
+
+
+class PcgOutcomeC(ctypes.Structure):
+    _fields_ = [("iterations", c_int), ("indefinite", c_int), ("nonfinite", c_int)]
 
 # Every symbol include/mo_b200.h declares, with its argument types.
 SIGNATURES = {
@@ -98,6 +107,8 @@ SIGNATURES = {
     "mo_kernel_launches": (c_int, [c_void_p, ctypes.POINTER(c_int64)]),
     "mo_apply_kernel": (c_int, [c_void_p, c_int, ctypes.c_char_p, ctypes.c_size_t]),
     "mo_plan_materialize": (c_int, [c_void_p, ctypes.POINTER(c_int)]),
+    "mo_pcg": (c_int, [c_int, c_int, c_int64, APPLY_FN, c_void_p, c_void_p, c_void_p, c_void_p,
+                       ctypes.POINTER(PcgOptionsC), c_void_p, ctypes.POINTER(PcgOutcomeC)]),
     "mo_linearize": (c_int, [c_void_p]),
     "mo_jacobian_size": (c_int, [c_void_p] + [ctypes.POINTER(c_int64)] * 3),
     "mo_get_jacobian": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64]),

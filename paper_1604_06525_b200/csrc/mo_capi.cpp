@@ -449,6 +449,23 @@ int mo_get_normal_matrix(mo_session s, int64_t* offs, int64_t* col, void* val, i
   });
 }
 
+int mo_pcg(int device, int precision, int64_t n, mo_apply_fn apply, void* user, const void* b, const void* m,
+           void* delta, const mo_pcg_options* opt, const uint8_t* excluded, mo_pcg_outcome* out) {
+  return guard([&] {
+    need(opt, "options");
+    need(out, "output");
+    mo::PcgOpts o;
+    o.max_iters = opt->max_iters;
+    o.tol_rel = opt->tol_rel;
+    o.tol_abs = opt->tol_abs;
+    o.use_preconditioner = opt->use_preconditioner != 0;
+    const mo::PcgOutcome r = mo::run_pcg(device, precision, n, apply, user, b, m, delta, o, excluded);
+    out->iterations = r.iterations;
+    out->indefinite = r.indefinite ? 1 : 0;
+    out->nonfinite = r.nonfinite ? 1 : 0;
+  });
+}
+
 int mo_apply_kernel(mo_session s, int gather_set, char* name, size_t len) {
   SESSION_CALL(need(name, "output"); const std::string k = s->impl->apply_kernel(gather_set);
                mo::check(len > k.size(), mo::Err::kShapeMismatch, "name buffer too small");

@@ -2469,6 +2469,105 @@ class Session final : public SessionBase {
   double* mu_h_ = nullptr;  // pinned staging of the LM radius
 };
 
+// ---------------------------------------------------------------- standalone PCG
+// pcg<Real>(apply_a, b, m, delta, opt, ws, excluded) (pcg.hpp:59-130) over
+// a caller-supplied operator: the session's PCG kernels (init, alpha from
+// p'Ap with the excluded outputs zeroed, update, direction), one host sync
+// per iteration for the stop test.  Not a hot path: the solver's own PCG
+// runs inside captured CUDA graphs with the generated J^T J p.
+namespace {
+template <class Real>
+PcgOutcome run_pcg_t(int device, int64_t n, PcgApply apply, void* user, const void* b, const void* m, void* delta,
+                     const PcgOpts& o, const uint8_t* excluded) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    fail(Err::kNoDevice, "no CUDA device available (the B200 path has no CPU fallback)");
+  check(device >= 0 && device < ndev, Err::kNoDevice, "device index out of range");
+  check(n >= 0, Err::kShapeMismatch, "pcg operand sizes do not match");
+  CK(cudaSetDevice(device));
+  int nsm = 0;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  const size_t N = size_t(std::max<int64_t>(n, 1));
+  std::vector<void*> owned;
+  auto alloc = [&](size_t bytes) {
+    void* q = nullptr;
+    CK(cudaMalloc(&q, std::max<size_t>(bytes, 16)));
+    owned.push_back(q);
+    return q;
+  };
+  Real* bd = static_cast<Real*>(alloc(N * sizeof(Real)));
+  Real* md = static_cast<Real*>(alloc(N * sizeof(Real)));
+  Real* dd = static_cast<Real*>(alloc(N * sizeof(Real)));
+  Real* r = static_cast<Real*>(alloc(N * sizeof(Real)));
+  Real* p = static_cast<Real*>(alloc(N * sizeof(Real)));
+  Real* ap = static_cast<Real*>(alloc(N * sizeof(Real)));
+  unsigned char* cm = excluded ? static_cast<unsigned char*>(alloc(N)) : nullptr;
+  mo_state* state = static_cast<mo_state*>(alloc(sizeof(mo_state)));
+  double* partials = static_cast<double*>(alloc(2 * size_t(kPartCap) * sizeof(double)));
+  mo_state h{};
+  h.tol_rel = o.tol_rel;
+  h.tol_abs = o.tol_abs;
+  h.use_precond = o.use_preconditioner;
+  PcgOutcome out;
+  try {
+    if (n) {
+      CK(cudaMemcpyAsync(bd, b, size_t(n) * sizeof(Real), cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(md, m, size_t(n) * sizeof(Real), cudaMemcpyHostToDevice, st));
+      if (cm) CK(cudaMemcpyAsync(cm, excluded, size_t(n), cudaMemcpyHostToDevice, st));
+    }
+    CK(cudaMemcpyAsync(state, &h, sizeof(mo_state), cudaMemcpyHostToDevice, st));
+    const int vg = vgrid(std::max<int64_t>(n, 1), nsm);
+    auto red = [&](int op) {
+      mo_red R;
+      R.partials = partials;
+      R.counter = &state->counters[0];
+      R.state = state;
+      R.part_base = 0;
+      R.part_total = vg;
+      R.fin_op = op;
+      R.fin_arg = 0;
+      return R;
+    };
+    const int pre = o.use_preconditioner ? 1 : 0;
+    k_pcg_init<Real><<<vg, MO_THREADS, 0, st>>>(red(MO_FIN_PCG_INIT), n, cm, bd, md, dd, r, p, pre);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(&h, state, sizeof(mo_state), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int k = 0; k < o.max_iters && !h.done; ++k) {
+      apply(p, ap, st, user);  // y = A x, complete on return or enqueued on `st`
+      k_apply_finish<Real><<<vg, MO_THREADS, 0, st>>>(red(MO_FIN_PCG_ALPHA), n, cm, p, nullptr, ap,
+                                                        MO_F_ZEROEXCL | MO_F_REDUCE);
+      k_pcg_update<Real><<<vg, MO_THREADS, 0, st>>>(red(MO_FIN_PCG_BETA), n, cm, md, dd, r, p, ap, pre, nullptr, 0, k);
+      k_pcg_p<Real><<<vg, MO_THREADS, 0, st>>>(state, n, cm, md, r, p, pre, nullptr, 0, k);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(&h, state, sizeof(mo_state), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+    }
+    if (n) CK(cudaMemcpyAsync(delta, dd, size_t(n) * sizeof(Real), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    out.iterations = h.iters;
+    out.indefinite = h.indefinite != 0;
+    out.nonfinite = h.nonfinite != 0;
+  } catch (...) {
+    for (void* q : owned) cudaFree(q);
+    cudaStreamDestroy(st);
+    throw;
+  }
+  for (void* q : owned) cudaFree(q);
+  cudaStreamDestroy(st);
+  return out;
+}
+}  // namespace
+
+PcgOutcome run_pcg(int device, int precision, int64_t n, PcgApply apply, void* user, const void* b, const void* m,
+                   void* delta, const PcgOpts& opt, const uint8_t* excluded) {
+  check(apply != nullptr, Err::kBindError, "pcg needs an operator");
+  if (precision == 0) return run_pcg_t<float>(device, n, apply, user, b, m, delta, opt, excluded);
+  return run_pcg_t<double>(device, n, apply, user, b, m, delta, opt, excluded);
+}
+
 std::unique_ptr<SessionBase> make_session(const Plan& plan, int device) {
   if (plan.cfg.precision == 0) return std::make_unique<Session<float>>(plan, device);
   return std::make_unique<Session<double>>(plan, device);

@@ -68,6 +68,20 @@ class SessionBase {
   virtual void local_layout(int64_t* lo, int64_t* hi, int64_t* row0, int64_t* row1) const = 0;
 };
 
+// Standalone Jacobi PCG (pcg.hpp:12-130) over a caller's operator.
+struct PcgOpts {  // PcgOptions defaults (pcg.hpp:12-17)
+  int max_iters = 10;
+  double tol_rel = 1e-3, tol_abs = 0.0;
+  bool use_preconditioner = true;
+};
+struct PcgOutcome {
+  int iterations = 0;
+  bool indefinite = false, nonfinite = false;
+};
+using PcgApply = void (*)(const void* x, void* y, void* stream, void* user);
+PcgOutcome run_pcg(int device, int precision, int64_t n, PcgApply apply, void* user, const void* b, const void* m,
+                   void* delta, const PcgOpts& opt, const uint8_t* excluded);
+
 class Comm;
 std::unique_ptr<SessionBase> make_session(const Plan& plan, int device);
 // Strip shard owning rows [row0, row1) of the plan's grid domain; `comm` must

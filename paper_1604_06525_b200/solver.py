@@ -399,3 +399,44 @@ class Solver:
         n = ctypes.c_int64()
         call("mo_kernel_launches", self._h, ctypes.byref(n))
         return n.value
+
+
+@dataclass
+class PcgOutcome:
+    """PcgOutcome (pcg.hpp:19-24)."""
+    iterations: int = 0
+    indefinite: bool = False
+    nonfinite: bool = False
+
+
+def pcg(apply, b, m, max_iters: int = 10, tol_rel: float = 1e-3, tol_abs: float = 0.0,
+        use_preconditioner: bool = True, excluded=None, device: int = 0):
+    """pcg<Real>(apply_a, b, m, delta, opt, ws, excluded) (pcg.hpp:59-130) on
+    the device, defaults of PcgOptions (pcg.hpp:12-17).  `apply(x, y, stream)`
+    receives device pointers (int) of len(b) Reals and must leave y = A x
+    complete on return (or enqueued on the cudaStream_t `stream`).  Real is
+    b's dtype (float32 / float64).  Returns (delta, PcgOutcome)."""
+    b = np.ascontiguousarray(b)
+    dt = np.float32 if b.dtype == np.float32 else np.float64
+    b = b.astype(dt, copy=False)
+    m = _as(m, dt)
+    if m.size != b.size:
+        raise MoError(10, "pcg operand sizes do not match")
+    delta = np.zeros(b.size, dt)
+    ex = None if excluded is None else np.ascontiguousarray(excluded, np.uint8)
+    err = []
+
+    def tramp(x, y, stream, _user):
+        try:
+            apply(x, y, stream)
+        except Exception as e:  # surfaced after mo_pcg returns
+            err.append(e)
+
+    cb = _lib.APPLY_FN(tramp)
+    opt = _lib.PcgOptionsC(int(max_iters), float(tol_rel), float(tol_abs), int(bool(use_preconditioner)))
+    out = _lib.PcgOutcomeC()
+    call("mo_pcg", int(device), 0 if dt == np.float32 else 1, b.size, cb, None, b.ctypes.data, m.ctypes.data,
+         delta.ctypes.data, ctypes.byref(opt), None if ex is None else ex.ctypes.data, ctypes.byref(out))
+    if err:
+        raise err[0]
+    return delta, PcgOutcome(out.iterations, bool(out.indefinite), bool(out.nonfinite))
