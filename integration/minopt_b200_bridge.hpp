@@ -312,21 +312,23 @@ class Solver {
   }
   // linearize() / jacobian() (solver.hpp:291-382): lanes evaluated on the
   // device, the CSR assembled exactly as the reference assembles it.
-  void linearize() {
-    ok(mo_linearize(s_));
-    J_ = SparseCSR<Real>{};
+  void linearize() { ok(mo_linearize(s_)); }
+  // (fetched on every call: like the reference it throws kBindError once a
+  // refresh - e.g. the end of solve() - has invalidated the linearization)
+  const SparseCSR<Real>& jacobian() const {
     int64_t rows = 0, cols = 0, nnz = 0;
     ok(mo_jacobian_size(s_, &rows, &cols, &nnz));
+    J_ = SparseCSR<Real>{};
     J_.rows = rows;
     J_.cols = cols;
     J_.offs.resize(size_t(rows) + 1);
     J_.col.resize(size_t(nnz));
     J_.val.resize(size_t(nnz));
     ok(mo_get_jacobian(s_, J_.offs.data(), J_.col.data(), J_.val.data(), nnz));
+    return J_;
   }
-  const SparseCSR<Real>& jacobian() const { return J_; }
   // normal_matrix() (solver.hpp:383-387): kJtJ sessions
-  const SparseCSR<Real>& normal_matrix() {
+  const SparseCSR<Real>& normal_matrix() const {
     int64_t nnz = 0;
     ok(mo_normal_matrix_size(s_, &nnz));
     H_ = SparseCSR<Real>{};
@@ -382,7 +384,7 @@ class Solver {
   mo_session s_ = nullptr;
   std::vector<Real> b_, m_;
   std::vector<uint8_t> excl_;
-  SparseCSR<Real> J_, H_;
+  mutable SparseCSR<Real> J_, H_;
   const std::function<void(int, SolveData<Real>&)>* cb_ = nullptr;
 };
 

@@ -132,6 +132,13 @@ energy 0.5 * (X(0) - X(1))
   const SparseCSR<double>& h = sh.normal_matrix();
   CHECK(h.rows == 9 && h.offs.size() == 10 && h.nnz() == 25);  // tridiagonal 9x9
   SolveResult rn = sn.solve(), rj = sj.solve(), rh = sh.solve();
+  bool stale = false;
+  try {
+    (void)sj.jacobian();  // solve() ends with refresh(): the linearization is gone (solver.hpp:167, 379)
+  } catch (const Error& e) {
+    stale = e.code() == Err::kBindError;
+  }
+  CHECK(stale);
   CHECK(approx(rn.final_cost, rj.final_cost, 1e-10));
   CHECK(approx(rn.final_cost, rh.final_cost, 1e-10));
   for (int i = 0; i < 9; ++i) {
