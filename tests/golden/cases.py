@@ -124,9 +124,11 @@ def unit_cases():
     C["mat_ops_f32"] = dict(C["mat_ops"], prec="f32")
     C["mat_volume"] = dict(C["volume"], cfg=dict(nl=2, materialize="j"), cmds=lin)
     C["mat_tri_graph"] = dict(C["tri_graph"], cfg=dict(nl=3, lin=6, materialize="j"), cmds=lin)
+    C["mat_cached"] = dict(C["cached"], cfg=dict(materialize="j"), cmds=lin)  # cache-mode computed array
+    C["mat_freeze"] = dict(C["freeze"], cfg=dict(materialize="j"), cmds=["cost", "normal", "linearize", "jtj"])
     # Materialize::kJtJ (H = 2 J^T J assembled, solver.hpp:370-374)
     for k in ("sinchain", "sinchain_lm", "graph_degenerate", "exclude", "dense", "ops", "ops_f32", "volume",
-              "tri_graph"):
+              "tri_graph", "cached", "freeze"):
         c = dict(C["mat_" + k])
         c["cfg"] = dict(c["cfg"], materialize="jtj")
         C["math_" + k] = c
