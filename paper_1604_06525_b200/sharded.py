@@ -12,7 +12,8 @@ takes the same alpha/beta.
 Graph energies whose vertices are the domain's elements (the ARAP mesh) shard
 as vertex ranges: the halo is the graph's row bandwidth (graph_halo_rows), a
 strip keeps every edge touching its rows and counts only its own edges in
-the cost.
+the cost.  `reorder=True` first renumbers the vertices by reverse
+Cuthill-McKee (VertexOrder), so any mesh gets a small halo.
 
     # one process per GPU (torchrun), NCCL underneath:
     s = ShardedSolver(plan, global_data, rank, world, device)
@@ -119,13 +120,69 @@ def assemble_x(plan: CompiledPlan, owned: List[List[np.ndarray]]) -> np.ndarray:
     return np.concatenate([np.concatenate([o[f] for o in owned]) for f in range(len(L.unknown_ch))])
 
 
+class VertexOrder:
+    """Reverse Cuthill-McKee renumbering of a graph energy's vertex domain, so
+    that vertex strips need only a small halo (the renumbered bandwidth) on
+    any mesh, not just banded ones.  Valid when the domain is 1-D and no grid
+    program reads it at a nonzero offset (per-vertex terms only, like the ARAP
+    mesh's fit): then the energy is invariant under the permutation."""
+
+    def __init__(self, plan: CompiledPlan, data: SolveData):
+        from scipy.sparse import coo_matrix
+        from scipy.sparse.csgraph import reverse_cuthill_mckee
+        L = layout(plan)
+        if L.S != 1 or L.halo != 0:
+            raise ValueError("vertex renumbering needs a 1-D domain read at offset 0 only")
+        n = L.d0
+        rows, cols = [], []
+        for g in data.graphs:
+            v = np.asarray(g.verts, np.int64).reshape(-1, g.arity)
+            for a in range(g.arity):
+                for b in range(g.arity):
+                    if a != b:
+                        rows.append(v[:, a])
+                        cols.append(v[:, b])
+        r = np.concatenate(rows) if rows else np.zeros(0, np.int64)
+        c = np.concatenate(cols) if cols else np.zeros(0, np.int64)
+        adj = coo_matrix((np.ones(r.size, np.int8), (r, c)), shape=(n, n)).tocsr()
+        self.perm = np.asarray(reverse_cuthill_mckee(adj, symmetric_mode=True), np.int64)  # new -> old
+        self.inv = np.empty(n, np.int64)
+        self.inv[self.perm] = np.arange(n)  # old -> new
+        self.L = L
+
+    def apply(self, data: SolveData) -> SolveData:
+        """The same problem with vertex i renamed inv[i]."""
+        L, n = self.L, self.L.d0
+        x, off, parts = np.asarray(data.x), 0, []
+        for C in L.unknown_ch:
+            parts.append(x[off:off + n * C].reshape(n, C)[self.perm].reshape(-1))
+            off += n * C
+        arrays = [np.asarray(a).reshape(n, C)[self.perm].reshape(-1) for a, C in zip(data.arrays, L.array_ch)]
+        graphs = [EdgeTable(g.arity, self.inv[np.asarray(g.verts, np.int64)].astype(np.uint64)) for g in data.graphs]
+        return SolveData(x=np.concatenate(parts) if parts else x[:0], arrays=arrays, params=list(data.params),
+                         graphs=graphs)
+
+    def restore_x(self, xp: np.ndarray) -> np.ndarray:
+        """x in the caller's vertex numbering from the renumbered x."""
+        L, n, off, parts = self.L, self.L.d0, 0, []
+        for C in L.unknown_ch:
+            f = np.empty((n, C), xp.dtype)
+            f[self.perm] = xp[off:off + n * C].reshape(n, C)
+            parts.append(f.reshape(-1))
+            off += n * C
+        return np.concatenate(parts) if parts else xp[:0]
+
+
 class LocalShardGroup:
     """`world` strip sessions of one plan on one GPU, driven from one host
     thread each (the LocalComm transport): the single-device fake that tests
     the exact partition / halo / reduction schedule the NCCL path runs."""
 
-    def __init__(self, plan: CompiledPlan, data: SolveData, world: int, device: int = 0):
+    def __init__(self, plan: CompiledPlan, data: SolveData, world: int, device: int = 0, reorder: bool = False):
         self.plan, self.world = plan, world
+        self.order = VertexOrder(plan, data) if reorder else None
+        if self.order:
+            data = self.order.apply(data)
         L = layout(plan, data)
         self.halo = L.halo
         self._w = ctypes.c_void_p()
@@ -167,8 +224,9 @@ class LocalShardGroup:
         return self._parallel(lambda s: s.cost())
 
     def gather_x(self):
-        return assemble_x(self.plan, [owned_x(self.plan, s.get_x(), *rw, halo=self.halo)
-                                      for s, rw in zip(self.solvers, self.rows)])
+        x = assemble_x(self.plan, [owned_x(self.plan, s.get_x(), *rw, halo=self.halo)
+                                   for s, rw in zip(self.solvers, self.rows)])
+        return self.order.restore_x(x) if self.order else x
 
     def close(self):
         for s in self.solvers:
@@ -191,9 +249,13 @@ class ShardedSolver:
     is broadcast with torch.distributed, halos and partials then travel over
     NCCL on the session's stream."""
 
-    def __init__(self, plan: CompiledPlan, data: SolveData, rank: int, world: int, device: int):
+    def __init__(self, plan: CompiledPlan, data: SolveData, rank: int, world: int, device: int,
+                 reorder: bool = False):
         import torch.distributed as dist
         self.plan, self.rank, self.world = plan, rank, world
+        self.order = VertexOrder(plan, data) if reorder else None  # deterministic: same on every rank
+        if self.order:
+            data = self.order.apply(data)
         L = layout(plan, data)
         self.halo = L.halo
         uid = (ctypes.c_char * 128)()
@@ -216,4 +278,5 @@ class ShardedSolver:
         mine = owned_x(self.plan, self.solver.get_x(), *self.rows, halo=self.halo)
         allp = [None] * self.world
         dist.all_gather_object(allp, mine)
-        return assemble_x(self.plan, allp)
+        x = assemble_x(self.plan, allp)
+        return self.order.restore_x(x) if self.order else x

@@ -105,3 +105,33 @@ def test_single_strip_equals_unsharded_bitwise():
         g.close()
     assert [t.cost for t in r.trace] == [t.cost for t in ref.trace]
     np.testing.assert_array_equal(x, ref_data.x)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_scrambled_mesh_strips_with_rcm(world):
+    """Any vertex numbering: the strips renumber by reverse Cuthill-McKee
+    (halo = the renumbered bandwidth) and still reproduce the unsharded solve
+    of the caller's numbering."""
+    from paper_1604_06525_b200 import EdgeTable, SolveData
+    prob = workloads.arap_mesh(16, nhandles=6)
+    n = 256
+    p = np.random.default_rng(7).permutation(n)
+    inv = np.argsort(p)
+    d = prob.data(np.float64)
+    data = SolveData(x=d.x.reshape(2, n, 3)[:, inv].reshape(-1), arrays=[a.reshape(n, 3)[inv].reshape(-1) for a in d.arrays],
+                     params=d.params, graphs=[EdgeTable(2, p[np.asarray(g.verts, np.int64)].astype(np.uint64))
+                                              for g in d.graphs])
+    c = cfg("gn", "f64")
+    ref_data = SolveData(x=data.x.copy(), arrays=data.arrays, params=data.params, graphs=data.graphs)
+    ref = Solver(load_plan(prob.name, c, prob.dims), ref_data).solve()
+    g = LocalShardGroup(load_plan(prob.name, c, prob.dims), data, world, reorder=True)
+    try:
+        assert g.halo < 40
+        results = g.solve()
+        x = g.gather_x()
+    finally:
+        g.close()
+    for r in results:
+        for a, b in zip(r.trace, ref.trace):
+            assert abs(a.cost - b.cost) <= 1e-9 * abs(b.cost), (a.cost, b.cost)
+    np.testing.assert_allclose(x, ref_data.x, rtol=1e-8, atol=1e-8)
