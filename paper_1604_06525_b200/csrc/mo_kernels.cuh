@@ -460,23 +460,26 @@ __device__ __forceinline__ int mo_mat_find(const mo_mat_tables& T, long long r) 
 template <class Real>
 __global__ void __launch_bounds__(MO_THREADS) k_mat_check(const __grid_constant__ mo_mat_tables G, mo_state* st) {
   MO_PDL_ENTRY();
-  const mo_mat_tables T = mo_mat_stage(G);
+  // gridDim.y = template (as k_mat_rows); graph rows need no check
+  const mo_mat_tmpl M = G.tm[blockIdx.y];
+  if (M.kind != 0) return;
+  __shared__ mo_mat_lane sl[MO_MAT_MAXL];
+  const int nl = M.nlanes < MO_MAT_MAXL ? M.nlanes : MO_MAT_MAXL;
+  if (threadIdx.x < nl) sl[threadIdx.x] = G.lanes[M.lane0 + threadIdx.x];
+  __syncthreads();
   int bad = 0;
-  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < T.nrows;
-       r += (long long)gridDim.x * blockDim.x) {
-    const mo_mat_tmpl M = T.tm[mo_mat_find(T, r)];
-    if (M.kind != 0) continue;
-    const long long e = r - M.rowbase;
-    if (static_cast<const Real*>(M.buf)[(long long)M.guard * M.nrows + e] == Real(0)) continue;
+  const Real* buf = static_cast<const Real*>(M.buf);
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < M.nrows;
+       e += (long long)gridDim.x * blockDim.x) {
+    if (buf[(long long)M.guard * M.nrows + e] == Real(0)) continue;
     long long prev = -1;
-    for (int k = 0; k < M.nlanes; ++k) {
-      const mo_mat_lane L = T.lanes[M.lane0 + k];
-      const long long el = e + L.lin;
+    for (int k = 0; k < nl; ++k) {
+      const long long el = e + sl[k].lin;
       if (el < 0 || el >= M.nrows) {
         bad |= 1;
         continue;
       }
-      const long long col = T.ubase[L.field] + el * T.chans[L.field] + L.ch;
+      const long long col = G.ubase[sl[k].field] + el * G.chans[sl[k].field] + sl[k].ch;
       if (col <= prev) bad |= 2;
       prev = col;
     }

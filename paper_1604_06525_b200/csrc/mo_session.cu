@@ -2013,9 +2013,9 @@ class Session final : public SessionBase {
     mt_smem_ = r16(sizeof(mo_mat_tmpl) * NT) + r16(sizeof(mo_mat_lane) * lanes.size()) +
                r16(sizeof(mo_mat_centry) * ce.size()) + r16(sizeof(int) * ceptr.size());
     check(mt_smem_ <= 200 * 1024, Err::kBindError, "materialized J: lane tables exceed shared memory");
-    if (mt_smem_ > 48 * 1024)
-      for (const void* f : {(const void*)k_mat_check<Real>, (const void*)k_mat_hbuild<Real>})
-        CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(mt_smem_)));
+    if (mt_smem_ > 48 * 1024)  // (k_mat_hbuild stages the tables)
+      CK(cudaFuncSetAttribute((const void*)k_mat_hbuild<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              int(mt_smem_)));
     if (mat_ == 2) {  // ELL width of H = 2 J^T J: an upper bound on the row widths
       std::vector<std::set<std::tuple<int, int, long long>>> S(size_t(cbase.back()));
       for (size_t t = 0; t < NT; ++t) {
@@ -2087,7 +2087,7 @@ class Session final : public SessionBase {
       grid_rows = true;
     }
     if (grid_rows && mt_ok_ && rows_ > 0) {
-      kls(k_mat_check<Real>, dim3(vgrid(rows_, nsm_, 8)), dim3(MO_THREADS), mt_smem_, mt_, state_);
+      kl(k_mat_check<Real>, mat_grid(max_trows_, mt_.ntm), dim3(MO_THREADS), mt_, state_);
       ++launches_;
     }
     bool pending_h = mat_ == 2;
