@@ -399,7 +399,7 @@ def run_ours(args):
     if prob.method == "lm":  # per trial (trace row) and the accept/reject sequence
         line["lm"] = {"trials_per_solve": len(accepted), "ms_per_trial": step_ms / max(1, len(accepted)),
                       "accept_sequence": "".join("A" if a else "R" for a in accepted)}
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:  # (contract: rank 0 at N=1 only)
         try:
             threads = os.cpu_count() or 1
             if prob.method == "lm":
