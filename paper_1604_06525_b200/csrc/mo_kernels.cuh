@@ -403,7 +403,7 @@ struct mo_mat_lane {
   long long lin;  // grid: linearised stencil offset
 };
 struct mo_mat_centry {  // one source of entries of a (field, channel) column
-  int t, lane;          // grid: the lane; graph: -1 (scan the template's lanes per edge)
+  int t, lane;          // grid: the lane; graph: ~(bitmask of the template's lanes on this column)
 };
 struct mo_mat_tables {
   const mo_mat_tmpl* tm;
@@ -581,11 +581,13 @@ k_mat_cols(const __grid_constant__ mo_mat_tables G, const mo_state* st, int skip
   __shared__ const Real* s_grd[MO_MAT_MAXCE];
   __shared__ long long s_rb[MO_MAT_MAXCE], s_lin[MO_MAT_MAXCE], s_n[MO_MAT_MAXCE];
   __shared__ int s_t[MO_MAT_MAXCE];
+  __shared__ unsigned s_mask[MO_MAT_MAXCE];
   for (int c = threadIdx.x; c < nce; c += blockDim.x) {
     const mo_mat_centry E = G.ce[c0 + c];
     const mo_mat_tmpl& M = G.tm[E.t];
     const Real* buf = static_cast<const Real*>(M.buf);
     s_t[c] = E.lane >= 0 ? -1 : E.t;
+    s_mask[c] = E.lane >= 0 ? 0u : ~unsigned(E.lane);
     s_rb[c] = M.rowbase;
     s_n[c] = M.nrows;
     if (E.lane >= 0) {
@@ -628,9 +630,9 @@ k_mat_cols(const __grid_constant__ mo_mat_tables G, const mo_state* st, int skip
           const int e = M.vedge[j];
           bool has = false;
           Real mv = Real(0);
-          for (int l = 0; l < M.nlanes; ++l) {
-            const mo_mat_lane L = G.lanes[M.lane0 + l];
-            if (L.field != f || L.ch != ch || M.verts[(long long)e * M.arity + L.slot] != el) continue;
+          for (unsigned mk = s_mask[c]; mk; mk &= mk - 1) {  // this column's lanes, in lane order
+            const mo_mat_lane L = G.lanes[M.lane0 + __ffs(mk) - 1];
+            if (M.verts[(long long)e * M.arity + L.slot] != el) continue;
             const Real val = buf[(long long)L.out * M.nrows + e];
             mv = has ? mo_add_rn(mv, val) : val;
             has = true;

@@ -1965,9 +1965,10 @@ class Session final : public SessionBase {
                          [&](int a, int b) { return lanes[size_t(a)].lin > lanes[size_t(b)].lin; });
         for (int k : idx) per[size_t(cbase[size_t(lanes[size_t(k)].field)] + lanes[size_t(k)].ch)].push_back({int(t), k});
       } else {
-        for (int k : idx) {
+        for (int k : idx) {  // one entry per (template, column pair): ~mask of its lanes
           auto& v = per[size_t(cbase[size_t(lanes[size_t(k)].field)] + lanes[size_t(k)].ch)];
-          if (v.empty() || v.back().t != int(t)) v.push_back({int(t), -1});
+          if (v.empty() || v.back().t != int(t)) v.push_back({int(t), ~0});
+          v.back().lane = ~(~v.back().lane | int(1u << unsigned(k - M.lane0)));
         }
       }
     }
