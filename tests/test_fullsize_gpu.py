@@ -182,3 +182,24 @@ def test_config4_mesh_vertex_strips(prec):
         for row, rc in zip(r.trace, ref["trace_cost"]):
             assert abs(row.cost - rc) <= tol * abs(rc), (row.cost, rc)
         assert abs(r.final_cost - float(ref["final_cost"][0])) <= tol * abs(float(ref["final_cost"][0]))
+
+
+def test_config5_arap_8192_strips_one_iteration():
+    """Config 5 at its full size: ARAP warp 8192² (201M unknowns) in 4 axis-0
+    strips, one GN iteration x 2 PCG (the reference takes minutes
+    per full iteration at this size) against the unmodified reference."""
+    from paper_1604_06525_b200.sharded import LocalShardGroup
+    prob = workloads.arap_warp(8192, 8192)
+    nl, lin = 1, 2
+    ref = pyoracle.run_ref(prob.energy, prob.data(np.float32), ["solve"], dims=prob.dims, prec="f32", nl=nl, lin=lin,
+                           rel=0.0, abs_tol=0.0, cost_stop=0.0, exec_mode="par", threads=THREADS)
+    g = LocalShardGroup(load_plan(prob.name, _cfg(prob, "f32", nl, lin), prob.dims), prob.data(np.float32), 4)
+    try:
+        results = g.solve()
+    finally:
+        g.close()
+    for r in results:
+        assert [t.pcg_iters for t in r.trace] == list(ref["trace_pcg"])
+        for row, rc in zip(r.trace, ref["trace_cost"]):
+            assert abs(row.cost - rc) <= 1e-4 * abs(rc), (row.cost, rc)
+        assert abs(r.final_cost - float(ref["final_cost"][0])) <= 1e-4 * abs(float(ref["final_cost"][0]))
