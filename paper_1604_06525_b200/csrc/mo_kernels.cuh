@@ -397,6 +397,7 @@ struct mo_mat_tmpl {
   const int* vptr;           // graph: vertex -> incident edges (unique, ascending)
   const int* vedge;
   long long nverts;
+  long long eoff, ecoff;     // kJtJ graph: offsets of this template's merged edge rows / counts (k_mat_erows)
 };
 struct mo_mat_lane {
   int out, field, ch, slot;
@@ -666,11 +667,54 @@ __device__ __forceinline__ void mo_h_acc(long long* cols, Real* vals, int& n, in
   vals[n] = mo_add_rn(Real(0), p);
   ++n;
 }
+// kJtJ: each graph row's sorted, merged entries, once per edge (slot-major:
+// entry k of edge e of template t at eoff + k * E + e); k_mat_hbuild reads
+// them for every column the row holds instead of re-sorting per column.
+template <class Real>
+__global__ void __launch_bounds__(MO_THREADS)
+k_mat_erows(const __grid_constant__ mo_mat_tables G, int* __restrict__ ecol, Real* __restrict__ eval,
+            unsigned char* __restrict__ ecnt) {
+  MO_PDL_ENTRY();
+  const mo_mat_tmpl M = G.tm[blockIdx.y];
+  if (M.kind != 1) return;
+  const Real* buf = static_cast<const Real*>(M.buf);
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < M.nrows;
+       e += (long long)gridDim.x * blockDim.x) {
+    long long rc[MO_MAT_MAXL];
+    Real rv[MO_MAT_MAXL];
+    int rn = 0;
+    for (int l = 0; l < M.nlanes; ++l) {
+      const mo_mat_lane B = G.lanes[M.lane0 + l];
+      const long long col = G.ubase[B.field] + (long long)M.verts[e * M.arity + B.slot] * G.chans[B.field] + B.ch;
+      const Real val = buf[(long long)B.out * M.nrows + e];
+      int x = rn++;
+      while (x > 0 && rc[x - 1] > col) {
+        rc[x] = rc[x - 1];
+        rv[x] = rv[x - 1];
+        --x;
+      }
+      rc[x] = col;
+      rv[x] = val;
+    }
+    int w = 0;
+    for (int k = 0; k < rn;) {
+      const long long col = rc[k];
+      Real mv = rv[k];
+      for (++k; k < rn && rc[k] == col; ++k) mv = mo_add_rn(mv, rv[k]);
+      ecol[M.eoff + (long long)w * M.nrows + e] = int(col);
+      eval[M.eoff + (long long)w * M.nrows + e] = mv;
+      ++w;
+    }
+    ecnt[M.ecoff + e] = (unsigned char)w;
+  }
+}
+
 #define MO_MAT_MAXK 64
 template <class Real>
 __global__ void __launch_bounds__(128)
 k_mat_hbuild(const __grid_constant__ mo_mat_tables G, mo_state* st, int K, int* __restrict__ hcol,
-             Real* __restrict__ hval, int* __restrict__ hcnt) {
+             Real* __restrict__ hval, int* __restrict__ hcnt, const int* __restrict__ ecol,
+             const Real* __restrict__ eval, const unsigned char* __restrict__ ecnt) {
   MO_PDL_ENTRY();
   const mo_mat_tables T = mo_mat_stage(G);
   int bad = 0;
@@ -704,43 +748,22 @@ k_mat_hbuild(const __grid_constant__ mo_mat_tables G, mo_state* st, int K, int* 
         }
       } else {
         if (el >= M.nverts) continue;
+        (void)buf;
+        const long long eo = M.eoff, E = M.nrows;
+        const unsigned char* cnt = ecnt + M.ecoff;
         for (int j = M.vptr[el]; j < M.vptr[el + 1]; ++j) {
           const int e = M.vedge[j];
-          long long rc[MO_MAT_MAXL];
-          Real rv[MO_MAT_MAXL];
-          int rn = 0;
-          for (int l = 0; l < M.nlanes; ++l) {  // the row's entries, sorted (stable) and merged below
-            const mo_mat_lane B = T.lanes[M.lane0 + l];
-            const long long col =
-                T.ubase[B.field] + (long long)M.verts[(long long)e * M.arity + B.slot] * T.chans[B.field] + B.ch;
-            const Real val = buf[(long long)B.out * M.nrows + e];
-            int x = rn++;
-            while (x > 0 && rc[x - 1] > col) {
-              rc[x] = rc[x - 1];
-              rv[x] = rv[x - 1];
-              --x;
-            }
-            rc[x] = col;
-            rv[x] = val;
-          }
-          int w = 0;
-          for (int k = 0; k < rn;) {
-            const long long col = rc[k];
-            Real mv = rv[k];
-            for (++k; k < rn && rc[k] == col; ++k) mv = mo_add_rn(mv, rv[k]);
-            rc[w] = col;
-            rv[w] = mv;
-            ++w;
-          }
+          const int w = cnt[e];  // the row's sorted, merged entries (k_mat_erows)
           Real a = Real(0);
           bool has = false;
           for (int k = 0; k < w; ++k)
-            if (rc[k] == q) {
-              a = rv[k];
+            if (ecol[eo + k * E + e] == q) {
+              a = eval[eo + k * E + e];
               has = true;
             }
           if (!has) continue;
-          for (int k = 0; k < w; ++k) mo_h_acc(cols, vals, n, K, rc[k], mo_mul_rn(a, rv[k]), bad);
+          for (int k = 0; k < w; ++k)
+            mo_h_acc(cols, vals, n, K, (long long)ecol[eo + k * E + e], mo_mul_rn(a, eval[eo + k * E + e]), bad);
         }
       }
     }

@@ -204,6 +204,9 @@ class Session final : public SessionBase {
     cudaFree(hcol_);
     cudaFree(hval_);
     cudaFree(hcnt_);
+    cudaFree(ecol_);
+    cudaFree(eval_);
+    cudaFree(ecnt_);
     for (auto& kv : stage_ev_)
       for (auto& ev : kv.second) {
         cudaEventDestroy(ev.a);
@@ -1011,6 +1014,11 @@ class Session final : public SessionBase {
   size_t jtmp_cap_ = 0;
   size_t mt_smem_ = 0;         // staged table bytes (mo_mat_stage)
   long long max_trows_ = 1, max_fel_ = 1;
+  int* ecol_ = nullptr;  // kJtJ: merged graph rows (k_mat_erows)
+  Real* eval_ = nullptr;
+  unsigned char* ecnt_ = nullptr;
+  size_t erow_cap_ = 0, ecnt_cap_ = 0;
+  bool has_graph_rows_ = false;
   int* hcol_ = nullptr;  // kJtJ: H = 2 J^T J, slot-major ELL (int32 columns)
   Real* hval_ = nullptr;
   int* hcnt_ = nullptr;
@@ -1906,6 +1914,7 @@ class Session final : public SessionBase {
     std::vector<mo_mat_tmpl> tm(NT);
     std::vector<bool> seen(NT, false);
     std::vector<mo_mat_lane> lanes;
+    long long erow_n = 0, ecnt_n = 0;
     for (size_t i = 0; i < P_.grid_sets.size(); ++i) {
       const GridSet& g = P_.grid_sets[i];
       const auto sh = P_.shape_of(g.dom);
@@ -1946,6 +1955,10 @@ class Session final : public SessionBase {
         M.vptr = mat_vptr_[size_t(g.graph)];
         M.vedge = mat_vedge_[size_t(g.graph)];
         M.nverts = mat_nverts_[size_t(g.graph)];
+        M.eoff = erow_n;  // kJtJ: merged edge rows (k_mat_erows)
+        M.ecoff = ecnt_n;
+        erow_n += (long long)jt.lanes.size() * gd.E;
+        ecnt_n += gd.E;
         for (const Lane& l : jt.lanes) lanes.push_back({l.out, l.field, l.channel, l.slot, 0});
         seen[size_t(jt.tmpl)] = true;
       }
@@ -2017,6 +2030,18 @@ class Session final : public SessionBase {
     if (mt_smem_ > 48 * 1024)  // (k_mat_hbuild stages the tables)
       CK(cudaFuncSetAttribute((const void*)k_mat_hbuild<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               int(mt_smem_)));
+    if (mat_ == 2 && (size_t(erow_n) > erow_cap_ || size_t(ecnt_n) > ecnt_cap_)) {
+      cudaFree(ecol_);
+      cudaFree(eval_);
+      cudaFree(ecnt_);
+      ecol_ = dalloc<int>(size_t(std::max<long long>(erow_n, 1)));
+      eval_ = dalloc<Real>(size_t(std::max<long long>(erow_n, 1)));
+      ecnt_ = dalloc<unsigned char>(size_t(std::max<long long>(ecnt_n, 1)));
+      erow_cap_ = size_t(erow_n);
+      ecnt_cap_ = size_t(ecnt_n);
+      realloc = true;
+    }
+    has_graph_rows_ = ecnt_n > 0;
     if (mat_ == 2) {  // ELL width of H = 2 J^T J: an upper bound on the row widths
       std::vector<std::set<std::tuple<int, int, long long>>> S(size_t(cbase.back()));
       for (size_t t = 0; t < NT; ++t) {
@@ -2107,8 +2132,13 @@ class Session final : public SessionBase {
     }
     if (pending_h && mt_ok_) {  // assemble H = 2 J^T J (solver.hpp:370-374)
       const long long n = P_.num_cols;
+      if (has_graph_rows_) {
+        kl(k_mat_erows<Real>, mat_grid(max_trows_, mt_.ntm), dim3(MO_THREADS), mt_, ecol_, eval_, ecnt_);
+        ++launches_;
+      }
       kls(k_mat_hbuild<Real>, dim3(unsigned(std::max<long long>(1, std::min<long long>((n + 127) / 128, 8LL * nsm_)))),
-          dim3(128), mt_smem_, mt_, state_, hK_, hcol_, hval_, hcnt_);
+          dim3(128), mt_smem_, mt_, state_, hK_, hcol_, hval_, hcnt_, static_cast<const int*>(ecol_),
+          static_cast<const Real*>(eval_), static_cast<const unsigned char*>(ecnt_));
       ++launches_;
     }
     jvalid_ = true;
