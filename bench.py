@@ -1,22 +1,37 @@
 """Benchmark: ms per GN/LM iteration (fixed PCG iterations) of the matrix-free
-solver, plus the J^T J p kernel's achieved HBM bandwidth vs the measured peak.
+solver, plus the J^T J p / J^T F kernels' achieved HBM bandwidth vs the
+measured peak.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config arap_warp|poisson|sfs|arap_mesh] [--prec f32|f64]
+                    [--config arap_warp|poisson|sfs|arap_mesh] [--size S]
+                    [--prec f32|f64] [--scaling strong|weak]
 
-Workload (BASELINE.json configs[1], the metric's headline config): ARAP image
-warping 1024x1024 (Off:2 + Ang:1 unknowns, 3,145,728 columns), Gauss-Newton,
-10 nonlinear x 20 PCG iterations with pcg_rel_tol = pcg_abs_tol =
-cost_stop_tol = 0 so every iteration count is exact, fp32, synthetic seeded
-inputs (paper_1604_06525_b200/workloads.py).
+Headline workload (no flags): BASELINE.json configs[4], the largest
+single-GPU configuration: ARAP image warping 8192x8192 (Off:2 + Ang:1
+unknowns, 201,326,592 columns), Gauss-Newton, 10 nonlinear x 20 PCG
+iterations with pcg_rel_tol = pcg_abs_tol = cost_stop_tol = 0 so every
+iteration count is exact, fp32, synthetic seeded inputs
+(paper_1604_06525_b200/workloads.py).  `--size 1024` gives configs[1];
+`--config poisson` (512^2) configs[0], `--config poisson --size 8192` the
+Poisson half of configs[4], `--config sfs` / `--config arap_mesh` configs[2]
+/ configs[3].
 
 A step = one solve() (10 GN iterations) from the same initial state; the
-value is step time / 10.  Inputs are resident in HBM before the timer starts;
-L2 is flushed (256 MiB write) between timed steps.  `e2e` runs the same solve
-through the public API with host buffers (pinned H2D of x + arrays, D2H of x)
-inside the timed region.  `--impl reference` times the unmodified reference
-CPU solver (oracle/_ref/ref_driver, all host threads) on the same workload,
-one GN iteration per step.
+value is step time / 10.  Inputs are resident in HBM before the timer starts
+and far larger than L2 at 8192^2; L2 is also flushed (256 MiB write) between
+timed steps.  `e2e` runs the same solve through the public C ABI with host
+buffers (pinned H2D of x + arrays, D2H of x) inside the timed region.
+
+N > 1 (torchrun, one GPU per rank): `--scaling strong` (default) splits the
+SAME grid into N axis-0 strips (halo exchange + fixed-order reductions over
+NCCL), so the value is the whole problem's ms per iteration; `--scaling weak`
+gives every rank its own W x H strip of an (N*W) x H grid.
+
+`--impl reference` times the unmodified reference CPU solver
+(oracle/_ref/ref_driver, all host threads) on the same workload: one GN
+iteration per step, bounded so the arm ends within a few minutes (at 8192^2
+one GN iteration takes ~2 minutes; it is timed once).  That arm never loads
+libmo_b200.so.
 """
 import argparse
 import json
@@ -42,17 +57,24 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="arap_warp")
     ap.add_argument("--prec", default="f32", choices=["f32", "f64"])
-    ap.add_argument("--size", type=int, default=0, help="override grid edge (testing)")
+    ap.add_argument("--size", type=int, default=0, help="grid edge (arap_warp default 8192, poisson 512)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
 
-def make_problem(cfg_name, size=0, rows_mult=1):
+DEFAULT_SIZE = {"arap_warp": 8192, "poisson": 512}
+
+
+def make_problem(cfg_name, size=0, rows_mult=1, rows=0):
+    """The workload generator of a config.  rows_mult > 1: weak-scaling grid of
+    rows_mult x W rows.  rows > 0: a W' = rows strip of the same W x H
+    workload (bounded CPU samples)."""
     from paper_1604_06525_b200 import workloads
-    if cfg_name == "arap_warp":
-        return workloads.arap_warp((size or 1024) * rows_mult, size or 1024)
-    if cfg_name == "poisson":
-        return workloads.poisson((size or 512) * rows_mult, size or 512)
+    if cfg_name in DEFAULT_SIZE:
+        n = size or DEFAULT_SIZE[cfg_name]
+        gen = workloads.arap_warp if cfg_name == "arap_warp" else workloads.poisson
+        return gen(rows or n * rows_mult, n)
     if cfg_name == "arap_mesh" and rows_mult != 1:  # vertex strips: rows_mult x 448 rows of 448 vertices
         return workloads.arap_mesh(size or 448, 64 * rows_mult, rows=(size or 448) * rows_mult)
     if rows_mult != 1:
@@ -148,35 +170,48 @@ def compute_roofline(info, units, avg_apply_us, nsm=148):
             "ops_per_elem": ops, "peak_kind": "derived: 128 FP32 lanes x SMs x sm_max_mhz"}
 
 
-def ncu_traffic(config, kernel):
-    """dram bytes per J^T J p launch from the committed ncu summary of this
-    round (profiles/ncu_summary.json, one `ncu --set full` capture of the
-    same kernel on the same workload), if any."""
+def profile_key(prob):
+    """profiles/ncu_summary.json key of a workload: name_<axis-0 extent> for
+    2-D grids (arap_warp_8192, poisson_512), the name otherwise."""
+    d = list(prob.dims.values())
+    return f"{prob.name}_{d[0]}" if len(d) == 2 else prob.name
+
+
+def ncu_traffic(config, kernel, part="jtj"):
+    """dram bytes per launch of `kernel` from the committed ncu summary
+    (profiles/ncu_summary.json, one `ncu --set full` capture of the same
+    kernel on the same workload), if any."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
-            e = json.load(f)[config]["jtj"]
+            e = json.load(f)[config][part]
         return e["dram_bytes"] if e.get("kernel") == kernel else None
     except Exception:
         return None
 
 
-def jtf_roofline(info, rb, units, ms, n, peak, prob):
+def jtf_roofline(info, rb, units, ms, n, peak, prob, kernel=None):
     """J^T F + Jacobi (build_normal) kernel: algorithmic bytes of the bm
     program per element (+ the PCG start it carries for GN grids: delta, r, p
     writes) over its mean launch time."""
     from paper_1604_06525_b200 import planinfo
     if not n:
         return None
-    per = planinfo.algorithmic_bytes_per_element(info, "gather_set", "bm", rb)
+    if prob.graphs:
+        g = prob.graphs[0]
+        per = planinfo.graph_bytes_per_launch(info, "bm", rb, units, int(g.verts.size // g.arity), g.arity) / units
+    else:
+        per = planinfo.algorithmic_bytes_per_element(info, "gather_set", "bm", rb)
     cols = sum(f[1] for f in info.fields["U"])  # unknown columns per element
     fused = prob.method == "gn" and not prob.graphs
     per_total = per + (3 * cols * rb if fused else 0)
     avg_us = ms / n * 1e3
     ach = per_total * units / (avg_us * 1e-6) / 1e9
-    return {"bound": "hbm", "kernel": "build_normal (b = -2 J^T F, m = diag 2 J^T J" +
-            (", + PCG start" if fused else "") + ")", "achieved": ach, "peak": peak, "unit": "GB/s",
-            "frac": ach / peak, "alg_bytes_per_elem": per_total, "avg_launch_us": avg_us, "launches": n}
+    return {"bound": "hbm", "kernel": "build_normal (" + (f"{kernel}: " if kernel else "") +
+            "b = -2 J^T F, m = diag 2 J^T J" + (", + PCG start" if fused else "") + ")",
+            "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "traffic": ncu_traffic(profile_key(prob), kernel, "bm") if kernel else None,
+            "alg_bytes_per_elem": per_total, "avg_launch_us": avg_us, "launches": n}
 
 
 def cpu_reference(prob, prec, repeat, threads, nl=1):
@@ -201,41 +236,63 @@ def cpu_lm_per_iteration(prob, prec, repeat, threads):
     return per, float(np.mean(rows)), tps
 
 
+STRIP_PX = 1024 * 8192  # bounded CPU sample of a large grid: ~16 s of 16-thread reference time (ARAP)
+
+
+def cpu_sample(args, prob, threads, budget_ms=30e3, full=False):
+    """One reference measurement of the workload, in ms per GN/LM iteration:
+    (value, sample description, kind of scaling).  GN: one GN iteration
+    (cost, build_normal, 20 PCG, trial cost) per repeat, median over as many
+    repeats as fit `budget_ms` (at most 5).  Grids larger than STRIP_PX pixels
+    run on a leading strip of W' rows of the same W x H workload (unless
+    `full`) and the iteration time is scaled by W / W' — every reference
+    routine is a per-element loop, so its cost is linear in the rows."""
+    if prob.method == "lm":  # whole solves (~13 s each for SFS)
+        per, ms_trial, tps = cpu_lm_per_iteration(prob, args.prec, 1, threads)
+        return per[0], f"reference solver, one whole {NL}-iteration LM solve / {NL} ({tps} trials)", \
+            {"ms_per_trial": ms_trial, "trials": tps}
+    dims = list(prob.dims.values())
+    npx = int(np.prod(dims))
+    scale, sample = 1.0, prob
+    if not full and len(dims) == 2 and npx > STRIP_PX:
+        rows = max(1, STRIP_PX // dims[1])
+        sample = make_problem(args.config, args.size, rows=rows)
+        scale = dims[0] / rows
+    first, _ = cpu_reference(sample, args.prec, 1, threads)
+    reps = int(min(5, max(0, budget_ms // max(first[0], 1.0) - 1)))
+    rows_ms = first
+    if reps >= 2:
+        rows_ms, _ = cpu_reference(sample, args.prec, reps, threads)  # (the first run was the warm-up)
+    v = float(np.median(rows_ms)) * scale
+    d = list(sample.dims.values())
+    what = (f"reference solver, median of {len(rows_ms)} x (1 GN iteration x {LIN} PCG) on "
+            f"{'x'.join(map(str, d))}")
+    if scale != 1.0:
+        what += f" (leading {d[0]}-row strip of the {'x'.join(map(str, dims))} workload), x{scale:g} rows"
+    return v, what, {}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    prob = make_problem(args.config, args.size, rows_mult=int(os.environ.get("WORLD_SIZE", "1")))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    prob = make_problem(args.config, args.size, rows_mult=world if args.scaling == "weak" else 1)
     threads = os.cpu_count() or 1
-    reps = args.warmup + args.steps
-    lm, sample_note = None, None
-    if prob.method == "lm":  # whole solves (≈13 s each for SFS): at most 1 warm-up + 3 timed
-        w, k = min(args.warmup, 1), min(args.steps, 3)
-        per, ms_trial, tps = cpu_lm_per_iteration(prob, args.prec, w + k, threads)
-        v = float(np.mean(per[w:]))
-        lm = {"trials_per_solve": tps, "ms_per_trial": ms_trial, "sample": f"{k} whole {NL}-iteration solves"}
-    else:  # one GN iteration per repeat, bounded to ~150 s of CPU time in total
-        first, _ = cpu_reference(prob, args.prec, 1, threads)  # (also the warm-up)
-        k = int(min(args.steps, max(1, 150e3 // max(first[0], 1.0))))
-        w = int(min(max(args.warmup - 1, 0), max(0, 150e3 // max(first[0], 1.0) - k)))
-        rows, solves = cpu_reference(prob, args.prec, w + k, threads)
-        timed = rows[w:] if len(rows) > w else rows
-        v = float(np.mean(timed))
-        if k < args.steps:
-            sample_note = f"{k} of {args.steps} steps timed (each ~{first[0] / 1e3:.1f} s of CPU work)"
+    # The arm's whole --steps/--warmup run must end within a few minutes: at
+    # 8192^2 one full GN iteration (~2 min on 16 threads) is timed once.
+    v, what, extra = cpu_sample(args, prob, threads, budget_ms=150e3, full=True)
     line = {"impl": "reference", "metric": "ms per GN/LM iteration (fixed PCG iters)", "value": v,
             "unit": "ms/iter", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": v, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": v * NL, "higher_is_better": False,
+            "scaling": args.scaling if world > 1 else "strong", "vs_baseline": None,
             "dtype": args.prec, "data": "synthetic (seeded splitmix64, workloads.py)",
             "config": {"workload": workload_name(prob), "threads": threads},
             "cpu_baseline": {"value": v, "unit": "ms/iter", "cores": threads, "kind": "reference",
-                             "sample": f"1 nonlinear iteration x {LIN} PCG of the full workload per step"},
+                             "sample": what + f"; bounded sample instead of {args.warmup}+{args.steps} steps"},
             "e2e": {"value": v, "unit": "ms/iter", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    if lm:
-        line["lm"] = lm
-        line["cpu_baseline"]["sample"] = lm["sample"]
-    elif sample_note:
-        line["cpu_baseline"]["sample"] += f"; {sample_note}"
+    if extra:
+        line["lm"] = extra
     print(json.dumps(line), flush=True)
 
 
@@ -254,10 +311,11 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
-    # N > 1: weak scaling over axis-0 strips — the grid grows to (N*W) x H and
-    # every GPU owns one W x H strip (halo exchange + fixed-order reductions
-    # over NCCL); N = 1 is the unsharded single-GPU session.
-    prob = make_problem(args.config, args.size, rows_mult=world)
+    # N > 1 strong scaling: the same grid in N axis-0 strips (halo exchange +
+    # fixed-order reductions over NCCL); weak: the grid grows to (N*W) x H and
+    # every GPU owns one W x H strip.  N = 1 is the unsharded session.
+    weak = world > 1 and args.scaling == "weak"
+    prob = make_problem(args.config, args.size, rows_mult=world if weak else 1)
     dt = np.float32 if args.prec == "f32" else np.float64
     cfg = solve_config(prob, args.prec)
     plan = load_plan(prob.name, cfg, prob.dims)
@@ -330,9 +388,15 @@ def run_ours(args):
     restore()
     solve_resident()  # capture the profiled graphs
     s.profile_reset()
+    prof_ms = 0.0
     for _ in range(max(2, args.steps)):
         restore()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(st)
         solve_resident()
+        ev1.record(st)
+        ev1.synchronize()
+        prof_ms += ev0.elapsed_time(ev1)
     torch.cuda.synchronize()
     apply_ms, apply_n = s.profile(0)
     upd_ms, upd_n = s.profile(1)
@@ -365,8 +429,14 @@ def run_ours(args):
     rb = np.dtype(dt).itemsize
     dims = list(prob.dims.values())
     units = int(owned_rows * np.prod(dims[1:]))  # elements one launch (rank 0's strip) processes
-    per_elem = planinfo.algorithmic_bytes_per_element(info, "gather_set", "jtj", rb)
-    alg = per_elem * units
+    if prob.graphs:  # per-vertex footprint + int32 vertex ids per edge
+        g = prob.graphs[0]
+        E = int(g.verts.size // g.arity)
+        alg = planinfo.graph_bytes_per_launch(info, "jtj", rb, units, E, g.arity)
+        per_elem = alg / units
+    else:
+        per_elem = planinfo.algorithmic_bytes_per_element(info, "gather_set", "jtj", rb)
+        alg = per_elem * units
     peak, peak_kind = measured_peak()
     avg_apply = apply_ms / max(apply_n, 1)
     achieved = alg / (avg_apply * 1e-3) / 1e9 if apply_n else None
@@ -374,21 +444,27 @@ def run_ours(args):
     line = {
         "metric": "ms per GN/LM iteration (fixed PCG iters)", "value": value, "unit": "ms/iter",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
-        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": args.prec,
+        "higher_is_better": False, "scaling": "weak" if weak else "strong", "vs_baseline": None,
+        "dtype": args.prec,
         "data": "synthetic (seeded splitmix64, workloads.py); inputs resident in HBM",
         "config": {"workload": workload_name(prob),
                    "parallelism": f"{world} axis-0 strips (NCCL halo + fixed-order reductions)" if world > 1 else "1 GPU",
-                   "l2": "flushed between timed steps (256 MiB write)", "step": f"solve() = {NL} iterations",
+                   "l2": "flushed between timed steps (256 MiB write)" + (
+                       "; inputs far larger than L2" if units * per_elem > 4 * 126e6 else ""), "step": f"solve() = {NL} iterations",
                    "final_cost": r.final_cost},
         "roofline": {"bound": "hbm", "kernel": f"J^T J p apply ({s.apply_kernel(0)}, fused p'Ap)",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None,
-                     "traffic": ncu_traffic(prob.name + (f"_{args.size}" if args.size else ""), s.apply_kernel(0))
-                     if world == 1 else None,
+                     "traffic": ncu_traffic(profile_key(prob), s.apply_kernel(0)) if world == 1 else None,
                      "alg_bytes_per_launch": alg, "alg_bytes_per_elem": per_elem,
                      "avg_launch_us": avg_apply * 1e3, "launches": apply_n,
+                     # share of the (profiled) step spent in this kernel: compare with the
+                     # ncu launch list's share in profiles/ (its absolute times are cold-cache)
+                     "share_of_step": apply_ms / prof_ms if prof_ms else None,
+                     "timing": "CUDA events around every launch inside the captured stage graphs "
+                               "(separate profiled solves on the session stream, not the headline timing)",
                      "pcg_update_avg_us": upd_ms / max(upd_n, 1) * 1e3},
-        "roofline_jtf": jtf_roofline(info, rb, units, bm_ms, bm_n, peak, prob),
+        "roofline_jtf": jtf_roofline(info, rb, units, bm_ms, bm_n, peak, prob, s.normal_kernel(0)),
         "roofline_compute": compute_roofline(info, units, avg_apply * 1e3 if apply_n else None,
                                              torch.cuda.get_device_properties(dev).multi_processor_count),
         "e2e": {"value": float(np.median(e2e)) / NL, "unit": "ms/iter", "h2d_bytes_per_step": h2d,
@@ -402,16 +478,9 @@ def run_ours(args):
     if not args.no_cpu_baseline and world == 1:  # (contract: rank 0 at N=1 only)
         try:
             threads = os.cpu_count() or 1
-            if prob.method == "lm":
-                per, ms_trial, tps = cpu_lm_per_iteration(prob, args.prec, 1, threads)
-                line["cpu_baseline"] = {"value": per[0], "unit": "ms/iter", "cores": threads, "kind": "reference",
-                                        "ms_per_trial": ms_trial, "trials": tps,
-                                        "sample": f"reference solver, one whole {NL}-iteration LM solve / {NL}"}
-            else:
-                rows, _ = cpu_reference(prob, args.prec, 1, threads)
-                line["cpu_baseline"] = {"value": float(np.mean(rows)), "unit": "ms/iter", "cores": threads,
-                                        "kind": "reference",
-                                        "sample": f"reference solver, 1 nonlinear iteration x {LIN} PCG of the full workload"}
+            v, what, extra = cpu_sample(args, prob, threads)
+            line["cpu_baseline"] = {"value": v, "unit": "ms/iter", "cores": threads, "kind": "reference",
+                                    "sample": what, **extra}
         except Exception as e:  # the baseline is reported, never the target
             line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
     print(json.dumps(line), flush=True)

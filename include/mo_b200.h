@@ -241,6 +241,9 @@ int mo_kernel_launches(mo_session s, int64_t* n);
 /* Name of the J^T J p kernel gather set i runs (autotuned on first use;
  * MO_B200_JTJ=gather|twophase|stream|tma|warp|gprog|tma4 forces it). */
 int mo_apply_kernel(mo_session s, int gather_set, char* name, size_t len);
+/* Name of the build_normal (J^T F + Jacobi) kernel gather set i runs
+ * (solver.hpp:220-251; tuned on first use like mo_apply_kernel). */
+int mo_normal_kernel(mo_session s, int gather_set, char* name, size_t len);
 
 #ifdef __cplusplus
 }

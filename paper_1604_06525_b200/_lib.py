@@ -1,8 +1,8 @@
 """ctypes binding of libmo_b200.so (include/mo_b200.h).
 
 The library is built in-tree (``python __graft_entry__.py`` or
-``make -C paper_1604_06525_b200/csrc``).  There is no fallback: importing the
-package without the built library raises immediately.
+``make -C paper_1604_06525_b200/csrc``).  It is loaded on first use; there is
+no fallback: any call without the built library raises ImportError.
 """
 import ctypes
 import os
@@ -10,12 +10,33 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmo_b200.so")
 
-if not os.path.exists(LIB_PATH):
-    raise ImportError(
-        f"{LIB_PATH} is missing: build it with `make -C {_HERE}/csrc` "
-        "(the B200 solver has no CPU fallback)")
+_LIB = None
 
-lib = ctypes.CDLL(LIB_PATH)
+
+def _load():
+    """dlopen libmo_b200.so on first use (not at package import, so that
+    importing the workload generators does not map the product library into
+    processes that never call it, e.g. bench.py's reference arm).  A missing
+    library raises: there is no CPU fallback."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `make -C {_HERE}/csrc` "
+                "(the B200 solver has no CPU fallback)")
+        lib_ = ctypes.CDLL(LIB_PATH)
+        for _name, (_res, _args) in SIGNATURES.items():
+            _f = getattr(lib_, _name)
+            _f.restype = _res
+            _f.argtypes = _args
+        _LIB = lib_
+    return _LIB
+
+
+def __getattr__(name):  # `_lib.lib` loads the library lazily (PEP 562)
+    if name == "lib":
+        return _load()
+    raise AttributeError(name)
 
 c_int, c_int64, c_double, c_void_p, c_char_p, c_size_t = (
     ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p, ctypes.c_char_p, ctypes.c_size_t)
@@ -106,6 +127,7 @@ SIGNATURES = {
     "mo_session_stream": (c_int, [c_void_p, ctypes.POINTER(c_void_p)]),
     "mo_kernel_launches": (c_int, [c_void_p, ctypes.POINTER(c_int64)]),
     "mo_apply_kernel": (c_int, [c_void_p, c_int, ctypes.c_char_p, ctypes.c_size_t]),
+    "mo_normal_kernel": (c_int, [c_void_p, c_int, ctypes.c_char_p, ctypes.c_size_t]),
     "mo_plan_materialize": (c_int, [c_void_p, ctypes.POINTER(c_int)]),
     "mo_pcg": (c_int, [c_int, c_int, c_int64, APPLY_FN, c_void_p, c_void_p, c_void_p, c_void_p,
                        ctypes.POINTER(PcgOptionsC), c_void_p, ctypes.POINTER(PcgOutcomeC)]),
@@ -116,10 +138,6 @@ SIGNATURES = {
     "mo_get_normal_matrix": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64]),
 }
 
-for _name, (_res, _args) in SIGNATURES.items():
-    _f = getattr(lib, _name)
-    _f.restype = _res
-    _f.argtypes = _args
 
 # minopt::Err names (common.hpp:13-32), indexed by ABI code - 1.
 ERR_NAMES = ["SyntaxError", "UndeclaredIdentifier", "ArityMismatch", "NonConstantOffset",
@@ -147,6 +165,7 @@ class MoError(RuntimeError):
 
 
 def call(name, *args):
+    lib = _load()
     rc = getattr(lib, name)(*args)
     if rc != 0:
         raise MoError(rc, lib.mo_last_error().decode(errors="replace"))

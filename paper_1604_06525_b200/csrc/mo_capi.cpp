@@ -472,4 +472,10 @@ int mo_apply_kernel(mo_session s, int gather_set, char* name, size_t len) {
                std::memcpy(name, k.c_str(), k.size() + 1));
 }
 
+int mo_normal_kernel(mo_session s, int gather_set, char* name, size_t len) {
+  SESSION_CALL(need(name, "output"); const std::string k = s->impl->normal_kernel(gather_set);
+               mo::check(len > k.size(), mo::Err::kShapeMismatch, "name buffer too small");
+               std::memcpy(name, k.c_str(), k.size() + 1));
+}
+
 }  // extern "C"

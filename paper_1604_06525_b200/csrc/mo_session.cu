@@ -349,6 +349,9 @@ class Session final : public SessionBase {
     }
     CK(cudaMemcpyAsync(out, colmask_, size_t(n), cudaMemcpyDeviceToHost, st_));
     CK(cudaStreamSynchronize(st_));
+    // bit 1 marks strip halo columns (internal); the reference's excluded()
+    // is 0/1 (solver.hpp:619)
+    for (int64_t i = 0; i < n; ++i) out[i] &= 1u;
   }
 
   // ------------------------------------------------------------ routines
@@ -630,6 +633,14 @@ class Session final : public SessionBase {
     if (mat_) return "k_mat_cols";
     if (vertex_apply_one_pass()) return "mo_graph_vjtjf_0";
     return jtj_kernel(size_t(i));
+  }
+  std::string normal_kernel(int i) override {
+    check(i >= 0 && size_t(i) < P_.gather_sets.size(), Err::kIndexOutOfRange, "no such gather set");
+    ensure_refreshed();
+    tune_apply();
+    if (!P_.graph_sets.empty() && vertex_path(0)) return "mo_graph_vbm_0";
+    return (bm_choice_.size() > size_t(i) && bm_choice_[size_t(i)] ? "mo_gather_bm4_" : "mo_gather_bm_") +
+           std::to_string(i);
   }
 
  private:
@@ -1148,9 +1159,8 @@ class Session final : public SessionBase {
     long long g = std::min<long long>(tiles_of(d), (long long)nsm_ * occupancy(f, smem));
     return int(std::max<long long>(g, 1));
   }
-  int edge_blocks(const std::string& name, int gi) {
+  int edge_blocks(const std::string& name, long long E) {
     const void* f = mod_.kernel(name);
-    long long E = graphs_[size_t(P_.graph_sets[size_t(gi)].graph)].E_own;
     long long g = std::min<long long>((E + MO_THREADS - 1) / MO_THREADS, (long long)nsm_ * occupancy(f));
     return int(std::max<long long>(g, 1));
   }
@@ -1492,7 +1502,8 @@ class Session final : public SessionBase {
   }
   void launch_edges(const std::string& name, int gi, const mo_kparams& kp, int grid = 0) {
     const void* f = mod_.kernel(name);
-    if (grid <= 0) grid = edge_blocks(name, gi);
+    (void)gi;
+    if (grid <= 0) grid = edge_blocks(name, kp.nedges);
     void* args[] = {const_cast<mo_kparams*>(&kp)};
     klc(f, dim3(grid), dim3(MO_THREADS), args, 0);
     ++launches_;
@@ -1590,7 +1601,8 @@ class Session final : public SessionBase {
       total += grids.back();
     }
     for (size_t i = 0; i < P_.graph_sets.size(); ++i) {
-      grids.push_back(edge_blocks("mo_graph_cost_" + std::to_string(i), int(i)));
+      grids.push_back(edge_blocks("mo_graph_cost_" + std::to_string(i),
+                                  graphs_[size_t(P_.graph_sets[i].graph)].E_own));
       total += grids.back();
     }
     if (total == 0) {
@@ -1711,6 +1723,9 @@ class Session final : public SessionBase {
           continue;
         }
         kp.out0 = gsets_[i].contrib;
+        // contributions of EVERY stored edge: the incidence CSR the gather
+        // walks also holds the strip's non-owned edges touching owned vertices
+        kp.nedges = graphs_[size_t(P_.graph_sets[i].graph)].E;
         launch_edges("mo_graph_bm_" + std::to_string(i), int(i), kp);
         gather_graph(int(i), true, b_, m_);
       }
@@ -1764,6 +1779,7 @@ class Session final : public SessionBase {
           continue;
         }
         kp.out0 = gsets_[i].contrib;
+        kp.nedges = graphs_[size_t(P_.graph_sets[i].graph)].E;  // (all stored edges, as for b/m)
         launch_edges("mo_graph_jtj_" + std::to_string(i), int(i), kp);
         gather_graph(int(i), false, out, nullptr);
       }

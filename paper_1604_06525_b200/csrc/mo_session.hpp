@@ -57,6 +57,7 @@ class SessionBase {
   virtual void* stream() = 0;
   virtual int64_t launches() const = 0;
   virtual std::string apply_kernel(int gather_set) = 0;
+  virtual std::string normal_kernel(int gather_set) = 0;
   // linearize / jacobian (solver.hpp:291-382): evaluate the Jacobian lanes on
   // the device; jacobian() assembles the reference's CSR from them (host).
   virtual void linearize() = 0;

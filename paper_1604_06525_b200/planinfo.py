@@ -74,3 +74,23 @@ def algorithmic_bytes_per_element(info: PlanInfo, section_kind: str, program: st
             n = len(p.loads) * real_bytes + p.n_outputs * real_bytes
             return n + (1 if mask else 0)
     raise KeyError(f"{section_kind}/{program} not in plan")
+
+
+def graph_bytes_per_launch(info: PlanInfo, program: str, real_bytes: int, n_vertices: int, n_edges: int,
+                           arity: int) -> int:
+    """Unique footprint of one launch of a plan whose `program` (jtj / bm) has
+    a grid gather part and a graph scatter part on the same vertex domain
+    (SURVEY §8d ARAP mesh: 76 B/vertex + 8 B/edge for J^T J p): every distinct
+    (kind, field, channel) either part loads, once per vertex, + the per-vertex
+    outputs (+ the uint8 mask if the plan has exclusion kernels) + the int32
+    vertex ids of every edge."""
+    loads, outs, mask = set(), 0, False
+    for hdr, progs in info.sections:
+        if program in progs and (hdr.startswith("gather_set") or hdr.startswith("graph_set")):
+            loads.update(progs[program].loads)
+            if hdr.startswith("gather_set"):
+                outs = max(outs, progs[program].n_outputs)
+        if hdr.startswith("exclude_kernel"):
+            mask = True
+    per_v = len(loads) * real_bytes + outs * real_bytes + (1 if mask else 0)
+    return per_v * n_vertices + arity * 4 * n_edges

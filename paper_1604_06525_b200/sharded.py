@@ -29,7 +29,8 @@ from typing import List
 import numpy as np
 
 from . import planinfo
-from ._lib import call, lib
+from . import _lib
+from ._lib import call
 from .solver import CompiledPlan, EdgeTable, SolveData, Solver
 
 
@@ -233,10 +234,10 @@ class LocalShardGroup:
             s.__del__()
         self.solvers = []
         for c in self.comms:
-            lib.mo_comm_destroy(c)
+            _lib.lib.mo_comm_destroy(c)
         self.comms = []
         if self._w:
-            lib.mo_world_destroy(self._w)
+            _lib.lib.mo_world_destroy(self._w)
             self._w = None
 
     def __del__(self):

@@ -306,6 +306,9 @@ class Solver:
         v = _as(v, self.dtype)
         if v.size != self.num_cols():
             raise MoError(10, "apply_jtj(): vector size mismatch")
+        if out is not None and (not isinstance(out, np.ndarray) or out.dtype != self.dtype
+                                or out.size != v.size or not out.flags.c_contiguous or not out.flags.writeable):
+            raise MoError(10, "apply_jtj(): out must be a writable C-contiguous vector of num_cols Reals")
         res = np.empty(v.size, self.dtype) if out is None else out
         call("mo_apply_jtj", self._h, v.ctypes.data, res.ctypes.data, v.size)
         return res
@@ -395,6 +398,12 @@ class Solver:
         call("mo_apply_kernel", self._h, int(gather_set), buf, 128)
         return buf.value.decode()
 
+    def normal_kernel(self, gather_set: int = 0) -> str:
+        """Name of the build_normal (J^T F + Jacobi) kernel of a gather set."""
+        buf = ctypes.create_string_buffer(128)
+        call("mo_normal_kernel", self._h, int(gather_set), buf, 128)
+        return buf.value.decode()
+
     def kernel_launches(self) -> int:
         n = ctypes.c_int64()
         call("mo_kernel_launches", self._h, ctypes.byref(n))
@@ -424,6 +433,8 @@ def pcg(apply, b, m, max_iters: int = 10, tol_rel: float = 1e-3, tol_abs: float 
         raise MoError(10, "pcg operand sizes do not match")
     delta = np.zeros(b.size, dt)
     ex = None if excluded is None else np.ascontiguousarray(excluded, np.uint8)
+    if ex is not None and ex.size != b.size:
+        raise MoError(10, "pcg operand sizes do not match")
     err = []
 
     def tramp(x, y, stream, _user):

@@ -82,3 +82,25 @@ def test_materialize_mode_travels_with_the_plan(name, mode):
     assert q.materialize == mode
     text = open(os.path.join(PLAN_DIR, name + ".moplan")).read()
     assert ("program jtj 0 0 0 0 0" in text) == (mode != 0)
+
+
+def test_workload_import_does_not_map_the_product_library():
+    """bench.py's reference arm generates inputs with workloads.py; that must
+    not dlopen libmo_b200.so (the library loads on first use only)."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "from paper_1604_06525_b200 import workloads\n"
+            "workloads.poisson(8, 8)\n"
+            "print(any('libmo_b200' in l for l in open('/proc/self/maps')))\n") % ROOT
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, check=True).stdout
+    assert out.strip() == "False"
+
+
+def test_pcg_operand_checks_precede_any_device_work():
+    from paper_1604_06525_b200 import pcg
+    b = np.ones(4)
+    with pytest.raises(_lib.MoError):
+        pcg(lambda x, y, s: None, b, np.ones(4), excluded=np.zeros(3, np.uint8))
+    with pytest.raises(_lib.MoError):
+        pcg(lambda x, y, s: None, b, np.ones(5))

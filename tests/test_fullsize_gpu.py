@@ -50,10 +50,10 @@ def test_arap_1024_apply_matches_reference(arap1024, variant, monkeypatch):
     k = s.apply_kernel(0)
     if not k.startswith(PREFIX[variant]):
         pytest.skip(f"{variant} not available here (runs {k})")
-    assert_close_vec(s.apply_jtj(v), ref["jtj"], 1e-5, f"2 J^T J v, 1024^2 ARAP [{k}]")
+    assert_close_vec(s.apply_jtj(v), ref["jtj"], 1e-5, f"2 J^T J v, 1024^2 ARAP [{k}]", floor=True)
     assert abs(s.cost() - float(ref["cost"][0])) <= 2e-5 * abs(float(ref["cost"][0]))
     s.build_normal()
-    assert_close_vec(s.rhs(), ref["b"], 1e-5, "b")
+    assert_close_vec(s.rhs(), ref["b"], 1e-5, "b", floor=True)
     assert_close_vec(s.precond(), ref["m"], 1e-5, "m")
 
 
@@ -92,46 +92,93 @@ def test_other_configs_apply_matches_reference(name, make, prec):
                            threads=THREADS, v=v)
     s = Solver(load_plan(prob.name, _cfg(prob, prec), prob.dims), prob.data(dt))
     tol = 1e-5 if prec == "f32" else 1e-10
-    assert_close_vec(s.apply_jtj(v), ref["jtj"], tol, f"2 J^T J v {name} [{s.apply_kernel(0)}]")
+    assert_close_vec(s.apply_jtj(v), ref["jtj"], tol, f"2 J^T J v {name} [{s.apply_kernel(0)}]", floor=True)
     s.build_normal()
-    assert_close_vec(s.rhs(), ref["b"], tol, "b")
+    assert_close_vec(s.rhs(), ref["b"], tol, "b", floor=True)
 
 
 SOLVE_CASES = {
-    # BASELINE configs 1-4 at their own sizes; a few nonlinear iterations so
-    # the reference (all host threads) finishes in seconds.
-    "poisson_512": (lambda: workloads.poisson(512, 512), 3, 20),
-    "arap_warp_1024": (lambda: workloads.arap_warp(1024, 1024), 2, 20),
-    "sfs_640x480": (lambda: workloads.sfs(640, 480), 3, 20),
-    "arap_mesh_200k": (lambda: workloads.arap_mesh(448), 2, 20),
+    # BASELINE configs 1-4 at their own sizes and the benchmarked iteration
+    # counts (10 nonlinear x 20 PCG, tolerances 0).
+    "poisson_512": (lambda: workloads.poisson(512, 512), 10, 20),
+    "arap_warp_1024": (lambda: workloads.arap_warp(1024, 1024), 10, 20),
+    "sfs_640x480": (lambda: workloads.sfs(640, 480), 10, 20),
+    "arap_mesh_200k": (lambda: workloads.arap_mesh(448), 10, 20),
 }
+
+
+def _ref_solve(prob, prec, nl, lin):
+    dt = np.float32 if prec == "f32" else np.float64
+    return pyoracle.run_ref(prob.energy, prob.data(dt), ["solve"], dims=prob.dims, prec=prec, method=prob.method,
+                            nl=nl, lin=lin, rel=0.0, abs_tol=0.0, cost_stop=0.0, exec_mode="par", threads=THREADS)
+
+
+def _rel(a, b):
+    return abs(a - b) / max(abs(b), 1e-300)
 
 
 @pytest.mark.parametrize("case", list(SOLVE_CASES))
 def test_config_solve_matches_reference(case):
     """north_star: per-iteration cost trajectory and final cost within 1e-4
-    (fp32) / 1e-8 (fp64) of the CPU reference on the BASELINE configs (fixed
-    iteration counts), identical accept/reject pattern and PCG counts.
+    (fp32) / 1e-8 (fp64) of the CPU reference on the BASELINE configs at the
+    benchmarked 10 nl x 20 PCG, identical accept/reject pattern and PCG counts.
 
-    The yardstick is the reference run in fp64: the fp32
-    reference sums costs and PCG dot products sequentially in fp32, which at
-    these sizes is itself off by up to ~3e-3 (ARAP mesh, 801k edges: 800.30
-    vs 802.66 after one GN step); this solver accumulates reductions in
-    double, and its fp32 trajectory tracks the fp64 reference to ~1e-6."""
+    Two yardsticks for fp32 (both printed):
+    * the reference in fp64, the parity truth (BASELINE.md §2): always;
+    * the reference in fp32: wherever that run is itself within 0.5e-4 of
+      the fp64 one.  It is not, where its sequential fp32 sums of costs and
+      PCG dot products (solver.hpp:182, pcg.hpp:43) drift: the ARAP mesh
+      (801k edges) is off by ~3e-3 after one GN step; this solver reduces
+      in double and tracks the fp64 trajectory."""
     make, nl, lin = SOLVE_CASES[case]
     prob = make()
-    ref = pyoracle.run_ref(prob.energy, prob.data(np.float64), ["solve"], dims=prob.dims, prec="f64",
-                           method=prob.method, nl=nl, lin=lin, rel=0.0, abs_tol=0.0, cost_stop=0.0, exec_mode="par",
-                           threads=THREADS)
+    ref64 = _ref_solve(prob, "f64", nl, lin)
+    ref32 = _ref_solve(prob, "f32", nl, lin)
+    f64 = float(ref64["final_cost"][0])
+    f32ref = float(ref32["final_cost"][0])
     for prec, tol in (("f32", 1e-4), ("f64", 1e-8)):
         dt = np.float32 if prec == "f32" else np.float64
         r = Solver(load_plan(prob.name, _cfg(prob, prec, nl, lin), prob.dims), prob.data(dt)).solve()
-        assert int(r.reason) == int(ref["reason"][0])
-        assert [int(t.accepted) for t in r.trace] == list(ref["trace_accepted"])
-        assert [t.pcg_iters for t in r.trace] == list(ref["trace_pcg"])
-        for row, rc in zip(r.trace, ref["trace_cost"]):
-            assert abs(row.cost - rc) <= tol * abs(rc), (case, prec, row.cost, rc)
-        assert abs(r.final_cost - float(ref["final_cost"][0])) <= tol * abs(float(ref["final_cost"][0]))
+        print(f"{case} {prec}: ours {r.final_cost!r}  ref64 {f64!r} ({_rel(r.final_cost, f64):.2e})  "
+              f"ref32 {f32ref!r} ({_rel(r.final_cost, f32ref):.2e}); ref32 vs ref64 {_rel(f32ref, f64):.2e}")
+        assert int(r.reason) == int(ref64["reason"][0])
+        assert [int(t.accepted) for t in r.trace] == list(ref64["trace_accepted"])
+        assert [t.pcg_iters for t in r.trace] == list(ref64["trace_pcg"])
+        for row, rc in zip(r.trace, ref64["trace_cost"]):
+            assert _rel(row.cost, rc) <= tol, (case, prec, row.cost, rc)
+        assert _rel(r.final_cost, f64) <= tol
+        if prec == "f32" and _rel(f32ref, f64) <= 0.5e-4:
+            assert [int(t.accepted) for t in r.trace] == list(ref32["trace_accepted"])
+            for row, rc in zip(r.trace, ref32["trace_cost"]):
+                assert _rel(row.cost, rc) <= tol, (case, "vs fp32 reference", row.cost, rc)
+            assert _rel(r.final_cost, f32ref) <= tol
+
+
+@pytest.mark.parametrize("name", ["arap_warp", "poisson"])
+def test_config5_8192_single_gpu(name):
+    """Config 5 at full size on ONE GPU, unsharded (the session bench.py's
+    N=1 headline times): per element J^T J v (1e-5, cancelling: floor),
+    b (floor) and m (pure relative) against the unmodified reference, and the
+    1 GN x 2 PCG trajectory within 1e-4 (the reference needs
+    minutes per full iteration at 201M unknowns)."""
+    n = 8192
+    prob = workloads.arap_warp(n, n) if name == "arap_warp" else workloads.poisson(n, n)
+    data = prob.data(np.float32)
+    v = (workloads.uniform(97, data.x.size) - 0.5).astype(np.float32)
+    nl, lin = 1, 2
+    ref = pyoracle.run_ref(prob.energy, data, ["cost", "normal", "jtj", "solve"], dims=prob.dims, prec="f32",
+                           nl=nl, lin=lin, rel=0.0, abs_tol=0.0, cost_stop=0.0, exec_mode="par", threads=THREADS, v=v)
+    s = Solver(load_plan(prob.name, _cfg(prob, "f32", nl, lin), prob.dims), prob.data(np.float32))
+    assert _rel(s.cost(), float(ref["cost"][0])) <= 1e-5
+    assert_close_vec(s.apply_jtj(v), ref["jtj"], 1e-5, f"2 J^T J v {name} 8192^2 [{s.apply_kernel(0)}]", floor=True)
+    s.build_normal()
+    assert_close_vec(s.rhs(), ref["b"], 1e-5, f"b [{s.normal_kernel(0)}]", floor=True)
+    assert_close_vec(s.precond(), ref["m"], 1e-5, "m")
+    r = s.solve()
+    assert [t.pcg_iters for t in r.trace] == list(ref["trace_pcg"])
+    for row, rc in zip(r.trace, ref["trace_cost"]):
+        assert _rel(row.cost, rc) <= 1e-4, (row.cost, rc)
+    assert _rel(r.final_cost, float(ref["final_cost"][0])) <= 1e-4
 
 
 @pytest.mark.parametrize("name", ["poisson", "arap_warp"])
