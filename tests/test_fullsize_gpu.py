@@ -141,9 +141,15 @@ def test_config_solve_matches_reference(case):
         r = Solver(load_plan(prob.name, _cfg(prob, prec, nl, lin), prob.dims), prob.data(dt)).solve()
         print(f"{case} {prec}: ours {r.final_cost!r}  ref64 {f64!r} ({_rel(r.final_cost, f64):.2e})  "
               f"ref32 {f32ref!r} ({_rel(r.final_cost, f32ref):.2e}); ref32 vs ref64 {_rel(f32ref, f64):.2e}")
+        # PCG counts against the same-precision reference: with tolerances 0
+        # a PCG only stops early on p'Ap <= 0 (pcg.hpp:105), which in fp32
+        # happens once the residual is at rounding level (SFS after the 8th
+        # trial: 16, 14, 12, ... in the fp32 reference, 20 in fp64).
+        same = ref64 if prec == "f64" else ref32
+        print(f"{case} {prec} pcg: ours {[t.pcg_iters for t in r.trace]} ref {list(same['trace_pcg'])}")
         assert int(r.reason) == int(ref64["reason"][0])
         assert [int(t.accepted) for t in r.trace] == list(ref64["trace_accepted"])
-        assert [t.pcg_iters for t in r.trace] == list(ref64["trace_pcg"])
+        assert [t.pcg_iters for t in r.trace] == list(same["trace_pcg"])
         for row, rc in zip(r.trace, ref64["trace_cost"]):
             assert _rel(row.cost, rc) <= tol, (case, prec, row.cost, rc)
         assert _rel(r.final_cost, f64) <= tol
@@ -166,19 +172,26 @@ def test_config5_8192_single_gpu(name):
     data = prob.data(np.float32)
     v = (workloads.uniform(97, data.x.size) - 0.5).astype(np.float32)
     nl, lin = 1, 2
-    ref = pyoracle.run_ref(prob.energy, data, ["cost", "normal", "jtj", "solve"], dims=prob.dims, prec="f32",
-                           nl=nl, lin=lin, rel=0.0, abs_tol=0.0, cost_stop=0.0, exec_mode="par", threads=THREADS, v=v)
+    # Per-element vectors against the fp32 reference; costs against the fp64
+    # reference on the same (widened) inputs: the reference sums costs
+    # sequentially in Real (solver.hpp:182), which in fp32 over 201M Poisson
+    # terms loses every term below half an ulp of the running sum (1.53e8 vs
+    # the true 2.68e8).
+    ref = pyoracle.run_ref(prob.energy, data, ["normal", "jtj"], dims=prob.dims, prec="f32",
+                           exec_mode="par", threads=THREADS, v=v)
+    ref64 = pyoracle.run_ref(prob.energy, prob.data(np.float64), ["cost", "solve"], dims=prob.dims, prec="f64",
+                             nl=nl, lin=lin, rel=0.0, abs_tol=0.0, cost_stop=0.0, exec_mode="par", threads=THREADS)
     s = Solver(load_plan(prob.name, _cfg(prob, "f32", nl, lin), prob.dims), prob.data(np.float32))
-    assert _rel(s.cost(), float(ref["cost"][0])) <= 1e-5
+    assert _rel(s.cost(), float(ref64["cost"][0])) <= 1e-5
     assert_close_vec(s.apply_jtj(v), ref["jtj"], 1e-5, f"2 J^T J v {name} 8192^2 [{s.apply_kernel(0)}]", floor=True)
     s.build_normal()
     assert_close_vec(s.rhs(), ref["b"], 1e-5, f"b [{s.normal_kernel(0)}]", floor=True)
     assert_close_vec(s.precond(), ref["m"], 1e-5, "m")
     r = s.solve()
-    assert [t.pcg_iters for t in r.trace] == list(ref["trace_pcg"])
-    for row, rc in zip(r.trace, ref["trace_cost"]):
+    assert [t.pcg_iters for t in r.trace] == list(ref64["trace_pcg"])
+    for row, rc in zip(r.trace, ref64["trace_cost"]):
         assert _rel(row.cost, rc) <= 1e-4, (row.cost, rc)
-    assert _rel(r.final_cost, float(ref["final_cost"][0])) <= 1e-4
+    assert _rel(r.final_cost, float(ref64["final_cost"][0])) <= 1e-4
 
 
 @pytest.mark.parametrize("name", ["poisson", "arap_warp"])

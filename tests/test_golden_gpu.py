@@ -74,7 +74,11 @@ def run_golden(g, exact):
             c = s.cost()
             assert rel_close(c, float(g.ref("cost")[0]), t["cost"]), (c, g.ref("cost"))
         elif cmd == "residuals":
-            assert_close_vec(s.residuals(), g.ref("residuals"), t["vec"], "residuals")
+            # Residuals are differences of O(1) terms (SFS: shading minus
+            # intensity), so with FMA contraction a near-zero residual has no
+            # 1e-5 relative accuracy: floor in fast mode.  Exact mode checks
+            # every element relative (and bitwise for the BITWISE plans).
+            assert_close_vec(s.residuals(), g.ref("residuals"), t["vec"], "residuals", floor=not exact)
         elif cmd == "normal":
             s.build_normal()
             assert_close_vec(s.rhs(), g.ref("b"), t["vec"], "b = -2 J^T F", floor=True)
