@@ -235,6 +235,11 @@ int mo_set_profiling(mo_session s, int enable);
 /* kind: 0 = J^T J p apply, 1 = PCG vector update, 2 = build_normal, 3 = cost */
 int mo_profile_read(mo_session s, int kind, double* total_ms, int64_t* launches);
 int mo_profile_reset(mo_session s);
+/* Unperturbed kernel time for the roofline: `reps` back-to-back launches of
+ * the J^T J p apply (which = 0, the PCG's own launch on the session's p) or
+ * of build_normal (which = 1) replayed as one CUDA graph, best of 3; writes
+ * ms per launch.  Clobbers the PCG scratch vectors (x is untouched). */
+int mo_bench_kernel(mo_session s, int which, int reps, double* ms_per_launch);
 int mo_session_stream(mo_session s, void** stream); /* cudaStream_t */
 /* Number of this library's kernels launched so far (host-side count). */
 int mo_kernel_launches(mo_session s, int64_t* n);

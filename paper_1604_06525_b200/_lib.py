@@ -124,6 +124,7 @@ SIGNATURES = {
     "mo_set_profiling": (c_int, [c_void_p, c_int]),
     "mo_profile_read": (c_int, [c_void_p, c_int, ctypes.POINTER(c_double), ctypes.POINTER(c_int64)]),
     "mo_profile_reset": (c_int, [c_void_p]),
+    "mo_bench_kernel": (c_int, [c_void_p, c_int, c_int, ctypes.POINTER(ctypes.c_double)]),
     "mo_session_stream": (c_int, [c_void_p, ctypes.POINTER(c_void_p)]),
     "mo_kernel_launches": (c_int, [c_void_p, ctypes.POINTER(c_int64)]),
     "mo_apply_kernel": (c_int, [c_void_p, c_int, ctypes.c_char_p, ctypes.c_size_t]),

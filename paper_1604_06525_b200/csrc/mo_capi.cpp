@@ -392,6 +392,9 @@ int mo_profile_read(mo_session s, int kind, double* ms, int64_t* n) {
   SESSION_CALL(need(ms, "output"); need(n, "output"); s->impl->profile_read(kind, ms, n));
 }
 int mo_profile_reset(mo_session s) { SESSION_CALL(s->impl->profile_reset()); }
+int mo_bench_kernel(mo_session s, int which, int reps, double* ms_per_launch) {
+  SESSION_CALL(need(ms_per_launch, "output"); *ms_per_launch = s->impl->bench_kernel(which, reps));
+}
 int mo_session_stream(mo_session s, void** st) { SESSION_CALL(need(st, "output"); *st = s->impl->stream()); }
 int mo_kernel_launches(mo_session s, int64_t* n) { SESSION_CALL(need(n, "output"); *n = s->impl->launches()); }
 int mo_linearize(mo_session s) { SESSION_CALL(s->impl->linearize()); }

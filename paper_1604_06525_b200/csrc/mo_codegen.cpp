@@ -119,20 +119,159 @@ struct Gen {
     }
     return r;
   }
-  static constexpr int MO_MAX_TMAPS_HOST = 12;  // = MO_MAX_TMAPS (mo_device.cuh)
+  static constexpr int MO_MAX_TMAPS_HOST = 16;  // = MO_MAX_TMAPS (mo_device.cuh)
+  // ---- lane cache: the x-dependent part of evalj, evaluated once per
+  // linearisation.  Every evalj instruction is either UNIFORM (built from
+  // immediates and parameters only, through uniform registers) or VARYING
+  // (reads a field, an index or InBounds, or a varying register written
+  // earlier in program order).  A lane whose roots are all uniform is a
+  // function of the parameters and of guard outcomes only; the others are
+  // cached by value.  Re-running the uniform instructions under the cached
+  // guard outcomes (block-entry guards, final output guards) reproduces
+  // every lane bit for bit, so an apply that reads the cache computes
+  // exactly what the full evalj would have.
+  struct LaneSplit {
+    bool ok = false;
+    std::vector<char> u;       // per instruction: uniform
+    std::vector<int> blk_bit;  // per block: bit of its entry guard outcome (-1: not needed)
+    std::vector<int> out_bit;  // per gid: bit of its final guard outcome (-1: not needed)
+    std::vector<int> varying;  // evalj outputs cached by value, in order
+    int nbits = 0;
+  };
+  static LaneSplit split_lanes(const Program& pg) {
+    LaneSplit ls;
+    std::vector<char> v(pg.num_regs, 0);  // register holds (or may hold) a varying value here
+    ls.u.assign(pg.instrs.size(), 0);
+    ls.blk_bit.assign(pg.blocks.size(), -1);
+    ls.out_bit.assign(pg.guard_regs.size(), -1);
+    for (size_t bi = 0; bi < pg.blocks.size(); ++bi) {
+      const Block& b = pg.blocks[bi];
+      bool any_u = false;
+      for (uint32_t i = b.begin; i < b.end; ++i) {
+        const Instr& in = pg.instrs[i];
+        bool var = false;
+        switch (in.op) {
+          case kImm: case kParam: break;
+          case kAdd: case kMul: case kCmp: case kAnd: case kOr: var = v[in.a] || v[in.b]; break;
+          case kPow: case kUn: case kNot: var = v[in.a]; break;
+          case kSel: var = v[in.a] || v[in.b] || v[in.c]; break;
+          default: var = true;  // loads, index, InBounds
+        }
+        ls.u[i] = !var;
+        // an unconditional write replaces the register's value; a guarded one
+        // may leave the old (possibly varying) value in place
+        if (b.gid == 0) v[in.dst] = var;
+        else if (var) v[in.dst] = 1;
+        any_u |= !var;
+      }
+      if (b.gid != 0 && any_u) ls.blk_bit[bi] = ls.nbits++;
+    }
+    // A root whose last write is a uniform instruction in a block guarded by
+    // the root's own guard (and that guard register is not rewritten after
+    // the block starts) always holds that uniform value when the root counts:
+    // the usual shape of generated code (guarded block computes, guarded
+    // root reads), even when the register held varying values earlier.
+    std::vector<int> last_w(pg.num_regs, -1), blk_of(pg.instrs.size(), -1);
+    for (size_t bi = 0; bi < pg.blocks.size(); ++bi)
+      for (uint32_t i = pg.blocks[bi].begin; i < pg.blocks[bi].end; ++i) {
+        last_w[pg.instrs[i].dst] = int(i);
+        blk_of[i] = int(bi);
+      }
+    auto root_var = [&](uint32_t gid, uint16_t reg) {
+      if (!v[reg]) return false;
+      const int w = last_w[reg];
+      if (w < 0 || !ls.u[size_t(w)] || gid == 0) return true;
+      const Block& b = pg.blocks[size_t(blk_of[size_t(w)])];
+      if (b.gid != gid) return true;
+      const uint16_t g = pg.guard_regs[gid];
+      for (size_t i = b.begin; i < pg.instrs.size(); ++i)
+        if (pg.instrs[i].dst == g) return true;
+      return false;
+    };
+    for (size_t o = 0; o < pg.outputs.size(); ++o) {
+      bool var = false;
+      for (auto [gid, reg] : pg.outputs[o]) var |= root_var(gid, reg);
+      if (var) {
+        ls.varying.push_back(int(o));
+        continue;
+      }
+      for (auto [gid, reg] : pg.outputs[o])
+        if (gid != 0 && ls.out_bit[gid] < 0) ls.out_bit[gid] = ls.nbits++;
+    }
+    ls.ok = ls.nbits <= 32;
+    return ls;
+  }
+  // split_mode 1: program() also returns the guard outcomes (`*bits_out`);
+  // split_mode 2: program() is the cache READER: uniform instructions only,
+  // guards from `bits`, varying outputs from `cv[]`.
+  const LaneSplit* cur_split = nullptr;
+  int split_mode = 0;
+
   std::string program(const Program& pg, bool graph, const Domain* dom = nullptr, bool sm = false) {
     std::string name = "mo_prog_" + std::to_string(nprog++);
     iter_dom = graph ? nullptr : dom;
     sm_mode = sm && !graph;
     reach = reach_of(pg, iter_dom);
+    const LaneSplit* ls = split_mode ? cur_split : nullptr;
+    if (ls && split_mode == 2) {
+      os << "__device__ __forceinline__ void " << name
+         << "(const mo_kparams& P, unsigned bits, const Real* cv, Real* out) {\n  (void)P; (void)bits; (void)cv;\n";
+      std::vector<char> used(pg.num_regs, 0);  // every register the uniform slice touches
+      for (size_t i = 0; i < pg.instrs.size(); ++i)
+        if (ls->u[i]) {
+          const Instr& in = pg.instrs[i];
+          used[in.dst] = 1;
+          if (in.op != kImm && in.op != kParam) used[in.a] = 1;
+          if (in.op == kAdd || in.op == kMul || in.op == kCmp || in.op == kAnd || in.op == kOr || in.op == kSel)
+            used[in.b] = 1;
+          if (in.op == kSel) used[in.c] = 1;
+        }
+      for (const auto& o : pg.outputs)
+        for (auto [gid, reg] : o) used[reg] = 1;
+      for (uint32_t r = 0; r < pg.num_regs; ++r)
+        if (used[r]) os << "  Real r" << r << " = (Real)0;\n";
+      for (size_t bi = 0; bi < pg.blocks.size(); ++bi) {
+        const Block& b = pg.blocks[bi];
+        bool any = false;
+        for (uint32_t i = b.begin; i < b.end; ++i) any |= ls->u[i] != 0;
+        if (!any) continue;
+        std::string ind = "  ";
+        if (b.gid != 0) {
+          os << "  if ((bits >> " << ls->blk_bit[bi] << ") & 1u) {\n";
+          ind = "    ";
+        }
+        for (uint32_t i = b.begin; i < b.end; ++i)
+          if (ls->u[i]) os << ind << instr(pg.instrs[i], graph) << "\n";
+        if (b.gid != 0) os << "  }\n";
+      }
+      size_t vi = 0;
+      for (size_t o = 0; o < pg.outputs.size(); ++o) {
+        if (vi < ls->varying.size() && ls->varying[vi] == int(o)) {
+          os << "  out[" << o << "] = cv[" << vi++ << "];\n";
+          continue;
+        }
+        os << "  { Real acc = (Real)0;";
+        for (auto [gid, reg] : pg.outputs[o]) {
+          if (gid != 0)
+            os << " if ((bits >> " << ls->out_bit[gid] << ") & 1u) acc += r" << reg << ";";
+          else
+            os << " acc += r" << reg << ";";
+        }
+        os << " out[" << o << "] = acc; }\n";
+      }
+      os << "}\n";
+      return name;
+    }
     if (sm_mode)
       os << "template <bool I> __device__ __forceinline__ void " << name
          << "(const mo_kparams& P, int p0, int p1, int p2, const int* ri, int lx, Real* out) {\n"
          << "  (void)P; (void)p0; (void)p1; (void)p2; (void)ri; (void)lx; const int eb = 0; (void)eb;\n";
     else
       os << "template <bool I> __device__ __forceinline__ void " << name
-         << "(const mo_kparams& P, int p0, int p1, int p2, int eb, const int* vs, Real* out) {\n"
+         << "(const mo_kparams& P, int p0, int p1, int p2, int eb, const int* vs, Real* out"
+         << (ls ? ", unsigned* bits_out" : "") << ") {\n"
          << "  (void)P; (void)p0; (void)p1; (void)p2; (void)eb; (void)vs;\n";
+    if (ls) os << "  unsigned bits = 0u;\n";
     if (iter_dom) {
       // Strides of the iteration domain are plan constants (the plan fixes the
       // global dims), so every interior stencil read is base + immediate.
@@ -156,8 +295,11 @@ struct Gen {
       if (!sm_mode) os << ldi_bases(slots);
     }
     for (uint32_t r = 0; r < pg.num_regs; ++r) os << "  Real r" << r << " = (Real)0;\n";
-    for (const Block& b : pg.blocks) {
+    for (size_t bi = 0; bi < pg.blocks.size(); ++bi) {
+      const Block& b = pg.blocks[bi];
       std::string ind = "  ";
+      if (ls && ls->blk_bit[bi] >= 0)
+        os << "  bits |= (r" << pg.guard_regs[b.gid] << " != (Real)0 ? 1u : 0u) << " << ls->blk_bit[bi] << ";\n";
       if (b.gid != 0) {
         os << "  if (r" << pg.guard_regs[b.gid] << " != (Real)0) {\n";
         ind = "    ";
@@ -190,6 +332,12 @@ struct Gen {
           os << " acc += r" << reg << ";";
       }
       os << " out[" << o << "] = acc; }\n";
+    }
+    if (ls) {
+      for (size_t gid = 0; gid < ls->out_bit.size(); ++gid)
+        if (ls->out_bit[gid] >= 0)
+          os << "  bits |= (r" << pg.guard_regs[gid] << " != (Real)0 ? 1u : 0u) << " << ls->out_bit[gid] << ";\n";
+      os << "  *bits_out = bits;\n";
     }
     os << "}\n";
     return name;
@@ -453,15 +601,24 @@ struct Gen {
        << "      } else {\n        " << call(pn) << "\n"
        << "        for (int k = 0; k < " << K << "; ++k) if (!mo_finite((double)o[k])) bad = true;\n"
        << "      }\n";
+    // An excluded element's outputs are 0 and so are its p'Ap terms (p is
+    // pinned to 0 on excluded columns, pcg.hpp:50-55): unless an undamped-
+    // then-unzeroed LM apply asks for damp * p there, nothing is read for it.
+    // The column mask of a field on the gather's domain is the element mask
+    // (k_colmask), so ZEROEXCL tests `ex`.
+    os << "      const bool ez = ex && (!(P.flags & MO_F_DAMP) || (P.flags & MO_F_ZEROEXCL));\n";
     for (size_t k = 0; k < K; ++k) {
       int f = g.chans[k].first, ch = g.chans[k].second;
       int C = P.unknowns[size_t(f)].channels;
       os << "      { const long long col = P.ubase[" << f << "] + e * " << C << " + " << ch << ";\n"
-         << "        Real v = o[" << k << "];\n"
-         << "        if (P.flags & MO_F_DAMP) v = v + DAMP[col] * PV[col];\n"
-         << "        if ((P.flags & MO_F_ZEROEXCL) && P.colmask && P.colmask[col]) v = (Real)0;\n"
-         << "        OUT[col] = v;\n"
-         << "        if (P.flags & MO_F_REDUCE) acc += (double)(PV[col] * v); }\n";
+         << "        if (ez) OUT[col] = (Real)0;\n"
+         << "        else {\n"
+         << "          Real v = o[" << k << "];\n"
+         << "          if (P.flags & MO_F_DAMP) v = v + DAMP[col] * PV[col];\n"
+         << "          if ((P.flags & MO_F_ZEROEXCL) && ex) v = (Real)0;\n"
+         << "          OUT[col] = v;\n"
+         << "          if (P.flags & MO_F_REDUCE) acc += (double)(PV[col] * v);\n"
+         << "        } }\n";
     }
     os << "    }\n  }\n  if (bad) atomicOr(&P.state->nonfinite_kernel, 1);\n"
        << "  if (P.flags & MO_F_REDUCE) mo_reduce_epilogue<Real>(P.red, acc, 0.0, false);\n}\n";
@@ -645,6 +802,10 @@ struct Gen {
       gather_jtj4(g, gi, *S, lg, lane_slot, merged_off(merged), H, 4);
       gather_jtj4(g, gi, *S, lg, lane_slot, merged_off(merged), H, 8, true);
       gather_jtj5(g, gi, *S, lg, lane_slot, merged_off(merged), H);
+      gather_jtj8(g, gi, *S, lg, lane_slot, merged_off(merged), H, 0);
+      gather_jtj8(g, gi, *S, lg, lane_slot, merged_off(merged), H, 1);
+      lane_cache(g, gi, *S, H);
+      if (lc_info.ok) gather_jtj8(g, gi, *S, lg, lane_slot, merged_off(merged), H, 2);
     }
     return tp;
   }
@@ -1175,6 +1336,480 @@ struct Gen {
     staged.clear();
   }
   ModuleInfo::Tma tma5_info;
+
+  // Warp-specialised streaming apply / build_normal (2-D domains),
+  // mo_gather_jtj8_<gi> / mo_gather_bm8_<gi>.  gather_jtj5's dataflow (every
+  // lane evaluates evalj of its element once per phase-1 row, routes the NM
+  // merged-lane contributions through warp shuffles (column offset) into
+  // 2H+1 rolling register accumulators (row offset), and writes output row
+  // q0 - H as soon as it is complete) with a producer/consumer pipeline:
+  //  * warps 0..NW-1 are consumers, each walking its own band of BW output
+  //    columns down the chunk; warp NW is the producer, whose lane 0 streams
+  //    R-row input blocks of every staged field into an NBUF-slot ring by TMA;
+  //  * FULL[s] (TMA transaction bytes) and EMPTY[s] (one arrival per consumer
+  //    warp) mbarriers per slot: consumers never meet at a block barrier and
+  //    never issue copies, the producer runs ahead across work items, so the
+  //    next item's first rows are in flight while the current one drains;
+  //  * the ring is a power of two rows deep, so a row's slot is one mask;
+  //  * the output pixel's exclusion mask is loaded before phase 1 (its latency
+  //    hides behind the row's arithmetic) and 2- / 4-channel outputs are
+  //    stored as one vector per pixel.
+  // Sums are formed per output pixel in row-arrival order (tolerance parity
+  // with the other fast variants, deterministic run to run).  bm = true:
+  // build_normal (solver.hpp:220-251) on the same schedule: phase 1 adds
+  // evalf, forms d_l r_t and d_l^2 per merged lane, two accumulator sets,
+  // and the epilogue applies the identity patch, unconstrained count and the
+  // fused PCG start exactly as mo_gather_bm4.
+  // Lane cache of a gather set (see LaneSplit): planes [NV varying lanes |
+  // guard bits] over the domain extended by H on every side (the phase-1
+  // elements of the border items), element (y, x) at (y + H) * PW + x + HX,
+  // HX = H rounded up to 16 bytes so TMA windows of the planes stay aligned.
+  // mo_lanecache_<gi> writes it once per linearisation (full evalj, global
+  // loads); mo_gather_jtj9_<gi> is gather_jtj8 with phase 1 fed from it.
+  struct LcInfo {
+    bool ok = false;
+    int nv = 0, H = 0, HX = 0, PW = 0, rows = 0, slot0 = 0;
+  } lc_info;
+  LaneSplit lc_split;
+  void lane_cache(const GatherSet& g, int gi, const GridSet& S, int H) {
+    lc_info = LcInfo{};
+    if (std::getenv("MO_B200_NO_LANECACHE") || f64_disabled_tma()) return;
+    if (g.dom.dims.size() != 2) return;
+    lc_split = split_lanes(S.evalj);
+    if (std::getenv("MO_B200_LC_LOG"))
+      fprintf(stderr, "[mo lanecache] gather set %d: %zu lanes, %zu varying, %d guard bits%s\n", gi,
+              S.evalj.outputs.size(), lc_split.varying.size(), lc_split.nbits, lc_split.ok ? "" : " (too many: off)");
+    if (!lc_split.ok) return;
+    const int U = int(P.unknowns.size()), A = int(P.arrays.size());
+    const int slot0 = 2 * U + A + int(P.computed.size());
+    const int nv = int(lc_split.varying.size());
+    if (slot0 + nv + 1 > 32) return;  // MO_MAX_VIEWS
+    const auto sh = P.shape_of(g.dom);
+    const int AU = f64 ? 2 : 4;
+    LcInfo li;
+    li.nv = nv;
+    li.H = H;
+    li.HX = (H + AU - 1) / AU * AU;
+    li.PW = int((sh[1] + li.HX + H + AU - 1) / AU * AU);
+    li.rows = int(sh[0] + 2 * H);
+    li.slot0 = slot0;
+    const std::string sfx = std::to_string(gi);
+    cur_split = &lc_split;
+    split_mode = 1;
+    const std::string pw = program(S.evalj, false, &g.dom);
+    split_mode = 0;
+    cur_split = nullptr;
+    const int NO = int(S.evalj.outputs.size());
+    const int R = reach_of(S.evalj, &g.dom);
+    os << "extern \"C\" __global__ void __launch_bounds__(MO_THREADS) mo_lanecache_" << sfx
+       << "(const __grid_constant__ mo_kparams P) {\n"
+       << "  MO_PDL_ENTRY();\n"
+       << "  constexpr int H = " << H << ", HX = " << li.HX << ", PW = " << li.PW << ", D0 = " << sh[0] << ", D1 = "
+       << sh[1] << ", RR = " << R << ";\n"
+       << "  constexpr long long S = (long long)PW * (D0 + 2 * H);  // plane stride\n"
+       << "  constexpr long long N = (long long)(D0 + 2 * H) * (D1 + 2 * H);\n"
+       << "  Real* const CC = (Real*)P.out0;\n"
+       << "  bool bad = false;\n"
+       << "  for (long long i = blockIdx.x * (long long)MO_THREADS + threadIdx.x + threadIdx.y * blockDim.x; i < N;\n"
+       << "       i += (long long)gridDim.x * MO_THREADS) {\n"
+       << "    const int y = int(i / (D1 + 2 * H)) - H, x = int(i % (D1 + 2 * H)) - H;\n"
+       << "    const bool it = y >= RR && y < D0 - RR && x >= RR && x < D1 - RR;\n"
+       << "    Real d[" << std::max(NO, 1) << "];\n"
+       << "    unsigned bits = 0u;\n"
+       << "    if (it) " << pw << "<true>(P, y, x, 0, y * D1 + x, nullptr, d, &bits); else " << pw
+       << "<false>(P, y, x, 0, 0, nullptr, d, &bits);\n"
+       << "    const long long c = (long long)(y + H) * PW + (x + HX);\n";
+    for (int j = 0; j < nv; ++j)
+      os << "    CC[" << j << " * S + c] = d[" << lc_split.varying[size_t(j)] << "];\n";
+    os << "    CC[" << nv << " * S + c] = " << (f64 ? "__longlong_as_double((long long)bits)" : "__uint_as_float(bits)")
+       << ";\n";
+    os << "  }\n  (void)bad;\n}\n";
+    li.ok = true;
+    lc_info = li;
+  }
+
+  void gather_jtj8(const GatherSet& g, int gi, const GridSet& S, const std::vector<LaneG>& lanes,
+                   const std::vector<int>& lane_slot, const std::vector<MLane>& merged, int H, int mode) {
+    const bool bm = mode == 1, cached = mode == 2;
+    if (f64_disabled_tma()) return;
+    if (bm && S.evalf.outputs.size() != S.jtemplates.size()) return;
+    auto envi = [](const char* n, int d) { const char* v = std::getenv(n); return v ? std::atoi(v) : d; };
+    const std::string sfx = std::to_string(gi);
+    const auto sh = P.shape_of(g.dom);
+    const long long D0 = sh[0], D1 = sh[1];
+    const int BW = 32 - 2 * H;
+    if (BW < 8) return;
+    const int U = int(P.unknowns.size());
+    const int RX = cached ? H : std::max(std::max(reach_of(S.evalj, &g.dom), bm ? reach_of(S.evalf, &g.dom) : 0), H);
+    const int AU = f64 ? 2 : 4;
+    const int RB = f64 ? 8 : 4;
+    int R = 1;
+    while (R < envi("MO_B200_JTJ8_R", 2)) R *= 2;  // rows per TMA box (power of two)
+    int NBUF = 1;
+    // No deadlock: the block a consumer releases last must not wait for a
+    // slot it still holds: NBUF >= 2 + ceil(2RX / R).
+    while (NBUF < std::max(envi("MO_B200_JTJ8_NBUF", 4), 2 + (2 * RX + R - 1) / R)) NBUF *= 2;
+    const int NR = NBUF * R;
+    const int NM = int(merged.size());
+    std::vector<std::pair<int, int>> slots;  // (slot, channels)
+    auto add = [&](int sl, int C) {
+      for (auto& x : slots)
+        if (x.first == sl) return;
+      slots.push_back({sl, C});
+    };
+    auto add_prog = [&](const Program& pg) {
+      for (const Instr& in : pg.instrs) {
+        if (!(in.op == kLoadU || in.op == kLoadA || in.op == kLoadC || in.op == kLoadP) || in.graph) continue;
+        const Field& f = field_of(in.op, in.field);
+        if (f.dom == g.dom) add(slot_of(in.op, in.field), f.channels);
+      }
+    };
+    if (!cached) add_prog(S.evalj);
+    if (bm) add_prog(S.evalf);
+    else {
+      for (const LaneG& l : lanes) add(U + l.f, P.unknowns[size_t(l.f)].channels);
+      for (auto& fc : g.chans) add(U + fc.first, P.unknowns[size_t(fc.first)].channels);
+    }
+    if (slots.empty() || int(slots.size()) > MO_MAX_TMAPS_HOST) return;
+    int cmax = 1;
+    for (auto& x : slots) cmax = std::max(cmax, x.second);
+    // Widest block whose window fits one TMA box row (<= 256 elements); the
+    // window unit keeps 16-byte aligned box starts and 128-byte slots.
+    const int WU = std::max(AU, 128 / (R * RB));
+    int NW = 0, WIN = 0;
+    for (int nw = std::min(4, std::max(1, envi("MO_B200_JTJ8_NW", 4))); nw >= 1; --nw) {
+      const int win = (nw * BW + 2 * H + 2 * RX + AU - 1 + WU - 1) / WU * WU;
+      if (win * cmax <= 256) {
+        NW = nw;
+        WIN = win;
+        break;
+      }
+    }
+    if (!NW) return;
+    long long off = 0;
+    staged.clear();
+    long long tx = 0;
+    std::vector<long long> boxbytes;
+    for (auto& x : slots) {
+      staged.push_back({x.first, {off, x.second}});
+      const long long bb = (long long)R * WIN * x.second * RB;
+      boxbytes.push_back(bb);
+      tx += bb;
+      off += (long long)NBUF * bb;
+    }
+    const long long mbar_off = off;
+    off += 16LL * NBUF;
+    st_rx = RX;
+    st_win = WIN;
+    if (cached) {
+      cur_split = &lc_split;
+      split_mode = 2;
+    }
+    const std::string pe = program(S.evalj, false, &g.dom, true);
+    split_mode = 0;
+    cur_split = nullptr;
+    sm_mode = true;  // (smx below reads the staged rings)
+    const std::string pf = bm ? program(S.evalf, false, &g.dom, true) : std::string();
+    const int NO = int(S.evalj.outputs.size());
+    const int NT = int(S.jtemplates.size());
+    const std::string LN = (bm ? "mo_lanesbm8_" : cached ? "mo_lanes9_" : "mo_lanes8_") + sfx;
+    os << "template <bool I> __device__ __forceinline__ void " << LN
+       << "(const mo_kparams& P, int p0, int p1, const int* ri, int lx, Real* c" << (bm ? ", Real* cm" : "")
+       << (cached ? ", const Real* cv, unsigned bits" : "") << ") {\n"
+       << "  const bool inside = I || mo_inb(P, p0, p1, 0); (void)inside;\n"
+       << "  Real d[" << NO << "];\n";
+    if (cached) {
+      os << "  " << pe << "(P, bits, cv, d);\n";
+    } else {
+      os << "  " << pe << "<I>(P, p0, p1, 0, ri, lx, d);\n";
+    }
+    if (bm) {
+      os << "  Real fv[" << NT << "];\n  " << pf << "<I>(P, p0, p1, 0, ri, lx, fv);\n";
+      for (int si = 0; si < NM; ++si) os << "  Real mb" << si << " = (Real)0, mm" << si << " = (Real)0;\n";
+      for (int t = 0; t < NT; ++t) {
+        const bool origin = S.jtemplates[size_t(t)].origin;
+        os << "  {" << (origin ? " if (inside) {" : "") << "\n";
+        for (size_t li = 0; li < lanes.size(); ++li)
+          if (lanes[li].t == t)
+            os << "    mb" << lane_slot[li] << " += d[" << lanes[li].out << "] * fv[" << t << "]; mm" << lane_slot[li]
+               << " += d[" << lanes[li].out << "] * d[" << lanes[li].out << "];\n";
+        os << "  }" << (origin ? " }" : "") << "\n";
+      }
+      for (int si = 0; si < NM; ++si) os << "  c[" << si << "] = mb" << si << "; cm[" << si << "] = mm" << si << ";\n";
+    } else {
+      for (int si = 0; si < NM; ++si) os << "  Real m" << si << " = (Real)0;\n";
+      for (int t = 0; t < NT; ++t) {
+        os << "  { Real jp = (Real)0;\n";
+        for (const LaneG& l : lanes)
+          if (l.t == t) os << "    jp += d[" << l.out << "] * " << smx(U + l.f, l.o0, l.o1, l.c) << ";\n";
+        const bool origin = S.jtemplates[size_t(t)].origin;
+        if (origin) os << "    if (inside) {\n";
+        for (size_t li = 0; li < lanes.size(); ++li)
+          if (lanes[li].t == t) os << "    m" << lane_slot[li] << " += d[" << lanes[li].out << "] * jp;\n";
+        if (origin) os << "    }\n";
+        os << "  }\n";
+      }
+      for (int si = 0; si < NM; ++si) os << "  c[" << si << "] = m" << si << ";\n";
+    }
+    os << "}\n";
+    sm_mode = false;
+
+    const int K = int(g.chans.size());
+    const int NA = 2 * H + 1;
+    const std::string kn = (bm ? "mo_gather_bm8_" : cached ? "mo_gather_jtj9_" : "mo_gather_jtj8_") + sfx;
+    const int minb = envi(bm ? "MO_B200_BM8_MINB" : "MO_B200_JTJ8_MINB", 0);
+    std::ostringstream is;  // TMA issue of input block j (inline: tensor maps in param space)
+    is << "{ const int s_ = gb & (NBUF - 1);\n"
+       << "          if (gb >= NBUF) mo_mbar_wait(EMPTY + s_, ((gb >> LNB) - 1) & 1);\n"
+       << "          mo_fence_proxy_async();\n"
+       << "          mo_mbar_expect_tx(FULL + s_, " << tx << "u);\n"
+       << "          const int r_ = y0 - H - RX + R * j - P.row_lo;\n";
+    for (size_t i = 0; i < slots.size(); ++i) {
+      const bool cp = cached && slots[i].first >= lc_info.slot0;  // lane-cache plane: extended-domain coordinates
+      is << "          mo_tma_load_2d(mo_dsm + " << staged[i].second.first << " + s_ * " << boxbytes[i] << ", &T.m[" << i
+         << "], " << (cp ? "cs + " + std::to_string(lc_info.HX) : "cs * " + std::to_string(slots[i].second)) << ", r_"
+         << (cp ? " + P.row_lo + " + std::to_string(lc_info.H) : std::string()) << ", FULL + s_);\n";
+    }
+    is << "        }\n";
+    int LNB = 0;
+    while ((1 << LNB) < NBUF) ++LNB;
+    int LR = 0;
+    while ((1 << LR) < R) ++LR;
+    os << "extern \"C\" __global__ void __launch_bounds__(" << 32 * (NW + 1) << (minb > 0 ? ", " + std::to_string(minb) : "")
+       << ") " << kn << "(const __grid_constant__ mo_kparams P, const __grid_constant__ mo_tmaps T) {\n"
+       << "  MO_PDL_ENTRY();\n"
+       << "  if ((P.flags & MO_F_SKIPDONE) && P.state->done) return;\n";
+    if (bm)
+      os << "  if ((P.flags & MO_F_PCGINIT) && blockIdx.x == 0 && threadIdx.x == 0) {\n"
+         << "    P.state->done = 0; P.state->iters = 0; P.state->indefinite = 0; P.state->nonfinite = 0;\n"
+         << "  }\n";
+    os << "  unsigned long long* const FULL = reinterpret_cast<unsigned long long*>(mo_dsm + " << mbar_off << ");\n"
+       << "  unsigned long long* const EMPTY = FULL + " << NBUF << ";\n"
+       << "  double acc = 0, cnt = 0, rz = 0; (void)cnt; (void)rz;\n"
+       << "  unsigned em = 0;  // max exponent field of the outputs: all ones <=> a non-finite output\n"
+       << "  const int tid = threadIdx.x;\n"
+       << "  const int w = tid >> 5, l = tid & 31;\n"
+       << "  constexpr int NW = " << NW << ", BW = " << BW << ", H = " << H << ", RX = " << RX << ", R = " << R
+       << ", LR = " << LR << ", NBUF = " << NBUF << ", LNB = " << LNB << ", NR = " << NR << ";\n"
+       << "  constexpr int D0 = " << D0 << ", D1 = " << D1 << ", NBG = " << (D1 + NW * BW - 1) / (NW * BW) << ";\n"
+       << "  (void)D0; (void)LR;\n"
+       << "  if (tid == 0) {\n"
+       << "    for (int i = 0; i < NBUF; ++i) { mo_mbar_init(FULL + i, 1); mo_mbar_init(EMPTY + i, NW); }\n"
+       << "    mo_mbar_fence_init();\n"
+       << "  }\n"
+       << "  __syncthreads();\n"
+       << "  const int CH = P.chunk;\n"
+       << "  const int nch = (P.row1 - P.row0 + CH - 1) / CH;\n"
+       << "  const int items = NBG * nch;\n"
+       << "  if (w == NW) {  // producer warp: lane 0 streams every item's input blocks\n"
+       << "    if (l == 0) {\n"
+       << "      int gb = 0;  // global input-block counter (slot gb % NBUF, use gb / NBUF)\n"
+       << "      for (int t = blockIdx.x; t < items; t += gridDim.x) {\n"
+       << "        const int ci = t / NBG, c0 = (t - ci * NBG) * (NW * BW);\n"
+       << "        const int y0 = P.row0 + ci * CH, y1 = min(y0 + CH, P.row1);\n"
+       << "        const int cs = (c0 - H - RX) - ((c0 - H - RX) & " << AU - 1 << ");\n"
+       << "        const int nblk = (y1 - y0 + 2 * H + 2 * RX + R - 1) >> LR;\n"
+       << "        for (int j = 0; j < nblk; ++j, ++gb) " << is.str()
+       << "      }\n"
+       << "    }\n"
+       << "    __syncwarp();\n"
+       << "  } else {\n"
+       << "    const int fl = P.flags; (void)fl;\n";
+    if (bm)
+      os << "    Real* const B = (Real*)P.out0; Real* const M = (Real*)P.out1;\n"
+         << "    Real* const PP = (Real*)P.out2; Real* const DL = (Real*)P.out3; Real* const RR = (Real*)P.out4;\n"
+         << "    const int pre = P.state->use_precond;\n";
+    else
+      os << "    Real* const OUT = (Real*)P.out0; const Real* const DAMP = (const Real*)P.in1; (void)DAMP;\n"
+         << "    const bool vec_ok = (reinterpret_cast<unsigned long long>(OUT) & 15) == 0; (void)vec_ok;\n";
+    os << "    int gb = 0;  // global index of the item's input block 0\n"
+       << "    for (int t = blockIdx.x; t < items; t += gridDim.x) {\n"
+       << "      const int ci = t / NBG, c0 = (t - ci * NBG) * (NW * BW);\n"
+       << "      const int y0 = P.row0 + ci * CH, y1 = min(y0 + CH, P.row1);\n"
+       << "      const bool it = y0 - H - RX >= 0 && y1 + H - 1 + RX < D0 && c0 - H - RX >= 0 && c0 + NW * BW + H - 1 + RX < D1;\n"
+       << "      const int sh = (c0 - H - RX) & " << AU - 1 << ";\n"
+       << "      const int nrows = y1 - y0 + 2 * H;  // phase-1 rows\n"
+       << "      const int nblk = (nrows + 2 * RX + R - 1) >> LR;\n"
+       << "      const int rb = (gb << LR) & (NR - 1);  // ring row of the item's input row 0\n"
+       << "      const int q1 = c0 + w * BW - H + l;\n"
+       << "      const int lx = w * BW + l + RX + sh;  // window column of this lane's element\n"
+       << "      const bool lane_out = l >= H && l < 32 - H && q1 < D1;\n"
+       << "      int nwt = 0;  // input blocks of this item waited so far\n";
+    for (int k = 0; k < K; ++k)
+      for (int a = 0; a < NA; ++a) {
+        os << "      Real A" << k << "_" << a << " = (Real)0;\n";
+        if (bm) os << "      Real Q" << k << "_" << a << " = (Real)0;\n";
+      }
+    os << "      int e = (y0 - 2 * H - P.row_lo) * D1 + q1;  // element of output row y0 - 2H + k\n";
+    const int NVC = cached ? lc_info.nv + 1 : 0;
+    if (cached) {
+      // Lane cache of this lane's phase-1 element, read straight from global
+      // memory (coalesced along the row, never a halo) one row ahead.
+      os << "      constexpr long long LSTR = (long long)" << lc_info.PW << " * " << lc_info.rows << ";\n"
+         << "      const Real* __restrict__ cp = (const Real*)P.in2 + (long long)y0 * " << lc_info.PW
+         << " + min(q1, D1 + H - 1) + " << lc_info.HX << ";  // row q0 + H of phase-1 row k = 0\n"
+         << "      Real cn[" << NVC << "];\n"
+         << "      #pragma unroll\n"
+         << "      for (int j = 0; j < " << NVC << "; ++j) cn[j] = __ldg(cp + j * LSTR);\n";
+    }
+    os << "      for (int k = 0; k < nrows; ++k, e += D1) {\n";
+    if (cached)
+      os << "        Real cc[" << NVC << "];\n"
+         << "        #pragma unroll\n"
+         << "        for (int j = 0; j < " << NVC << "; ++j) cc[j] = cn[j];\n"
+         << "        if (k + 1 < nrows) {\n"
+         << "          cp += " << lc_info.PW << ";\n"
+         << "          #pragma unroll\n"
+         << "          for (int j = 0; j < " << NVC << "; ++j) cn[j] = __ldg(cp + j * LSTR);\n"
+         << "        }\n"
+         << "        const unsigned cbits = " << (f64 ? "(unsigned)__double_as_longlong(cc[" : "__float_as_uint(cc[")
+         << NVC - 1 << "]);\n";
+    os << "        const int need = min(nblk - 1, (k + 2 * RX) >> LR);\n"
+       << "        while (nwt <= need) {\n"
+       << "          const int b = gb + nwt;\n"
+       << "          mo_mbar_wait(FULL + (b & (NBUF - 1)), (b >> LNB) & 1);\n"
+       << "          ++nwt;\n"
+       << "        }\n"
+       << "        const int q0 = y0 - H + k;\n"
+       << "        const int y = q0 - H;\n"
+       << "        const bool orow = k >= 2 * H && y < y1 && lane_out;\n"
+       << "        const bool ex = orow && P.mask && P.mask[e];  // (loaded before phase 1)\n"
+       << "        int ri[" << 2 * RX + 1 << "];\n"
+       << "        #pragma unroll\n"
+       << "        for (int o = 0; o < " << 2 * RX + 1 << "; ++o) ri[o] = (rb + k + o) & (NR - 1);\n"
+       << "        Real c[" << NM << "];\n";
+    if (bm)
+      os << "        Real cm[" << NM << "];\n"
+         << "        if (it) " << LN << "<true>(P, q0, q1, ri, lx, c, cm); else " << LN << "<false>(P, q0, q1, ri, lx, c, cm);\n";
+    else if (cached)
+      os << "        if (it) " << LN << "<true>(P, q0, q1, ri, lx, c, cc, cbits); else " << LN
+         << "<false>(P, q0, q1, ri, lx, c, cc, cbits);\n";
+    else
+      os << "        if (it) " << LN << "<true>(P, q0, q1, ri, lx, c); else " << LN << "<false>(P, q0, q1, ri, lx, c);\n";
+    for (int si = 0; si < NM; ++si) {
+      const MLane& m = merged[size_t(si)];
+      int kk = -1;
+      for (int k = 0; k < K; ++k)
+        if (g.chans[size_t(k)].first == m.f && g.chans[size_t(k)].second == m.c) kk = k;
+      if (kk < 0) continue;
+      auto route = [&](const std::string& acc, const std::string& arr) {
+        std::string v = arr + "[" + std::to_string(si) + "]";
+        if (m.o1 > 0) v = "__shfl_up_sync(0xffffffffu, " + v + ", " + std::to_string(m.o1) + ")";
+        if (m.o1 < 0) v = "__shfl_down_sync(0xffffffffu, " + v + ", " + std::to_string(-m.o1) + ")";
+        os << "        " << acc << kk << "_" << H + m.o0 << " += " << v << ";\n";
+      };
+      route("A", "c");
+      if (bm) route("Q", "cm");
+    }
+    os << "        if (orow) {\n";
+    if (bm) {
+      for (int k = 0; k < K; ++k) {
+        const int f = g.chans[size_t(k)].first, ch = g.chans[size_t(k)].second;
+        const int C = P.unknowns[size_t(f)].channels;
+        os << "          { Real b = ex ? (Real)0 : (Real)-2 * A" << k << "_0, m = ex ? (Real)0 : (Real)2 * Q" << k << "_0;\n"
+           << "            em = max(em, max(MO_EXP_BITS(b), MO_EXP_BITS(m)));\n"
+           << "            if (fl & MO_F_PATCH) {\n"
+           << "              if (ex) { b = (Real)0; m = (Real)1; }\n"
+           << "              else if (m == (Real)0) { m = (Real)1; cnt += 1.0; }\n"
+           << "            }\n"
+           << "            const int col = (int)P.ubase[" << f << "] + e * " << C << " + " << ch << ";\n"
+           << "            B[col] = b; M[col] = m;\n"
+           << "            if (fl & MO_F_PCGINIT) {\n"
+           << "              const Real zi = ex ? (Real)0 : (pre ? ((b == (Real)0 && m > (Real)0) ? b : b / m) : b);\n"
+           << "              DL[col] = (Real)0; RR[col] = b; PP[col] = zi; rz += (double)(b * zi);\n"
+           << "            } }\n";
+      }
+    } else {
+      os << "          const int rp = (rb + k - H + RX) & (NR - 1);  // staged p of the output pixel\n"
+         << "          Real pa = (Real)0;  // this pixel's p'Ap terms (products in Real, as pcg.hpp:43)\n";
+      std::vector<int> fields;
+      for (auto& fc : g.chans)
+        if (std::find(fields.begin(), fields.end(), fc.first) == fields.end()) fields.push_back(fc.first);
+      for (int f : fields) {
+        const int C = P.unknowns[size_t(f)].channels;
+        os << "          const int cb" << f << " = (int)P.ubase[" << f << "] + e * " << C << ";\n";
+        std::vector<int> ks;  // this field's output channels, channel order
+        for (int c = 0; c < C; ++c)
+          for (int k = 0; k < K; ++k)
+            if (g.chans[size_t(k)].first == f && g.chans[size_t(k)].second == c) ks.push_back(k);
+        for (int k : ks) {
+          const int ch = g.chans[size_t(k)].second;
+          const auto* st = staged_of(U + f);
+          os << "          Real v" << k << " = ex ? (Real)0 : (Real)2 * A" << k << "_0;\n"
+             << "          em = max(em, MO_EXP_BITS(v" << k << "));\n"
+             << "          { const Real pc = reinterpret_cast<const Real*>(mo_dsm + " << st->first << ")[rp * " << WIN * C
+             << " + lx * " << C << " + " << ch << "];\n"
+             << "            if (fl & MO_F_DAMP) v" << k << " = v" << k << " + DAMP[cb" << f << " + " << ch << "] * pc;\n"
+             << "            if ((fl & MO_F_ZEROEXCL) && ex) v" << k << " = (Real)0;\n"
+             << "            pa += pc * v" << k << "; }\n";
+        }
+        // one vector store per pixel when the field's channels are all outputs
+        const bool whole = int(ks.size()) == C;
+        const long long ub = P.ubase[size_t(f)];
+        const std::string vt = f64 ? (C == 2 ? "double2" : "") : (C == 2 ? "float2" : C == 4 ? "float4" : "");
+        if (whole && !vt.empty() && (ub % C) == 0) {
+          os << "          if (vec_ok) *reinterpret_cast<" << vt << "*>(OUT + cb" << f << ") = make_" << vt << "(";
+          for (int c = 0; c < C; ++c) os << (c ? ", " : "") << "v" << ks[size_t(c)];
+          os << ");\n          else {";
+          for (int c = 0; c < C; ++c) os << " OUT[cb" << f << " + " << c << "] = v" << ks[size_t(c)] << ";";
+          os << " }\n";
+        } else {
+          for (int k : ks) os << "          OUT[cb" << f << " + " << g.chans[size_t(k)].second << "] = v" << k << ";\n";
+        }
+      }
+      os << "          if (fl & MO_F_REDUCE) acc += (double)pa;\n";
+    }
+    os << "        }\n";
+    for (int k = 0; k < K; ++k)
+      for (const char* A : {"A", "Q"}) {
+        if (*A == 'Q' && !bm) continue;
+        for (int a = 0; a + 1 < NA; ++a) os << "        " << A << k << "_" << a << " = " << A << k << "_" << a + 1 << ";\n";
+        os << "        " << A << k << "_" << NA - 1 << " = (Real)0;\n";
+      }
+    os << "        if ((k & (R - 1)) == R - 1) {  // input block k / R: its last row as a phase-1 centre row\n"
+       << "          __syncwarp();\n"
+       << "          if (l == 0) mo_mbar_arrive(EMPTY + ((gb + (k >> LR)) & (NBUF - 1)));\n"
+       << "        }\n"
+       << "      }\n"
+       << "      // release the item's remaining input blocks (each waited first)\n"
+       << "      for (int j = nrows >> LR; j < nblk; ++j) {\n"
+       << "        while (nwt <= j) {\n"
+       << "          const int b = gb + nwt;\n"
+       << "          mo_mbar_wait(FULL + (b & (NBUF - 1)), (b >> LNB) & 1);\n"
+       << "          ++nwt;\n"
+       << "        }\n"
+       << "        __syncwarp();\n"
+       << "        if (l == 0) mo_mbar_arrive(EMPTY + ((gb + j) & (NBUF - 1)));\n"
+       << "      }\n"
+       << "      gb += nblk;\n"
+       << "    }\n"
+       << "  }\n"
+       << "  if (em == MO_EXP_MASK) atomicOr(&P.state->nonfinite_kernel, 1);\n";
+    if (bm)
+      os << "  if (P.flags & MO_F_REDUCE) mo_reduce_epilogue<Real>(P.red, cnt, rz, (P.flags & MO_F_PCGINIT) != 0);\n}\n";
+    else
+      os << "  if (P.flags & MO_F_REDUCE) mo_reduce_epilogue<Real>(P.red, acc, 0.0, false);\n}\n";
+    ModuleInfo::Tma ti;
+    ti.ok = true;
+    ti.smem = size_t(off);
+    ti.halo = H;
+    ti.band = NW * BW;
+    ti.rx = RX;
+    ti.win = WIN;
+    ti.rows = R;
+    ti.threads = 32 * (NW + 1);
+    for (auto& x : slots) ti.slots.push_back({x.first, x.second});
+    if (cached) {
+      ti.cache_planes = lc_info.nv + 1;
+      ti.cache_slot0 = lc_info.slot0;
+      ti.cache_hx = lc_info.HX;
+      ti.cache_pw = lc_info.PW;
+      ti.cache_rows = lc_info.rows;
+    }
+    (bm ? tmabm8_info : cached ? tma9_info : tma8_info) = ti;
+    staged.clear();
+  }
+  ModuleInfo::Tma tma8_info, tmabm8_info, tma9_info;
 
   // TMA-staged gather program (2-D domains): the reference's own J^T J p
   // gather program (transform.hpp:238-260, run_program semantics) per output
@@ -1715,6 +2350,9 @@ struct Gen {
         info.jtj6.push_back({});
         info.jtj7.push_back({});
         info.bm4.push_back({});
+        info.jtj8.push_back({});
+        info.bm8.push_back({});
+        info.jtj9.push_back({});
         continue;
       }
       gather_jtj(g, program(g.jtj, false, &g.dom), "mo_gather_jtj_" + std::to_string(i));
@@ -1725,6 +2363,9 @@ struct Gen {
       tma7_info = ModuleInfo::Tma{};
       tmabm_info = ModuleInfo::Tma{};
       tma5_info = ModuleInfo::Tma{};
+      tma8_info = ModuleInfo::Tma{};
+      tmabm8_info = ModuleInfo::Tma{};
+      tma9_info = ModuleInfo::Tma{};
       TwoPhase tp = gather_jtj2(g, int(i));
       info.jtj2.push_back({tp.ok, tp.smem, tp.nlanes, tp.H});
       info.jtj3.push_back(stream_info);
@@ -1733,6 +2374,9 @@ struct Gen {
       info.jtj6.push_back(tma6_info);
       info.jtj7.push_back(tma7_info);
       info.bm4.push_back(tmabm_info);
+      info.jtj8.push_back(tma8_info);
+      info.bm8.push_back(tmabm8_info);
+      info.jtj9.push_back(tma9_info);
     }
     for (size_t i = 0; i < P.graph_sets.size(); ++i) {
       const GraphSet& g = P.graph_sets[i];

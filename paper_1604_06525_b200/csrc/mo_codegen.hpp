@@ -32,6 +32,9 @@ struct ModuleInfo {
     int halo = 0, band = 0, rx = 0, win = 0;
     int rows = 8, threads = 256;             // box rows; block size
     std::vector<std::pair<int, int>> slots;  // (view slot, channels)
+    // lane-cache apply (mo_gather_jtj9): planes, their first view slot and the
+    // extended-domain plane geometry (column origin HX, pitch PW, rows)
+    int cache_planes = 0, cache_slot0 = 0, cache_hx = 0, cache_pw = 0, cache_rows = 0;
   };
   std::vector<TwoPhase> jtj2;  // per gather set
   std::vector<Stream> jtj3;    // per gather set
@@ -40,6 +43,9 @@ struct ModuleInfo {
   std::vector<Tma> jtj6;       // per gather set: TMA-staged gather program
   std::vector<Tma> jtj7;       // per gather set: variant 3 with 4-row steps (128 threads)
   std::vector<Tma> bm4;        // per gather set: TMA two-phase build_normal (mo_gather_bm4_<i>)
+  std::vector<Tma> jtj8;       // per gather set: warp-specialised streaming apply (mo_gather_jtj8_<i>)
+  std::vector<Tma> bm8;        // per gather set: warp-specialised streaming build_normal (mo_gather_bm8_<i>)
+  std::vector<Tma> jtj9;       // per gather set: lane-cache streaming apply (mo_gather_jtj9_<i>, mo_lanecache_<i>)
   std::vector<bool> vertex_kernels;  // per graph set: mo_graph_v{jtj,bm}_<g>_<dom> exist
   bool fused_vertex_apply = false;   // mo_graph_vjtjf_0: grid gather + graph gather + finish in one pass
 };

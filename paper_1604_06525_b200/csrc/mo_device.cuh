@@ -106,7 +106,7 @@ struct mo_kparams {
 // TMA tensor maps of the fields a staged apply kernel streams into shared
 // memory (second __grid_constant__ kernel parameter).  Same 128-byte, 64-byte
 // aligned layout as the driver's CUtensorMap.
-#define MO_MAX_TMAPS 12
+#define MO_MAX_TMAPS 16
 struct __align__(64) mo_tmap {
   unsigned long long w[16];
 };
@@ -148,6 +148,10 @@ __device__ __forceinline__ void mo_mbar_wait(unsigned long long* b, unsigned par
         : "r"(mo_smem_addr(b)), "r"(parity)
         : "memory");
   } while (!ok);
+}
+// One plain arrival (release): a consumer is done with a ring slot.
+__device__ __forceinline__ void mo_mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mo_smem_addr(b)) : "memory");
 }
 // Generic-proxy reads of a ring slot are ordered before the async-proxy
 // (TMA) writes that refill it.

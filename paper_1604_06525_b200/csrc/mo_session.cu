@@ -172,6 +172,7 @@ class Session final : public SessionBase {
     for (Real* p : {x_, xt_, b_, damp_, vtmp_, otmp_, resid_}) cudaFree(p);
     cudaFree(arena_);
     cudaFree(bd_);
+    for (Real* p : lcache_) cudaFree(p);
     for (Real* p : arr_) cudaFree(p);
     for (Real* p : comp_) cudaFree(p);
     for (unsigned char* p : masks_) cudaFree(p);
@@ -400,6 +401,7 @@ class Session final : public SessionBase {
     ensure_refreshed();
     tune_apply();
     check(n == P_.num_cols, Err::kShapeMismatch, "apply_jtj(): vector size mismatch");
+    lanecache_fill();  // (x may have changed since the last linearisation)
     if (device) {
       apply(static_cast<const Real*>(v), static_cast<Real*>(out), 0);
       CK(cudaStreamSynchronize(st_));
@@ -624,6 +626,42 @@ class Session final : public SessionBase {
       p.count = 0;
     }
   }
+  // Unperturbed kernel timing for the roofline (bench.py): `reps` launches
+  // of the J^T J p apply (which = 0, on the session's p, as a PCG iteration
+  // launches it) or of build_normal (which = 1) captured as one CUDA graph,
+  // best of 3 replays; ms per launch.  Clobbers the PCG scratch vectors.
+  double bench_kernel(int which, int reps) override {
+    check(which == 0 || which == 1, Err::kBindError, "bench_kernel: which must be 0 (apply) or 1 (build_normal)");
+    check(reps >= 1 && reps <= 1000, Err::kBindError, "bench_kernel: reps out of range");
+    ensure_refreshed();
+    tune_apply();
+    const int stage = cur_stage_;
+    cur_stage_ = -1;  // no profiling events
+    const int64_t launched = launches_;
+    const bool cons = !sh_.on && !mat_ && (P_.graph_sets.empty() || vertex_apply_one_pass());
+    float ms = 0;
+    if (which == 0) {
+      lanecache_fill();
+      auto body = [&] {
+        for (int r = 0; r < reps; ++r) {
+          consumer_ = cons;
+          apply(p_, ap_, MO_F_REDUCE | MO_F_ZEROEXCL);
+          consumer_ = false;
+        }
+      };
+      body();  // warm-up (tensor maps, module load)
+      ms = time_graph(body);
+    } else {
+      normal_device();
+      ms = time_graph([&] {
+        for (int r = 0; r < reps; ++r) normal_device();
+      });
+    }
+    CK(cudaStreamSynchronize(st_));
+    launches_ = launched;
+    cur_stage_ = stage;
+    return double(ms) / reps;
+  }
   void* stream() override { return st_; }
   int64_t launches() const override { return launches_; }
   std::string apply_kernel(int i) override {
@@ -639,7 +677,8 @@ class Session final : public SessionBase {
     ensure_refreshed();
     tune_apply();
     if (!P_.graph_sets.empty() && vertex_path(0)) return "mo_graph_vbm_0";
-    return (bm_choice_.size() > size_t(i) && bm_choice_[size_t(i)] ? "mo_gather_bm4_" : "mo_gather_bm_") +
+    const int bc = bm_choice_.size() > size_t(i) ? bm_choice_[size_t(i)] : 0;
+    return (bc == 2 ? "mo_gather_bm8_" : bc == 1 ? "mo_gather_bm4_" : "mo_gather_bm_") +
            std::to_string(i);
   }
 
@@ -1141,18 +1180,37 @@ class Session final : public SessionBase {
     if (nd == 2) return int(((s[1] + MO_TILE_X - 1) / MO_TILE_X) * ((rows + MO_TILE_Y - 1) / MO_TILE_Y));
     return int(((s[2] + MO_TILE_X - 1) / MO_TILE_X) * rows * ((s[1] + MO_TILE_Y - 1) / MO_TILE_Y));
   }
-  int occupancy(const void* f, size_t smem = 0) {
+  int occupancy(const void* f, size_t smem = 0, int threads = MO_THREADS) {
     auto it = occ_.find(f);
     if (it != occ_.end()) return it->second;
     if (smem > 48 * 1024)
       CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, f, MO_THREADS, smem) != cudaSuccess || n <= 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, f, threads, smem) != cudaSuccess || n <= 0) {
       cudaGetLastError();
       n = 1;
     }
     occ_[f] = n;
     return n;
+  }
+  // Rows per work item of the row-wise streaming kernels (variants 4, 7 and
+  // mo_gather_bm8): items are dealt to a fixed grid of resident blocks, so a
+  // launch takes ceil(items / grid) rounds of (chunk + 2H) phase-1 rows plus a
+  // small per-item cost; the larger chunk on ties.
+  static int stream_chunk(long long rows, long long nb, long long grid, int halo) {
+    static const int force = std::getenv("MO_B200_CHUNK") ? std::atoi(std::getenv("MO_B200_CHUNK")) : 0;
+    if (force > 0) return force;
+    int best = 0;
+    double best_cost = 1e300;
+    for (int ch = 1; ch <= 256; ++ch) {
+      const long long items = nb * ((rows + ch - 1) / ch);
+      const double cost = double((items + grid - 1) / grid) * (ch + 2 * halo + 4);
+      if (cost <= best_cost) {
+        best_cost = cost;
+        best = ch;
+      }
+    }
+    return std::max(best, 1);
   }
   int grid_blocks(const std::string& name, const Domain& d, size_t smem = 0) {
     const void* f = mod_.kernel(name);
@@ -1177,10 +1235,14 @@ class Session final : public SessionBase {
   // two-phase bands, 3 = TMA-staged row-streaming bands (block-wide 8-row
   // steps), 4 = TMA-staged warp-streaming bands, 5 = TMA-staged gather
   // program (2-D domains).
-  static constexpr int kVariants = 7;
+  static constexpr int kVariants = 9;
   static constexpr int kBm4 = 100;  // tma_info id of the TMA build_normal kernel
+  static constexpr int kBm8 = 101;  // tma_info id of the warp-specialised build_normal kernel
   const ModuleInfo::Tma* tma_info(size_t i, int v) const {
     if (v == kBm4 && i < minfo_.bm4.size()) return &minfo_.bm4[i];
+    if (v == kBm8 && i < minfo_.bm8.size()) return &minfo_.bm8[i];
+    if (v == 7 && i < minfo_.jtj8.size()) return &minfo_.jtj8[i];
+    if (v == 8 && i < minfo_.jtj9.size()) return &minfo_.jtj9[i];
     if (v == 3 && i < minfo_.jtj4.size()) return &minfo_.jtj4[i];
     if (v == 6 && i < minfo_.jtj7.size()) return &minfo_.jtj7[i];
     if (v == 4 && i < minfo_.jtj5.size()) return &minfo_.jtj5[i];
@@ -1193,16 +1255,18 @@ class Session final : public SessionBase {
     if (v == 1) return i < minfo_.jtj2.size() && minfo_.jtj2[i].ok;
     if (v == 2) return i < minfo_.jtj3.size() && minfo_.jtj3[i].ok;
     const ModuleInfo::Tma* t = tma_info(i, v);
+    if (v == 8 && (sh_.on || !t || t->cache_planes == 0)) return false;  // lane cache: unsharded grids
     return t && t->ok && tma_capable(i, *t);
   }
   int variant(size_t i) const {
     if (i < jtj_choice_.size() && variant_ok(i, jtj_choice_[i])) return jtj_choice_[i];
-    for (int v : {3, 6, 5, 4, 2, 1}) if (variant_ok(i, v)) return v;
+    for (int v : {8, 7, 3, 6, 5, 4, 2, 1}) if (variant_ok(i, v)) return v;
     return 0;
   }
   static const char* variant_prefix(int v) {
     static const char* n[] = {"mo_gather_jtj_",  "mo_gather_jtj2_", "mo_gather_jtj3_",
-                              "mo_gather_jtj4_", "mo_gather_jtj5_", "mo_gather_jtj6_", "mo_gather_jtj7_"};
+                              "mo_gather_jtj4_", "mo_gather_jtj5_", "mo_gather_jtj6_", "mo_gather_jtj7_",
+                              "mo_gather_jtj8_", "mo_gather_jtj9_"};
     return n[v];
   }
 
@@ -1253,8 +1317,10 @@ class Session final : public SessionBase {
       const int C = ti.slots[k].second;
       const void* ptr = kp.v[ti.slots[k].first].p;
       check(ptr != nullptr, Err::kInternal, "TMA apply: staged field is not bound");
-      const cuuint64_t dims[2] = {cuuint64_t(sh[1] * C), cuuint64_t(rows)};
-      const cuuint64_t strides[1] = {cuuint64_t(sh[1] * C * (long long)sizeof(Real))};
+      // lane-cache planes: the extended-domain plane geometry
+      const bool cp = ti.cache_planes && ti.slots[k].first >= ti.cache_slot0;
+      const cuuint64_t dims[2] = {cuuint64_t(cp ? ti.cache_pw : sh[1] * C), cuuint64_t(cp ? ti.cache_rows : rows)};
+      const cuuint64_t strides[1] = {cuuint64_t((cp ? ti.cache_pw : sh[1] * C) * (long long)sizeof(Real))};
       const cuuint32_t box[2] = {cuuint32_t(ti.win * C), cuuint32_t(ti.rows)};
       const cuuint32_t estr[2] = {1u, 1u};
       CUresult r = encoder()(reinterpret_cast<CUtensorMap*>(&T.m[k]),
@@ -1309,6 +1375,7 @@ class Session final : public SessionBase {
     static std::map<std::string, std::vector<int>> cache, bm_cache;
     const char* force = std::getenv("MO_B200_JTJ");
     std::string key = module_key_ + (force ? std::string("/force:") + force : "");
+    if (const char* bf = std::getenv("MO_B200_BM")) key += std::string("/bm:") + bf;
     for (auto& d : P_.dims) key += "/" + std::to_string(d.second);
     // A strip that owns the whole domain shares the unsharded decision.
     if (sh_.on && sh_.row1 - sh_.row0 != sh_.d0) key += "/s" + std::to_string(sh_.row1 - sh_.row0);
@@ -1332,7 +1399,9 @@ class Session final : public SessionBase {
                        : fs == "tma" ? 3
                        : fs == "warp" ? 4
                        : fs == "gprog" ? 5
-                                       : 6;
+                       : fs == "tma4" ? 6
+                       : fs == "ws" ? 7
+                                       : 8;
       if (want >= 0) {
         jtj_choice_[i] = variant_ok(i, want) ? want : -1;
         if (jtj_choice_[i] >= 0) continue;
@@ -1350,6 +1419,7 @@ class Session final : public SessionBase {
         t[v] = 1e30f;
         if (!variant_ok(i, v)) continue;
         jtj_choice_[i] = v;
+        if (v == 8) lanecache_fill(i);
         mo_kparams kp = kp_apply(i, x_, otmp_, 0);
         const int grid = jtj_grid(i);
         launch_apply(i, kp, grid);  // warm-up (module load, tensor maps)
@@ -1364,8 +1434,12 @@ class Session final : public SessionBase {
       }
       cudaEventDestroy(a);
       cudaEventDestroy(b);
+      if (std::getenv("MO_B200_TUNE_LOG")) {
+        for (int v = 0; v < kVariants; ++v)
+          if (t[v] < 1e29f) fprintf(stderr, "[mo tune] gather set %zu variant %d: %.1f us\n", i, v, t[v] * 1e3f / 8);
+      }
       int bestv = 0;
-      for (int v : {3, 6, 5, 4, 2, 1, 0})
+      for (int v : {8, 7, 3, 6, 5, 4, 2, 1, 0})
         if (t[v] <= 1.05f * best) {
           bestv = v;
           break;
@@ -1378,30 +1452,34 @@ class Session final : public SessionBase {
     cur_stage_ = -1;  // no profiling events while tuning
     const int64_t launched = launches_;
     for (size_t i = 0; i < P_.gather_sets.size(); ++i) {
-      if (!bm4_avail(i) || sh_.on) continue;  // (strips: normal_device has collectives)
-      float tb[2] = {1e30f, 1e30f};
-      cudaEvent_t a, b;
-      CK(cudaEventCreate(&a));
-      CK(cudaEventCreate(&b));
-      for (int v = 0; v < 2; ++v) {
+      if (sh_.on || (!bm4_avail(i) && !bm8_avail(i))) continue;  // (strips: normal_device has collectives)
+      float tb[3] = {1e30f, 1e30f, 1e30f};
+      for (int v = 0; v < 3; ++v) {
+        if ((v == 1 && !bm4_avail(i)) || (v == 2 && !bm8_avail(i))) continue;
         bm_choice_[i] = v;
         normal_device();  // warm-up
         tb[v] = time_graph([&] {
           for (int rep = 0; rep < 4; ++rep) normal_device();
         });
       }
-      cudaEventDestroy(a);
-      cudaEventDestroy(b);
-      // fp32: the two-phase kernel forms each residual once per element and
-      // sums d_l r_t per merged lane, which tracks the fp64 trajectory far
+      // fp32: the evalj-based kernels form each residual once per element and
+      // sum d_l r_t per merged lane, which tracks the fp64 trajectory far
       // more closely than the bm gather program's fp32 root sums (ARAP
       // 1024², 10 x 20: 1192.985 vs 1193.153, fp64 reference 1192.980), so
-      // it is kept unless it costs more than 30%.  fp64: the faster one.
-      // MO_B200_BM=prog|bm4 forces either.
-      static const char* bmf = std::getenv("MO_B200_BM");
+      // one of them is kept unless it costs more than 30%.  fp64: the
+      // fastest.  Between the two evalj kernels: the faster, bm8 on a 5% tie.
+      // MO_B200_BM=prog|bm4|bm8 forces one.
+      const char* bmf = std::getenv("MO_B200_BM");
       const float slack = sizeof(Real) == 4 ? 1.30f : 0.95f;
-      bm_choice_[i] = tb[1] < slack * tb[0] ? 1 : 0;
-      if (bmf) bm_choice_[i] = std::string(bmf) == "bm4" ? 1 : 0;
+      const int ev = tb[2] <= 1.05f * tb[1] ? 2 : 1;
+      bm_choice_[i] = tb[ev] < slack * tb[0] ? ev : 0;
+      if (std::getenv("MO_B200_TUNE_LOG"))
+        fprintf(stderr, "[mo tune] gather set %zu build_normal: program %.1f us, bm4 %.1f us, bm8 %.1f us\n", i,
+                tb[0] * 1e3f / 4, tb[1] * 1e3f / 4, tb[2] * 1e3f / 4);
+      if (bmf) {
+        const std::string b = bmf;
+        bm_choice_[i] = b == "bm4" && bm4_avail(i) ? 1 : b == "bm8" && bm8_avail(i) ? 2 : 0;
+      }
     }
     launches_ = launched;
     cur_stage_ = stage;
@@ -1454,7 +1532,7 @@ class Session final : public SessionBase {
     jtj_occupancy(i);  // sets the dynamic smem attribute once
     const mo_tmaps& T = tmaps_for(i, v, kp);
     void* args[] = {const_cast<mo_kparams*>(&kp), const_cast<mo_tmaps*>(&T)};
-    const dim3 block = v == 4 ? dim3(unsigned(jtj_threads(i)), 1, 1) : dim3(32, unsigned(jtj_threads(i) / 32), 1);
+    const dim3 block = v == 4 || v >= 7 ? dim3(unsigned(jtj_threads(i)), 1, 1) : dim3(32, unsigned(jtj_threads(i) / 32), 1);
     klc(f, dim3(grid), block, args, smem);
     ++launches_;
   }
@@ -1471,9 +1549,10 @@ class Session final : public SessionBase {
     const int halo = jtj_halo(i), band = jtj_band(i);
     const long long nb = (sh[1] + band - 1) / band;
     const long long grid = (long long)nsm_ * jtj_occupancy(i);
-    const bool rowwise = variant(i) == 4;
+    const bool rowwise = variant(i) == 4 || variant(i) >= 7;
+    if (rowwise) return stream_chunk(rows, nb, grid, halo);
     const ModuleInfo::Tma* ti = tma_info(i, variant(i));
-    const int step = ti && variant(i) != 4 ? ti->rows : 8;  // rows per step of the block-stepped variants
+    const int step = ti && !rowwise ? ti->rows : 8;  // rows per step of the block-stepped variants
     int best = 0;
     double best_cost = 1e300;
     for (int m = 1; m <= (rowwise ? 256 : 128 / step); ++m) {
@@ -1507,7 +1586,39 @@ class Session final : public SessionBase {
     kp.in1 = damp_;
     kp.flags = flags;
     if (variant(i) >= 2) kp.chunk = jtj3_chunk(i);
+    if (variant(i) == 8) {  // lane-cache planes (read directly by the kernel)
+      ensure_lanecache(i);
+      kp.in2 = lcache_[i];
+    }
     return kp;
+  }
+  // ---- lane cache (variant 8): planes of the x-dependent evalj lanes and
+  // guard outcomes, rewritten once per linearisation (normal_device) and
+  // before every standalone apply.
+  void ensure_lanecache(size_t i) {
+    if (lcache_.size() < P_.gather_sets.size()) lcache_.resize(P_.gather_sets.size(), nullptr);
+    if (lcache_[i]) return;
+    const ModuleInfo::Tma& ti = minfo_.jtj9[i];
+    const size_t bytes = size_t(ti.cache_planes) * size_t(ti.cache_pw) * size_t(ti.cache_rows) * sizeof(Real);
+    CK(cudaMalloc(&lcache_[i], bytes));
+    CK(cudaMemsetAsync(lcache_[i], 0, bytes, st_));
+  }
+  void lanecache_fill(size_t i) {
+    ensure_lanecache(i);
+    const std::string kn = "mo_lanecache_" + std::to_string(i);
+    mo_kparams kp = kp_grid(P_.gather_sets[i].dom, x_, nullptr);
+    kp.out0 = lcache_[i];
+    const void* f = mod_.kernel(kn);
+    const int grid = nsm_ * occupancy(f);
+    void* args[] = {&kp};
+    klc(f, dim3(grid), dim3(MO_TILE_X, MO_TILE_Y, 1), args, 0);
+    ++launches_;
+  }
+  void lanecache_fill() {
+    if (mat_) return;
+    tune_apply();
+    for (size_t i = 0; i < P_.gather_sets.size(); ++i)
+      if (variant(i) == 8) lanecache_fill(i);
   }
   void launch_edges(const std::string& name, int gi, const mo_kparams& kp, int grid = 0) {
     const void* f = mod_.kernel(name);
@@ -1648,7 +1759,25 @@ class Session final : public SessionBase {
   }
   // chosen by tune_apply (timed against the bm gather program; kept only
   // when >5% faster: it wins on large grids, loses on small ones)
-  bool bm4_ok(size_t i) const { return i < bm_choice_.size() && bm_choice_[i] && bm4_avail(i); }
+  bool bm4_ok(size_t i) const { return i < bm_choice_.size() && bm_choice_[i] == 1 && bm4_avail(i); }
+  // Warp-specialised streaming build_normal (mo_gather_bm8_<i>), fast mode only.
+  bool bm8_avail(size_t i) const {
+    if (std::getenv("MO_B200_NO_BM4") || P_.exact || i >= minfo_.bm8.size() || !minfo_.bm8[i].ok) return false;
+    return tma_capable(i, minfo_.bm8[i]);
+  }
+  bool bm8_ok(size_t i) const { return i < bm_choice_.size() && bm_choice_[i] == 2 && bm8_avail(i); }
+  // Grid and rows per work item of mo_gather_bm8 (the apply's row model).
+  int bm8_grid(size_t i, int* chunk) {
+    const ModuleInfo::Tma& ti = minfo_.bm8[i];
+    const void* f = mod_.kernel("mo_gather_bm8_" + std::to_string(i));
+    const int occ = occupancy(f, ti.smem, ti.threads);
+    const auto sh = P_.shape_of(P_.gather_sets[i].dom);
+    const long long rows = sh_.on ? sh_.row1 - sh_.row0 : sh[0];
+    const long long nb = (sh[1] + ti.band - 1) / ti.band, grid = (long long)nsm_ * occ;
+    *chunk = stream_chunk(rows, nb, grid, ti.halo);
+    const long long items = nb * ((rows + *chunk - 1) / *chunk);
+    return int(std::max<long long>(1, std::min(items, grid)));
+  }
   int bm4_grid(size_t i, int* chunk) {
     const ModuleInfo::Tma& ti = minfo_.bm4[i];
     const void* f = mod_.kernel("mo_gather_bm4_" + std::to_string(i));
@@ -1681,13 +1810,20 @@ class Session final : public SessionBase {
     return outs == chans;
   }
   void normal_device(bool pcg_init = false) {
+    if (tuned_ && !mat_)  // the linearisation point moved: refresh the lane cache
+      for (size_t i = 0; i < P_.gather_sets.size(); ++i)
+        if (variant(i) == 8) lanecache_fill(i);
     prof_begin(2);
     const bool fused = P_.graph_sets.empty();
     const long long n = P_.num_cols;
     std::vector<int> grids, chunks;
     int total = 0;
     for (size_t i = 0; i < P_.gather_sets.size(); ++i) {
-      if (bm4_ok(i)) {
+      if (bm8_ok(i)) {
+        int ch = 0;
+        grids.push_back(bm8_grid(i, &ch));
+        chunks.push_back(ch);
+      } else if (bm4_ok(i)) {
         int ch = 0;
         grids.push_back(bm4_grid(i, &ch));
         chunks.push_back(ch);
@@ -1713,7 +1849,13 @@ class Session final : public SessionBase {
         kp.out3 = delta_;
         kp.out4 = r_;
       }
-      if (chunks[i]) {  // TMA two-phase build_normal
+      if (chunks[i] && bm8_ok(i)) {  // warp-specialised streaming build_normal
+        const void* f = mod_.kernel("mo_gather_bm8_" + std::to_string(i));
+        const mo_tmaps& T = tmaps_for(i, kBm8, kp);
+        void* args[] = {&kp, const_cast<mo_tmaps*>(&T)};
+        klc(f, dim3(grids[i]), dim3(unsigned(minfo_.bm8[i].threads), 1, 1), args, minfo_.bm8[i].smem);
+        ++launches_;
+      } else if (chunks[i]) {  // TMA two-phase build_normal
         const void* f = mod_.kernel("mo_gather_bm4_" + std::to_string(i));
         const mo_tmaps& T = tmaps_for(i, kBm4, kp);
         void* args[] = {&kp, const_cast<mo_tmaps*>(&T)};
@@ -2509,6 +2651,7 @@ class Session final : public SessionBase {
   ModuleInfo minfo_;
   std::map<int, cudaGraphExec_t> stage_exec_;
   bool tuned_ = false;
+  std::vector<Real*> lcache_;    // per gather set: lane-cache planes (variant 8)
   std::vector<int> bm_choice_;   // per gather set: 1 = TMA two-phase build_normal
   std::vector<int> jtj_choice_;  // per gather set: 0 gather program, 1 two-phase tiles, 2 streaming, 3 TMA streaming
   std::map<std::string, mo_tmaps> tmaps_;  // per (gather set, staged buffers)

@@ -54,6 +54,7 @@ class SessionBase {
   virtual void set_profiling(bool on) = 0;
   virtual void profile_read(int kind, double* ms, int64_t* n) = 0;
   virtual void profile_reset() = 0;
+  virtual double bench_kernel(int which, int reps) = 0;
   virtual void* stream() = 0;
   virtual int64_t launches() const = 0;
   virtual std::string apply_kernel(int gather_set) = 0;

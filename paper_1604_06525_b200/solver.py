@@ -392,6 +392,14 @@ class Solver:
     def profile_reset(self):
         call("mo_profile_reset", self._h)
 
+    def bench_kernel(self, which: int = 0, reps: int = 20) -> float:
+        """ms per launch of the J^T J p apply (which=0) or build_normal (1):
+        `reps` launches replayed as one CUDA graph, best of 3 (mo_bench_kernel;
+        clobbers the PCG scratch vectors)."""
+        ms = ctypes.c_double()
+        call("mo_bench_kernel", self._h, int(which), int(reps), ctypes.byref(ms))
+        return ms.value
+
     def apply_kernel(self, gather_set: int = 0) -> str:
         """Name of the J^T J p kernel the session runs for a gather set."""
         buf = ctypes.create_string_buffer(128)
