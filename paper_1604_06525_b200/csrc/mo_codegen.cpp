@@ -539,7 +539,7 @@ struct Gen {
        << "  const bool pinit = (P.flags & MO_F_PCGINIT) != 0;\n"
        << "  const int pre = P.state->use_precond;\n"
        << "  if (pinit && blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0) {\n"
-       << "    P.state->done = 0; P.state->iters = 0; P.state->indefinite = 0; P.state->nonfinite = 0;\n"
+       << "    P.state->done = 0; P.state->iters = 0; P.state->indefinite = 0; P.state->nonfinite = 0; P.state->stop_code = 0x7fffffff;\n"
        << "  }\n"
           "  const int nt = mo_num_tiles(P);\n"
           "  for (int t = blockIdx.x; t < nt; t += gridDim.x) {\n"
@@ -949,7 +949,7 @@ struct Gen {
        << "  double cnt = 0, rz = 0; (void)cnt; (void)rz;\n";
     if (bm)
       os << "  if ((P.flags & MO_F_PCGINIT) && blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0) {\n"
-         << "    P.state->done = 0; P.state->iters = 0; P.state->indefinite = 0; P.state->nonfinite = 0;\n"
+         << "    P.state->done = 0; P.state->iters = 0; P.state->indefinite = 0; P.state->nonfinite = 0; P.state->stop_code = 0x7fffffff;\n"
          << "  }\n";
     os << "  unsigned long long* MB = reinterpret_cast<unsigned long long*>(mo_dsm + " << mbar_off << ");\n"
        << "  double acc = 0;\n"
@@ -1581,7 +1581,7 @@ struct Gen {
        << "  if ((P.flags & MO_F_SKIPDONE) && P.state->done) return;\n";
     if (bm)
       os << "  if ((P.flags & MO_F_PCGINIT) && blockIdx.x == 0 && threadIdx.x == 0) {\n"
-         << "    P.state->done = 0; P.state->iters = 0; P.state->indefinite = 0; P.state->nonfinite = 0;\n"
+         << "    P.state->done = 0; P.state->iters = 0; P.state->indefinite = 0; P.state->nonfinite = 0; P.state->stop_code = 0x7fffffff;\n"
          << "  }\n";
     os << "  unsigned long long* const FULL = reinterpret_cast<unsigned long long*>(mo_dsm + " << mbar_off << ");\n"
        << "  unsigned long long* const EMPTY = FULL + " << NBUF << ";\n"

@@ -37,6 +37,11 @@ struct mo_state {
   unsigned counters[8];
   double mu;  // LM trust-region radius of the current trial
   double rzs[2];  // consumer-side reductions: rz of PCG iteration k in rzs[k & 1]
+  // Deferred-delta PCG: where the PCG stopped, 2k (the update of iteration k
+  // found p'Ap unusable: no alpha_k) or 2k + 1 (r'z of iteration k ended it
+  // after alpha_k); INT_MAX while running.  Unlike `done`, a kernel of
+  // iteration k can test it against its own k while its block 0 writes it.
+  int stop_code;
 };
 
 // Finalisation ops run by the last block of a reduction.
@@ -234,6 +239,7 @@ __device__ void mo_finalize(mo_state* st, int op, int arg, double total, double 
       if (!mo_finite(double(rz))) {
         st->nonfinite = 1;
         st->done = 1;
+        st->stop_code = -1;  // before iteration 0
         break;
       }
       Real tr = Real(st->tol_rel);
@@ -241,7 +247,10 @@ __device__ void mo_finalize(mo_state* st, int op, int arg, double total, double 
       Real ta = Real(st->tol_abs);
       if (ta > stop) stop = ta;
       st->stop = double(stop);
-      if (rz <= stop) st->done = 1;
+      if (rz <= stop) {
+        st->done = 1;
+        st->stop_code = -1;
+      }
       break;
     }
     case MO_FIN_PCG_ALPHA: {
@@ -371,11 +380,11 @@ template <class Real>
 __device__ __forceinline__ bool mo_alpha_from(mo_state* st, double total, int k, bool writer, Real* alpha) {
   const Real pap = Real(total);
   if (!mo_finite(double(pap))) {
-    if (writer) { st->pap = double(pap); st->nonfinite = 1; st->done = 1; }
+    if (writer) { st->pap = double(pap); st->nonfinite = 1; st->done = 1; st->stop_code = 2 * k; }
     return false;
   }
   if (pap <= Real(0)) {
-    if (writer) { st->pap = double(pap); st->indefinite = 1; st->done = 1; }
+    if (writer) { st->pap = double(pap); st->indefinite = 1; st->done = 1; st->stop_code = 2 * k; }
     return false;
   }
   *alpha = Real(st->rzs[k & 1]) / pap;
@@ -388,11 +397,15 @@ template <class Real>
 __device__ __forceinline__ bool mo_beta_from(mo_state* st, double total, int k, bool writer, Real* beta) {
   const Real rzn = Real(total);
   if (!mo_finite(double(rzn))) {
-    if (writer) { st->rz_next = double(rzn); st->nonfinite = 1; st->done = 1; }
+    if (writer) { st->rz_next = double(rzn); st->nonfinite = 1; st->done = 1; st->stop_code = 2 * k + 1; }
     return false;
   }
   const bool stop = rzn <= Real(st->stop);
-  if (writer) { st->rz_next = double(rzn); st->iters += 1; if (stop) st->done = 1; }
+  if (writer) {
+    st->rz_next = double(rzn);
+    st->iters += 1;
+    if (stop) { st->done = 1; st->stop_code = 2 * k + 1; }
+  }
   if (stop) return false;
   *beta = rzn / Real(st->rzs[k & 1]);
   if (writer) { st->beta = double(*beta); st->rz = double(rzn); st->rzs[(k + 1) & 1] = double(rzn); }

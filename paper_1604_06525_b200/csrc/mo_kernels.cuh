@@ -74,6 +74,7 @@ k_pcg_init(mo_red R, long long n, const unsigned char* cm, const Real* __restric
   MO_PDL_ENTRY();
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     R.state->done = 0;
+    R.state->stop_code = 0x7fffffff;
     R.state->iters = 0;
     R.state->indefinite = 0;
     R.state->nonfinite = 0;
@@ -207,6 +208,132 @@ k_pcg_p(mo_state* st, long long n, const unsigned char* cm, const Real* __restri
     p[i] = pcg_p1(beta, cm ? cm[i] : (unsigned char)0, r[i], md[i], p[i], precond);
 }
 
+// Deferred-delta PCG (consumer-side reductions, unsharded grids).  The
+// update of iteration k only moves r (r -= alpha_k Ap; z = r/m; r'z
+// partials); the direction kernel of the same iteration first folds
+// delta += alpha_k p_k with the p it is about to replace, then p = z + beta p.
+// delta receives the same alpha_k p_k terms in the same order as
+// pcg.hpp:111-112, so every value is bitwise the eager scheme's, and a
+// column moves 42 instead of 46 bytes per iteration (the update no longer
+// reads p or reads and writes delta).  After the last iteration (or an r'z
+// stop) the same kernel runs with last = 1: delta only.  Iteration k's
+// kernels proceed while stop_code > 2k (update) / >= 2k + 1 (direction).
+template <class Real>
+__device__ __forceinline__ double pcg_update_r1(Real alpha, unsigned char m, Real& r, Real ap, Real md, int precond) {
+  if (m & 3) {  // excluded (halo columns do not occur on unsharded grids)
+    r = Real(0);
+    return 0.0;
+  }
+  r = r - alpha * ap;
+  const Real z = precond ? mo_precond_div(r, md) : r;
+  return double(r * z);
+}
+
+template <class Real>
+__global__ void __launch_bounds__(MO_THREADS)
+k_pcg_update_r(mo_red R, long long n, const unsigned char* cm, const Real* __restrict__ md, Real* __restrict__ r,
+               const Real* __restrict__ ap, int precond, const double* pap_part, int pap_n, int k) {
+  MO_PDL_ENTRY();
+  if (R.state->done) return;
+  Real alpha;
+  const double tot = mo_sum_partials(pap_part, pap_n);
+  const bool writer = blockIdx.x == 0 && threadIdx.x == 0;
+  if (!mo_alpha_from<Real>(R.state, tot, k, writer, &alpha)) return;
+  double acc = 0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long n4 = n >> 2;
+  long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  // two 4-wide groups per step, every load issued before the first use (few
+  // streams per column: the loads in flight per thread set the bandwidth)
+  for (; v + stride < n4; v += 2 * stride) {
+    const long long i = v << 2, j = (v + stride) << 2;
+    V4<Real> R0 = ld4(r + i), R1 = ld4(r + j);
+    const V4<Real> A0 = ld4(ap + i), A1 = ld4(ap + j), M0 = ld4(md + i), M1 = ld4(md + j);
+    const uchar4 e0 = ldm4(cm, i), e1 = ldm4(cm, j);
+    const unsigned char x0[4] = {e0.x, e0.y, e0.z, e0.w}, x1[4] = {e1.x, e1.y, e1.z, e1.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc += pcg_update_r1(alpha, x0[q], R0.a[q], A0.a[q], M0.a[q], precond);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc += pcg_update_r1(alpha, x1[q], R1.a[q], A1.a[q], M1.a[q], precond);
+    st4(r + i, R0);
+    st4(r + j, R1);
+  }
+  for (; v < n4; v += stride) {
+    const long long i = v << 2;
+    V4<Real> Rr = ld4(r + i);
+    const V4<Real> A = ld4(ap + i), M = ld4(md + i);
+    const uchar4 e = ldm4(cm, i);
+    const unsigned char ex[4] = {e.x, e.y, e.z, e.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc += pcg_update_r1(alpha, ex[q], Rr.a[q], A.a[q], M.a[q], precond);
+    st4(r + i, Rr);
+  }
+  for (long long i = (n4 << 2) + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride)
+    acc += pcg_update_r1(alpha, cm ? cm[i] : (unsigned char)0, r[i], ap[i], md[i], precond);
+  mo_reduce_epilogue<Real>(R, acc, 0.0, false);
+}
+
+template <class Real>
+__global__ void __launch_bounds__(MO_THREADS)
+k_pcg_dp(mo_state* st, long long n, const unsigned char* cm, const Real* __restrict__ md, const Real* __restrict__ r,
+         Real* __restrict__ delta, Real* __restrict__ p, int precond, const double* rz_part, int rz_n, int k, int last) {
+  MO_PDL_ENTRY();
+  if (st->stop_code < 2 * k + 1) return;  // stopped before alpha_k existed
+  const double tot = mo_sum_partials(rz_part, rz_n);
+  const bool writer = blockIdx.x == 0 && threadIdx.x == 0;
+  Real beta = Real(0);
+  const bool go = mo_beta_from<Real>(st, tot, k, writer, &beta) && !last;  // (writer: bookkeeping of r'z)
+  const Real alpha = Real(st->alpha);  // alpha_k, recorded by the update of iteration k
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long n4 = n >> 2;
+  long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (go) {  // two 4-wide groups per step, loads first (see k_pcg_update_r)
+    for (; v + stride < n4; v += 2 * stride) {
+      const long long i = v << 2, j = (v + stride) << 2;
+      V4<Real> D0 = ld4(delta + i), D1 = ld4(delta + j), P0 = ld4(p + i), P1 = ld4(p + j);
+      const V4<Real> R0 = ld4(r + i), R1 = ld4(r + j), M0 = ld4(md + i), M1 = ld4(md + j);
+      const uchar4 e0 = ldm4(cm, i), e1 = ldm4(cm, j);
+      const unsigned char x0[4] = {e0.x, e0.y, e0.z, e0.w}, x1[4] = {e1.x, e1.y, e1.z, e1.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        D0.a[q] = (x0[q] & 1) ? Real(0) : D0.a[q] + alpha * P0.a[q];
+        P0.a[q] = pcg_p1(beta, x0[q], R0.a[q], M0.a[q], P0.a[q], precond);
+        D1.a[q] = (x1[q] & 1) ? Real(0) : D1.a[q] + alpha * P1.a[q];
+        P1.a[q] = pcg_p1(beta, x1[q], R1.a[q], M1.a[q], P1.a[q], precond);
+      }
+      st4(delta + i, D0);
+      st4(delta + j, D1);
+      st4(p + i, P0);
+      st4(p + j, P1);
+    }
+  }
+  for (; v < n4; v += stride) {
+    const long long i = v << 2;
+    V4<Real> D = ld4(delta + i), Pp = ld4(p + i);
+    const uchar4 e = ldm4(cm, i);
+    const unsigned char ex[4] = {e.x, e.y, e.z, e.w};
+    if (go) {
+      const V4<Real> Rr = ld4(r + i), M = ld4(md + i);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        D.a[q] = (ex[q] & 1) ? Real(0) : D.a[q] + alpha * Pp.a[q];
+        Pp.a[q] = pcg_p1(beta, ex[q], Rr.a[q], M.a[q], Pp.a[q], precond);
+      }
+      st4(p + i, Pp);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) D.a[q] = (ex[q] & 1) ? Real(0) : D.a[q] + alpha * Pp.a[q];
+    }
+    st4(delta + i, D);
+  }
+  for (long long i = (n4 << 2) + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const unsigned char m = cm ? cm[i] : (unsigned char)0;
+    const Real pi = p[i];
+    delta[i] = (m & 1) ? Real(0) : delta[i] + alpha * pi;
+    if (go) p[i] = pcg_p1(beta, m, r[i], md[i], pi, precond);
+  }
+}
+
 // Last PCG iteration under consumer-side reductions: no direction update,
 // only the r'z bookkeeping (iteration count, stop / non-finite flags).
 template <class Real>
@@ -307,8 +434,35 @@ k_xtrial(mo_state* st, long long n, const unsigned char* cm, Real* __restrict__ 
   MO_PDL_ENTRY();
   if (in_place && (st->nonfinite || !mo_finite(st->sums[cost_slot]))) return;
   bool nz = false;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long n4 = n >> 2;  // 4-wide body (16-byte accesses), scalar tail
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n4; v += stride) {
+    const long long i = v << 2;
+    const V4<Real> D = ld4(delta + i);
+    V4<Real> X = ld4(x + i);
+    const uchar4 e = ldm4(cm, i);
+    const unsigned char ex[4] = {e.x, e.y, e.z, e.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (ex[q] & 2) continue;  // halo column: refreshed by the exchange
+      if (D.a[q] != Real(0)) nz = true;
+      if (!(ex[q] & 1)) X.a[q] = X.a[q] + D.a[q];
+    }
+    if (in_place) {
+      if (cm && (e.x | e.y | e.z | e.w) & 2) {  // (strips) never write a neighbour's halo column
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (!(ex[q] & 2)) x[i + q] = X.a[q];
+      } else {
+        st4(x + i, X);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (!(ex[q] & 2)) xt[i + q] = X.a[q];
+    }
+  }
+  for (long long i = (n4 << 2) + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
     if (halo_at(cm, i)) continue;  // refreshed by the halo exchange
     const Real d = delta[i];
     if (d != Real(0)) nz = true;

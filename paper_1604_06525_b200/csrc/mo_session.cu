@@ -2497,6 +2497,8 @@ class Session final : public SessionBase {
     // beta itself, removing the atomic + last-block tail from the producers.
     static const bool nocons = std::getenv("MO_B200_NO_CONSUMER") != nullptr;
     const bool cons = !nocons && !sh_.on && !mat_ && (P_.graph_sets.empty() || vertex_apply_one_pass());
+    static const bool nodefer = std::getenv("MO_B200_NO_DEFER") != nullptr;
+    const bool defer = cons && !nodefer;
     for (int k = 0; k < cfg_.linear_iters; ++k) {
       prof_begin(0);
       consumer_ = cons;
@@ -2504,6 +2506,18 @@ class Session final : public SessionBase {
       consumer_ = false;
       prof_end(0);
       prof_begin(1);
+      if (defer) {  // deferred-delta pair (k_pcg_update_r / k_pcg_dp, mo_kernels.cuh)
+        mo_red ru = red(0, vgu, MO_FIN_PARTIALS, 0);
+        ru.partials = partials2_;
+        kl(k_pcg_update_r<Real>, dim3(vgu), dim3(MO_THREADS), ru, n, colmask_, mdv, r_, ap_, pre,
+           (const double*)partials_, apply_parts_, k);
+        const int last = k + 1 < cfg_.linear_iters ? 0 : 1;  // the last direction is never applied
+        kl(k_pcg_dp<Real>, dim3(vgu), dim3(MO_THREADS), state_, n, colmask_, mdv, r_, delta_, p_, pre,
+           (const double*)partials2_, vgu, k, last);
+        launches_ += 2;
+        prof_end(1);
+        continue;
+      }
       // (A cooperative single-kernel update + direction with a grid barrier
       // was measured slower on B200 than this pair at every config size.)
       mo_red ru = red(0, vgu, cons ? MO_FIN_PARTIALS : MO_FIN_PCG_BETA, 0);
