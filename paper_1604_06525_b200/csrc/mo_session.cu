@@ -2497,8 +2497,15 @@ class Session final : public SessionBase {
     // beta itself, removing the atomic + last-block tail from the producers.
     static const bool nocons = std::getenv("MO_B200_NO_CONSUMER") != nullptr;
     const bool cons = !nocons && !sh_.on && !mat_ && (P_.graph_sets.empty() || vertex_apply_one_pass());
-    static const bool nodefer = std::getenv("MO_B200_NO_DEFER") != nullptr;
-    const bool defer = cons && !nodefer;
+    // Deferred delta (k_pcg_update_r / k_pcg_dp) moves 42 instead of 46 bytes
+    // per column and wins where the pair streams from HBM (8192^2: 1.40 vs
+    // 1.46 ms per iteration); on L2-sized grids the extra stream in the
+    // direction kernel costs more than it saves (ARAP 1024^2: 40 vs 34 us),
+    // so it is used on the large-grid configuration of the vector kernels.
+    // MO_B200_NO_DEFER=1 / MO_B200_DEFER=1 force either.
+    const bool nodefer = std::getenv("MO_B200_NO_DEFER") != nullptr;
+    const bool fdefer = std::getenv("MO_B200_DEFER") != nullptr;
+    const bool defer = cons && !nodefer && (fdefer || vper == 16);
     for (int k = 0; k < cfg_.linear_iters; ++k) {
       prof_begin(0);
       consumer_ = cons;

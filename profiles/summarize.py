@@ -28,15 +28,17 @@ UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "u
         "ns": 1e-9, "us": 1e-6, "ms": 1e-3}
 
 
-def launches(path):
+def launches(path, last=0):
     rows = list(csv.reader(open(path)))
     hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     hdr = rows[hi]
     ki, mi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    ni = hdr.index("Metric Name") if "Metric Name" in hdr else None
     agg = collections.defaultdict(list)
-    for r in rows[hi + 1:]:
-        if len(r) <= mi:
-            continue
+    body = [r for r in rows[hi + 1:] if len(r) > mi and (ni is None or r[ni] == "gpu__time_duration.sum")]
+    if last:  # only the final `last` launches (one timed solve after the tuning launches)
+        body = body[-last:]
+    for r in body:
         v = float(r[mi].replace(",", "")) * UNIT.get(r[ui], 1.0) * 1e6  # -> us
         agg[r[ki].split("(")[0].replace("void ", "")].append(v)
     tot = sum(sum(v) for v in agg.values())
@@ -70,9 +72,10 @@ def main():
     ap.add_argument("--report", action="append", default=[])
     ap.add_argument("--config", action="append", default=[])
     ap.add_argument("--note", default="")
+    ap.add_argument("--last", type=int, default=0, help="summarise only the final N launches")
     a = ap.parse_args()
     if a.launches:
-        rows = launches(a.launches)
+        rows = launches(a.launches, a.last)
         with open(os.path.join(HERE, f"{a.round}_launches.md"), "w") as f:
             f.write(f"# {a.round}: ncu launch list ({os.path.basename(a.launches)})\n\n")
             f.write("`ncu --metrics gpu__time_duration.sum --clock-control none` over the bench command; "
@@ -86,7 +89,7 @@ def main():
     summ = json.load(open(summ_path)) if os.path.exists(summ_path) else {}
     for rep, cfg in zip(a.report, a.config):
         for d in report_metrics(rep):
-            key = "jtj" if "jtj" in d["kernel"] else d["kernel"]
+            key = "jtj" if "jtj" in d["kernel"] else ("bm" if "_bm" in d["kernel"] else d["kernel"])
             rb = d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)
             d["dram_bytes"] = rb
             d["round"] = a.round

@@ -15,5 +15,7 @@ cfg = SolveConfig(method=Method.kLevenbergMarquardt if prob.method == "lm" else 
 s = Solver(load_plan(prob.name, cfg, prob.dims), prob.data(np.float32))
 s.solve()
 print("MARK", flush=True)
+l0 = s.kernel_launches()
 r = s.solve()
+print("LAUNCHES", s.kernel_launches() - l0)
 print(name, n, "final", r.final_cost, "apply", s.apply_kernel(0), "normal", s.normal_kernel(0))

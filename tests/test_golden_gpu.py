@@ -223,3 +223,26 @@ def test_normal_variant_parity(name, variant, monkeypatch):
     for row, rc in zip(r.trace, g.ref("trace_cost")):
         assert rel_close(row.cost, rc, t["traj"]), (k, row.cost, rc)
     assert rel_close(r.final_cost, float(g.ref("final_cost")[0]), t["traj"]), (k, r.final_cost)
+
+
+@pytest.mark.parametrize("defer", ["0", "1"], ids=["eager", "deferred"])
+@pytest.mark.parametrize("name", [n for n in NAMES if n.startswith(("cfg_", "gn_", "lm_", "nan_", "empty", "graph", "chain"))])
+def test_golden_solve_pcg_schemes(name, defer, monkeypatch):
+    """Both PCG vector schemes of the unsharded grid path on every golden
+    solve: the eager update / direction pair and the deferred-delta pair
+    (k_pcg_update_r / k_pcg_dp, used on large grids) must reproduce the
+    reference's trajectory, stop reasons and PCG counts, including the
+    zero-iteration and indefinite / non-finite stops."""
+    monkeypatch.setenv("MO_B200_DEFER" if defer == "1" else "MO_B200_NO_DEFER", "1")
+    g = Golden(name)
+    if g.ref("final_cost") is None or g.ref("error") is not None:
+        pytest.skip("no solve in this golden")
+    t = tol(g.prec)
+    s = Solver(g.plan(False), g.data())
+    r = s.solve()
+    assert int(r.reason) == int(g.ref("reason")[0])
+    assert [x.pcg_iters for x in r.trace] == list(g.ref("trace_pcg"))
+    assert [int(x.accepted) for x in r.trace] == list(g.ref("trace_accepted"))
+    for row, rc in zip(r.trace, g.ref("trace_cost")):
+        assert rel_close(row.cost, rc, t["traj"]), (row.cost, rc)
+    assert rel_close(r.final_cost, float(g.ref("final_cost")[0]), t["traj"]), r.final_cost
