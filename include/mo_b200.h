@@ -228,6 +228,22 @@ typedef void (*mo_apply_fn)(const void* x, void* y, void* stream, void* user);
 int mo_pcg(int device, int precision, int64_t n, mo_apply_fn apply, void* user, const void* b, const void* m,
            void* delta, const mo_pcg_options* opt, const uint8_t* excluded, mo_pcg_outcome* out);
 
+/* ---- on-disk formats (io.hpp:97-192) ------------------------------------ */
+/* .optd dense arrays: "OPTD", u32 version 1, u8 dtype (0 = f32, 1 = f64),
+ * u8 ndims, u16 channels, ndims x u64 extents, channel-interleaved row-major
+ * IEEE payload; all little-endian.  Errors as read_optd / write_optd:
+ * MO_ERR_FORMAT (bad magic / version / dtype, implausible extents, payload
+ * longer than promised), MO_ERR_TRUNCATED (file ends early). */
+int mo_optd_stat(const char* path, int* dtype, int* channels, int* ndims, int64_t* extents, int max_dims); /* io.hpp:122 */
+int mo_optd_read(const char* path, void* values, int64_t count, int dtype);                                /* io.hpp:122 */
+int mo_optd_write(const char* path, int dtype, int channels, int ndims, const int64_t* extents,
+                  const void* values);                                                                      /* io.hpp:97 */
+/* .optg hyperedge lists: "OPTG", u32 version 1, u16 arity, u64 edges,
+ * edges x arity u64 vertex ids (read_optg / write_optg, io.hpp:158-192). */
+int mo_optg_stat(const char* path, int* arity, int64_t* edges);                /* io.hpp:171 */
+int mo_optg_read(const char* path, uint64_t* verts, int64_t n);                /* io.hpp:171 */
+int mo_optg_write(const char* path, int arity, int64_t edges, const uint64_t* verts); /* io.hpp:158 */
+
 /* ---- measurement hooks (bench.py) -------------------------------------- */
 /* When enabled, CUDA events bracket every J^T J p apply and PCG vector update
  * launched by mo_solve (on the session stream, also inside CUDA graphs). */

@@ -125,6 +125,13 @@ SIGNATURES = {
     "mo_profile_read": (c_int, [c_void_p, c_int, ctypes.POINTER(c_double), ctypes.POINTER(c_int64)]),
     "mo_profile_reset": (c_int, [c_void_p]),
     "mo_bench_kernel": (c_int, [c_void_p, c_int, c_int, ctypes.POINTER(ctypes.c_double)]),
+    "mo_optd_stat": (c_int, [c_char_p, ctypes.POINTER(c_int), ctypes.POINTER(c_int), ctypes.POINTER(c_int),
+                             ctypes.POINTER(c_int64), c_int]),
+    "mo_optd_read": (c_int, [c_char_p, c_void_p, c_int64, c_int]),
+    "mo_optd_write": (c_int, [c_char_p, c_int, c_int, c_int, ctypes.POINTER(c_int64), c_void_p]),
+    "mo_optg_stat": (c_int, [c_char_p, ctypes.POINTER(c_int), ctypes.POINTER(c_int64)]),
+    "mo_optg_read": (c_int, [c_char_p, ctypes.POINTER(ctypes.c_uint64), c_int64]),
+    "mo_optg_write": (c_int, [c_char_p, c_int, c_int64, ctypes.POINTER(ctypes.c_uint64)]),
     "mo_session_stream": (c_int, [c_void_p, ctypes.POINTER(c_void_p)]),
     "mo_kernel_launches": (c_int, [c_void_p, ctypes.POINTER(c_int64)]),
     "mo_apply_kernel": (c_int, [c_void_p, c_int, ctypes.c_char_p, ctypes.c_size_t]),

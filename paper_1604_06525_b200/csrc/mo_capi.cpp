@@ -112,6 +112,11 @@ void trampoline(int iter, void* user) {
 
 }  // namespace
 
+namespace mo {
+// (mo_io.cpp records its errors here too: one mo_last_error() per thread)
+void set_last_error(const std::string& m) { g_err = m; }
+}  // namespace mo
+
 extern "C" {
 
 const char* mo_last_error(void) { return g_err.c_str(); }
