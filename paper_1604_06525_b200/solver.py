@@ -191,13 +191,6 @@ class CompiledPlan:
             self._h = None
 
 
-def plan(text: str, cfg: Optional[SolveConfig] = None, dims: Optional[dict] = None,
-         exact: bool = False) -> CompiledPlan:
-    """plan(spec, cfg) over an exported moplan text (plan.hpp:189).  exact=True
-    compiles the per-element kernels without FMA contraction (bitwise mode)."""
-    return CompiledPlan(text, cfg, dims, exact)
-
-
 def load_plan(name_or_path: str, cfg: Optional[SolveConfig] = None, dims: Optional[dict] = None,
               exact: bool = False) -> CompiledPlan:
     path = name_or_path
@@ -205,6 +198,25 @@ def load_plan(name_or_path: str, cfg: Optional[SolveConfig] = None, dims: Option
         path = os.path.join(PLAN_DIR, name_or_path + ".moplan")
     with open(path) as f:
         return CompiledPlan(f.read(), cfg, dims, exact)
+
+
+def plan(source: str, cfg: Optional[SolveConfig] = None, dims: Optional[dict] = None, materialize: int = 0,
+         exact: bool = False) -> CompiledPlan:
+    """plan(spec, cfg) (plan.hpp:189).  `source` is either an exported
+    "moplan 1" text, or energy text / a path to a .opt file, which this
+    package's own front end (frontend.py: compile_source + transform +
+    schedule) turns into a plan without the reference compiler.
+    `materialize` (front end only): 0 matrix-free, 1 Materialize::kJ,
+    2 Materialize::kJtJ.  exact=True compiles the per-element kernels without
+    FMA contraction (bitwise mode)."""
+    if source.lstrip().startswith("moplan"):
+        return CompiledPlan(source, cfg, dims, exact)
+    from . import frontend
+    if "\n" not in source and os.path.exists(source):
+        with open(source) as f:
+            source = f.read()
+    text = frontend.plan_source(source, cfg, dims=dims, materialize=materialize)
+    return CompiledPlan(text, cfg, None, exact)
 
 
 def _as(a, dtype):

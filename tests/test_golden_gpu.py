@@ -7,6 +7,9 @@ floor tied to ||ref||_inf for stencils with cancellation); cost trajectories
 within 1e-4 relative in fp32 (1e-8 in fp64); identical stop reasons, trace
 lengths, accept/reject sequences and PCG iteration counts.
 """
+import os
+import sys
+
 import numpy as np
 import pytest
 
@@ -246,3 +249,38 @@ def test_golden_solve_pcg_schemes(name, defer, monkeypatch):
     for row, rc in zip(r.trace, g.ref("trace_cost")):
         assert rel_close(row.cost, rc, t["traj"]), (row.cost, rc)
     assert rel_close(r.final_cost, float(g.ref("final_cost")[0]), t["traj"]), r.final_cost
+
+
+def _frontend_source(name):
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import test_frontend
+    return test_frontend._source(name)
+
+
+FRONTEND_CASES = ["cfg_poisson_f64", "cfg_poisson_f32", "cfg_arap_warp_f64", "cfg_arap_warp_f32", "cfg_sfs_f64",
+                  "cfg_sfs_f32", "cfg_arap_mesh_f64", "cfg_arap_mesh_f32", "cfg_poisson_mat_f64", "cfg_sfs_mat_f32",
+                  "chain", "dense", "ops", "tri_graph", "cached", "freeze", "lm_quadratic", "exclude", "volume"]
+
+
+@pytest.mark.parametrize("name", [n for n in FRONTEND_CASES if n in NAMES])
+def test_golden_case_frontend_plan(name, monkeypatch):
+    """The device solver on plans made by this package's own front end
+    (frontend.py) from the energy text, instead of the reference compiler's
+    export: every golden command (cost, residuals, b, m, 2 J^T J v, J, H,
+    solve) must still match the reference within the fast-mode tolerances."""
+    from paper_1604_06525_b200 import frontend
+    from paper_1604_06525_b200.solver import CompiledPlan
+    src = _frontend_source(name)
+    if src is None:
+        pytest.skip("no energy source for this golden")
+    g = Golden(name)
+    text = frontend.plan_source(src[0], g.cfg, dims=src[1], materialize=src[2])
+    monkeypatch.setattr(g, "plan", lambda exact=False: CompiledPlan(text, g.cfg, None, exact))
+    err = g.ref("error")
+    if err is None:
+        run_golden(g, False)
+        return
+    code = bytes(err).decode().split(":")[0]
+    with pytest.raises(MoError) as ei:
+        run_golden(g, False)
+    assert ei.value.code == code
