@@ -4,6 +4,7 @@
 // hash of the source and options.
 #include "mo_jit.hpp"
 
+#include <algorithm>
 #include <cuda_runtime.h>
 #include <nvrtc.h>
 
@@ -127,6 +128,25 @@ void Module::load(const std::vector<char>& cubin) {
   cudaError_t e = cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
   check(e == cudaSuccess, Err::kCuda, std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e));
   lib_ = lib;
+  // Large generated programs (f64 division / sqrt subroutine calls) can need
+  // a per-thread stack frame beyond the default 1 KiB limit: raise the
+  // device limit here, at load time, never inside a stream capture.
+  unsigned n = 0;
+  if (cudaLibraryGetKernelCount(&n, lib) == cudaSuccess && n) {
+    std::vector<cudaKernel_t> ks(n);
+    if (cudaLibraryEnumerateKernels(ks.data(), n, lib) == cudaSuccess) {
+      size_t need = 0;
+      for (cudaKernel_t k : ks) {
+        cudaFuncAttributes a{};
+        if (cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(k)) == cudaSuccess)
+          need = std::max(need, size_t(a.localSizeBytes));
+      }
+      size_t cur = 0;
+      cudaDeviceGetLimit(&cur, cudaLimitStackSize);
+      if (need + 1024 > cur) cudaDeviceSetLimit(cudaLimitStackSize, (need + 1024 + 255) / 256 * 256);
+    }
+  }
+  cudaGetLastError();
 }
 
 const void* Module::kernel(const std::string& name) {

@@ -1180,8 +1180,8 @@ class _Sched:
         self.p.num_regs += 1
         return r
 
-    def emit(self, op, sub=0, a=0, b=0, c=0, fld=0, ch=0, acc=ORIGIN, imm=0.0, pn=1, pd=1):
-        dst = self.reg()
+    def emit(self, op, sub=0, a=0, b=0, c=0, fld=0, ch=0, acc=ORIGIN, imm=0.0, pn=1, pd=1, dst=None):
+        dst = self.reg() if dst is None else dst
         ins = self.p.instrs
         if not self.p.blocks or self.p.blocks[-1][0] != self.cur:
             self.p.blocks.append([self.cur, len(ins), len(ins)])
@@ -1279,16 +1279,23 @@ class _Sched:
         return [(conds, i)]
 
     def run(self, outputs):
+        """Each output accumulates its guarded terms in order into one
+        register (acc = acc + v inside the term's block; registers start at
+        0), which is exactly run_program's Real(0) + sum of guarded roots
+        (program.hpp:159-166) while keeping one value live per output."""
         for e in outputs:
-            roots = []
-            for conds, v in self.terms(e):
-                if self.dag.is_const(v, 0.0):
-                    continue
+            terms = [(c, v) for c, v in self.terms(e) if not self.dag.is_const(v, 0.0)]
+            if len(terms) == 1 and not terms[0][0]:
+                self.cur = 0
+                self.p.outputs.append([(0, self.value(terms[0][1]))])
+                continue
+            acc = self.reg() if terms else None
+            for conds, v in terms:
                 g = self.guard(set(conds))
                 self.cur = g
-                roots.append((g, self.value(v)))
+                self.emit("add", a=acc, b=self.value(v), dst=acc)
                 self.cur = 0
-            self.p.outputs.append(roots)
+            self.p.outputs.append([(0, acc)] if terms else [])
         self.p.blocks = [tuple(b) for b in self.p.blocks]
         return self.p
 
