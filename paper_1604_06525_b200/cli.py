@@ -144,7 +144,8 @@ def _plan(spec, cfg, materialize):
     return CompiledPlan(frontend.plan_text(spec, cfg, materialize=materialize), cfg)
 
 
-def cmd_solve(a, out=sys.stdout):
+def cmd_solve(a, out=None):
+    out = out or sys.stdout
     spec, _, data = load_problem(a)
     cfg = _config(a)
     mat = {"none": 0, "j": 1, "jtj": 2}[a.materialize]
@@ -163,10 +164,11 @@ def cmd_solve(a, out=sys.stdout):
             write_optd(os.path.join(a.out, u.name + ".optd"), data.x[col:col + n], channels=u.channels,
                        extents=spec.shape(u.dom))
             col += n
-    return SOLVER_FAILURE if r.reason == StopReason.kNonFinite or not np.isfinite(r.final_cost) else 0
+    return SOLVER_FAILURE if r.reason == StopReason.kNonFiniteCost or not np.isfinite(r.final_cost) else 0
 
 
-def cmd_compare(a, out=sys.stdout):
+def cmd_compare(a, out=None):
+    out = out or sys.stdout
     spec, _, data0 = load_problem(a)
     cfg = _config(a)
     rows, x_free = [], None
