@@ -264,7 +264,8 @@ struct Gen {
     }
     if (sm_mode)
       os << "template <bool I> __device__ __forceinline__ void " << name
-         << "(const mo_kparams& P, int p0, int p1, int p2, const int* ri, int lx, Real* out) {\n"
+         << "(const mo_kparams& P, int p0, int p1, int p2, const int* ri, int lx, Real* out"
+         << (ls ? ", unsigned* bits_out" : "") << ") {\n"
          << "  (void)P; (void)p0; (void)p1; (void)p2; (void)ri; (void)lx; const int eb = 0; (void)eb;\n";
     else
       os << "template <bool I> __device__ __forceinline__ void " << name
@@ -806,6 +807,8 @@ struct Gen {
       gather_jtj8(g, gi, *S, lg, lane_slot, merged_off(merged), H, 1);
       lane_cache(g, gi, *S, H);
       if (lc_info.ok) gather_jtj8(g, gi, *S, lg, lane_slot, merged_off(merged), H, 2);
+      // build_normal that also writes the lane cache (mo_gather_bm8c_<gi>)
+      if (lc_info.ok) gather_jtj8(g, gi, *S, lg, lane_slot, merged_off(merged), H, 3);
     }
     return tp;
   }
@@ -1430,7 +1433,7 @@ struct Gen {
 
   void gather_jtj8(const GatherSet& g, int gi, const GridSet& S, const std::vector<LaneG>& lanes,
                    const std::vector<int>& lane_slot, const std::vector<MLane>& merged, int H, int mode) {
-    const bool bm = mode == 1, cached = mode == 2;
+    const bool bm = mode == 1 || mode == 3, cached = mode == 2, lcw = mode == 3;
     if (f64_disabled_tma()) return;
     if (bm && S.evalf.outputs.size() != S.jtemplates.size()) return;
     auto envi = [](const char* n, int d) { const char* v = std::getenv(n); return v ? std::atoi(v) : d; };
@@ -1501,9 +1504,9 @@ struct Gen {
     off += 16LL * NBUF;
     st_rx = RX;
     st_win = WIN;
-    if (cached) {
+    if (cached || lcw) {
       cur_split = &lc_split;
-      split_mode = 2;
+      split_mode = cached ? 2 : 1;
     }
     const std::string pe = program(S.evalj, false, &g.dom, true);
     split_mode = 0;
@@ -1512,7 +1515,7 @@ struct Gen {
     const std::string pf = bm ? program(S.evalf, false, &g.dom, true) : std::string();
     const int NO = int(S.evalj.outputs.size());
     const int NT = int(S.jtemplates.size());
-    const std::string LN = (bm ? "mo_lanesbm8_" : cached ? "mo_lanes9_" : "mo_lanes8_") + sfx;
+    const std::string LN = (lcw ? "mo_lanesbm8c_" : bm ? "mo_lanesbm8_" : cached ? "mo_lanes9_" : "mo_lanes8_") + sfx;
     os << "template <bool I> __device__ __forceinline__ void " << LN
        << "(const mo_kparams& P, int p0, int p1, const int* ri, int lx, Real* c" << (bm ? ", Real* cm" : "")
        << (cached ? ", const Real* cv, unsigned bits" : "") << ") {\n"
@@ -1520,6 +1523,19 @@ struct Gen {
        << "  Real d[" << NO << "];\n";
     if (cached) {
       os << "  " << pe << "(P, bits, cv, d);\n";
+    } else if (lcw) {
+      // evalj once, also the lane cache of the apply (its varying lanes and
+      // guard outcomes) for this phase-1 element of the extended domain;
+      // elements several items evaluate are written with identical values
+      os << "  unsigned bits_ = 0u;\n  " << pe << "<I>(P, p0, p1, 0, ri, lx, d, &bits_);\n"
+         << "  if ((P.flags & MO_F_LCACHE) && p1 < " << sh[1] + lc_info.H << ") {\n"
+         << "    Real* const CC = (Real*)P.in2 + (long long)(p0 + " << lc_info.H << ") * " << lc_info.PW << " + (p1 + "
+         << lc_info.HX << ");\n"
+         << "    constexpr long long LSTR = (long long)" << lc_info.PW << " * " << lc_info.rows << ";\n";
+      for (int j = 0; j < lc_info.nv; ++j)
+        os << "    CC[" << j << " * LSTR] = d[" << lc_split.varying[size_t(j)] << "];\n";
+      os << "    CC[" << lc_info.nv << " * LSTR] = "
+         << (f64 ? "__longlong_as_double((long long)bits_)" : "__uint_as_float(bits_)") << ";\n  }\n";
     } else {
       os << "  " << pe << "<I>(P, p0, p1, 0, ri, lx, d);\n";
     }
@@ -1556,7 +1572,7 @@ struct Gen {
 
     const int K = int(g.chans.size());
     const int NA = 2 * H + 1;
-    const std::string kn = (bm ? "mo_gather_bm8_" : cached ? "mo_gather_jtj9_" : "mo_gather_jtj8_") + sfx;
+    const std::string kn = (lcw ? "mo_gather_bm8c_" : bm ? "mo_gather_bm8_" : cached ? "mo_gather_jtj9_" : "mo_gather_jtj8_") + sfx;
     const int minb = envi(bm ? "MO_B200_BM8_MINB" : "MO_B200_JTJ8_MINB", 0);
     std::ostringstream is;  // TMA issue of input block j (inline: tensor maps in param space)
     is << "{ const int s_ = gb & (NBUF - 1);\n"
@@ -1806,10 +1822,10 @@ struct Gen {
       ti.cache_pw = lc_info.PW;
       ti.cache_rows = lc_info.rows;
     }
-    (bm ? tmabm8_info : cached ? tma9_info : tma8_info) = ti;
+    (lcw ? tmabm8c_info : bm ? tmabm8_info : cached ? tma9_info : tma8_info) = ti;
     staged.clear();
   }
-  ModuleInfo::Tma tma8_info, tmabm8_info, tma9_info;
+  ModuleInfo::Tma tma8_info, tmabm8_info, tma9_info, tmabm8c_info;
 
   // TMA-staged gather program (2-D domains): the reference's own J^T J p
   // gather program (transform.hpp:238-260, run_program semantics) per output
@@ -2353,6 +2369,7 @@ struct Gen {
         info.jtj8.push_back({});
         info.bm8.push_back({});
         info.jtj9.push_back({});
+        info.bm8c.push_back({});
         continue;
       }
       gather_jtj(g, program(g.jtj, false, &g.dom), "mo_gather_jtj_" + std::to_string(i));
@@ -2366,6 +2383,7 @@ struct Gen {
       tma8_info = ModuleInfo::Tma{};
       tmabm8_info = ModuleInfo::Tma{};
       tma9_info = ModuleInfo::Tma{};
+      tmabm8c_info = ModuleInfo::Tma{};
       TwoPhase tp = gather_jtj2(g, int(i));
       info.jtj2.push_back({tp.ok, tp.smem, tp.nlanes, tp.H});
       info.jtj3.push_back(stream_info);
@@ -2377,6 +2395,7 @@ struct Gen {
       info.jtj8.push_back(tma8_info);
       info.bm8.push_back(tmabm8_info);
       info.jtj9.push_back(tma9_info);
+      info.bm8c.push_back(tmabm8c_info);
     }
     for (size_t i = 0; i < P.graph_sets.size(); ++i) {
       const GraphSet& g = P.graph_sets[i];

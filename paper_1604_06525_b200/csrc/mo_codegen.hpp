@@ -46,6 +46,7 @@ struct ModuleInfo {
   std::vector<Tma> jtj8;       // per gather set: warp-specialised streaming apply (mo_gather_jtj8_<i>)
   std::vector<Tma> bm8;        // per gather set: warp-specialised streaming build_normal (mo_gather_bm8_<i>)
   std::vector<Tma> jtj9;       // per gather set: lane-cache streaming apply (mo_gather_jtj9_<i>, mo_lanecache_<i>)
+  std::vector<Tma> bm8c;       // per gather set: mo_gather_bm8 that also writes jtj9's lane cache
   std::vector<bool> vertex_kernels;  // per graph set: mo_graph_v{jtj,bm}_<g>_<dom> exist
   bool fused_vertex_apply = false;   // mo_graph_vjtjf_0: grid gather + graph gather + finish in one pass
 };

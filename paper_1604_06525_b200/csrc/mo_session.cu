@@ -678,6 +678,7 @@ class Session final : public SessionBase {
     tune_apply();
     if (!P_.graph_sets.empty() && vertex_path(0)) return "mo_graph_vbm_0";
     const int bc = bm_choice_.size() > size_t(i) ? bm_choice_[size_t(i)] : 0;
+    if (bc == 2 && bm8c_fuses(size_t(i))) return "mo_gather_bm8c_" + std::to_string(i);
     return (bc == 2 ? "mo_gather_bm8_" : bc == 1 ? "mo_gather_bm4_" : "mo_gather_bm_") +
            std::to_string(i);
   }
@@ -1238,9 +1239,11 @@ class Session final : public SessionBase {
   static constexpr int kVariants = 9;
   static constexpr int kBm4 = 100;  // tma_info id of the TMA build_normal kernel
   static constexpr int kBm8 = 101;  // tma_info id of the warp-specialised build_normal kernel
+  static constexpr int kBm8c = 102;  // ... that also writes the lane cache of variant 8
   const ModuleInfo::Tma* tma_info(size_t i, int v) const {
     if (v == kBm4 && i < minfo_.bm4.size()) return &minfo_.bm4[i];
     if (v == kBm8 && i < minfo_.bm8.size()) return &minfo_.bm8[i];
+    if (v == kBm8c && i < minfo_.bm8c.size()) return &minfo_.bm8c[i];
     if (v == 7 && i < minfo_.jtj8.size()) return &minfo_.jtj8[i];
     if (v == 8 && i < minfo_.jtj9.size()) return &minfo_.jtj9[i];
     if (v == 3 && i < minfo_.jtj4.size()) return &minfo_.jtj4[i];
@@ -1766,10 +1769,17 @@ class Session final : public SessionBase {
     return tma_capable(i, minfo_.bm8[i]);
   }
   bool bm8_ok(size_t i) const { return i < bm_choice_.size() && bm_choice_[i] == 2 && bm8_avail(i); }
-  // Grid and rows per work item of mo_gather_bm8 (the apply's row model).
+  // build_normal writes variant 8's lane cache itself (mo_gather_bm8c): no
+  // separate mo_lanecache pass per linearisation.
+  bool bm8c_fuses(size_t i) const {
+    return bm8_ok(i) && variant(i) == 8 && i < minfo_.bm8c.size() && minfo_.bm8c[i].ok &&
+           tma_capable(i, minfo_.bm8c[i]) && !std::getenv("MO_B200_NO_BM8C");
+  }
+  // Grid and rows per work item of mo_gather_bm8 / bm8c (the apply's row model).
   int bm8_grid(size_t i, int* chunk) {
-    const ModuleInfo::Tma& ti = minfo_.bm8[i];
-    const void* f = mod_.kernel("mo_gather_bm8_" + std::to_string(i));
+    const bool fz = bm8c_fuses(i);
+    const ModuleInfo::Tma& ti = fz ? minfo_.bm8c[i] : minfo_.bm8[i];
+    const void* f = mod_.kernel((fz ? "mo_gather_bm8c_" : "mo_gather_bm8_") + std::to_string(i));
     const int occ = occupancy(f, ti.smem, ti.threads);
     const auto sh = P_.shape_of(P_.gather_sets[i].dom);
     const long long rows = sh_.on ? sh_.row1 - sh_.row0 : sh[0];
@@ -1812,7 +1822,7 @@ class Session final : public SessionBase {
   void normal_device(bool pcg_init = false) {
     if (tuned_ && !mat_)  // the linearisation point moved: refresh the lane cache
       for (size_t i = 0; i < P_.gather_sets.size(); ++i)
-        if (variant(i) == 8) lanecache_fill(i);
+        if (variant(i) == 8 && !bm8c_fuses(i)) lanecache_fill(i);
     prof_begin(2);
     const bool fused = P_.graph_sets.empty();
     const long long n = P_.num_cols;
@@ -1850,10 +1860,17 @@ class Session final : public SessionBase {
         kp.out4 = r_;
       }
       if (chunks[i] && bm8_ok(i)) {  // warp-specialised streaming build_normal
-        const void* f = mod_.kernel("mo_gather_bm8_" + std::to_string(i));
-        const mo_tmaps& T = tmaps_for(i, kBm8, kp);
+        const bool fz = tuned_ && bm8c_fuses(i);  // (+ the lane cache of the apply)
+        const ModuleInfo::Tma& ti = fz ? minfo_.bm8c[i] : minfo_.bm8[i];
+        if (fz) {
+          ensure_lanecache(i);
+          kp.in2 = lcache_[i];
+          kp.flags |= MO_F_LCACHE;
+        }
+        const void* f = mod_.kernel((fz ? "mo_gather_bm8c_" : "mo_gather_bm8_") + std::to_string(i));
+        const mo_tmaps& T = tmaps_for(i, fz ? kBm8c : kBm8, kp);
         void* args[] = {&kp, const_cast<mo_tmaps*>(&T)};
-        klc(f, dim3(grids[i]), dim3(unsigned(minfo_.bm8[i].threads), 1, 1), args, minfo_.bm8[i].smem);
+        klc(f, dim3(grids[i]), dim3(unsigned(ti.threads), 1, 1), args, ti.smem);
         ++launches_;
       } else if (chunks[i]) {  // TMA two-phase build_normal
         const void* f = mod_.kernel("mo_gather_bm4_" + std::to_string(i));
