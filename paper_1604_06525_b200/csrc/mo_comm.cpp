@@ -212,6 +212,7 @@ class NcclComm final : public Comm {
   void allgather(const double* send, double* recv, int n, cudaStream_t st) override {
     nccl::ok(nccl::api().AllGather(send, recv, size_t(n), nccl::ncclFloat64, comm_, st), "ncclAllGather");
   }
+  bool capturable() const override { return true; }
 
  private:
   nccl::ncclComm_t comm_ = nullptr;

@@ -33,6 +33,8 @@ class Comm {
   virtual void halo(const std::vector<HaloSeg>& segs, cudaStream_t st) = 0;
   // recv[r*n + i] = rank r's send[i], identical on every rank.
   virtual void allgather(const double* send, double* recv, int n, cudaStream_t st) = 0;
+  // Pure stream operations (no host synchronisation): CUDA-graph capturable.
+  virtual bool capturable() const { return false; }
 };
 
 class LocalWorld;  // shared state of the single-process fake

@@ -1486,6 +1486,29 @@ class Session final : public SessionBase {
     }
     launches_ = launched;
     cur_stage_ = stage;
+    // Strips: every rank runs rank 0's kernels (one rounding behaviour across
+    // the whole grid, run to run).  Collective: all ranks tune in their first
+    // solve; later sessions of the same key take the per-process cache.
+    if (sh_.on && comm_ && comm_->world > 1) {
+      const size_t G = P_.gather_sets.size();
+      check(G <= 32, Err::kInternal, "too many gather sets for the kernel-choice broadcast");
+      std::vector<double> mine(64, 0.0), all(size_t(comm_->world) * 64);
+      for (size_t i = 0; i < G; ++i) {
+        mine[i] = jtj_choice_[i];
+        mine[32 + i] = bm_choice_.size() > i ? bm_choice_[i] : 0;
+      }
+      double* chob = nullptr;
+      CK(cudaMalloc(&chob, 64 * sizeof(double)));
+      CK(cudaMemcpyAsync(chob, mine.data(), 64 * sizeof(double), cudaMemcpyHostToDevice, st_));
+      comm_->allgather(chob, rankbuf_, 64, st_);
+      CK(cudaMemcpyAsync(all.data(), rankbuf_, all.size() * sizeof(double), cudaMemcpyDeviceToHost, st_));
+      CK(cudaStreamSynchronize(st_));
+      cudaFree(chob);
+      for (size_t i = 0; i < G; ++i) {  // rank 0's entries come first
+        jtj_choice_[i] = int(all[i]);
+        if (bm_choice_.size() > i) bm_choice_[i] = int(all[32 + i]);
+      }
+    }
     std::lock_guard<std::mutex> lk(mu);
     cache[key] = jtj_choice_;
     bm_cache[key] = bm_choice_;
@@ -2570,7 +2593,10 @@ class Session final : public SessionBase {
   void run_stage(int key, F&& body) {
     static const bool nograph = std::getenv("MO_B200_NOGRAPH") != nullptr;
     cur_stage_ = key;
-    if (nograph || sh_.on) {  // strips: the local transport uses host barriers
+    // Strips over NCCL capture like the unsharded stages (halo send/recv and
+    // the all-gathers are stream operations); the single-process transport
+    // (LocalComm) orders its peer copies with host barriers and runs eagerly.
+    if (nograph || (sh_.on && !(comm_ && comm_->capturable()))) {
       stage_pos_[key] = 0;
       body();
       return;

@@ -135,3 +135,20 @@ def test_scrambled_mesh_strips_with_rcm(world):
         for a, b in zip(r.trace, ref.trace):
             assert abs(a.cost - b.cost) <= 1e-9 * abs(b.cost), (a.cost, b.cost)
     np.testing.assert_allclose(x, ref_data.x, rtol=1e-8, atol=1e-8)
+
+
+@pytest.mark.parametrize("name", ["poisson", "arap_warp"])
+def test_nccl_two_ranks(name):
+    """Two processes, one GPU each, strips over NCCL (halo send/recv and the
+    fixed-order all-gathers inside captured stage graphs) against the
+    unsharded solve; runs whenever two GPUs are visible."""
+    import subprocess
+    import sys
+
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs (this box has one)")
+    root = __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--standalone", "--nproc-per-node", "2",
+                        "scripts/nccl_strip_check.py", name], cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "NCCL_STRIPS_OK" in r.stdout, (r.stdout[-2000:], r.stderr[-2000:])
