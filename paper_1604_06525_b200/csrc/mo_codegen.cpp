@@ -1573,7 +1573,9 @@ struct Gen {
     const int K = int(g.chans.size());
     const int NA = 2 * H + 1;
     const std::string kn = (lcw ? "mo_gather_bm8c_" : bm ? "mo_gather_bm8_" : cached ? "mo_gather_jtj9_" : "mo_gather_jtj8_") + sfx;
-    const int minb = envi(bm ? "MO_B200_BM8_MINB" : "MO_B200_JTJ8_MINB", 0);
+    // resident blocks the register allocator must allow (0: unconstrained);
+    // the lane-cache apply gains from 6 (ARAP 8192^2: 966 vs 976 us)
+    const int minb = envi(bm ? "MO_B200_BM8_MINB" : cached ? "MO_B200_JTJ9_MINB" : "MO_B200_JTJ8_MINB", cached ? 6 : 0);
     std::ostringstream is;  // TMA issue of input block j (inline: tensor maps in param space)
     is << "{ const int s_ = gb & (NBUF - 1);\n"
        << "          if (gb >= NBUF) mo_mbar_wait(EMPTY + s_, ((gb >> LNB) - 1) & 1);\n"
@@ -1660,26 +1662,41 @@ struct Gen {
     const int NVC = cached ? lc_info.nv + 1 : 0;
     if (cached) {
       // Lane cache of this lane's phase-1 element, read straight from global
-      // memory (coalesced along the row, never a halo) one row ahead.
+      // memory (coalesced along the row, never a halo), PF rows ahead.
+      // PF rows in flight per lane (MO_B200_JTJ9_PF; measured on ARAP
+      // 8192^2: 1 row 976 us, 2 rows 1165 us, 3 rows 1127 us: the extra
+      // registers cost more resident warps than the deeper prefetch gains).
+      const int PF = std::max(1, std::min(4, envi("MO_B200_JTJ9_PF", 1)));
       os << "      constexpr long long LSTR = (long long)" << lc_info.PW << " * " << lc_info.rows << ";\n"
          << "      const Real* __restrict__ cp = (const Real*)P.in2 + (long long)y0 * " << lc_info.PW
          << " + min(q1, D1 + H - 1) + " << lc_info.HX << ";  // row q0 + H of phase-1 row k = 0\n"
-         << "      Real cn[" << NVC << "];\n"
+         << "      Real cn[" << PF << "][" << NVC << "];\n"
          << "      #pragma unroll\n"
-         << "      for (int j = 0; j < " << NVC << "; ++j) cn[j] = __ldg(cp + j * LSTR);\n";
-    }
-    os << "      for (int k = 0; k < nrows; ++k, e += D1) {\n";
-    if (cached)
-      os << "        Real cc[" << NVC << "];\n"
+         << "      for (int a = 0; a < " << PF << "; ++a) {\n"
          << "        #pragma unroll\n"
-         << "        for (int j = 0; j < " << NVC << "; ++j) cc[j] = cn[j];\n"
-         << "        if (k + 1 < nrows) {\n"
-         << "          cp += " << lc_info.PW << ";\n"
+         << "        for (int j = 0; j < " << NVC << "; ++j) cn[a][j] = a < nrows ? __ldg(cp + a * " << lc_info.PW
+         << " + j * LSTR) : (Real)0;\n"
+         << "      }\n"
+         << "      cp += " << PF << " * " << lc_info.PW << ";\n";
+      os << "      for (int k = 0; k < nrows; ++k, e += D1) {\n"
+         << "        Real cc[" << NVC << "];\n"
+         << "        #pragma unroll\n"
+         << "        for (int j = 0; j < " << NVC << "; ++j) cc[j] = cn[0][j];\n"
+         << "        #pragma unroll\n"
+         << "        for (int a = 0; a + 1 < " << PF << "; ++a) {\n"
          << "          #pragma unroll\n"
-         << "          for (int j = 0; j < " << NVC << "; ++j) cn[j] = __ldg(cp + j * LSTR);\n"
+         << "          for (int j = 0; j < " << NVC << "; ++j) cn[a][j] = cn[a + 1][j];\n"
+         << "        }\n"
+         << "        if (k + " << PF << " < nrows) {\n"
+         << "          #pragma unroll\n"
+         << "          for (int j = 0; j < " << NVC << "; ++j) cn[" << PF - 1 << "][j] = __ldg(cp + j * LSTR);\n"
+         << "          cp += " << lc_info.PW << ";\n"
          << "        }\n"
          << "        const unsigned cbits = " << (f64 ? "(unsigned)__double_as_longlong(cc[" : "__float_as_uint(cc[")
          << NVC - 1 << "]);\n";
+    } else {
+      os << "      for (int k = 0; k < nrows; ++k, e += D1) {\n";
+    }
     os << "        const int need = min(nblk - 1, (k + 2 * RX) >> LR);\n"
        << "        while (nwt <= need) {\n"
        << "          const int b = gb + nwt;\n"
