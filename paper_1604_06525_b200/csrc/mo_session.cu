@@ -27,6 +27,8 @@
 #include <limits>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "mo_codegen.hpp"
 #include "mo_jit.hpp"
 #include "mo_kernels.cuh"
@@ -34,6 +36,15 @@
 #include "mo_session.hpp"
 
 namespace mo {
+
+// NVTX range per reference routine (SURVEY.md §5 tracing): visible in nsys /
+// ncu timelines, no cost without an attached tool (NVTX v3 is header-only).
+struct Range {
+  explicit Range(const char* name) { nvtxRangePushA(name); }
+  ~Range() { nvtxRangePop(); }
+  Range(const Range&) = delete;
+  Range& operator=(const Range&) = delete;
+};
 
 const char* device_prelude();
 
@@ -260,6 +271,7 @@ class Session final : public SessionBase {
   // residual rows) + device half (computed arrays, masks), the latter
   // captured into the per-iteration CUDA graphs.
   void refresh() override {
+    Range nv("minopt::refresh");
     refresh_host();
     refresh_device();
     refreshed_ = true;
@@ -357,6 +369,7 @@ class Session final : public SessionBase {
 
   // ------------------------------------------------------------ routines
   double cost() override {
+    Range nv("minopt::cost");
     ensure_refreshed();
     cost_at(x_, SLOT_COST);
     sync_state();
@@ -388,6 +401,7 @@ class Session final : public SessionBase {
   }
 
   void build_normal() override {
+    Range nv("minopt::build_normal");
     ensure_refreshed();
     cur_stage_ = -1;
     normal_device();
@@ -398,6 +412,7 @@ class Session final : public SessionBase {
   void get_precond(void* out, int64_t n) override { download(m_, out, n); }
 
   void apply_jtj(const void* v, void* out, int64_t n, bool device) override {
+    Range nv("minopt::apply_jtj");
     ensure_refreshed();
     tune_apply();
     check(n == P_.num_cols, Err::kShapeMismatch, "apply_jtj(): vector size mismatch");
@@ -420,6 +435,7 @@ class Session final : public SessionBase {
 
   // ------------------------------------------------------------ solve
   SolveResult solve(IterCallback cb, void* user) override {
+    Range nv("minopt::solve");
     using clock = std::chrono::steady_clock;
     CK(cudaSetDevice(dev_));
     const bool lm = cfg_.method == 1;
@@ -447,6 +463,7 @@ class Session final : public SessionBase {
       tune_apply();
     }
     for (int it = 0; it < cfg_.nonlinear_iters; ++it) {
+      Range nv_it(lm ? "LM iteration" : "GN iteration");
       refresh_host();
       if (!lm) {
         // One GN iteration = one graph, one host sync (solver.hpp:415-464).
@@ -2381,6 +2398,7 @@ class Session final : public SessionBase {
 
  public:
   void linearize() override {
+    Range nv("minopt::linearize");
     ensure_refreshed();
     check(plan_has_evalj(), Err::kBindError, "plan was compiled without Jacobian kernels");
     cur_stage_ = -1;
