@@ -119,6 +119,16 @@ __device__ __forceinline__ uchar4 ldm4(const unsigned char* cm, long long i) {
   return cm ? *reinterpret_cast<const uchar4*>(cm + i) : make_uchar4(0, 0, 0, 0);
 }
 
+// Four excluded (non-halo) columns: every PCG vector holds +0 there from the
+// start (pcg_init / the fused build_normal start write them, pcg.hpp:75-80)
+// and every update writes +0 again (zero_excluded, pcg.hpp:50-55), so the
+// vector kernels skip such a group without loading or storing anything:
+// bitwise the same vectors, and excluded regions (Poisson's frozen 3/4 of
+// the image) cost no bandwidth.
+__device__ __forceinline__ bool mo_all_excluded(uchar4 e) {
+  return (e.x & e.y & e.z & e.w & 1) && !((e.x | e.y | e.z | e.w) & 2);
+}
+
 // delta += alpha p; r -= alpha Ap; z = r/m; rz' = r'z   (pcg.hpp:111-118)
 template <class Real>
 __device__ __forceinline__ double pcg_update1(Real alpha, unsigned char m, Real& d, Real& r, Real p, Real ap, Real md,
@@ -155,9 +165,10 @@ k_pcg_update(mo_red R, long long n, const unsigned char* cm, const Real* __restr
   const long long n4 = n >> 2;
   for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n4; v += stride) {
     const long long i = v << 2;
+    const uchar4 e = ldm4(cm, i);
+    if (mo_all_excluded(e)) continue;
     V4<Real> D = ld4(delta + i), Rr = ld4(r + i);
     const V4<Real> Pp = ld4(p + i), A = ld4(ap + i), M = ld4(md + i);
-    const uchar4 e = ldm4(cm, i);
     const unsigned char ex[4] = {e.x, e.y, e.z, e.w};
 #pragma unroll
     for (int k = 0; k < 4; ++k) acc += pcg_update1(alpha, ex[k], D.a[k], Rr.a[k], Pp.a[k], A.a[k], M.a[k], precond);
@@ -196,9 +207,10 @@ k_pcg_p(mo_state* st, long long n, const unsigned char* cm, const Real* __restri
   const long long n4 = n >> 2;
   for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n4; v += stride) {
     const long long i = v << 2;
+    const uchar4 e = ldm4(cm, i);
+    if (mo_all_excluded(e)) continue;
     const V4<Real> Rr = ld4(r + i), M = ld4(md + i);
     V4<Real> Pp = ld4(p + i);
-    const uchar4 e = ldm4(cm, i);
     const unsigned char ex[4] = {e.x, e.y, e.z, e.w};
 #pragma unroll
     for (int k = 0; k < 4; ++k) Pp.a[k] = pcg_p1(beta, ex[k], Rr.a[k], M.a[k], Pp.a[k], precond);
@@ -247,9 +259,10 @@ k_pcg_update_r(mo_red R, long long n, const unsigned char* cm, const Real* __res
   // streams per column: the loads in flight per thread set the bandwidth)
   for (; v + stride < n4; v += 2 * stride) {
     const long long i = v << 2, j = (v + stride) << 2;
+    const uchar4 e0 = ldm4(cm, i), e1 = ldm4(cm, j);
+    if (mo_all_excluded(e0) && mo_all_excluded(e1)) continue;
     V4<Real> R0 = ld4(r + i), R1 = ld4(r + j);
     const V4<Real> A0 = ld4(ap + i), A1 = ld4(ap + j), M0 = ld4(md + i), M1 = ld4(md + j);
-    const uchar4 e0 = ldm4(cm, i), e1 = ldm4(cm, j);
     const unsigned char x0[4] = {e0.x, e0.y, e0.z, e0.w}, x1[4] = {e1.x, e1.y, e1.z, e1.w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc += pcg_update_r1(alpha, x0[q], R0.a[q], A0.a[q], M0.a[q], precond);
@@ -260,9 +273,10 @@ k_pcg_update_r(mo_red R, long long n, const unsigned char* cm, const Real* __res
   }
   for (; v < n4; v += stride) {
     const long long i = v << 2;
+    const uchar4 e = ldm4(cm, i);
+    if (mo_all_excluded(e)) continue;
     V4<Real> Rr = ld4(r + i);
     const V4<Real> A = ld4(ap + i), M = ld4(md + i);
-    const uchar4 e = ldm4(cm, i);
     const unsigned char ex[4] = {e.x, e.y, e.z, e.w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc += pcg_update_r1(alpha, ex[q], Rr.a[q], A.a[q], M.a[q], precond);
@@ -290,9 +304,10 @@ k_pcg_dp(mo_state* st, long long n, const unsigned char* cm, const Real* __restr
   if (go) {  // two 4-wide groups per step, loads first (see k_pcg_update_r)
     for (; v + stride < n4; v += 2 * stride) {
       const long long i = v << 2, j = (v + stride) << 2;
+      const uchar4 e0 = ldm4(cm, i), e1 = ldm4(cm, j);
+      if (mo_all_excluded(e0) && mo_all_excluded(e1)) continue;
       V4<Real> D0 = ld4(delta + i), D1 = ld4(delta + j), P0 = ld4(p + i), P1 = ld4(p + j);
       const V4<Real> R0 = ld4(r + i), R1 = ld4(r + j), M0 = ld4(md + i), M1 = ld4(md + j);
-      const uchar4 e0 = ldm4(cm, i), e1 = ldm4(cm, j);
       const unsigned char x0[4] = {e0.x, e0.y, e0.z, e0.w}, x1[4] = {e1.x, e1.y, e1.z, e1.w};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -309,8 +324,9 @@ k_pcg_dp(mo_state* st, long long n, const unsigned char* cm, const Real* __restr
   }
   for (; v < n4; v += stride) {
     const long long i = v << 2;
-    V4<Real> D = ld4(delta + i), Pp = ld4(p + i);
     const uchar4 e = ldm4(cm, i);
+    if (mo_all_excluded(e)) continue;
+    V4<Real> D = ld4(delta + i), Pp = ld4(p + i);
     const unsigned char ex[4] = {e.x, e.y, e.z, e.w};
     if (go) {
       const V4<Real> Rr = ld4(r + i), M = ld4(md + i);
@@ -438,9 +454,10 @@ k_xtrial(mo_state* st, long long n, const unsigned char* cm, Real* __restrict__ 
   const long long n4 = n >> 2;  // 4-wide body (16-byte accesses), scalar tail
   for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n4; v += stride) {
     const long long i = v << 2;
+    const uchar4 e = ldm4(cm, i);
+    if (in_place && mo_all_excluded(e)) continue;  // x stays, delta is 0 there
     const V4<Real> D = ld4(delta + i);
     V4<Real> X = ld4(x + i);
-    const uchar4 e = ldm4(cm, i);
     const unsigned char ex[4] = {e.x, e.y, e.z, e.w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
