@@ -49,6 +49,14 @@ __global__ void k_flags_in(mo_state* st, const double* rb, int world) {
   st->nonfinite_kernel = nf;
   st->any_nonzero = nz;
 }
+// *flag |= any byte of p[0, n) nonzero.
+__global__ void k_any_byte(const unsigned char* p, long long n, int* flag) {
+  MO_PDL_ENTRY();
+  bool any = false;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    any |= p[i] != 0;
+  if (__syncthreads_or(any) && threadIdx.x == 0) atomicOr(flag, 1);
+}
 __global__ void k_or_bits(unsigned char* p, long long n, unsigned char bits) {
   MO_PDL_ENTRY();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
@@ -257,9 +265,20 @@ k_pcg_update_r(mo_red R, long long n, const unsigned char* cm, const Real* __res
   long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   // two 4-wide groups per step, every load issued before the first use (few
   // streams per column: the loads in flight per thread set the bandwidth)
+  // (the masks of a pair are loaded one pair ahead, so the skip test never
+  // holds back the vector loads it guards)
+  uchar4 n0 = make_uchar4(0, 0, 0, 0), n1 = n0;
+  if (v + stride < n4) {
+    n0 = ldm4(cm, v << 2);
+    n1 = ldm4(cm, (v + stride) << 2);
+  }
   for (; v + stride < n4; v += 2 * stride) {
     const long long i = v << 2, j = (v + stride) << 2;
-    const uchar4 e0 = ldm4(cm, i), e1 = ldm4(cm, j);
+    const uchar4 e0 = n0, e1 = n1;
+    if (v + 3 * stride < n4) {
+      n0 = ldm4(cm, (v + 2 * stride) << 2);
+      n1 = ldm4(cm, (v + 3 * stride) << 2);
+    }
     if (mo_all_excluded(e0) && mo_all_excluded(e1)) continue;
     V4<Real> R0 = ld4(r + i), R1 = ld4(r + j);
     const V4<Real> A0 = ld4(ap + i), A1 = ld4(ap + j), M0 = ld4(md + i), M1 = ld4(md + j);
@@ -302,9 +321,18 @@ k_pcg_dp(mo_state* st, long long n, const unsigned char* cm, const Real* __restr
   const long long n4 = n >> 2;
   long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (go) {  // two 4-wide groups per step, loads first (see k_pcg_update_r)
+    uchar4 n0 = make_uchar4(0, 0, 0, 0), n1 = n0;  // (masks one pair ahead)
+    if (v + stride < n4) {
+      n0 = ldm4(cm, v << 2);
+      n1 = ldm4(cm, (v + stride) << 2);
+    }
     for (; v + stride < n4; v += 2 * stride) {
       const long long i = v << 2, j = (v + stride) << 2;
-      const uchar4 e0 = ldm4(cm, i), e1 = ldm4(cm, j);
+      const uchar4 e0 = n0, e1 = n1;
+      if (v + 3 * stride < n4) {
+        n0 = ldm4(cm, (v + 2 * stride) << 2);
+        n1 = ldm4(cm, (v + 3 * stride) << 2);
+      }
       if (mo_all_excluded(e0) && mo_all_excluded(e1)) continue;
       V4<Real> D0 = ld4(delta + i), D1 = ld4(delta + j), P0 = ld4(p + i), P1 = ld4(p + j);
       const V4<Real> R0 = ld4(r + i), R1 = ld4(r + j), M0 = ld4(md + i), M1 = ld4(md + j);

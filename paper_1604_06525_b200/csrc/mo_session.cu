@@ -184,6 +184,7 @@ class Session final : public SessionBase {
     cudaFree(arena_);
     cudaFree(bd_);
     for (Real* p : lcache_) cudaFree(p);
+    cudaFree(anyflag_);
     for (Real* p : arr_) cudaFree(p);
     for (Real* p : comp_) cudaFree(p);
     for (unsigned char* p : masks_) cudaFree(p);
@@ -276,7 +277,26 @@ class Session final : public SessionBase {
     refresh_device();
     refreshed_ = true;
     jvalid_ = false;  // solver.hpp:167
+    // Does any column carry a mask bit?  The PCG vector kernels then test
+    // the column mask (and skip fully excluded groups); otherwise they get no
+    // mask at all (1 B per column and a load dependency less).  Masks that
+    // follow x (exclude programs reading unknowns) and strips (halo bits)
+    // always keep it.
+    bool any = colmask_ != nullptr;
+    if (colmask_ && !sh_.on && !exclude_reads_x()) {
+      if (!anyflag_) anyflag_ = dalloc<int>(1);
+      CK(cudaMemsetAsync(anyflag_, 0, sizeof(int), st_));
+      kl(k_any_byte, dim3(vgrid(P_.num_cols, nsm_)), dim3(MO_THREADS), colmask_, (long long)P_.num_cols, anyflag_);
+      int h = 0;
+      CK(cudaMemcpyAsync(&h, anyflag_, sizeof(int), cudaMemcpyDeviceToHost, st_));
+      CK(cudaStreamSynchronize(st_));
+      any = h != 0;
+    }
+    if (any != cm_any_) invalidate_graphs();
+    cm_any_ = any;
   }
+  // The column mask the PCG vector kernels read (null: no column is masked).
+  const unsigned char* cmv() const { return cm_any_ ? colmask_ : nullptr; }
 
   // Do the exclusion programs read the unknowns (or computed arrays)?  If
   // not, the masks only change when arrays are re-bound.
@@ -488,7 +508,7 @@ class Session final : public SessionBase {
           if (mat_) linearize_device();  // solver.hpp:426
           pcg_body(false, fi);
           CK(cudaMemsetAsync(&state_->any_nonzero, 0, sizeof(int), st_));
-          kl(k_xtrial<Real>, dim3(vg), dim3(MO_THREADS), state_, n, colmask_, x_, delta_, xt_, 1, SLOT_COST);
+          kl(k_xtrial<Real>, dim3(vg), dim3(MO_THREADS), state_, n, cmv(), x_, delta_, xt_, 1, SLOT_COST);
           ++launches_;
           exchange_cols(x_);
           cost_at(x_, SLOT_COST + 1);
@@ -2574,10 +2594,10 @@ class Session final : public SessionBase {
       if (defer) {  // deferred-delta pair (k_pcg_update_r / k_pcg_dp, mo_kernels.cuh)
         mo_red ru = red(0, vgu, MO_FIN_PARTIALS, 0);
         ru.partials = partials2_;
-        kl(k_pcg_update_r<Real>, dim3(vgu), dim3(MO_THREADS), ru, n, colmask_, mdv, r_, ap_, pre,
+        kl(k_pcg_update_r<Real>, dim3(vgu), dim3(MO_THREADS), ru, n, cmv(), mdv, r_, ap_, pre,
            (const double*)partials_, apply_parts_, k);
         const int last = k + 1 < cfg_.linear_iters ? 0 : 1;  // the last direction is never applied
-        kl(k_pcg_dp<Real>, dim3(vgu), dim3(MO_THREADS), state_, n, colmask_, mdv, r_, delta_, p_, pre,
+        kl(k_pcg_dp<Real>, dim3(vgu), dim3(MO_THREADS), state_, n, cmv(), mdv, r_, delta_, p_, pre,
            (const double*)partials2_, vgu, k, last);
         launches_ += 2;
         prof_end(1);
@@ -2588,13 +2608,13 @@ class Session final : public SessionBase {
       mo_red ru = red(0, vgu, cons ? MO_FIN_PARTIALS : MO_FIN_PCG_BETA, 0);
       if (cons) ru.partials = partials2_;
       const double* pap_part = cons ? partials_ : nullptr;
-      kl(k_pcg_update<Real>, dim3(vgu), dim3(MO_THREADS), ru, n, colmask_, mdv, delta_, r_, p_, ap_, pre, pap_part,
+      kl(k_pcg_update<Real>, dim3(vgu), dim3(MO_THREADS), ru, n, cmv(), mdv, delta_, r_, p_, ap_, pre, pap_part,
          apply_parts_, k);
       ++launches_;
       if (!cons) reduce_done(MO_FIN_PCG_BETA, 0);
       const double* rz_part = cons ? partials2_ : nullptr;
       if (k + 1 < cfg_.linear_iters) {  // the last direction is never applied
-        kl(k_pcg_p<Real>, dim3(vgu), dim3(MO_THREADS), state_, n, colmask_, mdv, r_, p_, pre, rz_part, vgu, k);
+        kl(k_pcg_p<Real>, dim3(vgu), dim3(MO_THREADS), state_, n, cmv(), mdv, r_, p_, pre, rz_part, vgu, k);
         ++launches_;
         exchange_cols(p_);
       } else if (cons) {  // bookkeeping of the last r'z
@@ -2711,6 +2731,8 @@ class Session final : public SessionBase {
   std::vector<int64_t> arr_n_;
   std::vector<unsigned char*> masks_;
   unsigned char* colmask_ = nullptr;
+  bool cm_any_ = true;     // some column mask bit set (see refresh())
+  int* anyflag_ = nullptr;  // (device flag of that test)
   double* params_d_ = nullptr;
   std::vector<double> params_h_;
   mo_state* state_ = nullptr;
