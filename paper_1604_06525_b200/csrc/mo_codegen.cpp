@@ -1386,7 +1386,10 @@ struct Gen {
     const int U = int(P.unknowns.size()), A = int(P.arrays.size());
     const int slot0 = 2 * U + A + int(P.computed.size());
     const int nv = int(lc_split.varying.size());
-    if (slot0 + nv + 1 > 32) return;  // MO_MAX_VIEWS
+    // (the apply reads the planes straight from global memory: no view or
+    // tensor-map slot per plane, so the lane count is not bounded by them;
+    // past 48 varying lanes the cache costs more than the evalj it saves)
+    if (nv > 48) return;
     const auto sh = P.shape_of(g.dom);
     const int AU = f64 ? 2 : 4;
     LcInfo li;
