@@ -807,6 +807,7 @@ struct Gen {
       gather_jtj8(g, gi, *S, lg, lane_slot, merged_off(merged), H, 1);
       lane_cache(g, gi, *S, H);
       if (lc_info.ok) gather_jtj8(g, gi, *S, lg, lane_slot, merged_off(merged), H, 2);
+      if (lc_info.ok) gather_jtj8(g, gi, *S, lg, lane_slot, merged_off(merged), H, 4);
       // build_normal that also writes the lane cache (mo_gather_bm8c_<gi>)
       if (lc_info.ok) gather_jtj8(g, gi, *S, lg, lane_slot, merged_off(merged), H, 3);
     }
@@ -1436,7 +1437,7 @@ struct Gen {
 
   void gather_jtj8(const GatherSet& g, int gi, const GridSet& S, const std::vector<LaneG>& lanes,
                    const std::vector<int>& lane_slot, const std::vector<MLane>& merged, int H, int mode) {
-    const bool bm = mode == 1 || mode == 3, cached = mode == 2, lcw = mode == 3;
+    const bool bm = mode == 1 || mode == 3, cached = mode == 2 || mode == 4, lcw = mode == 3;
     if (f64_disabled_tma()) return;
     if (bm && S.evalf.outputs.size() != S.jtemplates.size()) return;
     auto envi = [](const char* n, int d) { const char* v = std::getenv(n); return v ? std::atoi(v) : d; };
@@ -1449,8 +1450,12 @@ struct Gen {
     const int RX = cached ? H : std::max(std::max(reach_of(S.evalj, &g.dom), bm ? reach_of(S.evalf, &g.dom) : 0), H);
     const int AU = f64 ? 2 : 4;
     const int RB = f64 ? 8 : 4;
+    // Lane cache staged by the producer warp too (MO_B200_JTJ9_TMA=1): its
+    // planes ride the TMA ring (one-row boxes, NBUF deep) instead of the
+    // consumers' row-ahead global loads.
+    const bool lc_tma = mode == 4;
     int R = 1;
-    while (R < envi("MO_B200_JTJ8_R", 2)) R *= 2;  // rows per TMA box (power of two)
+    while (R < envi("MO_B200_JTJ8_R", lc_tma ? 1 : 2)) R *= 2;  // rows per TMA box (power of two)
     int NBUF = 1;
     // No deadlock: the block a consumer releases last must not wait for a
     // slot it still holds: NBUF >= 2 + ceil(2RX / R).
@@ -1476,6 +1481,8 @@ struct Gen {
       for (const LaneG& l : lanes) add(U + l.f, P.unknowns[size_t(l.f)].channels);
       for (auto& fc : g.chans) add(U + fc.first, P.unknowns[size_t(fc.first)].channels);
     }
+    if (lc_tma)
+      for (int j = 0; j <= lc_info.nv; ++j) add(lc_info.slot0 + j, 1);
     if (slots.empty() || int(slots.size()) > MO_MAX_TMAPS_HOST) return;
     int cmax = 1;
     for (auto& x : slots) cmax = std::max(cmax, x.second);
@@ -1518,13 +1525,21 @@ struct Gen {
     const std::string pf = bm ? program(S.evalf, false, &g.dom, true) : std::string();
     const int NO = int(S.evalj.outputs.size());
     const int NT = int(S.jtemplates.size());
-    const std::string LN = (lcw ? "mo_lanesbm8c_" : bm ? "mo_lanesbm8_" : cached ? "mo_lanes9_" : "mo_lanes8_") + sfx;
+    const std::string LN =
+        (lcw ? "mo_lanesbm8c_" : bm ? "mo_lanesbm8_" : lc_tma ? "mo_lanes9t_" : cached ? "mo_lanes9_" : "mo_lanes8_") + sfx;
     os << "template <bool I> __device__ __forceinline__ void " << LN
        << "(const mo_kparams& P, int p0, int p1, const int* ri, int lx, Real* c" << (bm ? ", Real* cm" : "")
        << (cached ? ", const Real* cv, unsigned bits" : "") << ") {\n"
        << "  const bool inside = I || mo_inb(P, p0, p1, 0); (void)inside;\n"
        << "  Real d[" << NO << "];\n";
-    if (cached) {
+    if (lc_tma) {
+      const int nv = lc_info.nv;
+      os << "  (void)cv; (void)bits;\n  Real cs_[" << std::max(nv, 1) << "];\n";
+      for (int j = 0; j < nv; ++j) os << "  cs_[" << j << "] = " << smx(lc_info.slot0 + j, 0, 0, 0) << ";\n";
+      const std::string bv = smx(lc_info.slot0 + nv, 0, 0, 0);
+      os << "  " << pe << "(P, " << (f64 ? "(unsigned)__double_as_longlong(" + bv + ")" : "__float_as_uint(" + bv + ")")
+         << ", cs_, d);\n";
+    } else if (cached) {
       os << "  " << pe << "(P, bits, cv, d);\n";
     } else if (lcw) {
       // evalj once, also the lane cache of the apply (its varying lanes and
@@ -1575,10 +1590,16 @@ struct Gen {
 
     const int K = int(g.chans.size());
     const int NA = 2 * H + 1;
-    const std::string kn = (lcw ? "mo_gather_bm8c_" : bm ? "mo_gather_bm8_" : cached ? "mo_gather_jtj9_" : "mo_gather_jtj8_") + sfx;
+    const std::string kn = (lcw      ? "mo_gather_bm8c_"
+                            : bm     ? "mo_gather_bm8_"
+                            : lc_tma ? "mo_gather_jtj9t_"
+                            : cached ? "mo_gather_jtj9_"
+                                     : "mo_gather_jtj8_") +
+                           sfx;
     // resident blocks the register allocator must allow (0: unconstrained);
     // the lane-cache apply gains from 6 (ARAP 8192^2: 966 vs 976 us)
-    const int minb = envi(bm ? "MO_B200_BM8_MINB" : cached ? "MO_B200_JTJ9_MINB" : "MO_B200_JTJ8_MINB", cached ? 6 : 0);
+    const int minb = envi(bm ? "MO_B200_BM8_MINB" : cached ? "MO_B200_JTJ9_MINB" : "MO_B200_JTJ8_MINB",
+                          cached && !lc_tma ? 6 : 0);
     std::ostringstream is;  // TMA issue of input block j (inline: tensor maps in param space)
     is << "{ const int s_ = gb & (NBUF - 1);\n"
        << "          if (gb >= NBUF) mo_mbar_wait(EMPTY + s_, ((gb >> LNB) - 1) & 1);\n"
@@ -1663,7 +1684,10 @@ struct Gen {
       }
     os << "      int e = (y0 - 2 * H - P.row_lo) * D1 + q1;  // element of output row y0 - 2H + k\n";
     const int NVC = cached ? lc_info.nv + 1 : 0;
-    if (cached) {
+    if (lc_tma) {
+      os << "      for (int k = 0; k < nrows; ++k, e += D1) {\n"
+         << "        const Real* const cc = nullptr; const unsigned cbits = 0u;\n";
+    } else if (cached) {
       // Lane cache of this lane's phase-1 element, read straight from global
       // memory (coalesced along the row, never a halo), PF rows ahead.
       // PF rows in flight per lane (MO_B200_JTJ9_PF; measured on ARAP
@@ -1836,16 +1860,17 @@ struct Gen {
     ti.threads = 32 * (NW + 1);
     for (auto& x : slots) ti.slots.push_back({x.first, x.second});
     if (cached) {
+      ti.cache_tma = lc_tma;
       ti.cache_planes = lc_info.nv + 1;
       ti.cache_slot0 = lc_info.slot0;
       ti.cache_hx = lc_info.HX;
       ti.cache_pw = lc_info.PW;
       ti.cache_rows = lc_info.rows;
     }
-    (lcw ? tmabm8c_info : bm ? tmabm8_info : cached ? tma9_info : tma8_info) = ti;
+    (lcw ? tmabm8c_info : bm ? tmabm8_info : lc_tma ? tma9t_info : cached ? tma9_info : tma8_info) = ti;
     staged.clear();
   }
-  ModuleInfo::Tma tma8_info, tmabm8_info, tma9_info, tmabm8c_info;
+  ModuleInfo::Tma tma8_info, tmabm8_info, tma9_info, tma9t_info, tmabm8c_info;
 
   // TMA-staged gather program (2-D domains): the reference's own J^T J p
   // gather program (transform.hpp:238-260, run_program semantics) per output
@@ -2389,6 +2414,7 @@ struct Gen {
         info.jtj8.push_back({});
         info.bm8.push_back({});
         info.jtj9.push_back({});
+        info.jtj9t.push_back({});
         info.bm8c.push_back({});
         continue;
       }
@@ -2403,6 +2429,7 @@ struct Gen {
       tma8_info = ModuleInfo::Tma{};
       tmabm8_info = ModuleInfo::Tma{};
       tma9_info = ModuleInfo::Tma{};
+      tma9t_info = ModuleInfo::Tma{};
       tmabm8c_info = ModuleInfo::Tma{};
       TwoPhase tp = gather_jtj2(g, int(i));
       info.jtj2.push_back({tp.ok, tp.smem, tp.nlanes, tp.H});
@@ -2415,6 +2442,7 @@ struct Gen {
       info.jtj8.push_back(tma8_info);
       info.bm8.push_back(tmabm8_info);
       info.jtj9.push_back(tma9_info);
+      info.jtj9t.push_back(tma9t_info);
       info.bm8c.push_back(tmabm8c_info);
     }
     for (size_t i = 0; i < P.graph_sets.size(); ++i) {

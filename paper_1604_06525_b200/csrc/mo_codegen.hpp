@@ -35,6 +35,7 @@ struct ModuleInfo {
     // lane-cache apply (mo_gather_jtj9): planes, their first view slot and the
     // extended-domain plane geometry (column origin HX, pitch PW, rows)
     int cache_planes = 0, cache_slot0 = 0, cache_hx = 0, cache_pw = 0, cache_rows = 0;
+    bool cache_tma = false;  // planes staged by TMA (views cache_slot0 + j) instead of direct loads
   };
   std::vector<TwoPhase> jtj2;  // per gather set
   std::vector<Stream> jtj3;    // per gather set
@@ -47,6 +48,7 @@ struct ModuleInfo {
   std::vector<Tma> bm8;        // per gather set: warp-specialised streaming build_normal (mo_gather_bm8_<i>)
   std::vector<Tma> jtj9;       // per gather set: lane-cache streaming apply (mo_gather_jtj9_<i>, mo_lanecache_<i>)
   std::vector<Tma> bm8c;       // per gather set: mo_gather_bm8 that also writes jtj9's lane cache
+  std::vector<Tma> jtj9t;      // per gather set: jtj9 with the lane-cache planes TMA-staged (mo_gather_jtj9t_<i>)
   std::vector<bool> vertex_kernels;  // per graph set: mo_graph_v{jtj,bm}_<g>_<dom> exist
   bool fused_vertex_apply = false;   // mo_graph_vjtjf_0: grid gather + graph gather + finish in one pass
 };

@@ -1273,7 +1273,10 @@ class Session final : public SessionBase {
   // two-phase bands, 3 = TMA-staged row-streaming bands (block-wide 8-row
   // steps), 4 = TMA-staged warp-streaming bands, 5 = TMA-staged gather
   // program (2-D domains).
-  static constexpr int kVariants = 9;
+  static constexpr int kVariants = 10;
+  // variants 8 and 9 apply from the lane cache (direct loads / TMA-staged)
+  static bool lc_variant(int v) { return v == 8 || v == 9; }
+  bool uses_lcache(size_t i) const { return lc_variant(variant(i)); }
   static constexpr int kBm4 = 100;  // tma_info id of the TMA build_normal kernel
   static constexpr int kBm8 = 101;  // tma_info id of the warp-specialised build_normal kernel
   static constexpr int kBm8c = 102;  // ... that also writes the lane cache of variant 8
@@ -1283,6 +1286,7 @@ class Session final : public SessionBase {
     if (v == kBm8c && i < minfo_.bm8c.size()) return &minfo_.bm8c[i];
     if (v == 7 && i < minfo_.jtj8.size()) return &minfo_.jtj8[i];
     if (v == 8 && i < minfo_.jtj9.size()) return &minfo_.jtj9[i];
+    if (v == 9 && i < minfo_.jtj9t.size()) return &minfo_.jtj9t[i];
     if (v == 3 && i < minfo_.jtj4.size()) return &minfo_.jtj4[i];
     if (v == 6 && i < minfo_.jtj7.size()) return &minfo_.jtj7[i];
     if (v == 4 && i < minfo_.jtj5.size()) return &minfo_.jtj5[i];
@@ -1295,18 +1299,18 @@ class Session final : public SessionBase {
     if (v == 1) return i < minfo_.jtj2.size() && minfo_.jtj2[i].ok;
     if (v == 2) return i < minfo_.jtj3.size() && minfo_.jtj3[i].ok;
     const ModuleInfo::Tma* t = tma_info(i, v);
-    if (v == 8 && (sh_.on || !t || t->cache_planes == 0)) return false;  // lane cache: unsharded grids
+    if (lc_variant(v) && (sh_.on || !t || t->cache_planes == 0)) return false;  // lane cache: unsharded grids
     return t && t->ok && tma_capable(i, *t);
   }
   int variant(size_t i) const {
     if (i < jtj_choice_.size() && variant_ok(i, jtj_choice_[i])) return jtj_choice_[i];
-    for (int v : {8, 7, 3, 6, 5, 4, 2, 1}) if (variant_ok(i, v)) return v;
+    for (int v : {9, 8, 7, 3, 6, 5, 4, 2, 1}) if (variant_ok(i, v)) return v;
     return 0;
   }
   static const char* variant_prefix(int v) {
     static const char* n[] = {"mo_gather_jtj_",  "mo_gather_jtj2_", "mo_gather_jtj3_",
                               "mo_gather_jtj4_", "mo_gather_jtj5_", "mo_gather_jtj6_", "mo_gather_jtj7_",
-                              "mo_gather_jtj8_", "mo_gather_jtj9_"};
+                              "mo_gather_jtj8_", "mo_gather_jtj9_", "mo_gather_jtj9t_"};
     return n[v];
   }
 
@@ -1441,6 +1445,7 @@ class Session final : public SessionBase {
                        : fs == "gprog" ? 5
                        : fs == "tma4" ? 6
                        : fs == "ws" ? 7
+                       : fs == "lct" ? 9
                                        : 8;
       if (want >= 0) {
         jtj_choice_[i] = variant_ok(i, want) ? want : -1;
@@ -1459,7 +1464,7 @@ class Session final : public SessionBase {
         t[v] = 1e30f;
         if (!variant_ok(i, v)) continue;
         jtj_choice_[i] = v;
-        if (v == 8) lanecache_fill(i);
+        if (lc_variant(v)) lanecache_fill(i);
         mo_kparams kp = kp_apply(i, x_, otmp_, 0);
         const int grid = jtj_grid(i);
         launch_apply(i, kp, grid);  // warm-up (module load, tensor maps)
@@ -1479,7 +1484,7 @@ class Session final : public SessionBase {
           if (t[v] < 1e29f) fprintf(stderr, "[mo tune] gather set %zu variant %d: %.1f us\n", i, v, t[v] * 1e3f / 8);
       }
       int bestv = 0;
-      for (int v : {8, 7, 3, 6, 5, 4, 2, 1, 0})
+      for (int v : {9, 8, 7, 3, 6, 5, 4, 2, 1, 0})
         if (t[v] <= 1.05f * best) {
           bestv = v;
           break;
@@ -1649,9 +1654,14 @@ class Session final : public SessionBase {
     kp.in1 = damp_;
     kp.flags = flags;
     if (variant(i) >= 2) kp.chunk = jtj3_chunk(i);
-    if (variant(i) == 8) {  // lane-cache planes (read directly by the kernel)
+    if (uses_lcache(i)) {  // lane-cache planes (read directly, or as TMA-staged views)
       ensure_lanecache(i);
       kp.in2 = lcache_[i];
+      const ModuleInfo::Tma& ti = *tma_info(i, variant(i));
+      if (ti.cache_tma) {
+        const size_t ps = size_t(ti.cache_pw) * size_t(ti.cache_rows);
+        for (int j = 0; j < ti.cache_planes; ++j) kp.v[ti.cache_slot0 + j].p = lcache_[i] + size_t(j) * ps;
+      }
     }
     return kp;
   }
@@ -1661,7 +1671,7 @@ class Session final : public SessionBase {
   void ensure_lanecache(size_t i) {
     if (lcache_.size() < P_.gather_sets.size()) lcache_.resize(P_.gather_sets.size(), nullptr);
     if (lcache_[i]) return;
-    const ModuleInfo::Tma& ti = minfo_.jtj9[i];
+    const ModuleInfo::Tma& ti = minfo_.jtj9[i];  // (the same planes for jtj9t)
     const size_t bytes = size_t(ti.cache_planes) * size_t(ti.cache_pw) * size_t(ti.cache_rows) * sizeof(Real);
     CK(cudaMalloc(&lcache_[i], bytes));
     CK(cudaMemsetAsync(lcache_[i], 0, bytes, st_));
@@ -1681,7 +1691,7 @@ class Session final : public SessionBase {
     if (mat_) return;
     tune_apply();
     for (size_t i = 0; i < P_.gather_sets.size(); ++i)
-      if (variant(i) == 8) lanecache_fill(i);
+      if (uses_lcache(i)) lanecache_fill(i);
   }
   void launch_edges(const std::string& name, int gi, const mo_kparams& kp, int grid = 0) {
     const void* f = mod_.kernel(name);
@@ -1832,7 +1842,7 @@ class Session final : public SessionBase {
   // build_normal writes variant 8's lane cache itself (mo_gather_bm8c): no
   // separate mo_lanecache pass per linearisation.
   bool bm8c_fuses(size_t i) const {
-    return bm8_ok(i) && variant(i) == 8 && i < minfo_.bm8c.size() && minfo_.bm8c[i].ok &&
+    return bm8_ok(i) && uses_lcache(i) && i < minfo_.bm8c.size() && minfo_.bm8c[i].ok &&
            tma_capable(i, minfo_.bm8c[i]) && !std::getenv("MO_B200_NO_BM8C");
   }
   // Grid and rows per work item of mo_gather_bm8 / bm8c (the apply's row model).
@@ -1882,7 +1892,7 @@ class Session final : public SessionBase {
   void normal_device(bool pcg_init = false) {
     if (tuned_ && !mat_)  // the linearisation point moved: refresh the lane cache
       for (size_t i = 0; i < P_.gather_sets.size(); ++i)
-        if (variant(i) == 8 && !bm8c_fuses(i)) lanecache_fill(i);
+        if (uses_lcache(i) && !bm8c_fuses(i)) lanecache_fill(i);
     prof_begin(2);
     const bool fused = P_.graph_sets.empty();
     const long long n = P_.num_cols;

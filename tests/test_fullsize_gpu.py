@@ -20,10 +20,10 @@ from paper_1604_06525_b200 import Method, Precision, SolveConfig, Solver, load_p
 
 pytestmark = pytest.mark.gpu
 
-VARIANTS = ["gather", "twophase", "stream", "tma", "warp", "gprog", "tma4", "ws", "lc"]
+VARIANTS = ["gather", "twophase", "stream", "tma", "warp", "gprog", "tma4", "ws", "lc", "lct"]
 PREFIX = {"gather": "mo_gather_jtj_", "twophase": "mo_gather_jtj2_", "stream": "mo_gather_jtj3_",
           "tma": "mo_gather_jtj4_", "warp": "mo_gather_jtj5_", "gprog": "mo_gather_jtj6_", "tma4": "mo_gather_jtj7_",
-          "ws": "mo_gather_jtj8_", "lc": "mo_gather_jtj9_"}
+          "ws": "mo_gather_jtj8_", "lc": "mo_gather_jtj9_", "lct": "mo_gather_jtj9t_"}
 THREADS = os.cpu_count() or 1
 
 

@@ -166,10 +166,10 @@ def test_kernels_bitwise_deterministic(name):
     assert outs[0][3] == outs[1][3]
 
 
-VARIANTS = ["gather", "twophase", "stream", "tma", "warp", "gprog", "tma4", "ws", "lc"]
+VARIANTS = ["gather", "twophase", "stream", "tma", "warp", "gprog", "tma4", "ws", "lc", "lct"]
 PREFIX = {"gather": "mo_gather_jtj_", "twophase": "mo_gather_jtj2_", "stream": "mo_gather_jtj3_",
           "tma": "mo_gather_jtj4_", "warp": "mo_gather_jtj5_", "gprog": "mo_gather_jtj6_", "tma4": "mo_gather_jtj7_",
-          "ws": "mo_gather_jtj8_", "lc": "mo_gather_jtj9_"}
+          "ws": "mo_gather_jtj8_", "lc": "mo_gather_jtj9_", "lct": "mo_gather_jtj9t_"}
 GRID = [n for n in NAMES if n.startswith("cfg_") and "mesh" not in n and "_mat" not in n]
 
 
