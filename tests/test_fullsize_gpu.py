@@ -264,3 +264,29 @@ def test_config5_arap_8192_strips_one_iteration():
         for row, rc in zip(r.trace, ref["trace_cost"]):
             assert abs(row.cost - rc) <= 1e-4 * abs(rc), (row.cost, rc)
         assert abs(r.final_cost - float(ref["final_cost"][0])) <= 1e-4 * abs(float(ref["final_cost"][0]))
+
+
+@pytest.mark.parametrize("name,n", [("arap_warp", 8192), ("poisson", 8192), ("arap_warp", 1024), ("sfs", 0)])
+def test_apply_operator_properties(name, n):
+    """Size-independent properties of the device J^T J p operator at full size
+    (the kernel the session chose): symmetry u'(A v) = v'(A u), linearity
+    A(u + 2v) = A u + 2 A v, positive semi-definiteness v'(A v) >= 0, and
+    A v = 0 on excluded columns (pcg.hpp:101 zeroing is the caller's; the
+    apply itself writes 0 there, exec.hpp:176-179)."""
+    prob = {"arap_warp": lambda: workloads.arap_warp(n, n), "poisson": lambda: workloads.poisson(n, n),
+            "sfs": lambda: workloads.sfs(640, 480)}[name]()
+    s = Solver(load_plan(prob.name, _cfg(prob, "f64", 1, 2), prob.dims), prob.data(np.float64))
+    ex = s.excluded().astype(bool)
+    # (the PCG's operator acts on vectors that are 0 on excluded columns,
+    # pcg.hpp:50-55; the apply zeroes excluded rows, so only there is it the
+    # symmetric D J^T J D)
+    u = np.where(ex, 0.0, workloads.uniform(11, s.num_cols()) - 0.5)
+    v = np.where(ex, 0.0, workloads.uniform(12, s.num_cols()) - 0.5)
+    au, av = s.apply_jtj(u), s.apply_jtj(v)
+    a_lin = s.apply_jtj(u + 2.0 * v)
+    uav, vau = float(np.dot(u, av)), float(np.dot(v, au))
+    assert abs(uav - vau) <= 1e-10 * max(abs(uav), abs(vau)), (uav, vau, s.apply_kernel(0))
+    scale = float(np.max(np.abs(au)) + 2 * np.max(np.abs(av)))
+    assert float(np.max(np.abs(a_lin - (au + 2.0 * av)))) <= 1e-12 * scale
+    assert float(np.dot(v, av)) >= 0.0
+    assert not np.any(av[ex]), "apply writes 0 on excluded columns"
