@@ -1355,8 +1355,9 @@ struct Gen {
   //    never issue copies, the producer runs ahead across work items, so the
   //    next item's first rows are in flight while the current one drains;
   //  * the ring is a power of two rows deep, so a row's slot is one mask;
-  //  * the output pixel's exclusion mask is loaded before phase 1 (its latency
-  //    hides behind the row's arithmetic) and 2- / 4-channel outputs are
+  //  * the output pixel's exclusion mask is loaded two rows ahead (loaded in
+  //    the row itself, its use stalled every consumer warp: 27% of the stall
+  //    samples of jtj9t at 8192^2) and 2- / 4-channel outputs are
   //    stored as one vector per pixel.
   // Sums are formed per output pixel in row-arrival order (tolerance parity
   // with the other fast variants, deterministic run to run).  bm = true:
@@ -1455,7 +1456,7 @@ struct Gen {
     // consumers' row-ahead global loads.
     const bool lc_tma = mode == 4;
     int R = 1;
-    while (R < envi("MO_B200_JTJ8_R", lc_tma ? 1 : 2)) R *= 2;  // rows per TMA box (power of two)
+    while (R < envi("MO_B200_JTJ8_R", 2)) R *= 2;  // rows per TMA box (power of two)
     int NBUF = 1;
     // No deadlock: the block a consumer releases last must not wait for a
     // slot it still holds: NBUF >= 2 + ceil(2RX / R).
@@ -1597,9 +1598,10 @@ struct Gen {
                                      : "mo_gather_jtj8_") +
                            sfx;
     // resident blocks the register allocator must allow (0: unconstrained);
-    // the lane-cache apply gains from 6 (ARAP 8192^2: 966 vs 976 us)
+    // the lane-cache applies gain from 6 (jtj9, ARAP 8192^2: 966 vs 976 us)
+    // and 4 (jtj9t with 2-row boxes: 751 vs 766 us; 1-row boxes 854 us)
     const int minb = envi(bm ? "MO_B200_BM8_MINB" : cached ? "MO_B200_JTJ9_MINB" : "MO_B200_JTJ8_MINB",
-                          cached && !lc_tma ? 6 : 0);
+                          lc_tma ? 4 : cached ? 6 : 0);
     std::ostringstream is;  // TMA issue of input block j (inline: tensor maps in param space)
     is << "{ const int s_ = gb & (NBUF - 1);\n"
        << "          if (gb >= NBUF) mo_mbar_wait(EMPTY + s_, ((gb >> LNB) - 1) & 1);\n"
@@ -1682,7 +1684,14 @@ struct Gen {
         os << "      Real A" << k << "_" << a << " = (Real)0;\n";
         if (bm) os << "      Real Q" << k << "_" << a << " = (Real)0;\n";
       }
-    os << "      int e = (y0 - 2 * H - P.row_lo) * D1 + q1;  // element of output row y0 - 2H + k\n";
+    os << "      int e = (y0 - 2 * H - P.row_lo) * D1 + q1;  // element of output row y0 - 2H + k\n"
+       << "      // exclusion mask of phase-1 row k's output pixel, loaded two rows ahead\n"
+       << "      const unsigned char* const MK = P.mask;\n"
+       << "      const int e0 = e;\n"
+       << "      auto mrow = [&](int kk) -> unsigned {\n"
+       << "        return (MK && kk >= 2 * H && kk < nrows && lane_out) ? (unsigned)MK[e0 + kk * D1] : 0u;\n"
+       << "      };\n"
+       << "      unsigned mq0 = mrow(0), mq1 = mrow(1);\n";
     const int NVC = cached ? lc_info.nv + 1 : 0;
     if (lc_tma) {
       os << "      for (int k = 0; k < nrows; ++k, e += D1) {\n"
@@ -1733,7 +1742,9 @@ struct Gen {
        << "        const int q0 = y0 - H + k;\n"
        << "        const int y = q0 - H;\n"
        << "        const bool orow = k >= 2 * H && y < y1 && lane_out;\n"
-       << "        const bool ex = orow && P.mask && P.mask[e];  // (loaded before phase 1)\n"
+       << "        const bool ex = orow && mq0 != 0u;\n"
+       << "        mq0 = mq1;\n"
+       << "        mq1 = mrow(k + 2);\n"
        << "        int ri[" << 2 * RX + 1 << "];\n"
        << "        #pragma unroll\n"
        << "        for (int o = 0; o < " << 2 * RX + 1 << "; ++o) ri[o] = (rb + k + o) & (NR - 1);\n"

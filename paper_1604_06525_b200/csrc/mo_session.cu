@@ -94,6 +94,9 @@ class Session final : public SessionBase {
     CK(cudaSetDevice(dev_));
     CK(cudaDeviceGetAttribute(&nsm_, cudaDevAttrMultiProcessorCount, dev_));
     CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&sd_, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ev_p_, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev_h_, cudaEventDisableTiming));
     cfg_ = P_.cfg;
     if (cfg_.pcg_rel_tol < 0) cfg_.pcg_rel_tol = cfg_.precision == 0 ? 1e-4 : 1e-8;
     mat_ = P_.cfg.materialize;
@@ -227,6 +230,9 @@ class Session final : public SessionBase {
       }
     cudaFreeHost(mu_h_);
     cudaStreamDestroy(st_);
+    cudaStreamDestroy(sd_);
+    cudaEventDestroy(ev_p_);
+    cudaEventDestroy(ev_h_);
   }
 
   // ------------------------------------------------------------ binding
@@ -820,12 +826,12 @@ class Session final : public SessionBase {
     return s;
   }
   // Halo rows of a column-layout vector (p, x, x_trial, delta).
-  void exchange_cols(Real* v) {
+  void exchange_cols(Real* v, cudaStream_t s = nullptr) {
     if (!sh_.on) return;
     std::vector<HaloSeg> segs;
     for (size_t f = 0; f < P_.unknowns.size(); ++f)
       segs.push_back(seg(v + P_.ubase[f], size_t(sh_.S) * size_t(P_.unknowns[f].channels) * sizeof(Real)));
-    comm_->halo(segs, st_);
+    comm_->halo(segs, s ? s : st_);
   }
   void exchange_computed() {
     if (!sh_.on || comp_.empty()) return;
@@ -1212,7 +1218,7 @@ class Session final : public SessionBase {
   int tiles_of(const Domain& d) const {
     auto s = P_.shape_of(d);
     const int nd = std::max<int>(1, int(d.dims.size()));
-    long long rows = s[0];
+    long long rows = ov0_ >= 0 ? ov1_ - ov0_ : s[0];
     if (rows <= 0) return 0;
     if (nd == 1) return int((rows + MO_THREADS - 1) / MO_THREADS);
     if (nd == 2) return int(((s[1] + MO_TILE_X - 1) / MO_TILE_X) * ((rows + MO_TILE_Y - 1) / MO_TILE_Y));
@@ -1613,7 +1619,7 @@ class Session final : public SessionBase {
     static const int force = std::getenv("MO_B200_CHUNK") ? std::atoi(std::getenv("MO_B200_CHUNK")) : 0;
     if (force > 0) return force;
     const auto sh = P_.shape_of(P_.gather_sets[i].dom);
-    const long long rows = sh_.on ? sh_.row1 - sh_.row0 : sh[0];
+    const long long rows = apply_rows(sh[0]);
     const int halo = jtj_halo(i), band = jtj_band(i);
     const long long nb = (sh[1] + band - 1) / band;
     const long long grid = (long long)nsm_ * jtj_occupancy(i);
@@ -1636,10 +1642,16 @@ class Session final : public SessionBase {
     }
     return std::max(best, 1);
   }
+  // Output rows of one apply launch: the strip's, the whole domain's, or the
+  // sub-range of an overlapped strip apply (ov0_/ov1_).
+  long long apply_rows(long long d0) const {
+    if (ov0_ >= 0) return ov1_ - ov0_;
+    return sh_.on ? sh_.row1 - sh_.row0 : d0;
+  }
   int jtj_grid(size_t i) {
     if (variant(i) < 2) return grid_blocks(jtj_kernel(i), P_.gather_sets[i].dom, jtj_smem(i));
     const auto sh = P_.shape_of(P_.gather_sets[i].dom);
-    const long long rows = sh_.on ? sh_.row1 - sh_.row0 : sh[0];
+    const long long rows = apply_rows(sh[0]);
     const int band = jtj_band(i);
     const long long nb = (sh[1] + band - 1) / band;
     const int ch = jtj3_chunk(i);
@@ -1653,6 +1665,10 @@ class Session final : public SessionBase {
     kp.in0 = pv;
     kp.in1 = damp_;
     kp.flags = flags;
+    if (ov0_ >= 0) {
+      kp.row0 = int(ov0_);
+      kp.row1 = int(ov1_);
+    }
     if (variant(i) >= 2) kp.chunk = jtj3_chunk(i);
     if (uses_lcache(i)) {  // lane-cache planes (read directly, or as TMA-staged views)
       ensure_lanecache(i);
@@ -1982,6 +1998,16 @@ class Session final : public SessionBase {
   // out = 2 J^T J pv (+ damp pv), optionally zeroing excluded columns and
   // reducing p'Ap into alpha (flags: MO_F_DAMP | MO_F_REDUCE | MO_F_ZEROEXCL).
   void apply(const Real* pv, Real* out, int flags) {
+    if (pending_p_) {
+      const bool split = !mat_ && P_.graph_sets.empty() && pending_p_ == pv && comm_ && comm_->world > 1 &&
+                         !std::getenv("MO_B200_NO_OVERLAP") && sh_.row1 - sh_.row0 > 2 * int64_t(sh_.R);
+      if (split) {
+        apply_overlapped(pv, out, flags);
+        return;
+      }
+      exchange_cols(const_cast<Real*>(pending_p_));
+      pending_p_ = nullptr;
+    }
     if (mat_) {
       mat_apply(pv, out, flags);
       return;
@@ -2028,6 +2054,54 @@ class Session final : public SessionBase {
         if (flags & MO_F_REDUCE) reduce_done(MO_FIN_PCG_ALPHA, 0);  // (strips only)
       }
     }
+  }
+
+  // Strip apply with the p halo exchange overlapped (pcg_body defers the
+  // exchange of p to here): the interior rows [row0+R, row1-R), whose
+  // stencils read owned p rows only, are launched first on st_; the exchange
+  // runs on sd_ meanwhile (forked after the p update); st_ joins it and
+  // applies the R border rows on each side.  One reduction spans the three
+  // launches (disjoint partial slots, the last block of the last launch
+  // finalises), so alpha is the same deterministic fixed-order sum on every
+  // run.  LocalComm's host barriers sit between the interior launch and the
+  // border launches, so the overlap is real for both transports.
+  void apply_overlapped(const Real* pv, Real* out, int flags) {
+    pending_p_ = nullptr;
+    const int64_t a = sh_.row0, b = sh_.row1, M = sh_.R;
+    const int64_t parts[3][2] = {{a + M, b - M}, {a, a + M}, {b - M, b}};
+    const size_t ng = P_.gather_sets.size();
+    std::vector<int> grids;
+    int total = 0;
+    for (const auto& pr : parts) {
+      ov0_ = pr[0];
+      ov1_ = pr[1];
+      for (size_t i = 0; i < ng; ++i) {
+        grids.push_back(jtj_grid(i));
+        total += grids.back();
+      }
+    }
+    CK(cudaEventRecord(ev_p_, st_));
+    int base = 0;
+    size_t gi = 0;
+    for (int part = 0; part < 3; ++part) {
+      if (part == 1) {
+        CK(cudaStreamWaitEvent(sd_, ev_p_, 0));
+        exchange_cols(p_, sd_);
+        CK(cudaEventRecord(ev_h_, sd_));
+        CK(cudaStreamWaitEvent(st_, ev_h_, 0));
+      }
+      ov0_ = parts[part][0];
+      ov1_ = parts[part][1];
+      for (size_t i = 0; i < ng; ++i, ++gi) {
+        mo_kparams kp = kp_apply(i, pv, out, flags);
+        kp.red = red(base, total, MO_FIN_PCG_ALPHA, 0);
+        launch_apply(i, kp, grids[gi]);
+        base += grids[gi];
+      }
+    }
+    ov0_ = ov1_ = -1;
+    apply_parts_ = total;
+    if (flags & MO_F_REDUCE) reduce_done(MO_FIN_PCG_ALPHA, 0);
   }
 
   // ------------------------------------------------------------ materialized J
@@ -2577,7 +2651,7 @@ class Session final : public SessionBase {
       ++launches_;
       reduce_done(MO_FIN_PCG_INIT, 0);
     }
-    exchange_cols(p_);  // strips: neighbours' p rows for the stencil apply
+    pending_p_ = sh_.on ? p_ : nullptr;  // strips: neighbours' p rows, exchanged by apply()
     const int flags = MO_F_REDUCE | MO_F_ZEROEXCL | MO_F_SKIPDONE | (lm ? MO_F_DAMP : 0);
     // Consumer-side reductions (unsharded grid plans): the apply and the
     // update only store block partials; the next kernel sums them in every
@@ -2626,13 +2700,14 @@ class Session final : public SessionBase {
       if (k + 1 < cfg_.linear_iters) {  // the last direction is never applied
         kl(k_pcg_p<Real>, dim3(vgu), dim3(MO_THREADS), state_, n, cmv(), mdv, r_, p_, pre, rz_part, vgu, k);
         ++launches_;
-        exchange_cols(p_);
+        pending_p_ = sh_.on ? p_ : nullptr;
       } else if (cons) {  // bookkeeping of the last r'z
         kl(k_pcg_fin<Real>, dim3(1), dim3(MO_THREADS), state_, rz_part, vgu, k);
         ++launches_;
       }
       prof_end(1);
     }
+    pending_p_ = nullptr;
   }
 
   // Replay `body` as a CUDA graph captured on first use (per stage key);
@@ -2731,6 +2806,10 @@ class Session final : public SessionBase {
   Config cfg_;
   int dev_ = 0, nsm_ = 148;
   cudaStream_t st_ = nullptr;
+  cudaStream_t sd_ = nullptr;                      // strips: p halo exchange beside the interior apply
+  cudaEvent_t ev_p_ = nullptr, ev_h_ = nullptr;    // (fork after the p update / join after the exchange)
+  const Real* pending_p_ = nullptr;                // p whose halo the next apply exchanges
+  int64_t ov0_ = -1, ov1_ = -1;                    // apply row range override (overlapped strips)
   Module mod_;
   Real *x_ = nullptr, *xt_ = nullptr, *b_ = nullptr, *m_ = nullptr, *md_ = nullptr, *damp_ = nullptr;
   Real *delta_ = nullptr, *r_ = nullptr, *p_ = nullptr, *ap_ = nullptr, *vtmp_ = nullptr, *otmp_ = nullptr;

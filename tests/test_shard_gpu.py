@@ -56,6 +56,38 @@ def test_strips_match_unsharded(name, world, prec):
     np.testing.assert_allclose(x, ref_data.x, rtol=tol * 10, atol=tol * 10 * scale)
 
 
+@pytest.mark.parametrize("variant", ["gather", "twophase", "stream", "tma", "warp", "gprog", "tma4", "ws", "lc",
+                                     "lct"])
+def test_overlapped_strip_apply_every_variant(variant, monkeypatch):
+    """Grid strips apply the interior rows while the p halo is exchanged on a
+    side stream, then the border rows (mo_session.cu apply_overlapped): each
+    J^T J p variant over three row ranges must give the unsharded solve, and
+    MO_B200_NO_OVERLAP (exchange first, one launch) the same steps."""
+    monkeypatch.setenv("MO_B200_JTJ", variant)
+    prob = workloads.arap_warp(60, 20, nhandles=6)
+    c = cfg("gn", "f64")
+    ref_data = prob.data(np.float64)
+    ref = Solver(load_plan(prob.name, c, prob.dims), ref_data).solve()
+    xs = {}
+    for overlap in (True, False):
+        if overlap:
+            monkeypatch.delenv("MO_B200_NO_OVERLAP", raising=False)
+        else:
+            monkeypatch.setenv("MO_B200_NO_OVERLAP", "1")
+        g = LocalShardGroup(load_plan(prob.name, c, prob.dims), prob.data(np.float64), 3)
+        try:
+            results = g.solve()
+            xs[overlap] = g.gather_x()
+        finally:
+            g.close()
+        for r in results:
+            assert [t.pcg_iters for t in r.trace] == [t.pcg_iters for t in ref.trace]
+            assert abs(r.final_cost - ref.final_cost) <= 1e-9 * abs(ref.final_cost)
+    scale = np.max(np.abs(ref_data.x))
+    for x in xs.values():
+        np.testing.assert_allclose(x, ref_data.x, rtol=1e-8, atol=1e-8 * scale)
+
+
 @pytest.mark.parametrize("name", ["poisson", "arap_mesh"])
 def test_nccl_transport_world1(name):
     """The NCCL transport (dlopen'ed libnccl, unique id via torch.distributed,
