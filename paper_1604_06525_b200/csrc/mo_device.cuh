@@ -64,6 +64,7 @@ enum {
   MO_F_SKIPDONE = 16,  // return at once when the PCG has already stopped
   MO_F_PCGINIT = 64,   // bm: also delta = 0, r = b, p = z = b/m, rz0 (pcg.hpp:75-97)
   MO_F_LCACHE = 128,   // bm8: also write the lane cache of the J^T J p apply (in2)
+  MO_F_EXSKIP = 256,   // jtj (PCG): no stores for excluded elements (their Ap is never read)
 };
 
 // One deterministic reduction: partial slots [part_base, part_base+gridDim)

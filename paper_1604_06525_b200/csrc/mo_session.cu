@@ -688,7 +688,7 @@ class Session final : public SessionBase {
       auto body = [&] {
         for (int r = 0; r < reps; ++r) {
           consumer_ = cons;
-          apply(p_, ap_, MO_F_REDUCE | MO_F_ZEROEXCL);
+          apply(p_, ap_, MO_F_REDUCE | MO_F_ZEROEXCL | MO_F_EXSKIP);
           consumer_ = false;
         }
       };
@@ -1471,7 +1471,7 @@ class Session final : public SessionBase {
         if (!variant_ok(i, v)) continue;
         jtj_choice_[i] = v;
         if (lc_variant(v)) lanecache_fill(i);
-        mo_kparams kp = kp_apply(i, x_, otmp_, 0);
+        mo_kparams kp = kp_apply(i, x_, otmp_, MO_F_EXSKIP);  // (stores as inside the PCG)
         const int grid = jtj_grid(i);
         launch_apply(i, kp, grid);  // warm-up (module load, tensor maps)
         // Timed as a captured graph of 8 launches (as the solver runs them):
@@ -2652,7 +2652,7 @@ class Session final : public SessionBase {
       reduce_done(MO_FIN_PCG_INIT, 0);
     }
     pending_p_ = sh_.on ? p_ : nullptr;  // strips: neighbours' p rows, exchanged by apply()
-    const int flags = MO_F_REDUCE | MO_F_ZEROEXCL | MO_F_SKIPDONE | (lm ? MO_F_DAMP : 0);
+    const int flags = MO_F_REDUCE | MO_F_ZEROEXCL | MO_F_SKIPDONE | MO_F_EXSKIP | (lm ? MO_F_DAMP : 0);
     // Consumer-side reductions (unsharded grid plans): the apply and the
     // update only store block partials; the next kernel sums them in every
     // block (same fixed order, bitwise the same total) and derives alpha /
