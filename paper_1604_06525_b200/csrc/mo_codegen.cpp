@@ -1612,11 +1612,19 @@ struct Gen {
        << "          mo_fence_proxy_async();\n"
        << "          mo_mbar_expect_tx(FULL + s_, " << tx << "u);\n"
        << "          const int r_ = y0 - H - RX + R * j - P.row_lo;\n";
+    // Lane-cache planes read with an L2 evict_first hint where the PCG's
+    // working set could otherwise stay in L2 (cache <= 48 MB: ARAP 1024^2
+    // 1.028 -> 1.001 ms per GN iteration); on HBM-sized grids the hint
+    // costs the apply 2% (8192^2: 769 vs 751 us).  MO_B200_LC_EVICT=0/1.
+    const double lc_bytes = lc_tma ? double(lc_info.nv + 1) * lc_info.PW * lc_info.rows * (f64 ? 8 : 4) : 0.0;
+    const bool evict = envi("MO_B200_LC_EVICT", lc_bytes <= 48e6 ? 1 : 0) != 0;
     for (size_t i = 0; i < slots.size(); ++i) {
       const bool cp = cached && slots[i].first >= lc_info.slot0;  // lane-cache plane: extended-domain coordinates
-      is << "          mo_tma_load_2d(mo_dsm + " << staged[i].second.first << " + s_ * " << boxbytes[i] << ", &T.m[" << i
-         << "], " << (cp ? "cs + " + std::to_string(lc_info.HX) : "cs * " + std::to_string(slots[i].second)) << ", r_"
-         << (cp ? " + P.row_lo + " + std::to_string(lc_info.H) : std::string()) << ", FULL + s_);\n";
+      is << "          mo_tma_load_2d" << (cp && evict ? "_hint" : "") << "(mo_dsm + " << staged[i].second.first
+         << " + s_ * " << boxbytes[i] << ", &T.m[" << i << "], "
+         << (cp ? "cs + " + std::to_string(lc_info.HX) : "cs * " + std::to_string(slots[i].second)) << ", r_"
+         << (cp ? " + P.row_lo + " + std::to_string(lc_info.H) : std::string()) << ", FULL + s_"
+         << (cp && evict ? ", pol" : "") << ");\n";
     }
     is << "        }\n";
     int LNB = 0;
@@ -1652,6 +1660,7 @@ struct Gen {
        << "  if (w == NW) {  // producer warp: lane 0 streams every item's input blocks\n"
        << "    if (l == 0) {\n"
        << "      int gb = 0;  // global input-block counter (slot gb % NBUF, use gb / NBUF)\n"
+       << (lc_tma && evict ? "      const unsigned long long pol = mo_l2_evict_first();\n" : "")
        << "      for (int t = blockIdx.x; t < items; t += gridDim.x) {\n"
        << "        const int ci = t / NBG, c0 = (t - ci * NBG) * (NW * BW);\n"
        << "        const int y0 = P.row0 + ci * CH, y1 = min(y0 + CH, P.row1);\n"

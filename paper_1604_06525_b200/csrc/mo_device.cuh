@@ -175,6 +175,23 @@ __device__ __forceinline__ void mo_tma_load_2d(void* dst, const mo_tmap* m, int 
       : "memory");
 }
 
+// The same with an L2 eviction-priority hint (createpolicy): streamed-once
+// data (the lane cache) marked evict_first so it does not push the PCG
+// vectors out of L2 on grids whose working set nearly fits.
+__device__ __forceinline__ unsigned long long mo_l2_evict_first() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void mo_tma_load_2d_hint(void* dst, const mo_tmap* m, int c_inner, int c_outer,
+                                                    unsigned long long* b, unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;"
+      ::"r"(mo_smem_addr(dst)), "l"(reinterpret_cast<unsigned long long>(m)), "r"(c_inner), "r"(c_outer),
+      "r"(mo_smem_addr(b)), "l"(pol)
+      : "memory");
+}
+
 // ---------------------------------------------------------------- helpers
 __device__ __forceinline__ bool mo_finite(double x) { return x == x && fabs(x) <= 1.7976931348623157e308; }
 
