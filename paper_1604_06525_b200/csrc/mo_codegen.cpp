@@ -1697,14 +1697,20 @@ struct Gen {
         os << "      Real A" << k << "_" << a << " = (Real)0;\n";
         if (bm) os << "      Real Q" << k << "_" << a << " = (Real)0;\n";
       }
-    os << "      int e = (y0 - 2 * H - P.row_lo) * D1 + q1;  // element of output row y0 - 2H + k\n"
-       << "      // exclusion mask of phase-1 row k's output pixel, loaded two rows ahead\n"
-       << "      const unsigned char* const MK = P.mask;\n"
-       << "      const int e0 = e;\n"
-       << "      auto mrow = [&](int kk) -> unsigned {\n"
-       << "        return (MK && kk >= 2 * H && kk < nrows && lane_out) ? (unsigned)MK[e0 + kk * D1] : 0u;\n"
-       << "      };\n"
-       << "      unsigned mq0 = mrow(0), mq1 = mrow(1);\n";
+    // Mask two rows ahead: jtj9t 884 -> 854 us and bm8c 2144 -> 1882 us on
+    // ARAP 8192^2; the direct-load lane-cache apply of SFS (26 cached lanes,
+    // register-bound) loses 10% with it, so jtj8 / bm8 / jtj9 keep the
+    // in-row load.  MO_B200_MASK_PF=0/1 forces either.
+    const bool mask_pf = envi("MO_B200_MASK_PF", mode == 3 || mode == 4 ? 1 : 0) != 0;
+    os << "      int e = (y0 - 2 * H - P.row_lo) * D1 + q1;  // element of output row y0 - 2H + k\n";
+    if (mask_pf)
+      os << "      // exclusion mask of phase-1 row k's output pixel, loaded two rows ahead\n"
+         << "      const unsigned char* const MK = P.mask;\n"
+         << "      const int e0 = e;\n"
+         << "      auto mrow = [&](int kk) -> unsigned {\n"
+         << "        return (MK && kk >= 2 * H && kk < nrows && lane_out) ? (unsigned)MK[e0 + kk * D1] : 0u;\n"
+         << "      };\n"
+         << "      unsigned mq0 = mrow(0), mq1 = mrow(1);\n";
     const int NVC = cached ? lc_info.nv + 1 : 0;
     if (lc_tma) {
       os << "      for (int k = 0; k < nrows; ++k, e += D1) {\n"
@@ -1755,9 +1761,8 @@ struct Gen {
        << "        const int q0 = y0 - H + k;\n"
        << "        const int y = q0 - H;\n"
        << "        const bool orow = k >= 2 * H && y < y1 && lane_out;\n"
-       << "        const bool ex = orow && mq0 != 0u;\n"
-       << "        mq0 = mq1;\n"
-       << "        mq1 = mrow(k + 2);\n"
+       << (mask_pf ? "        const bool ex = orow && mq0 != 0u;\n        mq0 = mq1;\n        mq1 = mrow(k + 2);\n"
+                   : "        const bool ex = orow && P.mask && P.mask[e];\n")
        << "        int ri[" << 2 * RX + 1 << "];\n"
        << "        #pragma unroll\n"
        << "        for (int o = 0; o < " << 2 * RX + 1 << "; ++o) ri[o] = (rb + k + o) & (NR - 1);\n"

@@ -4,9 +4,11 @@
 #include <dlfcn.h>
 
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "mo_plan.hpp"
 
@@ -28,11 +30,15 @@ class LocalWorld {
       CKC(cudaEventCreateWithFlags(&cev[size_t(r)], cudaEventDisableTiming));
     }
     CKC(cudaMalloc(&gbuf, sizeof(double) * size_t(n) * 64));
+    CKC(cudaMalloc(&pblk, kPeerBlock * size_t(n)));
+    CKC(cudaMemset(pblk, 0, kPeerBlock * size_t(n)));
+    for (int r = 0; r < n; ++r) table.block[r] = pblk + kPeerBlock * size_t(r);
   }
   ~LocalWorld() {
     for (auto e : ev) cudaEventDestroy(e);
     for (auto e : cev) cudaEventDestroy(e);
     cudaFree(gbuf);
+    cudaFree(pblk);
   }
   // Reusable generation barrier.
   void barrier() {
@@ -50,6 +56,8 @@ class LocalWorld {
   std::vector<std::vector<HaloSeg>> posted;  // per rank, current exchange
   std::vector<cudaEvent_t> ev, cev;          // produced / consumed per rank
   double* gbuf = nullptr;
+  char* pblk = nullptr;  // the ranks' peer-exchange blocks (one device: plain pointers)
+  PeerTable table;
 
  private:
   std::mutex mu;
@@ -109,6 +117,7 @@ class LocalComm final : public Comm {
     for (int r = 0; r < world; ++r) CKC(cudaStreamWaitEvent(st, W->cev[size_t(r)], 0));
     W->barrier();
   }
+  const PeerTable* peers() override { return &W->table; }
 
  private:
   std::shared_ptr<LocalWorld> W;
@@ -184,9 +193,6 @@ class NcclComm final : public Comm {
     CKC(cudaSetDevice(dev));
     nccl::ok(nccl::api().CommInitRank(&comm_, w, id, r), "ncclCommInitRank");
   }
-  ~NcclComm() override {
-    if (comm_) nccl::api().CommDestroy(comm_);
-  }
   void halo(const std::vector<HaloSeg>& segs, cudaStream_t st) override {
     auto& A = nccl::api();
     nccl::ok(A.GroupStart(), "ncclGroupStart");
@@ -213,10 +219,92 @@ class NcclComm final : public Comm {
     nccl::ok(nccl::api().AllGather(send, recv, size_t(n), nccl::ncclFloat64, comm_, st), "ncclAllGather");
   }
   bool capturable() const override { return true; }
+  // Exchange blocks mapped with CUDA IPC (each rank allocates its own; the
+  // handles travel by one NCCL all-gather; peers open them with lazy peer
+  // access over NVLink).  Any failure leaves the NCCL reductions in place.
+  const PeerTable* peers() override {
+    if (peer_state_ == 0) {
+      peer_state_ = -1;
+      if (world <= kPeerMax && !std::getenv("MO_B200_NO_P2P")) try_map_peers();
+    }
+    return peer_state_ > 0 ? &table_ : nullptr;
+  }
+  ~NcclComm() override;
 
  private:
+  void try_map_peers() {
+    if (cudaMalloc(&mine_, kPeerBlock) != cudaSuccess) return;
+    CKC(cudaMemset(mine_, 0, kPeerBlock));
+    cudaIpcMemHandle_t h;
+    std::memset(&h, 0, sizeof h);
+    const bool can = world == 1 || cudaIpcGetMemHandle(&h, mine_) == cudaSuccess;
+    // every rank learns every rank's handle and whether it could export one
+    struct Msg {
+      cudaIpcMemHandle_t h;
+      int ok;
+      char pad[60];
+    };
+    static_assert(sizeof(Msg) == 128, "handle message is 128 bytes");
+    Msg m;
+    std::memset(&m, 0, sizeof m);
+    m.h = h;
+    m.ok = can ? 1 : 0;
+    char* d = nullptr;
+    CKC(cudaMalloc(&d, sizeof(Msg) * size_t(world + 1)));
+    CKC(cudaMemcpy(d, &m, sizeof m, cudaMemcpyHostToDevice));
+    cudaStream_t s;
+    CKC(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    nccl::ok(nccl::api().AllGather(d, d + sizeof(Msg), sizeof(Msg), nccl::ncclChar, comm_, s), "ncclAllGather");
+    CKC(cudaStreamSynchronize(s));
+    CKC(cudaStreamDestroy(s));
+    std::vector<Msg> all(static_cast<size_t>(world));
+    CKC(cudaMemcpy(all.data(), d + sizeof(Msg), sizeof(Msg) * size_t(world), cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    bool every = true;
+    for (const Msg& x : all) every = every && x.ok;
+    bool opened = every;
+    for (int r = 0; r < world && opened; ++r) {
+      if (r == rank) {
+        table_.block[r] = mine_;
+        continue;
+      }
+      void* p = nullptr;
+      if (cudaIpcOpenMemHandle(&p, all[size_t(r)].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        opened = false;
+        break;
+      }
+      table_.block[r] = static_cast<char*>(p);
+    }
+    // all ranks must agree (a rank that could not map every peer would stall
+    // the others): one more all-gather of the outcome
+    int* f = nullptr;
+    CKC(cudaMalloc(&f, sizeof(int) * size_t(world + 1)));
+    const int mineok = opened ? 1 : 0;
+    CKC(cudaMemcpy(f, &mineok, sizeof(int), cudaMemcpyHostToDevice));
+    CKC(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    nccl::ok(nccl::api().AllGather(f, f + 1, sizeof(int), nccl::ncclChar, comm_, s), "ncclAllGather");
+    CKC(cudaStreamSynchronize(s));
+    CKC(cudaStreamDestroy(s));
+    std::vector<int> oks(static_cast<size_t>(world));
+    CKC(cudaMemcpy(oks.data(), f + 1, sizeof(int) * size_t(world), cudaMemcpyDeviceToHost));
+    cudaFree(f);
+    bool all_ok = true;
+    for (int x : oks) all_ok = all_ok && x;
+    peer_state_ = all_ok ? 1 : -1;
+  }
   nccl::ncclComm_t comm_ = nullptr;
+  char* mine_ = nullptr;
+  PeerTable table_;
+  int peer_state_ = 0;  // 0 not tried, 1 mapped, -1 unavailable
 };
+
+NcclComm::~NcclComm() {
+  for (int r = 0; r < world && r < kPeerMax; ++r)
+    if (r != rank && table_.block[r]) cudaIpcCloseMemHandle(table_.block[r]);
+  if (mine_) cudaFree(mine_);
+  if (comm_) nccl::api().CommDestroy(comm_);
+}
 
 void nccl_unique_id(void* out128) {
   nccl::ncclUniqueId id;

@@ -25,6 +25,21 @@ struct HaloSeg {
   int send_up = 0, send_down = 0;      // rows the neighbours above/below hold as halo
 };
 
+// One-shot deterministic all-gather of the reductions' rank partials through
+// peer-mapped device memory: every rank owns a small
+// exchange block; a single-block kernel (k_peer_fin, mo_kernels.cuh) stores
+// this rank's pair into slot `rank` of EVERY rank's block, raises a flag
+// there, waits for all flags in its own block and sums the slots in rank
+// order - one kernel over NVLink instead of an NCCL all-gather plus a
+// finalisation kernel, and kernel-only (capturable).
+//   block layout: double val[2][kPeerMax][2] | u64 flag[2][kPeerMax] | u64 epoch
+// (two parities: a rank can be at most one reduction ahead of any peer).
+constexpr int kPeerMax = 64;
+constexpr size_t kPeerBlock = 4096;
+struct PeerTable {
+  char* block[kPeerMax] = {};  // every rank's block, in this process's address space
+};
+
 class Comm {
  public:
   virtual ~Comm() = default;
@@ -35,6 +50,9 @@ class Comm {
   virtual void allgather(const double* send, double* recv, int n, cudaStream_t st) = 0;
   // Pure stream operations (no host synchronisation): CUDA-graph capturable.
   virtual bool capturable() const { return false; }
+  // Peer-mapped exchange blocks for k_peer_fin, or nullptr if the transport
+  // has none (then reductions use allgather + k_global_fin).
+  virtual const PeerTable* peers() { return nullptr; }
 };
 
 class LocalWorld;  // shared state of the single-process fake

@@ -42,6 +42,7 @@ struct mo_state {
   // after alpha_k); INT_MAX while running.  Unlike `done`, a kernel of
   // iteration k can test it against its own k while its block 0 writes it.
   int stop_code;
+  int peer_timeout;  // k_peer_fin gave up waiting for a rank (ranks out of step)
 };
 
 // Finalisation ops run by the last block of a reduction.

@@ -34,6 +34,89 @@ __global__ void k_global_fin(mo_state* st, const double* rb, int world, int op, 
   }
   mo_finalize<Real>(st, op, arg, t, t2);
 }
+// Peer-memory all-gather + finalisation (mo_comm.hpp PeerTable): thread q
+// stores this rank's pair into slot `rank` of rank q's block, fences, raises
+// the slot's flag (release, system scope), then waits for rank q's flag in
+// this rank's block (acquire) and copies its pair; thread 0 sums the pairs
+// in rank order exactly as k_global_fin does.  Every rank runs every
+// exchange (the `done` skip applies to the finalisation only), so the
+// per-block epoch counters stay in step.  A bounded wait (20 s) raises
+// peer_timeout instead of hanging the device.  kind 0: finalise (op, arg);
+// kind 1: OR of the nonfinite / any-nonzero flags (reduce_flags).
+struct mo_peer {
+  char* block[64];
+  int rank, world;
+};
+__device__ __forceinline__ void mo_st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long mo_ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long mo_globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+template <class Real>
+__global__ void k_peer_fin(mo_state* st, mo_peer P, double* rb, int op, int arg, int kind) {
+  MO_PDL_ENTRY();
+  constexpr int KP = 64;  // = kPeerMax
+  __shared__ unsigned long long e_s;
+  const int t = threadIdx.x;
+  char* const mine = P.block[P.rank];
+  unsigned long long* const ep = reinterpret_cast<unsigned long long*>(mine + 3072);
+  if (t == 0) {
+    e_s = *ep + 1;
+    *ep = e_s;
+  }
+  __syncthreads();
+  const unsigned long long e = e_s;
+  const int par = int(e & 1);
+  const double s0 = kind ? double(st->nonfinite_kernel) : st->sums[4];
+  const double s1 = kind ? double(st->any_nonzero) : st->sums[5];
+  if (t < P.world) {
+    char* const dst = P.block[t];
+    double* const v = reinterpret_cast<double*>(dst) + (par * KP + P.rank) * 2;
+    v[0] = s0;
+    v[1] = s1;
+    __threadfence_system();
+    mo_st_release_sys(reinterpret_cast<unsigned long long*>(dst + 2048) + par * KP + P.rank, e);
+    const unsigned long long* f = reinterpret_cast<const unsigned long long*>(mine + 2048) + par * KP + t;
+    const unsigned long long t0 = mo_globaltimer();
+    while (mo_ld_acquire_sys(f) < e) {
+      if (mo_globaltimer() - t0 > 20000000000ull) {
+        st->peer_timeout = 1;
+        break;
+      }
+      __nanosleep(100);
+    }
+    const volatile double* w = reinterpret_cast<const volatile double*>(mine) + (par * KP + t) * 2;
+    rb[2 * t] = w[0];
+    rb[2 * t + 1] = w[1];
+  }
+  __syncthreads();
+  if (t != 0) return;
+  if (kind) {
+    int nf = 0, nz = 0;
+    for (int r = 0; r < P.world; ++r) {
+      nf |= rb[2 * r] != 0.0;
+      nz |= rb[2 * r + 1] != 0.0;
+    }
+    st->nonfinite_kernel = nf;
+    st->any_nonzero = nz;
+    return;
+  }
+  if ((op == MO_FIN_PCG_ALPHA || op == MO_FIN_PCG_BETA) && st->done) return;
+  double a = 0, a2 = 0;
+  for (int r = 0; r < P.world; ++r) {
+    a += rb[2 * r];
+    a2 += rb[2 * r + 1];
+  }
+  mo_finalize<Real>(st, op, arg, a, a2);
+}
 __global__ void k_flags_out(mo_state* st) {
   MO_PDL_ENTRY();
   st->sums[4] = double(st->nonfinite_kernel);

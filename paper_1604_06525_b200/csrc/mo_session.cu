@@ -150,6 +150,14 @@ class Session final : public SessionBase {
       CK(cudaMemsetAsync(colmask_, 0, n, st_));
     }
     if (comm_) rankbuf_ = dalloc<double>(size_t(comm_->world) * 64);
+    if (comm_ && !std::getenv("MO_B200_NO_P2P")) {  // one-shot peer reductions (mo_comm.hpp)
+      if (const PeerTable* t = comm_->peers()) {
+        for (int r = 0; r < comm_->world; ++r) peer_.block[r] = t->block[r];
+        peer_.rank = comm_->rank;
+        peer_.world = comm_->world;
+        peer_on_ = true;
+      }
+    }
     params_d_ = dalloc<double>(std::max<size_t>(P_.params.size(), 1));
     state_ = dalloc<mo_state>(1);
     CK(cudaMallocHost(&state_h_, sizeof(mo_state)));
@@ -844,12 +852,22 @@ class Session final : public SessionBase {
   // rank order and finalised identically everywhere (deterministic).
   void reduce_done(int op, int arg) {
     if (!sh_.on) return;
+    if (peer_on_) {
+      kl(k_peer_fin<Real>, dim3(1), dim3(64), state_, peer_, rankbuf_, op, arg, 0);
+      ++launches_;
+      return;
+    }
     comm_->allgather(&state_->sums[4], rankbuf_, 2, st_);
     kl(k_global_fin<Real>, dim3(1), dim3(32), state_, rankbuf_, comm_->world, op, arg);
     ++launches_;
   }
   void reduce_flags() {
     if (!sh_.on) return;
+    if (peer_on_) {
+      kl(k_peer_fin<Real>, dim3(1), dim3(64), state_, peer_, rankbuf_, 0, 0, 1);
+      ++launches_;
+      return;
+    }
     kl(k_flags_out, dim3(1), dim3(1), state_);
     comm_->allgather(&state_->sums[4], rankbuf_, 2, st_);
     kl(k_flags_in, dim3(1), dim3(1), state_, rankbuf_, comm_->world);
@@ -2795,6 +2813,7 @@ class Session final : public SessionBase {
   void sync_state() {
     CK(cudaMemcpyAsync(state_h_, state_, sizeof(mo_state), cudaMemcpyDeviceToHost, st_));
     CK(cudaStreamSynchronize(st_));
+    if (state_h_->peer_timeout) fail(Err::kInternal, "peer reduction timed out: the strip ranks are out of step");
   }
   void download(const Real* src, void* out, int64_t n) {
     check(n == P_.num_cols, Err::kShapeMismatch, "vector size mismatch");
@@ -2839,6 +2858,8 @@ class Session final : public SessionBase {
   Comm* comm_ = nullptr;      // strip-shard communicator (not owned)
   Shard sh_;
   double* rankbuf_ = nullptr;  // gathered per-rank partials
+  bool peer_on_ = false;       // reductions through k_peer_fin (peer-mapped blocks)
+  mo_peer peer_{};
   bool x_bound_ = false, params_bound_ = false, refreshed_ = false;
   std::map<const void*, int> occ_;
   ModuleInfo minfo_;

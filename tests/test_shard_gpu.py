@@ -88,6 +88,30 @@ def test_overlapped_strip_apply_every_variant(variant, monkeypatch):
         np.testing.assert_allclose(x, ref_data.x, rtol=1e-8, atol=1e-8 * scale)
 
 
+@pytest.mark.parametrize("name", ["poisson", "sfs", "arap_mesh"])
+def test_peer_reductions_bitwise_equal_allgather(name, monkeypatch):
+    """The one-shot peer-memory reductions (k_peer_fin: slots in every rank's
+    exchange block, release/acquire flags, rank-order sum) give bitwise the
+    same solve as the all-gather + k_global_fin path (MO_B200_NO_P2P=1)."""
+    make, method = CASES[name]
+    prob = make()
+    c = cfg(method, "f64")
+    out = {}
+    for p2p in (True, False):
+        if p2p:
+            monkeypatch.delenv("MO_B200_NO_P2P", raising=False)
+        else:
+            monkeypatch.setenv("MO_B200_NO_P2P", "1")
+        g = LocalShardGroup(load_plan(prob.name, c, prob.dims), prob.data(np.float64), 3)
+        try:
+            res = g.solve()
+            out[p2p] = (g.gather_x(), [[t.cost for t in r.trace] for r in res])
+        finally:
+            g.close()
+    np.testing.assert_array_equal(out[True][0], out[False][0])
+    assert out[True][1] == out[False][1]
+
+
 @pytest.mark.parametrize("name", ["poisson", "arap_mesh"])
 def test_nccl_transport_world1(name):
     """The NCCL transport (dlopen'ed libnccl, unique id via torch.distributed,
