@@ -583,11 +583,16 @@ struct Gen {
   // LM damping (401-405), excluded zeroing and p'Ap reduction (pcg.hpp:100-102).
   void gather_jtj(const GatherSet& g, const std::string& pn, const std::string& kn) {
     const size_t K = g.chans.size();
+    // Inside the PCG (MO_F_EXSKIP) with an active-tile list in in3 ([count,
+    // tile ids ascending]): fully excluded tiles store nothing, so only the
+    // listed tiles are visited (Poisson: 1/4 of them).
     os << kbegin(kn) << "  if ((P.flags & MO_F_SKIPDONE) && P.state->done) return;\n"
        << "  double acc = 0; bool bad = false;\n"
        << "  Real* OUT = (Real*)P.out0; const Real* PV = (const Real*)P.in0; const Real* DAMP = (const Real*)P.in1;\n"
-          "  const int nt = mo_num_tiles(P);\n"
-          "  for (int t = blockIdx.x; t < nt; t += gridDim.x) {\n"
+          "  const int* const TL = (P.flags & MO_F_EXSKIP) ? (const int*)P.in3 : nullptr;\n"
+          "  const int nt = TL ? __ldg(TL) : mo_num_tiles(P);\n"
+          "  for (int ti = blockIdx.x; ti < nt; ti += gridDim.x) {\n"
+          "    const int t = TL ? __ldg(TL + 1 + ti) : ti;\n"
        << "    const mo_tile T = mo_tile_at(P, t);\n"
        << "    const bool it = mo_tile_in(P, T, " << reach << ");\n"
           "    int p0, p1, p2;\n"

@@ -117,7 +117,11 @@ class LocalComm final : public Comm {
     for (int r = 0; r < world; ++r) CKC(cudaStreamWaitEvent(st, W->cev[size_t(r)], 0));
     W->barrier();
   }
-  const PeerTable* peers() override { return &W->table; }
+  // Opt-in (MO_B200_LOCAL_P2P=1): the ranks share one device, so a host
+  // call that waits for the whole device (cudaFree, graph re-upload) on one
+  // rank would wait for another rank's k_peer_fin spinning on its flag.
+  // One process per GPU (NcclComm) has no such coupling.
+  const PeerTable* peers() override { return std::getenv("MO_B200_LOCAL_P2P") ? &W->table : nullptr; }
 
  private:
   std::shared_ptr<LocalWorld> W;

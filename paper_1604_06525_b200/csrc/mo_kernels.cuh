@@ -40,12 +40,13 @@ __global__ void k_global_fin(mo_state* st, const double* rb, int world, int op, 
 // this rank's block (acquire) and copies its pair; thread 0 sums the pairs
 // in rank order exactly as k_global_fin does.  Every rank runs every
 // exchange (the `done` skip applies to the finalisation only), so the
-// per-block epoch counters stay in step.  A bounded wait (20 s) raises
+// per-block epoch counters stay in step.  A bounded wait (60 s) raises
 // peer_timeout instead of hanging the device.  kind 0: finalise (op, arg);
 // kind 1: OR of the nonfinite / any-nonzero flags (reduce_flags).
 struct mo_peer {
   char* block[64];
   int rank, world;
+  unsigned long long timeout_ns;
 };
 __device__ __forceinline__ void mo_st_release_sys(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -87,7 +88,7 @@ __global__ void k_peer_fin(mo_state* st, mo_peer P, double* rb, int op, int arg,
     const unsigned long long* f = reinterpret_cast<const unsigned long long*>(mine + 2048) + par * KP + t;
     const unsigned long long t0 = mo_globaltimer();
     while (mo_ld_acquire_sys(f) < e) {
-      if (mo_globaltimer() - t0 > 20000000000ull) {
+      if (mo_globaltimer() - t0 > P.timeout_ns) {
         st->peer_timeout = 1;
         break;
       }
@@ -511,6 +512,22 @@ k_bm_patch(mo_red R, long long n, const unsigned char* cm, Real* __restrict__ b,
     }
   }
   mo_reduce_epilogue<Real>(R, cnt, 0.0, false);
+}
+
+// Active tiles of a masked grid domain: flag[t] = some element of tile t is
+// not excluded (the PCG apply of the gather program then walks only those
+// tiles, mo_session.cu build_tile_lists).
+__global__ void __launch_bounds__(MO_THREADS) k_tile_active(const __grid_constant__ mo_kparams P, unsigned char* flag,
+                                                           int nt) {
+  MO_PDL_ENTRY();
+  for (int t = blockIdx.x; t < nt; t += gridDim.x) {
+    const mo_tile T = mo_tile_at(P, t);
+    int p0, p1, p2;
+    const bool in = mo_tile_elem(P, T, p0, p1, p2);
+    const bool act = in && !P.mask[mo_local_elem(P, p0, p1, p2)];
+    const int any = __syncthreads_or(act);
+    if (threadIdx.x == 0 && threadIdx.y == 0) flag[t] = any ? 1 : 0;
+  }
 }
 
 // Per-column exclusion from a per-element mask (solver.hpp:149-157).

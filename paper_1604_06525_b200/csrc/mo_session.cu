@@ -11,6 +11,8 @@
 //              captured once into a CUDA graph, device-side scalars/stop flags
 //   step       x_trial / in-place GN step, trial cost, LM predicted decrease
 // and synchronises once to read the scalar state for the trace row.
+#include <cub/device/device_select.cuh>
+#include <thrust/iterator/counting_iterator.h>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -149,12 +151,17 @@ class Session final : public SessionBase {
       colmask_ = dalloc<unsigned char>(n);
       CK(cudaMemsetAsync(colmask_, 0, n, st_));
     }
-    if (comm_) rankbuf_ = dalloc<double>(size_t(comm_->world) * 64);
+    if (comm_) {
+      rankbuf_ = dalloc<double>(size_t(comm_->world) * 64);
+      chob_ = dalloc<double>(64);
+    }
     if (comm_ && !std::getenv("MO_B200_NO_P2P")) {  // one-shot peer reductions (mo_comm.hpp)
       if (const PeerTable* t = comm_->peers()) {
         for (int r = 0; r < comm_->world; ++r) peer_.block[r] = t->block[r];
         peer_.rank = comm_->rank;
         peer_.world = comm_->world;
+        const char* to = std::getenv("MO_B200_P2P_TIMEOUT_S");
+        peer_.timeout_ns = (unsigned long long)((to ? std::atof(to) : 60.0) * 1e9);
         peer_on_ = true;
       }
     }
@@ -205,6 +212,10 @@ class Session final : public SessionBase {
     cudaFree(partials_);
     cudaFree(partials2_);
     cudaFree(rankbuf_);
+    cudaFree(chob_);
+    if (tl_temp_) cudaFree(tl_temp_);
+    for (int* t : tiles_) cudaFree(t);
+    for (unsigned char* f : tflags_) cudaFree(f);
     cudaFreeHost(state_h_);
     for (auto& g : graphs_) cudaFree(g.d_verts);
     for (auto& gs : gsets_) {
@@ -346,6 +357,46 @@ class Session final : public SessionBase {
         }
       if (sh_.on) mark_halo_cols();  // bit 1: halo column, skipped by vector kernels
     }
+    build_tile_lists();
+  }
+  // Tiles (mo_tile_at numbering of the strip / domain rows) with at least
+  // one non-excluded element, per gather set on a masked domain:
+  // tiles_[i] = [count, ids ascending].  Rebuilt whenever the masks are.
+  static int host_tiles(const mo_kparams& k) {
+    const int rows = k.row1 - k.row0;
+    if (rows <= 0) return 0;
+    if (k.dnd == 1) return (rows + MO_THREADS - 1) / MO_THREADS;
+    const int fx = k.dnd == 2 ? k.d1 : k.d2;
+    const int ntx = (fx + MO_TILE_X - 1) / MO_TILE_X;
+    return ntx * (k.dnd == 2 ? (rows + MO_TILE_Y - 1) / MO_TILE_Y : rows * ((k.d1 + MO_TILE_Y - 1) / MO_TILE_Y));
+  }
+  void build_tile_lists() {
+    if (std::getenv("MO_B200_NO_TILE_LIST")) return;
+    tiles_.resize(P_.gather_sets.size(), nullptr);
+    tflags_.resize(P_.gather_sets.size(), nullptr);
+    for (size_t i = 0; i < P_.gather_sets.size(); ++i) {
+      const mo_kparams kp = kp_grid(P_.gather_sets[i].dom, x_, nullptr);
+      if (!kp.mask) continue;
+      const int nt = host_tiles(kp);
+      if (nt <= 0) continue;
+      if (!tiles_[i]) {
+        tiles_[i] = dalloc<int>(size_t(nt) + 1);
+        tflags_[i] = dalloc<unsigned char>(size_t(nt));
+        size_t need = 0;
+        CK(cub::DeviceSelect::Flagged(nullptr, need, thrust::counting_iterator<int>(0), tflags_[i], tiles_[i] + 1,
+                                      tiles_[i], nt, st_));
+        if (need > tl_temp_bytes_) {
+          if (tl_temp_) cudaFree(tl_temp_);
+          CK(cudaMalloc(&tl_temp_, need));
+          tl_temp_bytes_ = need;
+        }
+      }
+      kl(k_tile_active, dim3(std::min(nt, nsm_ * 8)), dim3(MO_TILE_X, MO_TILE_Y), kp, tflags_[i], nt);
+      size_t bytes = tl_temp_bytes_;
+      CK(cub::DeviceSelect::Flagged(tl_temp_, bytes, thrust::counting_iterator<int>(0), tflags_[i], tiles_[i] + 1,
+                                    tiles_[i], nt, st_));
+      launches_ += 2;
+    }
   }
 
   void refresh_host() {
@@ -470,6 +521,17 @@ class Session final : public SessionBase {
   // ------------------------------------------------------------ solve
   SolveResult solve(IterCallback cb, void* user) override {
     Range nv("minopt::solve");
+    // Peer reductions spin on the device until every rank has joined: they
+    // start with the second solve, once every rank is past the one-time
+    // host work of the first (JIT compiles, kernel timing, allocations that
+    // wait for the device), which keeps ranks apart for seconds, unevenly.
+    struct PeerReady {
+      bool& ready;
+      bool on;
+      ~PeerReady() {
+        if (on) ready = true;
+      }
+    } peer_ready_at_exit{peer_ready_, peer_on_};
     using clock = std::chrono::steady_clock;
     CK(cudaSetDevice(dev_));
     const bool lm = cfg_.method == 1;
@@ -852,7 +914,7 @@ class Session final : public SessionBase {
   // rank order and finalised identically everywhere (deterministic).
   void reduce_done(int op, int arg) {
     if (!sh_.on) return;
-    if (peer_on_) {
+    if (peer_on_ && peer_ready_) {
       kl(k_peer_fin<Real>, dim3(1), dim3(64), state_, peer_, rankbuf_, op, arg, 0);
       ++launches_;
       return;
@@ -863,7 +925,7 @@ class Session final : public SessionBase {
   }
   void reduce_flags() {
     if (!sh_.on) return;
-    if (peer_on_) {
+    if (peer_on_ && peer_ready_) {
       kl(k_peer_fin<Real>, dim3(1), dim3(64), state_, peer_, rankbuf_, 0, 0, 1);
       ++launches_;
       return;
@@ -1436,6 +1498,9 @@ class Session final : public SessionBase {
   void tune_apply() {
     if (tuned_) return;
     tuned_ = true;
+    tune_apply_once();
+  }
+  void tune_apply_once() {
     if (mat_) return;  // one apply: the materialized J
     // One decision per (module, shape) per process, so every session of a plan
     // runs the same kernel (bitwise run-to-run reproducibility).
@@ -1563,13 +1628,13 @@ class Session final : public SessionBase {
         mine[i] = jtj_choice_[i];
         mine[32 + i] = bm_choice_.size() > i ? bm_choice_[i] : 0;
       }
-      double* chob = nullptr;
-      CK(cudaMalloc(&chob, 64 * sizeof(double)));
-      CK(cudaMemcpyAsync(chob, mine.data(), 64 * sizeof(double), cudaMemcpyHostToDevice, st_));
-      comm_->allgather(chob, rankbuf_, 64, st_);
+      // (chob_ is allocated with the session: a cudaFree here would wait for
+      // the whole device, i.e. for another LocalComm rank's peer reduction
+      // spinning on this rank's flag)
+      CK(cudaMemcpyAsync(chob_, mine.data(), 64 * sizeof(double), cudaMemcpyHostToDevice, st_));
+      comm_->allgather(chob_, rankbuf_, 64, st_);
       CK(cudaMemcpyAsync(all.data(), rankbuf_, all.size() * sizeof(double), cudaMemcpyDeviceToHost, st_));
       CK(cudaStreamSynchronize(st_));
-      cudaFree(chob);
       for (size_t i = 0; i < G; ++i) {  // rank 0's entries come first
         jtj_choice_[i] = int(all[i]);
         if (bm_choice_.size() > i) bm_choice_[i] = int(all[32 + i]);
@@ -1686,6 +1751,8 @@ class Session final : public SessionBase {
     if (ov0_ >= 0) {
       kp.row0 = int(ov0_);
       kp.row1 = int(ov1_);
+    } else if (variant(i) == 0 && i < tiles_.size() && tiles_[i]) {
+      kp.in3 = tiles_[i];  // active-tile list (read under MO_F_EXSKIP)
     }
     if (variant(i) >= 2) kp.chunk = jtj3_chunk(i);
     if (uses_lcache(i)) {  // lane-cache planes (read directly, or as TMA-staged views)
@@ -2858,7 +2925,13 @@ class Session final : public SessionBase {
   Comm* comm_ = nullptr;      // strip-shard communicator (not owned)
   Shard sh_;
   double* rankbuf_ = nullptr;  // gathered per-rank partials
+  double* chob_ = nullptr;     // this rank's kernel choices (tuning broadcast)
+  std::vector<int*> tiles_;              // active-tile lists of masked gather domains
+  std::vector<unsigned char*> tflags_;   // (their per-tile flags)
+  void* tl_temp_ = nullptr;              // cub::DeviceSelect scratch
+  size_t tl_temp_bytes_ = 0;
   bool peer_on_ = false;       // reductions through k_peer_fin (peer-mapped blocks)
+  bool peer_ready_ = false;    // (after the first tuning)
   mo_peer peer_{};
   bool x_bound_ = false, params_bound_ = false, refreshed_ = false;
   std::map<const void*, int> occ_;

@@ -92,7 +92,10 @@ def test_overlapped_strip_apply_every_variant(variant, monkeypatch):
 def test_peer_reductions_bitwise_equal_allgather(name, monkeypatch):
     """The one-shot peer-memory reductions (k_peer_fin: slots in every rank's
     exchange block, release/acquire flags, rank-order sum) give bitwise the
-    same solve as the all-gather + k_global_fin path (MO_B200_NO_P2P=1)."""
+    same solve as the all-gather + k_global_fin path (MO_B200_NO_P2P=1).
+    The single-GPU transport takes the peer path on request only
+    (MO_B200_LOCAL_P2P=1, mo_comm.cpp)."""
+    monkeypatch.setenv("MO_B200_LOCAL_P2P", "1")
     make, method = CASES[name]
     prob = make()
     c = cfg(method, "f64")
@@ -104,6 +107,7 @@ def test_peer_reductions_bitwise_equal_allgather(name, monkeypatch):
             monkeypatch.setenv("MO_B200_NO_P2P", "1")
         g = LocalShardGroup(load_plan(prob.name, c, prob.dims), prob.data(np.float64), 3)
         try:
+            g.solve()  # (the peer path starts with a session's second solve)
             res = g.solve()
             out[p2p] = (g.gather_x(), [[t.cost for t in r.trace] for r in res])
         finally:
