@@ -441,8 +441,13 @@ def run_ours(args):
         alg = planinfo.graph_bytes_per_launch(info, "jtj", rb, units, E, g.arity)
         per_elem = alg / units
     else:
+        # The PCG apply reads and writes nothing for an excluded element (no
+        # stores, fully excluded tiles not visited): algorithmic bytes count
+        # the non-excluded elements only (Poisson: 1/4 of the image).
         per_elem = planinfo.algorithmic_bytes_per_element(info, "gather_set", "jtj", rb)
-        alg = per_elem * units
+        exm = s.excluded()
+        active = 1.0 - float(np.count_nonzero(exm & 1)) / max(exm.size, 1)
+        alg = per_elem * units * active
     peak, peak_kind = measured_peak()
     avg_apply = k_apply_ms
     achieved = alg / (avg_apply * 1e-3) / 1e9
@@ -464,6 +469,7 @@ def run_ours(args):
                      "frac": (achieved / peak) if achieved else None,
                      "traffic": ncu_traffic(profile_key(prob), s.apply_kernel(0)) if world == 1 else None,
                      "alg_bytes_per_launch": alg, "alg_bytes_per_elem": per_elem,
+                     "active_elem_frac": None if prob.graphs else active,
                      "avg_launch_us": avg_apply * 1e3,
                      # share of the timed step spent in this kernel (unperturbed launch time x
                      # launches per solve / step time): compare with the ncu launch list's share

@@ -221,6 +221,27 @@ __device__ __forceinline__ bool mo_all_excluded(uchar4 e) {
   return (e.x & e.y & e.z & e.w & 1) && !((e.x | e.y | e.z | e.w) & 2);
 }
 
+// Active-group list (unsharded grids with excluded columns, mo_session.cu
+// build_group_list): gl[0] = count, gl[1..] = the 4-column groups holding a
+// non-excluded column, ascending; bit 31 marks a group with an excluded
+// column (its mask is loaded).  The vector kernels then walk only the active
+// groups: no mask stream, no loop trips over excluded regions (Poisson: 3/4
+// of the columns).  Calls body(i, mask) for column i = 4 * group; the next
+// entry is loaded one trip ahead.
+template <class F>
+__device__ __forceinline__ void mo_for_groups(const int* __restrict__ gl, const unsigned char* cm, F&& body) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long cnt = __ldg(gl);
+  long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  int an = v < cnt ? __ldg(gl + 1 + v) : 0;
+  for (; v < cnt; v += stride) {
+    const int a = an;
+    if (v + stride < cnt) an = __ldg(gl + 1 + v + stride);
+    const long long i = (long long)(a & 0x7fffffff) << 2;
+    body(i, a < 0 ? ldm4(cm, i) : make_uchar4(0, 0, 0, 0));
+  }
+}
+
 // delta += alpha p; r -= alpha Ap; z = r/m; rz' = r'z   (pcg.hpp:111-118)
 template <class Real>
 __device__ __forceinline__ double pcg_update1(Real alpha, unsigned char m, Real& d, Real& r, Real p, Real ap, Real md,
@@ -241,7 +262,8 @@ template <class Real>
 __global__ void __launch_bounds__(MO_THREADS)
 k_pcg_update(mo_red R, long long n, const unsigned char* cm, const Real* __restrict__ md,
              Real* __restrict__ delta, Real* __restrict__ r, const Real* __restrict__ p,
-             const Real* __restrict__ ap, int precond, const double* pap_part, int pap_n, int k) {
+             const Real* __restrict__ ap, int precond, const double* pap_part, int pap_n, int k,
+             const int* gl) {
   MO_PDL_ENTRY();
   if (R.state->done) return;
   Real alpha;
@@ -255,7 +277,18 @@ k_pcg_update(mo_red R, long long n, const unsigned char* cm, const Real* __restr
   double acc = 0;
   const long long stride = (long long)gridDim.x * blockDim.x;
   const long long n4 = n >> 2;
-  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n4; v += stride) {
+  if (gl) {
+    mo_for_groups(gl, cm, [&](long long i, uchar4 e) {
+      V4<Real> D = ld4(delta + i), Rr = ld4(r + i);
+      const V4<Real> Pp = ld4(p + i), A = ld4(ap + i), M = ld4(md + i);
+      const unsigned char ex[4] = {e.x, e.y, e.z, e.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc += pcg_update1(alpha, ex[q], D.a[q], Rr.a[q], Pp.a[q], A.a[q], M.a[q], precond);
+      st4(delta + i, D);
+      st4(r + i, Rr);
+    });
+  }
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; !gl && v < n4; v += stride) {
     const long long i = v << 2;
     const uchar4 e = ldm4(cm, i);
     if (mo_all_excluded(e)) continue;
@@ -284,7 +317,8 @@ __device__ __forceinline__ Real pcg_p1(Real beta, unsigned char m, Real r, Real 
 template <class Real>
 __global__ void __launch_bounds__(MO_THREADS)
 k_pcg_p(mo_state* st, long long n, const unsigned char* cm, const Real* __restrict__ md,
-        const Real* __restrict__ r, Real* __restrict__ p, int precond, const double* rz_part, int rz_n, int k) {
+        const Real* __restrict__ r, Real* __restrict__ p, int precond, const double* rz_part, int rz_n, int k,
+        const int* gl) {
   MO_PDL_ENTRY();
   if (st->done) return;
   Real beta;
@@ -297,7 +331,17 @@ k_pcg_p(mo_state* st, long long n, const unsigned char* cm, const Real* __restri
   }
   const long long stride = (long long)gridDim.x * blockDim.x;
   const long long n4 = n >> 2;
-  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n4; v += stride) {
+  if (gl) {
+    mo_for_groups(gl, cm, [&](long long i, uchar4 e) {
+      const V4<Real> Rr = ld4(r + i), M = ld4(md + i);
+      V4<Real> Pp = ld4(p + i);
+      const unsigned char ex[4] = {e.x, e.y, e.z, e.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) Pp.a[q] = pcg_p1(beta, ex[q], Rr.a[q], M.a[q], Pp.a[q], precond);
+      st4(p + i, Pp);
+    });
+  }
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; !gl && v < n4; v += stride) {
     const long long i = v << 2;
     const uchar4 e = ldm4(cm, i);
     if (mo_all_excluded(e)) continue;
@@ -336,7 +380,7 @@ __device__ __forceinline__ double pcg_update_r1(Real alpha, unsigned char m, Rea
 template <class Real>
 __global__ void __launch_bounds__(MO_THREADS)
 k_pcg_update_r(mo_red R, long long n, const unsigned char* cm, const Real* __restrict__ md, Real* __restrict__ r,
-               const Real* __restrict__ ap, int precond, const double* pap_part, int pap_n, int k) {
+               const Real* __restrict__ ap, int precond, const double* pap_part, int pap_n, int k, const int* gl) {
   MO_PDL_ENTRY();
   if (R.state->done) return;
   Real alpha;
@@ -347,6 +391,17 @@ k_pcg_update_r(mo_red R, long long n, const unsigned char* cm, const Real* __res
   const long long stride = (long long)gridDim.x * blockDim.x;
   const long long n4 = n >> 2;
   long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (gl) {
+    mo_for_groups(gl, cm, [&](long long i, uchar4 e) {
+      V4<Real> Rr = ld4(r + i);
+      const V4<Real> A = ld4(ap + i), M = ld4(md + i);
+      const unsigned char ex[4] = {e.x, e.y, e.z, e.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc += pcg_update_r1(alpha, ex[q], Rr.a[q], A.a[q], M.a[q], precond);
+      st4(r + i, Rr);
+    });
+    v = n4;  // (the tail below still runs)
+  }
   // two 4-wide groups per step, every load issued before the first use (few
   // streams per column: the loads in flight per thread set the bandwidth)
   // (the masks of a pair are loaded one pair ahead, so the skip test never
@@ -393,7 +448,8 @@ k_pcg_update_r(mo_red R, long long n, const unsigned char* cm, const Real* __res
 template <class Real>
 __global__ void __launch_bounds__(MO_THREADS)
 k_pcg_dp(mo_state* st, long long n, const unsigned char* cm, const Real* __restrict__ md, const Real* __restrict__ r,
-         Real* __restrict__ delta, Real* __restrict__ p, int precond, const double* rz_part, int rz_n, int k, int last) {
+         Real* __restrict__ delta, Real* __restrict__ p, int precond, const double* rz_part, int rz_n, int k, int last,
+         const int* gl) {
   MO_PDL_ENTRY();
   if (st->stop_code < 2 * k + 1) return;  // stopped before alpha_k existed
   const double tot = mo_sum_partials(rz_part, rz_n);
@@ -404,7 +460,27 @@ k_pcg_dp(mo_state* st, long long n, const unsigned char* cm, const Real* __restr
   const long long stride = (long long)gridDim.x * blockDim.x;
   const long long n4 = n >> 2;
   long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (go) {  // two 4-wide groups per step, loads first (see k_pcg_update_r)
+  if (gl) {
+    mo_for_groups(gl, cm, [&](long long i, uchar4 e) {
+      V4<Real> D = ld4(delta + i), Pp = ld4(p + i);
+      const unsigned char ex[4] = {e.x, e.y, e.z, e.w};
+      if (go) {
+        const V4<Real> Rr = ld4(r + i), M = ld4(md + i);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          D.a[q] = (ex[q] & 1) ? Real(0) : D.a[q] + alpha * Pp.a[q];
+          Pp.a[q] = pcg_p1(beta, ex[q], Rr.a[q], M.a[q], Pp.a[q], precond);
+        }
+        st4(p + i, Pp);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) D.a[q] = (ex[q] & 1) ? Real(0) : D.a[q] + alpha * Pp.a[q];
+      }
+      st4(delta + i, D);
+    });
+    v = n4;  // (the tail below still runs)
+  }
+  if (go && !gl) {  // two 4-wide groups per step, loads first (see k_pcg_update_r)
     uchar4 n0 = make_uchar4(0, 0, 0, 0), n1 = n0;  // (masks one pair ahead)
     if (v + stride < n4) {
       n0 = ldm4(cm, v << 2);
@@ -527,6 +603,18 @@ __global__ void __launch_bounds__(MO_THREADS) k_tile_active(const __grid_constan
     const bool act = in && !P.mask[mo_local_elem(P, p0, p1, p2)];
     const int any = __syncthreads_or(act);
     if (threadIdx.x == 0 && threadIdx.y == 0) flag[t] = any ? 1 : 0;
+  }
+}
+
+// Active-group list source (mo_for_groups): per 4-column group, flag = not
+// all excluded, val = group | bit 31 if some column is excluded.
+__global__ void __launch_bounds__(MO_THREADS) k_group_flags(const unsigned char* __restrict__ cm, long long n4,
+                                                           int* __restrict__ val, unsigned char* __restrict__ flag) {
+  MO_PDL_ENTRY();
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < n4; g += (long long)gridDim.x * blockDim.x) {
+    const uchar4 e = ldm4(cm, g << 2);
+    flag[g] = mo_all_excluded(e) ? 0 : 1;
+    val[g] = int(g) | ((e.x | e.y | e.z | e.w) ? int(0x80000000u) : 0);
   }
 }
 

@@ -214,6 +214,7 @@ class Session final : public SessionBase {
     cudaFree(rankbuf_);
     cudaFree(chob_);
     if (tl_temp_) cudaFree(tl_temp_);
+    for (void* q : {(void*)glist_, (void*)gvals_, (void*)gflags_, gl_temp_}) cudaFree(q);
     for (int* t : tiles_) cudaFree(t);
     for (unsigned char* f : tflags_) cudaFree(f);
     cudaFreeHost(state_h_);
@@ -358,7 +359,29 @@ class Session final : public SessionBase {
       if (sh_.on) mark_halo_cols();  // bit 1: halo column, skipped by vector kernels
     }
     build_tile_lists();
+    build_group_list();
   }
+  // Active 4-column groups of an unsharded problem with excluded columns
+  // (mo_for_groups, mo_kernels.cuh): the PCG vector kernels walk this list
+  // instead of streaming the column mask over every group.
+  void build_group_list() {
+    if (sh_.on || !colmask_ || std::getenv("MO_B200_NO_GROUP_LIST")) return;
+    const long long n4 = P_.num_cols >> 2;
+    if (n4 <= 0 || n4 >= (1LL << 31)) return;
+    if (!glist_) {
+      glist_ = dalloc<int>(size_t(n4) + 1);
+      gvals_ = dalloc<int>(size_t(n4));
+      gflags_ = dalloc<unsigned char>(size_t(n4));
+      CK(cub::DeviceSelect::Flagged(nullptr, gl_temp_bytes_, gvals_, gflags_, glist_ + 1, glist_, int(n4), st_));
+      CK(cudaMalloc(&gl_temp_, gl_temp_bytes_));
+    }
+    kl(k_group_flags, dim3(vgrid(n4, nsm_, 8)), dim3(MO_THREADS), (const unsigned char*)colmask_, n4, gvals_, gflags_);
+    size_t bytes = gl_temp_bytes_;
+    CK(cub::DeviceSelect::Flagged(gl_temp_, bytes, gvals_, gflags_, glist_ + 1, glist_, int(n4), st_));
+    launches_ += 2;
+  }
+  // The active-group list the PCG vector kernels walk (null: stream the mask).
+  const int* gl() const { return cm_any_ && !sh_.on ? glist_ : nullptr; }
   // Tiles (mo_tile_at numbering of the strip / domain rows) with at least
   // one non-excluded element, per gather set on a masked domain:
   // tiles_[i] = [count, ids ascending].  Rebuilt whenever the masks are.
@@ -2764,10 +2787,10 @@ class Session final : public SessionBase {
         mo_red ru = red(0, vgu, MO_FIN_PARTIALS, 0);
         ru.partials = partials2_;
         kl(k_pcg_update_r<Real>, dim3(vgu), dim3(MO_THREADS), ru, n, cmv(), mdv, r_, ap_, pre,
-           (const double*)partials_, apply_parts_, k);
+           (const double*)partials_, apply_parts_, k, gl());
         const int last = k + 1 < cfg_.linear_iters ? 0 : 1;  // the last direction is never applied
         kl(k_pcg_dp<Real>, dim3(vgu), dim3(MO_THREADS), state_, n, cmv(), mdv, r_, delta_, p_, pre,
-           (const double*)partials2_, vgu, k, last);
+           (const double*)partials2_, vgu, k, last, gl());
         launches_ += 2;
         prof_end(1);
         continue;
@@ -2778,12 +2801,12 @@ class Session final : public SessionBase {
       if (cons) ru.partials = partials2_;
       const double* pap_part = cons ? partials_ : nullptr;
       kl(k_pcg_update<Real>, dim3(vgu), dim3(MO_THREADS), ru, n, cmv(), mdv, delta_, r_, p_, ap_, pre, pap_part,
-         apply_parts_, k);
+         apply_parts_, k, gl());
       ++launches_;
       if (!cons) reduce_done(MO_FIN_PCG_BETA, 0);
       const double* rz_part = cons ? partials2_ : nullptr;
       if (k + 1 < cfg_.linear_iters) {  // the last direction is never applied
-        kl(k_pcg_p<Real>, dim3(vgu), dim3(MO_THREADS), state_, n, cmv(), mdv, r_, p_, pre, rz_part, vgu, k);
+        kl(k_pcg_p<Real>, dim3(vgu), dim3(MO_THREADS), state_, n, cmv(), mdv, r_, p_, pre, rz_part, vgu, k, gl());
         ++launches_;
         pending_p_ = sh_.on ? p_ : nullptr;
       } else if (cons) {  // bookkeeping of the last r'z
@@ -2929,6 +2952,11 @@ class Session final : public SessionBase {
   std::vector<int*> tiles_;              // active-tile lists of masked gather domains
   std::vector<unsigned char*> tflags_;   // (their per-tile flags)
   void* tl_temp_ = nullptr;              // cub::DeviceSelect scratch
+  int* glist_ = nullptr;                 // active-group list [count, groups] (build_group_list)
+  int* gvals_ = nullptr;
+  unsigned char* gflags_ = nullptr;
+  void* gl_temp_ = nullptr;
+  size_t gl_temp_bytes_ = 0;
   size_t tl_temp_bytes_ = 0;
   bool peer_on_ = false;       // reductions through k_peer_fin (peer-mapped blocks)
   bool peer_ready_ = false;    // (after the first tuning)
@@ -3025,8 +3053,9 @@ PcgOutcome run_pcg_t(int device, int64_t n, PcgApply apply, void* user, const vo
       apply(p, ap, st, user);  // y = A x, complete on return or enqueued on `st`
       k_apply_finish<Real><<<vg, MO_THREADS, 0, st>>>(red(MO_FIN_PCG_ALPHA), n, cm, p, nullptr, ap,
                                                         MO_F_ZEROEXCL | MO_F_REDUCE);
-      k_pcg_update<Real><<<vg, MO_THREADS, 0, st>>>(red(MO_FIN_PCG_BETA), n, cm, md, dd, r, p, ap, pre, nullptr, 0, k);
-      k_pcg_p<Real><<<vg, MO_THREADS, 0, st>>>(state, n, cm, md, r, p, pre, nullptr, 0, k);
+      k_pcg_update<Real><<<vg, MO_THREADS, 0, st>>>(red(MO_FIN_PCG_BETA), n, cm, md, dd, r, p, ap, pre, nullptr, 0, k,
+                                                    nullptr);
+      k_pcg_p<Real><<<vg, MO_THREADS, 0, st>>>(state, n, cm, md, r, p, pre, nullptr, 0, k, nullptr);
       CK(cudaGetLastError());
       CK(cudaMemcpyAsync(&h, state, sizeof(mo_state), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
