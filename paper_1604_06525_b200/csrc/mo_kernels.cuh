@@ -258,7 +258,7 @@ __device__ __forceinline__ double pcg_update1(Real alpha, unsigned char m, Real&
   return double(r * z);
 }
 
-template <class Real>
+template <class Real, bool GL>
 __global__ void __launch_bounds__(MO_THREADS)
 k_pcg_update(mo_red R, long long n, const unsigned char* cm, const Real* __restrict__ md,
              Real* __restrict__ delta, Real* __restrict__ r, const Real* __restrict__ p,
@@ -277,7 +277,7 @@ k_pcg_update(mo_red R, long long n, const unsigned char* cm, const Real* __restr
   double acc = 0;
   const long long stride = (long long)gridDim.x * blockDim.x;
   const long long n4 = n >> 2;
-  if (gl) {
+  if constexpr (GL) {
     mo_for_groups(gl, cm, [&](long long i, uchar4 e) {
       V4<Real> D = ld4(delta + i), Rr = ld4(r + i);
       const V4<Real> Pp = ld4(p + i), A = ld4(ap + i), M = ld4(md + i);
@@ -288,7 +288,7 @@ k_pcg_update(mo_red R, long long n, const unsigned char* cm, const Real* __restr
       st4(r + i, Rr);
     });
   }
-  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; !gl && v < n4; v += stride) {
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; !GL && v < n4; v += stride) {
     const long long i = v << 2;
     const uchar4 e = ldm4(cm, i);
     if (mo_all_excluded(e)) continue;
@@ -314,7 +314,7 @@ __device__ __forceinline__ Real pcg_p1(Real beta, unsigned char m, Real r, Real 
   return z + beta * p;
 }
 
-template <class Real>
+template <class Real, bool GL>
 __global__ void __launch_bounds__(MO_THREADS)
 k_pcg_p(mo_state* st, long long n, const unsigned char* cm, const Real* __restrict__ md,
         const Real* __restrict__ r, Real* __restrict__ p, int precond, const double* rz_part, int rz_n, int k,
@@ -331,7 +331,7 @@ k_pcg_p(mo_state* st, long long n, const unsigned char* cm, const Real* __restri
   }
   const long long stride = (long long)gridDim.x * blockDim.x;
   const long long n4 = n >> 2;
-  if (gl) {
+  if constexpr (GL) {
     mo_for_groups(gl, cm, [&](long long i, uchar4 e) {
       const V4<Real> Rr = ld4(r + i), M = ld4(md + i);
       V4<Real> Pp = ld4(p + i);
@@ -341,7 +341,7 @@ k_pcg_p(mo_state* st, long long n, const unsigned char* cm, const Real* __restri
       st4(p + i, Pp);
     });
   }
-  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; !gl && v < n4; v += stride) {
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; !GL && v < n4; v += stride) {
     const long long i = v << 2;
     const uchar4 e = ldm4(cm, i);
     if (mo_all_excluded(e)) continue;
@@ -377,7 +377,7 @@ __device__ __forceinline__ double pcg_update_r1(Real alpha, unsigned char m, Rea
   return double(r * z);
 }
 
-template <class Real>
+template <class Real, bool GL>
 __global__ void __launch_bounds__(MO_THREADS)
 k_pcg_update_r(mo_red R, long long n, const unsigned char* cm, const Real* __restrict__ md, Real* __restrict__ r,
                const Real* __restrict__ ap, int precond, const double* pap_part, int pap_n, int k, const int* gl) {
@@ -391,7 +391,7 @@ k_pcg_update_r(mo_red R, long long n, const unsigned char* cm, const Real* __res
   const long long stride = (long long)gridDim.x * blockDim.x;
   const long long n4 = n >> 2;
   long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (gl) {
+  if constexpr (GL) {
     mo_for_groups(gl, cm, [&](long long i, uchar4 e) {
       V4<Real> Rr = ld4(r + i);
       const V4<Real> A = ld4(ap + i), M = ld4(md + i);
@@ -445,7 +445,7 @@ k_pcg_update_r(mo_red R, long long n, const unsigned char* cm, const Real* __res
   mo_reduce_epilogue<Real>(R, acc, 0.0, false);
 }
 
-template <class Real>
+template <class Real, bool GL>
 __global__ void __launch_bounds__(MO_THREADS)
 k_pcg_dp(mo_state* st, long long n, const unsigned char* cm, const Real* __restrict__ md, const Real* __restrict__ r,
          Real* __restrict__ delta, Real* __restrict__ p, int precond, const double* rz_part, int rz_n, int k, int last,
@@ -460,7 +460,7 @@ k_pcg_dp(mo_state* st, long long n, const unsigned char* cm, const Real* __restr
   const long long stride = (long long)gridDim.x * blockDim.x;
   const long long n4 = n >> 2;
   long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (gl) {
+  if constexpr (GL) {
     mo_for_groups(gl, cm, [&](long long i, uchar4 e) {
       V4<Real> D = ld4(delta + i), Pp = ld4(p + i);
       const unsigned char ex[4] = {e.x, e.y, e.z, e.w};
@@ -480,7 +480,7 @@ k_pcg_dp(mo_state* st, long long n, const unsigned char* cm, const Real* __restr
     });
     v = n4;  // (the tail below still runs)
   }
-  if (go && !gl) {  // two 4-wide groups per step, loads first (see k_pcg_update_r)
+  if (go && !GL) {  // two 4-wide groups per step, loads first (see k_pcg_update_r)
     uchar4 n0 = make_uchar4(0, 0, 0, 0), n1 = n0;  // (masks one pair ahead)
     if (v + stride < n4) {
       n0 = ldm4(cm, v << 2);

@@ -2786,10 +2786,10 @@ class Session final : public SessionBase {
       if (defer) {  // deferred-delta pair (k_pcg_update_r / k_pcg_dp, mo_kernels.cuh)
         mo_red ru = red(0, vgu, MO_FIN_PARTIALS, 0);
         ru.partials = partials2_;
-        kl(k_pcg_update_r<Real>, dim3(vgu), dim3(MO_THREADS), ru, n, cmv(), mdv, r_, ap_, pre,
+        kl(gl() ? k_pcg_update_r<Real, true> : k_pcg_update_r<Real, false>, dim3(vgu), dim3(MO_THREADS), ru, n, cmv(), mdv, r_, ap_, pre,
            (const double*)partials_, apply_parts_, k, gl());
         const int last = k + 1 < cfg_.linear_iters ? 0 : 1;  // the last direction is never applied
-        kl(k_pcg_dp<Real>, dim3(vgu), dim3(MO_THREADS), state_, n, cmv(), mdv, r_, delta_, p_, pre,
+        kl(gl() ? k_pcg_dp<Real, true> : k_pcg_dp<Real, false>, dim3(vgu), dim3(MO_THREADS), state_, n, cmv(), mdv, r_, delta_, p_, pre,
            (const double*)partials2_, vgu, k, last, gl());
         launches_ += 2;
         prof_end(1);
@@ -2800,13 +2800,13 @@ class Session final : public SessionBase {
       mo_red ru = red(0, vgu, cons ? MO_FIN_PARTIALS : MO_FIN_PCG_BETA, 0);
       if (cons) ru.partials = partials2_;
       const double* pap_part = cons ? partials_ : nullptr;
-      kl(k_pcg_update<Real>, dim3(vgu), dim3(MO_THREADS), ru, n, cmv(), mdv, delta_, r_, p_, ap_, pre, pap_part,
+      kl(gl() ? k_pcg_update<Real, true> : k_pcg_update<Real, false>, dim3(vgu), dim3(MO_THREADS), ru, n, cmv(), mdv, delta_, r_, p_, ap_, pre, pap_part,
          apply_parts_, k, gl());
       ++launches_;
       if (!cons) reduce_done(MO_FIN_PCG_BETA, 0);
       const double* rz_part = cons ? partials2_ : nullptr;
       if (k + 1 < cfg_.linear_iters) {  // the last direction is never applied
-        kl(k_pcg_p<Real>, dim3(vgu), dim3(MO_THREADS), state_, n, cmv(), mdv, r_, p_, pre, rz_part, vgu, k, gl());
+        kl(gl() ? k_pcg_p<Real, true> : k_pcg_p<Real, false>, dim3(vgu), dim3(MO_THREADS), state_, n, cmv(), mdv, r_, p_, pre, rz_part, vgu, k, gl());
         ++launches_;
         pending_p_ = sh_.on ? p_ : nullptr;
       } else if (cons) {  // bookkeeping of the last r'z
@@ -3053,9 +3053,9 @@ PcgOutcome run_pcg_t(int device, int64_t n, PcgApply apply, void* user, const vo
       apply(p, ap, st, user);  // y = A x, complete on return or enqueued on `st`
       k_apply_finish<Real><<<vg, MO_THREADS, 0, st>>>(red(MO_FIN_PCG_ALPHA), n, cm, p, nullptr, ap,
                                                         MO_F_ZEROEXCL | MO_F_REDUCE);
-      k_pcg_update<Real><<<vg, MO_THREADS, 0, st>>>(red(MO_FIN_PCG_BETA), n, cm, md, dd, r, p, ap, pre, nullptr, 0, k,
+      k_pcg_update<Real, false><<<vg, MO_THREADS, 0, st>>>(red(MO_FIN_PCG_BETA), n, cm, md, dd, r, p, ap, pre, nullptr, 0, k,
                                                     nullptr);
-      k_pcg_p<Real><<<vg, MO_THREADS, 0, st>>>(state, n, cm, md, r, p, pre, nullptr, 0, k, nullptr);
+      k_pcg_p<Real, false><<<vg, MO_THREADS, 0, st>>>(state, n, cm, md, r, p, pre, nullptr, 0, k, nullptr);
       CK(cudaGetLastError());
       CK(cudaMemcpyAsync(&h, state, sizeof(mo_state), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
