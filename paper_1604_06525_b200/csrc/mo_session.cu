@@ -319,7 +319,12 @@ class Session final : public SessionBase {
       any = h != 0;
     }
     if (any != cm_any_) invalidate_graphs();
+    const bool was = cm_any_;
     cm_any_ = any;
+    if (any && !was) {  // (refresh_device skipped the lists under the old value)
+      build_tile_lists();
+      build_group_list();
+    }
   }
   // The column mask the PCG vector kernels read (null: no column is masked).
   const unsigned char* cmv() const { return cm_any_ ? colmask_ : nullptr; }
@@ -365,7 +370,7 @@ class Session final : public SessionBase {
   // (mo_for_groups, mo_kernels.cuh): the PCG vector kernels walk this list
   // instead of streaming the column mask over every group.
   void build_group_list() {
-    if (sh_.on || !colmask_ || std::getenv("MO_B200_NO_GROUP_LIST")) return;
+    if (sh_.on || !colmask_ || !cm_any_ || std::getenv("MO_B200_NO_GROUP_LIST")) return;
     const long long n4 = P_.num_cols >> 2;
     if (n4 <= 0 || n4 >= (1LL << 31)) return;
     if (!glist_) {
@@ -394,7 +399,7 @@ class Session final : public SessionBase {
     return ntx * (k.dnd == 2 ? (rows + MO_TILE_Y - 1) / MO_TILE_Y : rows * ((k.d1 + MO_TILE_Y - 1) / MO_TILE_Y));
   }
   void build_tile_lists() {
-    if (std::getenv("MO_B200_NO_TILE_LIST")) return;
+    if (std::getenv("MO_B200_NO_TILE_LIST") || !cm_any_) return;  // (nothing excluded: every tile active)
     tiles_.resize(P_.gather_sets.size(), nullptr);
     tflags_.resize(P_.gather_sets.size(), nullptr);
     for (size_t i = 0; i < P_.gather_sets.size(); ++i) {
@@ -1774,7 +1779,7 @@ class Session final : public SessionBase {
     if (ov0_ >= 0) {
       kp.row0 = int(ov0_);
       kp.row1 = int(ov1_);
-    } else if (variant(i) == 0 && i < tiles_.size() && tiles_[i]) {
+    } else if (cm_any_ && variant(i) == 0 && i < tiles_.size() && tiles_[i]) {
       kp.in3 = tiles_[i];  // active-tile list (read under MO_F_EXSKIP)
     }
     if (variant(i) >= 2) kp.chunk = jtj3_chunk(i);

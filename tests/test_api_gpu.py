@@ -168,3 +168,44 @@ def test_lm_radius_triples_on_quadratic():
         if row.accepted:
             assert row.cost < prev
             prev = row.cost
+
+
+@pytest.mark.parametrize("first,second", [("quarter", "none"), ("none", "quarter"), ("quarter", "half")])
+def test_rebound_masks_rebuild_the_active_lists(first, second):
+    """The Poisson apply walks a list of active tiles and the PCG vector
+    kernels a list of active column groups, both built with the masks
+    (mo_session.cu build_tile_lists / build_group_list).  Re-binding the mask
+    array between solves (nothing excluded <-> a quarter or half active) must
+    give exactly what a fresh solver on the new data gives."""
+    from paper_1604_06525_b200 import Method, Precision, SolveConfig, load_plan, workloads
+    prob = workloads.poisson(96, 64)
+    W, H = prob.dims["W"], prob.dims["H"]
+    i = np.arange(W)[:, None]
+    j = np.arange(H)[None, :]
+
+    def mask(kind):
+        if kind == "none":
+            return np.zeros(W * H)
+        keep = (i >= W // 4) & (i < 3 * W // 4) & (j >= H // 4) & (j < 3 * H // 4)
+        if kind == "half":
+            keep = np.broadcast_to(i < W // 2, (W, H))
+        return np.where(keep, 0.0, 1.0).reshape(-1)
+
+    cfg = SolveConfig(method=Method.kGaussNewton, precision=Precision.kF64, nonlinear_iters=2, linear_iters=8,
+                      pcg_rel_tol=0.0)
+    plan = load_plan(prob.name, cfg, prob.dims)
+    d = prob.data(np.float64)
+    d.arrays[1] = mask(first)
+    s = Solver(plan, d)
+    s.solve()
+    d.x[:] = prob.data(np.float64).x
+    d.arrays[1] = mask(second)
+    s._bind_all()
+    s.refresh()
+    r = s.solve()
+    fresh = prob.data(np.float64)
+    fresh.arrays[1] = mask(second)
+    r2 = Solver(load_plan(prob.name, cfg, prob.dims), fresh).solve()
+    assert [t.pcg_iters for t in r.trace] == [t.pcg_iters for t in r2.trace]
+    np.testing.assert_allclose(d.x, fresh.x, rtol=1e-12, atol=1e-12 * np.max(np.abs(fresh.x)))
+    assert abs(r.final_cost - r2.final_cost) <= 1e-12 * abs(r2.final_cost)

@@ -117,9 +117,12 @@ def test_peer_reductions_bitwise_equal_allgather(name, monkeypatch):
 
 
 @pytest.mark.parametrize("name", ["poisson", "arap_mesh"])
-def test_nccl_transport_world1(name):
+def test_nccl_transport_world1(name, monkeypatch):
     """The NCCL transport (dlopen'ed libnccl, unique id via torch.distributed,
-    all-gather on the session stream) on the one GPU available: world 1."""
+    all-gather on the session stream) on the one GPU available: world 1.
+    (The unsharded reference solve walks the column mask like a strip does,
+    MO_B200_NO_GROUP_LIST=1, so the comparison is bitwise.)"""
+    monkeypatch.setenv("MO_B200_NO_GROUP_LIST", "1")
     import os
     import socket
 
@@ -151,8 +154,11 @@ def test_nccl_transport_world1(name):
         dist.destroy_process_group()
 
 
-def test_single_strip_equals_unsharded_bitwise():
-    """world=1: the shard path with no neighbours is the unsharded algorithm."""
+def test_single_strip_equals_unsharded_bitwise(monkeypatch):
+    """world=1: the shard path with no neighbours is the unsharded algorithm
+    (with the unsharded PCG walking the column mask like a strip,
+    MO_B200_NO_GROUP_LIST=1)."""
+    monkeypatch.setenv("MO_B200_NO_GROUP_LIST", "1")
     prob = workloads.poisson(32, 16)
     c = cfg("gn", "f64")
     ref_data = prob.data(np.float64)
