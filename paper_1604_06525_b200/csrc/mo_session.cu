@@ -2518,6 +2518,10 @@ class Session final : public SessionBase {
         hcol_ = dalloc<int>(K * n + 1);
         hval_ = dalloc<Real>(K * n + 1);
         hcnt_ = dalloc<int>(n + 1);
+        // (ELL slots past a row's count are never written; normal_matrix()
+        // downloads whole slot planes, so they hold defined zeros)
+        CK(cudaMemsetAsync(hcol_, 0, (K * n + 1) * sizeof(int), st_));
+        CK(cudaMemsetAsync(hval_, 0, (K * n + 1) * sizeof(Real), st_));
         hK_ = int(K);
         hn_ = n;
         realloc = true;
