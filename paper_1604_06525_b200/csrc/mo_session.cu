@@ -325,6 +325,22 @@ class Session final : public SessionBase {
       build_tile_lists();
       build_group_list();
     }
+    // Active counts on the host (masks that do not follow x change only
+    // here): the apply and PCG vector grids are sized to the active work,
+    // so small problems launch and reduce over fewer blocks (grid-stride
+    // loops stay correct for any grid, so a stale count costs speed only).
+    gl_count_ = -1;
+    tl_count_.assign(P_.gather_sets.size(), -1);
+    if (cm_any_ && !exclude_reads_x() && !sh_.on) {
+      int gc = -1;
+      if (glist_) CK(cudaMemcpyAsync(&gc, glist_, sizeof(int), cudaMemcpyDeviceToHost, st_));
+      std::vector<int> tc(P_.gather_sets.size(), -1);
+      for (size_t i = 0; i < tiles_.size(); ++i)
+        if (tiles_[i]) CK(cudaMemcpyAsync(&tc[i], tiles_[i], sizeof(int), cudaMemcpyDeviceToHost, st_));
+      CK(cudaStreamSynchronize(st_));
+      gl_count_ = gc;
+      for (size_t i = 0; i < tc.size(); ++i) tl_count_[i] = tc[i];
+    }
   }
   // The column mask the PCG vector kernels read (null: no column is masked).
   const unsigned char* cmv() const { return cm_any_ ? colmask_ : nullptr; }
@@ -1760,6 +1776,8 @@ class Session final : public SessionBase {
     return sh_.on ? sh_.row1 - sh_.row0 : d0;
   }
   int jtj_grid(size_t i) {
+    if (variant(i) == 0 && ov0_ < 0 && cm_any_ && i < tl_count_.size() && tl_count_[i] >= 0)
+      return std::max(1, std::min(tl_count_[i], grid_blocks(jtj_kernel(i), P_.gather_sets[i].dom, jtj_smem(i))));
     if (variant(i) < 2) return grid_blocks(jtj_kernel(i), P_.gather_sets[i].dom, jtj_smem(i));
     const auto sh = P_.shape_of(P_.gather_sets[i].dom);
     const long long rows = apply_rows(sh[0]);
@@ -2759,7 +2777,9 @@ class Session final : public SessionBase {
     // ARAP).  MO_B200_VEC_PER_SM overrides.
     static const int vper_env = std::getenv("MO_B200_VEC_PER_SM") ? std::atoi(std::getenv("MO_B200_VEC_PER_SM")) : 0;
     const int vper = vper_env > 0 ? vper_env : (n / 4 > 8LL * nsm_ * 4 * MO_THREADS ? 16 : 4);
-    const int vgu = vgrid(n, nsm_, vper);
+    // (over the active groups when the kernels walk the list)
+    const int vgu = gl() && gl_count_ >= 0 ? vgrid(std::max<long long>(gl_count_, 1), nsm_, vper)  // (a thread per group)
+                                          : vgrid(n, nsm_, vper);
     const Real* mdv = lm ? md_ : m_;
     const int pre = cfg_.use_preconditioner ? 1 : 0;
     if (!init_done) {
@@ -2962,6 +2982,8 @@ class Session final : public SessionBase {
   std::vector<unsigned char*> tflags_;   // (their per-tile flags)
   void* tl_temp_ = nullptr;              // cub::DeviceSelect scratch
   int* glist_ = nullptr;                 // active-group list [count, groups] (build_group_list)
+  long long gl_count_ = -1;              // (its count on the host, -1 unknown)
+  std::vector<int> tl_count_;            // active-tile counts on the host
   int* gvals_ = nullptr;
   unsigned char* gflags_ = nullptr;
   void* gl_temp_ = nullptr;
